@@ -1,0 +1,118 @@
+/*
+ * gala_b200.h -- C-ABI of the B200-native GALA HE linear-layer library.
+ *
+ * The reference (arxiv 2105.01827, package `gala`) has no native code: its
+ * drop-in seam is the Python module `gala.backend` ("Swapping in a real
+ * lattice backend means re-implementing the functions in this module",
+ * pkg/src/gala/backend.py:12-16) plus the two scheme entry points on the hot
+ * path, `mv_gala` (pkg/src/gala/matvec.py:305-320) and
+ * `mimo_kernel_grouping` (pkg/src/gala/conv.py:268-293).  Each entry point
+ * below names the reference function it replaces.  The Python package
+ * paper_2105_01827_b200 binds these with ctypes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "dev" pointers are CUDA device memory,
+ *    "host" pointers are host memory.  All device work is enqueued on the
+ *    context's stream (gala_set_stream); calls return after enqueueing
+ *    unless stated otherwise.
+ *  - Ciphertext (device): uint64 [2][L][N], RNS limbs, NTT domain in the
+ *    library's internal (bit-reversed) order.  Canonical words (coefficient
+ *    domain, natural order, values in [0, q_j)) are produced by
+ *    gala_ct_export / consumed by gala_ct_import.
+ *  - Plaintext operand (device): uint64 [L][N], internal form (NTT,
+ *    Montgomery-scaled).  Produced only by gala_encode_plain.
+ *  - Slot vectors: uint32 [N]; slots [0, N/2) are hypercube row 0 and
+ *    [N/2, N) row 1.  A rotation by `step` rotates both rows left by step
+ *    (Galois element 3^step mod 2N), i.e. ring.py:86-91 on each row.
+ *  - Return value: GALA_OK or a negative status; gala_last_error() has text.
+ */
+#ifndef GALA_B200_H
+#define GALA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GALA_OK 0
+#define GALA_ERR_PARAM (-1)   /* -> gala.errors.ParameterError */
+#define GALA_ERR_DIM (-2)     /* -> gala.errors.DimensionError */
+#define GALA_ERR_NOKEY (-3)   /* -> ParameterError: rotation key missing */
+#define GALA_ERR_CUDA (-4)    /* -> gala.errors.GalaError */
+#define GALA_ERR_STATE (-5)   /* -> GalaError: e.g. secret not set */
+
+typedef struct gala_ctx gala_ctx;
+
+const char *gala_last_error(void);
+int gala_version(void);
+
+/* Context: HEParams (backend.py:80-114) + the BFV instance derived from it.
+ * primes: L ciphertext primes followed by the special prime (L+1 values);
+ * psis: a primitive 2N-th root for each of them; psi_p: same for p. */
+int gala_ctx_create(gala_ctx **out, int N, int L, const uint64_t *primes, const uint64_t *psis,
+                    uint64_t p, uint64_t psi_p, int device);
+void gala_ctx_destroy(gala_ctx *ctx);
+int gala_set_stream(gala_ctx *ctx, void *cuda_stream);
+int gala_sync(gala_ctx *ctx);
+
+/* Keys (client side, from host-supplied randomness). */
+int gala_set_secret(gala_ctx *ctx, const int8_t *s_host /* [N] ternary */);
+/* a_host: [L][L+1][N] uniform coefficients; e_host: [L][N] signed errors */
+int gala_gen_rotation_key(gala_ctx *ctx, int step, const uint64_t *a_host, const int64_t *e_host);
+int gala_has_rotation_key(gala_ctx *ctx, int step);
+size_t gala_key_bytes(gala_ctx *ctx);
+
+/* encrypt (backend.py:228-234): a_dev [L][N] uniform coefficients, e_dev [N] */
+int gala_encrypt(gala_ctx *ctx, const uint32_t *slots_dev, const uint64_t *a_dev, const int64_t *e_dev,
+                 uint64_t *ct_dev);
+/* decrypt (backend.py:237-243); slots_dev [N] */
+int gala_decrypt(gala_ctx *ctx, const uint64_t *ct_dev, uint32_t *slots_dev);
+/* batch encode of B slot vectors into plaintext operands [B][L][N] */
+int gala_encode_plain(gala_ctx *ctx, const uint32_t *slots_dev, int B, uint64_t *pt_dev);
+
+/* op seam (backend.py:246-311) */
+int gala_add(gala_ctx *ctx, const uint64_t *a_dev, const uint64_t *b_dev, uint64_t *out_dev);   /* he_add */
+int gala_scmult(gala_ctx *ctx, const uint64_t *ct_dev, const uint64_t *pt_dev, uint64_t *out_dev); /* he_scmult */
+int gala_sub_plain(gala_ctx *ctx, const uint64_t *ct_dev, const uint32_t *r_slots_dev,
+                   uint64_t *out_dev);                                                            /* subtract_plain */
+int gala_rotate(gala_ctx *ctx, const uint64_t *ct_dev, int step, uint64_t *out_dev);             /* he_perm */
+/* he_decperm: digits [L][L+1][N] */
+int gala_decompose(gala_ctx *ctx, const uint64_t *ct_dev, uint64_t *digits_dev);
+size_t gala_digits_words(gala_ctx *ctx);
+/* he_hstperm: ct_dev is the group's source (its c0 is rotated directly) */
+int gala_rotate_hoisted(gala_ctx *ctx, const uint64_t *ct_dev, const uint64_t *digits_dev, int step,
+                        uint64_t *out_dev);
+
+/* Fused GALA dot product (mv_gala + gen_additive_share, matvec.py:305-320,
+ * sharing.py:34-45): out = sum_t rot_t(ct (.) pts[t]) over a BSGS tree
+ * (baby <= 0: automatic), masked = out - Delta encode(r).  r_slots_dev
+ * and masked_dev may be NULL. */
+int gala_mv_gala(gala_ctx *ctx, const uint64_t *ct_dev, const uint64_t *pts_dev, int T, int baby,
+                 const uint32_t *r_slots_dev, uint64_t *out_dev, uint64_t *masked_dev);
+int gala_bsgs_baby(int T);
+/* Same with host buffers (canonical words in/out), copies on the context
+ * stream; blocks until the result is in host memory. */
+int gala_mv_gala_host(gala_ctx *ctx, const uint64_t *ct_host, const uint64_t *pts_dev, int T, int baby,
+                      const uint32_t *r_slots_host, uint64_t *masked_host);
+
+/* Fused kernel-grouping convolution (mimo_kernel_grouping, conv.py:268-293):
+ * cts_dev [n_ib][2][L][N]; pts_dev [n_obp][n_ib][c_n][k][L][N];
+ * tap_steps_host [k] (rotation per tap, conv.py:84-91); out [n_obp][2][L][N] */
+int gala_conv_kg(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *pts_dev, int n_obp,
+                 int c_n, int k, const int *tap_steps_host, int band_step, uint64_t *outs_dev);
+
+/* canonical word import/export of `count` ciphertexts */
+int gala_ct_export(gala_ctx *ctx, const uint64_t *ct_dev, uint64_t *coef_dev, int count);
+int gala_ct_import(gala_ctx *ctx, const uint64_t *coef_dev, uint64_t *ct_dev, int count);
+/* canonical plaintext-operand words (coefficients of the centred lift) */
+int gala_pt_export(gala_ctx *ctx, const uint64_t *pt_dev, uint64_t *coef_dev, int count);
+
+/* kernel launches issued by this process so far (for bench accounting) */
+uint64_t gala_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,208 @@
+// gala_device.cuh -- sm_100a device primitives for 60-bit-class RNS arithmetic.
+//
+// Modular multiply flavours (all on the 32-bit IMAD pipe via mul.lo/mul.hi.u64):
+//   * Shoup   (fixed operand w with companion w' = floor(w 2^64 / q)): NTT twiddles
+//   * Montgomery REDC (R = 2^64): plaintext and key operands stored pre-scaled by R,
+//     so products and 128-bit lazy sums reduce with one REDC
+// Harvey lazy butterflies keep NTT values in [0, 4q); all primes are < 2^62.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+typedef uint64_t u64;
+typedef int64_t i64;
+
+#define GALA_MAXM 8   // ciphertext primes + special prime + plaintext modulus
+
+struct ModC {
+    u64 q;        // modulus
+    u64 qinv_neg; // -q^-1 mod 2^64
+    u64 r2;       // 2^128 mod q (to Montgomery form via REDC(x * r2))
+};
+
+// Everything a kernel needs about one BFV context, passed by value.
+struct DevCtx {
+    int N, logN, L, M;          // M = L + 1 (special prime at index L); plaintext at index M
+    ModC mod[GALA_MAXM];
+    const ulonglong2* twf[GALA_MAXM]; // psi^brv(k), Shoup companion
+    const ulonglong2* twi[GALA_MAXM]; // psi^-brv(k), Shoup companion
+    u64 ninv[GALA_MAXM], ninv_sh[GALA_MAXM];
+    u64 delta[GALA_MAXM];       // floor(Q/p) mod q_j
+    u64 delta_sh[GALA_MAXM];
+    u64 pinv_mont[GALA_MAXM];   // P^-1 * R mod q_j (Montgomery operand)
+    u64 qhat_inv[GALA_MAXM];    // [(Q/q_i)^-1]_{q_i}
+    u64 qhat_inv_sh[GALA_MAXM];
+    u64 p;                      // plaintext modulus
+    const u64* S;               // secret, NTT (bit-reversed), Montgomery form, [M][N]
+    const int* slot_pos;        // slot index -> bit-reversed NTT_p position
+};
+
+// ---------------------------------------------------------------------------
+// scalar arithmetic
+__device__ __forceinline__ u64 csub(u64 x, u64 q) { return x >= q ? x - q : x; }
+__device__ __forceinline__ u64 add_mod(u64 a, u64 b, u64 q) { return csub(a + b, q); }
+__device__ __forceinline__ u64 sub_mod(u64 a, u64 b, u64 q) { return a >= b ? a - b : a + q - b; }
+
+// Shoup: x * w mod q, result in [0, 2q) for any x < 2^64 (w < q)
+__device__ __forceinline__ u64 shoup_lazy(u64 x, u64 w, u64 wsh, u64 q)
+{
+    u64 hi = __umul64hi(x, wsh);
+    return x * w - hi * q;
+}
+__device__ __forceinline__ u64 shoup(u64 x, u64 w, u64 wsh, u64 q) { return csub(shoup_lazy(x, w, wsh, q), q); }
+
+// Montgomery REDC of hi:lo < q 2^64: returns (hi:lo) 2^-64 mod q in [0, 2q)
+__device__ __forceinline__ u64 redc_lazy(u64 hi, u64 lo, const ModC& m)
+{
+    u64 mm = lo * m.qinv_neg;
+    u64 t = __umul64hi(mm, m.q);
+    return hi + t + (lo != 0ull ? 1ull : 0ull);
+}
+__device__ __forceinline__ u64 mont_mul(u64 a, u64 b, const ModC& m)
+{
+    return csub(redc_lazy(__umul64hi(a, b), a * b, m), m.q);
+}
+struct Acc128 {
+    u64 lo, hi;
+    __device__ __forceinline__ Acc128() : lo(0), hi(0) {}
+    __device__ __forceinline__ void mac(u64 a, u64 b)
+    {
+        u64 l = a * b, h = __umul64hi(a, b);
+        lo += l;
+        hi += h + (lo < l ? 1ull : 0ull);
+    }
+    __device__ __forceinline__ u64 reduce(const ModC& m) const { return csub(redc_lazy(hi, lo, m), m.q); }
+};
+
+__device__ __forceinline__ int brv(int x, int logN) { return (int)(__brev((unsigned)x) >> (32 - logN)); }
+
+// Galois automorphism X -> X^g on the bit-reversed NTT domain:
+// out[i] = in[ auto_src(i) ]
+__device__ __forceinline__ int auto_src(int i, u64 g, int logN)
+{
+    unsigned two_n_mask = (2u << logN) - 1u;
+    unsigned nat = (unsigned)brv(i, logN);
+    unsigned e = ((2u * nat + 1u) * (unsigned)g) & two_n_mask;
+    return brv((int)((e - 1u) >> 1), logN);
+}
+
+// shared-memory index padding: one 8-byte word per 32 (bank-conflict relief
+// for the small-stride NTT passes)
+__device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
+__host__ __device__ constexpr int padded_words(int n) { return n + (n >> 5); }
+
+// ---------------------------------------------------------------------------
+// In-shared-memory negacyclic NTT.  Forward: Cooley-Tukey, natural -> bit-reversed,
+// merged psi powers; inverse: Gentleman-Sande, bit-reversed -> natural (without the
+// N^-1 scale).  A pass processes R consecutive stages in registers: each thread owns
+// groups of 2^R elements spaced t_end apart.
+template <int R>
+__device__ __forceinline__ void fwd_pass(u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, int s0)
+{
+    const int N = 1 << logN;
+    const int G = N >> R;
+    const int lt = logN - s0 - R;      // log2(t_end)
+    const int t_end = 1 << lt;
+    const u64 q2 = 2 * q;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const int blk = g >> lt, off = g & (t_end - 1);
+        const int base = (blk << (logN - s0)) + off;
+        u64 x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) x[k] = s[pad(base + (k << lt))];
+#pragma unroll
+        for (int l = 0; l < R; l++) {
+            const int m = 1 << (s0 + l);
+            const int half = 1 << (R - 1 - l);
+#pragma unroll
+            for (int k = 0; k < (1 << R); k++) {
+                if (k & half) continue;
+                const ulonglong2 w = __ldg(&tw[m + (blk << l) + (k >> (R - l))]);
+                u64 U = x[k];
+                U = U >= q2 ? U - q2 : U;
+                u64 V = shoup_lazy(x[k + half], w.x, w.y, q);
+                x[k] = U + V;
+                x[k + half] = U - V + q2;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) s[pad(base + (k << lt))] = x[k];
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void inv_pass(u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, int s0)
+{
+    const int N = 1 << logN;
+    const int G = N >> R;
+    const int lt = logN - s0 - R;
+    const int t_end = 1 << lt;
+    const u64 q2 = 2 * q;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const int blk = g >> lt, off = g & (t_end - 1);
+        const int base = (blk << (logN - s0)) + off;
+        u64 x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) x[k] = s[pad(base + (k << lt))];
+#pragma unroll
+        for (int l = R - 1; l >= 0; l--) {
+            const int m = 1 << (s0 + l);
+            const int half = 1 << (R - 1 - l);
+#pragma unroll
+            for (int k = 0; k < (1 << R); k++) {
+                if (k & half) continue;
+                const ulonglong2 w = __ldg(&tw[m + (blk << l) + (k >> (R - l))]);
+                u64 U = x[k], V = x[k + half];
+                u64 a = U + V;
+                x[k] = a >= q2 ? a - q2 : a;
+                x[k + half] = shoup_lazy(U - V + q2, w.x, w.y, q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) s[pad(base + (k << lt))] = x[k];
+    }
+}
+
+#define GALA_NTT_R 4
+
+// input: s[pad(i)] in [0, 4q); output in [0, 4q) (bit-reversed order)
+__device__ __forceinline__ void ntt_fwd_smem(u64* s, const ulonglong2* tw, u64 q, int logN)
+{
+    int s0 = 0;
+    while (s0 < logN) {
+        int r = logN - s0 < GALA_NTT_R ? logN - s0 : GALA_NTT_R;
+        switch (r) {
+            case 4: fwd_pass<4>(s, tw, q, logN, s0); break;
+            case 3: fwd_pass<3>(s, tw, q, logN, s0); break;
+            case 2: fwd_pass<2>(s, tw, q, logN, s0); break;
+            default: fwd_pass<1>(s, tw, q, logN, s0); break;
+        }
+        __syncthreads();
+        s0 += r;
+    }
+}
+
+// input: s[pad(i)] in [0, 2q) bit-reversed; output in [0, 2q) natural, *not* scaled by N^-1
+__device__ __forceinline__ void ntt_inv_smem(u64* s, const ulonglong2* tw, u64 q, int logN)
+{
+    // passes mirror the forward split, executed from the last stage group down
+    int first = logN % GALA_NTT_R;
+    int s0 = logN - (first ? first : GALA_NTT_R);
+    while (s0 >= 0) {
+        int r = logN - s0 < GALA_NTT_R ? logN - s0 : GALA_NTT_R;
+        switch (r) {
+            case 4: inv_pass<4>(s, tw, q, logN, s0); break;
+            case 3: inv_pass<3>(s, tw, q, logN, s0); break;
+            case 2: inv_pass<2>(s, tw, q, logN, s0); break;
+            default: inv_pass<1>(s, tw, q, logN, s0); break;
+        }
+        __syncthreads();
+        s0 -= GALA_NTT_R;
+    }
+}
+
+__host__ __device__ inline int ntt_threads(int N)
+{
+    int t = N >> GALA_NTT_R;
+    return t < 32 ? 32 : t;
+}

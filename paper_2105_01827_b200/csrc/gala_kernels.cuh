@@ -1,0 +1,406 @@
+// gala_kernels.cuh -- sm_100a kernels of the GALA HE linear-layer path.
+//
+// Ciphertexts: u64 [2][L][N] (bit-reversed NTT domain); digits: u64 [L][M][N];
+// keys: u64 [L][2][M][N] Montgomery form; plaintext operands: u64 [L][N]
+// NTT + Montgomery form.  One CTA per polynomial for every transform (the
+// polynomial lives in shared memory for all log N stages); elementwise and
+// key-switch kernels are one thread per coefficient.
+#pragma once
+#include "gala_device.cuh"
+
+// ---------------------------------------------------------------------------
+// addressing of a batch of polynomials (one CTA each)
+struct PolyMap {
+    int per;          // polynomials per item
+    int nprimes;      // prime index = prime_base + (w % nprimes)
+    int prime_base;
+    int src_div;      // source poly within item: w / nprimes (1) or w (0)
+    long long src_is; // item strides (words)
+    long long dst_is;
+    int skip_per;     // >0: item index x -> (x/(skip_per-1))*skip_per + 1 + x%(skip_per-1)
+};
+
+__device__ __forceinline__ void polymap_resolve(const PolyMap& pm, int p, int N, long long& src_off,
+                                                long long& dst_off, int& prime)
+{
+    int item = p / pm.per, w = p - item * pm.per;
+    long long src_item = item;
+    if (pm.skip_per > 0) {
+        int sp = pm.skip_per - 1;
+        src_item = (long long)(item / sp) * pm.skip_per + 1 + item % sp;
+    }
+    prime = pm.prime_base + w % pm.nprimes;
+    src_off = src_item * pm.src_is + (long long)(pm.src_div ? w / pm.nprimes : w) * N;
+    dst_off = (long long)item * pm.dst_is + (long long)w * N;
+}
+
+template <typename T>
+__device__ __forceinline__ u64 to_residue(T v, u64 q);
+template <>
+__device__ __forceinline__ u64 to_residue<u64>(u64 v, u64 q) { return v; } // caller guarantees < 4q
+template <>
+__device__ __forceinline__ u64 to_residue<i64>(i64 v, u64 q)
+{
+    if (v >= 0) return (u64)v % q;
+    u64 r = ((u64)(-v)) % q;
+    return r ? q - r : 0;
+}
+template <>
+__device__ __forceinline__ u64 to_residue<int8_t>(int8_t v, u64 q) { return v >= 0 ? (u64)v : q - (u64)(-v); }
+
+// forward NTT of a batch; output reduced to [0, q), optionally Montgomery-scaled
+template <typename T, bool TO_MONT>
+__global__ void __launch_bounds__(512) k_ntt_fwd(DevCtx c, const T* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
+{
+    extern __shared__ u64 sm[];
+    long long so, dof;
+    int j;
+    polymap_resolve(pm, blockIdx.x, c.N, so, dof, j);
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
+        sm[pad(i)] = to_residue<T>(src[so + i], q);
+    }
+    __syncthreads();
+    ntt_fwd_smem(sm, c.twf[j], q, c.logN);
+    for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
+        u64 v = sm[pad(i)];
+        v = csub(csub(v, 2 * q), q);
+        if (TO_MONT) v = mont_mul(v, md.r2, md);
+        dst[dof + i] = v;
+    }
+}
+
+// inverse NTT of a batch -> coefficients in [0, q)
+template <bool FROM_MONT>
+__global__ void __launch_bounds__(512) k_ntt_inv(DevCtx c, const u64* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
+{
+    extern __shared__ u64 sm[];
+    long long so, dof;
+    int j;
+    polymap_resolve(pm, blockIdx.x, c.N, so, dof, j);
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
+        u64 v = src[so + i];
+        if (FROM_MONT) v = csub(redc_lazy(0, v, md), q);
+        sm[pad(i)] = v;
+    }
+    __syncthreads();
+    ntt_inv_smem(sm, c.twi[j], q, c.logN);
+    const u64 ni = c.ninv[j], nsh = c.ninv_sh[j];
+    for (int i = threadIdx.x; i < c.N; i += blockDim.x) dst[dof + i] = shoup(sm[pad(i)], ni, nsh, q);
+}
+
+// ---------------------------------------------------------------------------
+// ModDown epilogue: items g, w in [0, 2L): comp = w / L, prime j = w % L.
+//   out[g][comp][j] = (U[g][comp][j] - NTT_j(centred r[g][comp])) * P^-1 + add_comp[g][j]
+struct MdArgs {
+    const u64* r;      // [G][2][N] coefficients mod P
+    const u64* U;      // [G][2][M][N]
+    const u64* add0;   // [G] stride add_is, c0 addend [L][N] (may be null)
+    const u64* add1;   // c1 addend
+    long long add_is;
+    u64* out;          // [G] stride out_is, [2][L][N]
+    long long out_is;
+};
+
+__global__ void __launch_bounds__(512) k_moddown(DevCtx c, MdArgs a)
+{
+    extern __shared__ u64 sm[];
+    const int L = c.L, M = c.M, N = c.N;
+    const int g = blockIdx.x / (2 * L), w = blockIdx.x % (2 * L);
+    const int comp = w / L, j = w % L;
+    const ModC md = c.mod[j];
+    const u64 q = md.q, P = c.mod[L].q, halfP = P >> 1;
+    const u64* r = a.r + ((long long)g * 2 + comp) * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        u64 v = r[i];
+        // centred lift of v in [0, P) into [0, 2q): |v - P| < P/2 < q
+        sm[pad(i)] = v > halfP ? q - (P - v) : v; // P/2 < q_j asserted at context creation
+    }
+    __syncthreads();
+    ntt_fwd_smem(sm, c.twf[j], q, c.logN);
+    const u64* U = a.U + (((long long)g * 2 + comp) * M + j) * N;
+    const u64* add = comp == 0 ? a.add0 : a.add1;
+    if (add) add += (long long)g * a.add_is + (long long)j * N;
+    u64* out = a.out + (long long)g * a.out_is + ((long long)comp * L + j) * N;
+    const u64 pinv = c.pinv_mont[j];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        u64 R = csub(csub(sm[pad(i)], 2 * q), q);
+        u64 v = mont_mul(sub_mod(U[i], R, q), pinv, md);
+        if (add) v = add_mod(v, add[i], q);
+        out[i] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Key-switch inner product with automorphism, accumulated over the items of a
+// group (lazy ModDown: one ModDown per group afterwards).
+struct KsItem {
+    const u64* D;     // digits [L][M][N] (NTT), null for a step-0 item
+    const u64* X;     // source ciphertext [2][L][N]
+    const u64* key;   // [L][2][M][N], null for a step-0 item
+    unsigned galois;  // 3^step mod 2N (1 for step 0)
+    int step0;
+};
+
+// grid: (N / blockDim.x, M, G); U [G][2][M][N]; Cacc [G][2][L][N]
+__global__ void __launch_bounds__(256) k_ks_accum(DevCtx c, const KsItem* __restrict__ items,
+                                                  const int* __restrict__ group_off, u64* __restrict__ U,
+                                                  u64* __restrict__ Cacc)
+{
+    const int N = c.N, L = c.L, M = c.M;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, g = blockIdx.z;
+    if (k >= N) return;
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    u64 u0 = 0, u1 = 0, a0 = 0, a1 = 0;
+    const int lo = group_off[g], hi = group_off[g + 1];
+    for (int it = lo; it < hi; it++) {
+        const KsItem I = items[it];
+        if (I.step0) {
+            if (j < L) {
+                a0 = add_mod(a0, I.X[(long long)j * N + k], q);
+                a1 = add_mod(a1, I.X[((long long)L + j) * N + k], q);
+            }
+            continue;
+        }
+        const int src = auto_src(k, I.galois, c.logN);
+        Acc128 s0, s1;
+#pragma unroll 4
+        for (int i = 0; i < L; i++) {
+            const u64 d = I.D[((long long)i * M + j) * N + src];
+            s0.mac(d, I.key[(((long long)i * 2 + 0) * M + j) * N + k]);
+            s1.mac(d, I.key[(((long long)i * 2 + 1) * M + j) * N + k]);
+        }
+        u0 = add_mod(u0, s0.reduce(md), q);
+        u1 = add_mod(u1, s1.reduce(md), q);
+        if (j < L) a0 = add_mod(a0, I.X[(long long)j * N + src], q);
+    }
+    U[(((long long)g * 2 + 0) * M + j) * N + k] = u0;
+    U[(((long long)g * 2 + 1) * M + j) * N + k] = u1;
+    if (j < L) {
+        Cacc[(((long long)g * 2 + 0) * L + j) * N + k] = a0;
+        Cacc[(((long long)g * 2 + 1) * L + j) * N + k] = a1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise
+// out[t] = ct (.) pt[t]; grid (2 L N / blockDim, T)
+__global__ void k_ct_mul_pts(DevCtx c, const u64* __restrict__ ct, const u64* __restrict__ pts,
+                             u64* __restrict__ out)
+{
+    const int LN = c.L * c.N;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long t = blockIdx.y;
+    if (x >= 2 * LN) return;
+    const int jl = x < LN ? x : x - LN;
+    const int j = jl >> c.logN;
+    out[t * 2 * LN + x] = mont_mul(ct[x], __ldg(&pts[t * LN + jl]), c.mod[j]);
+}
+
+// out = a + b (sign = +1) or a - b (sign = -1) over `polys` polys of nprimes-periodic primes
+__global__ void k_addsub(DevCtx c, const u64* __restrict__ a, const u64* __restrict__ b, u64* __restrict__ out,
+                         long long total, int nprimes, int sign)
+{
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        int j = (int)((x / c.N) % nprimes);
+        u64 q = c.mod[j].q;
+        out[x] = sign > 0 ? add_mod(a[x], b[x], q) : sub_mod(a[x], b[x], q);
+    }
+}
+
+// conv first-Add: acc[o][d][comp][j][k] = sum_ib sum_tap R[ib][tap][comp][j][k] * pt[o][ib][d][tap][j][k]
+// grid: (N/blockDim, L, n_obp * c_n)
+__global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __restrict__ R, int n_ib, int k,
+                                                       const u64* __restrict__ pts, int c_n, u64* __restrict__ acc)
+{
+    const int N = c.N, L = c.L;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, od = blockIdx.z;
+    const int o = od / c_n, d = od % c_n;
+    if (x >= N) return;
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    const long long LN = (long long)L * N, W = 2 * LN;
+    u64 s0 = 0, s1 = 0;
+    for (int ib = 0; ib < n_ib; ib++) {
+        const u64* pt = pts + ((((long long)o * n_ib + ib) * c_n + d) * k) * LN + (long long)j * N + x;
+        const u64* Rb = R + ((long long)ib * k) * W + (long long)j * N + x;
+        Acc128 a0, a1;
+        for (int t = 0; t < k; t++) {
+            const u64 w = __ldg(pt + t * LN);
+            a0.mac(Rb[t * W], w);
+            a1.mac(Rb[t * W + LN], w);
+            if ((t & 3) == 3 || t == k - 1) { // four products < 4 q^2 < q 2^64 (q < 2^62)
+                s0 = add_mod(s0, a0.reduce(md), q);
+                s1 = add_mod(s1, a1.reduce(md), q);
+                a0 = Acc128();
+                a1 = Acc128();
+            }
+        }
+    }
+    u64* out = acc + (long long)od * W + (long long)j * N + x;
+    out[0] = s0;
+    out[LN] = s1;
+}
+
+// ---------------------------------------------------------------------------
+// encoding.  MODE 0: plaintext operand (centred lift, Montgomery);
+//            MODE 1: Delta * m (plain), for encrypt / subtract_plain
+// one CTA per (vector b, prime j); each CTA recomputes the mod-p INTT (cheap,
+// p is a 20-bit modulus) to keep the kernel single-pass.
+template <int MODE>
+__global__ void __launch_bounds__(512) k_encode(DevCtx c, const uint32_t* __restrict__ slots, u64* __restrict__ out)
+{
+    extern __shared__ u64 smem_enc[];
+    u64* sm = smem_enc;
+    const int N = c.N, L = c.L, PM = c.M; // plaintext tables at index M
+    const int b = blockIdx.x / L, j = blockIdx.x % L;
+    const uint32_t* sl = slots + (long long)b * N;
+    const u64 p = c.p;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(c.slot_pos[i])] = sl[i] % p;
+    __syncthreads();
+    ntt_inv_smem(sm, c.twi[PM], p, c.logN);
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    u64* sm2 = sm + padded_words(N);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        u64 m = shoup(sm[pad(i)], c.ninv[PM], c.ninv_sh[PM], p);
+        u64 v;
+        if (MODE == 0) v = m > (p >> 1) ? q - (p - m) : m;
+        else v = shoup(m, c.delta[j], c.delta_sh[j], q);
+        sm2[pad(i)] = v;
+    }
+    __syncthreads();
+    sm = sm2;
+    ntt_fwd_smem(sm, c.twf[j], q, c.logN);
+    u64* o = out + ((long long)b * L + j) * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        u64 v = csub(csub(sm[pad(i)], 2 * q), q);
+        if (MODE == 0) v = mont_mul(v, md.r2, md);
+        o[i] = v;
+    }
+}
+
+// decrypt phase 1: per prime j: x_j = INTT(c0 + c1 * S)
+__global__ void __launch_bounds__(512) k_dec_phase1(DevCtx c, const u64* __restrict__ ct, u64* __restrict__ x)
+{
+    extern __shared__ u64 sm[];
+    const int N = c.N, L = c.L, j = blockIdx.x;
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    const u64* c0 = ct + (long long)j * N;
+    const u64* c1 = ct + ((long long)L + j) * N;
+    const u64* S = c.S + (long long)j * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(i)] = add_mod(c0[i], mont_mul(c1[i], S[i], md), q);
+    __syncthreads();
+    ntt_inv_smem(sm, c.twi[j], q, c.logN);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) x[(long long)j * N + i] = shoup(sm[pad(i)], c.ninv[j], c.ninv_sh[j], q);
+}
+
+// floor(b 2^64 / q) for b < q < 2^63 (restoring division)
+__device__ __forceinline__ u64 frac64(u64 b, u64 q)
+{
+    u64 r = b, qt = 0;
+#pragma unroll 8
+    for (int i = 0; i < 64; i++) {
+        r <<= 1;
+        qt <<= 1;
+        if (r >= q) { r -= q; qt |= 1; }
+    }
+    return qt;
+}
+
+// decrypt phase 2 (one CTA): m = round(p x / Q) mod p via RNS; slots = decode(m)
+__global__ void __launch_bounds__(512) k_dec_phase2(DevCtx c, const u64* __restrict__ x, uint32_t* __restrict__ slots)
+{
+    extern __shared__ u64 sm[];
+    const int N = c.N, L = c.L, PM = c.M;
+    const u64 p = c.p;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        u64 sum_a = 0, f_lo = 0, f_hi = 0;
+        for (int j = 0; j < L; j++) {
+            const u64 q = c.mod[j].q;
+            u64 y = shoup(x[(long long)j * N + i], c.qhat_inv[j], c.qhat_inv_sh[j], q);
+            // y * p = a q + b
+            u64 lo = y * p, hi = __umul64hi(y, p);
+            u64 a = (u64)((double)y * ((double)p / (double)q));
+            // exact correction: rem = y p - a q (signed 128)
+            u64 aql = a * q, aqh = __umul64hi(a, q);
+            u64 rl = lo - aql;
+            i64 rh = (i64)(hi - aqh - (lo < aql ? 1 : 0));
+            while (rh < 0) { // rem += q, a -= 1
+                u64 n = rl + q;
+                rh += (n < rl) ? 1 : 0;
+                rl = n;
+                a -= 1;
+            }
+            while (rh > 0 || rl >= q) {
+                u64 n = rl - q;
+                rh -= (rl < q) ? 1 : 0;
+                rl = n;
+                a += 1;
+            }
+            sum_a += a;
+            u64 f = frac64(rl, q);
+            f_lo += f;
+            f_hi += (f_lo < f) ? 1 : 0;
+        }
+        // round: add 2^63 to the 128-bit fraction sum, take the integer part
+        u64 t = f_lo + (1ull << 63);
+        u64 carry = (t < f_lo) ? 1 : 0;
+        u64 rounded = sum_a + f_hi + carry;
+        sm[pad(i)] = rounded % p;
+    }
+    __syncthreads();
+    ntt_fwd_smem(sm, c.twf[PM], p, c.logN);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        u64 v = sm[pad(c.slot_pos[i])];
+        slots[i] = (uint32_t)(v % p);
+    }
+}
+
+// key generation combine: per (i, j) poly and coefficient k
+//   key[i][0][j] = mont(E - A S + [i==j] (P mod q_j) sigma(S)),  key[i][1][j] = mont(A)
+__global__ void k_keygen_combine(DevCtx c, const u64* __restrict__ A, const u64* __restrict__ E, unsigned galois,
+                                 const u64* __restrict__ pmod, u64* __restrict__ key)
+{
+    const int N = c.N, L = c.L, M = c.M;
+    const long long total = (long long)L * M * N;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        int k = (int)(x % N);
+        int ij = (int)(x / N);
+        int i = ij / M, j = ij % M;
+        const ModC md = c.mod[j];
+        const u64 q = md.q;
+        const u64* S = c.S + (long long)j * N;
+        u64 a = A[x];
+        u64 b = sub_mod(E[x], mont_mul(a, S[k], md), q);
+        if (i == j) b = add_mod(b, mont_mul(S[auto_src(k, galois, c.logN)], pmod[j], md), q);
+        key[(((long long)i * 2 + 0) * M + j) * N + k] = mont_mul(b, md.r2, md);
+        key[(((long long)i * 2 + 1) * M + j) * N + k] = mont_mul(a, md.r2, md);
+    }
+}
+
+// encrypt combine: ct.c1 = A, ct.c0 = E - A S + DM
+__global__ void k_encrypt_combine(DevCtx c, const u64* __restrict__ A, const u64* __restrict__ E,
+                                  const u64* __restrict__ DM, u64* __restrict__ ct)
+{
+    const int N = c.N, L = c.L;
+    const long long total = (long long)L * N;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        int j = (int)(x / N);
+        const ModC md = c.mod[j];
+        const u64 q = md.q;
+        u64 a = A[x];
+        ct[x] = add_mod(sub_mod(E[x], mont_mul(a, c.S[x], md), q), DM[x], q);
+        ct[total + x] = a;
+    }
+}

@@ -1,0 +1,98 @@
+"""Word-level parity: CUDA library vs the CPU BFV oracle (same randomness)."""
+import numpy as np
+import pytest
+
+from twins import P, Twin
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(4, 1), (32, 1), (32, 3), (256, 2), (2048, 1), (4096, 3)]
+
+
+@pytest.fixture(scope="module", params=SHAPES, ids=lambda s: f"n{s[0]}L{s[1]}")
+def tw(request):
+    n, L = request.param
+    return Twin(n, L)
+
+
+def test_encrypt_words_and_decrypt(tw):
+    x = tw.slots()
+    g, c = tw.encrypt(x)
+    assert np.array_equal(tw.gpu.export_words(g), c)
+    assert np.array_equal(tw.gpu.decrypt_physical(g), x.astype(np.int64))
+
+
+def test_encode_plain_words(tw):
+    s = tw.slots(3)
+    pts = tw.gpu.encode_plain(s)
+    got = tw.gpu.export_plain(pts)
+    for i in range(3):
+        assert np.array_equal(got[i], tw.cpu.encode(s[i]))
+
+
+def test_add_scmult_subplain_words(tw):
+    x, y, r = tw.slots(), tw.slots(), tw.slots()
+    g1, c1 = tw.encrypt(x)
+    g2, c2 = tw.encrypt(y)
+    assert np.array_equal(tw.gpu.export_words(tw.gpu.add(g1, g2)), tw.cpu.add(c1, c2))
+    pt = tw.gpu.encode_plain(y)[0]
+    gs = tw.gpu.scmult(g1, pt)
+    assert np.array_equal(tw.gpu.export_words(gs), tw.cpu.scmult(c1, y))
+    assert np.array_equal(tw.gpu.decrypt_physical(gs), (x.astype(np.int64) * y) % P)
+    gsub = tw.gpu.sub_plain(g1, r)
+    assert np.array_equal(tw.gpu.export_words(gsub), tw.cpu.sub_plain(c1, r))
+
+
+def test_rotations_words(tw):
+    n = tw.bfv.n
+    steps = sorted({1, 3 % n, n - 1, n // 2})
+    tw.keys_for(steps)
+    x = tw.slots()
+    g, c = tw.encrypt(x)
+    want = tw.cpu.rotate_hoisted(c, steps)
+    D = tw.gpu.decompose(g)
+    for s, w in zip(steps, want):
+        gr = tw.gpu.rotate(g, s)
+        assert np.array_equal(tw.gpu.export_words(gr), w), s
+        gh = tw.gpu.rotate_hoisted(g, D, s)
+        assert np.array_equal(tw.gpu.export_words(gh), w), s
+        dec = tw.gpu.decrypt_physical(gr)
+        xs = x.astype(np.int64)
+        assert np.array_equal(dec, np.concatenate([np.roll(xs[:n], -s), np.roll(xs[n:], -s)]))
+
+
+@pytest.mark.parametrize("T", [1, 2, 4, 8, 16])
+def test_mv_gala_words(tw, T):
+    n = tw.bfv.n
+    if T > n:
+        pytest.skip("T > n")
+    b, steps = tw.gpu.bsgs_steps(T)
+    tw.keys_for(steps)
+    x = tw.slots()
+    pts = tw.slots(T)
+    r = tw.slots()
+    g, c = tw.encrypt(x)
+    out, masked = tw.gpu.mv_gala(g, tw.gpu.encode_plain(pts), T, r)
+    c_out, c_masked = tw.cpu.mv_gala(c, pts, r, baby=b)
+    assert np.array_equal(tw.gpu.export_words(out), c_out)
+    assert np.array_equal(tw.gpu.export_words(masked), c_masked)
+
+
+def test_conv_kg_words(tw):
+    n = tw.bfv.n
+    if n < 16:
+        pytest.skip("tiny")
+    band = n // 4
+    c_n, k, n_ib, n_obp = 4, 3, 2, 2
+    tap_steps = [0, 1, n - 1]
+    tw.keys_for(tap_steps + [d * band for d in range(1, c_n)])
+    xs = [tw.encrypt(tw.slots()) for _ in range(n_ib)]
+    pts = tw.slots(n_obp * n_ib * c_n * k).reshape(n_obp, n_ib, c_n, k, tw.N)
+    import torch
+
+    g_in = torch.stack([g for g, _ in xs])
+    c_in = np.stack([c for _, c in xs])
+    d_pts = tw.gpu.encode_plain(pts.reshape(-1, tw.N)).view(n_obp, n_ib, c_n, k, tw.L, tw.N)
+    g_out = tw.gpu.conv_kg(g_in, d_pts, tap_steps, band)
+    c_out = tw.cpu.conv_kg(c_in, pts, tap_steps, band)
+    assert np.array_equal(tw.gpu.export_words(g_out), c_out)
