@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""bench.py -- GALA FC dot product at scale on B200 (BASELINE.json configs[1]).
+
+Workload (one "layer"): a 1024 x 4096 int8 weight matrix (mapped into Z_p,
+p = 1032193) against one encrypted input vector of 4096 values, RNS-BFV with
+N = 8192, three 60-bit ciphertext primes + one special prime.  The layer is
+split into two reference MvTasks (512 x 4096 each, n = 4096, T = 512) paired
+on the two hypercube rows of one ciphertext; every layer runs the fused GALA
+product (T ScMult, T-1 key-switched rotations on a BSGS tree, lazy ModDown)
+and the share-mask subtraction.  A step = one pass over a batch of
+independent encrypted inputs already resident in HBM.
+
+Output: one JSON line (driver contract); see DESIGN.md "Measurement".
+  --impl reference : the CPU path (oracle/ port of the same algorithm, all host
+                     threads) on the same config/metric -- the reference package
+                     itself is a pure-Python mock without HE arithmetic.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HE linear-layer throughput (layers/s, rotations/s) + % of INT/HBM roofline"
+P = 1032193
+N_OUT, N_IN, SLOTS = 1024, 4096, 4096   # configs[1]
+WORKLOAD = "gala_fc_1024x4096_N8192_L3"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=8, help="independent layers (inputs) per step per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="run one profiled step and print the breakdown")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def weights(seed=2105):
+    rng = np.random.default_rng(seed)
+    return rng.integers(-128, 128, (N_OUT, N_IN), dtype=np.int64) % P
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def modmul_model(N, L, T, baby):
+    from paper_2105_01827_b200.analytics import ks_modmuls, ntt_modmuls, physical_mv_counts
+
+    G = T // baby
+    h = ntt_modmuls(N)
+    M = L + 1
+    rot_items = G * (baby - 1) + (G - 1)
+    groups = G + (1 if G > 1 else 0)
+    per_kernel = {
+        "k_ct_mul_pts": 2 * L * N * T,
+        "k_digits_intt": rot_items * L * h + 2 * L * N * rot_items,
+        "k_digits_perm": rot_items * L * L * h,          # digit i into the L other primes (j != i)
+        "k_ks_mac": rot_items * 2 * L * M * N,
+        "k_ntt_inv[moddown]": groups * 2 * h,
+        "k_moddown": groups * (2 * L * h + 2 * L * N),
+    }
+    total = physical_mv_counts(N, L, T, baby)["modmuls"]
+    return per_kernel, total
+
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2105_01827_b200 import _lib
+    from paper_2105_01827_b200.backend import HEParams
+    from paper_2105_01827_b200.matvec import GalaFC
+
+    params = HEParams(n=SLOTS, p=P, rns_limbs=3, device=local, seed=7)
+    t_setup = time.perf_counter()
+    layer = GalaFC(weights(), params)
+    ctx = layer.ctx
+    N, L, T, baby = ctx.N, ctx.L, layer.T, layer.baby
+    B = args.batch
+    rng = np.random.default_rng(1000 + rank)
+    xs = [rng.integers(0, P, N_IN) for _ in range(B)]
+    cts = [layer.encrypt_input(x)[0] for x in xs]                     # client side, resident in HBM
+    masks = [layer.draw_masks(5000 + 100 * rank + b) for b in range(B)]
+    phys_r = [ctx.physical(m[0][0].slots, m[0][1].slots) for m in masks]
+    d_r = [ctx.to_device_u32(r) for r in phys_r]
+    pts = layer.blocks[0][1]
+    outs = [ctx.empty_ct() for _ in range(B)]
+    masked = [ctx.empty_ct() for _ in range(B)]
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    def step():
+        for b in range(B):
+            ctx.mv_gala(cts[b], pts, T, d_r[b], baby, out=outs[b], masked=masked[b])
+
+    # correctness gate before timing: decrypted shares == W x mod p
+    w = weights()
+    step()
+    for b in range(min(B, 2)):
+        got = (layer.client_shares([masked[b]]) + layer.server_shares(masks[b])) % P
+        want = (w @ xs[b]) % P
+        if not np.array_equal(got, want):
+            raise SystemExit(f"parity gate failed on input {b}")
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # profile pass (untimed): per-kernel CUDA-event breakdown of one step
+    ctx.profile(True)
+    step()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    if args.profile_only and rank == 0:
+        print(json.dumps(prof, indent=1))
+        return
+
+    stream = torch.cuda.current_stream(dev)
+    launches0 = _lib.launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = _lib.launch_count() - launches0
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    layers = B * args.steps * world
+    value = layers / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+
+    # e2e: host buffers through the C-ABI host entry point (H2D ct + r, fused layer, D2H masked)
+    import ctypes
+
+    host_ct = [torch.from_numpy(ctx.export_words(c).view(np.int64)).pin_memory() for c in cts]
+    host_r = [torch.from_numpy(r.view(np.int32)).pin_memory() for r in phys_r]
+    host_out = [torch.empty((2, L, N), dtype=torch.int64).pin_memory() for _ in range(B)]
+    h = ctx._bind()
+
+    def e2e_step():
+        for b in range(B):
+            _lib.check(ctx.lib.gala_mv_gala_host(h, ctypes.c_void_p(host_ct[b].data_ptr()),
+                                                 ctypes.c_void_p(pts.data_ptr()), T, baby,
+                                                 ctypes.c_void_p(host_r[b].data_ptr()),
+                                                 ctypes.c_void_p(host_out[b].data_ptr())))
+
+    e2e_step()
+    # e2e parity: host-path masked words equal the device-path masked words
+    for b in range(min(B, 2)):
+        if not np.array_equal(host_out[b].numpy().view(np.uint64), ctx.export_words(masked[b])):
+            raise SystemExit("e2e host path disagrees with device path")
+    e2e_times = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_times.append(e0.elapsed_time(e1))
+    e2e_ms = sum(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = layers / (e2e_ms / 1e3)
+
+    # roofline: integer-multiply bound (modmul count) -- peak measured live with the library's own modmul
+    peak_modmul = ctx.bench_modmul()
+    per_kernel, layer_modmuls = modmul_model(N, L, T, baby)
+    dominant = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    dom_name, dom = dominant
+    step_ms_prof = sum(v["ms"] for v in prof.values())
+    dom_work = per_kernel.get(dom_name, 0) * B
+    dom_achieved = dom_work / (dom["ms"] / 1e3) if dom["ms"] else 0.0
+    layer_achieved = layer_modmuls * layers / world / (total_ms / 1e3)
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    pt_bytes = T * L * N * 8
+    key_bytes = ctx.key_bytes()
+    ct_bytes = 2 * L * N * 8
+    layer_bytes = pt_bytes / B + key_bytes / B + 3 * ct_bytes + N * 4   # weights/keys amortised over the batch
+
+    result = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "layers/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64 (RNS residues mod 60-bit primes)",
+        "data": "synthetic (seeded int8 weights mapped to Z_p, uniform Z_p inputs)",
+        "config": {"workload": WORKLOAD, "layer": "GALA FC 1024x4096 (2 paired MvTasks of 512x4096, T=512)",
+                   "N": N, "L": L, "special_primes": 1, "p": P, "bsgs_baby": baby, "batch_per_gpu": B,
+                   "parallelism": f"replicas x{world} (independent inputs per GPU)",
+                   "l2": "flushed (256 MB write) before every timed step"},
+        "rotations_per_s": round(value * (T - 1), 1),
+        "roofline": {
+            "bound": "int",
+            "kernel": dom_name,
+            "achieved": round(dom_achieved / 1e9, 2),
+            "peak": round(peak_modmul / 1e9, 2),
+            "unit": "Gmodmul/s",
+            "frac": round(dom_achieved / peak_modmul, 4) if peak_modmul else None,
+            "traffic": None,
+            "kernel_share_of_step": round(dom["ms"] / step_ms_prof, 4) if step_ms_prof else None,
+            "peak_source": "measured live: gala_bench_modmul (60-bit Shoup modmul chains, all SMs)",
+            "layer": {"achieved": round(layer_achieved / 1e9, 2), "frac": round(layer_achieved / peak_modmul, 4),
+                      "modmuls_per_layer": layer_modmuls},
+            "hbm": {"algorithmic_bytes_per_layer": int(layer_bytes),
+                    "achieved_gbs": round(layer_bytes * layers / world / (total_ms / 1e3) / 1e9, 2),
+                    "peak_gbs": hbm_peak},
+        },
+        "kernel_breakdown_ms_per_step": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
+        "e2e": {"value": round(e2e_value, 3), "unit": "layers/s",
+                "h2d_bytes_per_step": B * (ct_bytes + N * 4), "d2h_bytes_per_step": B * ct_bytes,
+                "path": "gala_mv_gala_host (C-ABI, pinned host buffers, canonical words)"},
+        "gpu_launches": int(launches),
+        "setup_s": round(setup_s, 2),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(ctx, layer, cts[0], phys_r[0], masked[0])
+    if rank == 0:
+        print(json.dumps(result))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def _oracle_for(bfv, seed):
+    """CPU oracle with the GPU context's secret and rotation keys (same host randomness)."""
+    from oracle.bfv import Oracle
+    from paper_2105_01827_b200 import sampling
+
+    o = Oracle(bfv)
+    o.set_secret(sampling.secret(np.random.default_rng([seed, 0]), bfv.N))
+    return o
+
+
+def cpu_baseline(ctx, layer, ct, phys_r, masked_gpu):
+    """Oracle port of the same fused layer, timed on the host cores (one layer = the sample)."""
+    from oracle.bfv import num_threads
+    from paper_2105_01827_b200 import sampling
+
+    bfv = ctx.bfv
+    o = _oracle_for(bfv, ctx.seed)
+    for s in layer.steps:
+        a, e = sampling.rotation_key_randomness(np.random.default_rng([ctx.seed, 1, s]), bfv)
+        o.gen_rotkey(s, a, e)
+    tasks = layer.blocks[0][0]
+    from paper_2105_01827_b200.matvec import gala_weight_slots
+
+    pts = np.concatenate([gala_weight_slots(tasks[0]), gala_weight_slots(tasks[1])], axis=1).astype(np.uint32)
+    words = ctx.export_words(ct)
+    t0 = time.perf_counter()
+    _, m = o.mv_gala(words, pts, phys_r, baby=layer.baby)
+    dt = time.perf_counter() - t0
+    match = bool(np.array_equal(m, ctx.export_words(masked_gpu)))
+    return {"value": round(1.0 / dt, 4), "unit": "layers/s", "cores": num_threads(), "kind": "port",
+            "sample": "1 layer (same input ct, keys and mask as GPU input 0); oracle/bfv_oracle.c, OpenMP",
+            "words_match_gpu": match, "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.bfv import num_threads
+    from paper_2105_01827_b200 import sampling
+    from paper_2105_01827_b200.matvec import MvTask, gala_weight_slots, pack_input
+    from paper_2105_01827_b200.params import derive
+
+    bfv = derive(SLOTS, P, 3)
+    seed = 7
+    o = _oracle_for(bfv, seed)
+    w = weights()
+    from paper_2105_01827_b200.backend import HEParams
+
+    params = HEParams(n=SLOTS, p=P, rns_limbs=3, seed=seed)
+    tasks = [MvTask(N_IN, N_OUT // 2, w[:N_OUT // 2], params), MvTask(N_IN, N_OUT // 2, w[N_OUT // 2:], params)]
+    pts = np.concatenate([gala_weight_slots(tasks[0]), gala_weight_slots(tasks[1])], axis=1).astype(np.uint32)
+    T = pts.shape[0]
+    from oracle.bfv import bsgs_baby
+
+    baby = bsgs_baby(T)
+    G = T // baby
+    for s in sorted({j for j in range(1, baby)} | {g * baby for g in range(1, G)}):
+        a, e = sampling.rotation_key_randomness(np.random.default_rng([seed, 1, s]), bfv)
+        o.gen_rotkey(s, a, e)
+    rng = np.random.default_rng(1000)
+    x = rng.integers(0, P, N_IN)
+    xs = pack_input(x, tasks[0]).slots
+    phys = np.concatenate([xs, xs]).astype(np.uint32)
+    a, e = sampling.encryption_randomness(np.random.default_rng([seed, 2, 0]), bfv)
+    ct = o.encrypt(phys, a, e)
+    r = np.random.default_rng(5000).integers(0, P, 2 * SLOTS).astype(np.uint32)
+    if args.warmup > 0:
+        o.mv_gala(ct, pts, r, baby=baby)   # one warm-up layer (bounded CPU sample)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.mv_gala(ct, pts, r, baby=baby)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = args.steps / total
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": "layers/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues mod 60-bit primes)",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "N": bfv.N, "L": bfv.L, "bsgs_baby": baby, "batch_per_step": 1},
+        "cpu_baseline": {"value": round(value, 4), "unit": "layers/s", "cores": num_threads(), "kind": "port",
+                         "sample": "1 layer per step: oracle/bfv_oracle.c (same algorithm), OpenMP, all host threads"},
+        "e2e": {"value": round(value, 4), "unit": "layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference package's own backend is a pure-Python slot mock without HE arithmetic; "
+                "the CPU arm runs the restated RNS-BFV algorithm (oracle/) on the host cores",
+    }
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

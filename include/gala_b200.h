@@ -112,6 +112,16 @@ int gala_pt_export(gala_ctx *ctx, const uint64_t *pt_dev, uint64_t *coef_dev, in
 /* kernel launches issued by this process so far (for bench accounting) */
 uint64_t gala_launch_count(void);
 
+/* Tracing: per-kernel CUDA-event timing of every launch while enabled.
+ * gala_profile_json synchronises, writes {"kernel": [launches, total_ms], ...}
+ * and clears the records. */
+int gala_profile_enable(gala_ctx *ctx, int on);
+int gala_profile_json(gala_ctx *ctx, char *buf, size_t cap);
+
+/* Throughput probe of the library's 60-bit Shoup modmul (modmul/s); the
+ * integer-roofline denominator used by bench.py. */
+int gala_bench_modmul(gala_ctx *ctx, int blocks, int iters, double *modmul_per_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -364,7 +364,7 @@ class Context:
 
     def decompose(self, ct):
         torch = _torch()
-        D = torch.empty((self.L, self.L + 1, self.N), dtype=torch.int64, device=self.device)
+        D = torch.empty(int(self.lib.gala_digits_words(self._h)), dtype=torch.int64, device=self.device)
         self.call("gala_decompose", ctypes.c_void_p(_ptr(ct)), ctypes.c_void_p(_ptr(D)))
         return D
 
@@ -380,12 +380,19 @@ class Context:
         G = T // b
         return b, sorted({self.norm_step(j) for j in range(1, b)} | {self.norm_step(g * b) for g in range(1, G)} - {0})
 
-    def mv_gala(self, ct, pts, T: int, phys_r: np.ndarray | None, baby: int | None = None):
+    def mv_gala(self, ct, pts, T: int, phys_r=None, baby: int | None = None, out=None, masked=None):
+        """Fused GALA product; phys_r: physical mask slots (numpy or device int32 tensor)."""
         b, steps = self.bsgs_steps(T, baby)
         self.ensure_keys(steps)
-        out = self.empty_ct()
-        masked = self.empty_ct() if phys_r is not None else None
-        d_r = self.to_device_u32(phys_r) if phys_r is not None else None
+        out = self.empty_ct() if out is None else out
+        if phys_r is not None and masked is None:
+            masked = self.empty_ct()
+        if phys_r is None:
+            d_r = None
+        elif isinstance(phys_r, np.ndarray):
+            d_r = self.to_device_u32(phys_r)
+        else:
+            d_r = phys_r
         self.call("gala_mv_gala", ctypes.c_void_p(_ptr(ct)), ctypes.c_void_p(_ptr(pts)), int(T), int(b),
                   ctypes.c_void_p(_ptr(d_r)) if d_r is not None else None, ctypes.c_void_p(_ptr(out)),
                   ctypes.c_void_p(_ptr(masked)) if masked is not None else None)
@@ -403,6 +410,21 @@ class Context:
 
     def sync(self):
         self.call("gala_sync")
+
+    # -- tracing / probes ------------------------------------------------------
+    def profile(self, on: bool) -> None:
+        self.call("gala_profile_enable", int(bool(on)))
+
+    def profile_read(self) -> dict:
+        buf = ctypes.create_string_buffer(1 << 16)
+        self.call("gala_profile_json", buf, len(buf))
+        raw = json.loads(buf.value.decode())
+        return {k: {"launches": int(v[0]), "ms": float(v[1])} for k, v in raw.items()}
+
+    def bench_modmul(self, blocks: int = 148 * 16, iters: int = 4096) -> float:
+        out = ctypes.c_double()
+        self.call("gala_bench_modmul", int(blocks), int(iters), ctypes.byref(out))
+        return float(out.value)
 
 
 def context(params: HEParams) -> Context:

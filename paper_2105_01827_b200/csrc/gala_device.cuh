@@ -163,7 +163,7 @@ __device__ __forceinline__ void inv_pass(u64* s, const ulonglong2* __restrict__ 
     }
 }
 
-#define GALA_NTT_R 4
+#define GALA_NTT_R 3
 
 // input: s[pad(i)] in [0, 4q); output in [0, 4q) (bit-reversed order)
 __device__ __forceinline__ void ntt_fwd_smem(u64* s, const ulonglong2* tw, u64 q, int logN)

@@ -50,7 +50,7 @@ __device__ __forceinline__ u64 to_residue<int8_t>(int8_t v, u64 q) { return v >=
 
 // forward NTT of a batch; output reduced to [0, q), optionally Montgomery-scaled
 template <typename T, bool TO_MONT>
-__global__ void __launch_bounds__(512) k_ntt_fwd(DevCtx c, const T* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
+__global__ void __launch_bounds__(1024, 1) k_ntt_fwd(DevCtx c, const T* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
 {
     extern __shared__ u64 sm[];
     long long so, dof;
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(512) k_ntt_fwd(DevCtx c, const T* __restrict__
 
 // inverse NTT of a batch -> coefficients in [0, q)
 template <bool FROM_MONT>
-__global__ void __launch_bounds__(512) k_ntt_inv(DevCtx c, const u64* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
+__global__ void __launch_bounds__(1024, 1) k_ntt_inv(DevCtx c, const u64* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
 {
     extern __shared__ u64 sm[];
     long long so, dof;
@@ -101,11 +101,12 @@ struct MdArgs {
     const u64* add0;   // [G] stride add_is, c0 addend [L][N] (may be null)
     const u64* add1;   // c1 addend
     long long add_is;
-    u64* out;          // [G] stride out_is, [2][L][N]
+    u64* out;          // [G] stride out_is, [2][L][N]   (used when outs == null)
     long long out_is;
+    u64* const* outs;  // optional per-group output pointers
 };
 
-__global__ void __launch_bounds__(512) k_moddown(DevCtx c, MdArgs a)
+__global__ void __launch_bounds__(1024, 1) k_moddown(DevCtx c, MdArgs a)
 {
     extern __shared__ u64 sm[];
     const int L = c.L, M = c.M, N = c.N;
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(512) k_moddown(DevCtx c, MdArgs a)
     const u64* U = a.U + (((long long)g * 2 + comp) * M + j) * N;
     const u64* add = comp == 0 ? a.add0 : a.add1;
     if (add) add += (long long)g * a.add_is + (long long)j * N;
-    u64* out = a.out + (long long)g * a.out_is + ((long long)comp * L + j) * N;
+    u64* out = (a.outs ? a.outs[g] : a.out + (long long)g * a.out_is) + ((long long)comp * L + j) * N;
     const u64 pinv = c.pinv_mont[j];
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         u64 R = csub(csub(sm[pad(i)], 2 * q), q);
@@ -135,20 +136,113 @@ __global__ void __launch_bounds__(512) k_moddown(DevCtx c, MdArgs a)
 }
 
 // ---------------------------------------------------------------------------
-// Key-switch inner product with automorphism, accumulated over the items of a
-// group (lazy ModDown: one ModDown per group afterwards).
-struct KsItem {
-    const u64* D;     // digits [L][M][N] (NTT), null for a step-0 item
-    const u64* X;     // source ciphertext [2][L][N]
-    const u64* key;   // [L][2][M][N], null for a step-0 item
-    unsigned galois;  // 3^step mod 2N (1 for step 0)
-    int step0;
+// Key-switch engine v2.  A "term" is a source ciphertext X, optionally times a
+// plaintext operand pt (so ScMult fuses into the key switch), to be rotated by
+// one or more Galois elements.
+//   k_digits_intt : digits d_i = INTT_i((X (.) pt).c1[i])            [term][L][N]
+//   k_digits_perm : for every rotation r of the term, the block
+//                   [ sigma_r(NTT_j(d_i)) for i<L, j<M ;  sigma_r(c0_j) for j<L ]
+//                   (NTT only for j != i; the j == i limb is the NTT-domain c1)
+//   k_ks_mac      : per group, sum over its rotated blocks of
+//                   sum_i D'[i][j] * key[i][c][j]  (128-bit lazy) and the c0 sums;
+//                   step-0 members add (X (.) pt) directly.
+struct TermDesc {
+    const u64* X;      // [2][L][N] NTT
+    const u64* pt;     // [L][N] Montgomery or null
+    u64* dig;          // [L][N] digit coefficients (scratch)
+    u64* blk;          // first permuted block [(L*M + L)][N]; rotation r at blk + r * blk_words
+    int rot_off, rot_cnt;
 };
 
-// grid: (N / blockDim.x, M, G); U [G][2][M][N]; Cacc [G][2][L][N]
-__global__ void __launch_bounds__(256) k_ks_accum(DevCtx c, const KsItem* __restrict__ items,
-                                                  const int* __restrict__ group_off, u64* __restrict__ U,
-                                                  u64* __restrict__ Cacc)
+__device__ __forceinline__ u64 src_limb(const DevCtx& c, const TermDesc& t, int comp, int j, int k)
+{
+    const long long o = ((long long)comp * c.L + j) * c.N + k;
+    u64 v = t.X[o];
+    if (t.pt) v = mont_mul(v, t.pt[(long long)j * c.N + k], c.mod[j]);
+    return v;
+}
+
+__global__ void __launch_bounds__(1024, 1) k_digits_intt(DevCtx c, const TermDesc* __restrict__ terms)
+{
+    extern __shared__ u64 sm[];
+    const int L = c.L, N = c.N;
+    const int ti = blockIdx.x / L, i = blockIdx.x % L;
+    const TermDesc t = terms[ti];
+    const u64 q = c.mod[i].q;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 1, i, k);
+    __syncthreads();
+    ntt_inv_smem(sm, c.twi[i], q, c.logN);
+    u64* d = t.dig + (long long)i * N;
+    const u64 ni = c.ninv[i], nsh = c.ninv_sh[i];
+    for (int k = threadIdx.x; k < N; k += blockDim.x) d[k] = shoup(sm[pad(k)], ni, nsh, q);
+}
+
+// grid: terms * (L*M + L) CTAs
+__global__ void __launch_bounds__(1024, 1) k_digits_perm(DevCtx c, const TermDesc* __restrict__ terms,
+                                                         const unsigned* __restrict__ galois, long long blk_words)
+{
+    extern __shared__ u64 sm[];
+    const int L = c.L, M = c.M, N = c.N;
+    const int per = L * M + L;
+    const int ti = blockIdx.x / per, slot = blockIdx.x % per;
+    const TermDesc t = terms[ti];
+    int j;
+    if (slot < L * M) {
+        const int i = slot / M;
+        j = slot % M;
+        const u64 q = c.mod[j].q;
+        if (i != j) {
+            const u64* d = t.dig + (long long)i * N;   // d < q_i < 4 q_j: lazy NTT input
+            for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = d[k];
+            __syncthreads();
+            ntt_fwd_smem(sm, c.twf[j], q, c.logN);
+            for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = csub(csub(sm[pad(k)], 2 * q), q);
+        } else {
+            for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 1, j, k);
+        }
+    } else {
+        j = slot - L * M;
+        for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 0, j, k);
+    }
+    __syncthreads();
+    for (int r = 0; r < t.rot_cnt; r++) {
+        const unsigned g = galois[t.rot_off + r];
+        u64* o = t.blk + r * blk_words + (long long)slot * N;
+        for (int k = threadIdx.x; k < N; k += blockDim.x) o[k] = sm[pad(auto_src(k, g, c.logN))];
+    }
+}
+
+// hoisted rotations from a precomputed identity block (the DecPerm output):
+// permutation only.  t.X points at the identity block [(L*M + L)][N].
+__global__ void __launch_bounds__(1024, 1) k_block_perm(DevCtx c, const TermDesc* __restrict__ terms,
+                                                        const unsigned* __restrict__ galois, long long blk_words)
+{
+    extern __shared__ u64 sm[];
+    const int L = c.L, M = c.M, N = c.N;
+    const int per = L * M + L;
+    const int ti = blockIdx.x / per, slot = blockIdx.x % per;
+    const TermDesc t = terms[ti];
+    const u64* src = t.X + (long long)slot * N;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src[k];
+    __syncthreads();
+    for (int r = 0; r < t.rot_cnt; r++) {
+        const unsigned g = galois[t.rot_off + r];
+        u64* o = t.blk + r * blk_words + (long long)slot * N;
+        for (int k = threadIdx.x; k < N; k += blockDim.x) o[k] = sm[pad(auto_src(k, g, c.logN))];
+    }
+}
+
+struct MacMember {
+    const u64* blk;    // permuted block (rotated member) or null (step-0 member)
+    const u64* key;    // [L][2][M][N]
+    const u64* X;      // step-0 member source
+    const u64* pt;
+};
+
+// grid (N / blockDim, M, G); U [G][2][M][N]; Cacc [G][2][L][N]
+__global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __restrict__ mem,
+                                                const int* __restrict__ group_off, u64* __restrict__ U,
+                                                u64* __restrict__ Cacc)
 {
     const int N = c.N, L = c.L, M = c.M;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -156,34 +250,39 @@ __global__ void __launch_bounds__(256) k_ks_accum(DevCtx c, const KsItem* __rest
     if (k >= N) return;
     const ModC md = c.mod[j];
     const u64 q = md.q;
+    const long long NN = N;
     u64 u0 = 0, u1 = 0, a0 = 0, a1 = 0;
     const int lo = group_off[g], hi = group_off[g + 1];
     for (int it = lo; it < hi; it++) {
-        const KsItem I = items[it];
-        if (I.step0) {
+        const MacMember m = mem[it];
+        if (!m.blk) {
             if (j < L) {
-                a0 = add_mod(a0, I.X[(long long)j * N + k], q);
-                a1 = add_mod(a1, I.X[((long long)L + j) * N + k], q);
+                u64 x0 = m.X[(long long)j * NN + k], x1 = m.X[((long long)L + j) * NN + k];
+                if (m.pt) {
+                    const u64 w = m.pt[(long long)j * NN + k];
+                    x0 = mont_mul(x0, w, md);
+                    x1 = mont_mul(x1, w, md);
+                }
+                a0 = add_mod(a0, x0, q);
+                a1 = add_mod(a1, x1, q);
             }
             continue;
         }
-        const int src = auto_src(k, I.galois, c.logN);
         Acc128 s0, s1;
-#pragma unroll 4
         for (int i = 0; i < L; i++) {
-            const u64 d = I.D[((long long)i * M + j) * N + src];
-            s0.mac(d, I.key[(((long long)i * 2 + 0) * M + j) * N + k]);
-            s1.mac(d, I.key[(((long long)i * 2 + 1) * M + j) * N + k]);
+            const u64 d = m.blk[((long long)i * M + j) * NN + k];
+            s0.mac(d, __ldg(&m.key[(((long long)i * 2 + 0) * M + j) * NN + k]));
+            s1.mac(d, __ldg(&m.key[(((long long)i * 2 + 1) * M + j) * NN + k]));
         }
         u0 = add_mod(u0, s0.reduce(md), q);
         u1 = add_mod(u1, s1.reduce(md), q);
-        if (j < L) a0 = add_mod(a0, I.X[(long long)j * N + src], q);
+        if (j < L) a0 = add_mod(a0, m.blk[((long long)L * M + j) * NN + k], q);
     }
-    U[(((long long)g * 2 + 0) * M + j) * N + k] = u0;
-    U[(((long long)g * 2 + 1) * M + j) * N + k] = u1;
+    U[(((long long)g * 2 + 0) * M + j) * NN + k] = u0;
+    U[(((long long)g * 2 + 1) * M + j) * NN + k] = u1;
     if (j < L) {
-        Cacc[(((long long)g * 2 + 0) * L + j) * N + k] = a0;
-        Cacc[(((long long)g * 2 + 1) * L + j) * N + k] = a1;
+        Cacc[(((long long)g * 2 + 0) * L + j) * NN + k] = a0;
+        Cacc[(((long long)g * 2 + 1) * L + j) * NN + k] = a1;
     }
 }
 
@@ -255,7 +354,7 @@ __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __re
 // one CTA per (vector b, prime j); each CTA recomputes the mod-p INTT (cheap,
 // p is a 20-bit modulus) to keep the kernel single-pass.
 template <int MODE>
-__global__ void __launch_bounds__(512) k_encode(DevCtx c, const uint32_t* __restrict__ slots, u64* __restrict__ out)
+__global__ void __launch_bounds__(1024, 1) k_encode(DevCtx c, const uint32_t* __restrict__ slots, u64* __restrict__ out)
 {
     extern __shared__ u64 smem_enc[];
     u64* sm = smem_enc;
@@ -288,7 +387,7 @@ __global__ void __launch_bounds__(512) k_encode(DevCtx c, const uint32_t* __rest
 }
 
 // decrypt phase 1: per prime j: x_j = INTT(c0 + c1 * S)
-__global__ void __launch_bounds__(512) k_dec_phase1(DevCtx c, const u64* __restrict__ ct, u64* __restrict__ x)
+__global__ void __launch_bounds__(1024, 1) k_dec_phase1(DevCtx c, const u64* __restrict__ ct, u64* __restrict__ x)
 {
     extern __shared__ u64 sm[];
     const int N = c.N, L = c.L, j = blockIdx.x;
@@ -317,7 +416,7 @@ __device__ __forceinline__ u64 frac64(u64 b, u64 q)
 }
 
 // decrypt phase 2 (one CTA): m = round(p x / Q) mod p via RNS; slots = decode(m)
-__global__ void __launch_bounds__(512) k_dec_phase2(DevCtx c, const u64* __restrict__ x, uint32_t* __restrict__ slots)
+__global__ void __launch_bounds__(1024, 1) k_dec_phase2(DevCtx c, const u64* __restrict__ x, uint32_t* __restrict__ slots)
 {
     extern __shared__ u64 sm[];
     const int N = c.N, L = c.L, PM = c.M;
@@ -403,4 +502,25 @@ __global__ void k_encrypt_combine(DevCtx c, const u64* __restrict__ A, const u64
         ct[x] = add_mod(sub_mod(E[x], mont_mul(a, c.S[x], md), q), DM[x], q);
         ct[total + x] = a;
     }
+}
+
+// modmul throughput probe: 8 independent lazy-Shoup chains per thread, each
+// step = one butterfly-style multiply (shoup_lazy + conditional 2q fold)
+__global__ void __launch_bounds__(256) k_bench_modmul(u64 q, u64 w, u64 wsh, int iters, u64* __restrict__ sink)
+{
+    u64 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = (threadIdx.x * 8 + i + blockIdx.x) % q;
+    const u64 q2 = 2 * q;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            u64 v = shoup_lazy(x[i], w, wsh, q);
+            x[i] = v >= q2 ? v - q2 : v;
+        }
+    }
+    u64 acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) acc ^= x[i];
+    sink[blockIdx.x * 256 + threadIdx.x] = acc;
 }

@@ -50,6 +50,16 @@ static int set_err(int code, const char* fmt, ...)
                            __FILE__, __LINE__);                                                    \
     } while (0)
 
+// launch with optional per-kernel CUDA-event timing (gala_profile_*)
+#define KLAUNCH(ctx, name, ...)                                                                    \
+    do {                                                                                           \
+        cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;                                                \
+        if ((ctx)->prof_on) prof_begin((ctx), &ev0_, &ev1_);                                       \
+        __VA_ARGS__;                                                                               \
+        if ((ctx)->prof_on) prof_end((ctx), name, ev0_, ev1_);                                     \
+        LAUNCHED();                                                                                \
+    } while (0)
+
 #define RET(...)                      \
     do {                              \
         int r_ = (__VA_ARGS__);       \
@@ -107,7 +117,33 @@ struct gala_ctx {
     Staging stage;
     int smem_ntt = 0;         // bytes of one padded polynomial
     std::mutex mu;
+    // per-kernel CUDA-event profiling
+    bool prof_on = false;
+    struct Rec {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
 };
+
+static void prof_begin(gala_ctx* c, cudaEvent_t* a, cudaEvent_t* b)
+{
+    for (cudaEvent_t* e : {a, b}) {
+        if (!c->pool.empty()) {
+            *e = c->pool.back();
+            c->pool.pop_back();
+        } else {
+            cudaEventCreate(e);
+        }
+    }
+    cudaEventRecord(*a, c->stream);
+}
+static void prof_end(gala_ctx* c, const char* name, cudaEvent_t a, cudaEvent_t b)
+{
+    cudaEventRecord(b, c->stream);
+    c->recs.push_back({name, a, b});
+}
 
 static inline int norm_step(const gala_ctx* c, int step)
 {
@@ -168,19 +204,17 @@ static PolyMap pm_make(int per, int nprimes, int prime_base, int src_div, long l
 }
 
 template <typename T, bool MONT>
-static int launch_fwd(gala_ctx* c, const T* src, u64* dst, int polys, PolyMap pm)
+static int launch_fwd(gala_ctx* c, const T* src, u64* dst, int polys, PolyMap pm, const char* tag = "k_ntt_fwd")
 {
     if (polys <= 0) return GALA_OK;
-    k_ntt_fwd<T, MONT><<<polys, ntt_threads(c->dc.N), c->smem_ntt, c->stream>>>(c->dc, src, dst, pm);
-    LAUNCHED();
+    KLAUNCH(c, tag, k_ntt_fwd<T, MONT><<<polys, ntt_threads(c->dc.N), c->smem_ntt, c->stream>>>(c->dc, src, dst, pm));
     return GALA_OK;
 }
 template <bool MONT>
-static int launch_inv(gala_ctx* c, const u64* src, u64* dst, int polys, PolyMap pm)
+static int launch_inv(gala_ctx* c, const u64* src, u64* dst, int polys, PolyMap pm, const char* tag = "k_ntt_inv")
 {
     if (polys <= 0) return GALA_OK;
-    k_ntt_inv<MONT><<<polys, ntt_threads(c->dc.N), c->smem_ntt, c->stream>>>(c->dc, src, dst, pm);
-    LAUNCHED();
+    KLAUNCH(c, tag, k_ntt_inv<MONT><<<polys, ntt_threads(c->dc.N), c->smem_ntt, c->stream>>>(c->dc, src, dst, pm));
     return GALA_OK;
 }
 static int grid_for(long long total, int threads)
@@ -193,62 +227,143 @@ static int grid_for(long long total, int threads)
 // ---------------------------------------------------------------------------
 // key switching building blocks
 
-// digits of `count` items' c1 (items at X + x * x_stride, with optional skip
-// remap), D [count][L][M][N]
-static int decompose_items(gala_ctx* c, const u64* X, long long x_stride, int count, int skip_per, u64* D)
-{
-    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
-    if (count <= 0) return GALA_OK;
-    u64* dig;
-    RET(scratch(c, &dig, (size_t)count * L * N));
-    // INTT of c1 limbs -> digits in [0, q_i)
-    RET(launch_inv<false>(c, X + (long long)L * N, dig, count * L,
-                          pm_make(L, L, 0, 0, x_stride, (long long)L * N, skip_per)));
-    // NTT of digit i into every prime j (digit < q_i < 4 q_j)
-    RET(launch_fwd<u64, false>(c, dig, D, count * L * M,
-                               pm_make(L * M, M, 0, 1, (long long)L * N, (long long)L * M * N)));
-    release(c, dig);
-    return GALA_OK;
-}
+// ---------------------------------------------------------------------------
+// Key-switch engine: any set of "terms" (X or X (.) pt), each rotated by one
+// or more steps, summed into groups with one lazy ModDown per group.
+//   group output = sum over members of rot_step(member)
+// A member is either a rotation (term, r) or a step-0 term added directly.
+struct EngTerm {
+    const u64* X;
+    const u64* pt;
+    std::vector<int> steps;   // nonzero rotation steps of this term
+    const u64* ntt_block;     // optional: precomputed identity block (hoisted DecPerm)
+};
+struct EngMember {
+    int term;
+    int rot;                  // index into term.steps, or -1 for a step-0 member
+};
 
-// U[G] (QP) and Cacc[G] from item descriptors; then ModDown into out[g]
-static int ks_groups(gala_ctx* c, const std::vector<KsItem>& items, const std::vector<int>& off, u64* out,
-                     long long out_is)
+static const u64* key_for(gala_ctx* c, int step);
+
+static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
+                         const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
-    const int G = (int)off.size() - 1;
-    if (G <= 0) return GALA_OK;
-    // descriptor upload (items then offsets, one staging copy)
-    size_t ib = items.size() * sizeof(KsItem), ob = off.size() * sizeof(int);
-    std::vector<char> blob(ib + ob);
-    memcpy(blob.data(), items.data(), ib);
-    memcpy(blob.data() + ib, off.data(), ob);
-    void* d_blob;
-    RET(upload(c, blob.data(), blob.size(), &d_blob));
+    const int G = (int)groups.size();
+    if (G == 0) return GALA_OK;
+    const long long blk_words = (long long)(L * M + L) * N;
+    // rotated terms and their rotation slices
+    std::vector<int> term_rot_base(terms.size(), -1);
+    int n_rot = 0, n_dig = 0;
+    for (size_t t = 0; t < terms.size(); t++) {
+        for (int s : terms[t].steps)
+            if (!key_for(c, s)) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, s));
+        if (!terms[t].steps.empty()) {
+            term_rot_base[t] = n_rot;
+            n_rot += (int)terms[t].steps.size();
+            if (!terms[t].ntt_block) n_dig++;
+        }
+    }
+    u64 *dig = nullptr, *blk = nullptr;
+    if (n_dig) RET(scratch(c, &dig, (size_t)n_dig * L * N));
+    if (n_rot) RET(scratch(c, &blk, (size_t)n_rot * blk_words));
+    std::vector<TermDesc> td, td_hoisted;
+    std::vector<unsigned> gal;
+    int di = 0;
+    for (size_t t = 0; t < terms.size(); t++) {
+        if (terms[t].steps.empty()) continue;
+        TermDesc d;
+        d.X = terms[t].X;
+        d.pt = terms[t].pt;
+        d.dig = terms[t].ntt_block ? nullptr : dig + (long long)(di++) * L * N;
+        d.blk = blk + (long long)term_rot_base[t] * blk_words;
+        d.rot_off = (int)gal.size();
+        d.rot_cnt = (int)terms[t].steps.size();
+        for (int s : terms[t].steps) gal.push_back(galois_of(c, s));
+        if (terms[t].ntt_block) {
+            d.X = terms[t].ntt_block;   // identity block as the permutation source
+            td_hoisted.push_back(d);
+        } else {
+            td.push_back(d);
+        }
+    }
+    std::vector<MacMember> mem;
+    std::vector<int> off;
+    for (auto& g : groups) {
+        off.push_back((int)mem.size());
+        for (auto& m : g) {
+            MacMember mm;
+            const EngTerm& T = terms[m.term];
+            if (m.rot < 0) {
+                mm.blk = nullptr;
+                mm.key = nullptr;
+                mm.X = T.X;
+                mm.pt = T.pt;
+            } else {
+                mm.blk = blk + (long long)(term_rot_base[m.term] + m.rot) * blk_words;
+                mm.key = key_for(c, T.steps[m.rot]);
+                mm.X = nullptr;
+                mm.pt = nullptr;
+            }
+            mem.push_back(mm);
+        }
+    }
+    off.push_back((int)mem.size());
+    // one descriptor blob
+    auto align = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    size_t o_td = 0, o_th = align(o_td + td.size() * sizeof(TermDesc));
+    size_t o_gal = align(o_th + td_hoisted.size() * sizeof(TermDesc));
+    size_t o_mem = align(o_gal + gal.size() * sizeof(unsigned));
+    size_t o_off = align(o_mem + mem.size() * sizeof(MacMember));
+    size_t o_out = align(o_off + off.size() * sizeof(int));
+    size_t total = o_out + outs.size() * sizeof(u64*);
+    std::vector<char> blob(total);
+    if (!td.empty()) memcpy(blob.data() + o_td, td.data(), td.size() * sizeof(TermDesc));
+    if (!td_hoisted.empty()) memcpy(blob.data() + o_th, td_hoisted.data(), td_hoisted.size() * sizeof(TermDesc));
+    if (!gal.empty()) memcpy(blob.data() + o_gal, gal.data(), gal.size() * sizeof(unsigned));
+    memcpy(blob.data() + o_mem, mem.data(), mem.size() * sizeof(MacMember));
+    memcpy(blob.data() + o_off, off.data(), off.size() * sizeof(int));
+    memcpy(blob.data() + o_out, outs.data(), outs.size() * sizeof(u64*));
+    char* d_blob;
+    RET(upload(c, blob.data(), total, (void**)&d_blob));
+    const int nt = ntt_threads(N);
+    if (!td.empty()) {
+        KLAUNCH(c, "k_digits_intt", k_digits_intt<<<(unsigned)(td.size() * L), nt, c->smem_ntt, c->stream>>>(
+                                        c->dc, (const TermDesc*)(d_blob + o_td)));
+        KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(td.size() * (L * M + L)), nt, c->smem_ntt,
+                                                    c->stream>>>(c->dc, (const TermDesc*)(d_blob + o_td),
+                                                                 (const unsigned*)(d_blob + o_gal), blk_words));
+    }
+    if (!td_hoisted.empty()) {
+        KLAUNCH(c, "k_block_perm", k_block_perm<<<(unsigned)(td_hoisted.size() * (L * M + L)), nt, c->smem_ntt,
+                                                  c->stream>>>(c->dc, (const TermDesc*)(d_blob + o_th),
+                                                               (const unsigned*)(d_blob + o_gal), blk_words));
+    }
     u64 *U, *Cacc, *r;
     RET(scratch(c, &U, (size_t)G * 2 * M * N));
     RET(scratch(c, &Cacc, (size_t)G * 2 * L * N));
     RET(scratch(c, &r, (size_t)G * 2 * N));
     const int th = N < 256 ? N : 256;
     dim3 grid((N + th - 1) / th, M, G);
-    k_ks_accum<<<grid, th, 0, c->stream>>>(c->dc, (const KsItem*)d_blob, (const int*)((char*)d_blob + ib), U,
-                                           Cacc);
-    LAUNCHED();
-    // r = INTT_P(U[g][comp][P])
-    RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N)));
+    KLAUNCH(c, "k_ks_mac", k_ks_mac<<<grid, th, 0, c->stream>>>(c->dc, (const MacMember*)(d_blob + o_mem),
+                                                                (const int*)(d_blob + o_off), U, Cacc));
+    RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
+                          "k_ntt_inv[moddown]"));
     MdArgs a;
     a.r = r;
     a.U = U;
     a.add0 = Cacc;
     a.add1 = Cacc + (long long)L * N;
     a.add_is = 2LL * L * N;
-    a.out = out;
-    a.out_is = out_is;
-    k_moddown<<<G * 2 * L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, a);
-    LAUNCHED();
+    a.out = nullptr;
+    a.out_is = 0;
+    a.outs = (u64* const*)(d_blob + o_out);
+    KLAUNCH(c, "k_moddown", k_moddown<<<G * 2 * L, nt, c->smem_ntt, c->stream>>>(c->dc, a));
     release(c, U);
     release(c, Cacc);
     release(c, r);
+    release(c, dig);
+    release(c, blk);
     release(c, d_blob);
     return GALA_OK;
 }
@@ -259,50 +374,30 @@ static const u64* key_for(gala_ctx* c, int step)
     return it == c->keys.end() ? nullptr : it->second;
 }
 
-// out[g] = sum_{j < per} rot_{j * unit}(X[g * per + j]), one lazy ModDown per g
-static int rotate_sum_regular(gala_ctx* c, const u64* X, int G, int per, int unit, u64* out)
+// out[g] = sum_{j < per} rot_{j * unit}(X[g * per + j] (.) pt[...]), one lazy ModDown per g
+static int rotate_sum_regular(gala_ctx* c, const u64* X, long long x_stride, const u64* pts, int G, int per,
+                              int unit, u64* out)
 {
-    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
-    const long long W = 2LL * L * N, DW = (long long)L * M * N;
-    if (per == 1) {
-        CK(cudaMemcpyAsync(out, X, sizeof(u64) * W * G, cudaMemcpyDeviceToDevice, c->stream));
-        return GALA_OK;
-    }
-    // key check first
-    for (int j = 1; j < per; j++)
-        if (norm_step(c, j * unit) != 0 && !key_for(c, j * unit))
-            return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, j * unit));
-    u64* D;
-    const int nrot = G * (per - 1);
-    RET(scratch(c, &D, (size_t)nrot * DW));
-    RET(decompose_items(c, X, W, nrot, per, D));
-    std::vector<KsItem> items;
-    std::vector<int> off;
-    items.reserve((size_t)G * per);
+    const int N = c->dc.N, L = c->dc.L;
+    const long long W = 2LL * L * N, PW = (long long)L * N;
+    std::vector<EngTerm> terms;
+    std::vector<std::vector<EngMember>> groups(G);
+    std::vector<u64*> outs;
     for (int g = 0; g < G; g++) {
-        off.push_back((int)items.size());
         for (int j = 0; j < per; j++) {
-            KsItem it;
-            it.X = X + (long long)(g * per + j) * W;
+            const int idx = g * per + j;
+            EngTerm t;
+            t.X = X + (long long)idx * x_stride;
+            t.pt = pts ? pts + (long long)idx * PW : nullptr;
+            t.ntt_block = nullptr;
             int s = norm_step(c, j * unit);
-            if (s == 0) {
-                it.D = nullptr;
-                it.key = nullptr;
-                it.galois = 1;
-                it.step0 = 1;
-            } else {
-                it.D = D + (long long)(g * (per - 1) + (j - 1)) * DW;
-                it.key = key_for(c, s);
-                it.galois = galois_of(c, s);
-                it.step0 = 0;
-            }
-            items.push_back(it);
+            if (s) t.steps.push_back(s);
+            terms.push_back(t);
+            groups[g].push_back({(int)terms.size() - 1, s ? 0 : -1});
         }
+        outs.push_back(out + (long long)g * W);
     }
-    off.push_back((int)items.size());
-    RET(ks_groups(c, items, off, out, W));
-    release(c, D);
-    return GALA_OK;
+    return rotate_engine(c, terms, groups, outs);
 }
 
 // ---------------------------------------------------------------------------
@@ -325,6 +420,11 @@ static void free_ctx(gala_ctx* c)
     if (c->d_pmod) cudaFree(c->d_pmod);
     if (c->stage.host) cudaFreeHost(c->stage.host);
     if (c->stage.done) cudaEventDestroy(c->stage.done);
+    for (auto& r : c->recs) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
 }
 
@@ -472,6 +572,9 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_ntt_inv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
     CKC(cudaFuncSetAttribute(k_ntt_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
     CKC(cudaFuncSetAttribute(k_moddown, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
+    CKC(cudaFuncSetAttribute(k_digits_intt, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
+    CKC(cudaFuncSetAttribute(k_digits_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
+    CKC(cudaFuncSetAttribute(k_block_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
     CKC(cudaFuncSetAttribute(k_encode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * c->smem_ntt));
     CKC(cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * c->smem_ntt));
     CKC(cudaFuncSetAttribute(k_dec_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
@@ -539,9 +642,8 @@ int gala_gen_rotation_key(gala_ctx* c, int step, const uint64_t* a_host, const i
         c->keys[s] = key;
         c->key_bytes += sizeof(u64) * kw;
     }
-    k_keygen_combine<<<grid_for((long long)L * M * N, 256), 256, 0, c->stream>>>(c->dc, A, E, galois_of(c, s),
-                                                                                 c->d_pmod, key);
-    LAUNCHED();
+    KLAUNCH(c, "k_keygen_combine", k_keygen_combine<<<grid_for((long long)L * M * N, 256), 256, 0, c->stream>>>(c->dc, A, E, galois_of(c, s),
+                                                                                 c->d_pmod, key));
     release(c, da);
     release(c, A);
     release(c, E);
@@ -560,8 +662,7 @@ size_t gala_key_bytes(gala_ctx* c) { return c->key_bytes; }
 int gala_encode_plain(gala_ctx* c, const uint32_t* slots, int B, uint64_t* pt)
 {
     if (B <= 0) return GALA_OK;
-    k_encode<0><<<B * c->dc.L, ntt_threads(c->dc.N), 2 * c->smem_ntt, c->stream>>>(c->dc, slots, pt);
-    LAUNCHED();
+    KLAUNCH(c, "k_encode", k_encode<0><<<B * c->dc.L, ntt_threads(c->dc.N), 2 * c->smem_ntt, c->stream>>>(c->dc, slots, pt));
     return GALA_OK;
 }
 
@@ -575,10 +676,8 @@ int gala_encrypt(gala_ctx* c, const uint32_t* slots, const uint64_t* a, const in
     RET(scratch(c, &DM, (size_t)L * N));
     RET(launch_fwd<u64, false>(c, a, A, L, pm_make(L, L, 0, 0, 0, 0)));
     RET(launch_fwd<i64, false>(c, e, E, L, pm_make(L, L, 0, 1, 0, 0)));
-    k_encode<1><<<L, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(c->dc, slots, DM);
-    LAUNCHED();
-    k_encrypt_combine<<<grid_for((long long)L * N, 256), 256, 0, c->stream>>>(c->dc, A, E, DM, ct);
-    LAUNCHED();
+    KLAUNCH(c, "k_encode", k_encode<1><<<L, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(c->dc, slots, DM));
+    KLAUNCH(c, "k_encrypt_combine", k_encrypt_combine<<<grid_for((long long)L * N, 256), 256, 0, c->stream>>>(c->dc, A, E, DM, ct));
     release(c, A);
     release(c, E);
     release(c, DM);
@@ -591,10 +690,8 @@ int gala_decrypt(gala_ctx* c, const uint64_t* ct, uint32_t* slots)
     const int N = c->dc.N, L = c->dc.L;
     u64* x;
     RET(scratch(c, &x, (size_t)L * N));
-    k_dec_phase1<<<L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, ct, x);
-    LAUNCHED();
-    k_dec_phase2<<<1, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, x, slots);
-    LAUNCHED();
+    KLAUNCH(c, "k_dec_phase1", k_dec_phase1<<<L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, ct, x));
+    KLAUNCH(c, "k_dec_phase2", k_dec_phase2<<<1, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, x, slots));
     release(c, x);
     return GALA_OK;
 }
@@ -602,8 +699,7 @@ int gala_decrypt(gala_ctx* c, const uint64_t* ct, uint32_t* slots)
 int gala_add(gala_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out)
 {
     long long total = 2LL * c->dc.L * c->dc.N;
-    k_addsub<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, a, b, out, total, c->dc.L, 1);
-    LAUNCHED();
+    KLAUNCH(c, "k_addsub", k_addsub<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, a, b, out, total, c->dc.L, 1));
     return GALA_OK;
 }
 
@@ -611,8 +707,7 @@ int gala_scmult(gala_ctx* c, const uint64_t* ct, const uint64_t* pt, uint64_t* o
 {
     const int N = c->dc.N, L = c->dc.L;
     dim3 grid((2 * L * N + 255) / 256, 1);
-    k_ct_mul_pts<<<grid, 256, 0, c->stream>>>(c->dc, ct, pt, out);
-    LAUNCHED();
+    KLAUNCH(c, "k_ct_mul_pts", k_ct_mul_pts<<<grid, 256, 0, c->stream>>>(c->dc, ct, pt, out));
     return GALA_OK;
 }
 
@@ -621,24 +716,47 @@ int gala_sub_plain(gala_ctx* c, const uint64_t* ct, const uint32_t* r, uint64_t*
     const int N = c->dc.N, L = c->dc.L;
     u64* DM;
     RET(scratch(c, &DM, (size_t)L * N));
-    k_encode<1><<<L, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(c->dc, r, DM);
-    LAUNCHED();
+    KLAUNCH(c, "k_encode", k_encode<1><<<L, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(c->dc, r, DM));
     if (out != ct) CK(cudaMemcpyAsync(out + (long long)L * N, ct + (long long)L * N, sizeof(u64) * L * N,
                                       cudaMemcpyDeviceToDevice, c->stream));
     long long total = (long long)L * N;
-    k_addsub<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, ct, DM, out, total, L, -1);
-    LAUNCHED();
+    KLAUNCH(c, "k_addsub", k_addsub<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, ct, DM, out, total, L, -1));
     release(c, DM);
     return GALA_OK;
 }
 
-size_t gala_digits_words(gala_ctx* c) { return (size_t)c->dc.L * c->dc.M * c->dc.N; }
+size_t gala_digits_words(gala_ctx* c) { return (size_t)(c->dc.L * c->dc.M + c->dc.L) * c->dc.N; }
 
+// DecPerm: the identity-permuted digit block [(L*M + L)][N] (NTT digits of c1, then c0)
 int gala_decompose(gala_ctx* c, const uint64_t* ct, uint64_t* digits)
 {
-    return decompose_items(c, ct, 0, 1, 0, digits);
+    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
+    u64* dig;
+    RET(scratch(c, &dig, (size_t)L * N));
+    TermDesc d;
+    d.X = ct;
+    d.pt = nullptr;
+    d.dig = dig;
+    d.blk = digits;
+    d.rot_off = 0;
+    d.rot_cnt = 1;
+    struct {
+        TermDesc t;
+        unsigned g;
+    } b = {d, 1u};
+    char* d_blob;
+    RET(upload(c, &b, sizeof(b), (void**)&d_blob));
+    const int nt = ntt_threads(N);
+    KLAUNCH(c, "k_digits_intt", k_digits_intt<<<L, nt, c->smem_ntt, c->stream>>>(c->dc, (const TermDesc*)d_blob));
+    KLAUNCH(c, "k_digits_perm", k_digits_perm<<<L * M + L, nt, c->smem_ntt, c->stream>>>(
+                                    c->dc, (const TermDesc*)d_blob, (const unsigned*)(d_blob + offsetof(decltype(b), g)),
+                                    (long long)(L * M + L) * N));
+    release(c, dig);
+    release(c, d_blob);
+    return GALA_OK;
 }
 
+// HstPerm: rotation of the group's source from its DecPerm block
 int gala_rotate_hoisted(gala_ctx* c, const uint64_t* ct, const uint64_t* digits, int step, uint64_t* out)
 {
     const int N = c->dc.N, L = c->dc.L;
@@ -647,33 +765,28 @@ int gala_rotate_hoisted(gala_ctx* c, const uint64_t* ct, const uint64_t* digits,
         if (out != ct) CK(cudaMemcpyAsync(out, ct, sizeof(u64) * 2 * L * N, cudaMemcpyDeviceToDevice, c->stream));
         return GALA_OK;
     }
-    const u64* key = key_for(c, s);
-    if (!key) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", s);
-    std::vector<KsItem> items(1);
-    items[0].D = digits;
-    items[0].X = ct;
-    items[0].key = key;
-    items[0].galois = galois_of(c, s);
-    items[0].step0 = 0;
-    std::vector<int> off = {0, 1};
-    return ks_groups(c, items, off, out, 2LL * L * N);
+    EngTerm t;
+    t.X = ct;
+    t.pt = nullptr;
+    t.steps = {s};
+    t.ntt_block = digits;
+    return rotate_engine(c, {t}, {{{0, 0}}}, {out});
 }
 
 int gala_rotate(gala_ctx* c, const uint64_t* ct, int step, uint64_t* out)
 {
-    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
+    const int N = c->dc.N, L = c->dc.L;
     int s = norm_step(c, step);
     if (s == 0) {
         if (out != ct) CK(cudaMemcpyAsync(out, ct, sizeof(u64) * 2 * L * N, cudaMemcpyDeviceToDevice, c->stream));
         return GALA_OK;
     }
-    if (!key_for(c, s)) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", s);
-    u64* D;
-    RET(scratch(c, &D, (size_t)L * M * N));
-    RET(gala_decompose(c, ct, D));
-    RET(gala_rotate_hoisted(c, ct, D, s, out));
-    release(c, D);
-    return GALA_OK;
+    EngTerm t;
+    t.X = ct;
+    t.pt = nullptr;
+    t.steps = {s};
+    t.ntt_block = nullptr;
+    return rotate_engine(c, {t}, {{{0, 0}}}, {out});
 }
 
 int gala_bsgs_baby(int T)
@@ -697,21 +810,18 @@ int gala_mv_gala(gala_ctx* c, const uint64_t* ct, const uint64_t* pts, int T, in
     for (int g = 1; g < G; g++)
         if (!gala_has_rotation_key(c, g * baby))
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, g * baby));
-    u64* U;
-    RET(scratch(c, &U, (size_t)T * W));
-    dim3 grid((unsigned)((2 * L * N + 255) / 256), (unsigned)T);
-    k_ct_mul_pts<<<grid, 256, 0, c->stream>>>(c->dc, ct, pts, U);
-    LAUNCHED();
-    if (G == 1) {
-        RET(rotate_sum_regular(c, U, 1, baby, 1, out));
+    if (T == 1) {
+        dim3 grid((unsigned)((2 * L * N + 255) / 256), 1);
+        KLAUNCH(c, "k_ct_mul_pts", k_ct_mul_pts<<<grid, 256, 0, c->stream>>>(c->dc, ct, pts, out));
+    } else if (G == 1) {
+        RET(rotate_sum_regular(c, ct, 0, pts, 1, baby, 1, out));
     } else {
         u64* inner;
         RET(scratch(c, &inner, (size_t)G * W));
-        RET(rotate_sum_regular(c, U, G, baby, 1, inner));
-        RET(rotate_sum_regular(c, inner, 1, G, baby, out));
+        RET(rotate_sum_regular(c, ct, 0, pts, G, baby, 1, inner));   // baby steps, ScMult fused
+        RET(rotate_sum_regular(c, inner, W, nullptr, 1, G, baby, out));
         release(c, inner);
     }
-    release(c, U);
     if (r && masked) RET(gala_sub_plain(c, out, r, masked));
     return GALA_OK;
 }
@@ -747,7 +857,7 @@ int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts
                  const int* tap_steps, int band_step, uint64_t* outs)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
-    const long long W = 2LL * L * N, DW = (long long)L * M * N;
+    const long long W = 2LL * L * N;
     if (n_ib <= 0 || n_obp <= 0 || c_n <= 0 || k <= 0) return set_err(GALA_ERR_DIM, "empty convolution");
     std::vector<int> rot_taps;
     for (int t = 0; t < k; t++) {
@@ -760,7 +870,7 @@ int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts
     for (int d = 1; d < c_n; d++)
         if (!gala_has_rotation_key(c, d * band_step))
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, d * band_step));
-    // input rotations R[ib][tap]: one DecPerm per input, HstPerm per nonzero tap
+    // input rotations R[ib][tap]: one DecPerm per input (digit NTTs once), HstPerm per nonzero tap
     u64* R;
     RET(scratch(c, &R, (size_t)n_ib * k * W));
     for (int ib = 0; ib < n_ib; ib++)
@@ -769,41 +879,32 @@ int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts
                 CK(cudaMemcpyAsync(R + ((long long)ib * k + t) * W, cts + (long long)ib * W, sizeof(u64) * W,
                                    cudaMemcpyDeviceToDevice, c->stream));
     if (!rot_taps.empty()) {
-        u64* D;
-        RET(scratch(c, &D, (size_t)n_ib * DW));
-        RET(decompose_items(c, cts, W, n_ib, 0, D));
-        // one group per (ib, rotated tap), each its own ModDown; outputs land
-        // directly in R via per-group output stride: process tap by tap so the
-        // output stride is regular (k * W per ib)
-        for (int t : rot_taps) {
-            std::vector<KsItem> items;
-            std::vector<int> off;
-            int s = norm_step(c, tap_steps[t]);
-            for (int ib = 0; ib < n_ib; ib++) {
-                off.push_back((int)items.size());
-                KsItem it;
-                it.D = D + (long long)ib * DW;
-                it.X = cts + (long long)ib * W;
-                it.key = key_for(c, s);
-                it.galois = galois_of(c, s);
-                it.step0 = 0;
-                items.push_back(it);
+        std::vector<EngTerm> terms;
+        std::vector<std::vector<EngMember>> groups;
+        std::vector<u64*> outs;
+        for (int ib = 0; ib < n_ib; ib++) {
+            EngTerm t;
+            t.X = cts + (long long)ib * W;
+            t.pt = nullptr;
+            t.ntt_block = nullptr;
+            for (int tap : rot_taps) t.steps.push_back(norm_step(c, tap_steps[tap]));
+            terms.push_back(t);
+            for (size_t r = 0; r < rot_taps.size(); r++) {
+                groups.push_back({{ib, (int)r}});
+                outs.push_back(R + ((long long)ib * k + rot_taps[r]) * W);
             }
-            off.push_back((int)items.size());
-            RET(ks_groups(c, items, off, R + (long long)t * W, (long long)k * W));
         }
-        release(c, D);
+        RET(rotate_engine(c, terms, groups, outs));
     }
     // first-Add: acc[o][d] over all input blocks and taps
     u64* acc;
     RET(scratch(c, &acc, (size_t)n_obp * c_n * W));
     const int th = N < 256 ? N : 256;
     dim3 grid((N + th - 1) / th, L, n_obp * c_n);
-    k_kg_accumulate<<<grid, th, 0, c->stream>>>(c->dc, R, n_ib, k, pts, c_n, acc);
-    LAUNCHED();
+    KLAUNCH(c, "k_kg_accumulate", k_kg_accumulate<<<grid, th, 0, c->stream>>>(c->dc, R, n_ib, k, pts, c_n, acc));
     release(c, R);
     // second-Perm: out[o] = sum_d rot_{d * band}(acc[o][d]), one lazy ModDown per o
-    RET(rotate_sum_regular(c, acc, n_obp, c_n, band_step, outs));
+    RET(rotate_sum_regular(c, acc, W, nullptr, n_obp, c_n, band_step, outs));
     release(c, acc);
     return GALA_OK;
 }
@@ -824,6 +925,68 @@ int gala_pt_export(gala_ctx* c, const uint64_t* pt, uint64_t* coef, int count)
 {
     const int N = c->dc.N, L = c->dc.L;
     return launch_inv<true>(c, pt, coef, count * L, pm_make(L, L, 0, 0, (long long)L * N, (long long)L * N));
+}
+
+int gala_profile_enable(gala_ctx* c, int on)
+{
+    c->prof_on = on != 0;
+    return GALA_OK;
+}
+
+// aggregate recorded launches by kernel name into JSON {"name": [count, total_ms], ...};
+// synchronises the stream and clears the records
+int gala_profile_json(gala_ctx* c, char* buf, size_t cap)
+{
+    CK(cudaStreamSynchronize(c->stream));
+    std::map<std::string, std::pair<long, double>> agg;
+    for (auto& r : c->recs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto& e = agg[r.name];
+        e.first += 1;
+        e.second += ms;
+        c->pool.push_back(r.a);
+        c->pool.push_back(r.b);
+    }
+    c->recs.clear();
+    std::string out = "{";
+    bool first = true;
+    for (auto& kv : agg) {
+        char tmp[256];
+        snprintf(tmp, sizeof(tmp), "%s\"%s\": [%ld, %.6f]", first ? "" : ", ", kv.first.c_str(), kv.second.first,
+                 kv.second.second);
+        out += tmp;
+        first = false;
+    }
+    out += "}";
+    if (out.size() + 1 > cap) return set_err(GALA_ERR_DIM, "profile buffer too small (%zu)", out.size() + 1);
+    memcpy(buf, out.c_str(), out.size() + 1);
+    return GALA_OK;
+}
+
+// Throughput of the library's own 60-bit Shoup modmul (the NTT butterfly
+// multiply) in modmul/s: every thread runs 8 independent dependency chains.
+int gala_bench_modmul(gala_ctx* c, int blocks, int iters, double* modmul_per_s)
+{
+    u64* sink;
+    RET(scratch(c, &sink, (size_t)blocks * 256));
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    const u64 q = c->primes[0];
+    const u64 w = (q >> 3) | 1, wsh = h_shoup(w % q, q);
+    k_bench_modmul<<<blocks, 256, 0, c->stream>>>(q, w % q, wsh, iters, sink); // warm-up
+    CK(cudaEventRecord(a, c->stream));
+    KLAUNCH(c, "k_bench_modmul", k_bench_modmul<<<blocks, 256, 0, c->stream>>>(q, w % q, wsh, iters, sink));
+    CK(cudaEventRecord(b, c->stream));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    *modmul_per_s = (double)blocks * 256.0 * 8.0 * iters / (ms * 1e-3);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    release(c, sink);
+    return GALA_OK;
 }
 
 } // extern "C"
