@@ -91,6 +91,11 @@ int gala_rotate_hoisted(gala_ctx *ctx, const uint64_t *ct_dev, const uint64_t *d
  * and masked_dev may be NULL. */
 int gala_mv_gala(gala_ctx *ctx, const uint64_t *ct_dev, const uint64_t *pts_dev, int T, int baby,
                  const uint32_t *r_slots_dev, uint64_t *out_dev, uint64_t *masked_dev);
+/* Batched form: B independent inputs cts_dev [B][2][L][N] against the same
+ * plaintexts; r_slots_dev [B][N]; outs/masked [B][2][L][N].  All inputs share
+ * every launch (grids scale with B). */
+int gala_mv_gala_batch(gala_ctx *ctx, const uint64_t *cts_dev, int B, const uint64_t *pts_dev, int T, int baby,
+                       const uint32_t *r_slots_dev, uint64_t *outs_dev, uint64_t *masked_dev);
 int gala_bsgs_baby(int T);
 /* Same with host buffers (canonical words in/out), copies on the context
  * stream; blocks until the result is in host memory. */

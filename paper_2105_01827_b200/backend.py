@@ -398,6 +398,19 @@ class Context:
                   ctypes.c_void_p(_ptr(masked)) if masked is not None else None)
         return out, masked
 
+    def mv_gala_batch(self, cts, pts, T: int, d_r=None, baby: int | None = None, outs=None, masked=None):
+        """Fused GALA product over a batch: cts [B][2][L][N] (device), d_r [B][N] int32 device masks."""
+        b, steps = self.bsgs_steps(T, baby)
+        self.ensure_keys(steps)
+        B = cts.shape[0]
+        outs = self.empty_ct(B) if outs is None else outs
+        if d_r is not None and masked is None:
+            masked = self.empty_ct(B)
+        self.call("gala_mv_gala_batch", ctypes.c_void_p(_ptr(cts)), int(B), ctypes.c_void_p(_ptr(pts)), int(T),
+                  int(b), ctypes.c_void_p(_ptr(d_r)) if d_r is not None else None, ctypes.c_void_p(_ptr(outs)),
+                  ctypes.c_void_p(_ptr(masked)) if masked is not None else None)
+        return outs, masked
+
     def conv_kg(self, cts, pts, tap_steps, band_step: int):
         """cts [n_ib][2][L][N]; pts [n_obp][n_ib][c_n][k][L][N] -> [n_obp][2][L][N]."""
         n_obp, n_ib, c_n, k = pts.shape[:4]

@@ -74,6 +74,11 @@ struct Acc128 {
     __device__ __forceinline__ u64 reduce(const ModC& m) const { return csub(redc_lazy(hi, lo, m), m.q); }
 };
 
+// streaming (evict-first) global accesses for polynomial data, so the twiddle
+// tables keep their L1 residency
+__device__ __forceinline__ u64 ld_cs(const u64* p) { return (u64)__ldcs((const unsigned long long*)p); }
+__device__ __forceinline__ void st_cs(u64* p, u64 v) { __stcs((unsigned long long*)p, (unsigned long long)v); }
+
 __device__ __forceinline__ int brv(int x, int logN) { return (int)(__brev((unsigned)x) >> (32 - logN)); }
 
 // Galois automorphism X -> X^g on the bit-reversed NTT domain:
@@ -96,7 +101,14 @@ __host__ __device__ constexpr int padded_words(int n) { return n + (n >> 5); }
 // merged psi powers; inverse: Gentleman-Sande, bit-reversed -> natural (without the
 // N^-1 scale).  A pass processes R consecutive stages in registers: each thread owns
 // groups of 2^R elements spaced t_end apart.
-template <int R>
+template <bool TW_SMEM>
+__device__ __forceinline__ ulonglong2 tw_load(const ulonglong2* p)
+{
+    if (TW_SMEM) return *p;
+    return __ldg(p);
+}
+
+template <int R, bool TW_SMEM = false>
 __device__ __forceinline__ void fwd_pass(u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, int s0)
 {
     const int N = 1 << logN;
@@ -117,7 +129,7 @@ __device__ __forceinline__ void fwd_pass(u64* s, const ulonglong2* __restrict__ 
 #pragma unroll
             for (int k = 0; k < (1 << R); k++) {
                 if (k & half) continue;
-                const ulonglong2 w = __ldg(&tw[m + (blk << l) + (k >> (R - l))]);
+                const ulonglong2 w = tw_load<TW_SMEM>(&tw[m + (blk << l) + (k >> (R - l))]);
                 u64 U = x[k];
                 U = U >= q2 ? U - q2 : U;
                 u64 V = shoup_lazy(x[k + half], w.x, w.y, q);
@@ -130,7 +142,7 @@ __device__ __forceinline__ void fwd_pass(u64* s, const ulonglong2* __restrict__ 
     }
 }
 
-template <int R>
+template <int R, bool TW_SMEM = false>
 __device__ __forceinline__ void inv_pass(u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, int s0)
 {
     const int N = 1 << logN;
@@ -151,7 +163,7 @@ __device__ __forceinline__ void inv_pass(u64* s, const ulonglong2* __restrict__ 
 #pragma unroll
             for (int k = 0; k < (1 << R); k++) {
                 if (k & half) continue;
-                const ulonglong2 w = __ldg(&tw[m + (blk << l) + (k >> (R - l))]);
+                const ulonglong2 w = tw_load<TW_SMEM>(&tw[m + (blk << l) + (k >> (R - l))]);
                 u64 U = x[k], V = x[k + half];
                 u64 a = U + V;
                 x[k] = a >= q2 ? a - q2 : a;
@@ -165,44 +177,57 @@ __device__ __forceinline__ void inv_pass(u64* s, const ulonglong2* __restrict__ 
 
 #define GALA_NTT_R 3
 
+template <int RMAX, bool TW_SMEM>
+__device__ __forceinline__ void fwd_dispatch(u64* s, const ulonglong2* tw, u64 q, int logN, int s0, int r)
+{
+    if (RMAX >= 5 && r == 5) fwd_pass<(RMAX >= 5 ? 5 : 1), TW_SMEM>(s, tw, q, logN, s0);
+    else if (RMAX >= 4 && r == 4) fwd_pass<(RMAX >= 4 ? 4 : 1), TW_SMEM>(s, tw, q, logN, s0);
+    else if (r == 3) fwd_pass<3, TW_SMEM>(s, tw, q, logN, s0);
+    else if (r == 2) fwd_pass<2, TW_SMEM>(s, tw, q, logN, s0);
+    else fwd_pass<1, TW_SMEM>(s, tw, q, logN, s0);
+}
+template <int RMAX, bool TW_SMEM>
+__device__ __forceinline__ void inv_dispatch(u64* s, const ulonglong2* tw, u64 q, int logN, int s0, int r)
+{
+    if (RMAX >= 5 && r == 5) inv_pass<(RMAX >= 5 ? 5 : 1), TW_SMEM>(s, tw, q, logN, s0);
+    else if (RMAX >= 4 && r == 4) inv_pass<(RMAX >= 4 ? 4 : 1), TW_SMEM>(s, tw, q, logN, s0);
+    else if (r == 3) inv_pass<3, TW_SMEM>(s, tw, q, logN, s0);
+    else if (r == 2) inv_pass<2, TW_SMEM>(s, tw, q, logN, s0);
+    else inv_pass<1, TW_SMEM>(s, tw, q, logN, s0);
+}
+
 // input: s[pad(i)] in [0, 4q); output in [0, 4q) (bit-reversed order)
+template <bool TW_SMEM = false, int RMAX = GALA_NTT_R>
 __device__ __forceinline__ void ntt_fwd_smem(u64* s, const ulonglong2* tw, u64 q, int logN)
 {
     int s0 = 0;
     while (s0 < logN) {
-        int r = logN - s0 < GALA_NTT_R ? logN - s0 : GALA_NTT_R;
-        switch (r) {
-            case 4: fwd_pass<4>(s, tw, q, logN, s0); break;
-            case 3: fwd_pass<3>(s, tw, q, logN, s0); break;
-            case 2: fwd_pass<2>(s, tw, q, logN, s0); break;
-            default: fwd_pass<1>(s, tw, q, logN, s0); break;
-        }
+        int r = logN - s0 < RMAX ? logN - s0 : RMAX;
+        fwd_dispatch<RMAX, TW_SMEM>(s, tw, q, logN, s0, r);
         __syncthreads();
         s0 += r;
     }
 }
 
 // input: s[pad(i)] in [0, 2q) bit-reversed; output in [0, 2q) natural, *not* scaled by N^-1
+template <bool TW_SMEM = false, int RMAX = GALA_NTT_R>
 __device__ __forceinline__ void ntt_inv_smem(u64* s, const ulonglong2* tw, u64 q, int logN)
 {
     // passes mirror the forward split, executed from the last stage group down
-    int first = logN % GALA_NTT_R;
-    int s0 = logN - (first ? first : GALA_NTT_R);
+    int first = logN % RMAX;
+    int s0 = logN - (first ? first : RMAX);
     while (s0 >= 0) {
-        int r = logN - s0 < GALA_NTT_R ? logN - s0 : GALA_NTT_R;
-        switch (r) {
-            case 4: inv_pass<4>(s, tw, q, logN, s0); break;
-            case 3: inv_pass<3>(s, tw, q, logN, s0); break;
-            case 2: inv_pass<2>(s, tw, q, logN, s0); break;
-            default: inv_pass<1>(s, tw, q, logN, s0); break;
-        }
+        int r = logN - s0 < RMAX ? logN - s0 : RMAX;
+        inv_dispatch<RMAX, TW_SMEM>(s, tw, q, logN, s0, r);
         __syncthreads();
-        s0 -= GALA_NTT_R;
+        s0 -= RMAX;
     }
 }
 
+// 512 threads for N = 8192 (two radix-8 groups per thread per pass) so that two
+// CTAs (2 x 66 KB smem, <= 64 registers) share an SM and overlap their memory phases
 __host__ __device__ inline int ntt_threads(int N)
 {
-    int t = N >> GALA_NTT_R;
+    int t = N >> (GALA_NTT_R + 1);
     return t < 32 ? 32 : t;
 }

@@ -50,7 +50,7 @@ __device__ __forceinline__ u64 to_residue<int8_t>(int8_t v, u64 q) { return v >=
 
 // forward NTT of a batch; output reduced to [0, q), optionally Montgomery-scaled
 template <typename T, bool TO_MONT>
-__global__ void __launch_bounds__(1024, 1) k_ntt_fwd(DevCtx c, const T* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
+__global__ void __launch_bounds__(512, 2) k_ntt_fwd(DevCtx c, const T* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
 {
     extern __shared__ u64 sm[];
     long long so, dof;
@@ -67,13 +67,13 @@ __global__ void __launch_bounds__(1024, 1) k_ntt_fwd(DevCtx c, const T* __restri
         u64 v = sm[pad(i)];
         v = csub(csub(v, 2 * q), q);
         if (TO_MONT) v = mont_mul(v, md.r2, md);
-        dst[dof + i] = v;
+        st_cs(dst + dof + i, v);
     }
 }
 
 // inverse NTT of a batch -> coefficients in [0, q)
 template <bool FROM_MONT>
-__global__ void __launch_bounds__(1024, 1) k_ntt_inv(DevCtx c, const u64* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
+__global__ void __launch_bounds__(512, 2) k_ntt_inv(DevCtx c, const u64* __restrict__ src, u64* __restrict__ dst, PolyMap pm)
 {
     extern __shared__ u64 sm[];
     long long so, dof;
@@ -82,14 +82,14 @@ __global__ void __launch_bounds__(1024, 1) k_ntt_inv(DevCtx c, const u64* __rest
     const ModC md = c.mod[j];
     const u64 q = md.q;
     for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
-        u64 v = src[so + i];
+        u64 v = ld_cs(src + so + i);
         if (FROM_MONT) v = csub(redc_lazy(0, v, md), q);
         sm[pad(i)] = v;
     }
     __syncthreads();
     ntt_inv_smem(sm, c.twi[j], q, c.logN);
     const u64 ni = c.ninv[j], nsh = c.ninv_sh[j];
-    for (int i = threadIdx.x; i < c.N; i += blockDim.x) dst[dof + i] = shoup(sm[pad(i)], ni, nsh, q);
+    for (int i = threadIdx.x; i < c.N; i += blockDim.x) st_cs(dst + dof + i, shoup(sm[pad(i)], ni, nsh, q));
 }
 
 // ---------------------------------------------------------------------------
@@ -106,7 +106,7 @@ struct MdArgs {
     u64* const* outs;  // optional per-group output pointers
 };
 
-__global__ void __launch_bounds__(1024, 1) k_moddown(DevCtx c, MdArgs a)
+__global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
 {
     extern __shared__ u64 sm[];
     const int L = c.L, M = c.M, N = c.N;
@@ -162,7 +162,7 @@ __device__ __forceinline__ u64 src_limb(const DevCtx& c, const TermDesc& t, int 
     return v;
 }
 
-__global__ void __launch_bounds__(1024, 1) k_digits_intt(DevCtx c, const TermDesc* __restrict__ terms)
+__global__ void __launch_bounds__(512, 2) k_digits_intt(DevCtx c, const TermDesc* __restrict__ terms)
 {
     extern __shared__ u64 sm[];
     const int L = c.L, N = c.N;
@@ -174,11 +174,11 @@ __global__ void __launch_bounds__(1024, 1) k_digits_intt(DevCtx c, const TermDes
     ntt_inv_smem(sm, c.twi[i], q, c.logN);
     u64* d = t.dig + (long long)i * N;
     const u64 ni = c.ninv[i], nsh = c.ninv_sh[i];
-    for (int k = threadIdx.x; k < N; k += blockDim.x) d[k] = shoup(sm[pad(k)], ni, nsh, q);
+    for (int k = threadIdx.x; k < N; k += blockDim.x) st_cs(d + k, shoup(sm[pad(k)], ni, nsh, q));
 }
 
 // grid: terms * (L*M + L) CTAs
-__global__ void __launch_bounds__(1024, 1) k_digits_perm(DevCtx c, const TermDesc* __restrict__ terms,
+__global__ void __launch_bounds__(512, 2) k_digits_perm(DevCtx c, const TermDesc* __restrict__ terms,
                                                          const unsigned* __restrict__ galois, long long blk_words)
 {
     extern __shared__ u64 sm[];
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(1024, 1) k_digits_perm(DevCtx c, const TermDes
         const u64 q = c.mod[j].q;
         if (i != j) {
             const u64* d = t.dig + (long long)i * N;   // d < q_i < 4 q_j: lazy NTT input
-            for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = d[k];
+            for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = ld_cs(d + k);
             __syncthreads();
             ntt_fwd_smem(sm, c.twf[j], q, c.logN);
             for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = csub(csub(sm[pad(k)], 2 * q), q);
@@ -208,13 +208,13 @@ __global__ void __launch_bounds__(1024, 1) k_digits_perm(DevCtx c, const TermDes
     for (int r = 0; r < t.rot_cnt; r++) {
         const unsigned g = galois[t.rot_off + r];
         u64* o = t.blk + r * blk_words + (long long)slot * N;
-        for (int k = threadIdx.x; k < N; k += blockDim.x) o[k] = sm[pad(auto_src(k, g, c.logN))];
+        for (int k = threadIdx.x; k < N; k += blockDim.x) st_cs(o + k, sm[pad(auto_src(k, g, c.logN))]);
     }
 }
 
 // hoisted rotations from a precomputed identity block (the DecPerm output):
 // permutation only.  t.X points at the identity block [(L*M + L)][N].
-__global__ void __launch_bounds__(1024, 1) k_block_perm(DevCtx c, const TermDesc* __restrict__ terms,
+__global__ void __launch_bounds__(512, 2) k_block_perm(DevCtx c, const TermDesc* __restrict__ terms,
                                                         const unsigned* __restrict__ galois, long long blk_words)
 {
     extern __shared__ u64 sm[];
@@ -223,12 +223,12 @@ __global__ void __launch_bounds__(1024, 1) k_block_perm(DevCtx c, const TermDesc
     const int ti = blockIdx.x / per, slot = blockIdx.x % per;
     const TermDesc t = terms[ti];
     const u64* src = t.X + (long long)slot * N;
-    for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src[k];
+    for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = ld_cs(src + k);
     __syncthreads();
     for (int r = 0; r < t.rot_cnt; r++) {
         const unsigned g = galois[t.rot_off + r];
         u64* o = t.blk + r * blk_words + (long long)slot * N;
-        for (int k = threadIdx.x; k < N; k += blockDim.x) o[k] = sm[pad(auto_src(k, g, c.logN))];
+        for (int k = threadIdx.x; k < N; k += blockDim.x) st_cs(o + k, sm[pad(auto_src(k, g, c.logN))]);
     }
 }
 
@@ -313,6 +313,23 @@ __global__ void k_addsub(DevCtx c, const u64* __restrict__ a, const u64* __restr
     }
 }
 
+// out[b] = ct[b] with c0 -= DM[b]  (batched subtract_plain)
+__global__ void k_sub_plain(DevCtx c, const u64* __restrict__ ct, const u64* __restrict__ DM, u64* __restrict__ out,
+                            int B)
+{
+    const long long LN = (long long)c.L * c.N, W = 2 * LN;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < B * W;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long b = x / W, r = x - b * W;
+        u64 v = ct[x];
+        if (r < LN) {
+            const int j = (int)(r >> c.logN);
+            v = sub_mod(v, DM[b * LN + r], c.mod[j].q);
+        }
+        out[x] = v;
+    }
+}
+
 // conv first-Add: acc[o][d][comp][j][k] = sum_ib sum_tap R[ib][tap][comp][j][k] * pt[o][ib][d][tap][j][k]
 // grid: (N/blockDim, L, n_obp * c_n)
 __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __restrict__ R, int n_ib, int k,
@@ -354,7 +371,7 @@ __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __re
 // one CTA per (vector b, prime j); each CTA recomputes the mod-p INTT (cheap,
 // p is a 20-bit modulus) to keep the kernel single-pass.
 template <int MODE>
-__global__ void __launch_bounds__(1024, 1) k_encode(DevCtx c, const uint32_t* __restrict__ slots, u64* __restrict__ out)
+__global__ void __launch_bounds__(512, 2) k_encode(DevCtx c, const uint32_t* __restrict__ slots, u64* __restrict__ out)
 {
     extern __shared__ u64 smem_enc[];
     u64* sm = smem_enc;
@@ -387,7 +404,7 @@ __global__ void __launch_bounds__(1024, 1) k_encode(DevCtx c, const uint32_t* __
 }
 
 // decrypt phase 1: per prime j: x_j = INTT(c0 + c1 * S)
-__global__ void __launch_bounds__(1024, 1) k_dec_phase1(DevCtx c, const u64* __restrict__ ct, u64* __restrict__ x)
+__global__ void __launch_bounds__(512, 2) k_dec_phase1(DevCtx c, const u64* __restrict__ ct, u64* __restrict__ x)
 {
     extern __shared__ u64 sm[];
     const int N = c.N, L = c.L, j = blockIdx.x;
@@ -416,7 +433,7 @@ __device__ __forceinline__ u64 frac64(u64 b, u64 q)
 }
 
 // decrypt phase 2 (one CTA): m = round(p x / Q) mod p via RNS; slots = decode(m)
-__global__ void __launch_bounds__(1024, 1) k_dec_phase2(DevCtx c, const u64* __restrict__ x, uint32_t* __restrict__ slots)
+__global__ void __launch_bounds__(512, 2) k_dec_phase2(DevCtx c, const u64* __restrict__ x, uint32_t* __restrict__ slots)
 {
     extern __shared__ u64 sm[];
     const int N = c.N, L = c.L, PM = c.M;

@@ -374,30 +374,48 @@ static const u64* key_for(gala_ctx* c, int step)
     return it == c->keys.end() ? nullptr : it->second;
 }
 
-// out[g] = sum_{j < per} rot_{j * unit}(X[g * per + j] (.) pt[...]), one lazy ModDown per g
-static int rotate_sum_regular(gala_ctx* c, const u64* X, long long x_stride, const u64* pts, int G, int per,
-                              int unit, u64* out)
+// For each batch element b and group g:
+//   out_b[g] = sum_{j < per} rot_{j * unit}(X_b[g * per + j] (.) pt[g * per + j]),
+// one lazy ModDown per (b, g); all batch elements share the launches.
+static int rotate_sum_regular(gala_ctx* c, const u64* X, long long x_stride, long long x_bstride, const u64* pts,
+                              int B, int G, int per, int unit, u64* out, long long out_bstride)
 {
     const int N = c->dc.N, L = c->dc.L;
     const long long W = 2LL * L * N, PW = (long long)L * N;
     std::vector<EngTerm> terms;
-    std::vector<std::vector<EngMember>> groups(G);
+    std::vector<std::vector<EngMember>> groups((size_t)B * G);
     std::vector<u64*> outs;
-    for (int g = 0; g < G; g++) {
-        for (int j = 0; j < per; j++) {
-            const int idx = g * per + j;
-            EngTerm t;
-            t.X = X + (long long)idx * x_stride;
-            t.pt = pts ? pts + (long long)idx * PW : nullptr;
-            t.ntt_block = nullptr;
-            int s = norm_step(c, j * unit);
-            if (s) t.steps.push_back(s);
-            terms.push_back(t);
-            groups[g].push_back({(int)terms.size() - 1, s ? 0 : -1});
+    terms.reserve((size_t)B * G * per);
+    for (int b = 0; b < B; b++)
+        for (int g = 0; g < G; g++) {
+            auto& grp = groups[(size_t)b * G + g];
+            for (int j = 0; j < per; j++) {
+                const int idx = g * per + j;
+                EngTerm t;
+                t.X = X + b * x_bstride + (long long)idx * x_stride;
+                t.pt = pts ? pts + (long long)idx * PW : nullptr;
+                t.ntt_block = nullptr;
+                int s = norm_step(c, j * unit);
+                if (s) t.steps.push_back(s);
+                terms.push_back(t);
+                grp.push_back({(int)terms.size() - 1, s ? 0 : -1});
+            }
+            outs.push_back(out + b * out_bstride + (long long)g * W);
         }
-        outs.push_back(out + (long long)g * W);
-    }
     return rotate_engine(c, terms, groups, outs);
+}
+
+// masked[b] = ct[b] - Delta encode(r[b]) for a batch (one encode launch for all b)
+static int sub_plain_batch(gala_ctx* c, const u64* ct, const uint32_t* r, int B, u64* out)
+{
+    const int N = c->dc.N, L = c->dc.L;
+    const long long W = 2LL * L * N, LN = (long long)L * N;
+    u64* DM;
+    RET(scratch(c, &DM, (size_t)B * LN));
+    KLAUNCH(c, "k_encode", k_encode<1><<<B * L, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(c->dc, r, DM));
+    KLAUNCH(c, "k_sub_plain", k_sub_plain<<<grid_for((long long)B * W, 256), 256, 0, c->stream>>>(c->dc, ct, DM, out, B));
+    release(c, DM);
+    return GALA_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -796,11 +814,11 @@ int gala_bsgs_baby(int T)
     return 1 << ((lg + 1) / 2);
 }
 
-int gala_mv_gala(gala_ctx* c, const uint64_t* ct, const uint64_t* pts, int T, int baby, const uint32_t* r,
-                 uint64_t* out, uint64_t* masked)
+int gala_mv_gala_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts, int T, int baby,
+                       const uint32_t* r, uint64_t* outs, uint64_t* masked)
 {
     const int N = c->dc.N, L = c->dc.L;
-    if (T <= 0) return set_err(GALA_ERR_DIM, "T must be positive");
+    if (T <= 0 || B <= 0) return set_err(GALA_ERR_DIM, "T and B must be positive");
     if (baby <= 0) baby = gala_bsgs_baby(T);
     if (T % baby) return set_err(GALA_ERR_PARAM, "baby step %d does not divide T=%d", baby, T);
     const int G = T / baby;
@@ -811,19 +829,28 @@ int gala_mv_gala(gala_ctx* c, const uint64_t* ct, const uint64_t* pts, int T, in
         if (!gala_has_rotation_key(c, g * baby))
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, g * baby));
     if (T == 1) {
-        dim3 grid((unsigned)((2 * L * N + 255) / 256), 1);
-        KLAUNCH(c, "k_ct_mul_pts", k_ct_mul_pts<<<grid, 256, 0, c->stream>>>(c->dc, ct, pts, out));
+        for (int b = 0; b < B; b++) {
+            dim3 grid((unsigned)((2 * L * N + 255) / 256), 1);
+            KLAUNCH(c, "k_ct_mul_pts", k_ct_mul_pts<<<grid, 256, 0, c->stream>>>(c->dc, cts + b * W, pts, outs + b * W));
+        }
     } else if (G == 1) {
-        RET(rotate_sum_regular(c, ct, 0, pts, 1, baby, 1, out));
+        RET(rotate_sum_regular(c, cts, 0, W, pts, B, 1, baby, 1, outs, W));
     } else {
         u64* inner;
-        RET(scratch(c, &inner, (size_t)G * W));
-        RET(rotate_sum_regular(c, ct, 0, pts, G, baby, 1, inner));   // baby steps, ScMult fused
-        RET(rotate_sum_regular(c, inner, W, nullptr, 1, G, baby, out));
+        RET(scratch(c, &inner, (size_t)B * G * W));
+        // baby steps with ScMult fused, then giant steps; each over the whole batch
+        RET(rotate_sum_regular(c, cts, 0, W, pts, B, G, baby, 1, inner, (long long)G * W));
+        RET(rotate_sum_regular(c, inner, W, (long long)G * W, nullptr, B, 1, G, baby, outs, W));
         release(c, inner);
     }
-    if (r && masked) RET(gala_sub_plain(c, out, r, masked));
+    if (r && masked) RET(sub_plain_batch(c, outs, r, B, masked));
     return GALA_OK;
+}
+
+int gala_mv_gala(gala_ctx* c, const uint64_t* ct, const uint64_t* pts, int T, int baby, const uint32_t* r,
+                 uint64_t* out, uint64_t* masked)
+{
+    return gala_mv_gala_batch(c, ct, 1, pts, T, baby, r, out, masked);
 }
 
 int gala_mv_gala_host(gala_ctx* c, const uint64_t* ct_host, const uint64_t* pts, int T, int baby,
@@ -904,7 +931,7 @@ int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts
     KLAUNCH(c, "k_kg_accumulate", k_kg_accumulate<<<grid, th, 0, c->stream>>>(c->dc, R, n_ib, k, pts, c_n, acc));
     release(c, R);
     // second-Perm: out[o] = sum_d rot_{d * band}(acc[o][d]), one lazy ModDown per o
-    RET(rotate_sum_regular(c, acc, W, nullptr, n_obp, c_n, band_step, outs));
+    RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, n_obp, c_n, band_step, outs, 0));
     release(c, acc);
     return GALA_OK;
 }

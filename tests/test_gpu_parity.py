@@ -96,3 +96,22 @@ def test_conv_kg_words(tw):
     g_out = tw.gpu.conv_kg(g_in, d_pts, tap_steps, band)
     c_out = tw.cpu.conv_kg(c_in, pts, tap_steps, band)
     assert np.array_equal(tw.gpu.export_words(g_out), c_out)
+
+
+def test_mv_gala_batch_words(tw):
+    """Batched entry point == per-input fused calls == oracle."""
+    import torch
+
+    n = tw.bfv.n
+    T = min(8, n)
+    b, steps = tw.gpu.bsgs_steps(T)
+    tw.keys_for(steps)
+    pts = tw.slots(T)
+    d_pts = tw.gpu.encode_plain(pts)
+    xs = [tw.encrypt(tw.slots()) for _ in range(3)]
+    rs = tw.slots(3)
+    outs, masked = tw.gpu.mv_gala_batch(torch.stack([g for g, _ in xs]), d_pts, T, tw.gpu.to_device_u32(rs))
+    for i, (g, c) in enumerate(xs):
+        c_out, c_masked = tw.cpu.mv_gala(c, pts, rs[i], baby=b)
+        assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
+        assert np.array_equal(tw.gpu.export_words(masked[i]), c_masked)

@@ -1,0 +1,191 @@
+// ntt_bench.cu -- standalone microbenchmark of forward-NTT kernel variants
+// (N = 8192, one 60-bit prime).  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
+//   -I paper_2105_01827_b200/csrc tools/ntt_bench.cu -o tools/ntt_bench
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "gala_device.cuh"
+
+typedef unsigned __int128 u128;
+static u64 h_mulmod(u64 a, u64 b, u64 q) { return (u64)(((u128)a * b) % q); }
+static u64 h_pow(u64 b, u64 e, u64 q)
+{
+    u64 r = 1;
+    b %= q;
+    while (e) {
+        if (e & 1) r = h_mulmod(r, b, q);
+        b = h_mulmod(b, b, q);
+        e >>= 1;
+    }
+    return r;
+}
+static int h_brv(int x, int logN)
+{
+    int r = 0;
+    for (int i = 0; i < logN; i++) r |= ((x >> i) & 1) << (logN - 1 - i);
+    return r;
+}
+
+#define CKE(x)                                                                      \
+    do {                                                                            \
+        cudaError_t e = (x);                                                        \
+        if (e != cudaSuccess) {                                                     \
+            printf("CUDA error %s at %d\n", cudaGetErrorString(e), __LINE__);       \
+            exit(1);                                                                \
+        }                                                                           \
+    } while (0)
+
+// A/C: one CTA per polynomial, twiddles from global
+template <int RMAX, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) v_percta(const u64* in, u64* out, const ulonglong2* tw, u64 q, int logN)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    const u64* src = in + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(i)] = src[i];
+    __syncthreads();
+    ntt_fwd_smem<false, RMAX>(sm, tw, q, logN);
+    u64* dst = out + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
+}
+
+// B: persistent CTA, twiddle table staged once in shared memory
+template <int RMAX, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) v_persist(const u64* in, u64* out, const ulonglong2* tw, u64 q, int logN,
+                                                       int polys)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    ulonglong2* stw = (ulonglong2*)(sm + padded_words(N));
+    for (int i = threadIdx.x; i < N; i += blockDim.x) stw[i] = tw[i];
+    for (int p = blockIdx.x; p < polys; p += gridDim.x) {
+        const u64* src = in + (long long)p * N;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(i)] = src[i];
+        __syncthreads();
+        ntt_fwd_smem<true, RMAX>(sm, stw, q, logN);
+        u64* dst = out + (long long)p * N;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
+        __syncthreads();
+    }
+}
+
+// H: 2 CTAs/SM (512 threads, 64 regs), each thread owns two radix-8 groups per pass
+template <int RMAX, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) v_percta2(const u64* in, u64* out, const ulonglong2* tw, u64 q, int logN)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    const u64* src = in + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(i)] = src[i];
+    __syncthreads();
+    ntt_fwd_smem<false, RMAX>(sm, tw, q, logN);
+    u64* dst = out + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
+}
+
+// I: persistent, double-buffered: cp.async prefetch of the next polynomial while transforming the current
+template <int RMAX, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) v_pipe(const u64* in, u64* out, const ulonglong2* tw, u64 q, int logN, int polys)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    u64* buf[2] = {sm, sm + padded_words(N)};
+    int p = blockIdx.x, cur = 0;
+    auto prefetch = [&](int pp, u64* b) {
+        const u64* src = in + (long long)pp * N;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            unsigned sa = (unsigned)__cvta_generic_to_shared(b + pad(i));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(src + i));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    };
+    if (p < polys) prefetch(p, buf[0]);
+    for (; p < polys; p += gridDim.x) {
+        int nxt = p + gridDim.x;
+        if (nxt < polys) prefetch(nxt, buf[cur ^ 1]);
+        if (nxt < polys) asm volatile("cp.async.wait_group 1;\n" ::);
+        else asm volatile("cp.async.wait_group 0;\n" ::);
+        __syncthreads();
+        ntt_fwd_smem<false, RMAX>(buf[cur], tw, q, logN);
+        u64* dst = out + (long long)p * N;
+        for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(buf[cur][pad(i)], 2 * q), q);
+        __syncthreads();
+        cur ^= 1;
+    }
+}
+
+int main()
+{
+    const int logN = 13, N = 1 << logN;
+    const u64 q = 1152921504606830593ull; // 60-bit, 1 mod 2^14
+    // primitive 2N-th root: g^((q-1)/2N), g least non-residue
+    u64 g = 2;
+    while (h_pow(g, (q - 1) / 2, q) == 1) g++;
+    u64 psi = h_pow(g, (q - 1) / (2 * N), q);
+    std::vector<ulonglong2> tw(N);
+    for (int k = 0; k < N; k++) {
+        u64 w = h_pow(psi, (u64)h_brv(k, logN), q);
+        tw[k] = make_ulonglong2(w, (u64)(((u128)w << 64) / q));
+    }
+    const int P = 4096;
+    std::vector<u64> h(P * (size_t)N);
+    srand(1);
+    for (auto& x : h) x = (((u64)rand() << 40) ^ ((u64)rand() << 20) ^ (u64)rand()) % q;
+    u64 *din, *dref, *dout;
+    ulonglong2* dtw;
+    CKE(cudaMalloc(&din, h.size() * 8));
+    CKE(cudaMalloc(&dref, h.size() * 8));
+    CKE(cudaMalloc(&dout, h.size() * 8));
+    CKE(cudaMalloc(&dtw, N * 16));
+    CKE(cudaMemcpy(din, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    CKE(cudaMemcpy(dtw, tw.data(), N * 16, cudaMemcpyHostToDevice));
+    const int smem = padded_words(N) * 8;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    double bfly = (double)P * (N / 2) * logN;
+    std::vector<u64> ref(h.size()), got(h.size());
+
+    auto run = [&](const char* name, auto launch, bool is_ref) {
+        launch();
+        CKE(cudaDeviceSynchronize());
+        cudaEventRecord(a);
+        for (int it = 0; it < 5; it++) launch();
+        cudaEventRecord(b);
+        CKE(cudaEventSynchronize(b));
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        ms /= 5;
+        CKE(cudaMemcpy(got.data(), is_ref ? dref : dout, got.size() * 8, cudaMemcpyDeviceToHost));
+        if (is_ref) ref = got;
+        bool ok = got == ref;
+        printf("%-28s %8.3f ms  %7.1f Gbfly/s  %s\n", name, ms, bfly / (ms * 1e-3) / 1e9, ok ? "ok" : "MISMATCH");
+    };
+
+    CKE(cudaFuncSetAttribute(v_percta<3, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("A percta R3 T1024", [&] { v_percta<3, 1024><<<P, 1024, smem>>>(din, dref, dtw, q, logN); }, true);
+    CKE(cudaFuncSetAttribute(v_percta<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("C percta R4 T512", [&] { v_percta<4, 512><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    CKE(cudaFuncSetAttribute(v_percta<5, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("F percta R5 T256", [&] { v_percta<5, 256><<<P, 256, smem>>>(din, dout, dtw, q, logN); }, false);
+    CKE(cudaFuncSetAttribute(v_percta<2, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("G percta R2 T1024", [&] { v_percta<2, 1024><<<P, 1024, smem>>>(din, dout, dtw, q, logN); }, false);
+    const int smemB = smem + N * 16;
+    CKE(cudaFuncSetAttribute(v_persist<3, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemB));
+    run("B persist R3 T1024", [&] { v_persist<3, 1024><<<148, 1024, smemB>>>(din, dout, dtw, q, logN, P); }, false);
+    CKE(cudaFuncSetAttribute(v_persist<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemB));
+    run("E persist R4 T512", [&] { v_persist<4, 512><<<148, 512, smemB>>>(din, dout, dtw, q, logN, P); }, false);
+    CKE(cudaFuncSetAttribute(v_percta2<3, 512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("H percta R3 T512 x2", [&] { v_percta2<3, 512, 2><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    CKE(cudaFuncSetAttribute(v_percta2<2, 512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("H2 percta R2 T512 x2", [&] { v_percta2<2, 512, 2><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    CKE(cudaFuncSetAttribute(v_percta2<3, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("H3 percta R3 T256 x3", [&] { v_percta2<3, 256, 3><<<P, 256, smem>>>(din, dout, dtw, q, logN); }, false);
+    const int smemI = 2 * smem;
+    CKE(cudaFuncSetAttribute(v_pipe<3, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemI));
+    run("I pipe R3 T1024", [&] { v_pipe<3, 1024><<<148, 1024, smemI>>>(din, dout, dtw, q, logN, P); }, false);
+    CKE(cudaFuncSetAttribute(v_pipe<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemI));
+    run("I2 pipe R4 T512", [&] { v_pipe<4, 512><<<148, 512, smemI>>>(din, dout, dtw, q, logN, P); }, false);
+    return 0;
+}
