@@ -227,23 +227,22 @@ def run_ours(args):
     # e2e: host buffers through the C-ABI host entry point (H2D ct + r, fused layer, D2H masked)
     import ctypes
 
-    host_ct = [torch.from_numpy(ctx.export_words(c).view(np.int64)).pin_memory() for c in cts]
-    host_r = [torch.from_numpy(r.view(np.int32)).pin_memory() for r in phys_r]
-    host_out = [torch.empty((2, L, N), dtype=torch.int64).pin_memory() for _ in range(B)]
+    host_ct = torch.from_numpy(ctx.export_words(cts_b).view(np.int64)).pin_memory()
+    host_r = torch.from_numpy(np.stack(phys_r).view(np.int32)).pin_memory()
+    host_out = torch.empty((B, 2, L, N), dtype=torch.int64).pin_memory()
     h = ctx._bind()
 
     def e2e_step():
-        for b in range(B):
-            _lib.check(ctx.lib.gala_mv_gala_host(h, ctypes.c_void_p(host_ct[b].data_ptr()),
-                                                 ctypes.c_void_p(pts.data_ptr()), T, baby,
-                                                 ctypes.c_void_p(host_r[b].data_ptr()),
-                                                 ctypes.c_void_p(host_out[b].data_ptr())))
+        # one C-ABI call per step: H2D of B canonical ciphertexts + masks, fused layers, D2H of masked words
+        _lib.check(ctx.lib.gala_mv_gala_batch_host(h, ctypes.c_void_p(host_ct.data_ptr()), B,
+                                                   ctypes.c_void_p(pts.data_ptr()), T, baby,
+                                                   ctypes.c_void_p(host_r.data_ptr()),
+                                                   ctypes.c_void_p(host_out.data_ptr())))
 
     e2e_step()
     # e2e parity: host-path masked words equal the device-path masked words
-    for b in range(min(B, 2)):
-        if not np.array_equal(host_out[b].numpy().view(np.uint64), ctx.export_words(masked[b])):
-            raise SystemExit("e2e host path disagrees with device path")
+    if not np.array_equal(host_out.numpy().view(np.uint64), ctx.export_words(masked)):
+        raise SystemExit("e2e host path disagrees with device path")
     e2e_times = []
     for _ in range(args.steps):
         flush.zero_()
@@ -323,7 +322,7 @@ def run_ours(args):
         "kernel_breakdown_ms_per_step": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
         "e2e": {"value": round(e2e_value, 3), "unit": "layers/s",
                 "h2d_bytes_per_step": B * (ct_bytes + N * 4), "d2h_bytes_per_step": B * ct_bytes,
-                "path": "gala_mv_gala_host (C-ABI, pinned host buffers, canonical words)"},
+                "path": "gala_mv_gala_batch_host (C-ABI, pinned host buffers, canonical words, one call per step)"},
         "gpu_launches": int(launches),
         "setup_s": round(setup_s, 2),
         "clocks": clk.summary(),

@@ -101,6 +101,9 @@ int gala_bsgs_baby(int T);
  * stream; blocks until the result is in host memory. */
 int gala_mv_gala_host(gala_ctx *ctx, const uint64_t *ct_host, const uint64_t *pts_dev, int T, int baby,
                       const uint32_t *r_slots_host, uint64_t *masked_host);
+/* Batched host-buffer form: cts_host [B][2][L][N] canonical words, r [B][N]. */
+int gala_mv_gala_batch_host(gala_ctx *ctx, const uint64_t *cts_host, int B, const uint64_t *pts_dev, int T,
+                            int baby, const uint32_t *r_slots_host, uint64_t *masked_host);
 
 /* Fused kernel-grouping convolution (mimo_kernel_grouping, conv.py:268-293):
  * cts_dev [n_ib][2][L][N]; pts_dev [n_obp][n_ib][c_n][k][L][N];

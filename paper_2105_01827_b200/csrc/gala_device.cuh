@@ -226,6 +226,105 @@ __device__ __forceinline__ void ntt_inv_smem(u64* s, const ulonglong2* tw, u64 q
 
 // 512 threads for N = 8192 (two radix-8 groups per thread per pass) so that two
 // CTAs (2 x 66 KB smem, <= 64 registers) share an SM and overlap their memory phases
+// ---------------------------------------------------------------------------
+// Production NTT plans (radix-8 passes, the odd remainder pass at the global
+// edge): forward = [first pass fed straight from global memory through a loader
+// functor] + radix-8 smem passes; inverse = radix-8 smem passes + [last pass
+// written straight to global memory through a storer functor].  For log N = 13
+// the split is 1,3,3,3,3 (forward) and 3,3,3,3,1 (inverse).
+__host__ __device__ constexpr int edge_r(int logN) { return logN % 3 == 0 ? 3 : logN % 3; }
+
+template <int R, class Loader>
+__device__ __forceinline__ void fwd_first_pass(Loader ld, u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN)
+{
+    const int N = 1 << logN;
+    const int G = N >> R;
+    const int lt = logN - R;
+    const u64 q2 = 2 * q;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        u64 x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) x[k] = ld(g + (k << lt));
+#pragma unroll
+        for (int l = 0; l < R; l++) {
+            const int m = 1 << l;
+            const int half = 1 << (R - 1 - l);
+#pragma unroll
+            for (int k = 0; k < (1 << R); k++) {
+                if (k & half) continue;
+                const ulonglong2 w = __ldg(&tw[m + (k >> (R - l))]);
+                u64 U = x[k];
+                U = U >= q2 ? U - q2 : U;
+                u64 V = shoup_lazy(x[k + half], w.x, w.y, q);
+                x[k] = U + V;
+                x[k + half] = U - V + q2;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) s[pad(g + (k << lt))] = x[k];
+    }
+}
+
+template <int R, class Storer>
+__device__ __forceinline__ void inv_last_pass(const u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, Storer st)
+{
+    const int N = 1 << logN;
+    const int G = N >> R;
+    const int lt = logN - R;
+    const u64 q2 = 2 * q;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        u64 x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) x[k] = s[pad(g + (k << lt))];
+#pragma unroll
+        for (int l = R - 1; l >= 0; l--) {
+            const int m = 1 << l;
+            const int half = 1 << (R - 1 - l);
+#pragma unroll
+            for (int k = 0; k < (1 << R); k++) {
+                if (k & half) continue;
+                const ulonglong2 w = __ldg(&tw[m + (k >> (R - l))]);
+                u64 U = x[k], V = x[k + half];
+                u64 a = U + V;
+                x[k] = a >= q2 ? a - q2 : a;
+                x[k + half] = shoup_lazy(U - V + q2, w.x, w.y, q);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) st(g + (k << lt), x[k]);
+    }
+}
+
+// forward: ld(i) -> natural-order input in [0, 4q); result in s (bit-reversed, [0, 4q)); ends synced
+template <class Loader>
+__device__ __forceinline__ void ntt_fwd_g(Loader ld, u64* s, const ulonglong2* tw, u64 q, int logN)
+{
+    const int r0 = edge_r(logN);
+    if (r0 == 1) fwd_first_pass<1>(ld, s, tw, q, logN);
+    else if (r0 == 2) fwd_first_pass<2>(ld, s, tw, q, logN);
+    else fwd_first_pass<3>(ld, s, tw, q, logN);
+    __syncthreads();
+    for (int s0 = r0; s0 < logN; s0 += 3) {
+        fwd_pass<3>(s, tw, q, logN, s0);
+        __syncthreads();
+    }
+}
+
+// inverse: s holds bit-reversed input in [0, 2q) (synced); st(i, v) receives the natural-order
+// output v in [0, 2q) *before* the N^-1 scaling
+template <class Storer>
+__device__ __forceinline__ void ntt_inv_g(u64* s, const ulonglong2* tw, u64 q, int logN, Storer st)
+{
+    const int rl = edge_r(logN);
+    for (int s0 = logN - 3; s0 >= rl; s0 -= 3) {
+        inv_pass<3>(s, tw, q, logN, s0);
+        __syncthreads();
+    }
+    if (rl == 1) inv_last_pass<1>(s, tw, q, logN, st);
+    else if (rl == 2) inv_last_pass<2>(s, tw, q, logN, st);
+    else inv_last_pass<3>(s, tw, q, logN, st);
+}
+
 __host__ __device__ inline int ntt_threads(int N)
 {
     int t = N >> (GALA_NTT_R + 1);

@@ -58,11 +58,8 @@ __global__ void __launch_bounds__(512, 2) k_ntt_fwd(DevCtx c, const T* __restric
     polymap_resolve(pm, blockIdx.x, c.N, so, dof, j);
     const ModC md = c.mod[j];
     const u64 q = md.q;
-    for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
-        sm[pad(i)] = to_residue<T>(src[so + i], q);
-    }
-    __syncthreads();
-    ntt_fwd_smem(sm, c.twf[j], q, c.logN);
+    const T* sp = src + so;
+    ntt_fwd_g([&](int i) { return to_residue<T>(sp[i], q); }, sm, c.twf[j], q, c.logN);
     for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
         u64 v = sm[pad(i)];
         v = csub(csub(v, 2 * q), q);
@@ -87,9 +84,9 @@ __global__ void __launch_bounds__(512, 2) k_ntt_inv(DevCtx c, const u64* __restr
         sm[pad(i)] = v;
     }
     __syncthreads();
-    ntt_inv_smem(sm, c.twi[j], q, c.logN);
     const u64 ni = c.ninv[j], nsh = c.ninv_sh[j];
-    for (int i = threadIdx.x; i < c.N; i += blockDim.x) st_cs(dst + dof + i, shoup(sm[pad(i)], ni, nsh, q));
+    u64* dp = dst + dof;
+    ntt_inv_g(sm, c.twi[j], q, c.logN, [&](int i, u64 v) { st_cs(dp + i, shoup(v, ni, nsh, q)); });
 }
 
 // ---------------------------------------------------------------------------
@@ -115,13 +112,11 @@ __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
     const ModC md = c.mod[j];
     const u64 q = md.q, P = c.mod[L].q, halfP = P >> 1;
     const u64* r = a.r + ((long long)g * 2 + comp) * N;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        u64 v = r[i];
-        // centred lift of v in [0, P) into [0, 2q): |v - P| < P/2 < q
-        sm[pad(i)] = v > halfP ? q - (P - v) : v; // P/2 < q_j asserted at context creation
-    }
-    __syncthreads();
-    ntt_fwd_smem(sm, c.twf[j], q, c.logN);
+    // centred lift of v in [0, P) into [0, 2q): |v - P| < P/2 < q_j (asserted at context creation)
+    ntt_fwd_g([&](int i) {
+        const u64 v = r[i];
+        return v > halfP ? q - (P - v) : v;
+    }, sm, c.twf[j], q, c.logN);
     const u64* U = a.U + (((long long)g * 2 + comp) * M + j) * N;
     const u64* add = comp == 0 ? a.add0 : a.add1;
     if (add) add += (long long)g * a.add_is + (long long)j * N;
@@ -171,10 +166,9 @@ __global__ void __launch_bounds__(512, 2) k_digits_intt(DevCtx c, const TermDesc
     const u64 q = c.mod[i].q;
     for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 1, i, k);
     __syncthreads();
-    ntt_inv_smem(sm, c.twi[i], q, c.logN);
     u64* d = t.dig + (long long)i * N;
     const u64 ni = c.ninv[i], nsh = c.ninv_sh[i];
-    for (int k = threadIdx.x; k < N; k += blockDim.x) st_cs(d + k, shoup(sm[pad(k)], ni, nsh, q));
+    ntt_inv_g(sm, c.twi[i], q, c.logN, [&](int k, u64 v) { st_cs(d + k, shoup(v, ni, nsh, q)); });
 }
 
 // grid: terms * (L*M + L) CTAs
@@ -193,10 +187,7 @@ __global__ void __launch_bounds__(512, 2) k_digits_perm(DevCtx c, const TermDesc
         const u64 q = c.mod[j].q;
         if (i != j) {
             const u64* d = t.dig + (long long)i * N;   // d < q_i < 4 q_j: lazy NTT input
-            for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = ld_cs(d + k);
-            __syncthreads();
-            ntt_fwd_smem(sm, c.twf[j], q, c.logN);
-            for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = csub(csub(sm[pad(k)], 2 * q), q);
+            ntt_fwd_g([&](int k) { return ld_cs(d + k); }, sm, c.twf[j], q, c.logN);
         } else {
             for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 1, j, k);
         }
@@ -205,10 +196,12 @@ __global__ void __launch_bounds__(512, 2) k_digits_perm(DevCtx c, const TermDesc
         for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 0, j, k);
     }
     __syncthreads();
+    const u64 q = c.mod[j].q;   // NTT outputs are in [0, 4q): fold on the permuted read
     for (int r = 0; r < t.rot_cnt; r++) {
         const unsigned g = galois[t.rot_off + r];
         u64* o = t.blk + r * blk_words + (long long)slot * N;
-        for (int k = threadIdx.x; k < N; k += blockDim.x) st_cs(o + k, sm[pad(auto_src(k, g, c.logN))]);
+        for (int k = threadIdx.x; k < N; k += blockDim.x)
+            st_cs(o + k, csub(csub(sm[pad(auto_src(k, g, c.logN))], 2 * q), q));
     }
 }
 

@@ -853,24 +853,24 @@ int gala_mv_gala(gala_ctx* c, const uint64_t* ct, const uint64_t* pts, int T, in
     return gala_mv_gala_batch(c, ct, 1, pts, T, baby, r, out, masked);
 }
 
-int gala_mv_gala_host(gala_ctx* c, const uint64_t* ct_host, const uint64_t* pts, int T, int baby,
-                      const uint32_t* r_host, uint64_t* masked_host)
+int gala_mv_gala_batch_host(gala_ctx* c, const uint64_t* cts_host, int B, const uint64_t* pts, int T, int baby,
+                            const uint32_t* r_host, uint64_t* masked_host)
 {
     const int N = c->dc.N, L = c->dc.L;
     const long long W = 2LL * L * N;
     u64 *coef, *ct, *out, *masked;
     uint32_t* r;
-    RET(scratch(c, &coef, (size_t)W));
-    RET(scratch(c, &ct, (size_t)W));
-    RET(scratch(c, &out, (size_t)W));
-    RET(scratch(c, &masked, (size_t)W));
-    RET(scratch(c, &r, (size_t)N));
-    CK(cudaMemcpyAsync(coef, ct_host, sizeof(u64) * W, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(r, r_host, sizeof(uint32_t) * N, cudaMemcpyHostToDevice, c->stream));
-    RET(gala_ct_import(c, coef, ct, 1));
-    RET(gala_mv_gala(c, ct, pts, T, baby, r, out, masked));
-    RET(gala_ct_export(c, masked, coef, 1));
-    CK(cudaMemcpyAsync(masked_host, coef, sizeof(u64) * W, cudaMemcpyDeviceToHost, c->stream));
+    RET(scratch(c, &coef, (size_t)B * W));
+    RET(scratch(c, &ct, (size_t)B * W));
+    RET(scratch(c, &out, (size_t)B * W));
+    RET(scratch(c, &masked, (size_t)B * W));
+    RET(scratch(c, &r, (size_t)B * N));
+    CK(cudaMemcpyAsync(coef, cts_host, sizeof(u64) * B * W, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(r, r_host, sizeof(uint32_t) * B * N, cudaMemcpyHostToDevice, c->stream));
+    RET(gala_ct_import(c, coef, ct, B));
+    RET(gala_mv_gala_batch(c, ct, B, pts, T, baby, r, out, masked));
+    RET(gala_ct_export(c, masked, coef, B));
+    CK(cudaMemcpyAsync(masked_host, coef, sizeof(u64) * B * W, cudaMemcpyDeviceToHost, c->stream));
     release(c, coef);
     release(c, ct);
     release(c, out);
@@ -878,6 +878,12 @@ int gala_mv_gala_host(gala_ctx* c, const uint64_t* ct_host, const uint64_t* pts,
     release(c, r);
     CK(cudaStreamSynchronize(c->stream));
     return GALA_OK;
+}
+
+int gala_mv_gala_host(gala_ctx* c, const uint64_t* ct_host, const uint64_t* pts, int T, int baby,
+                      const uint32_t* r_host, uint64_t* masked_host)
+{
+    return gala_mv_gala_batch_host(c, ct_host, 1, pts, T, baby, r_host, masked_host);
 }
 
 int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts, int n_obp, int c_n, int k,

@@ -115,6 +115,57 @@ __global__ void __launch_bounds__(THREADS, 1) v_pipe(const u64* in, u64* out, co
     }
 }
 
+// J: explicit pass plan; the first pass loads straight from global into registers
+template <int R>
+__device__ __forceinline__ void fwd_pass_from_global(const u64* __restrict__ g, u64* s, const ulonglong2* __restrict__ tw,
+                                                     u64 q, int logN)
+{
+    const int N = 1 << logN;
+    const int G = N >> R;
+    const int lt = logN - R;
+    const u64 q2 = 2 * q;
+    for (int gi = threadIdx.x; gi < G; gi += blockDim.x) {
+        const int off = gi;   // s0 = 0: blk = 0
+        u64 x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) x[k] = g[off + (k << lt)];
+#pragma unroll
+        for (int l = 0; l < R; l++) {
+            const int m = 1 << l;
+            const int half = 1 << (R - 1 - l);
+#pragma unroll
+            for (int k = 0; k < (1 << R); k++) {
+                if (k & half) continue;
+                const ulonglong2 w = __ldg(&tw[m + (k >> (R - l))]);
+                u64 U = x[k];
+                U = U >= q2 ? U - q2 : U;
+                u64 V = shoup_lazy(x[k + half], w.x, w.y, q);
+                x[k] = U + V;
+                x[k + half] = U - V + q2;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) s[pad(off + (k << lt))] = x[k];
+    }
+}
+
+template <int R0, int R1, int R2, int R3, int R4, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) v_plan(const u64* in, u64* out, const ulonglong2* tw, u64 q, int logN)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    const u64* src = in + (long long)blockIdx.x * N;
+    fwd_pass_from_global<R0>(src, sm, tw, q, logN);
+    __syncthreads();
+    int s0 = R0;
+    if (R1) { fwd_pass<(R1 ? R1 : 1)>(sm, tw, q, logN, s0); __syncthreads(); s0 += R1; }
+    if (R2) { fwd_pass<(R2 ? R2 : 1)>(sm, tw, q, logN, s0); __syncthreads(); s0 += R2; }
+    if (R3) { fwd_pass<(R3 ? R3 : 1)>(sm, tw, q, logN, s0); __syncthreads(); s0 += R3; }
+    if (R4) { fwd_pass<(R4 ? R4 : 1)>(sm, tw, q, logN, s0); __syncthreads(); s0 += R4; }
+    u64* dst = out + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
+}
+
 int main()
 {
     const int logN = 13, N = 1 << logN;
@@ -182,6 +233,16 @@ int main()
     run("H2 percta R2 T512 x2", [&] { v_percta2<2, 512, 2><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
     CKE(cudaFuncSetAttribute(v_percta2<3, 256, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     run("H3 percta R3 T256 x3", [&] { v_percta2<3, 256, 3><<<P, 256, smem>>>(din, dout, dtw, q, logN); }, false);
+#define PLAN(name, a, b, c, d, e, T, MB)                                                                      \
+    CKE(cudaFuncSetAttribute(v_plan<a, b, c, d, e, T, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));      \
+    run(name, [&] { v_plan<a, b, c, d, e, T, MB><<<P, T, smem>>>(din, dout, dtw, q, logN); }, false);
+    PLAN("J 3,3,3,3,1 T512x2 gl", 3, 3, 3, 3, 1, 512, 2)
+    PLAN("J 4,3,3,3 T512x2 gl", 4, 3, 3, 3, 0, 512, 2)
+    PLAN("J 3,3,3,4 T512x2 gl", 3, 3, 3, 4, 0, 512, 2)
+    PLAN("J 1,3,3,3,3 T512x2 gl", 1, 3, 3, 3, 3, 512, 2)
+    PLAN("J 4,4,4,1 T512x2 gl", 4, 4, 4, 1, 0, 512, 2)
+    PLAN("J 3,3,3,3,1 T256x3 gl", 3, 3, 3, 3, 1, 256, 3)
+    PLAN("J 3,3,3,3,1 T1024x1 gl", 3, 3, 3, 3, 1, 1024, 1)
     const int smemI = 2 * smem;
     CKE(cudaFuncSetAttribute(v_pipe<3, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemI));
     run("I pipe R3 T1024", [&] { v_pipe<3, 1024><<<148, 1024, smemI>>>(din, dout, dtw, q, logN, P); }, false);
