@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(512, 2) k_ntt_fwd(DevCtx c, const T* __restric
     const ModC md = c.mod[j];
     const u64 q = md.q;
     const T* sp = src + so;
-    ntt_fwd_g([&](int i) { return to_residue<T>(sp[i], q); }, sm, c.twf[j], q, c.logN);
+    ntt_fwd_g([=](int i) { return to_residue<T>(sp[i], q); }, sm, c.twf[j], q, c.logN);
     for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
         u64 v = sm[pad(i)];
         v = csub(csub(v, 2 * q), q);
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(512, 2) k_ntt_inv(DevCtx c, const u64* __restr
     __syncthreads();
     const u64 ni = c.ninv[j], nsh = c.ninv_sh[j];
     u64* dp = dst + dof;
-    ntt_inv_g(sm, c.twi[j], q, c.logN, [&](int i, u64 v) { st_cs(dp + i, shoup(v, ni, nsh, q)); });
+    ntt_inv_g(sm, c.twi[j], q, c.logN, [=](int i, u64 v) { st_cs(dp + i, shoup(v, ni, nsh, q)); });
 }
 
 // ---------------------------------------------------------------------------
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
     const u64 q = md.q, P = c.mod[L].q, halfP = P >> 1;
     const u64* r = a.r + ((long long)g * 2 + comp) * N;
     // centred lift of v in [0, P) into [0, 2q): |v - P| < P/2 < q_j (asserted at context creation)
-    ntt_fwd_g([&](int i) {
+    ntt_fwd_g([=](int i) {
         const u64 v = r[i];
         return v > halfP ? q - (P - v) : v;
     }, sm, c.twf[j], q, c.logN);
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(512, 2) k_digits_intt(DevCtx c, const TermDesc
     __syncthreads();
     u64* d = t.dig + (long long)i * N;
     const u64 ni = c.ninv[i], nsh = c.ninv_sh[i];
-    ntt_inv_g(sm, c.twi[i], q, c.logN, [&](int k, u64 v) { st_cs(d + k, shoup(v, ni, nsh, q)); });
+    ntt_inv_g(sm, c.twi[i], q, c.logN, [=](int k, u64 v) { st_cs(d + k, shoup(v, ni, nsh, q)); });
 }
 
 // grid: terms * (L*M + L) CTAs
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(512, 2) k_digits_perm(DevCtx c, const TermDesc
         const u64 q = c.mod[j].q;
         if (i != j) {
             const u64* d = t.dig + (long long)i * N;   // d < q_i < 4 q_j: lazy NTT input
-            ntt_fwd_g([&](int k) { return ld_cs(d + k); }, sm, c.twf[j], q, c.logN);
+            ntt_fwd_g([=](int k) { return ld_cs(d + k); }, sm, c.twf[j], q, c.logN);
         } else {
             for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 1, j, k);
         }
