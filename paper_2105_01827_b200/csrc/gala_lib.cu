@@ -582,21 +582,24 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaMalloc(&c->d_S, sizeof(u64) * (size_t)M * N));
     d.S = c->d_S;
     c->smem_ntt = padded_words(N) * (int)sizeof(u64);
-    // opt in to large dynamic shared memory for every NTT-carrying kernel
-    CKC(cudaFuncSetAttribute(k_ntt_fwd<u64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_ntt_fwd<u64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_ntt_fwd<i64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_ntt_fwd<int8_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_ntt_inv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_ntt_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_moddown, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_digits_intt, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_digits_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_block_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_encode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_dec_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
-    CKC(cudaFuncSetAttribute(k_dec_phase2, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_ntt));
+    // opt in to large dynamic shared memory for every NTT-carrying kernel.  The attribute is
+    // process-global per function, so always request the largest ring (N = 8192): contexts of
+    // different N coexist.
+    const int kMaxSmem = padded_words(8192) * (int)sizeof(u64);
+    CKC(cudaFuncSetAttribute(k_ntt_fwd<u64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_ntt_fwd<u64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_ntt_fwd<i64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_ntt_fwd<int8_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_ntt_inv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_ntt_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_moddown, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_digits_intt, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_digits_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_block_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_encode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_dec_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_dec_phase2, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     // keep freed scratch in the pool (stream-ordered allocator as a caching pool)
     cudaMemPool_t pool;
     CKC(cudaDeviceGetDefaultMemPool(&pool, device));
