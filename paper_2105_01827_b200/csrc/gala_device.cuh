@@ -32,6 +32,7 @@ struct DevCtx {
     u64 pinv_mont[GALA_MAXM];   // P^-1 * R mod q_j (Montgomery operand)
     u64 qhat_inv[GALA_MAXM];    // [(Q/q_i)^-1]_{q_i}
     u64 qhat_inv_sh[GALA_MAXM];
+    int lazy[GALA_MAXM];        // products a 128-bit accumulator may take before REDC: k q^2 < q 2^64
     u64 p;                      // plaintext modulus
     const u64* S;               // secret, NTT (bit-reversed), Montgomery form, [M][N]
     const int* slot_pos;        // slot index -> bit-reversed NTT_p position

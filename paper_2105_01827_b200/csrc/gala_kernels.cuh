@@ -232,45 +232,82 @@ struct MacMember {
     const u64* pt;
 };
 
-// grid (N / blockDim, M, G); U [G][2][M][N]; Cacc [G][2][L][N]
+// grid (N / blockDim, M, G); U [G][2][M][N]; Cacc [G][2][L][N].
+// Step-0 members come first in every group (host guarantees the order); the
+// rotated members follow.  Digit/key products accumulate in 128 bits across
+// digits *and* members and are Montgomery-reduced only every c.lazy[j]
+// products (k q^2 < q 2^64).  The next member's loads are issued before the
+// current member's multiplies (software pipelining over the member loop).
+template <int L>
 __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __restrict__ mem,
                                                 const int* __restrict__ group_off, u64* __restrict__ U,
                                                 u64* __restrict__ Cacc)
 {
-    const int N = c.N, L = c.L, M = c.M;
+    const int N = c.N, M = L + 1;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y, g = blockIdx.z;
     if (k >= N) return;
     const ModC md = c.mod[j];
     const u64 q = md.q;
+    const int lazy = c.lazy[j];
     const long long NN = N;
     u64 u0 = 0, u1 = 0, a0 = 0, a1 = 0;
-    const int lo = group_off[g], hi = group_off[g + 1];
-    for (int it = lo; it < hi; it++) {
+    int it = group_off[g];
+    const int hi = group_off[g + 1];
+    for (; it < hi; it++) {                       // step-0 members
         const MacMember m = mem[it];
-        if (!m.blk) {
-            if (j < L) {
-                u64 x0 = m.X[(long long)j * NN + k], x1 = m.X[((long long)L + j) * NN + k];
-                if (m.pt) {
-                    const u64 w = m.pt[(long long)j * NN + k];
-                    x0 = mont_mul(x0, w, md);
-                    x1 = mont_mul(x1, w, md);
-                }
-                a0 = add_mod(a0, x0, q);
-                a1 = add_mod(a1, x1, q);
+        if (m.blk) break;
+        if (j < L) {
+            u64 x0 = m.X[(long long)j * NN + k], x1 = m.X[((long long)L + j) * NN + k];
+            if (m.pt) {
+                const u64 w = __ldg(&m.pt[(long long)j * NN + k]);
+                x0 = mont_mul(x0, w, md);
+                x1 = mont_mul(x1, w, md);
             }
-            continue;
+            a0 = add_mod(a0, x0, q);
+            a1 = add_mod(a1, x1, q);
         }
-        Acc128 s0, s1;
-        for (int i = 0; i < L; i++) {
-            const u64 d = m.blk[((long long)i * M + j) * NN + k];
-            s0.mac(d, __ldg(&m.key[(((long long)i * 2 + 0) * M + j) * NN + k]));
-            s1.mac(d, __ldg(&m.key[(((long long)i * 2 + 1) * M + j) * NN + k]));
-        }
-        u0 = add_mod(u0, s0.reduce(md), q);
-        u1 = add_mod(u1, s1.reduce(md), q);
-        if (j < L) a0 = add_mod(a0, m.blk[((long long)L * M + j) * NN + k], q);
     }
+    Acc128 s0, s1;
+    int pending = 0;
+    constexpr int LMAX = L;
+    u64 dv[LMAX], kb[LMAX], ka[LMAX], cv = 0;
+    auto fetch = [&](const MacMember& m) {
+#pragma unroll
+        for (int i = 0; i < LMAX; i++) {
+            if (i < L) {
+                dv[i] = __ldcs((const unsigned long long*)(m.blk + ((long long)i * M + j) * NN + k));
+                kb[i] = __ldg(&m.key[(((long long)i * 2 + 0) * M + j) * NN + k]);
+                ka[i] = __ldg(&m.key[(((long long)i * 2 + 1) * M + j) * NN + k]);
+            }
+        }
+        if (j < L) cv = __ldcs((const unsigned long long*)(m.blk + ((long long)L * M + j) * NN + k));
+    };
+    if (it < hi) fetch(mem[it]);
+    for (; it < hi; it++) {
+        u64 d[LMAX], b[LMAX], a[LMAX], cc = cv;
+#pragma unroll
+        for (int i = 0; i < LMAX; i++) { d[i] = dv[i]; b[i] = kb[i]; a[i] = ka[i]; }
+        if (it + 1 < hi) fetch(mem[it + 1]);      // prefetch the next member
+        if (pending + L > lazy) {
+            u0 = add_mod(u0, s0.reduce(md), q);
+            u1 = add_mod(u1, s1.reduce(md), q);
+            s0 = Acc128();
+            s1 = Acc128();
+            pending = 0;
+        }
+#pragma unroll
+        for (int i = 0; i < LMAX; i++) {
+            if (i < L) {
+                s0.mac(d[i], b[i]);
+                s1.mac(d[i], a[i]);
+            }
+        }
+        pending += L;
+        if (j < L) a0 = add_mod(a0, cc, q);
+    }
+    u0 = add_mod(u0, s0.reduce(md), q);
+    u1 = add_mod(u1, s1.reduce(md), q);
     U[(((long long)g * 2 + 0) * M + j) * NN + k] = u0;
     U[(((long long)g * 2 + 1) * M + j) * NN + k] = u1;
     if (j < L) {
@@ -294,7 +331,7 @@ __global__ void k_ct_mul_pts(DevCtx c, const u64* __restrict__ ct, const u64* __
     out[t * 2 * LN + x] = mont_mul(ct[x], __ldg(&pts[t * LN + jl]), c.mod[j]);
 }
 
-// out = a + b (sign = +1) or a - b (sign = -1) over `polys` polys of nprimes-periodic primes
+// out = a + b (sign = +1) or a - b (sign = -1) over nprimes-periodic polynomials
 __global__ void k_addsub(DevCtx c, const u64* __restrict__ a, const u64* __restrict__ b, u64* __restrict__ out,
                          long long total, int nprimes, int sign)
 {

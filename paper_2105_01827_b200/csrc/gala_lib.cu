@@ -5,6 +5,7 @@
 // for operation, so ciphertext words agree exactly.  See include/gala_b200.h.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -289,8 +290,10 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     }
     std::vector<MacMember> mem;
     std::vector<int> off;
-    for (auto& g : groups) {
+    for (auto& g0 : groups) {
         off.push_back((int)mem.size());
+        std::vector<EngMember> g(g0);   // k_ks_mac expects the step-0 members first
+        std::stable_partition(g.begin(), g.end(), [](const EngMember& m) { return m.rot < 0; });
         for (auto& m : g) {
             MacMember mm;
             const EngTerm& T = terms[m.term];
@@ -345,8 +348,16 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     RET(scratch(c, &r, (size_t)G * 2 * N));
     const int th = N < 256 ? N : 256;
     dim3 grid((N + th - 1) / th, M, G);
-    KLAUNCH(c, "k_ks_mac", k_ks_mac<<<grid, th, 0, c->stream>>>(c->dc, (const MacMember*)(d_blob + o_mem),
-                                                                (const int*)(d_blob + o_off), U, Cacc));
+    {
+        const MacMember* dm = (const MacMember*)(d_blob + o_mem);
+        const int* doff = (const int*)(d_blob + o_off);
+        switch (L) {
+            case 1: KLAUNCH(c, "k_ks_mac", k_ks_mac<1><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
+            case 2: KLAUNCH(c, "k_ks_mac", k_ks_mac<2><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
+            case 3: KLAUNCH(c, "k_ks_mac", k_ks_mac<3><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
+            default: KLAUNCH(c, "k_ks_mac", k_ks_mac<4><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
+        }
+    }
     RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
     MdArgs a;
@@ -505,6 +516,11 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
         d.mod[j].qinv_neg = (u64)0 - inv;
         u64 r1 = (u64)(((u128)1 << 64) % q);
         d.mod[j].r2 = h_mulmod(r1, r1, q);
+        {
+            u128 kmax = (((u128)1) << 64) / q; // k q < 2^64  =>  k products of (< q) x (< q) stay below q 2^64
+            d.lazy[j] = (int)(kmax > 64 ? 64 : kmax) - 1;
+            if (d.lazy[j] < 1) d.lazy[j] = 1;
+        }
         d.ninv[j] = h_inv((u64)N % q, q);
         d.ninv_sh[j] = h_shoup(d.ninv[j], q);
     }
