@@ -52,6 +52,22 @@ __device__ __forceinline__ u64 shoup_lazy(u64 x, u64 w, u64 wsh, u64 q)
 }
 __device__ __forceinline__ u64 shoup(u64 x, u64 w, u64 wsh, u64 q) { return csub(shoup_lazy(x, w, wsh, q), q); }
 
+// Shoup for special-form primes q = a 2^32 + 1: hi * q mod 2^64 = hi + ((lo32(hi) a mod 2^32) << 32),
+// one 32-bit IMAD instead of a 64x64 low product.  Same result as shoup_lazy.
+__device__ __forceinline__ u64 shoup_lazy_sf(u64 x, u64 w, u64 wsh, u64 q)
+{
+    const u64 hi = __umul64hi(x, wsh);
+    const uint32_t a = (uint32_t)(q >> 32);
+    const u64 hq = hi + ((u64)((uint32_t)hi * a) << 32);
+    return x * w - hq;
+}
+template <bool SF>
+__device__ __forceinline__ u64 shoup_lz(u64 x, u64 w, u64 wsh, u64 q)
+{
+    if (SF) return shoup_lazy_sf(x, w, wsh, q);
+    return shoup_lazy(x, w, wsh, q);
+}
+
 // Montgomery REDC of hi:lo < q 2^64: returns (hi:lo) 2^-64 mod q in [0, 2q)
 __device__ __forceinline__ u64 redc_lazy(u64 hi, u64 lo, const ModC& m)
 {
@@ -109,7 +125,7 @@ __device__ __forceinline__ ulonglong2 tw_load(const ulonglong2* p)
     return __ldg(p);
 }
 
-template <int R, bool TW_SMEM = false>
+template <int R, bool TW_SMEM = false, bool SF = false>
 __device__ __forceinline__ void fwd_pass(u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, int s0)
 {
     const int N = 1 << logN;
@@ -133,7 +149,7 @@ __device__ __forceinline__ void fwd_pass(u64* s, const ulonglong2* __restrict__ 
                 const ulonglong2 w = tw_load<TW_SMEM>(&tw[m + (blk << l) + (k >> (R - l))]);
                 u64 U = x[k];
                 U = U >= q2 ? U - q2 : U;
-                u64 V = shoup_lazy(x[k + half], w.x, w.y, q);
+                u64 V = shoup_lz<SF>(x[k + half], w.x, w.y, q);
                 x[k] = U + V;
                 x[k + half] = U - V + q2;
             }
@@ -143,7 +159,7 @@ __device__ __forceinline__ void fwd_pass(u64* s, const ulonglong2* __restrict__ 
     }
 }
 
-template <int R, bool TW_SMEM = false>
+template <int R, bool TW_SMEM = false, bool SF = false>
 __device__ __forceinline__ void inv_pass(u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, int s0)
 {
     const int N = 1 << logN;
@@ -168,7 +184,7 @@ __device__ __forceinline__ void inv_pass(u64* s, const ulonglong2* __restrict__ 
                 u64 U = x[k], V = x[k + half];
                 u64 a = U + V;
                 x[k] = a >= q2 ? a - q2 : a;
-                x[k + half] = shoup_lazy(U - V + q2, w.x, w.y, q);
+                x[k + half] = shoup_lz<SF>(U - V + q2, w.x, w.y, q);
             }
         }
 #pragma unroll
@@ -235,7 +251,7 @@ __device__ __forceinline__ void ntt_inv_smem(u64* s, const ulonglong2* tw, u64 q
 // the split is 1,3,3,3,3 (forward) and 3,3,3,3,1 (inverse).
 __host__ __device__ constexpr int edge_r(int logN) { return logN % 3 == 0 ? 3 : logN % 3; }
 
-template <int R, class Loader>
+template <int R, bool SF, class Loader>
 __device__ __forceinline__ void fwd_first_pass(Loader ld, u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN)
 {
     const int N = 1 << logN;
@@ -256,7 +272,7 @@ __device__ __forceinline__ void fwd_first_pass(Loader ld, u64* s, const ulonglon
                 const ulonglong2 w = __ldg(&tw[m + (k >> (R - l))]);
                 u64 U = x[k];
                 U = U >= q2 ? U - q2 : U;
-                u64 V = shoup_lazy(x[k + half], w.x, w.y, q);
+                u64 V = shoup_lz<SF>(x[k + half], w.x, w.y, q);
                 x[k] = U + V;
                 x[k + half] = U - V + q2;
             }
@@ -266,7 +282,7 @@ __device__ __forceinline__ void fwd_first_pass(Loader ld, u64* s, const ulonglon
     }
 }
 
-template <int R, class Storer>
+template <int R, bool SF, class Storer>
 __device__ __forceinline__ void inv_last_pass(const u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, Storer st)
 {
     const int N = 1 << logN;
@@ -288,7 +304,7 @@ __device__ __forceinline__ void inv_last_pass(const u64* s, const ulonglong2* __
                 u64 U = x[k], V = x[k + half];
                 u64 a = U + V;
                 x[k] = a >= q2 ? a - q2 : a;
-                x[k + half] = shoup_lazy(U - V + q2, w.x, w.y, q);
+                x[k + half] = shoup_lz<SF>(U - V + q2, w.x, w.y, q);
             }
         }
 #pragma unroll
@@ -297,33 +313,33 @@ __device__ __forceinline__ void inv_last_pass(const u64* s, const ulonglong2* __
 }
 
 // forward: ld(i) -> natural-order input in [0, 4q); result in s (bit-reversed, [0, 4q)); ends synced
-template <class Loader>
+template <bool SF = true, class Loader>
 __device__ __forceinline__ void ntt_fwd_g(Loader ld, u64* s, const ulonglong2* tw, u64 q, int logN)
 {
     const int r0 = edge_r(logN);
-    if (r0 == 1) fwd_first_pass<1>(ld, s, tw, q, logN);
-    else if (r0 == 2) fwd_first_pass<2>(ld, s, tw, q, logN);
-    else fwd_first_pass<3>(ld, s, tw, q, logN);
+    if (r0 == 1) fwd_first_pass<1, SF>(ld, s, tw, q, logN);
+    else if (r0 == 2) fwd_first_pass<2, SF>(ld, s, tw, q, logN);
+    else fwd_first_pass<3, SF>(ld, s, tw, q, logN);
     __syncthreads();
     for (int s0 = r0; s0 < logN; s0 += 3) {
-        fwd_pass<3>(s, tw, q, logN, s0);
+        fwd_pass<3, false, SF>(s, tw, q, logN, s0);
         __syncthreads();
     }
 }
 
 // inverse: s holds bit-reversed input in [0, 2q) (synced); st(i, v) receives the natural-order
 // output v in [0, 2q) *before* the N^-1 scaling
-template <class Storer>
+template <bool SF = true, class Storer>
 __device__ __forceinline__ void ntt_inv_g(u64* s, const ulonglong2* tw, u64 q, int logN, Storer st)
 {
     const int rl = edge_r(logN);
     for (int s0 = logN - 3; s0 >= rl; s0 -= 3) {
-        inv_pass<3>(s, tw, q, logN, s0);
+        inv_pass<3, false, SF>(s, tw, q, logN, s0);
         __syncthreads();
     }
-    if (rl == 1) inv_last_pass<1>(s, tw, q, logN, st);
-    else if (rl == 2) inv_last_pass<2>(s, tw, q, logN, st);
-    else inv_last_pass<3>(s, tw, q, logN, st);
+    if (rl == 1) inv_last_pass<1, SF>(s, tw, q, logN, st);
+    else if (rl == 2) inv_last_pass<2, SF>(s, tw, q, logN, st);
+    else inv_last_pass<3, SF>(s, tw, q, logN, st);
 }
 
 __host__ __device__ inline int ntt_threads(int N)

@@ -152,51 +152,65 @@ struct TermDesc {
 __device__ __forceinline__ u64 src_limb(const DevCtx& c, const TermDesc& t, int comp, int j, int k)
 {
     const long long o = ((long long)comp * c.L + j) * c.N + k;
-    u64 v = t.X[o];
-    if (t.pt) v = mont_mul(v, t.pt[(long long)j * c.N + k], c.mod[j]);
+    u64 v = __ldg(t.X + o);
+    if (t.pt) v = mont_mul(v, __ldg(t.pt + (long long)j * c.N + k), c.mod[j]);
     return v;
 }
 
-__global__ void __launch_bounds__(512, 2) k_digits_intt(DevCtx c, const TermDesc* __restrict__ terms)
+// sigma-permuted copies of the NTT-domain polynomial held in smem into block slot `slot`
+// of every rotation of the term
+__device__ __forceinline__ void write_perm(const DevCtx& c, const u64* sm, const TermDesc& t,
+                                           const unsigned* __restrict__ galois, long long blk_words, int slot)
+{
+    for (int r = 0; r < t.rot_cnt; r++) {
+        const unsigned g = galois[t.rot_off + r];
+        u64* o = t.blk + r * blk_words + (long long)slot * c.N;
+        for (int k = threadIdx.x; k < c.N; k += blockDim.x) st_cs(o + k, sm[pad(auto_src(k, g, c.logN))]);
+    }
+}
+
+// grid: terms * L CTAs.  Per (term, prime i): the sigma-copies of c0_i and of the c1_i limb
+// (the j == i digit needs no NTT), then INTT of c1_i -> digit coefficients.  (X (.) pt) is formed
+// here once (ScMult fused).
+__global__ void __launch_bounds__(512, 2) k_digits_intt(DevCtx c, const TermDesc* __restrict__ terms,
+                                                        const unsigned* __restrict__ galois, long long blk_words)
 {
     extern __shared__ u64 sm[];
-    const int L = c.L, N = c.N;
+    const int L = c.L, M = c.M, N = c.N;
     const int ti = blockIdx.x / L, i = blockIdx.x % L;
     const TermDesc t = terms[ti];
     const u64 q = c.mod[i].q;
+    if (t.blk) {
+        for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 0, i, k);
+        __syncthreads();
+        write_perm(c, sm, t, galois, blk_words, L * M + i);
+        __syncthreads();
+    }
     for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 1, i, k);
     __syncthreads();
+    if (t.blk) {
+        write_perm(c, sm, t, galois, blk_words, i * M + i);
+        __syncthreads();
+    }
     u64* d = t.dig + (long long)i * N;
     const u64 ni = c.ninv[i], nsh = c.ninv_sh[i];
     ntt_inv_g(sm, c.twi[i], q, c.logN, [=](int k, u64 v) { st_cs(d + k, shoup(v, ni, nsh, q)); });
 }
 
-// grid: terms * (L*M + L) CTAs
+// grid: terms * L * L CTAs: NTT of digit i into every prime j != i, then the sigma-permuted writes
 __global__ void __launch_bounds__(512, 2) k_digits_perm(DevCtx c, const TermDesc* __restrict__ terms,
                                                          const unsigned* __restrict__ galois, long long blk_words)
 {
     extern __shared__ u64 sm[];
     const int L = c.L, M = c.M, N = c.N;
-    const int per = L * M + L;
-    const int ti = blockIdx.x / per, slot = blockIdx.x % per;
+    const int per = L * L;
+    const int ti = blockIdx.x / per, s = blockIdx.x % per;
+    const int i = s / L, jj = s % L, j = jj < i ? jj : jj + 1;
     const TermDesc t = terms[ti];
-    int j;
-    if (slot < L * M) {
-        const int i = slot / M;
-        j = slot % M;
-        const u64 q = c.mod[j].q;
-        if (i != j) {
-            const u64* d = t.dig + (long long)i * N;   // d < q_i < 4 q_j: lazy NTT input
-            ntt_fwd_g([=](int k) { return ld_cs(d + k); }, sm, c.twf[j], q, c.logN);
-        } else {
-            for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 1, j, k);
-        }
-    } else {
-        j = slot - L * M;
-        for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 0, j, k);
-    }
-    __syncthreads();
-    const u64 q = c.mod[j].q;   // NTT outputs are in [0, 4q): fold on the permuted read
+    const u64 q = c.mod[j].q;
+    const u64* d = t.dig + (long long)i * N;   // d < q_i < 4 q_j: lazy NTT input
+    ntt_fwd_g([=](int k) { return ld_cs(d + k); }, sm, c.twf[j], q, c.logN);
+    const int slot = i * M + j;               // NTT outputs are in [0, 4q): fold on the permuted read
     for (int r = 0; r < t.rot_cnt; r++) {
         const unsigned g = galois[t.rot_off + r];
         u64* o = t.blk + r * blk_words + (long long)slot * N;

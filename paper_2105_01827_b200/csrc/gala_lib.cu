@@ -332,8 +332,9 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     const int nt = ntt_threads(N);
     if (!td.empty()) {
         KLAUNCH(c, "k_digits_intt", k_digits_intt<<<(unsigned)(td.size() * L), nt, c->smem_ntt, c->stream>>>(
-                                        c->dc, (const TermDesc*)(d_blob + o_td)));
-        KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(td.size() * (L * M + L)), nt, c->smem_ntt,
+                                        c->dc, (const TermDesc*)(d_blob + o_td), (const unsigned*)(d_blob + o_gal),
+                                        blk_words));
+        KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(td.size() * L * L), nt, c->smem_ntt,
                                                     c->stream>>>(c->dc, (const TermDesc*)(d_blob + o_td),
                                                                  (const unsigned*)(d_blob + o_gal), blk_words));
     }
@@ -467,6 +468,8 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     for (int j = 0; j < M; j++) {
         if (primes[j] >= (1ull << 62)) return set_err(GALA_ERR_PARAM, "prime %d exceeds 2^62", j);
         if ((primes[j] - 1) % (2ull * N)) return set_err(GALA_ERR_PARAM, "prime %d not 1 mod 2N", j);
+        if ((primes[j] & 0xffffffffull) != 1)
+            return set_err(GALA_ERR_PARAM, "prime %d is not of the special form a*2^32 + 1 required by the NTT", j);
     }
     for (int i = 0; i < M; i++)
         for (int j = 0; j < M; j++) {
@@ -784,10 +787,11 @@ int gala_decompose(gala_ctx* c, const uint64_t* ct, uint64_t* digits)
     char* d_blob;
     RET(upload(c, &b, sizeof(b), (void**)&d_blob));
     const int nt = ntt_threads(N);
-    KLAUNCH(c, "k_digits_intt", k_digits_intt<<<L, nt, c->smem_ntt, c->stream>>>(c->dc, (const TermDesc*)d_blob));
-    KLAUNCH(c, "k_digits_perm", k_digits_perm<<<L * M + L, nt, c->smem_ntt, c->stream>>>(
-                                    c->dc, (const TermDesc*)d_blob, (const unsigned*)(d_blob + offsetof(decltype(b), g)),
-                                    (long long)(L * M + L) * N));
+    const unsigned* dg = (const unsigned*)(d_blob + offsetof(decltype(b), g));
+    const long long bw = (long long)(L * M + L) * N;
+    KLAUNCH(c, "k_digits_intt", k_digits_intt<<<L, nt, c->smem_ntt, c->stream>>>(c->dc, (const TermDesc*)d_blob, dg, bw));
+    KLAUNCH(c, "k_digits_perm", k_digits_perm<<<L * L, nt, c->smem_ntt, c->stream>>>(c->dc, (const TermDesc*)d_blob,
+                                                                                     dg, bw));
     release(c, dig);
     release(c, d_blob);
     return GALA_OK;

@@ -12,14 +12,17 @@ CPU oracle (``oracle/``) are always built on the same numbers:
   independently under the Galois element ``3^k mod 2N``.
 * ``p`` must satisfy ``p = 1 (mod 2N)`` (batching).  The reference default
   1048573 does not; 1032193 = 2^14 * 63 + 1 does for every N <= 8192.
+* every ciphertext and special prime has the *special form* ``q = a 2^32 + 1``
+  (so ``q = 1 (mod 2N)`` for every N <= 8192): the CUDA NTT's Shoup reduction
+  then needs one 32-bit multiply for ``hi * q`` instead of a 64x64 product.
 * ``rns_limbs == 1`` (default for N <= 4096): one ciphertext prime
-  ``q < 2^62`` with ``q = 1 (mod 2N p)`` so the BFV plaintext-product
+  ``q < 2^62`` with ``q = 1 (mod 2^32 p)`` so the BFV plaintext-product
   rounding term ``(q mod p) * k`` collapses to ``k``.
-* ``rns_limbs == 3`` (default for N >= 8192): the three largest primes below
-  2^60 that are ``1 (mod 2N)``.
+* ``rns_limbs == 3`` (default for N >= 8192): the three largest special-form
+  primes below 2^60.
 * one special prime ``P`` (hybrid key switching, one digit per ciphertext
-  prime): the largest prime ``= 1 (mod 2N)`` below 2^62 (L = 1) or the next
-  prime below the ciphertext primes (L = 3).
+  prime): the largest special-form prime below 2^62 (L = 1) or the next one
+  below the ciphertext primes (L = 3).
 
 Roots: for every modulus m the primitive 2N-th root is ``g^((m-1)/2N)`` with
 ``g`` the smallest quadratic non-residue mod m.  The plaintext root pins the
@@ -135,12 +138,13 @@ def derive(n: int, p: int, rns_limbs: int | None = None) -> BFVParams:
     if (p - 1) % (2 * N):
         raise ValueError(f"p = {p} is not 1 mod 2N = {2 * N}: slot batching impossible")
     L = rns_limbs or default_limbs(N)
+    SF = 1 << 32      # special form q = a 2^32 + 1 (also 1 mod 2N since 2N <= 2^14)
     if L == 1:
-        primes = tuple(_primes_below(62, 2 * N * p, 1))
-        special = _primes_below(62, 2 * N, 1, exclude=primes)[0]
+        primes = tuple(_primes_below(62, SF * p, 1))
+        special = _primes_below(62, SF, 1, exclude=primes)[0]
     elif L in (2, 3, 4):
-        primes = tuple(_primes_below(60, 2 * N, L))
-        special = _primes_below(60, 2 * N, 1, exclude=primes)[0]
+        primes = tuple(_primes_below(60, SF, L))
+        special = _primes_below(60, SF, 1, exclude=primes)[0]
     else:
         raise ValueError("rns_limbs must be 1..4")
     psis = tuple(primitive_root_2n(m, 2 * N) for m in primes + (special,))
