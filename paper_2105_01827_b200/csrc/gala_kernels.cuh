@@ -374,37 +374,52 @@ __global__ void k_sub_plain(DevCtx c, const u64* __restrict__ ct, const u64* __r
     }
 }
 
-// conv first-Add: acc[o][d][comp][j][k] = sum_ib sum_tap R[ib][tap][comp][j][k] * pt[o][ib][d][tap][j][k]
-// grid: (N/blockDim, L, n_obp * c_n)
-__global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __restrict__ R, int n_ib, int k,
-                                                       const u64* __restrict__ pts, int c_n, u64* __restrict__ acc)
+// conv first-Add over one chunk of input blocks [ib0, ib1):
+//   acc[o][d][comp][j][x] (+)= sum_{ib in chunk} sum_tap R[ib][tap][comp][j][x] * pt[o][ib][d][tap][j][x]
+// The host sizes chunks so R[ib0:ib1] stays resident in L2 while every (o, d) re-reads it; plaintexts
+// stream once from HBM with evict-first loads.  128-bit lazy accumulation, REDC every c.lazy[j]
+// products.  grid: (N / blockDim, L, n_obp * c_n)
+__global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __restrict__ R, int n_ib, int ib0,
+                                                       int ib1, int k, const u64* __restrict__ pts, int c_n,
+                                                       int accumulate, u64* __restrict__ acc)
 {
     const int N = c.N, L = c.L;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     const int j = blockIdx.y, od = blockIdx.z;
-    const int o = od / c_n, d = od % c_n;
+    const int o = od / c_n, d = od - o * c_n;
     if (x >= N) return;
     const ModC md = c.mod[j];
     const u64 q = md.q;
+    const int lazy = c.lazy[j];
     const long long LN = (long long)L * N, W = 2 * LN;
     u64 s0 = 0, s1 = 0;
-    for (int ib = 0; ib < n_ib; ib++) {
+    Acc128 a0, a1;
+    int pending = 0;
+    for (int ib = ib0; ib < ib1; ib++) {
         const u64* pt = pts + ((((long long)o * n_ib + ib) * c_n + d) * k) * LN + (long long)j * N + x;
         const u64* Rb = R + ((long long)ib * k) * W + (long long)j * N + x;
-        Acc128 a0, a1;
         for (int t = 0; t < k; t++) {
-            const u64 w = __ldg(pt + t * LN);
-            a0.mac(Rb[t * W], w);
-            a1.mac(Rb[t * W + LN], w);
-            if ((t & 3) == 3 || t == k - 1) { // four products < 4 q^2 < q 2^64 (q < 2^62)
+            const u64 w = __ldcs((const unsigned long long*)(pt + t * LN));
+            const u64 r0 = __ldg(Rb + t * W), r1 = __ldg(Rb + t * W + LN);
+            if (pending == lazy) {
                 s0 = add_mod(s0, a0.reduce(md), q);
                 s1 = add_mod(s1, a1.reduce(md), q);
                 a0 = Acc128();
                 a1 = Acc128();
+                pending = 0;
             }
+            a0.mac(r0, w);
+            a1.mac(r1, w);
+            pending++;
         }
     }
+    s0 = add_mod(s0, a0.reduce(md), q);
+    s1 = add_mod(s1, a1.reduce(md), q);
     u64* out = acc + (long long)od * W + (long long)j * N + x;
+    if (accumulate) {
+        s0 = add_mod(s0, out[0], q);
+        s1 = add_mod(s1, out[LN], q);
+    }
     out[0] = s0;
     out[LN] = s1;
 }

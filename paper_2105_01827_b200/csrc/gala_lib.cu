@@ -957,7 +957,15 @@ int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts
     RET(scratch(c, &acc, (size_t)n_obp * c_n * W));
     const int th = N < 256 ? N : 256;
     dim3 grid((N + th - 1) / th, L, n_obp * c_n);
-    KLAUNCH(c, "k_kg_accumulate", k_kg_accumulate<<<grid, th, 0, c->stream>>>(c->dc, R, n_ib, k, pts, c_n, acc));
+    // input-block chunks whose rotated inputs (k * W words each) fit comfortably in L2 (~48 MB)
+    const long long chunk_bytes = 48ll << 20;
+    int per_chunk = (int)(chunk_bytes / ((long long)k * W * 8));
+    if (per_chunk < 1) per_chunk = 1;
+    for (int ib0 = 0; ib0 < n_ib; ib0 += per_chunk) {
+        const int ib1 = ib0 + per_chunk < n_ib ? ib0 + per_chunk : n_ib;
+        KLAUNCH(c, "k_kg_accumulate", k_kg_accumulate<<<grid, th, 0, c->stream>>>(c->dc, R, n_ib, ib0, ib1, k, pts,
+                                                                                  c_n, ib0 > 0, acc));
+    }
     release(c, R);
     // second-Perm: out[o] = sum_d rot_{d * band}(acc[o][d]), one lazy ModDown per o
     RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, n_obp, c_n, band_step, outs, 0));

@@ -1,0 +1,113 @@
+#!/usr/bin/env python
+"""Side benchmark of every BASELINE config's fused layer on one GPU (not the driver's bench line).
+
+cfg1: GALA FC 16x2048, N=4096 L=1          cfg2: GALA FC 1024x4096, N=8192 L=3
+cfg3: KG conv 16x16x64->64 3x3, N=4096 L=1  cfg4: KG conv 56x56x64->64 3x3 (64x64 frame), N=8192 L=3
+Prints one JSON object per config: ms per layer (CUDA events, L2 flushed between reps), layers/s,
+kernel breakdown, algorithmic modmuls, and a decrypted-result check against the plaintext truth.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from oracle.plain import conv2d_mod_p, dot_mod_p  # noqa: E402
+from paper_2105_01827_b200 import ConvTask, CostMeter, GalaFC, HEParams, KernelGroupingConv  # noqa: E402
+from paper_2105_01827_b200.conv import encrypt_inputs, unpack_channels  # noqa: E402
+from paper_2105_01827_b200.backend import decrypt  # noqa: E402
+
+P = 1032193
+dev = torch.device("cuda", 0)
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
+
+
+def timeit(fn, reps=5):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def fc(name, n, L, n_out, n_in, B):
+    params = HEParams(n=n, rns_limbs=L, seed=31)
+    rng = np.random.default_rng(1)
+    w = rng.integers(-128, 128, (n_out, n_in)) % P
+    layer = GalaFC(w, params)
+    ctx = layer.ctx
+    xs = [rng.integers(0, P, n_in) for _ in range(B)]
+    cts = torch.stack([layer.encrypt_input(x)[0] for x in xs])
+    masks = [layer.draw_masks(100 + b) for b in range(B)]
+    d_r = ctx.to_device_u32(np.stack([ctx.physical(m[0][0].slots, m[0][1].slots if layer.paired else None)
+                                      for m in masks]))
+    pts = layer.blocks[0][1]
+    outs, masked = ctx.empty_ct(B), ctx.empty_ct(B)
+    run = lambda: ctx.mv_gala_batch(cts, pts, layer.T, d_r, layer.baby, outs=outs, masked=masked)  # noqa: E731
+    ms = timeit(run)
+    ctx.profile(True)
+    run()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ok = all(np.array_equal((layer.client_shares([masked[b]]) + layer.server_shares(masks[b])) % P,
+                            dot_mod_p(w, xs[b], P)) for b in range(min(B, 2)))
+    return {"config": name, "N": ctx.N, "L": ctx.L, "T": layer.T, "batch": B, "ms_per_layer": ms / B,
+            "layers_per_s": 1e3 * B / ms, "correct": ok,
+            "breakdown_ms_per_layer": {k: round(v["ms"] / B, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+
+
+def conv(name, n, L, u, frame, c_i, c_o, k):
+    params = HEParams(n=n, rns_limbs=L, seed=32)
+    rng = np.random.default_rng(2)
+    kern = rng.integers(-128, 128, (c_o, c_i, k, k)) % P
+    ch = rng.integers(0, P, (c_i, u, u))
+    img = np.zeros((c_i, frame, frame), dtype=np.int64)
+    img[:, :u, :u] = ch
+    task = ConvTask(frame, frame, c_i, k, k, c_o, kern, params)
+    t0 = time.perf_counter()
+    layer = KernelGroupingConv(task)
+    setup = time.perf_counter() - t0
+    ctx = layer.ctx
+    cts = encrypt_inputs(task, img)
+    stacked = torch.stack([c.data for c in cts])
+    run = lambda: layer.forward_device(stacked)  # noqa: E731
+    ms = timeit(run, reps=3)
+    ctx.profile(True)
+    run()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    meter = CostMeter()
+    outs = layer(cts, meter)
+    got = np.concatenate([unpack_channels(decrypt(o), task) for o in outs])[:, :u, :u]
+    ok = bool(np.array_equal(got, conv2d_mod_p(ch, kern, P)))
+    return {"config": name, "N": ctx.N, "L": ctx.L, "c_n": layer.c_n, "n_ib": layer.n_ib, "n_obp": layer.n_obp,
+            "ms_per_layer": ms, "layers_per_s": 1e3 / ms, "correct": ok, "weight_encode_s": round(setup, 2),
+            "plaintext_bytes": int(layer.pts.numel() * 8), "meter": repr(meter),
+            "breakdown_ms": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4"]
+    for w in which:
+        if w == "cfg1":
+            r = fc("cfg1", 2048, 1, 16, 2048, 64)
+        elif w == "cfg2":
+            r = fc("cfg2", 4096, 3, 1024, 4096, 8)
+        elif w == "cfg3":
+            r = conv("cfg3", 2048, 1, 16, 16, 64, 64, 3)
+        elif w == "cfg4":
+            r = conv("cfg4", 4096, 3, 56, 64, 64, 64, 3)
+        print(json.dumps(r), flush=True)
