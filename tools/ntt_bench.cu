@@ -166,10 +166,82 @@ __global__ void __launch_bounds__(THREADS, MINB) v_plan(const u64* in, u64* out,
     for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
 }
 
+// K: special-form prime + reduced lazy reductions for q < 2^60 (16q < 2^64): the U fold to [0,2q)
+// happens only at the first stage of each radix-8 pass; bounds grow by 2q per stage within the pass.
+template <int R, bool SF>
+__device__ __forceinline__ void fwd_pass_k(u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, int s0)
+{
+    const int N = 1 << logN;
+    const int G = N >> R;
+    const int lt = logN - s0 - R;
+    const int t_end = 1 << lt;
+    const u64 q2 = 2 * q, q4 = 4 * q, q8 = 8 * q;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const int blk = g >> lt, off = g & (t_end - 1);
+        const int base = (blk << (logN - s0)) + off;
+        u64 x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) {
+            u64 v = s[pad(base + (k << lt))];     // input < 8q: fold to [0, 2q)
+            v = v >= q4 ? v - q4 : v;
+            x[k] = v >= q2 ? v - q2 : v;
+        }
+#pragma unroll
+        for (int l = 0; l < R; l++) {
+            const int m = 1 << (s0 + l);
+            const int half = 1 << (R - 1 - l);
+#pragma unroll
+            for (int k = 0; k < (1 << R); k++) {
+                if (k & half) continue;
+                const ulonglong2 w = __ldg(&tw[m + (blk << l) + (k >> (R - l))]);
+                u64 U = x[k];
+                u64 V = shoup_lz<SF>(x[k + half], w.x, w.y, q);
+                x[k] = U + V;
+                x[k + half] = U - V + q2;   // bounds: [0, (2 + 2(l+1)) q)
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) s[pad(base + (k << lt))] = x[k];   // < 8q
+    }
+    (void)q8;
+}
+
+template <bool SF>
+__global__ void __launch_bounds__(512, 2) v_k(const u64* in, u64* out, const ulonglong2* tw, u64 q, int logN)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    const u64* src = in + (long long)blockIdx.x * N;
+    fwd_first_pass<1, SF>([=](int i) { return src[i]; }, sm, tw, q, logN);
+    __syncthreads();
+    for (int s0 = 1; s0 < logN; s0 += 3) {
+        fwd_pass_k<3, SF>(sm, tw, q, logN, s0);
+        __syncthreads();
+    }
+    u64* dst = out + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        u64 v = sm[pad(i)];
+        v = v >= 4 * q ? v - 4 * q : v;
+        v = v >= 2 * q ? v - 2 * q : v;
+        dst[i] = v >= q ? v - q : v;
+    }
+}
+
+template <bool SF>
+__global__ void __launch_bounds__(512, 2) v_g(const u64* in, u64* out, const ulonglong2* tw, u64 q, int logN)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    const u64* src = in + (long long)blockIdx.x * N;
+    ntt_fwd_g<SF>([=](int i) { return src[i]; }, sm, tw, q, logN);
+    u64* dst = out + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
+}
+
 int main()
 {
     const int logN = 13, N = 1 << logN;
-    const u64 q = 1152921504606830593ull; // 60-bit, 1 mod 2^14
+    const u64 q = 1152921092289986561ull; // 60-bit special form a*2^32+1
     // primitive 2N-th root: g^((q-1)/2N), g least non-residue
     u64 g = 2;
     while (h_pow(g, (q - 1) / 2, q) == 1) g++;
@@ -243,6 +315,14 @@ int main()
     PLAN("J 4,4,4,1 T512x2 gl", 4, 4, 4, 1, 0, 512, 2)
     PLAN("J 3,3,3,3,1 T256x3 gl", 3, 3, 3, 3, 1, 256, 3)
     PLAN("J 3,3,3,3,1 T1024x1 gl", 3, 3, 3, 3, 1, 1024, 1)
+    CKE(cudaFuncSetAttribute(v_g<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("G prod plan generic", [&] { v_g<false><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    CKE(cudaFuncSetAttribute(v_g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("G prod plan SF", [&] { v_g<true><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    CKE(cudaFuncSetAttribute(v_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("K SF + pass-level folds", [&] { v_k<true><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    CKE(cudaFuncSetAttribute(v_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("K generic + pass-level folds", [&] { v_k<false><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
     const int smemI = 2 * smem;
     CKE(cudaFuncSetAttribute(v_pipe<3, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemI));
     run("I pipe R3 T1024", [&] { v_pipe<3, 1024><<<148, 1024, smemI>>>(din, dout, dtw, q, logN, P); }, false);
