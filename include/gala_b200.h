@@ -111,6 +111,13 @@ int gala_mv_gala_batch_host(gala_ctx *ctx, const uint64_t *cts_host, int B, cons
 int gala_conv_kg(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *pts_dev, int n_obp,
                  int c_n, int k, const int *tap_steps_host, int band_step, uint64_t *outs_dev);
 
+/* On-GPU kernel-grouping weight encoding (coef_vectors, conv.py:220-235, in the physical
+ * two-row form): kernels_dev int32 [c_o][c_i][k_h][k_w] (values mod p) -> pts_dev
+ * [n_obp][n_ib][c_n][k_h k_w][L][N] ready for gala_conv_kg.  pair = 2 puts output blocks
+ * 2o and 2o+1 on hypercube rows 0 and 1; pair = 1 replicates. */
+int gala_kg_encode_weights(gala_ctx *ctx, const int32_t *kernels_dev, int c_o, int c_i, int k_h, int k_w, int u_w,
+                           int u_h, int pair, uint64_t *pts_dev);
+
 /* canonical word import/export of `count` ciphertexts */
 int gala_ct_export(gala_ctx *ctx, const uint64_t *ct_dev, uint64_t *coef_dev, int count);
 int gala_ct_import(gala_ctx *ctx, const uint64_t *coef_dev, uint64_t *ct_dev, int count);

@@ -425,6 +425,48 @@ __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __re
 }
 
 // ---------------------------------------------------------------------------
+// On-GPU kernel-grouping plaintext slots (conv.py:220-235 coef_vectors, physical two-row form):
+// for plaintext (obp, ib, d, tap) and physical slot s = row * n + ch * B + y * u_w + x:
+//   ob = obp * pair + row;  value = kernels[ob c_n + (ch - d) mod c_n][ib c_n + ch][dh + kh/2][dw + kw/2]
+//   when (x + dw, y + dh) is inside the image and ob < n_ob, else 0.
+// `first` is the flat index of the first plaintext generated; out [count][N] u32.
+struct KgGeom {
+    int c_o, c_i, k_h, k_w, u_w, u_h, c_n, n_ib, n_ob, pair;
+};
+__global__ void k_kg_slots(DevCtx c, const int32_t* __restrict__ kern, KgGeom g, long long first, int count,
+                           uint32_t* __restrict__ out)
+{
+    const int N = c.N, n = N / 2;
+    const int B = g.u_w * g.u_h, k = g.k_h * g.k_w;
+    const long long total = (long long)count * N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long pidx = first + e / N;
+        const int s = (int)(e % N);
+        int tap = (int)(pidx % k);
+        long long rest = pidx / k;
+        const int d = (int)(rest % g.c_n);
+        rest /= g.c_n;
+        const int ib = (int)(rest % g.n_ib);
+        const int obp = (int)(rest / g.n_ib);
+        const int row = s / n, cs = s % n;
+        const int ob = g.pair == 2 ? obp * 2 + row : obp;
+        uint32_t v = 0;
+        const int ch = cs / B, pos = cs % B;
+        if (ob < g.n_ob && ch < g.c_n) {
+            const int y = pos / g.u_w, x = pos % g.u_w;
+            const int dh = tap / g.k_w - g.k_h / 2, dw = tap % g.k_w - g.k_w / 2;
+            if (x + dw >= 0 && x + dw < g.u_w && y + dh >= 0 && y + dh < g.u_h) {
+                const int o = ob * g.c_n + ((ch - d) % g.c_n + g.c_n) % g.c_n;
+                const int i = ib * g.c_n + ch;
+                v = (uint32_t)kern[(((long long)o * g.c_i + i) * g.k_h + (dh + g.k_h / 2)) * g.k_w + (dw + g.k_w / 2)];
+            }
+        }
+        out[e] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // encoding.  MODE 0: plaintext operand (centred lift, Montgomery);
 //            MODE 1: Delta * m (plain), for encrypt / subtract_plain
 // one CTA per (vector b, prime j); each CTA recomputes the mod-p INTT (cheap,

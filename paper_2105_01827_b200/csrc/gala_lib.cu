@@ -973,6 +973,40 @@ int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts
     return GALA_OK;
 }
 
+int gala_kg_encode_weights(gala_ctx* c, const int32_t* kern, int c_o, int c_i, int k_h, int k_w, int u_w, int u_h,
+                           int pair, uint64_t* pts)
+{
+    const int N = c->dc.N, L = c->dc.L, n = N / 2;
+    const int B = u_w * u_h;
+    if (B <= 0 || n % B || (k_h % 2) == 0 || (k_w % 2) == 0 || (pair != 1 && pair != 2))
+        return set_err(GALA_ERR_PARAM, "bad kernel-grouping geometry");
+    KgGeom g;
+    g.c_o = c_o;
+    g.c_i = c_i;
+    g.k_h = k_h;
+    g.k_w = k_w;
+    g.u_w = u_w;
+    g.u_h = u_h;
+    g.c_n = n / B;
+    if (c_i % g.c_n || c_o % g.c_n) return set_err(GALA_ERR_PARAM, "channels must be multiples of c_n=%d", g.c_n);
+    g.n_ib = c_i / g.c_n;
+    g.n_ob = c_o / g.c_n;
+    g.pair = pair;
+    const int n_obp = (g.n_ob + pair - 1) / pair;
+    const long long total = (long long)n_obp * g.n_ib * g.c_n * k_h * k_w;
+    const int chunk = 4096;   // plaintexts per generate+encode round (32 MB of slots at N = 8192)
+    uint32_t* slots;
+    RET(scratch(c, &slots, (size_t)chunk * N));
+    for (long long first = 0; first < total; first += chunk) {
+        const int cnt = (int)(total - first < chunk ? total - first : chunk);
+        KLAUNCH(c, "k_kg_slots", k_kg_slots<<<grid_for((long long)cnt * N, 256), 256, 0, c->stream>>>(c->dc, kern, g, first,
+                                                                                                  cnt, slots));
+        RET(gala_encode_plain(c, slots, cnt, pts + first * L * N));
+    }
+    release(c, slots);
+    return GALA_OK;
+}
+
 int gala_ct_export(gala_ctx* c, const uint64_t* ct, uint64_t* coef, int count)
 {
     const int N = c->dc.N, L = c->dc.L;

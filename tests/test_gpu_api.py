@@ -326,3 +326,41 @@ def test_cfg4_conv_56x56x64_in_64x64_frame_n8192():
     got = np.concatenate([unpack_channels(decrypt(o), task) for o in outs])[:, :56, :56]
     assert np.array_equal(got, conv2d_mod_p(ch, kern, P))
     assert OpCounts.from_meter(meter) == OpCounts(perm=0, dec_perm=64, hst_perm=512, sc_mult=36864, add=36800)
+
+
+@pytest.mark.parametrize("u,c_i,k,c_o,n", [(4, 8, 3, 16, 64), (16, 64, 3, 64, 2048), (8, 4, 5, 4, 64), (2, 4, 3, 4, 16)])
+def test_gpu_weight_encoding_equals_host_encoding(u, c_i, k, c_o, n):
+    """On-GPU coef_vectors + encode == the reference-order host construction, word for word."""
+    params = with_overrides(BASE, n=n)
+    rng = np.random.default_rng(u + c_i)
+    task = ConvTask(u, u, c_i, k, k, c_o, rng.integers(0, P, (c_o, c_i, k, k)), params)
+    for pair in (True, False):
+        a = KernelGroupingConv(task, pair_rows=pair)
+        b = KernelGroupingConv(task, pair_rows=pair, host_encode=True)
+        assert bool((a.pts == b.pts).all())
+
+
+# --- config 5 building blocks: frames, halo tiling, strides, padded FC -----------------
+def test_resnet_rules_small():
+    from paper_2105_01827_b200.resnet import ConvLayer, FCLayer, LayerSpec
+
+    params = HEParams(n=1024, seed=25)           # frames up to 32x32
+    rng = np.random.default_rng(5)
+    cases = [LayerSpec("tiled7x7s2", "conv", 3, 4, 7, 2, 70),      # 70 > 32: halo tiles, stride 2
+             LayerSpec("s2", "conv", 4, 8, 3, 2, 14),              # 14 -> 16 frame, stride 2
+             LayerSpec("ds1x1s2", "conv", 4, 8, 1, 2, 28),         # 1x1 downsample
+             LayerSpec("s1", "conv", 16, 16, 3, 1, 7)]             # 7 -> 8 frame, c_n = 16
+    for spec in cases:
+        w = rng.integers(-128, 128, (spec.c_out, spec.c_in, spec.k, spec.k)) % P
+        x = rng.integers(0, P, (spec.c_in, spec.size, spec.size))
+        layer = ConvLayer(spec, w, params)
+        got = layer.decrypt_output(layer.forward_device(layer.encrypt_frames(x)))
+        want = conv2d_mod_p(x, w, P)[:, ::spec.stride, ::spec.stride]
+        assert got.shape == (spec.c_out, spec.out_size, spec.out_size)
+        assert np.array_equal(got, want), spec.name
+    spec = LayerSpec("fc", "fc", 24, 40)
+    w = rng.integers(-128, 128, (40, 24)) % P
+    x = rng.integers(0, P, 24)
+    fc = FCLayer(spec, w, params)
+    masks = fc.layer.draw_masks(3)
+    assert np.array_equal(fc.shares(fc.forward_device(fc.encrypt_frames(x), masks), masks), dot_mod_p(w, x, P))

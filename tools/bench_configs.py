@@ -17,7 +17,8 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-from oracle.plain import conv2d_mod_p, dot_mod_p  # noqa: E402
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from plain_check import conv2d_mod_p, dot_mod_p  # noqa: E402
 from paper_2105_01827_b200 import ConvTask, CostMeter, GalaFC, HEParams, KernelGroupingConv  # noqa: E402
 from paper_2105_01827_b200.conv import encrypt_inputs, unpack_channels  # noqa: E402
 from paper_2105_01827_b200.backend import decrypt  # noqa: E402
