@@ -117,7 +117,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def modmul_model(N, L, T, baby):
+def modmul_model(N, L, T, baby, schedule):
     from paper_2105_01827_b200.analytics import ks_modmuls, ntt_modmuls, physical_mv_counts
 
     G = T // baby
@@ -125,6 +125,17 @@ def modmul_model(N, L, T, baby):
     M = L + 1
     rot_items = G * (baby - 1) + (G - 1)
     groups = G + (1 if G > 1 else 0)
+    if schedule == 2:
+        giant = G - 1
+        per_kernel = {
+            "k_gala_mac": G * (baby - 1) * (M * N * 3 * L + L * N) + G * 2 * L * N,
+            "k_digits_intt": (1 + giant) * L * h,
+            "k_digits_perm": (1 + giant) * L * L * h,
+            "k_ks_mac": giant * 2 * L * M * N,
+            "k_ntt_inv[moddown]": groups * 2 * h,
+            "k_moddown": groups * (2 * L * h + 2 * L * N),
+        }
+        return per_kernel, physical_mv_counts(N, L, T, baby, 2)["modmuls"]
     per_kernel = {
         "k_ct_mul_pts": 2 * L * N * T,
         "k_digits_intt": rot_items * L * h + 2 * L * N * rot_items,
@@ -133,7 +144,7 @@ def modmul_model(N, L, T, baby):
         "k_ntt_inv[moddown]": groups * 2 * h,
         "k_moddown": groups * (2 * L * h + 2 * L * N),
     }
-    total = physical_mv_counts(N, L, T, baby)["modmuls"]
+    total = physical_mv_counts(N, L, T, baby, 1)["modmuls"]
     return per_kernel, total
 
 
@@ -173,7 +184,7 @@ def run_ours(args):
 
     def step():
         # one batched library call: all B layers share every launch
-        ctx.mv_gala_batch(cts_b, pts, T, d_r, baby, outs=outs, masked=masked)
+        layer.run_batch(cts_b, pts, d_r, outs=outs, masked=masked)
 
     # correctness gate before timing: decrypted shares == W x mod p
     w = weights()
@@ -234,7 +245,8 @@ def run_ours(args):
 
     def e2e_step():
         # one C-ABI call per step: H2D of B canonical ciphertexts + masks, fused layers, D2H of masked words
-        _lib.check(ctx.lib.gala_mv_gala_batch_host(h, ctypes.c_void_p(host_ct.data_ptr()), B,
+        host_fn = ctx.lib.gala_mv_gala2_batch_host if layer.schedule == 2 else ctx.lib.gala_mv_gala_batch_host
+        _lib.check(host_fn(h, ctypes.c_void_p(host_ct.data_ptr()), B,
                                                    ctypes.c_void_p(pts.data_ptr()), T, baby,
                                                    ctypes.c_void_p(host_r.data_ptr()),
                                                    ctypes.c_void_p(host_out.data_ptr())))
@@ -265,7 +277,7 @@ def run_ours(args):
 
     # roofline: integer-multiply bound (modmul count) -- peak measured live with the library's own modmul
     peak_modmul = ctx.bench_modmul()
-    per_kernel, layer_modmuls = modmul_model(N, L, T, baby)
+    per_kernel, layer_modmuls = modmul_model(N, L, T, baby, layer.schedule)
     dominant = max(prof.items(), key=lambda kv: kv[1]["ms"])
     dom_name, dom = dominant
     step_ms_prof = sum(v["ms"] for v in prof.values())
@@ -299,6 +311,7 @@ def run_ours(args):
         "dtype": "u64 (RNS residues mod 60-bit primes)",
         "data": "synthetic (seeded int8 weights mapped to Z_p, uniform Z_p inputs)",
         "config": {"workload": WORKLOAD, "layer": "GALA FC 1024x4096 (2 paired MvTasks of 512x4096, T=512)",
+                   "gala_schedule": layer.schedule,
                    "N": N, "L": L, "special_primes": 1, "p": P, "bsgs_baby": baby, "batch_per_gpu": B,
                    "parallelism": f"replicas x{world} (independent inputs per GPU)",
                    "l2": "flushed (256 MB write) before every timed step"},
@@ -322,7 +335,7 @@ def run_ours(args):
         "kernel_breakdown_ms_per_step": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
         "e2e": {"value": round(e2e_value, 3), "unit": "layers/s",
                 "h2d_bytes_per_step": B * (ct_bytes + N * 4), "d2h_bytes_per_step": B * ct_bytes,
-                "path": "gala_mv_gala_batch_host (C-ABI, pinned host buffers, canonical words, one call per step)"},
+                "path": f"gala_mv_gala{layer.schedule if layer.schedule == 2 else ''}_batch_host (C-ABI, pinned host buffers, canonical words, one call per step)"},
         "gpu_launches": int(launches),
         "setup_s": round(setup_s, 2),
         "clocks": clk.summary(),
@@ -361,7 +374,7 @@ def cpu_baseline(ctx, layer, ct, phys_r, masked_gpu):
     pts = np.concatenate([gala_weight_slots(tasks[0]), gala_weight_slots(tasks[1])], axis=1).astype(np.uint32)
     words = ctx.export_words(ct)
     t0 = time.perf_counter()
-    _, m = o.mv_gala(words, pts, phys_r, baby=layer.baby)
+    _, m = o.mv_gala(words, pts, phys_r, baby=layer.baby, schedule=layer.schedule)
     dt = time.perf_counter() - t0
     match = bool(np.array_equal(m, ctx.export_words(masked_gpu)))
     return {"value": round(1.0 / dt, 4), "unit": "layers/s", "cores": num_threads(), "kind": "port",
@@ -402,12 +415,13 @@ def run_reference(args):
     a, e = sampling.encryption_randomness(np.random.default_rng([seed, 2, 0]), bfv)
     ct = o.encrypt(phys, a, e)
     r = np.random.default_rng(5000).integers(0, P, 2 * SLOTS).astype(np.uint32)
+    schedule = 2   # the production schedule for L = 3 (same algorithm as the GPU arm)
     if args.warmup > 0:
-        o.mv_gala(ct, pts, r, baby=baby)   # one warm-up layer (bounded CPU sample)
+        o.mv_gala(ct, pts, r, baby=baby, schedule=schedule)   # one warm-up layer (bounded CPU sample)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        o.mv_gala(ct, pts, r, baby=baby)
+        o.mv_gala(ct, pts, r, baby=baby, schedule=schedule)
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = args.steps / total

@@ -97,6 +97,19 @@ int gala_mv_gala(gala_ctx *ctx, const uint64_t *ct_dev, const uint64_t *pts_dev,
 int gala_mv_gala_batch(gala_ctx *ctx, const uint64_t *cts_dev, int B, const uint64_t *pts_dev, int T, int baby,
                        const uint32_t *r_slots_dev, uint64_t *outs_dev, uint64_t *masked_dev);
 int gala_bsgs_baby(int T);
+
+/* GALA schedule 2 (the production schedule when the noise budget allows; see
+ * DESIGN.md): one gadget decomposition of each input's c1, digits hoisted
+ * across the plaintext product (sum_i (d_i p_t) g_i = c1 p_t mod Q), so the
+ * T-1 baby-step key switches need no NTTs.  Plaintexts come from
+ * gala_encode_gala_weights: slots [T][N] -> pts2 [T][L+1][N] (every prime of
+ * QP, pre-permuted by sigma_{t mod baby}).  Matches oracle o_mv_gala2. */
+int gala_encode_gala_weights(gala_ctx *ctx, const uint32_t *slots_dev, int T, int baby, uint64_t *pts2_dev);
+int gala_mv_gala2_batch(gala_ctx *ctx, const uint64_t *cts_dev, int B, const uint64_t *pts2_dev, int T, int baby,
+                        const uint32_t *r_slots_dev, uint64_t *outs_dev, uint64_t *masked_dev);
+/* host-buffer form of gala_mv_gala2_batch (canonical words in/out, blocks until done) */
+int gala_mv_gala2_batch_host(gala_ctx *ctx, const uint64_t *cts_host, int B, const uint64_t *pts2_dev, int T,
+                             int baby, const uint32_t *r_slots_host, uint64_t *masked_host);
 /* Same with host buffers (canonical words in/out), copies on the context
  * stream; blocks until the result is in host memory. */
 int gala_mv_gala_host(gala_ctx *ctx, const uint64_t *ct_host, const uint64_t *pts_dev, int T, int baby,

@@ -53,6 +53,7 @@ def lib():
         L.o_scmult.argtypes = [ctypes.c_void_p, u64p, u32p, u64p]
         L.o_rotate_hoisted.argtypes = [ctypes.c_void_p, u64p, ip, ctypes.c_int, u64p]
         L.o_mv_gala.argtypes = [ctypes.c_void_p, u64p, u32p, ctypes.c_int, ctypes.c_int, u32p, u64p, u64p]
+        L.o_mv_gala2.argtypes = [ctypes.c_void_p, u64p, u32p, ctypes.c_int, ctypes.c_int, u32p, u64p, u64p]
         L.o_conv_kg.argtypes = [ctypes.c_void_p, u64p, ctypes.c_int, u32p, ctypes.c_int, ctypes.c_int,
                                 ctypes.c_int, ip, ctypes.c_int, u64p]
         L.o_ntt.argtypes = [ctypes.c_void_p, ctypes.c_int, u64p, ctypes.c_int]
@@ -167,7 +168,8 @@ class Oracle:
     def rotate(self, ct, step):
         return self.rotate_hoisted(ct, [step])[0]
 
-    def mv_gala(self, ct, pts, r=None, baby=0):
+    def mv_gala(self, ct, pts, r=None, baby=0, schedule=1):
+        """schedule 1: per-term decomposition; schedule 2: digits hoisted across the plaintext product."""
         ct, pts = _c(ct, np.uint64), _c(pts, np.uint32)
         T = pts.shape[0]
         out = np.zeros(self.ct_shape, np.uint64)
@@ -176,8 +178,8 @@ class Oracle:
         if r is not None:
             r = _c(r, np.uint32)
             rp = _p(r, u32p)
-        _check(lib().o_mv_gala(self._h, _p(ct, u64p), _p(pts, u32p), T, baby, rp,
-                               _p(out, u64p), _p(masked, u64p)))
+        fn = lib().o_mv_gala2 if schedule == 2 else lib().o_mv_gala
+        _check(fn(self._h, _p(ct, u64p), _p(pts, u32p), T, baby, rp, _p(out, u64p), _p(masked, u64p)))
         return out, (masked if r is not None else None)
 
     def conv_kg(self, cts, pts, tap_steps, band_step):

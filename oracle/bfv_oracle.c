@@ -738,6 +738,115 @@ int o_mv_gala(void *h, const u64 *ct, const uint32_t *pts, int T, int baby,
     return rc;
 }
 
+/* plaintext operand in all L+1 primes (centred lift), NTT domain [M][N] */
+static void encode_pt_ntt_qp(const octx *c, const uint32_t *slots, u64 *pt)
+{
+    int N = c->N;
+    u64 *m = malloc(sizeof(u64) * N);
+    o_encode_p((void *)c, slots, m);
+    u64 half = c->p >> 1;
+    for (int j = 0; j < c->M; j++) {
+        u64 q = c->t[j].q;
+        u64 *d = pt + (size_t)j * N;
+        for (int i = 0; i < N; i++) d[i] = m[i] > half ? q - (c->p - m[i]) : m[i];
+        ntt_fwd(&c->t[j], d, N);
+    }
+    free(m);
+}
+
+/*
+ * GALA dot product, schedule v2 ("digits hoisted across the plaintext product").
+ * Same logical tree as o_mv_gala (T ScMult, T-1 Perm, T-1 Add), but every
+ * baby-step key switch reuses ONE decomposition of the input: for term t,
+ *   d'_i = d_i * p_t   (integer polynomials; sum_i d'_i g_i = c1 p_t mod Q)
+ * so  KSraw(sigma_j, x (.) p_t) = sum_i sigma_j(D_i (.) P_t) * ksk_j[i]  over QP,
+ * with P_t the centred lift of p_t in every prime of QP.  Giant steps rotate
+ * the group sums with their own decompositions (as in o_mv_gala).
+ */
+int o_mv_gala2(void *h, const u64 *ct, const uint32_t *pts, int T, int baby, const uint32_t *r, u64 *out,
+               u64 *masked)
+{
+    octx *c = h;
+    int N = c->N, L = c->L, M = c->M, n = N / 2;
+    if (baby <= 0) baby = o_bsgs_baby(T);
+    if (T % baby) return -4;
+    int G = T / baby;
+    size_t W = 2 * (size_t)L * N, UW = 2 * (size_t)M * N;
+    u64 *ctn = malloc(sizeof(u64) * W);
+    ct_to_ntt(c, ct, ctn);
+    u64 *D = malloc(sizeof(u64) * (size_t)L * M * N);
+    decompose(c, ctn + (size_t)L * N, D);
+    u64 *inner = malloc(sizeof(u64) * W * (size_t)G);
+    int rc = 0;
+    for (int j = 1; j < baby; j++) if (!c->ksk[j % n]) rc = -2;
+    if (rc) { free(ctn); free(D); free(inner); return rc; }
+#pragma omp parallel for schedule(dynamic)
+    for (int g = 0; g < G; g++) {
+        u64 *U = calloc(UW, sizeof(u64));
+        u64 *C0 = calloc((size_t)L * N, sizeof(u64));
+        u64 *P = malloc(sizeof(u64) * (size_t)M * N);
+        u64 *X = malloc(sizeof(u64) * N), *Y = malloc(sizeof(u64) * N);
+        u64 *res = inner + (size_t)g * W;
+        for (int jj = 0; jj < baby; jj++) {
+            int t = g * baby + jj;
+            encode_pt_ntt_qp(c, pts + (size_t)t * N, P);
+            if (jj == 0) {
+                for (int j = 0; j < L; j++) {
+                    u64 q = c->t[j].q;
+                    for (int k = 0; k < N; k++) {
+                        C0[(size_t)j * N + k] = addmod(C0[(size_t)j * N + k],
+                                                       mulmod(ctn[(size_t)j * N + k], P[(size_t)j * N + k], q), q);
+                        res[((size_t)L + j) * N + k] = mulmod(ctn[((size_t)L + j) * N + k], P[(size_t)j * N + k], q);
+                    }
+                }
+                continue;
+            }
+            u64 gal = galois(jj, N);
+            const u64 *key = c->ksk[jj % n];
+            for (int i = 0; i < L; i++)
+                for (int j = 0; j < M; j++) {
+                    u64 q = c->t[j].q;
+                    const u64 *Dij = D + ((size_t)i * M + j) * N;
+                    for (int k = 0; k < N; k++) X[k] = mulmod(Dij[k], P[(size_t)j * N + k], q);
+                    automorph_ntt(X, Y, N, gal);
+                    for (int comp = 0; comp < 2; comp++) {
+                        const u64 *kk = key + (((size_t)i * 2 + comp) * M + j) * N;
+                        u64 *u = U + ((size_t)comp * M + j) * N;
+                        for (int k = 0; k < N; k++) u[k] = addmod(u[k], mulmod(Y[k], kk[k], q), q);
+                    }
+                }
+            for (int j = 0; j < L; j++) {
+                u64 q = c->t[j].q;
+                for (int k = 0; k < N; k++) X[k] = mulmod(ctn[(size_t)j * N + k], P[(size_t)j * N + k], q);
+                automorph_ntt(X, Y, N, gal);
+                for (int k = 0; k < N; k++) C0[(size_t)j * N + k] = addmod(C0[(size_t)j * N + k], Y[k], q);
+            }
+        }
+        u64 *md = malloc(sizeof(u64) * (size_t)L * N);
+        moddown(c, U, md);
+        for (size_t i = 0; i < (size_t)L * N; i++) {
+            u64 q = c->t[i / N].q;
+            res[i] = addmod(C0[i], md[i], q);
+        }
+        moddown(c, U + (size_t)M * N, md);
+        for (size_t i = 0; i < (size_t)L * N; i++) {
+            u64 q = c->t[i / N].q;
+            res[(size_t)L * N + i] = addmod(res[(size_t)L * N + i], md[i], q);
+        }
+        free(U); free(C0); free(P); free(X); free(Y); free(md);
+    }
+    u64 *resn = malloc(sizeof(u64) * W);
+    int *steps = malloc(sizeof(int) * (size_t)G);
+    for (int g = 0; g < G; g++) steps[g] = g * baby;
+    rc = rotate_sum_lazy(c, inner, steps, G, resn);
+    if (!rc) {
+        ct_from_ntt(c, resn, out);
+        if (r && masked) o_sub_plain(c, out, r, masked);
+    }
+    free(ctn); free(D); free(inner); free(resn); free(steps);
+    return rc;
+}
+
 /*
  * Kernel-grouping convolution (conv.py:268-293), physical form:
  *   R[ib][tap] = HstPerm(DecPerm(x_ib), tap_steps[tap])   (tap step 0 -> x)

@@ -52,6 +52,9 @@ SIGNATURES = [
     ("gala_mv_gala", i32, [vp, vp, vp, i32, i32, vp, vp, vp]),
     ("gala_bsgs_baby", i32, [i32]),
     ("gala_mv_gala_batch", i32, [vp, vp, i32, vp, i32, i32, vp, vp, vp]),
+    ("gala_encode_gala_weights", i32, [vp, vp, i32, i32, vp]),
+    ("gala_mv_gala2_batch", i32, [vp, vp, i32, vp, i32, i32, vp, vp, vp]),
+    ("gala_mv_gala2_batch_host", i32, [vp, vp, i32, vp, i32, i32, vp, vp]),
     ("gala_mv_gala_host", i32, [vp, vp, vp, i32, i32, vp, vp]),
     ("gala_mv_gala_batch_host", i32, [vp, vp, i32, vp, i32, i32, vp, vp]),
     ("gala_conv_kg", i32, [vp, vp, i32, vp, i32, i32, i32, vp, i32, vp]),

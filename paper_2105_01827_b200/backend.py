@@ -411,6 +411,33 @@ class Context:
                   ctypes.c_void_p(_ptr(masked)) if masked is not None else None)
         return outs, masked
 
+    # -- GALA schedule 2 (digits hoisted across the plaintext product) -----------
+    def gala_schedule(self, T: int) -> int:
+        """2 when the hoisted-digit key-switch noise fits the budget, else 1."""
+        return 2 if (self.L >= 2 or T <= 64) else 1
+
+    def encode_gala_weights(self, phys_slots: np.ndarray, baby: int):
+        """[T][N] physical slots -> [T][L+1][N] schedule-2 plaintexts (all QP primes, pre-permuted)."""
+        torch = _torch()
+        phys = np.atleast_2d(phys_slots)
+        T = phys.shape[0]
+        d_sl = self.to_device_u32(phys)
+        pts2 = torch.empty((T, self.L + 1, self.N), dtype=torch.int64, device=self.device)
+        self.call("gala_encode_gala_weights", ctypes.c_void_p(_ptr(d_sl)), T, int(baby), ctypes.c_void_p(_ptr(pts2)))
+        return pts2
+
+    def mv_gala2_batch(self, cts, pts2, T: int, d_r=None, baby: int | None = None, outs=None, masked=None):
+        b, steps = self.bsgs_steps(T, baby)
+        self.ensure_keys(steps)
+        B = cts.shape[0]
+        outs = self.empty_ct(B) if outs is None else outs
+        if d_r is not None and masked is None:
+            masked = self.empty_ct(B)
+        self.call("gala_mv_gala2_batch", ctypes.c_void_p(_ptr(cts)), int(B), ctypes.c_void_p(_ptr(pts2)), int(T),
+                  int(b), ctypes.c_void_p(_ptr(d_r)) if d_r is not None else None, ctypes.c_void_p(_ptr(outs)),
+                  ctypes.c_void_p(_ptr(masked)) if masked is not None else None)
+        return outs, masked
+
     def conv_kg(self, cts, pts, tap_steps, band_step: int):
         """cts [n_ib][2][L][N]; pts [n_obp][n_ib][c_n][k][L][N] -> [n_obp][2][L][N]."""
         n_obp, n_ib, c_n, k = pts.shape[:4]

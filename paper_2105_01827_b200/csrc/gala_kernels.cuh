@@ -357,6 +357,96 @@ __global__ void k_addsub(DevCtx c, const u64* __restrict__ a, const u64* __restr
     }
 }
 
+// GALA schedule-2 plaintexts: out[t][j][k] = in[t][j][ sigma_{t mod baby}^src(k) ]  (identity for t mod baby == 0)
+__global__ void k_gala_pt_perm(DevCtx c, const u64* __restrict__ in, int T, int baby, const unsigned* __restrict__ gal,
+                               u64* __restrict__ out)
+{
+    const int N = c.N, M = c.M;
+    const long long total = (long long)T * M * N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(e % N);
+        const long long tj = e / N;
+        const int t = (int)(tj / M);
+        const int jj = t % baby;
+        const int src = jj ? auto_src(k, gal[jj], c.logN) : k;
+        out[e] = in[tj * N + src];
+    }
+}
+
+// GALA schedule-2 baby-step MAC.  Group z = (input bi, group g); member jj = 0..baby-1, term t = g*baby + jj.
+//   jj = 0 : C0 += x.c0 (.) P_t,  C1 = x.c1 (.) P_t                     (no rotation)
+//   jj > 0 : U_c,j += sum_i (sigma_jj(D_i) (.) sigma_jj(P_t))_j * ksk_jj[i][c][j]   (QP, 128-bit lazy)
+//            C0   += sigma_jj(x.c0) (.) sigma_jj(P_t)
+// blocks: per input (baby-1) sigma-permuted digit blocks [(L*M + L)][N] from one decomposition of x.c1;
+// pts2: [T][M][N] Montgomery, pre-permuted by sigma_{t mod baby}.  grid (N/blockDim, M, B*G).
+template <int L>
+__global__ void __launch_bounds__(256) k_gala_mac(DevCtx c, const u64* __restrict__ X, const u64* __restrict__ blocks,
+                                                  const u64* __restrict__ pts2, const u64* const* __restrict__ keys,
+                                                  int baby, int G, u64* __restrict__ U, u64* __restrict__ Cacc)
+{
+    const int N = c.N, M = L + 1;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, z = blockIdx.z;
+    const int bi = z / G, g = z % G;
+    if (k >= N) return;
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    const int lazy = c.lazy[j];
+    const long long NN = N, LN = (long long)L * N, W = 2 * LN, MN = (long long)M * N;
+    const long long blk_words = (long long)(L * M + L) * N;
+    const u64* x = X + bi * W;
+    const u64* blk0 = blocks + (long long)bi * (baby - 1) * blk_words;
+    u64 a0 = 0, a1 = 0, u0 = 0, u1 = 0;
+    {   // step-0 member
+        const u64 w = __ldg(pts2 + ((long long)g * baby) * MN + j * NN + k);
+        if (j < L) {
+            a0 = mont_mul(__ldg(x + j * NN + k), w, md);
+            a1 = mont_mul(__ldg(x + LN + j * NN + k), w, md);
+        }
+    }
+    Acc128 s0, s1;
+    int pending = 0;
+    for (int jj = 1; jj < baby; jj++) {
+        const long long t = (long long)g * baby + jj;
+        const u64 w = __ldcs((const unsigned long long*)(pts2 + t * MN + j * NN + k));
+        const u64* blk = blk0 + (long long)(jj - 1) * blk_words;
+        const u64* key = keys[jj];
+        u64 dv[L], kb[L], ka[L];
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+            dv[i] = __ldg(blk + ((long long)i * M + j) * NN + k);
+            kb[i] = __ldg(key + (((long long)i * 2 + 0) * M + j) * NN + k);
+            ka[i] = __ldg(key + (((long long)i * 2 + 1) * M + j) * NN + k);
+        }
+        u64 cc = 0;
+        if (j < L) cc = __ldg(blk + ((long long)L * M + j) * NN + k);
+        if (pending + L > lazy) {
+            u0 = add_mod(u0, s0.reduce(md), q);
+            u1 = add_mod(u1, s1.reduce(md), q);
+            s0 = Acc128();
+            s1 = Acc128();
+            pending = 0;
+        }
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+            const u64 d = mont_mul(dv[i], w, md);      // digit of (x.c1 (.) p_t), rotated
+            s0.mac(d, kb[i]);
+            s1.mac(d, ka[i]);
+        }
+        pending += L;
+        if (j < L) a0 = add_mod(a0, mont_mul(cc, w, md), q);
+    }
+    u0 = add_mod(u0, s0.reduce(md), q);
+    u1 = add_mod(u1, s1.reduce(md), q);
+    U[(((long long)z * 2 + 0) * M + j) * NN + k] = u0;
+    U[(((long long)z * 2 + 1) * M + j) * NN + k] = u1;
+    if (j < L) {
+        Cacc[(((long long)z * 2 + 0) * L + j) * NN + k] = a0;
+        Cacc[(((long long)z * 2 + 1) * L + j) * NN + k] = a1;
+    }
+}
+
 // out[b] = ct[b] with c0 -= DM[b]  (batched subtract_plain)
 __global__ void k_sub_plain(DevCtx c, const u64* __restrict__ ct, const u64* __restrict__ DM, u64* __restrict__ out,
                             int B)
@@ -476,7 +566,8 @@ __global__ void __launch_bounds__(512, 2) k_encode(DevCtx c, const uint32_t* __r
 {
     extern __shared__ u64 smem_enc[];
     u64* sm = smem_enc;
-    const int N = c.N, L = c.L, PM = c.M; // plaintext tables at index M
+    const int N = c.N, PM = c.M; // plaintext tables at index M
+    const int L = MODE == 2 ? c.M : c.L;   // MODE 2: operand in every prime of QP
     const int b = blockIdx.x / L, j = blockIdx.x % L;
     const uint32_t* sl = slots + (long long)b * N;
     const u64 p = c.p;
@@ -489,7 +580,7 @@ __global__ void __launch_bounds__(512, 2) k_encode(DevCtx c, const uint32_t* __r
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         u64 m = shoup(sm[pad(i)], c.ninv[PM], c.ninv_sh[PM], p);
         u64 v;
-        if (MODE == 0) v = m > (p >> 1) ? q - (p - m) : m;
+        if (MODE != 1) v = m > (p >> 1) ? q - (p - m) : m;
         else v = shoup(m, c.delta[j], c.delta_sh[j], q);
         sm2[pad(i)] = v;
     }
@@ -499,7 +590,7 @@ __global__ void __launch_bounds__(512, 2) k_encode(DevCtx c, const uint32_t* __r
     u64* o = out + ((long long)b * L + j) * N;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         u64 v = csub(csub(sm[pad(i)], 2 * q), q);
-        if (MODE == 0) v = mont_mul(v, md.r2, md);
+        if (MODE != 1) v = mont_mul(v, md.r2, md);
         o[i] = v;
     }
 }

@@ -617,6 +617,7 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_block_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_encode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
     CKC(cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_encode<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
     CKC(cudaFuncSetAttribute(k_dec_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_dec_phase2, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     // keep freed scratch in the pool (stream-ordered allocator as a caching pool)
@@ -876,8 +877,138 @@ int gala_mv_gala(gala_ctx* c, const uint64_t* ct, const uint64_t* pts, int T, in
     return gala_mv_gala_batch(c, ct, 1, pts, T, baby, r, out, masked);
 }
 
-int gala_mv_gala_batch_host(gala_ctx* c, const uint64_t* cts_host, int B, const uint64_t* pts, int T, int baby,
-                            const uint32_t* r_host, uint64_t* masked_host)
+// ---------------------------------------------------------------------------
+// GALA schedule 2: one decomposition of x.c1 per input, digits hoisted across the
+// plaintext product (oracle o_mv_gala2).  Plaintexts in every prime of QP, pre-permuted.
+int gala_encode_gala_weights(gala_ctx* c, const uint32_t* slots, int T, int baby, uint64_t* pts2)
+{
+    const int N = c->dc.N, M = c->dc.M;
+    if (T <= 0 || baby <= 0 || T % baby) return set_err(GALA_ERR_PARAM, "baby %d must divide T=%d", baby, T);
+    u64* tmp;
+    RET(scratch(c, &tmp, (size_t)T * M * N));
+    KLAUNCH(c, "k_encode", k_encode<2><<<T * M, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(c->dc, slots, tmp));
+    std::vector<unsigned> gal(baby, 1u);
+    for (int jj = 1; jj < baby; jj++) gal[jj] = galois_of(c, jj);
+    void* d_gal;
+    RET(upload(c, gal.data(), gal.size() * sizeof(unsigned), &d_gal));
+    KLAUNCH(c, "k_gala_pt_perm", k_gala_pt_perm<<<grid_for((long long)T * M * N, 256), 256, 0, c->stream>>>(
+                                     c->dc, tmp, T, baby, (const unsigned*)d_gal, pts2));
+    release(c, tmp);
+    release(c, d_gal);
+    return GALA_OK;
+}
+
+int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2, int T, int baby,
+                        const uint32_t* r, uint64_t* outs, uint64_t* masked)
+{
+    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
+    if (T <= 0 || B <= 0) return set_err(GALA_ERR_DIM, "T and B must be positive");
+    if (baby <= 0) baby = gala_bsgs_baby(T);
+    if (T % baby) return set_err(GALA_ERR_PARAM, "baby step %d does not divide T=%d", baby, T);
+    const int G = T / baby;
+    const long long W = 2LL * L * N, MN = (long long)M * N;
+    const long long blk_words = (long long)(L * M + L) * N;
+    for (int j = 1; j < baby; j++)
+        if (!gala_has_rotation_key(c, j)) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", j);
+    for (int g = 1; g < G; g++)
+        if (!gala_has_rotation_key(c, g * baby))
+            return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, g * baby));
+    if (baby == 1) {   // T == 1 (a single group with one member) or degenerate trees: plain products + giant sum
+        u64* prods;
+        RET(scratch(c, &prods, (size_t)B * T * W));
+        for (int b = 0; b < B; b++)
+            for (int t = 0; t < T; t++) {
+                dim3 grid((unsigned)((2 * L * N + 255) / 256), 1);
+                KLAUNCH(c, "k_ct_mul_pts", k_ct_mul_pts<<<grid, 256, 0, c->stream>>>(
+                                               c->dc, cts + b * W, pts2 + t * MN, prods + ((long long)b * T + t) * W));
+            }
+        RET(rotate_sum_regular(c, prods, W, (long long)T * W, nullptr, B, 1, T, 1, outs, W));
+        release(c, prods);
+        if (r && masked) RET(sub_plain_batch(c, outs, r, B, masked));
+        return GALA_OK;
+    }
+    // 1. one decomposition per input, written as (baby-1) sigma-permuted digit blocks
+    u64 *dig, *blocks;
+    RET(scratch(c, &dig, (size_t)B * L * N));
+    RET(scratch(c, &blocks, (size_t)B * (baby - 1) * blk_words));
+    std::vector<TermDesc> td(B);
+    for (int b = 0; b < B; b++) {
+        td[b].X = cts + b * W;
+        td[b].pt = nullptr;
+        td[b].dig = dig + (long long)b * L * N;
+        td[b].blk = blocks + (long long)b * (baby - 1) * blk_words;
+        td[b].rot_off = 0;
+        td[b].rot_cnt = baby - 1;
+    }
+    std::vector<unsigned> gal(baby - 1);
+    std::vector<const u64*> keys(baby, nullptr);
+    for (int jj = 1; jj < baby; jj++) {
+        gal[jj - 1] = galois_of(c, jj);
+        keys[jj] = key_for(c, jj);
+    }
+    size_t o_gal = (td.size() * sizeof(TermDesc) + 15) & ~(size_t)15;
+    size_t o_keys = (o_gal + gal.size() * sizeof(unsigned) + 15) & ~(size_t)15;
+    std::vector<char> blob(o_keys + keys.size() * sizeof(u64*));
+    memcpy(blob.data(), td.data(), td.size() * sizeof(TermDesc));
+    memcpy(blob.data() + o_gal, gal.data(), gal.size() * sizeof(unsigned));
+    memcpy(blob.data() + o_keys, keys.data(), keys.size() * sizeof(u64*));
+    char* d_blob;
+    RET(upload(c, blob.data(), blob.size(), (void**)&d_blob));
+    const int nt = ntt_threads(N);
+    KLAUNCH(c, "k_digits_intt", k_digits_intt<<<(unsigned)(B * L), nt, c->smem_ntt, c->stream>>>(
+                                    c->dc, (const TermDesc*)d_blob, (const unsigned*)(d_blob + o_gal), blk_words));
+    KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(B * L * L), nt, c->smem_ntt, c->stream>>>(
+                                    c->dc, (const TermDesc*)d_blob, (const unsigned*)(d_blob + o_gal), blk_words));
+    // 2. fused baby-step MAC over all (input, group)
+    const int Z = B * G;
+    u64 *U, *Cacc, *rr, *inner;
+    RET(scratch(c, &U, (size_t)Z * 2 * M * N));
+    RET(scratch(c, &Cacc, (size_t)Z * 2 * L * N));
+    RET(scratch(c, &rr, (size_t)Z * 2 * N));
+    RET(scratch(c, &inner, (size_t)Z * W));
+    {
+        const int th = N < 256 ? N : 256;
+        dim3 grid((N + th - 1) / th, M, Z);
+        const u64* const* dk = (const u64* const*)(d_blob + o_keys);
+        switch (L) {
+            case 1: KLAUNCH(c, "k_gala_mac", k_gala_mac<1><<<grid, th, 0, c->stream>>>(c->dc, cts, blocks, pts2, dk, baby, G, U, Cacc)); break;
+            case 2: KLAUNCH(c, "k_gala_mac", k_gala_mac<2><<<grid, th, 0, c->stream>>>(c->dc, cts, blocks, pts2, dk, baby, G, U, Cacc)); break;
+            case 3: KLAUNCH(c, "k_gala_mac", k_gala_mac<3><<<grid, th, 0, c->stream>>>(c->dc, cts, blocks, pts2, dk, baby, G, U, Cacc)); break;
+            default: KLAUNCH(c, "k_gala_mac", k_gala_mac<4><<<grid, th, 0, c->stream>>>(c->dc, cts, blocks, pts2, dk, baby, G, U, Cacc)); break;
+        }
+    }
+    // 3. one ModDown per (input, group) -> inner[b][g]
+    RET(launch_inv<false>(c, U + (long long)L * N, rr, Z * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
+                          "k_ntt_inv[moddown]"));
+    MdArgs a;
+    a.r = rr;
+    a.U = U;
+    a.add0 = Cacc;
+    a.add1 = Cacc + (long long)L * N;
+    a.add_is = 2LL * L * N;
+    a.out = inner;
+    a.out_is = W;
+    a.outs = nullptr;
+    KLAUNCH(c, "k_moddown", k_moddown<<<Z * 2 * L, nt, c->smem_ntt, c->stream>>>(c->dc, a));
+    release(c, U);
+    release(c, Cacc);
+    release(c, rr);
+    release(c, dig);
+    release(c, blocks);
+    release(c, d_blob);
+    // 4. giant steps (each group sum has its own decomposition), one lazy ModDown per input
+    if (G > 1) {
+        RET(rotate_sum_regular(c, inner, W, (long long)G * W, nullptr, B, 1, G, baby, outs, W));
+    } else {
+        CK(cudaMemcpyAsync(outs, inner, sizeof(u64) * B * W, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    release(c, inner);
+    if (r && masked) RET(sub_plain_batch(c, outs, r, B, masked));
+    return GALA_OK;
+}
+
+static int mv_batch_host(gala_ctx* c, int schedule, const uint64_t* cts_host, int B, const uint64_t* pts, int T,
+                         int baby, const uint32_t* r_host, uint64_t* masked_host)
 {
     const int N = c->dc.N, L = c->dc.L;
     const long long W = 2LL * L * N;
@@ -891,7 +1022,8 @@ int gala_mv_gala_batch_host(gala_ctx* c, const uint64_t* cts_host, int B, const 
     CK(cudaMemcpyAsync(coef, cts_host, sizeof(u64) * B * W, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(r, r_host, sizeof(uint32_t) * B * N, cudaMemcpyHostToDevice, c->stream));
     RET(gala_ct_import(c, coef, ct, B));
-    RET(gala_mv_gala_batch(c, ct, B, pts, T, baby, r, out, masked));
+    if (schedule == 2) RET(gala_mv_gala2_batch(c, ct, B, pts, T, baby, r, out, masked));
+    else RET(gala_mv_gala_batch(c, ct, B, pts, T, baby, r, out, masked));
     RET(gala_ct_export(c, masked, coef, B));
     CK(cudaMemcpyAsync(masked_host, coef, sizeof(u64) * B * W, cudaMemcpyDeviceToHost, c->stream));
     release(c, coef);
@@ -901,6 +1033,18 @@ int gala_mv_gala_batch_host(gala_ctx* c, const uint64_t* cts_host, int B, const 
     release(c, r);
     CK(cudaStreamSynchronize(c->stream));
     return GALA_OK;
+}
+
+int gala_mv_gala_batch_host(gala_ctx* c, const uint64_t* cts_host, int B, const uint64_t* pts, int T, int baby,
+                            const uint32_t* r_host, uint64_t* masked_host)
+{
+    return mv_batch_host(c, 1, cts_host, B, pts, T, baby, r_host, masked_host);
+}
+
+int gala_mv_gala2_batch_host(gala_ctx* c, const uint64_t* cts_host, int B, const uint64_t* pts2, int T, int baby,
+                             const uint32_t* r_host, uint64_t* masked_host)
+{
+    return mv_batch_host(c, 2, cts_host, B, pts2, T, baby, r_host, masked_host);
 }
 
 int gala_mv_gala_host(gala_ctx* c, const uint64_t* ct_host, const uint64_t* pts, int T, int baby,

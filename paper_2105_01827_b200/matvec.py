@@ -250,10 +250,17 @@ def mv_gala(task: MvTask, ct_xpack: Ciphertext, meter: CostMeter, rng=None) -> M
     lin = CostMeter(meter.cost_model)
     slots = gala_weight_slots(task)
     T = slots.shape[0]
-    pts = ctx.encode_plain(np.concatenate([slots, slots], axis=1))
+    phys = np.concatenate([slots, slots], axis=1)
     gen, seed = _resolve_rng(rng)
     r = draw_mask(gen, params.p, params.n)
-    out, masked = ctx.mv_gala(ct_xpack.data, pts, T, ctx.physical(r.slots))
+    if ctx.gala_schedule(T) == 2:
+        baby, _ = ctx.bsgs_steps(T)
+        pts2 = ctx.encode_gala_weights(phys, baby)
+        outs, masked_b = ctx.mv_gala2_batch(ct_xpack.data.unsqueeze(0), pts2, T,
+                                            ctx.to_device_u32(ctx.physical(r.slots)[None, :]), baby)
+        out, masked = outs[0], masked_b[0]
+    else:
+        out, masked = ctx.mv_gala(ct_xpack.data, ctx.encode_plain(phys), T, ctx.physical(r.slots))
     book_gala(lin, T)
     meter.merge(lin)
     out_noise = _gala_noise(ct_xpack.noise, T, params)
@@ -317,10 +324,13 @@ class GalaFC:
             s1 = gala_weight_slots(tasks[1]) if self.paired else s0
             if s0.shape != s1.shape:
                 raise ParameterError("paired row blocks must share T")
-            pts = self.ctx.encode_plain(np.concatenate([s0, s1], axis=1))
-            self.blocks.append((tasks, pts, s0.shape[0]))
+            self.blocks.append([tasks, np.concatenate([s0, s1], axis=1), s0.shape[0]])
         self.T = self.blocks[0][2]
         self.baby, self.steps = self.ctx.bsgs_steps(self.T)
+        self.schedule = self.ctx.gala_schedule(self.T)
+        for blk in self.blocks:    # resident encoded weights, in the layout of the chosen schedule
+            blk[1] = (self.ctx.encode_gala_weights(blk[1], self.baby) if self.schedule == 2
+                      else self.ctx.encode_plain(blk[1]))
         self.ctx.ensure_keys(self.steps)
 
     def encrypt_input(self, x) -> list:
@@ -345,9 +355,15 @@ class GalaFC:
         outs = []
         for (tasks, pts, T), ct, rs in zip(self.blocks, cts, masks):
             phys_r = self.ctx.physical(rs[0].slots, rs[1].slots if self.paired else None)
-            _, masked = self.ctx.mv_gala(ct, pts, T, phys_r, self.baby)
-            outs.append(masked)
+            _, masked = self.run_batch(ct.unsqueeze(0), pts, self.ctx.to_device_u32(phys_r[None, :]))
+            outs.append(masked[0])
         return outs
+
+    def run_batch(self, cts, pts, d_r, outs=None, masked=None):
+        """Fused layer over a batch of inputs (cts [B][2][L][N], d_r [B][N]) for one column block."""
+        if self.schedule == 2:
+            return self.ctx.mv_gala2_batch(cts, pts, self.T, d_r, self.baby, outs=outs, masked=masked)
+        return self.ctx.mv_gala_batch(cts, pts, self.T, d_r, self.baby, outs=outs, masked=masked)
 
     def server_shares(self, masks) -> np.ndarray:
         res = np.zeros(self.n_out, dtype=np.int64)

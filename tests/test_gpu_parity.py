@@ -115,3 +115,24 @@ def test_mv_gala_batch_words(tw):
         c_out, c_masked = tw.cpu.mv_gala(c, pts, rs[i], baby=b)
         assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
         assert np.array_equal(tw.gpu.export_words(masked[i]), c_masked)
+
+
+@pytest.mark.parametrize("T", [1, 2, 4, 8, 16])
+def test_mv_gala2_words(tw, T):
+    """Schedule 2 (digits hoisted across the plaintext product) == oracle o_mv_gala2, batched."""
+    import torch
+
+    n = tw.bfv.n
+    if T > n:
+        pytest.skip("T > n")
+    b, steps = tw.gpu.bsgs_steps(T)
+    tw.keys_for(steps)
+    pts = tw.slots(T)
+    pts2 = tw.gpu.encode_gala_weights(pts, b)
+    xs = [tw.encrypt(tw.slots()) for _ in range(2)]
+    rs = tw.slots(2)
+    outs, masked = tw.gpu.mv_gala2_batch(torch.stack([g for g, _ in xs]), pts2, T, tw.gpu.to_device_u32(rs), b)
+    for i, (g, c) in enumerate(xs):
+        c_out, c_masked = tw.cpu.mv_gala(c, pts, rs[i], baby=b, schedule=2)
+        assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
+        assert np.array_equal(tw.gpu.export_words(masked[i]), c_masked)
