@@ -447,6 +447,99 @@ __global__ void __launch_bounds__(256) k_gala_mac(DevCtx c, const u64* __restric
     }
 }
 
+// GALA schedule 2, stage A (per input and baby rotation jj, shared by every group):
+//   E[bi][jj][c][j][k] = sum_i sigma_jj(D_i)_j[k] * ksk_jj[i][c][j][k]          (QP)
+//   R0[bi][jj][j][k]   = sigma_jj(x.c0)_j[k]                                     (Q)
+// D: identity digit block of the input ([(L*M + L)][N], NTT), gathered through sigma (L2 resident).
+// grid (N / blockDim, M, B * (baby - 1)).
+template <int L>
+__global__ void __launch_bounds__(256) k_gala_e(DevCtx c, const u64* __restrict__ Dblk, const u64* const* __restrict__ keys,
+                                                const unsigned* __restrict__ gal, int baby, u64* __restrict__ E,
+                                                u64* __restrict__ R0)
+{
+    const int N = c.N, M = L + 1;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, z = blockIdx.z;
+    const int bi = z / (baby - 1), jj = z % (baby - 1) + 1;
+    if (k >= N) return;
+    const ModC md = c.mod[j];
+    const long long NN = N, MN = (long long)M * N;
+    const u64* D = Dblk + (long long)bi * (L * M + L) * NN;
+    const u64* key = keys[jj];
+    const int src = auto_src(k, gal[jj], c.logN);
+    Acc128 s0, s1;
+#pragma unroll
+    for (int i = 0; i < L; i++) {
+        const u64 d = __ldg(D + ((long long)i * M + j) * NN + src);
+        s0.mac(d, __ldg(key + (((long long)i * 2 + 0) * M + j) * NN + k));
+        s1.mac(d, __ldg(key + (((long long)i * 2 + 1) * M + j) * NN + k));
+    }
+    u64* e = E + (long long)z * 2 * MN + j * NN + k;
+    e[0] = s0.reduce(md);
+    e[MN] = s1.reduce(md);
+    if (j < L) R0[((long long)z * L + j) * NN + k] = __ldg(D + ((long long)L * M + j) * NN + src);
+}
+
+// GALA schedule 2, stage B (per input bi and group g):
+//   U_c,j = sum_{jj >= 1} w_t (.) E[bi][jj][c][j]      C0_j = sum_{jj >= 1} w_t (.) R0[bi][jj][j] + x.c0 (.) P_{g b}
+//   C1_j  = x.c1 (.) P_{g b}                            (t = g b + jj, w_t = sigma_jj(P_t) pre-permuted)
+// 128-bit lazy accumulation; grid (N / blockDim, M, B * G).
+__global__ void __launch_bounds__(256) k_gala_mac2(DevCtx c, const u64* __restrict__ X, const u64* __restrict__ E,
+                                                   const u64* __restrict__ R0, const u64* __restrict__ pts2, int baby,
+                                                   int G, u64* __restrict__ U, u64* __restrict__ Cacc)
+{
+    const int N = c.N, L = c.L, M = c.M;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, z = blockIdx.z;
+    const int bi = z / G, g = z % G;
+    if (k >= N) return;
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    const int lazy = c.lazy[j];
+    const long long NN = N, LN = (long long)L * N, W = 2 * LN, MN = (long long)M * N;
+    const u64* x = X + bi * W;
+    u64 a1 = 0;
+    Acc128 s0, s1, sc;
+    {   // step-0 member: x (.) P_{g b}
+        const u64 w = __ldg(pts2 + ((long long)g * baby) * MN + j * NN + k);
+        if (j < L) {
+            sc.mac(__ldg(x + j * NN + k), w);
+            a1 = mont_mul(__ldg(x + LN + j * NN + k), w, md);
+        }
+    }
+    u64 u0 = 0, u1 = 0, a0 = 0;
+    int pending = 1;
+    const u64* Eb = E + (long long)bi * (baby - 1) * 2 * MN + j * NN + k;
+    const u64* Rb = R0 + (long long)bi * (baby - 1) * LN + j * NN + k;
+    for (int jj = 1; jj < baby; jj++) {
+        const long long t = (long long)g * baby + jj;
+        const u64 w = __ldcs((const unsigned long long*)(pts2 + t * MN + j * NN + k));
+        const u64* e = Eb + (long long)(jj - 1) * 2 * MN;
+        if (pending == lazy) {
+            u0 = add_mod(u0, s0.reduce(md), q);
+            u1 = add_mod(u1, s1.reduce(md), q);
+            a0 = add_mod(a0, sc.reduce(md), q);
+            s0 = Acc128();
+            s1 = Acc128();
+            sc = Acc128();
+            pending = 0;
+        }
+        s0.mac(w, __ldg(e));
+        s1.mac(w, __ldg(e + MN));
+        if (j < L) sc.mac(w, __ldg(Rb + (long long)(jj - 1) * LN));
+        pending++;
+    }
+    u0 = add_mod(u0, s0.reduce(md), q);
+    u1 = add_mod(u1, s1.reduce(md), q);
+    a0 = add_mod(a0, sc.reduce(md), q);
+    U[(((long long)z * 2 + 0) * M + j) * NN + k] = u0;
+    U[(((long long)z * 2 + 1) * M + j) * NN + k] = u1;
+    if (j < L) {
+        Cacc[(((long long)z * 2 + 0) * L + j) * NN + k] = a0;
+        Cacc[(((long long)z * 2 + 1) * L + j) * NN + k] = a1;
+    }
+}
+
 // out[b] = ct[b] with c0 -= DM[b]  (batched subtract_plain)
 __global__ void k_sub_plain(DevCtx c, const u64* __restrict__ ct, const u64* __restrict__ DM, u64* __restrict__ out,
                             int B)

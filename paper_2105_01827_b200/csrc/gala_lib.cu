@@ -927,23 +927,24 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
         if (r && masked) RET(sub_plain_batch(c, outs, r, B, masked));
         return GALA_OK;
     }
-    // 1. one decomposition per input, written as (baby-1) sigma-permuted digit blocks
-    u64 *dig, *blocks;
+    // 1. one decomposition per input: identity digit block [(L*M + L)][N] (digits of x.c1 in every
+    //    prime of QP, then x.c0)
+    u64 *dig, *Dblk;
     RET(scratch(c, &dig, (size_t)B * L * N));
-    RET(scratch(c, &blocks, (size_t)B * (baby - 1) * blk_words));
+    RET(scratch(c, &Dblk, (size_t)B * blk_words));
     std::vector<TermDesc> td(B);
     for (int b = 0; b < B; b++) {
         td[b].X = cts + b * W;
         td[b].pt = nullptr;
         td[b].dig = dig + (long long)b * L * N;
-        td[b].blk = blocks + (long long)b * (baby - 1) * blk_words;
+        td[b].blk = Dblk + (long long)b * blk_words;
         td[b].rot_off = 0;
-        td[b].rot_cnt = baby - 1;
+        td[b].rot_cnt = 1;
     }
-    std::vector<unsigned> gal(baby - 1);
+    std::vector<unsigned> gal(baby, 1u);          // gal[0] = identity (the decomposition block)
     std::vector<const u64*> keys(baby, nullptr);
     for (int jj = 1; jj < baby; jj++) {
-        gal[jj - 1] = galois_of(c, jj);
+        gal[jj] = galois_of(c, jj);
         keys[jj] = key_for(c, jj);
     }
     size_t o_gal = (td.size() * sizeof(TermDesc) + 15) & ~(size_t)15;
@@ -955,28 +956,36 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
     char* d_blob;
     RET(upload(c, blob.data(), blob.size(), (void**)&d_blob));
     const int nt = ntt_threads(N);
+    const unsigned* d_gal = (const unsigned*)(d_blob + o_gal);
     KLAUNCH(c, "k_digits_intt", k_digits_intt<<<(unsigned)(B * L), nt, c->smem_ntt, c->stream>>>(
-                                    c->dc, (const TermDesc*)d_blob, (const unsigned*)(d_blob + o_gal), blk_words));
+                                    c->dc, (const TermDesc*)d_blob, d_gal, blk_words));
     KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(B * L * L), nt, c->smem_ntt, c->stream>>>(
-                                    c->dc, (const TermDesc*)d_blob, (const unsigned*)(d_blob + o_gal), blk_words));
-    // 2. fused baby-step MAC over all (input, group)
+                                    c->dc, (const TermDesc*)d_blob, d_gal, blk_words));
+    // 2. stage A: E_jj = sum_i sigma_jj(D_i) ksk_jj[i] per input and baby rotation (shared by all groups);
+    //    stage B: per (input, group) U = sum_jj w_t E_jj, C0 = sum_jj w_t sigma_jj(c0) (+ step-0 member)
     const int Z = B * G;
-    u64 *U, *Cacc, *rr, *inner;
+    u64 *E, *R0, *U, *Cacc, *rr, *inner;
+    RET(scratch(c, &E, (size_t)B * (baby - 1) * 2 * MN));
+    RET(scratch(c, &R0, (size_t)B * (baby - 1) * L * N));
     RET(scratch(c, &U, (size_t)Z * 2 * M * N));
     RET(scratch(c, &Cacc, (size_t)Z * 2 * L * N));
     RET(scratch(c, &rr, (size_t)Z * 2 * N));
     RET(scratch(c, &inner, (size_t)Z * W));
     {
         const int th = N < 256 ? N : 256;
-        dim3 grid((N + th - 1) / th, M, Z);
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
+        dim3 ga((N + th - 1) / th, M, B * (baby - 1));
         switch (L) {
-            case 1: KLAUNCH(c, "k_gala_mac", k_gala_mac<1><<<grid, th, 0, c->stream>>>(c->dc, cts, blocks, pts2, dk, baby, G, U, Cacc)); break;
-            case 2: KLAUNCH(c, "k_gala_mac", k_gala_mac<2><<<grid, th, 0, c->stream>>>(c->dc, cts, blocks, pts2, dk, baby, G, U, Cacc)); break;
-            case 3: KLAUNCH(c, "k_gala_mac", k_gala_mac<3><<<grid, th, 0, c->stream>>>(c->dc, cts, blocks, pts2, dk, baby, G, U, Cacc)); break;
-            default: KLAUNCH(c, "k_gala_mac", k_gala_mac<4><<<grid, th, 0, c->stream>>>(c->dc, cts, blocks, pts2, dk, baby, G, U, Cacc)); break;
+            case 1: KLAUNCH(c, "k_gala_e", k_gala_e<1><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
+            case 2: KLAUNCH(c, "k_gala_e", k_gala_e<2><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
+            case 3: KLAUNCH(c, "k_gala_e", k_gala_e<3><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
+            default: KLAUNCH(c, "k_gala_e", k_gala_e<4><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
         }
+        dim3 gb((N + th - 1) / th, M, Z);
+        KLAUNCH(c, "k_gala_mac2", k_gala_mac2<<<gb, th, 0, c->stream>>>(c->dc, cts, E, R0, pts2, baby, G, U, Cacc));
     }
+    release(c, E);
+    release(c, R0);
     // 3. one ModDown per (input, group) -> inner[b][g]
     RET(launch_inv<false>(c, U + (long long)L * N, rr, Z * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
@@ -994,7 +1003,7 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
     release(c, Cacc);
     release(c, rr);
     release(c, dig);
-    release(c, blocks);
+    release(c, Dblk);
     release(c, d_blob);
     // 4. giant steps (each group sum has its own decomposition), one lazy ModDown per input
     if (G > 1) {
