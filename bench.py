@@ -128,7 +128,8 @@ def modmul_model(N, L, T, baby, schedule):
     if schedule == 2:
         giant = G - 1
         per_kernel = {
-            "k_gala_mac": G * (baby - 1) * (M * N * 3 * L + L * N) + G * 2 * L * N,
+            "k_gala_e": (baby - 1) * 2 * L * M * N,
+            "k_gala_mac2": G * (baby - 1) * (2 * M * N + L * N) + G * 2 * L * N,
             "k_digits_intt": (1 + giant) * L * h,
             "k_digits_perm": (1 + giant) * L * L * h,
             "k_ks_mac": giant * 2 * L * M * N,

@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -981,8 +982,9 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
             case 3: KLAUNCH(c, "k_gala_e", k_gala_e<3><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
             default: KLAUNCH(c, "k_gala_e", k_gala_e<4><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
         }
-        dim3 gb((N + th - 1) / th, M, Z);
-        KLAUNCH(c, "k_gala_mac2", k_gala_mac2<<<gb, th, 0, c->stream>>>(c->dc, cts, E, R0, pts2, baby, G, U, Cacc));
+        // one (input, group) per thread: measured best (CB = 2, 4 share plaintext loads but lose occupancy)
+        dim3 gb((N + th - 1) / th, M, G * B);
+        KLAUNCH(c, "k_gala_mac2", k_gala_mac2<1><<<gb, th, 0, c->stream>>>(c->dc, cts, E, R0, pts2, baby, G, B, U, Cacc));
     }
     release(c, E);
     release(c, R0);
