@@ -286,6 +286,14 @@ def run_ours(args):
     dom_achieved = dom_work / (dom["ms"] / 1e3) if dom["ms"] else 0.0
     layer_achieved = layer_modmuls * layers / world / (total_ms / 1e3)
 
+    traffic = None    # DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            tj = json.load(f)
+        if dom_name in tj and B == 8:
+            traffic = int(tj[dom_name])
+    except Exception:
+        pass
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -324,7 +332,8 @@ def run_ours(args):
             "peak": round(peak_modmul / 1e9, 2),
             "unit": "Gmodmul/s",
             "frac": round(dom_achieved / peak_modmul, 4) if peak_modmul else None,
-            "traffic": None,
+            "traffic": traffic,
+            "traffic_unit": "bytes per launch (dram read + write, ncu --set full, profiles/r1_ncu_summary.md)",
             "kernel_share_of_step": round(dom["ms"] / step_ms_prof, 4) if step_ms_prof else None,
             "peak_source": "measured live: gala_bench_modmul (60-bit Shoup modmul chains, all SMs)",
             "layer": {"achieved": round(layer_achieved / 1e9, 2), "frac": round(layer_achieved / peak_modmul, 4),
