@@ -40,10 +40,11 @@ WORKLOAD = "gala_fc_1024x4096_N8192_L3"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=8, help="independent layers (inputs) per step per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--baby", type=int, default=0, help="BSGS baby-step count (0: library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="run one profiled step and print the breakdown")
     return ap.parse_args()
@@ -78,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "10"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except Exception:
@@ -166,7 +167,7 @@ def run_ours(args):
 
     params = HEParams(n=SLOTS, p=P, rns_limbs=3, device=local, seed=7)
     t_setup = time.perf_counter()
-    layer = GalaFC(weights(), params)
+    layer = GalaFC(weights(), params, baby=args.baby or None)
     ctx = layer.ctx
     N, L, T, baby = ctx.N, ctx.L, layer.T, layer.baby
     B = args.batch

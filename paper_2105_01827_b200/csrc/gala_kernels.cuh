@@ -480,81 +480,68 @@ __global__ void __launch_bounds__(256) k_gala_e(DevCtx c, const u64* __restrict_
     if (j < L) R0[((long long)z * L + j) * NN + k] = __ldg(D + ((long long)L * M + j) * NN + src);
 }
 
-// GALA schedule 2, stage B (per group g and a chunk of CB inputs):
+// GALA schedule 2, stage B (per input bi and group g):
 //   U_c,j = sum_{jj >= 1} w_t (.) E[bi][jj][c][j]      C0_j = sum_{jj >= 1} w_t (.) R0[bi][jj][j] + x.c0 (.) P_{g b}
 //   C1_j  = x.c1 (.) P_{g b}                            (t = g b + jj, w_t = sigma_jj(P_t) pre-permuted)
-// Each plaintext word w_t is loaded once and applied to CB inputs (the weights are shared by the
-// batch); 128-bit lazy accumulation, REDC every c.lazy[j] products.
-// grid (N / blockDim, M, B/CB chunks * G) with z = chunk * G + g (input-major: E of a chunk stays in L2).
-template <int CB>
+// Members are processed in chunks of CH: all loads of a chunk are issued before its multiplies
+// (memory-level parallelism), and the 128-bit accumulators are Montgomery-reduced once per chunk
+// (CH <= c.lazy[j] products).  grid (N / blockDim, M, B * G), z = bi * G + g (input-major: E of an
+// input stays in L2 while its groups run).
+template <int CH>
 __global__ void __launch_bounds__(256) k_gala_mac2(DevCtx c, const u64* __restrict__ X, const u64* __restrict__ E,
                                                    const u64* __restrict__ R0, const u64* __restrict__ pts2, int baby,
-                                                   int G, int B, u64* __restrict__ U, u64* __restrict__ Cacc)
+                                                   int G, u64* __restrict__ U, u64* __restrict__ Cacc)
 {
     const int N = c.N, L = c.L, M = c.M;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
-    const int g = blockIdx.z % G, b0 = (blockIdx.z / G) * CB;
+    const int j = blockIdx.y, z = blockIdx.z;
+    const int bi = z / G, g = z % G;
     if (k >= N) return;
     const ModC md = c.mod[j];
     const u64 q = md.q;
-    const int lazy = c.lazy[j];
+    const bool jq = j < L;
     const long long NN = N, LN = (long long)L * N, W = 2 * LN, MN = (long long)M * N;
-    const long long Estride = (long long)(baby - 1) * 2 * MN, Rstride = (long long)(baby - 1) * LN;
-    u64 u0[CB], u1[CB], a0[CB], a1[CB];
-    Acc128 s0[CB], s1[CB], sc[CB];
+    const u64* x = X + bi * W;
+    const u64* Eb = E + (long long)bi * (baby - 1) * 2 * MN + j * NN + k;
+    const u64* Rb = R0 + (long long)bi * (baby - 1) * LN + j * NN + k;
+    const u64* Pb = pts2 + ((long long)g * baby) * MN + j * NN + k;
+    u64 u0 = 0, u1 = 0, a0 = 0, a1 = 0;
     {   // step-0 member: x (.) P_{g b}
-        const u64 w = __ldg(pts2 + ((long long)g * baby) * MN + j * NN + k);
-#pragma unroll
-        for (int b = 0; b < CB; b++) {
-            u0[b] = u1[b] = a0[b] = a1[b] = 0;
-            if (b0 + b < B && j < L) {
-                const u64* x = X + (b0 + b) * W;
-                sc[b].mac(__ldg(x + j * NN + k), w);
-                a1[b] = mont_mul(__ldg(x + LN + j * NN + k), w, md);
-            }
+        const u64 w = __ldg(Pb);
+        if (jq) {
+            a0 = mont_mul(__ldg(x + j * NN + k), w, md);
+            a1 = mont_mul(__ldg(x + LN + j * NN + k), w, md);
         }
     }
-    int pending = 1;
-#pragma unroll 4
-    for (int jj = 1; jj < baby; jj++) {
-        const long long t = (long long)g * baby + jj;
-        const u64 w = __ldcs((const unsigned long long*)(pts2 + t * MN + j * NN + k));
-        const long long eo = (long long)(jj - 1) * 2 * MN + j * NN + k;
-        const long long ro = (long long)(jj - 1) * LN + j * NN + k;
-        if (pending == lazy) {
+    for (int jj0 = 1; jj0 < baby; jj0 += CH) {
+        u64 w[CH], e0[CH], e1[CH], r0[CH];
 #pragma unroll
-            for (int b = 0; b < CB; b++) {
-                u0[b] = add_mod(u0[b], s0[b].reduce(md), q);
-                u1[b] = add_mod(u1[b], s1[b].reduce(md), q);
-                a0[b] = add_mod(a0[b], sc[b].reduce(md), q);
-                s0[b] = Acc128();
-                s1[b] = Acc128();
-                sc[b] = Acc128();
-            }
-            pending = 0;
-        }
-#pragma unroll
-        for (int b = 0; b < CB; b++) {
-            if (b0 + b < B) {
-                const u64* e = E + (b0 + b) * Estride + eo;
-                s0[b].mac(w, __ldg(e));
-                s1[b].mac(w, __ldg(e + MN));
-                if (j < L) sc[b].mac(w, __ldg(R0 + (b0 + b) * Rstride + ro));
+        for (int m = 0; m < CH; m++) {
+            const int jj = jj0 + m;
+            w[m] = e0[m] = e1[m] = r0[m] = 0;
+            if (jj < baby) {
+                w[m] = __ldcs((const unsigned long long*)(Pb + (long long)jj * MN));
+                e0[m] = __ldg(Eb + (long long)(jj - 1) * 2 * MN);
+                e1[m] = __ldg(Eb + (long long)(jj - 1) * 2 * MN + MN);
+                if (jq) r0[m] = __ldg(Rb + (long long)(jj - 1) * LN);
             }
         }
-        pending++;
+        Acc128 s0, s1, sc;
+#pragma unroll
+        for (int m = 0; m < CH; m++) {
+            s0.mac(w[m], e0[m]);
+            s1.mac(w[m], e1[m]);
+            if (jq) sc.mac(w[m], r0[m]);
+        }
+        u0 = add_mod(u0, s0.reduce(md), q);
+        u1 = add_mod(u1, s1.reduce(md), q);
+        if (jq) a0 = add_mod(a0, sc.reduce(md), q);
     }
-#pragma unroll
-    for (int b = 0; b < CB; b++) {
-        if (b0 + b >= B) continue;
-        const long long z = (long long)(b0 + b) * G + g;    // output order [input][group]
-        U[((z * 2 + 0) * M + j) * NN + k] = add_mod(u0[b], s0[b].reduce(md), q);
-        U[((z * 2 + 1) * M + j) * NN + k] = add_mod(u1[b], s1[b].reduce(md), q);
-        if (j < L) {
-            Cacc[((z * 2 + 0) * L + j) * NN + k] = add_mod(a0[b], sc[b].reduce(md), q);
-            Cacc[((z * 2 + 1) * L + j) * NN + k] = a1[b];
-        }
+    U[(((long long)z * 2 + 0) * M + j) * NN + k] = u0;
+    U[(((long long)z * 2 + 1) * M + j) * NN + k] = u1;
+    if (jq) {
+        Cacc[(((long long)z * 2 + 0) * L + j) * NN + k] = a0;
+        Cacc[(((long long)z * 2 + 1) * L + j) * NN + k] = a1;
     }
 }
 

@@ -118,6 +118,8 @@ struct gala_ctx {
     size_t key_bytes = 0;
     Staging stage;
     int smem_ntt = 0;         // bytes of one padded polynomial
+    cudaStream_t side = nullptr;              // independent work (mask encoding) overlapped with the layer
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::mutex mu;
     // per-kernel CUDA-event profiling
     bool prof_on = false;
@@ -418,6 +420,37 @@ static int rotate_sum_regular(gala_ctx* c, const u64* X, long long x_stride, lon
     return rotate_engine(c, terms, groups, outs);
 }
 
+// Delta encode(r[b]) for a batch, issued on the side stream so it overlaps the layer; the main
+// stream joins before the subtraction (mask_finish).  DM is allocated on the main stream first.
+static int mask_begin(gala_ctx* c, const uint32_t* r, int B, u64** DM)
+{
+    const int N = c->dc.N, L = c->dc.L;
+    RET(scratch(c, DM, (size_t)B * L * N));
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    cudaStream_t main = c->stream;
+    cudaEvent_t a = nullptr, b = nullptr;
+    c->stream = c->side;   // profiling events belong on the side stream
+    if (c->prof_on) prof_begin(c, &a, &b);
+    k_encode<1><<<B * L, ntt_threads(N), 2 * c->smem_ntt, c->side>>>(c->dc, r, *DM);
+    if (c->prof_on) prof_end(c, "k_encode", a, b);
+    c->stream = main;
+    g_launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(GALA_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    CK(cudaEventRecord(c->ev_join, c->side));
+    return GALA_OK;
+}
+static int mask_finish(gala_ctx* c, const u64* ct, u64* DM, int B, u64* out)
+{
+    const int N = c->dc.N, L = c->dc.L;
+    const long long W = 2LL * L * N;
+    CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    KLAUNCH(c, "k_sub_plain", k_sub_plain<<<grid_for((long long)B * W, 256), 256, 0, c->stream>>>(c->dc, ct, DM, out, B));
+    release(c, DM);
+    return GALA_OK;
+}
+
 // masked[b] = ct[b] - Delta encode(r[b]) for a batch (one encode launch for all b)
 static int sub_plain_batch(gala_ctx* c, const u64* ct, const uint32_t* r, int B, u64* out)
 {
@@ -451,6 +484,12 @@ static void free_ctx(gala_ctx* c)
     if (c->d_pmod) cudaFree(c->d_pmod);
     if (c->stage.host) cudaFreeHost(c->stage.host);
     if (c->stage.done) cudaEventDestroy(c->stage.done);
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaStreamDestroy(c->side);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (auto& r : c->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -588,6 +627,9 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
         }                                                                                         \
     } while (0)
     CKC(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CKC(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CKC(cudaMalloc(&c->d_tables, tw.size() * sizeof(ulonglong2)));
     CKC(cudaMemcpy(c->d_tables, tw.data(), tw.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice));
     for (int j = 0; j < NM; j++) {
@@ -853,6 +895,8 @@ int gala_mv_gala_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* 
     for (int g = 1; g < G; g++)
         if (!gala_has_rotation_key(c, g * baby))
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, g * baby));
+    u64* DM = nullptr;
+    if (r && masked) RET(mask_begin(c, r, B, &DM));   // overlaps the layer on the side stream
     if (T == 1) {
         for (int b = 0; b < B; b++) {
             dim3 grid((unsigned)((2 * L * N + 255) / 256), 1);
@@ -868,7 +912,7 @@ int gala_mv_gala_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* 
         RET(rotate_sum_regular(c, inner, W, (long long)G * W, nullptr, B, 1, G, baby, outs, W));
         release(c, inner);
     }
-    if (r && masked) RET(sub_plain_batch(c, outs, r, B, masked));
+    if (DM) RET(mask_finish(c, outs, DM, B, masked));
     return GALA_OK;
 }
 
@@ -928,6 +972,8 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
         if (r && masked) RET(sub_plain_batch(c, outs, r, B, masked));
         return GALA_OK;
     }
+    u64* DM = nullptr;
+    if (r && masked) RET(mask_begin(c, r, B, &DM));   // overlaps the layer on the side stream
     // 1. one decomposition per input: identity digit block [(L*M + L)][N] (digits of x.c1 in every
     //    prime of QP, then x.c0)
     u64 *dig, *Dblk;
@@ -982,9 +1028,12 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
             case 3: KLAUNCH(c, "k_gala_e", k_gala_e<3><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
             default: KLAUNCH(c, "k_gala_e", k_gala_e<4><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
         }
-        // one (input, group) per thread: measured best (CB = 2, 4 share plaintext loads but lose occupancy)
+        // one (input, group) per thread (measured best: sharing plaintext loads across inputs, or an
+        // smem-tiled modular GEMM, costs occupancy / Montgomery products and runs slower)
+        // one member per REDC, 48 registers: measured best (larger chunks of lazy accumulation or
+        // sharing plaintext loads across inputs raise register pressure and lose to occupancy)
         dim3 gb((N + th - 1) / th, M, G * B);
-        KLAUNCH(c, "k_gala_mac2", k_gala_mac2<1><<<gb, th, 0, c->stream>>>(c->dc, cts, E, R0, pts2, baby, G, B, U, Cacc));
+        KLAUNCH(c, "k_gala_mac2", k_gala_mac2<1><<<gb, th, 0, c->stream>>>(c->dc, cts, E, R0, pts2, baby, G, U, Cacc));
     }
     release(c, E);
     release(c, R0);
@@ -1014,7 +1063,7 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
         CK(cudaMemcpyAsync(outs, inner, sizeof(u64) * B * W, cudaMemcpyDeviceToDevice, c->stream));
     }
     release(c, inner);
-    if (r && masked) RET(sub_plain_batch(c, outs, r, B, masked));
+    if (DM) RET(mask_finish(c, outs, DM, B, masked));
     return GALA_OK;
 }
 

@@ -300,7 +300,7 @@ class GalaFC:
     and returns the masked output ciphertexts plus the server's folded shares.
     """
 
-    def __init__(self, w, params: HEParams, pair_rows: bool = True):
+    def __init__(self, w, params: HEParams, pair_rows: bool = True, baby: int | None = None):
         self.params = params
         self.ctx = context(params)
         w = np.asarray(w, dtype=np.int64) % params.p
@@ -326,7 +326,7 @@ class GalaFC:
                 raise ParameterError("paired row blocks must share T")
             self.blocks.append([tasks, np.concatenate([s0, s1], axis=1), s0.shape[0]])
         self.T = self.blocks[0][2]
-        self.baby, self.steps = self.ctx.bsgs_steps(self.T)
+        self.baby, self.steps = self.ctx.bsgs_steps(self.T, baby)
         self.schedule = self.ctx.gala_schedule(self.T)
         for blk in self.blocks:    # resident encoded weights, in the layout of the chosen schedule
             blk[1] = (self.ctx.encode_gala_weights(blk[1], self.baby) if self.schedule == 2
