@@ -57,7 +57,7 @@ def fc(name, n, L, n_out, n_in, B):
                                       for m in masks]))
     pts = layer.blocks[0][1]
     outs, masked = ctx.empty_ct(B), ctx.empty_ct(B)
-    run = lambda: ctx.mv_gala_batch(cts, pts, layer.T, d_r, layer.baby, outs=outs, masked=masked)  # noqa: E731
+    run = lambda: layer.run_batch(cts, pts, d_r, outs=outs, masked=masked)  # noqa: E731
     ms = timeit(run)
     ctx.profile(True)
     run()
@@ -65,7 +65,8 @@ def fc(name, n, L, n_out, n_in, B):
     ctx.profile(False)
     ok = all(np.array_equal((layer.client_shares([masked[b]]) + layer.server_shares(masks[b])) % P,
                             dot_mod_p(w, xs[b], P)) for b in range(min(B, 2)))
-    return {"config": name, "N": ctx.N, "L": ctx.L, "T": layer.T, "batch": B, "ms_per_layer": ms / B,
+    return {"config": name, "N": ctx.N, "L": ctx.L, "T": layer.T, "schedule": layer.schedule, "batch": B,
+            "ms_per_layer": ms / B,
             "layers_per_s": 1e3 * B / ms, "correct": ok,
             "breakdown_ms_per_layer": {k: round(v["ms"] / B, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
 

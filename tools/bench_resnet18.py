@@ -49,14 +49,18 @@ def main():
             run = lambda: layer.forward_device(enc)  # noqa: E731
         out = run()
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        out = run()
-        b.record()
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b)
+        reps = []
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            out = run()
+            b.record()
+            torch.cuda.synchronize()
+            reps.append(a.elapsed_time(b))
+        ms = float(np.median(reps))
         total_ms += ms
         res = {"layer": spec.name, "shape": [spec.c_in, spec.c_out, spec.k, spec.stride, spec.size], "ms": round(ms, 3),
+               "ms_reps": [round(v, 3) for v in reps],
                "plaintext_GB": round(layer.plaintext_bytes / 1e9, 3)}
         if spec.kind == "conv":
             res.update(frame=layer.frame, c_n=layer.kg.c_n, tiles=layer.tiles ** 2)
