@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=8, help="independent layers (inputs) per step per GPU")
+    ap.add_argument("--batch", type=int, default=32, help="independent layers (inputs) per step per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--baby", type=int, default=0, help="BSGS baby-step count (0: library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

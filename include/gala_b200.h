@@ -131,6 +131,19 @@ int gala_conv_kg(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_
 int gala_kg_encode_weights(gala_ctx *ctx, const int32_t *kernels_dev, int c_o, int c_i, int k_h, int k_w, int u_w,
                            int u_h, int pair, uint64_t *pts_dev);
 
+/* Kernel grouping, schedule 2 (factored plaintexts; same outputs as gala_conv_kg up to the
+ * exact integer evaluation order -- oracle o_conv_kg2).  The KG plaintexts of
+ * coef_vectors (conv.py:220-235) factor into 0/1 band masks times one kernel coefficient each.
+ * gala_kg2_encode_masks: masks_dev [k_h k_w][pair c_n][L][N] (NTT, Montgomery).
+ * gala_conv_kg2: coef_dev int8 [Mr][Kp] (Mr = n_obp c_n rows (o, d); K = (ib, tap, beta)
+ * columns, zero-padded to Kp % 16 == 0; entry = centred kernel coefficient
+ * kern[pair o + row][ib c_n + ch][tap] of band beta = row c_n + ch at rotation offset d),
+ * rowsum_dev int32 [Mr] = row sums of coef; outs_dev [n_obp][2][L][N]. */
+int gala_kg2_encode_masks(gala_ctx *ctx, int k_h, int k_w, int u_w, int u_h, int pair, uint64_t *masks_dev);
+int gala_conv_kg2(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *masks_dev, int k, int nb,
+                  const int8_t *coef_dev, const int32_t *rowsum_dev, int Mr, int Kp, const int *tap_steps_host,
+                  int band_step, int c_n, uint64_t *outs_dev);
+
 /* canonical word import/export of `count` ciphertexts */
 int gala_ct_export(gala_ctx *ctx, const uint64_t *ct_dev, uint64_t *coef_dev, int count);
 int gala_ct_import(gala_ctx *ctx, const uint64_t *coef_dev, uint64_t *ct_dev, int count);

@@ -908,6 +908,106 @@ int o_conv_kg(void *h, const u64 *cts, int n_ib, const uint32_t *pts, int n_obp,
     return rc;
 }
 
+/*
+ * Kernel-grouping convolution, schedule 2 (factored plaintexts; used for L >= 2 and int8 kernels).
+ * Every KG plaintext is sum over bands beta of coef * M_{tap,beta}, with M_{tap,beta} the 0/1 mask of
+ * band beta's valid pixels for the tap (conv.py:220-235).  So
+ *   Y[ib][tap][beta] = R[ib][tap] (.) encode(M_{tap,beta})
+ *   acc[o][d]        = sum_{ib,tap,beta} c(o,d,ib,tap,beta) * Y[ib][tap][beta]   (integer scalars, mod q)
+ *   out[o]           = sum_d rot_{d B}(acc[o][d])                                (lazy ModDown, as o_conv_kg)
+ * c = kern[ob c_n + (ch - d) mod c_n][ib c_n + ch][tap] (centred integers), ob = pair*o + row.
+ * Bands: pair == 2 -> beta = row * c_n + ch (rows hold output blocks 2o, 2o+1); pair == 1 -> beta = ch
+ * over both rows.  kern: int32 [c_o][c_i][k_h][k_w] centred.
+ */
+int o_conv_kg2(void *h, const u64 *cts, int n_ib, const int32_t *kern, int c_o, int c_i, int k_h, int k_w,
+               int u_w, int u_h, int pair, u64 *outs)
+{
+    octx *c = h;
+    int N = c->N, L = c->L, M = c->M, n = N / 2;
+    size_t W = 2 * (size_t)L * N;
+    int B = u_w * u_h;
+    if (B <= 0 || n % B || (pair != 1 && pair != 2)) return -4;
+    int c_n = n / B, n_ob = c_o / c_n, n_obp = (n_ob + pair - 1) / pair, k = k_h * k_w;
+    int nb = pair * c_n;
+    int *tap_steps = malloc(sizeof(int) * (size_t)k);
+    for (int t = 0; t < k; t++) {
+        int dh = t / k_w - k_h / 2, dw = t % k_w - k_w / 2;
+        tap_steps[t] = (((dh * u_w + dw) % n) + n) % n;
+    }
+    /* 1. input rotations (DecPerm once per input, HstPerm per tap, ModDown each) */
+    u64 *R = malloc(sizeof(u64) * W * (size_t)n_ib * k);
+    int rc = 0;
+    int *rcs = calloc((size_t)n_ib, sizeof(int));
+#pragma omp parallel for schedule(dynamic)
+    for (int ib = 0; ib < n_ib; ib++) {
+        u64 *ctn = malloc(sizeof(u64) * W);
+        u64 *D = malloc(sizeof(u64) * (size_t)L * M * N);
+        ct_to_ntt(c, cts + (size_t)ib * W, ctn);
+        decompose(c, ctn + (size_t)L * N, D);
+        for (int t = 0; t < k && !rcs[ib]; t++)
+            rcs[ib] = rotate_from_digits(c, ctn, D, tap_steps[t], R + ((size_t)ib * k + t) * W);
+        free(ctn); free(D);
+    }
+    for (int ib = 0; ib < n_ib; ib++) if (rcs[ib]) rc = rcs[ib];
+    free(rcs);
+    if (rc) { free(R); free(tap_steps); return rc; }
+    /* 2. band masks, encoded: Mk[tap][beta] NTT [L][N] */
+    u64 *Mk = malloc(sizeof(u64) * (size_t)L * N * (size_t)k * nb);
+#pragma omp parallel for collapse(2)
+    for (int t = 0; t < k; t++)
+        for (int beta = 0; beta < nb; beta++) {
+            uint32_t *sl = malloc(sizeof(uint32_t) * N);
+            int dh = t / k_w - k_h / 2, dw = t % k_w - k_w / 2;
+            for (int s = 0; s < N; s++) {
+                int row = s / n, cs = s % n, ch = cs / B, pos = cs % B, y = pos / u_w, x = pos % u_w;
+                int band = pair == 2 ? row * c_n + ch : ch;
+                int ok = x + dw >= 0 && x + dw < u_w && y + dh >= 0 && y + dh < u_h;
+                sl[s] = (uint32_t)(band == beta && ok);
+            }
+            encode_pt_ntt(c, sl, Mk + ((size_t)t * nb + beta) * L * N);
+            free(sl);
+        }
+    /* 3.+4. Y and the integer-coefficient first-Add */
+    u64 *acc = calloc(W * (size_t)n_obp * c_n, sizeof(u64));
+    u64 *Y = malloc(sizeof(u64) * W * (size_t)n_ib * k * nb);
+#pragma omp parallel for collapse(3)
+    for (int ib = 0; ib < n_ib; ib++)
+        for (int t = 0; t < k; t++)
+            for (int beta = 0; beta < nb; beta++)
+                scmult_ntt(c, R + ((size_t)ib * k + t) * W, Mk + ((size_t)t * nb + beta) * L * N,
+                           Y + (((size_t)ib * k + t) * nb + beta) * W);
+#pragma omp parallel for collapse(2) schedule(dynamic)
+    for (int o = 0; o < n_obp; o++)
+        for (int d = 0; d < c_n; d++) {
+            u64 *A = acc + ((size_t)o * c_n + d) * W;
+            for (int ib = 0; ib < n_ib; ib++)
+                for (int t = 0; t < k; t++)
+                    for (int beta = 0; beta < nb; beta++) {
+                        int row = pair == 2 ? beta / c_n : 0, ch = beta % c_n;
+                        int ob = pair * o + row;
+                        if (ob >= n_ob) continue;
+                        int oo = ob * c_n + ((ch - d) % c_n + c_n) % c_n, ii = ib * c_n + ch;
+                        int32_t cf = kern[(((size_t)oo * c_i + ii) * k_h + t / k_w) * k_w + t % k_w];
+                        if (!cf) continue;
+                        const u64 *Yv = Y + (((size_t)ib * k + t) * nb + beta) * W;
+                        for (size_t i2 = 0; i2 < W; i2++) {
+                            u64 q = c->t[(i2 / N) % L].q;
+                            A[i2] = addmod(A[i2], mulmod(from_signed(cf, q), Yv[i2], q), q);
+                        }
+                    }
+        }
+    /* 5. second-Perm with one lazy ModDown per output */
+    int *steps = malloc(sizeof(int) * (size_t)c_n);
+    for (int d = 0; d < c_n; d++) steps[d] = d * B;
+    u64 *res = malloc(sizeof(u64) * W);
+    for (int o = 0; o < n_obp && !rc; o++) {
+        rc = rotate_sum_lazy(c, acc + (size_t)o * c_n * W, steps, c_n, res);
+        if (!rc) ct_from_ntt(c, res, outs + (size_t)o * W);
+    }
+    free(R); free(Mk); free(acc); free(Y); free(steps); free(res); free(tap_steps);
+    return rc;
+}
+
 /* test hooks: raw NTT on a single modulus (idx < 0: plaintext modulus) */
 void o_ntt(void *h, int idx, u64 *a, int inverse)
 {

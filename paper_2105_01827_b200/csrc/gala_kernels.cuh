@@ -655,6 +655,81 @@ __global__ void k_kg_slots(DevCtx c, const int32_t* __restrict__ kern, KgGeom g,
 }
 
 // ---------------------------------------------------------------------------
+// Kernel-grouping schedule 2 (factored plaintexts; oracle o_conv_kg2).
+// Band masks: slot s of mask (tap, beta) is 1 iff s lies in band beta and the tap's source pixel is
+// inside the image.  pair == 2: beta = row * c_n + ch; pair == 1: beta = ch over both rows.
+__global__ void k_kg_mask_slots(DevCtx c, KgGeom g, uint32_t* __restrict__ out)
+{
+    const int N = c.N, n = N / 2, B = g.u_w * g.u_h, k = g.k_h * g.k_w;
+    const int nb = g.pair * g.c_n;
+    const long long total = (long long)k * nb * N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int s = (int)(e % N);
+        const long long tb = e / N;
+        const int beta = (int)(tb % nb), tap = (int)(tb / nb);
+        const int row = s / n, cs = s % n, ch = cs / B, pos = cs % B, y = pos / g.u_w, x = pos % g.u_w;
+        const int band = g.pair == 2 ? row * g.c_n + ch : ch;
+        const int dh = tap / g.k_w - g.k_h / 2, dw = tap % g.k_w - g.k_w / 2;
+        const bool ok = x + dw >= 0 && x + dw < g.u_w && y + dh >= 0 && y + dh < g.u_h;
+        out[e] = (band == beta && ok) ? 1u : 0u;
+    }
+}
+
+// Y[K][pos] = R[ib][tap][pos] (.) Mask[tap][beta][pos mod LN], K = (ib, tap, beta), written as the 8
+// little-endian bytes of each word, biased by 0x80 (signed int8 for the tensor-core GEMM), in the
+// K-contiguous layout Bt[8 pos + b][Kp] (K padded to Kp; padding bytes = 0x80 i.e. value 0 after
+// the bias correction, multiplied by zero coefficients anyway).  Threads run fastest along K.
+__global__ void k_kg_y(DevCtx c, const u64* __restrict__ R, const u64* __restrict__ masks, int k, int nb, int n_ib,
+                       int Kp, int8_t* __restrict__ Bt)
+{
+    const long long LN = (long long)c.L * c.N, P = 2 * LN;
+    const long long total = P * Kp;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int K = (int)(e % Kp);
+        const long long pos = e / Kp;
+        u64 v = 0;
+        if (K < n_ib * k * nb) {
+            const int beta = K % nb, tap = (K / nb) % k, ib = K / (nb * k);
+            const long long jl = pos % LN;
+            const int j = (int)(jl / c.N);
+            v = mont_mul(__ldg(R + ((long long)ib * k + tap) * P + pos), __ldg(masks + ((long long)tap * nb + beta) * LN + jl),
+                         c.mod[j]);
+        }
+        v ^= 0x8080808080808080ull;
+        int8_t* o = Bt + pos * 8 * Kp + K;
+#pragma unroll
+        for (int b = 0; b < 8; b++) o[(long long)b * Kp] = (int8_t)(uint8_t)(v >> (8 * b));
+    }
+}
+
+// acc[m][pos] = (sum_b (C[8 pos + b][m] + 128 rowsum[m]) 256^b) mod q_j.  C is the int32 GEMM output
+// (column-major [Mr][8P]).  The signed 128-bit total is made non-negative with a multiple of q
+// (off[j] >= 2^84) and reduced exactly with two Montgomery steps.
+__global__ void k_kg_recombine(DevCtx c, const int32_t* __restrict__ C, const int32_t* __restrict__ rowsum, int Mr,
+                               const ulonglong2* __restrict__ off, u64* __restrict__ acc)
+{
+    const long long LN = (long long)c.L * c.N, P = 2 * LN;
+    const long long total = P * Mr;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int m = (int)(e % Mr);
+        const long long pos = e / Mr;
+        const int j = (int)((pos % LN) / c.N);
+        const long long bias = 128LL * rowsum[m];
+        __int128 t = 0;
+#pragma unroll
+        for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)C[(8 * pos + b) * Mr + m] + bias);
+        const ulonglong2 o = off[j];
+        unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
+        const ModC md = c.mod[j];
+        const u64 r = csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q);   // u 2^-64 mod q
+        acc[(long long)m * P + pos] = mont_mul(r, md.r2, md);               // * 2^64 -> u mod q
+    }
+}
+
+// ---------------------------------------------------------------------------
 // encoding.  MODE 0: plaintext operand (centred lift, Montgomery);
 //            MODE 1: Delta * m (plain), for encrypt / subtract_plain
 // one CTA per (vector b, prime j); each CTA recomputes the mod-p INTT (cheap,

@@ -4,6 +4,7 @@
 // Every schedule here mirrors the CPU oracle (oracle/bfv_oracle.c) operation
 // for operation, so ciphertext words agree exactly.  See include/gala_b200.h.
 #include <cuda_runtime.h>
+#include <cublasLt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -129,6 +130,8 @@ struct gala_ctx {
     };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
+    cublasLtHandle_t lt = nullptr;            // int8 tensor-core GEMM of the conv schedule 2 first-Add
+    u64* d_kg_off = nullptr;                  // per prime: multiple of q >= 2^90 (128-bit, hi/lo)
 };
 
 static void prof_begin(gala_ctx* c, cudaEvent_t* a, cudaEvent_t* b)
@@ -495,6 +498,8 @@ static void free_ctx(gala_ctx* c)
         cudaEventDestroy(r.b);
     }
     for (auto e : c->pool) cudaEventDestroy(e);
+    if (c->lt) cublasLtDestroy(c->lt);
+    if (c->d_kg_off) cudaFree(c->d_kg_off);
     delete c;
 }
 
@@ -1208,6 +1213,176 @@ int gala_kg_encode_weights(gala_ctx* c, const int32_t* kern, int c_o, int c_i, i
         RET(gala_encode_plain(c, slots, cnt, pts + first * L * N));
     }
     release(c, slots);
+    return GALA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel grouping, schedule 2 (factored plaintexts).  Every KG plaintext is a sum over the c_n
+// bands of a 0/1 band mask times one kernel coefficient, so
+//   acc[o][d] = sum_{ib, tap, beta} A[(o, d)][(ib, tap, beta)] * (R[ib][tap] (.) Mask[tap][beta])
+// with small signed integer A.  The masked products Y are split into bytes and the contraction over
+// K = (ib, tap, beta) runs as an int8 tensor-core GEMM (cuBLASLt, exact int32 accumulation); a
+// recombination kernel rebuilds each word mod q exactly.  Oracle: o_conv_kg2.
+
+int gala_kg2_encode_masks(gala_ctx* c, int k_h, int k_w, int u_w, int u_h, int pair, uint64_t* masks)
+{
+    const int N = c->dc.N, L = c->dc.L, n = N / 2;
+    const int B = u_w * u_h;
+    if (B <= 0 || n % B || (k_h % 2) == 0 || (k_w % 2) == 0 || (pair != 1 && pair != 2))
+        return set_err(GALA_ERR_PARAM, "bad kernel-grouping geometry");
+    KgGeom g{};
+    g.k_h = k_h;
+    g.k_w = k_w;
+    g.u_w = u_w;
+    g.u_h = u_h;
+    g.c_n = n / B;
+    g.pair = pair;
+    const int count = k_h * k_w * pair * g.c_n;
+    uint32_t* slots;
+    RET(scratch(c, &slots, (size_t)count * N));
+    KLAUNCH(c, "k_kg_mask_slots", k_kg_mask_slots<<<grid_for((long long)count * N, 256), 256, 0, c->stream>>>(c->dc, g, slots));
+    for (int first = 0; first < count; first += 4096) {
+        const int cnt = count - first < 4096 ? count - first : 4096;
+        RET(gala_encode_plain(c, slots + (long long)first * N, cnt, masks + (long long)first * L * N));
+    }
+    release(c, slots);
+    return GALA_OK;
+}
+
+static int lt_gemm_i8(gala_ctx* c, const int8_t* A, int lda, const int8_t* Bm, int ldb, int32_t* C, int ldc, int m,
+                      long long n, int k, int beta)
+{
+    // C[m x n] (column-major, int32) = A^T B (+ C), A column-major [k x m], B column-major [k x n]
+    if (!c->lt && cublasLtCreate(&c->lt) != CUBLAS_STATUS_SUCCESS) return set_err(GALA_ERR_CUDA, "cublasLtCreate failed");
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+    cublasLtMatmulPreference_t pref = nullptr;
+    const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+    const int32_t alpha = 1, bet = beta;
+    const size_t ws_bytes = 32u << 20;
+    void* ws = nullptr;
+    int rc = GALA_OK;
+    cublasLtMatmulHeuristicResult_t heur{};
+    int found = 0;
+    cublasStatus_t st = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I);
+    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
+    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
+    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, k, m, lda);
+    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, k, n, ldb);
+    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32I, m, n, ldc);
+    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulPreferenceCreate(&pref);
+    if (st == CUBLAS_STATUS_SUCCESS)
+        st = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes, sizeof(ws_bytes));
+    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulAlgoGetHeuristic(c->lt, op, la, lb, lc, lc, pref, 1, &heur, &found);
+    if (st != CUBLAS_STATUS_SUCCESS || found == 0) {
+        rc = set_err(GALA_ERR_CUDA, "cuBLASLt int8 GEMM setup failed (status %d, %d algos)", (int)st, found);
+    } else {
+        rc = scratch(c, (char**)&ws, heur.workspaceSize ? heur.workspaceSize : 8);
+        if (rc == GALA_OK) {
+            if (c->prof_on) {
+                cudaEvent_t a, b;
+                prof_begin(c, &a, &b);
+                st = cublasLtMatmul(c->lt, op, &alpha, A, la, Bm, lb, &bet, C, lc, C, lc, &heur.algo, ws, heur.workspaceSize,
+                                    c->stream);
+                prof_end(c, "cublasLt_i8_gemm", a, b);
+            } else {
+                st = cublasLtMatmul(c->lt, op, &alpha, A, la, Bm, lb, &bet, C, lc, C, lc, &heur.algo, ws, heur.workspaceSize,
+                                    c->stream);
+            }
+            if (st != CUBLAS_STATUS_SUCCESS) rc = set_err(GALA_ERR_CUDA, "cublasLtMatmul failed (status %d)", (int)st);
+            release(c, ws);
+        }
+    }
+    if (pref) cublasLtMatmulPreferenceDestroy(pref);
+    if (lc) cublasLtMatrixLayoutDestroy(lc);
+    if (lb) cublasLtMatrixLayoutDestroy(lb);
+    if (la) cublasLtMatrixLayoutDestroy(la);
+    if (op) cublasLtMatmulDescDestroy(op);
+    return rc;
+}
+
+static unsigned __int128 kg_offset(u64 q)
+{
+    const unsigned __int128 two90 = (unsigned __int128)1 << 90;
+    return (two90 / q + 1) * q;
+}
+
+int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* masks, int k, int nb,
+                  const int8_t* coef, const int32_t* rowsum, int Mr, int Kp, const int* tap_steps, int band_step,
+                  int c_n, uint64_t* outs)
+{
+    const int N = c->dc.N, L = c->dc.L;
+    const long long W = 2LL * L * N;
+    if (n_ib <= 0 || k <= 0 || nb <= 0 || c_n <= 0 || Mr <= 0 || Mr % c_n) return set_err(GALA_ERR_DIM, "bad schedule-2 dims");
+    if (Kp % 16 || Kp < n_ib * k * nb) return set_err(GALA_ERR_DIM, "Kp=%d must be a multiple of 16 covering K=%d", Kp,
+                                                    n_ib * k * nb);
+    if (Kp > (1 << 17)) return set_err(GALA_ERR_DIM, "K too large for exact int32 accumulation");
+    std::vector<int> rot_taps;
+    for (int t = 0; t < k; t++) {
+        int s = norm_step(c, tap_steps[t]);
+        if (s != 0) {
+            if (!key_for(c, s)) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", s);
+            rot_taps.push_back(t);
+        }
+    }
+    for (int d = 1; d < c_n; d++)
+        if (!gala_has_rotation_key(c, d * band_step))
+            return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, d * band_step));
+    if (!c->d_kg_off) {
+        std::vector<u64> off(2 * GALA_MAXM, 0);
+        for (int j = 0; j < L; j++) {
+            unsigned __int128 o = kg_offset(c->primes[j]);
+            off[2 * j] = (u64)(o >> 64);
+            off[2 * j + 1] = (u64)o;
+        }
+        CK(cudaMalloc(&c->d_kg_off, sizeof(u64) * off.size()));
+        CK(cudaMemcpy(c->d_kg_off, off.data(), sizeof(u64) * off.size(), cudaMemcpyHostToDevice));
+    }
+    // 1. input rotations R[ib][tap] (hoisted: one decomposition per input)
+    u64* R;
+    RET(scratch(c, &R, (size_t)n_ib * k * W));
+    for (int ib = 0; ib < n_ib; ib++)
+        for (int t = 0; t < k; t++)
+            if (norm_step(c, tap_steps[t]) == 0)
+                CK(cudaMemcpyAsync(R + ((long long)ib * k + t) * W, cts + (long long)ib * W, sizeof(u64) * W,
+                                   cudaMemcpyDeviceToDevice, c->stream));
+    if (!rot_taps.empty()) {
+        std::vector<EngTerm> terms;
+        std::vector<std::vector<EngMember>> groups;
+        std::vector<u64*> routs;
+        for (int ib = 0; ib < n_ib; ib++) {
+            EngTerm t;
+            t.X = cts + (long long)ib * W;
+            t.pt = nullptr;
+            t.ntt_block = nullptr;
+            for (int tap : rot_taps) t.steps.push_back(norm_step(c, tap_steps[tap]));
+            terms.push_back(t);
+            for (size_t r = 0; r < rot_taps.size(); r++) {
+                groups.push_back({{ib, (int)r}});
+                routs.push_back(R + ((long long)ib * k + rot_taps[r]) * W);
+            }
+        }
+        RET(rotate_engine(c, terms, groups, routs));
+    }
+    // 2. masked products as biased bytes, K-contiguous: Bt[8 W][Kp]
+    int8_t* Bt;
+    int32_t* C;
+    RET(scratch(c, &Bt, (size_t)8 * W * Kp));
+    RET(scratch(c, &C, (size_t)8 * W * Mr));
+    KLAUNCH(c, "k_kg_y", k_kg_y<<<grid_for(W * Kp, 256), 256, 0, c->stream>>>(c->dc, R, masks, k, nb, n_ib, Kp, Bt));
+    release(c, R);
+    // 3. exact integer first-Add on the tensor cores: C[Mr][8 W] = A . Bt
+    RET(lt_gemm_i8(c, coef, Kp, Bt, Kp, C, Mr, Mr, 8 * W, Kp, 0));
+    release(c, Bt);
+    // 4. recombine bytes -> words mod q
+    u64* acc;
+    RET(scratch(c, &acc, (size_t)Mr * W));
+    KLAUNCH(c, "k_kg_recombine", k_kg_recombine<<<grid_for(W * Mr, 256), 256, 0, c->stream>>>(
+                                     c->dc, C, rowsum, Mr, (const ulonglong2*)c->d_kg_off, acc));
+    release(c, C);
+    // 5. second-Perm: out[o] = sum_d rot_{d * band}(acc[o][d]), one lazy ModDown per o
+    RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, Mr / c_n, c_n, band_step, outs, 0));
+    release(c, acc);
     return GALA_OK;
 }
 

@@ -136,3 +136,41 @@ def test_mv_gala2_words(tw, T):
         c_out, c_masked = tw.cpu.mv_gala(c, pts, rs[i], baby=b, schedule=2)
         assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
         assert np.array_equal(tw.gpu.export_words(masked[i]), c_masked)
+
+
+KG2_GEOM = {32: (4, 4), 256: (8, 8), 2048: (16, 16), 4096: (16, 16)}
+
+
+@pytest.mark.parametrize("pair", [1, 2])
+def test_conv_kg2_words(tw, pair):
+    """Schedule 2 (band masks x int8 coefficients on the tensor cores) == oracle o_conv_kg2, word for word,
+    and decrypts to the plaintext convolution when the noise budget allows (L >= 2)."""
+    import torch
+
+    from oracle.plain import conv2d_mod_p
+    from paper_2105_01827_b200.conv import ConvTask, kg2_coefficients
+
+    n = tw.bfv.n
+    if n not in KG2_GEOM:
+        pytest.skip("no geometry for this ring")
+    u_w, u_h = KG2_GEOM[n]
+    c_n = n // (u_w * u_h)
+    c_i, c_o = 2 * c_n, 3 * c_n
+    kern = tw.rng.integers(-128, 128, (c_o, c_i, 3, 3))
+    task = ConvTask(u_w, u_h, c_i, 3, 3, c_o, kern, tw.params)
+    taps = [rot for _, _, rot in task.offsets()]
+    tw.keys_for(taps + [d * u_w * u_h for d in range(1, c_n)])
+    x = tw.rng.integers(0, P, (c_i, u_h, u_w))
+    blocks = x.reshape(c_i // c_n, c_n * u_w * u_h)
+    xs = [tw.encrypt(np.concatenate([b, b]).astype(np.uint32)) for b in blocks]
+    A, rowsum, _ = kg2_coefficients(task, c_n, pair)
+    masks = tw.gpu.kg2_encode_masks(3, 3, u_w, u_h, pair)
+    g_out = tw.gpu.conv_kg2(torch.stack([g for g, _ in xs]), masks, torch.from_numpy(A).to(tw.gpu.device),
+                            torch.from_numpy(rowsum).to(tw.gpu.device), 9, pair * c_n, taps, u_w * u_h, c_n)
+    c_out = tw.cpu.conv_kg2(np.stack([c for _, c in xs]), kern, u_w, u_h, pair)
+    assert np.array_equal(tw.gpu.export_words(g_out), c_out)
+    if tw.L >= 2:
+        want = conv2d_mod_p(x, kern, P).reshape(c_o // c_n, c_n * u_w * u_h)
+        for ob in range(c_o // c_n):
+            got = tw.gpu.decrypt_physical(g_out[ob // pair]).reshape(2, -1)[ob % pair if pair == 2 else 0]
+            assert np.array_equal(got, want[ob])

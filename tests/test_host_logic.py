@@ -252,3 +252,50 @@ def test_fold_linearity():
         assert lhs == fold_ras(m, 8, 2)
     with pytest.raises(ParameterError):
         fold_ras(SlotVector(np.zeros(8), P), 16, 1)
+
+
+@pytest.mark.parametrize("n,u,c_o,c_i,pair", [(64, 4, 12, 8, 2), (64, 4, 8, 8, 1), (256, 16, 3, 2, 2)])
+def test_kg2_coefficients_factor_the_convolution(n, u, c_o, c_i, pair):
+    """Band masks x int8 coefficient matrix, evaluated on slot vectors, is the convolution (mod p)."""
+    from oracle.plain import conv2d_mod_p
+    from paper_2105_01827_b200.backend import HEParams
+    from paper_2105_01827_b200.conv import ConvTask, kg2_coefficients
+
+    P = 1032193
+    rng = np.random.default_rng(1)
+    kern = rng.integers(-128, 128, (c_o, c_i, 3, 3))
+    t = ConvTask(u, u, c_i, 3, 3, c_o, kern, HEParams(n=n, p=P))
+    c_n, B = n // (u * u), u * u
+    nb = pair * c_n
+    A, rowsum, K = kg2_coefficients(t, c_n, pair)
+    assert A.shape[1] % 16 == 0 and K == (c_i // c_n) * 9 * nb
+    assert np.array_equal(rowsum, A.astype(np.int64).sum(axis=1))
+    x = rng.integers(0, P, (c_i, u, u))
+    phys = [np.concatenate([b, b]) for b in x.reshape(c_i // c_n, -1)]
+
+    def rot(v, s):
+        return np.concatenate([np.roll(v[:n], -s), np.roll(v[n:], -s)])
+
+    s = np.arange(2 * n)
+    row, cs = s // n, s % n
+    ch, pos = cs // B, cs % B
+    yy, xx = pos // u, pos % u
+    band = row * c_n + ch if pair == 2 else ch
+    out = []
+    for o in range(A.shape[0] // c_n):
+        tot = np.zeros(2 * n, np.int64)
+        for d in range(c_n):
+            acc = np.zeros(2 * n, np.int64)
+            for ib, v in enumerate(phys):
+                for ti, (dw, dh, r) in enumerate(t.offsets()):
+                    R = rot(v, r)
+                    ok = (xx + dw >= 0) & (xx + dw < u) & (yy + dh >= 0) & (yy + dh < u)
+                    for beta in range(nb):
+                        m = ((band == beta) & ok).astype(np.int64)
+                        acc = (acc + int(A[o * c_n + d, (ib * 9 + ti) * nb + beta]) * R * m) % P
+            tot = (tot + rot(acc, d * B)) % P
+        out.append(tot)
+    want = conv2d_mod_p(x, kern, P).reshape(c_o // c_n, -1)
+    for ob in range(c_o // c_n):
+        r = ob % pair if pair == 2 else 0
+        assert np.array_equal(out[ob // pair][r * n:(r + 1) * n], want[ob])
