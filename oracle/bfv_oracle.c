@@ -919,40 +919,72 @@ int o_conv_kg(void *h, const u64 *cts, int n_ib, const uint32_t *pts, int n_obp,
  * Bands: pair == 2 -> beta = row * c_n + ch (rows hold output blocks 2o, 2o+1); pair == 1 -> beta = ch
  * over both rows.  kern: int32 [c_o][c_i][k_h][k_w] centred.
  */
+/*
+ * Kernel grouping, schedule 2 ("factored plaintexts", GPU gala_conv_kg2).  Every KG plaintext
+ * pt[ob][ib][d][tap] of o_conv_kg is a sum over bands beta of a 0/1 band mask Mask[tap][beta]
+ * times one kernel coefficient, so the first-Add becomes
+ *   acc[o][d] = sum_{ib, tap, beta} kern[(o, d), (ib, tap, beta)] * (Z[ib][tap] (.) Mask[tap][beta])
+ * with small signed integer coefficients (the GPU evaluates it as an int8 GEMM over byte limbs).
+ * The rotated inputs stay in the extended basis QP:  Z = KSraw(step, D) + P * sigma(c0)
+ * (Z = P * X for tap step 0), masks are encoded in all L+1 primes, and one ModDown per acc[o][d]
+ * replaces one per rotated input (ModDown(U + P V) = ModDown(U) + V exactly).  The second-Perm is
+ * the lazy rotate-and-sum of o_conv_kg.  pair == 2: band beta = row * c_n + ch (output block
+ * pair * o + row on hypercube row `row`); pair == 1: beta = ch over both rows.
+ * kern: centred int32 [c_o][c_i][k_h][k_w] (reference kernels, conv.py:220-235).
+ */
 int o_conv_kg2(void *h, const u64 *cts, int n_ib, const int32_t *kern, int c_o, int c_i, int k_h, int k_w,
                int u_w, int u_h, int pair, u64 *outs)
 {
     octx *c = h;
     int N = c->N, L = c->L, M = c->M, n = N / 2;
-    size_t W = 2 * (size_t)L * N;
+    size_t W = 2 * (size_t)L * N, WQ = 2 * (size_t)M * N, MN = (size_t)M * N;
     int B = u_w * u_h;
     if (B <= 0 || n % B || (pair != 1 && pair != 2)) return -4;
     int c_n = n / B, n_ob = c_o / c_n, n_obp = (n_ob + pair - 1) / pair, k = k_h * k_w;
     int nb = pair * c_n;
+    u64 P = c->t[L].q;
     int *tap_steps = malloc(sizeof(int) * (size_t)k);
     for (int t = 0; t < k; t++) {
         int dh = t / k_w - k_h / 2, dw = t % k_w - k_w / 2;
         tap_steps[t] = (((dh * u_w + dw) % n) + n) % n;
     }
-    /* 1. input rotations (DecPerm once per input, HstPerm per tap, ModDown each) */
-    u64 *R = malloc(sizeof(u64) * W * (size_t)n_ib * k);
+    /* 1. rotated inputs in QP: Z[ib][tap] [2][M][N] (DecPerm once per input, HstPerm per tap) */
+    u64 *Z = calloc(WQ * (size_t)n_ib * k, sizeof(u64));
     int rc = 0;
     int *rcs = calloc((size_t)n_ib, sizeof(int));
 #pragma omp parallel for schedule(dynamic)
     for (int ib = 0; ib < n_ib; ib++) {
-        u64 *ctn = malloc(sizeof(u64) * W);
+        u64 *ctn = malloc(sizeof(u64) * W), *sc0 = malloc(sizeof(u64) * (size_t)L * N);
         u64 *D = malloc(sizeof(u64) * (size_t)L * M * N);
         ct_to_ntt(c, cts + (size_t)ib * W, ctn);
         decompose(c, ctn + (size_t)L * N, D);
-        for (int t = 0; t < k && !rcs[ib]; t++)
-            rcs[ib] = rotate_from_digits(c, ctn, D, tap_steps[t], R + ((size_t)ib * k + t) * W);
-        free(ctn); free(D);
+        for (int t = 0; t < k && !rcs[ib]; t++) {
+            u64 *z = Z + ((size_t)ib * k + t) * WQ;
+            int s = tap_steps[t];
+            if (s == 0) {
+                for (int comp = 0; comp < 2; comp++)
+                    for (int j = 0; j < L; j++) {
+                        u64 q = c->t[j].q, Pq = P % q;
+                        for (int i = 0; i < N; i++)
+                            z[(comp * MN) + (size_t)j * N + i] = mulmod(ctn[((size_t)comp * L + j) * N + i], Pq, q);
+                    }
+                continue;
+            }
+            rcs[ib] = ks_accumulate(c, s, D, z);
+            automorph_ct(c, ctn, sc0, L, galois(s, N));
+            for (int j = 0; j < L; j++) {
+                u64 q = c->t[j].q, Pq = P % q;
+                for (int i = 0; i < N; i++)
+                    z[(size_t)j * N + i] = addmod(z[(size_t)j * N + i], mulmod(sc0[(size_t)j * N + i], Pq, q), q);
+            }
+        }
+        free(ctn); free(sc0); free(D);
     }
     for (int ib = 0; ib < n_ib; ib++) if (rcs[ib]) rc = rcs[ib];
     free(rcs);
-    if (rc) { free(R); free(tap_steps); return rc; }
-    /* 2. band masks, encoded: Mk[tap][beta] NTT [L][N] */
-    u64 *Mk = malloc(sizeof(u64) * (size_t)L * N * (size_t)k * nb);
+    if (rc) { free(Z); free(tap_steps); return rc; }
+    /* 2. band masks in all L+1 primes: Mk[tap][beta] NTT [M][N] */
+    u64 *Mk = malloc(sizeof(u64) * MN * (size_t)k * nb);
 #pragma omp parallel for collapse(2)
     for (int t = 0; t < k; t++)
         for (int beta = 0; beta < nb; beta++) {
@@ -964,22 +996,24 @@ int o_conv_kg2(void *h, const u64 *cts, int n_ib, const int32_t *kern, int c_o, 
                 int ok = x + dw >= 0 && x + dw < u_w && y + dh >= 0 && y + dh < u_h;
                 sl[s] = (uint32_t)(band == beta && ok);
             }
-            encode_pt_ntt(c, sl, Mk + ((size_t)t * nb + beta) * L * N);
+            encode_pt_ntt_qp(c, sl, Mk + ((size_t)t * nb + beta) * MN);
             free(sl);
         }
-    /* 3.+4. Y and the integer-coefficient first-Add */
-    u64 *acc = calloc(W * (size_t)n_obp * c_n, sizeof(u64));
-    u64 *Y = malloc(sizeof(u64) * W * (size_t)n_ib * k * nb);
+    /* 3. Y = Z (.) Mask and the integer-coefficient first-Add, in QP */
+    u64 *Y = malloc(sizeof(u64) * WQ * (size_t)n_ib * k * nb);
 #pragma omp parallel for collapse(3)
     for (int ib = 0; ib < n_ib; ib++)
         for (int t = 0; t < k; t++)
-            for (int beta = 0; beta < nb; beta++)
-                scmult_ntt(c, R + ((size_t)ib * k + t) * W, Mk + ((size_t)t * nb + beta) * L * N,
-                           Y + (((size_t)ib * k + t) * nb + beta) * W);
+            for (int beta = 0; beta < nb; beta++) {
+                const u64 *z = Z + ((size_t)ib * k + t) * WQ, *mk = Mk + ((size_t)t * nb + beta) * MN;
+                u64 *y = Y + (((size_t)ib * k + t) * nb + beta) * WQ;
+                for (size_t i2 = 0; i2 < WQ; i2++) y[i2] = mulmod(z[i2], mk[i2 % MN], c->t[(i2 / N) % M].q);
+            }
+    u64 *acc = malloc(sizeof(u64) * W * (size_t)n_obp * c_n);
 #pragma omp parallel for collapse(2) schedule(dynamic)
     for (int o = 0; o < n_obp; o++)
         for (int d = 0; d < c_n; d++) {
-            u64 *A = acc + ((size_t)o * c_n + d) * W;
+            u64 *A = calloc(WQ, sizeof(u64));
             for (int ib = 0; ib < n_ib; ib++)
                 for (int t = 0; t < k; t++)
                     for (int beta = 0; beta < nb; beta++) {
@@ -989,14 +1023,19 @@ int o_conv_kg2(void *h, const u64 *cts, int n_ib, const int32_t *kern, int c_o, 
                         int oo = ob * c_n + ((ch - d) % c_n + c_n) % c_n, ii = ib * c_n + ch;
                         int32_t cf = kern[(((size_t)oo * c_i + ii) * k_h + t / k_w) * k_w + t % k_w];
                         if (!cf) continue;
-                        const u64 *Yv = Y + (((size_t)ib * k + t) * nb + beta) * W;
-                        for (size_t i2 = 0; i2 < W; i2++) {
-                            u64 q = c->t[(i2 / N) % L].q;
+                        const u64 *Yv = Y + (((size_t)ib * k + t) * nb + beta) * WQ;
+                        for (size_t i2 = 0; i2 < WQ; i2++) {
+                            u64 q = c->t[(i2 / N) % M].q;
                             A[i2] = addmod(A[i2], mulmod(from_signed(cf, q), Yv[i2], q), q);
                         }
                     }
+            /* one ModDown per accumulator */
+            u64 *dst = acc + ((size_t)o * c_n + d) * W;
+            moddown(c, A, dst);
+            moddown(c, A + MN, dst + (size_t)L * N);
+            free(A);
         }
-    /* 5. second-Perm with one lazy ModDown per output */
+    /* 4. second-Perm with one lazy ModDown per output */
     int *steps = malloc(sizeof(int) * (size_t)c_n);
     for (int d = 0; d < c_n; d++) steps[d] = d * B;
     u64 *res = malloc(sizeof(u64) * W);
@@ -1004,7 +1043,7 @@ int o_conv_kg2(void *h, const u64 *cts, int n_ib, const int32_t *kern, int c_o, 
         rc = rotate_sum_lazy(c, acc + (size_t)o * c_n * W, steps, c_n, res);
         if (!rc) ct_from_ntt(c, res, outs + (size_t)o * W);
     }
-    free(R); free(Mk); free(acc); free(Y); free(steps); free(res); free(tap_steps);
+    free(Z); free(Mk); free(acc); free(Y); free(steps); free(res); free(tap_steps);
     return rc;
 }
 

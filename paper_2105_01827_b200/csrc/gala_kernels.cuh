@@ -676,51 +676,83 @@ __global__ void k_kg_mask_slots(DevCtx c, KgGeom g, uint32_t* __restrict__ out)
     }
 }
 
-// Y[K][pos] = R[ib][tap][pos] (.) Mask[tap][beta][pos mod LN], K = (ib, tap, beta), written as the 8
-// little-endian bytes of each word, biased by 0x80 (signed int8 for the tensor-core GEMM), in the
-// K-contiguous layout Bt[8 pos + b][Kp] (K padded to Kp; padding bytes = 0x80 i.e. value 0 after
-// the bias correction, multiplied by zero coefficients anyway).  Threads run fastest along K.
-__global__ void k_kg_y(DevCtx c, const u64* __restrict__ R, const u64* __restrict__ masks, int k, int nb, int n_ib,
-                       int Kp, int8_t* __restrict__ Bt)
+// Masked products of the extended-basis rotated inputs, K = (ib, tap, beta), pos = (comp, j, i):
+//   Y[K][pos] = (U[g][pos] + P Cacc[g][comp][j][i]) (.) Mask[tap][beta][j][i],  g = ib k + tap
+// (Cacc term only for j < L), written as the 8 little-endian bytes of each word biased by 0x80
+// (signed int8 for the tensor-core GEMM) in the K-contiguous layout Bt[8 pos + b][Kp].  One CTA
+// transposes a KG_PT x KG_KT tile through shared memory: loads run along pos (coalesced), the
+// 16-byte stores along K.  The XOR swizzle keeps both phases at the 2-wavefront minimum.
+#define KG_PT 32
+#define KG_KT 128
+__device__ __forceinline__ int kg_swz(int pp, int kk) { return pp * KG_KT + (kk ^ ((pp + 4 * (kk >> 4)) & 15)); }
+
+__global__ void __launch_bounds__(256) k_kg_y(DevCtx c, const u64* __restrict__ U, const u64* __restrict__ Cacc,
+                                              const u64* __restrict__ masks, const u64* __restrict__ pmont, int k, int nb,
+                                              int n_ib, int Kp, int8_t* __restrict__ Bt)
 {
-    const long long LN = (long long)c.L * c.N, P = 2 * LN;
-    const long long total = P * Kp;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int K = (int)(e % Kp);
-        const long long pos = e / Kp;
+    __shared__ u64 sm[KG_PT * KG_KT];
+    const int N = c.N, L = c.L, M = c.M;
+    const long long MN = (long long)M * N, P = 2 * MN;
+    const long long pos0 = (long long)blockIdx.x * KG_PT;
+    const int K0 = blockIdx.y * KG_KT, Kreal = n_ib * k * nb;
+    for (int idx = threadIdx.x; idx < KG_PT * KG_KT; idx += blockDim.x) {
+        const int kk = idx / KG_PT, pp = idx % KG_PT;
+        const int K = K0 + kk;
+        const long long pos = pos0 + pp;
         u64 v = 0;
-        if (K < n_ib * k * nb) {
+        if (K < Kreal && pos < P) {
             const int beta = K % nb, tap = (K / nb) % k, ib = K / (nb * k);
-            const long long jl = pos % LN;
-            const int j = (int)(jl / c.N);
-            v = mont_mul(__ldg(R + ((long long)ib * k + tap) * P + pos), __ldg(masks + ((long long)tap * nb + beta) * LN + jl),
-                         c.mod[j]);
+            const long long g = (long long)ib * k + tap;
+            const int comp = (int)(pos / MN);
+            const long long jl = pos - comp * MN;
+            const int j = (int)(jl / N);
+            const ModC md = c.mod[j];
+            u64 z = __ldg(U + g * P + pos);
+            if (j < L) z = add_mod(z, mont_mul(__ldg(Cacc + (g * 2 + comp) * L * N + jl), pmont[j], md), md.q);
+            v = mont_mul(z, __ldg(masks + ((long long)tap * nb + beta) * MN + jl), md);
         }
-        v ^= 0x8080808080808080ull;
-        int8_t* o = Bt + pos * 8 * Kp + K;
+        sm[kg_swz(pp, kk)] = v ^ 0x8080808080808080ull;
+    }
+    __syncthreads();
+    const int pp = threadIdx.x >> 3, ch = threadIdx.x & 7;
+    const long long pos = pos0 + pp;
+    if (K0 + ch * 16 >= Kp || pos >= P) return;
+    u64 w[16];
 #pragma unroll
-        for (int b = 0; b < 8; b++) o[(long long)b * Kp] = (int8_t)(uint8_t)(v >> (8 * b));
+    for (int i = 0; i < 16; i++) w[i] = sm[kg_swz(pp, ch * 16 + i)];
+    int8_t* o = Bt + pos * 8 * Kp + K0 + ch * 16;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        uint32_t x[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; q4++) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int t = 0; t < 4; t++) r |= (uint32_t)((w[q4 * 4 + t] >> (8 * b)) & 0xff) << (8 * t);
+            x[q4] = r;
+        }
+        *(uint4*)(o + (long long)b * Kp) = make_uint4(x[0], x[1], x[2], x[3]);
     }
 }
 
-// acc[m][pos] = (sum_b (C[8 pos + b][m] + 128 rowsum[m]) 256^b) mod q_j.  C is the int32 GEMM output
-// (column-major [Mr][8P]).  The signed 128-bit total is made non-negative with a multiple of q
-// (off[j] >= 2^84) and reduced exactly with two Montgomery steps.
+// acc[m][pos] = (sum_b (C[8 pos + b][m] + 128 rowsum[m]) 256^b) mod q_j over the extended basis
+// (pos = (comp, j, i), j < M).  C is the int32 GEMM output (column-major [Mp][8P]).  The signed
+// 128-bit total is made non-negative with a multiple of q (off[j] >= 2^90) and reduced exactly with
+// two Montgomery steps.
 __global__ void k_kg_recombine(DevCtx c, const int32_t* __restrict__ C, const int32_t* __restrict__ rowsum, int Mr,
-                               const ulonglong2* __restrict__ off, u64* __restrict__ acc)
+                               int Mp, const ulonglong2* __restrict__ off, u64* __restrict__ acc)
 {
-    const long long LN = (long long)c.L * c.N, P = 2 * LN;
+    const long long MN = (long long)c.M * c.N, P = 2 * MN;
     const long long total = P * Mr;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
          e += (long long)gridDim.x * blockDim.x) {
         const int m = (int)(e % Mr);
         const long long pos = e / Mr;
-        const int j = (int)((pos % LN) / c.N);
+        const int j = (int)((pos % MN) / c.N);
         const long long bias = 128LL * rowsum[m];
         __int128 t = 0;
 #pragma unroll
-        for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)C[(8 * pos + b) * Mr + m] + bias);
+        for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)C[(8 * pos + b) * Mp + m] + bias);
         const ulonglong2 o = off[j];
         unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
         const ModC md = c.mod[j];

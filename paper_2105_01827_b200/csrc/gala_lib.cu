@@ -252,8 +252,17 @@ struct EngMember {
 
 static const u64* key_for(gala_ctx* c, int step);
 
+// raw != nullptr: skip the ModDown and hand back the extended-basis sums (caller releases):
+// U [G][2][M][N] key products, Cacc [G][2][L][N] plain sums; the group's rotated ciphertext is
+// ModDown(U) + Cacc = ModDown(U + P Cacc).
+struct EngRaw {
+    u64* U = nullptr;
+    u64* Cacc = nullptr;
+};
+
 static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
-                         const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs)
+                         const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs,
+                         EngRaw* raw = nullptr)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const int G = (int)groups.size();
@@ -349,10 +358,10 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
                                                   c->stream>>>(c->dc, (const TermDesc*)(d_blob + o_th),
                                                                (const unsigned*)(d_blob + o_gal), blk_words));
     }
-    u64 *U, *Cacc, *r;
+    u64 *U, *Cacc, *r = nullptr;
     RET(scratch(c, &U, (size_t)G * 2 * M * N));
     RET(scratch(c, &Cacc, (size_t)G * 2 * L * N));
-    RET(scratch(c, &r, (size_t)G * 2 * N));
+    if (!raw) RET(scratch(c, &r, (size_t)G * 2 * N));
     const int th = N < 256 ? N : 256;
     dim3 grid((N + th - 1) / th, M, G);
     {
@@ -364,6 +373,14 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
             case 3: KLAUNCH(c, "k_ks_mac", k_ks_mac<3><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
             default: KLAUNCH(c, "k_ks_mac", k_ks_mac<4><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
         }
+    }
+    if (raw) {
+        raw->U = U;
+        raw->Cacc = Cacc;
+        release(c, dig);
+        release(c, blk);
+        release(c, d_blob);
+        return GALA_OK;
     }
     RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
@@ -1241,11 +1258,14 @@ int gala_kg2_encode_masks(gala_ctx* c, int k_h, int k_w, int u_w, int u_h, int p
     uint32_t* slots;
     RET(scratch(c, &slots, (size_t)count * N));
     KLAUNCH(c, "k_kg_mask_slots", k_kg_mask_slots<<<grid_for((long long)count * N, 256), 256, 0, c->stream>>>(c->dc, g, slots));
+    const int M = c->dc.M;
     for (int first = 0; first < count; first += 4096) {
         const int cnt = count - first < 4096 ? count - first : 4096;
-        RET(gala_encode_plain(c, slots + (long long)first * N, cnt, masks + (long long)first * L * N));
+        KLAUNCH(c, "k_encode", k_encode<2><<<cnt * M, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(
+                                   c->dc, slots + (long long)first * N, masks + (long long)first * M * N));
     }
     release(c, slots);
+    (void)L;
     return GALA_OK;
 }
 
@@ -1311,78 +1331,112 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
                   const int8_t* coef, const int32_t* rowsum, int Mr, int Kp, const int* tap_steps, int band_step,
                   int c_n, uint64_t* outs)
 {
-    const int N = c->dc.N, L = c->dc.L;
-    const long long W = 2LL * L * N;
+    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
+    const long long W = 2LL * L * N, WQ = 2LL * M * N;
     if (n_ib <= 0 || k <= 0 || nb <= 0 || c_n <= 0 || Mr <= 0 || Mr % c_n) return set_err(GALA_ERR_DIM, "bad schedule-2 dims");
     if (Kp % 16 || Kp < n_ib * k * nb) return set_err(GALA_ERR_DIM, "Kp=%d must be a multiple of 16 covering K=%d", Kp,
                                                     n_ib * k * nb);
     if (Kp > (1 << 17)) return set_err(GALA_ERR_DIM, "K too large for exact int32 accumulation");
-    std::vector<int> rot_taps;
+    std::vector<int> tsteps(k);
+    bool any_rot = false;
     for (int t = 0; t < k; t++) {
-        int s = norm_step(c, tap_steps[t]);
-        if (s != 0) {
-            if (!key_for(c, s)) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", s);
-            rot_taps.push_back(t);
+        tsteps[t] = norm_step(c, tap_steps[t]);
+        if (tsteps[t] != 0) {
+            if (!key_for(c, tsteps[t])) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", tsteps[t]);
+            any_rot = true;
         }
     }
     for (int d = 1; d < c_n; d++)
         if (!gala_has_rotation_key(c, d * band_step))
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, d * band_step));
     if (!c->d_kg_off) {
-        std::vector<u64> off(2 * GALA_MAXM, 0);
-        for (int j = 0; j < L; j++) {
+        // [0, 2 GALA_MAXM): 128-bit offsets (hi, lo) per prime; [2 GALA_MAXM, 3 GALA_MAXM): P 2^64 mod q_j
+        std::vector<u64> off(3 * GALA_MAXM, 0);
+        const u64 P = c->primes[L];
+        for (int j = 0; j < M; j++) {
             unsigned __int128 o = kg_offset(c->primes[j]);
             off[2 * j] = (u64)(o >> 64);
             off[2 * j + 1] = (u64)o;
+            off[2 * GALA_MAXM + j] = (u64)((((unsigned __int128)(P % c->primes[j])) << 64) % c->primes[j]);
         }
         CK(cudaMalloc(&c->d_kg_off, sizeof(u64) * off.size()));
         CK(cudaMemcpy(c->d_kg_off, off.data(), sizeof(u64) * off.size(), cudaMemcpyHostToDevice));
     }
-    // 1. input rotations R[ib][tap] (hoisted: one decomposition per input)
-    u64* R;
-    RET(scratch(c, &R, (size_t)n_ib * k * W));
-    for (int ib = 0; ib < n_ib; ib++)
-        for (int t = 0; t < k; t++)
-            if (norm_step(c, tap_steps[t]) == 0)
-                CK(cudaMemcpyAsync(R + ((long long)ib * k + t) * W, cts + (long long)ib * W, sizeof(u64) * W,
-                                   cudaMemcpyDeviceToDevice, c->stream));
-    if (!rot_taps.empty()) {
+    // 1. rotated inputs in the extended basis, no ModDown: U [g][2][M][N], Cacc [g][2][L][N], g = ib k + tap
+    //    (one decomposition per input; step-0 taps are plain members: U = 0, Cacc = X)
+    EngRaw raw;
+    {
         std::vector<EngTerm> terms;
         std::vector<std::vector<EngMember>> groups;
-        std::vector<u64*> routs;
+        std::vector<u64*> none;
         for (int ib = 0; ib < n_ib; ib++) {
             EngTerm t;
             t.X = cts + (long long)ib * W;
             t.pt = nullptr;
             t.ntt_block = nullptr;
-            for (int tap : rot_taps) t.steps.push_back(norm_step(c, tap_steps[tap]));
+            for (int tap = 0; tap < k; tap++)
+                if (tsteps[tap]) t.steps.push_back(tsteps[tap]);
             terms.push_back(t);
-            for (size_t r = 0; r < rot_taps.size(); r++) {
-                groups.push_back({{ib, (int)r}});
-                routs.push_back(R + ((long long)ib * k + rot_taps[r]) * W);
-            }
+            int r = 0;
+            for (int tap = 0; tap < k; tap++) groups.push_back({{ib, tsteps[tap] ? r++ : -1}});
         }
-        RET(rotate_engine(c, terms, groups, routs));
+        (void)any_rot;
+        RET(rotate_engine(c, terms, groups, none, &raw));
     }
-    // 2. masked products as biased bytes, K-contiguous: Bt[8 W][Kp]
+    // 2. masked products as biased bytes, K-contiguous: Bt[8 WQ][Kp]
     int8_t* Bt;
+    RET(scratch(c, &Bt, (size_t)8 * WQ * Kp));
+    {
+        dim3 grid((unsigned)((WQ + KG_PT - 1) / KG_PT), (unsigned)((Kp + KG_KT - 1) / KG_KT));
+        KLAUNCH(c, "k_kg_y", k_kg_y<<<grid, 256, 0, c->stream>>>(c->dc, raw.U, raw.Cacc, masks, c->d_kg_off + 2 * GALA_MAXM,
+                                                                 k, nb, n_ib, Kp, Bt));
+    }
+    release(c, raw.U);
+    release(c, raw.Cacc);
+    // 3. exact integer first-Add on the tensor cores: C[Mp][8 WQ] = A . Bt (rows padded to 16)
+    const int Mp = (Mr + 15) / 16 * 16;
+    const int8_t* A = coef;
+    int8_t* Apad = nullptr;
+    if (Mp != Mr) {
+        RET(scratch(c, &Apad, (size_t)Mp * Kp));
+        CK(cudaMemsetAsync(Apad, 0, (size_t)Mp * Kp, c->stream));
+        CK(cudaMemcpyAsync(Apad, coef, (size_t)Mr * Kp, cudaMemcpyDeviceToDevice, c->stream));
+        A = Apad;
+    }
     int32_t* C;
-    RET(scratch(c, &Bt, (size_t)8 * W * Kp));
-    RET(scratch(c, &C, (size_t)8 * W * Mr));
-    KLAUNCH(c, "k_kg_y", k_kg_y<<<grid_for(W * Kp, 256), 256, 0, c->stream>>>(c->dc, R, masks, k, nb, n_ib, Kp, Bt));
-    release(c, R);
-    // 3. exact integer first-Add on the tensor cores: C[Mr][8 W] = A . Bt
-    RET(lt_gemm_i8(c, coef, Kp, Bt, Kp, C, Mr, Mr, 8 * W, Kp, 0));
+    RET(scratch(c, &C, (size_t)8 * WQ * Mp));
+    RET(lt_gemm_i8(c, A, Kp, Bt, Kp, C, Mp, Mp, 8 * WQ, Kp, 0));
     release(c, Bt);
-    // 4. recombine bytes -> words mod q
-    u64* acc;
-    RET(scratch(c, &acc, (size_t)Mr * W));
-    KLAUNCH(c, "k_kg_recombine", k_kg_recombine<<<grid_for(W * Mr, 256), 256, 0, c->stream>>>(
-                                     c->dc, C, rowsum, Mr, (const ulonglong2*)c->d_kg_off, acc));
+    release(c, Apad);
+    // 4. recombine bytes -> words mod q_j over QP
+    u64* accq;
+    RET(scratch(c, &accq, (size_t)Mr * WQ));
+    KLAUNCH(c, "k_kg_recombine", k_kg_recombine<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
+                                     c->dc, C, rowsum, Mr, Mp, (const ulonglong2*)c->d_kg_off, accq));
     release(c, C);
-    // 5. second-Perm: out[o] = sum_d rot_{d * band}(acc[o][d]), one lazy ModDown per o
-    RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, Mr / c_n, c_n, band_step, outs, 0));
-    release(c, acc);
+    // 5. one ModDown per accumulator (straight into outs when there is no second-Perm)
+    u64 *acc = outs, *rr;
+    if (c_n > 1) RET(scratch(c, &acc, (size_t)Mr * W));
+    RET(scratch(c, &rr, (size_t)Mr * 2 * N));
+    RET(launch_inv<false>(c, accq + (long long)L * N, rr, Mr * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
+                          "k_ntt_inv[moddown]"));
+    MdArgs a;
+    a.r = rr;
+    a.U = accq;
+    a.add0 = nullptr;
+    a.add1 = nullptr;
+    a.add_is = 0;
+    a.out = acc;
+    a.out_is = W;
+    a.outs = nullptr;
+    KLAUNCH(c, "k_moddown", k_moddown<<<Mr * 2 * L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, a));
+    release(c, rr);
+    release(c, accq);
+    // 6. second-Perm: out[o] = sum_d rot_{d * band}(acc[o][d]), one lazy ModDown per o
+    if (c_n > 1) {
+        RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, Mr / c_n, c_n, band_step, outs, 0));
+        release(c, acc);
+    }
     return GALA_OK;
 }
 
