@@ -676,51 +676,77 @@ __global__ void k_kg_mask_slots(DevCtx c, KgGeom g, uint32_t* __restrict__ out)
     }
 }
 
-// Masked products of the extended-basis rotated inputs, K = (ib, tap, beta), pos = (comp, j, i):
-//   Y[K][pos] = (U[g][pos] + P Cacc[g][comp][j][i]) (.) Mask[tap][beta][j][i],  g = ib k + tap
-// (Cacc term only for j < L), written as the 8 little-endian bytes of each word biased by 0x80
-// (signed int8 for the tensor-core GEMM) in the K-contiguous layout Bt[8 pos + b][Kp].  One CTA
-// transposes a KG_PT x KG_KT tile through shared memory: loads run along pos (coalesced), the
-// 16-byte stores along K.  The XOR swizzle keeps both phases at the 2-wavefront minimum.
+// Masked products of the rotated inputs in the extended basis QP, K = (ib, tap, beta),
+// pos = (comp, j, i), g = ib k + tap:
+//   Z[g][pos]  = sum_l sigma_tap(D_ib)[l][j][i] ksk_tap[l][comp][j][i] + P sigma_tap(c0_ib)[j][i]
+//                (the key switch without ModDown; P c0 term for comp 0, j < L; Z = P x for step 0)
+//   Y[K][pos]  = Z[g][pos] (.) Mask[tap][beta][j][i]
+// written as the 8 little-endian bytes of each word biased by 0x80 (signed int8 for the
+// tensor-core GEMM) in the K-contiguous layout Bt[8 pos + b][Kp].  D is the identity digit block
+// of each input ([(L M + L)][N], NTT), gathered through sigma: in bit-reversed order an
+// automorphism maps each aligned run of 32 slots onto one aligned run, so the gathers stay
+// coalesced.  One CTA owns a KG_PT x KG_KT tile (KG_KT / nb groups g): Z is formed once per
+// (g, pos) and multiplied by the nb masks; the tile is transposed through shared memory so the
+// loads run along pos and the 16-byte stores along K (XOR swizzle: both phases conflict-free).
 #define KG_PT 32
 #define KG_KT 128
 __device__ __forceinline__ int kg_swz(int pp, int kk) { return pp * KG_KT + (kk ^ ((pp + 4 * (kk >> 4)) & 15)); }
 
-__global__ void __launch_bounds__(256) k_kg_y(DevCtx c, const u64* __restrict__ U, const u64* __restrict__ Cacc,
-                                              const u64* __restrict__ masks, const u64* __restrict__ pmont, int k, int nb,
-                                              int n_ib, int Kp, int8_t* __restrict__ Bt)
+template <int L>
+__global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__ Dblk, const u64* __restrict__ X,
+                                               const u64* const* __restrict__ keys, const unsigned* __restrict__ gal,
+                                               const u64* __restrict__ masks, const u64* __restrict__ pmont, int k,
+                                               int nb, int n_ib, int Kp, int8_t* __restrict__ Bt)
 {
     __shared__ u64 sm[KG_PT * KG_KT];
-    const int N = c.N, L = c.L, M = c.M;
-    const long long MN = (long long)M * N, P = 2 * MN;
-    const long long pos0 = (long long)blockIdx.x * KG_PT;
-    const int K0 = blockIdx.y * KG_KT, Kreal = n_ib * k * nb;
-    for (int idx = threadIdx.x; idx < KG_PT * KG_KT; idx += blockDim.x) {
-        const int kk = idx / KG_PT, pp = idx % KG_PT;
-        const int K = K0 + kk;
-        const long long pos = pos0 + pp;
-        u64 v = 0;
-        if (K < Kreal && pos < P) {
-            const int beta = K % nb, tap = (K / nb) % k, ib = K / (nb * k);
-            const long long g = (long long)ib * k + tap;
-            const int comp = (int)(pos / MN);
-            const long long jl = pos - comp * MN;
-            const int j = (int)(jl / N);
-            const ModC md = c.mod[j];
-            u64 z = __ldg(U + g * P + pos);
-            if (j < L) z = add_mod(z, mont_mul(__ldg(Cacc + (g * 2 + comp) * L * N + jl), pmont[j], md), md.q);
-            v = mont_mul(z, __ldg(masks + ((long long)tap * nb + beta) * MN + jl), md);
+    constexpr int M = L + 1;
+    const int N = c.N, logN = c.logN, MN = M * N, P2 = 2 * MN;
+    const int pos0 = blockIdx.x * KG_PT, K0 = blockIdx.y * KG_KT;
+    {
+        const int pp = threadIdx.x & 31, w = threadIdx.x >> 5;
+        const int pos = pos0 + pp;
+        const int comp = pos >= MN ? 1 : 0, jl = pos - comp * MN, j = jl >> logN, i = jl & (N - 1);
+        const ModC md = c.mod[j < M ? j : 0];
+        const int gpt = KG_KT / nb, g0 = K0 / nb, G = n_ib * k;
+        const long long bw = (long long)(L * M + L) * N;
+        for (int gl = w; gl < gpt; gl += 8) {
+            const int g = g0 + gl;
+            const bool valid = g < G && pos < P2;
+            u64 z = 0;
+            int t = 0;
+            if (valid) {
+                const int ib = g / k;
+                t = g - ib * k;
+                const u64* key = keys[t];
+                if (key == nullptr) {
+                    if (j < L) z = mont_mul(__ldg(X + ((long long)ib * 2 + comp) * L * N + jl), pmont[j], md);
+                } else {
+                    const int src = auto_src(i, gal[t], logN);
+                    const u64* D = Dblk + ib * bw;
+                    Acc128 s;
+#pragma unroll
+                    for (int l = 0; l < L; l++)
+                        s.mac(__ldg(D + ((long long)l * M + j) * N + src), __ldg(key + (((long long)l * 2 + comp) * M + j) * N + i));
+                    z = s.reduce(md);
+                    if (comp == 0 && j < L)
+                        z = add_mod(z, mont_mul(__ldg(D + ((long long)L * M + j) * N + src), pmont[j], md), md.q);
+                }
+            }
+            const u64* mk = masks + (long long)t * nb * MN + jl;
+            for (int beta = 0; beta < nb; beta++) {
+                const u64 v = valid ? mont_mul(z, __ldg(mk + (long long)beta * MN), md) : 0;
+                sm[kg_swz(pp, gl * nb + beta)] = v ^ 0x8080808080808080ull;
+            }
         }
-        sm[kg_swz(pp, kk)] = v ^ 0x8080808080808080ull;
     }
     __syncthreads();
     const int pp = threadIdx.x >> 3, ch = threadIdx.x & 7;
-    const long long pos = pos0 + pp;
-    if (K0 + ch * 16 >= Kp || pos >= P) return;
+    const int pos = pos0 + pp;
+    if (K0 + ch * 16 >= Kp || pos >= P2) return;
     u64 w[16];
 #pragma unroll
     for (int i = 0; i < 16; i++) w[i] = sm[kg_swz(pp, ch * 16 + i)];
-    int8_t* o = Bt + pos * 8 * Kp + K0 + ch * 16;
+    int8_t* o = Bt + (long long)pos * 8 * Kp + K0 + ch * 16;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
         uint32_t x[4];

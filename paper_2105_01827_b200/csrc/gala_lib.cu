@@ -252,17 +252,8 @@ struct EngMember {
 
 static const u64* key_for(gala_ctx* c, int step);
 
-// raw != nullptr: skip the ModDown and hand back the extended-basis sums (caller releases):
-// U [G][2][M][N] key products, Cacc [G][2][L][N] plain sums; the group's rotated ciphertext is
-// ModDown(U) + Cacc = ModDown(U + P Cacc).
-struct EngRaw {
-    u64* U = nullptr;
-    u64* Cacc = nullptr;
-};
-
 static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
-                         const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs,
-                         EngRaw* raw = nullptr)
+                         const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const int G = (int)groups.size();
@@ -358,10 +349,10 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
                                                   c->stream>>>(c->dc, (const TermDesc*)(d_blob + o_th),
                                                                (const unsigned*)(d_blob + o_gal), blk_words));
     }
-    u64 *U, *Cacc, *r = nullptr;
+    u64 *U, *Cacc, *r;
     RET(scratch(c, &U, (size_t)G * 2 * M * N));
     RET(scratch(c, &Cacc, (size_t)G * 2 * L * N));
-    if (!raw) RET(scratch(c, &r, (size_t)G * 2 * N));
+    RET(scratch(c, &r, (size_t)G * 2 * N));
     const int th = N < 256 ? N : 256;
     dim3 grid((N + th - 1) / th, M, G);
     {
@@ -373,14 +364,6 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
             case 3: KLAUNCH(c, "k_ks_mac", k_ks_mac<3><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
             default: KLAUNCH(c, "k_ks_mac", k_ks_mac<4><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
         }
-    }
-    if (raw) {
-        raw->U = U;
-        raw->Cacc = Cacc;
-        release(c, dig);
-        release(c, blk);
-        release(c, d_blob);
-        return GALA_OK;
     }
     RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
@@ -1362,37 +1345,66 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
         CK(cudaMalloc(&c->d_kg_off, sizeof(u64) * off.size()));
         CK(cudaMemcpy(c->d_kg_off, off.data(), sizeof(u64) * off.size(), cudaMemcpyHostToDevice));
     }
-    // 1. rotated inputs in the extended basis, no ModDown: U [g][2][M][N], Cacc [g][2][L][N], g = ib k + tap
-    //    (one decomposition per input; step-0 taps are plain members: U = 0, Cacc = X)
-    EngRaw raw;
-    {
-        std::vector<EngTerm> terms;
-        std::vector<std::vector<EngMember>> groups;
-        std::vector<u64*> none;
-        for (int ib = 0; ib < n_ib; ib++) {
-            EngTerm t;
-            t.X = cts + (long long)ib * W;
-            t.pt = nullptr;
-            t.ntt_block = nullptr;
-            for (int tap = 0; tap < k; tap++)
-                if (tsteps[tap]) t.steps.push_back(tsteps[tap]);
-            terms.push_back(t);
-            int r = 0;
-            for (int tap = 0; tap < k; tap++) groups.push_back({{ib, tsteps[tap] ? r++ : -1}});
-        }
-        (void)any_rot;
-        RET(rotate_engine(c, terms, groups, none, &raw));
+    if (KG_KT % nb) return set_err(GALA_ERR_DIM, "band count %d must divide %d", nb, KG_KT);
+    // 1. one decomposition per input: identity digit block [(L M + L)][N]
+    const long long blk_words = (long long)(L * M + L) * N;
+    u64 *dig, *Dblk;
+    RET(scratch(c, &dig, (size_t)n_ib * L * N));
+    RET(scratch(c, &Dblk, (size_t)n_ib * blk_words));
+    std::vector<TermDesc> td(n_ib);
+    for (int b = 0; b < n_ib; b++) {
+        td[b].X = cts + b * W;
+        td[b].pt = nullptr;
+        td[b].dig = dig + (long long)b * L * N;
+        td[b].blk = Dblk + (long long)b * blk_words;
+        td[b].rot_off = 0;
+        td[b].rot_cnt = 1;
     }
-    // 2. masked products as biased bytes, K-contiguous: Bt[8 WQ][Kp]
+    std::vector<unsigned> gal(k + 1, 1u);     // gal[0] = identity (the decomposition); gal[1 + t] per tap
+    std::vector<const u64*> keys(k, nullptr);
+    for (int t = 0; t < k; t++) {
+        if (tsteps[t]) {
+            gal[1 + t] = galois_of(c, tsteps[t]);
+            keys[t] = key_for(c, tsteps[t]);
+        }
+    }
+    size_t o_gal = (td.size() * sizeof(TermDesc) + 15) & ~(size_t)15;
+    size_t o_keys = (o_gal + gal.size() * sizeof(unsigned) + 15) & ~(size_t)15;
+    std::vector<char> blob(o_keys + keys.size() * sizeof(u64*));
+    memcpy(blob.data(), td.data(), td.size() * sizeof(TermDesc));
+    memcpy(blob.data() + o_gal, gal.data(), gal.size() * sizeof(unsigned));
+    memcpy(blob.data() + o_keys, keys.data(), keys.size() * sizeof(u64*));
+    char* d_blob;
+    RET(upload(c, blob.data(), blob.size(), (void**)&d_blob));
+    const int nt = ntt_threads(N);
+    const unsigned* d_gal = (const unsigned*)(d_blob + o_gal);
+    if (any_rot) {
+        KLAUNCH(c, "k_digits_intt", k_digits_intt<<<(unsigned)(n_ib * L), nt, c->smem_ntt, c->stream>>>(
+                                        c->dc, (const TermDesc*)d_blob, d_gal, blk_words));
+        KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(n_ib * L * L), nt, c->smem_ntt, c->stream>>>(
+                                        c->dc, (const TermDesc*)d_blob, d_gal, blk_words));
+    }
+    // 2. fused key switch (no ModDown) + band masks -> biased bytes, K-contiguous: Bt[8 WQ][Kp]
     int8_t* Bt;
     RET(scratch(c, &Bt, (size_t)8 * WQ * Kp));
     {
         dim3 grid((unsigned)((WQ + KG_PT - 1) / KG_PT), (unsigned)((Kp + KG_KT - 1) / KG_KT));
-        KLAUNCH(c, "k_kg_y", k_kg_y<<<grid, 256, 0, c->stream>>>(c->dc, raw.U, raw.Cacc, masks, c->d_kg_off + 2 * GALA_MAXM,
-                                                                 k, nb, n_ib, Kp, Bt));
+        const u64* const* dk = (const u64* const*)(d_blob + o_keys);
+        const u64* pm = c->d_kg_off + 2 * GALA_MAXM;
+#define KG_ZY(LL)                                                                                                  \
+    KLAUNCH(c, "k_kg_zy", k_kg_zy<LL><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1, masks, pm, k, nb, \
+                                                                   n_ib, Kp, Bt))
+        switch (L) {
+            case 1: KG_ZY(1); break;
+            case 2: KG_ZY(2); break;
+            case 3: KG_ZY(3); break;
+            default: KG_ZY(4); break;
+        }
+#undef KG_ZY
     }
-    release(c, raw.U);
-    release(c, raw.Cacc);
+    release(c, dig);
+    release(c, Dblk);
+    release(c, d_blob);
     // 3. exact integer first-Add on the tensor cores: C[Mp][8 WQ] = A . Bt (rows padded to 16)
     const int Mp = (Mr + 15) / 16 * 16;
     const int8_t* A = coef;
