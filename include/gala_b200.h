@@ -135,7 +135,8 @@ int gala_kg_encode_weights(gala_ctx *ctx, const int32_t *kernels_dev, int c_o, i
  * exact integer evaluation order -- oracle o_conv_kg2).  The KG plaintexts of
  * coef_vectors (conv.py:220-235) factor into 0/1 band masks times one kernel coefficient each.
  * The rotated inputs stay in the extended basis QP (no ModDown per rotation); one ModDown per
- * accumulator.  gala_kg2_encode_masks: masks_dev [k_h k_w][pair c_n][L+1][N] (NTT, Montgomery).
+ * accumulator.  gala_kg2_encode_masks: masks_dev [k_h k_w][pair c_n][L+1][N][2] (NTT, Shoup pairs
+ * (w, floor(w 2^64 / q))).
  * gala_conv_kg2: coef_dev int8 [Mr][Kp] (Mr = n_obp c_n rows (o, d); K = (ib, tap, beta)
  * columns, zero-padded to Kp % 16 == 0; entry = centred kernel coefficient
  * kern[pair o + row][ib c_n + ch][tap] of band beta = row c_n + ch at rotation offset d),

@@ -463,7 +463,7 @@ class Context:
     def kg2_encode_masks(self, k_h: int, k_w: int, u_w: int, u_h: int, pair: int):
         torch = _torch()
         c_n = self.params.n // (u_w * u_h)
-        masks = torch.empty((k_h * k_w, pair * c_n, self.L + 1, self.N), dtype=torch.int64, device=self.device)
+        masks = torch.empty((k_h * k_w, pair * c_n, self.L + 1, self.N, 2), dtype=torch.int64, device=self.device)
         self.call("gala_kg2_encode_masks", int(k_h), int(k_w), int(u_w), int(u_h), int(pair),
                   ctypes.c_void_p(_ptr(masks)))
         return masks

@@ -692,11 +692,35 @@ __global__ void k_kg_mask_slots(DevCtx c, KgGeom g, uint32_t* __restrict__ out)
 #define KG_KT 128
 __device__ __forceinline__ int kg_swz(int pp, int kk) { return pp * KG_KT + (kk ^ ((pp + 4 * (kk >> 4)) & 15)); }
 
+// Montgomery-form operands [count][M][N] -> Shoup pairs (w, floor(w 2^64 / q)).  With w_m = w 2^64
+// mod q: w = REDC(w_m) and w 2^64 = q wsh + w_m, so wsh = (w 2^64 - w_m) / q = w_m (-q^-1) mod 2^64.
+__global__ void k_mont_to_shoup(DevCtx c, const u64* __restrict__ in, long long count, ulonglong2* __restrict__ out)
+{
+    const int N = c.N, M = c.M;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count * M * N;
+         e += (long long)gridDim.x * blockDim.x) {
+        const ModC md = c.mod[(int)((e / N) % M)];
+        const u64 wm = in[e];
+        out[e] = make_ulonglong2(csub(redc_lazy(0, wm, md), md.q), wm * md.qinv_neg);
+    }
+}
+
+// 4x4 byte transpose: out[b] = byte b of x0..x3 (PRMT)
+__device__ __forceinline__ void bytes4x4(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t* o)
+{
+    const uint32_t t0 = __byte_perm(x0, x1, 0x5140), t1 = __byte_perm(x0, x1, 0x7362);
+    const uint32_t t2 = __byte_perm(x2, x3, 0x5140), t3 = __byte_perm(x2, x3, 0x7362);
+    o[0] = __byte_perm(t0, t2, 0x5410);
+    o[1] = __byte_perm(t0, t2, 0x7632);
+    o[2] = __byte_perm(t1, t3, 0x5410);
+    o[3] = __byte_perm(t1, t3, 0x7632);
+}
+
 template <int L>
 __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__ Dblk, const u64* __restrict__ X,
                                                const u64* const* __restrict__ keys, const unsigned* __restrict__ gal,
-                                               const u64* __restrict__ masks, const u64* __restrict__ pmont, int k,
-                                               int nb, int n_ib, int Kp, int8_t* __restrict__ Bt)
+                                               const ulonglong2* __restrict__ masks, const ulonglong2* __restrict__ pconst,
+                                               int k, int nb, int n_ib, int Kp, int8_t* __restrict__ Bt)
 {
     __shared__ u64 sm[KG_PT * KG_KT];
     constexpr int M = L + 1;
@@ -707,6 +731,8 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
         const int pos = pos0 + pp;
         const int comp = pos >= MN ? 1 : 0, jl = pos - comp * MN, j = jl >> logN, i = jl & (N - 1);
         const ModC md = c.mod[j < M ? j : 0];
+        const u64 q = md.q;
+        const ulonglong2 pc = pconst[j < M ? j : 0];   // P mod q_j, Shoup companion
         const int gpt = KG_KT / nb, g0 = K0 / nb, G = n_ib * k;
         const long long bw = (long long)(L * M + L) * N;
         for (int gl = w; gl < gpt; gl += 8) {
@@ -719,22 +745,26 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
                 t = g - ib * k;
                 const u64* key = keys[t];
                 if (key == nullptr) {
-                    if (j < L) z = mont_mul(__ldg(X + ((long long)ib * 2 + comp) * L * N + jl), pmont[j], md);
+                    if (j < L) z = csub(shoup_lazy_sf(__ldg(X + ((long long)ib * 2 + comp) * L * N + jl), pc.x, pc.y, q), q);
                 } else {
                     const int src = auto_src(i, gal[t], logN);
-                    const u64* D = Dblk + ib * bw;
+                    const u64* D = Dblk + ib * bw + (long long)j * N + src;
+                    const u64* kp = key + ((long long)comp * M + j) * N + i;
                     Acc128 s;
 #pragma unroll
-                    for (int l = 0; l < L; l++)
-                        s.mac(__ldg(D + ((long long)l * M + j) * N + src), __ldg(key + (((long long)l * 2 + comp) * M + j) * N + i));
+                    for (int l = 0; l < L; l++) s.mac(__ldg(D + (long long)l * MN), __ldg(kp + (long long)l * 2 * MN));
                     z = s.reduce(md);
                     if (comp == 0 && j < L)
-                        z = add_mod(z, mont_mul(__ldg(D + ((long long)L * M + j) * N + src), pmont[j], md), md.q);
+                        z = add_mod(z, csub(shoup_lazy_sf(__ldg(D + (long long)L * MN), pc.x, pc.y, q), q), q);
                 }
             }
-            const u64* mk = masks + (long long)t * nb * MN + jl;
+            const ulonglong2* mk = masks + (long long)t * nb * MN + jl;
             for (int beta = 0; beta < nb; beta++) {
-                const u64 v = valid ? mont_mul(z, __ldg(mk + (long long)beta * MN), md) : 0;
+                u64 v = 0;
+                if (valid) {
+                    const ulonglong2 m = __ldg(mk + (long long)beta * MN);
+                    v = csub(shoup_lazy_sf(z, m.x, m.y, q), q);
+                }
                 sm[kg_swz(pp, gl * nb + beta)] = v ^ 0x8080808080808080ull;
             }
         }
@@ -743,22 +773,28 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
     const int pp = threadIdx.x >> 3, ch = threadIdx.x & 7;
     const int pos = pos0 + pp;
     if (K0 + ch * 16 >= Kp || pos >= P2) return;
-    u64 w[16];
+    uint32_t lo[16], hi[16];
 #pragma unroll
-    for (int i = 0; i < 16; i++) w[i] = sm[kg_swz(pp, ch * 16 + i)];
+    for (int i = 0; i < 16; i++) {
+        const u64 v = sm[kg_swz(pp, ch * 16 + i)];
+        lo[i] = (uint32_t)v;
+        hi[i] = (uint32_t)(v >> 32);
+    }
+    // plane b holds byte b of the 16 words: [b][q4] from the 4x4 transposes of words 4 q4 .. 4 q4 + 3
+    uint32_t pl[8][4];
+#pragma unroll
+    for (int q4 = 0; q4 < 4; q4++) {
+        uint32_t o[4];
+        bytes4x4(lo[4 * q4], lo[4 * q4 + 1], lo[4 * q4 + 2], lo[4 * q4 + 3], o);
+#pragma unroll
+        for (int b = 0; b < 4; b++) pl[b][q4] = o[b];
+        bytes4x4(hi[4 * q4], hi[4 * q4 + 1], hi[4 * q4 + 2], hi[4 * q4 + 3], o);
+#pragma unroll
+        for (int b = 0; b < 4; b++) pl[4 + b][q4] = o[b];
+    }
     int8_t* o = Bt + (long long)pos * 8 * Kp + K0 + ch * 16;
 #pragma unroll
-    for (int b = 0; b < 8; b++) {
-        uint32_t x[4];
-#pragma unroll
-        for (int q4 = 0; q4 < 4; q4++) {
-            uint32_t r = 0;
-#pragma unroll
-            for (int t = 0; t < 4; t++) r |= (uint32_t)((w[q4 * 4 + t] >> (8 * b)) & 0xff) << (8 * t);
-            x[q4] = r;
-        }
-        *(uint4*)(o + (long long)b * Kp) = make_uint4(x[0], x[1], x[2], x[3]);
-    }
+    for (int b = 0; b < 8; b++) *(uint4*)(o + (long long)b * Kp) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
 }
 
 // acc[m][pos] = (sum_b (C[8 pos + b][m] + 128 rowsum[m]) 256^b) mod q_j over the extended basis

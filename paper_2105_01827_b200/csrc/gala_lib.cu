@@ -1242,12 +1242,17 @@ int gala_kg2_encode_masks(gala_ctx* c, int k_h, int k_w, int u_w, int u_h, int p
     RET(scratch(c, &slots, (size_t)count * N));
     KLAUNCH(c, "k_kg_mask_slots", k_kg_mask_slots<<<grid_for((long long)count * N, 256), 256, 0, c->stream>>>(c->dc, g, slots));
     const int M = c->dc.M;
+    u64* mont;
+    RET(scratch(c, &mont, (size_t)count * M * N));
     for (int first = 0; first < count; first += 4096) {
         const int cnt = count - first < 4096 ? count - first : 4096;
         KLAUNCH(c, "k_encode", k_encode<2><<<cnt * M, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(
-                                   c->dc, slots + (long long)first * N, masks + (long long)first * M * N));
+                                   c->dc, slots + (long long)first * N, mont + (long long)first * M * N));
     }
+    KLAUNCH(c, "k_mont_to_shoup", k_mont_to_shoup<<<grid_for((long long)count * M * N, 256), 256, 0, c->stream>>>(
+                                      c->dc, mont, count, (ulonglong2*)masks));
     release(c, slots);
+    release(c, mont);
     (void)L;
     return GALA_OK;
 }
@@ -1333,14 +1338,16 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
         if (!gala_has_rotation_key(c, d * band_step))
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, d * band_step));
     if (!c->d_kg_off) {
-        // [0, 2 GALA_MAXM): 128-bit offsets (hi, lo) per prime; [2 GALA_MAXM, 3 GALA_MAXM): P 2^64 mod q_j
-        std::vector<u64> off(3 * GALA_MAXM, 0);
+        // [0, 2 GALA_MAXM): 128-bit offsets (hi, lo) per prime; [2 GALA_MAXM, 4 GALA_MAXM): (P mod q_j, Shoup)
+        std::vector<u64> off(4 * GALA_MAXM, 0);
         const u64 P = c->primes[L];
         for (int j = 0; j < M; j++) {
             unsigned __int128 o = kg_offset(c->primes[j]);
             off[2 * j] = (u64)(o >> 64);
             off[2 * j + 1] = (u64)o;
-            off[2 * GALA_MAXM + j] = (u64)((((unsigned __int128)(P % c->primes[j])) << 64) % c->primes[j]);
+            const u64 pj = P % c->primes[j];
+            off[2 * GALA_MAXM + 2 * j] = pj;
+            off[2 * GALA_MAXM + 2 * j + 1] = (u64)((((unsigned __int128)pj) << 64) / c->primes[j]);
         }
         CK(cudaMalloc(&c->d_kg_off, sizeof(u64) * off.size()));
         CK(cudaMemcpy(c->d_kg_off, off.data(), sizeof(u64) * off.size(), cudaMemcpyHostToDevice));
@@ -1390,9 +1397,9 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
     {
         dim3 grid((unsigned)((WQ + KG_PT - 1) / KG_PT), (unsigned)((Kp + KG_KT - 1) / KG_KT));
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
-        const u64* pm = c->d_kg_off + 2 * GALA_MAXM;
+        const ulonglong2* pm = (const ulonglong2*)(c->d_kg_off + 2 * GALA_MAXM);
 #define KG_ZY(LL)                                                                                                  \
-    KLAUNCH(c, "k_kg_zy", k_kg_zy<LL><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1, masks, pm, k, nb, \
+    KLAUNCH(c, "k_kg_zy", k_kg_zy<LL><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1, (const ulonglong2*)masks, pm, k, nb, \
                                                                    n_ib, Kp, Bt))
         switch (L) {
             case 1: KG_ZY(1); break;
