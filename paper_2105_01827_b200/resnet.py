@@ -96,7 +96,7 @@ class ConvLayer:
 
     @property
     def plaintext_bytes(self) -> int:
-        return int(self.kg.pts.numel() * 8)
+        return self.kg.resident_bytes
 
     def frames(self, x: np.ndarray):
         """Yield (origin_y, origin_x, frame array) covering the input x [c_in][s][s]."""

@@ -98,8 +98,7 @@ def conv(name, n, L, u, frame, c_i, c_o, k):
     return {"config": name, "N": ctx.N, "L": ctx.L, "c_n": layer.c_n, "n_ib": layer.n_ib, "n_obp": layer.n_obp,
             "ms_per_layer": ms, "layers_per_s": 1e3 / ms, "correct": ok, "weight_encode_s": round(setup, 2),
             "schedule": layer.schedule,
-            "plaintext_bytes": int(layer.pts.numel() * 8 if layer.pts is not None else
-                                   layer.masks.numel() * 8 + layer.coef.numel()), "meter": repr(meter),
+            "plaintext_bytes": layer.resident_bytes, "meter": repr(meter),
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
 
 

@@ -63,7 +63,7 @@ def main():
                "ms_reps": [round(v, 3) for v in reps],
                "plaintext_GB": round(layer.plaintext_bytes / 1e9, 3)}
         if spec.kind == "conv":
-            res.update(frame=layer.frame, c_n=layer.kg.c_n, tiles=layer.tiles ** 2)
+            res.update(frame=layer.frame, c_n=layer.kg.c_n, tiles=layer.tiles ** 2, schedule=layer.kg.schedule)
         if check:
             got = layer.shares(out, masks) if spec.kind == "fc" else layer.decrypt_output(out)
             ok = bool(np.array_equal(got, plain_layer(spec, x, net.weights[i], net.params.p)))
