@@ -141,10 +141,19 @@ int gala_kg_encode_weights(gala_ctx *ctx, const int32_t *kernels_dev, int c_o, i
  * columns, zero-padded to Kp % 16 == 0; entry = centred kernel coefficient
  * kern[pair o + row][ib c_n + ch][tap] of band beta = row c_n + ch at rotation offset d),
  * rowsum_dev int32 [Mr] = row sums of coef; outs_dev [n_obp][2][L][N]. */
-int gala_kg2_encode_masks(gala_ctx *ctx, int k_h, int k_w, int u_w, int u_h, int pair, uint64_t *masks_dev);
+int gala_kg2_encode_masks(gala_ctx *ctx, int k_h, int k_w, int u_w, int u_h, int pair, int band_only,
+                          uint64_t *masks_dev);
 int gala_conv_kg2(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *masks_dev, int k, int nb,
                   const int8_t *coef_dev, const int32_t *rowsum_dev, int Mr, int Kp, const int *tap_steps_host,
                   int band_step, int c_n, uint64_t *outs_dev);
+/* Post-mask form for frame-embedded inputs (band_only masks [pair c_n][L+1][N][2], no tap
+ * factor: exact on every output pixel whose receptive field stays inside the frame's zero margin
+ * or halo).  The masks leave the K columns: acc[m] = sum_beta Mask_beta (.) (A_(m, beta) . Z), so the
+ * GEMM runs on the bytes of the rotated inputs Z (K = (ib, tap)) with rows (m, beta):
+ * coef_dev int8 [Mr nb][Kp], rowsum_dev int32 [Mr nb]. */
+int gala_conv_kg2_post(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *masks_dev, int k, int nb,
+                       const int8_t *coef_dev, const int32_t *rowsum_dev, int Mr, int Kp, const int *tap_steps_host,
+                       int band_step, int c_n, uint64_t *outs_dev);
 
 /* canonical word import/export of `count` ciphertexts */
 int gala_ct_export(gala_ctx *ctx, const uint64_t *ct_dev, uint64_t *coef_dev, int count);

@@ -58,7 +58,7 @@ def lib():
                                 ctypes.c_int, ip, ctypes.c_int, u64p]
         L.o_conv_kg2.argtypes = [ctypes.c_void_p, u64p, ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int,
                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                 u64p]
+                                 ctypes.c_int, u64p]
         L.o_ntt.argtypes = [ctypes.c_void_p, ctypes.c_int, u64p, ctypes.c_int]
         L.o_bsgs_baby.argtypes = [ctypes.c_int]
         L.o_num_threads.restype = ctypes.c_int
@@ -195,8 +195,9 @@ class Oracle:
                                _p(st, ip), int(band_step), _p(outs, u64p)))
         return outs
 
-    def conv_kg2(self, cts, kern_centred, u_w, u_h, pair=2):
-        """Schedule 2 (factored plaintexts, integer first-Add); kern_centred int [c_o][c_i][k_h][k_w]."""
+    def conv_kg2(self, cts, kern_centred, u_w, u_h, pair=2, band_only=False):
+        """Schedule 2 (factored plaintexts, integer first-Add); kern_centred int [c_o][c_i][k_h][k_w].
+        band_only: masks without the tap-validity factor (frame-embedded inputs)."""
         cts = _c(cts, np.uint64)
         kern = _c(kern_centred, np.int32)
         c_o, c_i, k_h, k_w = kern.shape
@@ -205,7 +206,7 @@ class Oracle:
         n_obp = (c_o // c_n + pair - 1) // pair
         outs = np.zeros((n_obp,) + self.ct_shape, np.uint64)
         _check(lib().o_conv_kg2(self._h, _p(cts, u64p), cts.shape[0], kern.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
-                                c_o, c_i, k_h, k_w, u_w, u_h, pair, _p(outs, u64p)))
+                                c_o, c_i, k_h, k_w, u_w, u_h, pair, int(bool(band_only)), _p(outs, u64p)))
         return outs
 
     def ntt(self, a, idx, inverse=False):

@@ -930,10 +930,13 @@ int o_conv_kg(void *h, const u64 *cts, int n_ib, const uint32_t *pts, int n_obp,
  * replaces one per rotated input (ModDown(U + P V) = ModDown(U) + V exactly).  The second-Perm is
  * the lazy rotate-and-sum of o_conv_kg.  pair == 2: band beta = row * c_n + ch (output block
  * pair * o + row on hypercube row `row`); pair == 1: beta = ch over both rows.
+ * band_only != 0 drops the tap-validity factor of the masks (the taps read the cyclic neighbours
+ * inside each band): exact for every output pixel whose receptive field stays inside the zero
+ * margin or halo of a frame embedding, which is how the GPU's post-mask form is used.
  * kern: centred int32 [c_o][c_i][k_h][k_w] (reference kernels, conv.py:220-235).
  */
 int o_conv_kg2(void *h, const u64 *cts, int n_ib, const int32_t *kern, int c_o, int c_i, int k_h, int k_w,
-               int u_w, int u_h, int pair, u64 *outs)
+               int u_w, int u_h, int pair, int band_only, u64 *outs)
 {
     octx *c = h;
     int N = c->N, L = c->L, M = c->M, n = N / 2;
@@ -993,7 +996,7 @@ int o_conv_kg2(void *h, const u64 *cts, int n_ib, const int32_t *kern, int c_o, 
             for (int s = 0; s < N; s++) {
                 int row = s / n, cs = s % n, ch = cs / B, pos = cs % B, y = pos / u_w, x = pos % u_w;
                 int band = pair == 2 ? row * c_n + ch : ch;
-                int ok = x + dw >= 0 && x + dw < u_w && y + dh >= 0 && y + dh < u_h;
+                int ok = band_only || (x + dw >= 0 && x + dw < u_w && y + dh >= 0 && y + dh < u_h);
                 sl[s] = (uint32_t)(band == beta && ok);
             }
             encode_pt_ntt_qp(c, sl, Mk + ((size_t)t * nb + beta) * MN);

@@ -448,23 +448,28 @@ class Context:
                   int(c_n), int(k), st, int(band_step), ctypes.c_void_p(_ptr(outs)))
         return outs
 
-    def conv_kg2(self, cts, masks, coef, rowsum, k: int, nb: int, tap_steps, band_step: int, c_n: int):
-        """Schedule 2: cts [n_ib][2][L][N]; masks [k][nb][L][N]; coef int8 [Mr][Kp] -> [Mr/c_n][2][L][N]."""
+    def conv_kg2(self, cts, masks, coef, rowsum, k: int, nb: int, tap_steps, band_step: int, c_n: int,
+                 post: bool = False):
+        """Schedule 2: cts [n_ib][2][L][N] -> [Mr/c_n][2][L][N].  Pre-mask: masks [k][nb][M][N][2],
+        coef int8 [Mr][Kp]; post-mask (band-only masks [nb][M][N][2]): coef int8 [Mr nb][Kp]."""
         n_ib = cts.shape[0]
-        Mr, Kp = coef.shape
+        rows, Kp = coef.shape
+        Mr = rows // nb if post else rows
         self.ensure_keys(list(tap_steps) + [d * band_step for d in range(1, c_n)])
         outs = self.empty_ct(Mr // c_n)
         st = (ctypes.c_int * k)(*[int(s) for s in tap_steps])
-        self.call("gala_conv_kg2", ctypes.c_void_p(_ptr(cts)), int(n_ib), ctypes.c_void_p(_ptr(masks)), int(k), int(nb),
-                  ctypes.c_void_p(_ptr(coef)), ctypes.c_void_p(_ptr(rowsum)), int(Mr), int(Kp), st, int(band_step),
-                  int(c_n), ctypes.c_void_p(_ptr(outs)))
+        self.call("gala_conv_kg2_post" if post else "gala_conv_kg2", ctypes.c_void_p(_ptr(cts)), int(n_ib),
+                  ctypes.c_void_p(_ptr(masks)), int(k), int(nb), ctypes.c_void_p(_ptr(coef)),
+                  ctypes.c_void_p(_ptr(rowsum)), int(Mr), int(Kp), st, int(band_step), int(c_n),
+                  ctypes.c_void_p(_ptr(outs)))
         return outs
 
-    def kg2_encode_masks(self, k_h: int, k_w: int, u_w: int, u_h: int, pair: int):
+    def kg2_encode_masks(self, k_h: int, k_w: int, u_w: int, u_h: int, pair: int, band_only: bool = False):
         torch = _torch()
         c_n = self.params.n // (u_w * u_h)
-        masks = torch.empty((k_h * k_w, pair * c_n, self.L + 1, self.N, 2), dtype=torch.int64, device=self.device)
-        self.call("gala_kg2_encode_masks", int(k_h), int(k_w), int(u_w), int(u_h), int(pair),
+        taps = 1 if band_only else k_h * k_w
+        masks = torch.empty((taps, pair * c_n, self.L + 1, self.N, 2), dtype=torch.int64, device=self.device)
+        self.call("gala_kg2_encode_masks", int(k_h), int(k_w), int(u_w), int(u_h), int(pair), int(bool(band_only)),
                   ctypes.c_void_p(_ptr(masks)))
         return masks
 

@@ -758,6 +758,10 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
                         z = add_mod(z, csub(shoup_lazy_sf(__ldg(D + (long long)L * MN), pc.x, pc.y, q), q), q);
                 }
             }
+            if (masks == nullptr) {            // post-mask form: the GEMM takes Z itself (nb == 1)
+                sm[kg_swz(pp, gl)] = z ^ 0x8080808080808080ull;
+                continue;
+            }
             const ulonglong2* mk = masks + (long long)t * nb * MN + jl;
             for (int beta = 0; beta < nb; beta++) {
                 u64 v = 0;
@@ -797,10 +801,22 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
     for (int b = 0; b < 8; b++) *(uint4*)(o + (long long)b * Kp) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
 }
 
-// acc[m][pos] = (sum_b (C[8 pos + b][m] + 128 rowsum[m]) 256^b) mod q_j over the extended basis
-// (pos = (comp, j, i), j < M).  C is the int32 GEMM output (column-major [Mp][8P]).  The signed
-// 128-bit total is made non-negative with a multiple of q (off[j] >= 2^90) and reduced exactly with
+// One word of the integer first-Add back from its byte planes: (sum_b (C[8 pos + b][m] + 128 rowsum)
+// 256^b) mod q.  C is the int32 GEMM output (column-major, leading dimension ld).  The signed
+// 128-bit total is made non-negative with a multiple of q (off >= 2^90) and reduced exactly with
 // two Montgomery steps.
+__device__ __forceinline__ u64 kg_rec_word(const int32_t* __restrict__ C, long long pos, int ld, int m, long long bias,
+                                           ulonglong2 off, const ModC& md)
+{
+    __int128 t = 0;
+#pragma unroll
+    for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)C[(8 * pos + b) * ld + m] + bias);
+    unsigned __int128 u = (unsigned __int128)(t + (((__int128)off.x << 64) | (__int128)off.y));
+    const u64 r = csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q);   // u 2^-64 mod q
+    return mont_mul(r, md.r2, md);                                      // * 2^64 -> u mod q
+}
+
+// pre-mask form: acc[m][pos] = word m of the GEMM, pos = (comp, j, i) over the extended basis
 __global__ void k_kg_recombine(DevCtx c, const int32_t* __restrict__ C, const int32_t* __restrict__ rowsum, int Mr,
                                int Mp, const ulonglong2* __restrict__ off, u64* __restrict__ acc)
 {
@@ -811,15 +827,31 @@ __global__ void k_kg_recombine(DevCtx c, const int32_t* __restrict__ C, const in
         const int m = (int)(e % Mr);
         const long long pos = e / Mr;
         const int j = (int)((pos % MN) / c.N);
-        const long long bias = 128LL * rowsum[m];
-        __int128 t = 0;
-#pragma unroll
-        for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)C[(8 * pos + b) * Mp + m] + bias);
-        const ulonglong2 o = off[j];
-        unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
+        acc[(long long)m * P + pos] = kg_rec_word(C, pos, Mp, m, 128LL * rowsum[m], off[j], c.mod[j]);
+    }
+}
+
+// post-mask form: acc[m][pos] = sum_beta Mask[beta][j][i] (.) word (m nb + beta) of the GEMM
+__global__ void k_kg_recombine_post(DevCtx c, const int32_t* __restrict__ C, const int32_t* __restrict__ rowsum, int Mr,
+                                    int nb, int Mp, const ulonglong2* __restrict__ off,
+                                    const ulonglong2* __restrict__ masks, u64* __restrict__ acc)
+{
+    const long long MN = (long long)c.M * c.N, P = 2 * MN;
+    const long long total = P * Mr;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int m = (int)(e % Mr);
+        const long long pos = e / Mr, jl = pos % MN;
+        const int j = (int)(jl / c.N);
         const ModC md = c.mod[j];
-        const u64 r = csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q);   // u 2^-64 mod q
-        acc[(long long)m * P + pos] = mont_mul(r, md.r2, md);               // * 2^64 -> u mod q
+        u64 a = 0;
+        for (int beta = 0; beta < nb; beta++) {
+            const int r = m * nb + beta;
+            const u64 w = kg_rec_word(C, pos, Mp, r, 128LL * rowsum[r], off[j], md);
+            const ulonglong2 mk = __ldg(masks + (long long)beta * MN + jl);
+            a = add_mod(a, csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q), md.q);
+        }
+        acc[(long long)m * P + pos] = a;
     }
 }
 

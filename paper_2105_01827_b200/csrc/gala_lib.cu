@@ -1224,20 +1224,20 @@ int gala_kg_encode_weights(gala_ctx* c, const int32_t* kern, int c_o, int c_i, i
 // K = (ib, tap, beta) runs as an int8 tensor-core GEMM (cuBLASLt, exact int32 accumulation); a
 // recombination kernel rebuilds each word mod q exactly.  Oracle: o_conv_kg2.
 
-int gala_kg2_encode_masks(gala_ctx* c, int k_h, int k_w, int u_w, int u_h, int pair, uint64_t* masks)
+int gala_kg2_encode_masks(gala_ctx* c, int k_h, int k_w, int u_w, int u_h, int pair, int band_only, uint64_t* masks)
 {
     const int N = c->dc.N, L = c->dc.L, n = N / 2;
     const int B = u_w * u_h;
     if (B <= 0 || n % B || (k_h % 2) == 0 || (k_w % 2) == 0 || (pair != 1 && pair != 2))
         return set_err(GALA_ERR_PARAM, "bad kernel-grouping geometry");
     KgGeom g{};
-    g.k_h = k_h;
-    g.k_w = k_w;
+    g.k_h = band_only ? 1 : k_h;   // band-only masks: no tap dimension
+    g.k_w = band_only ? 1 : k_w;
     g.u_w = u_w;
     g.u_h = u_h;
     g.c_n = n / B;
     g.pair = pair;
-    const int count = k_h * k_w * pair * g.c_n;
+    const int count = g.k_h * g.k_w * pair * g.c_n;
     uint32_t* slots;
     RET(scratch(c, &slots, (size_t)count * N));
     KLAUNCH(c, "k_kg_mask_slots", k_kg_mask_slots<<<grid_for((long long)count * N, 256), 256, 0, c->stream>>>(c->dc, g, slots));
@@ -1315,15 +1315,16 @@ static unsigned __int128 kg_offset(u64 q)
     return (two90 / q + 1) * q;
 }
 
-int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* masks, int k, int nb,
-                  const int8_t* coef, const int32_t* rowsum, int Mr, int Kp, const int* tap_steps, int band_step,
-                  int c_n, uint64_t* outs)
+static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, const uint64_t* masks, int k, int nb,
+                        const int8_t* coef, const int32_t* rowsum, int Mr, int Kp, const int* tap_steps, int band_step,
+                        int c_n, uint64_t* outs)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const long long W = 2LL * L * N, WQ = 2LL * M * N;
     if (n_ib <= 0 || k <= 0 || nb <= 0 || c_n <= 0 || Mr <= 0 || Mr % c_n) return set_err(GALA_ERR_DIM, "bad schedule-2 dims");
-    if (Kp % 16 || Kp < n_ib * k * nb) return set_err(GALA_ERR_DIM, "Kp=%d must be a multiple of 16 covering K=%d", Kp,
-                                                    n_ib * k * nb);
+    const int Kreal = n_ib * k * (post ? 1 : nb);
+    const int rows = post ? Mr * nb : Mr;     // GEMM rows
+    if (Kp % 16 || Kp < Kreal) return set_err(GALA_ERR_DIM, "Kp=%d must be a multiple of 16 covering K=%d", Kp, Kreal);
     if (Kp > (1 << 17)) return set_err(GALA_ERR_DIM, "K too large for exact int32 accumulation");
     std::vector<int> tsteps(k);
     bool any_rot = false;
@@ -1352,7 +1353,8 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
         CK(cudaMalloc(&c->d_kg_off, sizeof(u64) * off.size()));
         CK(cudaMemcpy(c->d_kg_off, off.data(), sizeof(u64) * off.size(), cudaMemcpyHostToDevice));
     }
-    if (KG_KT % nb) return set_err(GALA_ERR_DIM, "band count %d must divide %d", nb, KG_KT);
+    const int nb_y = post ? 1 : nb;          // masks applied per K column (pre) or per GEMM row group (post)
+    if (KG_KT % nb_y) return set_err(GALA_ERR_DIM, "band count %d must divide %d", nb, KG_KT);
     // 1. one decomposition per input: identity digit block [(L M + L)][N]
     const long long blk_words = (long long)(L * M + L) * N;
     u64 *dig, *Dblk;
@@ -1399,8 +1401,9 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
         const ulonglong2* pm = (const ulonglong2*)(c->d_kg_off + 2 * GALA_MAXM);
 #define KG_ZY(LL)                                                                                                  \
-    KLAUNCH(c, "k_kg_zy", k_kg_zy<LL><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1, (const ulonglong2*)masks, pm, k, nb, \
-                                                                   n_ib, Kp, Bt))
+    KLAUNCH(c, "k_kg_zy", k_kg_zy<LL><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1,                \
+                                                                   post ? nullptr : (const ulonglong2*)masks, pm, k,  \
+                                                                   nb_y, n_ib, Kp, Bt))
         switch (L) {
             case 1: KG_ZY(1); break;
             case 2: KG_ZY(2); break;
@@ -1413,13 +1416,13 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
     release(c, Dblk);
     release(c, d_blob);
     // 3. exact integer first-Add on the tensor cores: C[Mp][8 WQ] = A . Bt (rows padded to 16)
-    const int Mp = (Mr + 15) / 16 * 16;
+    const int Mp = (rows + 15) / 16 * 16;
     const int8_t* A = coef;
     int8_t* Apad = nullptr;
-    if (Mp != Mr) {
+    if (Mp != rows) {
         RET(scratch(c, &Apad, (size_t)Mp * Kp));
         CK(cudaMemsetAsync(Apad, 0, (size_t)Mp * Kp, c->stream));
-        CK(cudaMemcpyAsync(Apad, coef, (size_t)Mr * Kp, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(Apad, coef, (size_t)rows * Kp, cudaMemcpyDeviceToDevice, c->stream));
         A = Apad;
     }
     int32_t* C;
@@ -1430,8 +1433,14 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
     // 4. recombine bytes -> words mod q_j over QP
     u64* accq;
     RET(scratch(c, &accq, (size_t)Mr * WQ));
-    KLAUNCH(c, "k_kg_recombine", k_kg_recombine<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
-                                     c->dc, C, rowsum, Mr, Mp, (const ulonglong2*)c->d_kg_off, accq));
+    if (post) {
+        KLAUNCH(c, "k_kg_recombine_post", k_kg_recombine_post<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
+                                              c->dc, C, rowsum, Mr, nb, Mp, (const ulonglong2*)c->d_kg_off,
+                                              (const ulonglong2*)masks, accq));
+    } else {
+        KLAUNCH(c, "k_kg_recombine", k_kg_recombine<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
+                                         c->dc, C, rowsum, Mr, Mp, (const ulonglong2*)c->d_kg_off, accq));
+    }
     release(c, C);
     // 5. one ModDown per accumulator (straight into outs when there is no second-Perm)
     u64 *acc = outs, *rr;
@@ -1457,6 +1466,20 @@ int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ma
         release(c, acc);
     }
     return GALA_OK;
+}
+
+int gala_conv_kg2(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* masks, int k, int nb,
+                  const int8_t* coef, const int32_t* rowsum, int Mr, int Kp, const int* tap_steps, int band_step,
+                  int c_n, uint64_t* outs)
+{
+    return conv_kg2_run(c, false, cts, n_ib, masks, k, nb, coef, rowsum, Mr, Kp, tap_steps, band_step, c_n, outs);
+}
+
+int gala_conv_kg2_post(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* masks, int k, int nb,
+                       const int8_t* coef, const int32_t* rowsum, int Mr, int Kp, const int* tap_steps, int band_step,
+                       int c_n, uint64_t* outs)
+{
+    return conv_kg2_run(c, true, cts, n_ib, masks, k, nb, coef, rowsum, Mr, Kp, tap_steps, band_step, c_n, outs);
 }
 
 int gala_ct_export(gala_ctx* c, const uint64_t* ct, uint64_t* coef, int count)

@@ -91,7 +91,9 @@ class ConvLayer:
         if spec.c_in % task.channels_per_ct or spec.c_out % task.channels_per_ct:
             raise ParameterError(f"{spec.name}: channels do not pack into {frame}x{frame} frames")
         self.task = task
-        self.kg = KernelGroupingConv(task)
+        # every kept output pixel reads inside the frame's zero margin (or the tile's halo)
+        margin_ok = self.tiled or frame - spec.size >= h
+        self.kg = KernelGroupingConv(task, band_only=margin_ok)
         self.ctx = self.kg.ctx
 
     @property

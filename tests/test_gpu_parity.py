@@ -174,3 +174,41 @@ def test_conv_kg2_words(tw, pair):
         for ob in range(c_o // c_n):
             got = tw.gpu.decrypt_physical(g_out[ob // pair]).reshape(2, -1)[ob % pair if pair == 2 else 0]
             assert np.array_equal(got, want[ob])
+
+
+def test_conv_kg2_post_words(tw):
+    """Post-mask form (band-only masks applied after the GEMM) == oracle o_conv_kg2(band_only=1), word
+    for word; on a zero-margin frame it decrypts to the plaintext convolution inside the image."""
+    import torch
+
+    from oracle.plain import conv2d_mod_p
+    from paper_2105_01827_b200.conv import ConvTask, kg2_coefficients, kg2_post_coefficients
+
+    n = tw.bfv.n
+    if n not in KG2_GEOM:
+        pytest.skip("no geometry for this ring")
+    u_w, u_h = KG2_GEOM[n]
+    c_n = n // (u_w * u_h)
+    c_i, c_o, pair = 2 * c_n, 3 * c_n, 2
+    kern = tw.rng.integers(-128, 128, (c_o, c_i, 3, 3))
+    task = ConvTask(u_w, u_h, c_i, 3, 3, c_o, kern, tw.params)
+    taps = [rot for _, _, rot in task.offsets()]
+    tw.keys_for(taps + [d * u_w * u_h for d in range(1, c_n)])
+    x = np.zeros((c_i, u_h, u_w), dtype=np.int64)
+    x[:, :u_h - 1, :u_w - 1] = tw.rng.integers(0, P, (c_i, u_h - 1, u_w - 1))   # zero margin of 1
+    blocks = x.reshape(c_i // c_n, c_n * u_w * u_h)
+    xs = [tw.encrypt(np.concatenate([b, b]).astype(np.uint32)) for b in blocks]
+    A, _, K = kg2_coefficients(task, c_n, pair)
+    B, rowsum = kg2_post_coefficients(A, K, pair * c_n)
+    masks = tw.gpu.kg2_encode_masks(3, 3, u_w, u_h, pair, band_only=True)
+    dev = tw.gpu.device
+    g_out = tw.gpu.conv_kg2(torch.stack([g for g, _ in xs]), masks, torch.from_numpy(B).to(dev),
+                            torch.from_numpy(rowsum).to(dev), 9, pair * c_n, taps, u_w * u_h, c_n, post=True)
+    c_out = tw.cpu.conv_kg2(np.stack([c for _, c in xs]), kern, u_w, u_h, pair, band_only=True)
+    assert np.array_equal(tw.gpu.export_words(g_out), c_out)
+    if tw.L >= 2:
+        want = conv2d_mod_p(x, kern, P)[:, :u_h - 1, :u_w - 1]
+        for ob in range(c_o // c_n):
+            got = tw.gpu.decrypt_physical(g_out[ob // pair]).reshape(2, -1)[ob % pair]
+            got = got.reshape(c_n, u_h, u_w)[:, :u_h - 1, :u_w - 1]
+            assert np.array_equal(got, want[ob * c_n:(ob + 1) * c_n])

@@ -80,7 +80,7 @@ def conv(name, n, L, u, frame, c_i, c_o, k):
     img[:, :u, :u] = ch
     task = ConvTask(frame, frame, c_i, k, k, c_o, kern, params)
     t0 = time.perf_counter()
-    layer = KernelGroupingConv(task, schedule=SCHED)
+    layer = KernelGroupingConv(task, schedule=SCHED, band_only=frame - u >= k // 2)
     setup = time.perf_counter() - t0
     ctx = layer.ctx
     cts = encrypt_inputs(task, img)
@@ -97,7 +97,7 @@ def conv(name, n, L, u, frame, c_i, c_o, k):
     ok = bool(np.array_equal(got, conv2d_mod_p(ch, kern, P)))
     return {"config": name, "N": ctx.N, "L": ctx.L, "c_n": layer.c_n, "n_ib": layer.n_ib, "n_obp": layer.n_obp,
             "ms_per_layer": ms, "layers_per_s": 1e3 / ms, "correct": ok, "weight_encode_s": round(setup, 2),
-            "schedule": layer.schedule,
+            "schedule": layer.schedule, "post_mask": layer.post,
             "plaintext_bytes": layer.resident_bytes, "meter": repr(meter),
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
 
