@@ -291,7 +291,7 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
             tj = json.load(f)
-        if dom_name in tj and B == 8:
+        if dom_name in tj and int(tj.get("batch", 0)) == B:
             traffic = int(tj[dom_name])
     except Exception:
         pass
