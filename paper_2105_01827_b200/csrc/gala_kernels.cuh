@@ -451,15 +451,16 @@ __global__ void __launch_bounds__(256) k_gala_mac(DevCtx c, const u64* __restric
 //   E[bi][jj][c][j][k] = sum_i sigma_jj(D_i)_j[k] * ksk_jj[i][c][j][k]          (QP)
 //   R0[bi][jj][j][k]   = sigma_jj(x.c0)_j[k]                                     (Q)
 // D: identity digit block of the input ([(L*M + L)][N], NTT), gathered through sigma (L2 resident).
-// grid (N / blockDim, M, B * (baby - 1)).
+// grid (B (baby - 1), M, N / blockDim): all (input, rotation) pairs of one coefficient slice run
+// together, so the slice of every key stays in L2 across the inputs.
 template <int L>
 __global__ void __launch_bounds__(256) k_gala_e(DevCtx c, const u64* __restrict__ Dblk, const u64* const* __restrict__ keys,
                                                 const unsigned* __restrict__ gal, int baby, u64* __restrict__ E,
                                                 u64* __restrict__ R0)
 {
     const int N = c.N, M = L + 1;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y, z = blockIdx.z;
+    const int k = blockIdx.z * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, z = blockIdx.x;
     const int bi = z / (baby - 1), jj = z % (baby - 1) + 1;
     if (k >= N) return;
     const ModC md = c.mod[j];
@@ -487,14 +488,16 @@ __global__ void __launch_bounds__(256) k_gala_e(DevCtx c, const u64* __restrict_
 // (memory-level parallelism), and the 128-bit accumulators are Montgomery-reduced once per chunk
 // (CH <= c.lazy[j] products).  grid (N / blockDim, M, B * G), z = bi * G + g (input-major: E of an
 // input stays in L2 while its groups run).
-template <int CH>
+template <int CH, bool SLICED>
 __global__ void __launch_bounds__(256) k_gala_mac2(DevCtx c, const u64* __restrict__ X, const u64* __restrict__ E,
                                                    const u64* __restrict__ R0, const u64* __restrict__ pts2, int baby,
                                                    int G, u64* __restrict__ U, u64* __restrict__ Cacc)
 {
     const int N = c.N, L = c.L, M = c.M;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y, z = blockIdx.z;
+    // SLICED: grid (B G, M, N / blockDim) -- every (input, group) of one coefficient slice runs
+    // together, so the slice's plaintexts and E stay in L2 across all inputs and groups
+    const int k = (SLICED ? blockIdx.z : blockIdx.x) * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, z = SLICED ? blockIdx.x : blockIdx.z;
     const int bi = z / G, g = z % G;
     if (k >= N) return;
     const ModC md = c.mod[j];
@@ -513,6 +516,10 @@ __global__ void __launch_bounds__(256) k_gala_mac2(DevCtx c, const u64* __restri
             a1 = mont_mul(__ldg(x + LN + j * NN + k), w, md);
         }
     }
+    // 128-bit lazy accumulation: one Montgomery reduction per c.lazy[j] products (k q^2 < q 2^64)
+    Acc128 s0, s1, sc;
+    const int lazy = c.lazy[j];
+    int pending = 0;
     for (int jj0 = 1; jj0 < baby; jj0 += CH) {
         u64 w[CH], e0[CH], e1[CH], r0[CH];
 #pragma unroll
@@ -520,23 +527,32 @@ __global__ void __launch_bounds__(256) k_gala_mac2(DevCtx c, const u64* __restri
             const int jj = jj0 + m;
             w[m] = e0[m] = e1[m] = r0[m] = 0;
             if (jj < baby) {
-                w[m] = __ldcs((const unsigned long long*)(Pb + (long long)jj * MN));
+                w[m] = SLICED ? __ldg(Pb + (long long)jj * MN) : __ldcs((const unsigned long long*)(Pb + (long long)jj * MN));
                 e0[m] = __ldg(Eb + (long long)(jj - 1) * 2 * MN);
                 e1[m] = __ldg(Eb + (long long)(jj - 1) * 2 * MN + MN);
                 if (jq) r0[m] = __ldg(Rb + (long long)(jj - 1) * LN);
             }
         }
-        Acc128 s0, s1, sc;
+        if (pending + CH > lazy) {
+            u0 = add_mod(u0, s0.reduce(md), q);
+            u1 = add_mod(u1, s1.reduce(md), q);
+            if (jq) a0 = add_mod(a0, sc.reduce(md), q);
+            s0 = Acc128();
+            s1 = Acc128();
+            sc = Acc128();
+            pending = 0;
+        }
 #pragma unroll
         for (int m = 0; m < CH; m++) {
             s0.mac(w[m], e0[m]);
             s1.mac(w[m], e1[m]);
             if (jq) sc.mac(w[m], r0[m]);
         }
-        u0 = add_mod(u0, s0.reduce(md), q);
-        u1 = add_mod(u1, s1.reduce(md), q);
-        if (jq) a0 = add_mod(a0, sc.reduce(md), q);
+        pending += CH;
     }
+    u0 = add_mod(u0, s0.reduce(md), q);
+    u1 = add_mod(u1, s1.reduce(md), q);
+    if (jq) a0 = add_mod(a0, sc.reduce(md), q);
     U[(((long long)z * 2 + 0) * M + j) * NN + k] = u0;
     U[(((long long)z * 2 + 1) * M + j) * NN + k] = u1;
     if (jq) {

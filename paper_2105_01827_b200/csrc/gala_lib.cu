@@ -1026,7 +1026,7 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
     {
         const int th = N < 256 ? N : 256;
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
-        dim3 ga((N + th - 1) / th, M, B * (baby - 1));
+        dim3 ga(B * (baby - 1), M, (N + th - 1) / th);
         switch (L) {
             case 1: KLAUNCH(c, "k_gala_e", k_gala_e<1><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
             case 2: KLAUNCH(c, "k_gala_e", k_gala_e<2><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
@@ -1035,10 +1035,11 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
         }
         // one (input, group) per thread (measured best: sharing plaintext loads across inputs, or an
         // smem-tiled modular GEMM, costs occupancy / Montgomery products and runs slower)
-        // one member per REDC, 48 registers: measured best (larger chunks of lazy accumulation or
-        // sharing plaintext loads across inputs raise register pressure and lose to occupancy)
-        dim3 gb((N + th - 1) / th, M, G * B);
-        KLAUNCH(c, "k_gala_mac2", k_gala_mac2<1><<<gb, th, 0, c->stream>>>(c->dc, cts, E, R0, pts2, baby, G, U, Cacc));
+        // one member's loads in flight at a time (larger load chunks or sharing plaintext loads across
+        // inputs raise register pressure and lose to occupancy), 128-bit lazy accumulation with one
+        // REDC per c.lazy[j] members, coefficient-slice-major grid (measured best on B200)
+        dim3 gb(G * B, M, (N + th - 1) / th);
+        KLAUNCH(c, "k_gala_mac2", (k_gala_mac2<1, true><<<gb, th, 0, c->stream>>>(c->dc, cts, E, R0, pts2, baby, G, U, Cacc)));
     }
     release(c, E);
     release(c, R0);
