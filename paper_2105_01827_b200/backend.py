@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import math
 import threading
 from dataclasses import dataclass, fields, replace
 
@@ -412,6 +413,16 @@ class Context:
         return outs, masked
 
     # -- GALA schedule 2 (digits hoisted across the plaintext product) -----------
+    def gala2_baby(self, T: int) -> int:
+        """Baby-step count for schedule 2.  Cost ~ a b (one E_jj key product per baby rotation) +
+        c T / b (a ModDown, a decomposition and a giant key switch per group); measured on B200 at
+        N = 8192, L = 3: c / a ~ 7, so b = 2^round(log2 sqrt(7 T)) (T = 512 -> 64).  Small trees keep
+        the balanced split."""
+        if T < 64:
+            return int(self.lib.gala_bsgs_baby(int(T)))
+        b = 1 << int(round(math.log2(math.sqrt(7 * T))))
+        return max(1, min(T, b))
+
     def gala_schedule(self, T: int) -> int:
         """2 when the hoisted-digit key-switch noise fits the budget, else 1."""
         return 2 if (self.L >= 2 or T <= 64) else 1

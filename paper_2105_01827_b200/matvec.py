@@ -326,8 +326,10 @@ class GalaFC:
                 raise ParameterError("paired row blocks must share T")
             self.blocks.append([tasks, np.concatenate([s0, s1], axis=1), s0.shape[0]])
         self.T = self.blocks[0][2]
-        self.baby, self.steps = self.ctx.bsgs_steps(self.T, baby)
         self.schedule = self.ctx.gala_schedule(self.T)
+        if baby is None and self.schedule == 2:
+            baby = self.ctx.gala2_baby(self.T)
+        self.baby, self.steps = self.ctx.bsgs_steps(self.T, baby)
         for blk in self.blocks:    # resident encoded weights, in the layout of the chosen schedule
             blk[1] = (self.ctx.encode_gala_weights(blk[1], self.baby) if self.schedule == 2
                       else self.ctx.encode_plain(blk[1]))
