@@ -452,33 +452,45 @@ __global__ void __launch_bounds__(256) k_gala_mac(DevCtx c, const u64* __restric
 //   R0[bi][jj][j][k]   = sigma_jj(x.c0)_j[k]                                     (Q)
 // D: identity digit block of the input ([(L*M + L)][N], NTT), gathered through sigma (L2 resident).
 // grid (B (baby - 1), M, N / blockDim): all (input, rotation) pairs of one coefficient slice run
-// together, so the slice of every key stays in L2 across the inputs.
-template <int L>
+// together, so the slice of every key stays in L2 across the inputs.  Each thread serves CB inputs
+// with one register copy of the key limbs (key loads amortised over the inputs).
+template <int L, int CB>
 __global__ void __launch_bounds__(256) k_gala_e(DevCtx c, const u64* __restrict__ Dblk, const u64* const* __restrict__ keys,
                                                 const unsigned* __restrict__ gal, int baby, u64* __restrict__ E,
                                                 u64* __restrict__ R0)
 {
     const int N = c.N, M = L + 1;
     const int k = blockIdx.z * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y, z = blockIdx.x;
-    const int bi = z / (baby - 1), jj = z % (baby - 1) + 1;
+    const int j = blockIdx.y;
+    const int bg = blockIdx.x / (baby - 1), jj = blockIdx.x % (baby - 1) + 1;
     if (k >= N) return;
     const ModC md = c.mod[j];
     const long long NN = N, MN = (long long)M * N;
-    const u64* D = Dblk + (long long)bi * (L * M + L) * NN;
     const u64* key = keys[jj];
     const int src = auto_src(k, gal[jj], c.logN);
-    Acc128 s0, s1;
+    u64 ka[L], kb[L];
 #pragma unroll
     for (int i = 0; i < L; i++) {
-        const u64 d = __ldg(D + ((long long)i * M + j) * NN + src);
-        s0.mac(d, __ldg(key + (((long long)i * 2 + 0) * M + j) * NN + k));
-        s1.mac(d, __ldg(key + (((long long)i * 2 + 1) * M + j) * NN + k));
+        ka[i] = __ldg(key + (((long long)i * 2 + 0) * M + j) * NN + k);
+        kb[i] = __ldg(key + (((long long)i * 2 + 1) * M + j) * NN + k);
     }
-    u64* e = E + (long long)z * 2 * MN + j * NN + k;
-    e[0] = s0.reduce(md);
-    e[MN] = s1.reduce(md);
-    if (j < L) R0[((long long)z * L + j) * NN + k] = __ldg(D + ((long long)L * M + j) * NN + src);
+#pragma unroll
+    for (int cb = 0; cb < CB; cb++) {
+        const int bi = bg * CB + cb;
+        const long long z = (long long)bi * (baby - 1) + (jj - 1);
+        const u64* D = Dblk + (long long)bi * (L * M + L) * NN;
+        Acc128 s0, s1;
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+            const u64 d = __ldg(D + ((long long)i * M + j) * NN + src);
+            s0.mac(d, ka[i]);
+            s1.mac(d, kb[i]);
+        }
+        u64* e = E + z * 2 * MN + j * NN + k;
+        e[0] = s0.reduce(md);
+        e[MN] = s1.reduce(md);
+        if (j < L) R0[(z * L + j) * NN + k] = __ldg(D + ((long long)L * M + j) * NN + src);
+    }
 }
 
 // GALA schedule 2, stage B (per input bi and group g):

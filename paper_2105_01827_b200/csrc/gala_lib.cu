@@ -1026,13 +1026,21 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
     {
         const int th = N < 256 ? N : 256;
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
-        dim3 ga(B * (baby - 1), M, (N + th - 1) / th);
+        const int cb = B % 4 == 0 ? 4 : (B % 2 == 0 ? 2 : 1);   // inputs per thread (key reuse)
+        dim3 ga((B / cb) * (baby - 1), M, (N + th - 1) / th);
+#define GALA_E(LL)                                                                                              \
+    do {                                                                                                        \
+        if (cb == 4) KLAUNCH(c, "k_gala_e", (k_gala_e<LL, 4><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0))); \
+        else if (cb == 2) KLAUNCH(c, "k_gala_e", (k_gala_e<LL, 2><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0))); \
+        else KLAUNCH(c, "k_gala_e", (k_gala_e<LL, 1><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)));     \
+    } while (0)
         switch (L) {
-            case 1: KLAUNCH(c, "k_gala_e", k_gala_e<1><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
-            case 2: KLAUNCH(c, "k_gala_e", k_gala_e<2><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
-            case 3: KLAUNCH(c, "k_gala_e", k_gala_e<3><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
-            default: KLAUNCH(c, "k_gala_e", k_gala_e<4><<<ga, th, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, E, R0)); break;
+            case 1: GALA_E(1); break;
+            case 2: GALA_E(2); break;
+            case 3: GALA_E(3); break;
+            default: GALA_E(4); break;
         }
+#undef GALA_E
         // one (input, group) per thread (measured best: sharing plaintext loads across inputs, or an
         // smem-tiled modular GEMM, costs occupancy / Montgomery products and runs slower)
         // one member's loads in flight at a time (larger load chunks or sharing plaintext loads across

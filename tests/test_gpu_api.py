@@ -295,7 +295,7 @@ def test_cfg2_fc_1024x4096_n8192():
     rng = np.random.default_rng(2)
     w, x = _int8(rng, (1024, 4096)), rng.integers(0, P, 4096)
     layer = GalaFC(w, params)
-    assert layer.T == 512 and layer.baby == 32
+    assert layer.T == 512 and layer.baby == 64      # schedule-2 baby count (Context.gala2_baby)
     masks = layer.draw_masks(8)
     masked = layer.forward_device(layer.encrypt_input(x), masks)
     got = (layer.client_shares(masked) + layer.server_shares(masks)) % P
