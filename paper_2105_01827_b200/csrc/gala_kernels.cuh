@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(256) k_gala_e(DevCtx c, const u64* __restrict_
 // (CH <= c.lazy[j] products).  grid (N / blockDim, M, B * G), z = bi * G + g (input-major: E of an
 // input stays in L2 while its groups run).
 template <int CH, bool SLICED>
-__global__ void __launch_bounds__(256) k_gala_mac2(DevCtx c, const u64* __restrict__ X, const u64* __restrict__ E,
+__global__ void __launch_bounds__(256, 4) k_gala_mac2(DevCtx c, const u64* __restrict__ X, const u64* __restrict__ E,
                                                    const u64* __restrict__ R0, const u64* __restrict__ pts2, int baby,
                                                    int G, u64* __restrict__ U, u64* __restrict__ Cacc)
 {
@@ -528,24 +528,23 @@ __global__ void __launch_bounds__(256) k_gala_mac2(DevCtx c, const u64* __restri
             a1 = mont_mul(__ldg(x + LN + j * NN + k), w, md);
         }
     }
-    // 128-bit lazy accumulation: one Montgomery reduction per c.lazy[j] products (k q^2 < q 2^64)
+    // 128-bit lazy accumulation: one Montgomery reduction per c.lazy[j] products (k q^2 < q 2^64);
+    // the next member's loads are issued before the current member's products (software pipeline)
     Acc128 s0, s1, sc;
     const int lazy = c.lazy[j];
     int pending = 0;
-    for (int jj0 = 1; jj0 < baby; jj0 += CH) {
-        u64 w[CH], e0[CH], e1[CH], r0[CH];
-#pragma unroll
-        for (int m = 0; m < CH; m++) {
-            const int jj = jj0 + m;
-            w[m] = e0[m] = e1[m] = r0[m] = 0;
-            if (jj < baby) {
-                w[m] = SLICED ? __ldg(Pb + (long long)jj * MN) : __ldcs((const unsigned long long*)(Pb + (long long)jj * MN));
-                e0[m] = __ldg(Eb + (long long)(jj - 1) * 2 * MN);
-                e1[m] = __ldg(Eb + (long long)(jj - 1) * 2 * MN + MN);
-                if (jq) r0[m] = __ldg(Rb + (long long)(jj - 1) * LN);
-            }
-        }
-        if (pending + CH > lazy) {
+    u64 nw = 0, ne0 = 0, ne1 = 0, nr0 = 0;
+    auto fetch = [&](int jj) {
+        nw = SLICED ? __ldg(Pb + (long long)jj * MN) : __ldcs((const unsigned long long*)(Pb + (long long)jj * MN));
+        ne0 = __ldg(Eb + (long long)(jj - 1) * 2 * MN);
+        ne1 = __ldg(Eb + (long long)(jj - 1) * 2 * MN + MN);
+        if (jq) nr0 = __ldg(Rb + (long long)(jj - 1) * LN);
+    };
+    if (baby > 1) fetch(1);
+    for (int jj = 1; jj < baby; jj++) {
+        const u64 w = nw, e0 = ne0, e1 = ne1, r0 = nr0;
+        if (jj + 1 < baby) fetch(jj + 1);
+        if (pending == lazy) {
             u0 = add_mod(u0, s0.reduce(md), q);
             u1 = add_mod(u1, s1.reduce(md), q);
             if (jq) a0 = add_mod(a0, sc.reduce(md), q);
@@ -554,13 +553,10 @@ __global__ void __launch_bounds__(256) k_gala_mac2(DevCtx c, const u64* __restri
             sc = Acc128();
             pending = 0;
         }
-#pragma unroll
-        for (int m = 0; m < CH; m++) {
-            s0.mac(w[m], e0[m]);
-            s1.mac(w[m], e1[m]);
-            if (jq) sc.mac(w[m], r0[m]);
-        }
-        pending += CH;
+        s0.mac(w, e0);
+        s1.mac(w, e1);
+        if (jq) sc.mac(w, r0);
+        pending++;
     }
     u0 = add_mod(u0, s0.reduce(md), q);
     u1 = add_mod(u1, s1.reduce(md), q);

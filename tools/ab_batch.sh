@@ -1,5 +1,5 @@
 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-for b in 32 8; do
+for b in 32; do
 python bench.py --steps 20 --warmup 3 --batch $b --no-cpu-baseline > gpurun_out/abB_${b}.json 2> gpurun_out/abB_${b}.err || tail -3 gpurun_out/abB_${b}.err
 python -c "
 import json; d=json.load(open('gpurun_out/abB_${b}.json'))
