@@ -137,7 +137,7 @@ int gala_kg_encode_weights(gala_ctx *ctx, const int32_t *kernels_dev, int c_o, i
  * The rotated inputs stay in the extended basis QP (no ModDown per rotation); one ModDown per
  * accumulator.  gala_kg2_encode_masks: masks_dev [k_h k_w][pair c_n][L+1][N][2] (NTT, Shoup pairs
  * (w, floor(w 2^64 / q))).
- * gala_conv_kg2: coef_dev int8 [Mr][Kp] (Mr = n_obp c_n rows (o, d); K = (tap, ib, beta)
+ * gala_conv_kg2: coef_dev int8 [Mr][Kp] (Mr = n_obp c_n rows (o, d); K = (ib, tap, beta)
  * columns, zero-padded to Kp % 16 == 0; entry = centred kernel coefficient
  * kern[pair o + row][ib c_n + ch][tap] of band beta = row c_n + ch at rotation offset d),
  * rowsum_dev int32 [Mr] = row sums of coef; outs_dev [n_obp][2][L][N]. */
@@ -149,7 +149,7 @@ int gala_conv_kg2(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64
 /* Post-mask form for frame-embedded inputs (band_only masks [pair c_n][L+1][N][2], no tap
  * factor: exact on every output pixel whose receptive field stays inside the frame's zero margin
  * or halo).  The masks leave the K columns: acc[m] = sum_beta Mask_beta (.) (A_(m, beta) . Z), so the
- * GEMM runs on the bytes of the rotated inputs Z (K = (tap, ib)) with rows (m, beta):
+ * GEMM runs on the bytes of the rotated inputs Z (K = (ib, tap)) with rows (m, beta):
  * coef_dev int8 [Mr nb][Kp], rowsum_dev int32 [Mr nb]. */
 int gala_conv_kg2_post(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *masks_dev, int k, int nb,
                        const int8_t *coef_dev, const int32_t *rowsum_dev, int Mr, int Kp, const int *tap_steps_host,

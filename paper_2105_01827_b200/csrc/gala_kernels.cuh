@@ -700,8 +700,8 @@ __global__ void k_kg_mask_slots(DevCtx c, KgGeom g, uint32_t* __restrict__ out)
     }
 }
 
-// Masked products of the rotated inputs in the extended basis QP, K = (tap, ib, beta),
-// pos = (comp, j, i), g = tap n_ib + ib:
+// Masked products of the rotated inputs in the extended basis QP, K = (ib, tap, beta),
+// pos = (comp, j, i), g = ib k + tap:
 //   Z[g][pos]  = sum_l sigma_tap(D_ib)[l][j][i] ksk_tap[l][comp][j][i] + P sigma_tap(c0_ib)[j][i]
 //                (the key switch without ModDown; P c0 term for comp 0, j < L; Z = P x for step 0)
 //   Y[K][pos]  = Z[g][pos] (.) Mask[tap][beta][j][i]
@@ -759,38 +759,24 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
         const ulonglong2 pc = pconst[j < M ? j : 0];   // P mod q_j, Shoup companion
         const int gpt = KG_KT / nb, g0 = K0 / nb, G = n_ib * k;
         const long long bw = (long long)(L * M + L) * N;
-        // K columns are tap-major (g = tap n_ib + ib): a thread's consecutive groups share the tap, so
-        // its key limbs and sigma source index are loaded once per tap
-        int t_cur = -1, src = 0;
-        const u64* key = nullptr;
-        u64 kl[L];
-#pragma unroll
-        for (int l = 0; l < L; l++) kl[l] = 0;
         for (int gl = w; gl < gpt; gl += 8) {
             const int g = g0 + gl;
             const bool valid = g < G && pos < P2;
             u64 z = 0;
             int t = 0;
             if (valid) {
-                t = g / n_ib;
-                const int ib = g - t * n_ib;
-                if (t != t_cur) {
-                    t_cur = t;
-                    key = keys[t];
-                    if (key != nullptr) {
-                        src = auto_src(i, gal[t], logN);
-                        const u64* kp = key + ((long long)comp * M + j) * N + i;
-#pragma unroll
-                        for (int l = 0; l < L; l++) kl[l] = __ldg(kp + (long long)l * 2 * MN);
-                    }
-                }
+                const int ib = g / k;
+                t = g - ib * k;
+                const u64* key = keys[t];
                 if (key == nullptr) {
                     if (j < L) z = csub(shoup_lazy_sf(__ldg(X + ((long long)ib * 2 + comp) * L * N + jl), pc.x, pc.y, q), q);
                 } else {
+                    const int src = auto_src(i, gal[t], logN);
                     const u64* D = Dblk + ib * bw + (long long)j * N + src;
+                    const u64* kp = key + ((long long)comp * M + j) * N + i;
                     Acc128 s;
 #pragma unroll
-                    for (int l = 0; l < L; l++) s.mac(__ldg(D + (long long)l * MN), kl[l]);
+                    for (int l = 0; l < L; l++) s.mac(__ldg(D + (long long)l * MN), __ldg(kp + (long long)l * 2 * MN));
                     z = s.reduce(md);
                     if (comp == 0 && j < L)
                         z = add_mod(z, csub(shoup_lazy_sf(__ldg(D + (long long)L * MN), pc.x, pc.y, q), q), q);

@@ -292,7 +292,7 @@ def test_kg2_coefficients_factor_the_convolution(n, u, c_o, c_i, pair):
                     ok = (xx + dw >= 0) & (xx + dw < u) & (yy + dh >= 0) & (yy + dh < u)
                     for beta in range(nb):
                         m = ((band == beta) & ok).astype(np.int64)
-                        acc = (acc + int(A[o * c_n + d, (ti * len(phys) + ib) * nb + beta]) * R * m) % P
+                        acc = (acc + int(A[o * c_n + d, (ib * 9 + ti) * nb + beta]) * R * m) % P
             tot = (tot + rot(acc, d * B)) % P
         out.append(tot)
     want = conv2d_mod_p(x, kern, P).reshape(c_o // c_n, -1)
