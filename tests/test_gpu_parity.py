@@ -212,3 +212,33 @@ def test_conv_kg2_post_words(tw):
             got = tw.gpu.decrypt_physical(g_out[ob // pair]).reshape(2, -1)[ob % pair]
             got = got.reshape(c_n, u_h, u_w)[:, :u_h - 1, :u_w - 1]
             assert np.array_equal(got, want[ob * c_n:(ob + 1) * c_n])
+
+
+@pytest.mark.parametrize("ksz,post", [(1, False), (1, True), (5, False), (5, True)])
+def test_conv_kg2_kernel_sizes(tw, ksz, post):
+    """Schedule 2 with 1x1 kernels (no rotated tap: the decomposition is skipped) and 5x5 kernels."""
+    import torch
+
+    from paper_2105_01827_b200.conv import ConvTask, kg2_coefficients, kg2_post_coefficients
+
+    n = tw.bfv.n
+    if n not in KG2_GEOM or n < 256:
+        pytest.skip("no geometry for this ring")
+    u_w, u_h = KG2_GEOM[n]
+    c_n = n // (u_w * u_h)
+    c_i, c_o, pair = 2 * c_n, 2 * c_n, 2
+    kern = tw.rng.integers(-128, 128, (c_o, c_i, ksz, ksz))
+    task = ConvTask(u_w, u_h, c_i, ksz, ksz, c_o, kern, tw.params)
+    taps = [rot for _, _, rot in task.offsets()]
+    tw.keys_for(taps + [d * u_w * u_h for d in range(1, c_n)])
+    x = tw.rng.integers(0, P, (c_i, u_h, u_w))
+    xs = [tw.encrypt(np.concatenate([b, b]).astype(np.uint32)) for b in x.reshape(c_i // c_n, -1)]
+    A, rowsum, K = kg2_coefficients(task, c_n, pair)
+    if post:
+        A, rowsum = kg2_post_coefficients(A, K, pair * c_n)
+    masks = tw.gpu.kg2_encode_masks(ksz, ksz, u_w, u_h, pair, band_only=post)
+    dev = tw.gpu.device
+    g_out = tw.gpu.conv_kg2(torch.stack([g for g, _ in xs]), masks, torch.from_numpy(A).to(dev),
+                            torch.from_numpy(rowsum).to(dev), ksz * ksz, pair * c_n, taps, u_w * u_h, c_n, post=post)
+    c_out = tw.cpu.conv_kg2(np.stack([c for _, c in xs]), kern, u_w, u_h, pair, band_only=post)
+    assert np.array_equal(tw.gpu.export_words(g_out), c_out)

@@ -299,3 +299,42 @@ def test_kg2_coefficients_factor_the_convolution(n, u, c_o, c_i, pair):
     for ob in range(c_o // c_n):
         r = ob % pair if pair == 2 else 0
         assert np.array_equal(out[ob // pair][r * n:(r + 1) * n], want[ob])
+
+
+def test_kg2_post_coefficients_are_a_column_regrouping():
+    """Post-mask matrix [(m, beta)][(ib, tap)] holds exactly the pre-mask entries A[m][(ib, tap, beta)]."""
+    from paper_2105_01827_b200.backend import HEParams
+    from paper_2105_01827_b200.conv import ConvTask, kg2_coefficients, kg2_post_coefficients
+
+    rng = np.random.default_rng(4)
+    n, u, c_i, c_o = 64, 4, 8, 12
+    t = ConvTask(u, u, c_i, 3, 3, c_o, rng.integers(-128, 128, (c_o, c_i, 3, 3)), HEParams(n=n, p=1032193))
+    c_n = n // (u * u)
+    for pair in (1, 2):
+        nb = pair * c_n
+        A, _, K = kg2_coefficients(t, c_n, pair)
+        B, rs = kg2_post_coefficients(A, K, nb)
+        Kq = K // nb
+        assert B.shape == (A.shape[0] * nb, (Kq + 15) // 16 * 16)
+        assert np.array_equal(rs, B.astype(np.int64).sum(axis=1))
+        for m in range(A.shape[0]):
+            for beta in range(nb):
+                assert np.array_equal(B[m * nb + beta, :Kq], A[m, beta:K:nb])
+        assert not B[:, Kq:].any()
+
+
+def test_kg_schedule_selection():
+    """Schedule 2 needs L >= 2, int8 kernels and c_n <= KG2_MAX_CN; otherwise schedule 1."""
+    from paper_2105_01827_b200.backend import HEParams
+    from paper_2105_01827_b200.conv import KG2_MAX_CN, ConvTask, kg_schedule
+
+    p = 1032193
+    params = HEParams(n=64, p=p)
+    small = ConvTask(8, 8, 2, 3, 3, 2, np.ones((2, 2, 3, 3), dtype=np.int64), params)
+    assert kg_schedule(small, 1, 3) == 2
+    assert kg_schedule(small, 1, 1) == 1                       # one 62-bit prime: noise budget
+    assert kg_schedule(small, KG2_MAX_CN * 2, 3) == 1          # too many bands
+    big = ConvTask(8, 8, 2, 3, 3, 2, np.full((2, 2, 3, 3), 300, dtype=np.int64), params)
+    assert kg_schedule(big, 1, 3) == 1                         # not int8 after centring
+    neg = ConvTask(8, 8, 2, 3, 3, 2, np.full((2, 2, 3, 3), p - 128, dtype=np.int64), params)
+    assert kg_schedule(neg, 1, 3) == 2                         # -128 mod p centres into int8
