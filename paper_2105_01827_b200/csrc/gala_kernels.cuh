@@ -880,6 +880,160 @@ __global__ void k_kg_recombine_post(DevCtx c, const int32_t* __restrict__ C, con
 }
 
 // ---------------------------------------------------------------------------
+// Conv schedule 2, post-mask form, fused on the 5th-generation tensor cores (tcgen05):
+//   D[(m, beta)][(pos, b)] = sum_K A[(m, beta)][K] * Bt[8 pos + b][K]          (int8 x int8 -> int32, TMEM)
+//   acc[m][pos]            = sum_beta Mask[beta][pos] (.) rec(D[(m, beta)][(pos, 0..7)])  mod q_j
+// One CTA owns a 128-row block of A (resident in shared memory) and walks 256-column tiles of Bt
+// (32 QP words x 8 byte planes).  Thread 0 issues K/32 tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32)
+// from SWIZZLE_NONE K-major descriptors and commits to an mbarrier; the 4 warps then read their 32
+// TMEM lanes (= rows) with tcgen05.ld.32x32b.x8 (one QP word's 8 byte sums per load), rebuild each
+// word mod q exactly, multiply by the row's band mask and sum the nb bands with warp shuffles.
+// No int32 GEMM output ever reaches HBM.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo)
+{
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;   // descriptor version 1 (sm_100); base offset 0, SWIZZLE_NONE
+    return d;
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+
+// K-major, no swizzle: 16-byte chunk (row r, k-chunk c) at (r % 8) 16 + (r / 8) SBO + c 128, SBO = 8 Kp
+__device__ __forceinline__ uint32_t kg_tc_off(int r, int c, int Kp) { return (r & 7) * 16 + (r >> 3) * 8 * Kp + c * 128; }
+
+#define KG_TC_N 256
+__global__ void __launch_bounds__(128, 1) k_kg_tc(DevCtx c, const int8_t* __restrict__ A, const int32_t* __restrict__ rowsum,
+                                                 int rows_real, int nb, int Mr, const int8_t* __restrict__ Bt, int Kp,
+                                                 int ntiles, const ulonglong2* __restrict__ off,
+                                                 const ulonglong2* __restrict__ masks, u64* __restrict__ accq)
+{
+    extern __shared__ __align__(128) uint8_t kg_sm[];
+    uint8_t* sA = kg_sm;                              // 128 x Kp
+    uint8_t* sB = kg_sm + 128 * Kp;                   // 256 x Kp
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base_sh;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rb = blockIdx.x;
+    const int kc = Kp / 16;                           // 16-byte chunks per row
+    // A block -> shared memory (constant for the CTA)
+    for (int q = tid; q < 128 * (kc / 2); q += 128) {
+        const int r = q % 128, c2 = q / 128;          // rows fastest: 32-byte global reads, conflict-free stores
+        const int R = rb * 128 + r;
+        const uint4* src = (const uint4*)(A + (long long)R * Kp + c2 * 32);
+        const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
+        *(uint4*)(sA + kg_tc_off(r, 2 * c2, Kp)) = v0;
+        *(uint4*)(sA + kg_tc_off(r, 2 * c2 + 1, Kp)) = v1;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(KG_TC_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base_sh;
+    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(KG_TC_N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t aaddr = smem_u32(sA), baddr = smem_u32(sB);
+    // epilogue constants of this thread's row
+    const int r = warp * 32 + lane, R = rb * 128 + r;
+    const bool row_ok = R < rows_real;
+    const int m = R / nb, beta = R - m * nb;
+    const long long bias = row_ok ? 128LL * rowsum[R] : 0;
+    const long long MN = (long long)c.M * c.N, WQ = 2 * MN;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.y; tile < ntiles; tile += gridDim.y) {
+        const long long pos0 = (long long)tile * (KG_TC_N / 8);
+        // B tile: rows 8 pos0 .. 8 pos0 + 255 of Bt (contiguous) -> shared memory
+        const int8_t* gB = Bt + pos0 * 8 * Kp;
+        for (int q = tid; q < KG_TC_N * (kc / 2); q += 128) {
+            const int rr = q % KG_TC_N, c2 = q / KG_TC_N;
+            const uint4* src = (const uint4*)(gB + (long long)rr * Kp + c2 * 32);
+            const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
+            *(uint4*)(sB + kg_tc_off(rr, 2 * c2, Kp)) = v0;
+            *(uint4*)(sB + kg_tc_off(rr, 2 * c2 + 1, Kp)) = v1;
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (tid == 0) {
+            for (int ks = 0; ks < Kp / 32; ks++) {
+                const uint64_t ad = umma_desc_kmajor(aaddr + ks * 256, 128, 8 * Kp);
+                const uint64_t bd = umma_desc_kmajor(baddr + ks * 256, 128, 8 * Kp);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                    ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&mbar)));
+        }
+        while (!mbar_try_wait(smem_u32(&mbar), phase)) {
+        }
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        // epilogue: 32 QP words per row
+        const int jq = (int)((pos0 % MN) / c.N);        // the tile never straddles a prime (N % 32 == 0)
+        const ModC md = c.mod[jq];
+        const ulonglong2 o = off[jq];
+        u64 keep[4];
+        for (int p = 0; p < KG_TC_N / 8; p++) {
+            uint32_t x[8];
+            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(8 * p);
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
+                         : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const long long pos = pos0 + p;
+            u64 v = 0;
+            if (row_ok) {
+                __int128 t = 0;
+#pragma unroll
+                for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)(int32_t)x[b] + bias);
+                unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
+                const u64 w = mont_mul(csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q), md.r2, md);
+                const ulonglong2 mk = __ldg(masks + (long long)beta * MN + (pos % MN));
+                v = csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q);
+            }
+            for (int sh = 1; sh < nb; sh <<= 1) v = add_mod(v, __shfl_xor_sync(0xffffffffu, v, sh), md.q);
+            keep[p & 3] = v;
+            if ((p & 3) == 3 && beta == 0 && row_ok && m < Mr) {
+                u64* dst = accq + (long long)m * WQ + pos - 3;
+                *(ulonglong2*)dst = make_ulonglong2(keep[0], keep[1]);
+                *(ulonglong2*)(dst + 2) = make_ulonglong2(keep[2], keep[3]);
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();   // TMEM drained and shared B tile free before the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(KG_TC_N));
+}
+
+// ---------------------------------------------------------------------------
 // encoding.  MODE 0: plaintext operand (centred lift, Montgomery);
 //            MODE 1: Delta * m (plain), for encrypt / subtract_plain
 // one CTA per (vector b, prime j); each CTA recomputes the mod-p INTT (cheap,

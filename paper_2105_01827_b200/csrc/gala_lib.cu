@@ -18,6 +18,8 @@
 #include <vector>
 
 #include "gala_kernels.cuh"
+
+static const int kMaxDynSmem = 220 * 1024;   // k_kg_tc: 384 Kp bytes of A + B tiles
 #include "../../include/gala_b200.h"
 
 typedef unsigned __int128 u128;
@@ -132,6 +134,7 @@ struct gala_ctx {
     std::vector<cudaEvent_t> pool;
     cublasLtHandle_t lt = nullptr;            // int8 tensor-core GEMM of the conv schedule 2 first-Add
     u64* d_kg_off = nullptr;                  // per prime: multiple of q >= 2^90 (128-bit, hi/lo)
+    int num_sms = 148;
 };
 
 static void prof_begin(gala_ctx* c, cudaEvent_t* a, cudaEvent_t* b)
@@ -660,6 +663,13 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_ntt_inv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_ntt_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_moddown, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_kg_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        c->num_sms = sms > 0 ? sms : 148;
+    }
     CKC(cudaFuncSetAttribute(k_digits_intt, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_digits_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_block_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
@@ -1428,33 +1438,55 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     release(c, dig);
     release(c, Dblk);
     release(c, d_blob);
-    // 3. exact integer first-Add on the tensor cores: C[Mp][8 WQ] = A . Bt (rows padded to 16)
-    const int Mp = (rows + 15) / 16 * 16;
-    const int8_t* A = coef;
-    int8_t* Apad = nullptr;
-    if (Mp != rows) {
-        RET(scratch(c, &Apad, (size_t)Mp * Kp));
-        CK(cudaMemsetAsync(Apad, 0, (size_t)Mp * Kp, c->stream));
-        CK(cudaMemcpyAsync(Apad, coef, (size_t)rows * Kp, cudaMemcpyDeviceToDevice, c->stream));
-        A = Apad;
-    }
-    int32_t* C;
-    RET(scratch(c, &C, (size_t)8 * WQ * Mp));
-    RET(lt_gemm_i8(c, A, Kp, Bt, Kp, C, Mp, Mp, 8 * WQ, Kp, 0));
-    release(c, Bt);
-    release(c, Apad);
-    // 4. recombine bytes -> words mod q_j over QP
     u64* accq;
     RET(scratch(c, &accq, (size_t)Mr * WQ));
-    if (post) {
-        KLAUNCH(c, "k_kg_recombine_post", k_kg_recombine_post<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
-                                              c->dc, C, rowsum, Mr, nb, Mp, (const ulonglong2*)c->d_kg_off,
-                                              (const ulonglong2*)masks, accq));
+    // fused tcgen05 path: post-mask form, bands within a warp, K in 32-byte steps, A + B tiles in smem
+    const bool tc = post && nb <= 32 && (32 % nb) == 0 && Kp % 32 == 0 && 384LL * Kp <= kMaxDynSmem &&
+                    (c->dc.N % 32) == 0 && getenv("GALA_KG_NO_TC") == nullptr;
+    if (tc) {
+        // 3+4. first-Add on the tensor cores with the byte recombination and band masks in the epilogue
+        const int rows_p = (rows + 127) / 128 * 128;
+        int8_t* Apad;
+        RET(scratch(c, &Apad, (size_t)rows_p * Kp));
+        CK(cudaMemsetAsync(Apad, 0, (size_t)rows_p * Kp, c->stream));
+        CK(cudaMemcpyAsync(Apad, coef, (size_t)rows * Kp, cudaMemcpyDeviceToDevice, c->stream));
+        const int ntiles = (int)(8 * WQ / KG_TC_N);
+        const int rbs = rows_p / 128;
+        int gy = (2 * c->num_sms + rbs - 1) / rbs;
+        if (gy > ntiles) gy = ntiles;
+        dim3 grid((unsigned)rbs, (unsigned)gy);
+        KLAUNCH(c, "k_kg_tc", k_kg_tc<<<grid, 128, (size_t)384 * Kp, c->stream>>>(
+                                  c->dc, Apad, rowsum, rows, nb, Mr, Bt, Kp, ntiles, (const ulonglong2*)c->d_kg_off,
+                                  (const ulonglong2*)masks, accq));
+        release(c, Apad);
+        release(c, Bt);
     } else {
-        KLAUNCH(c, "k_kg_recombine", k_kg_recombine<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
-                                         c->dc, C, rowsum, Mr, Mp, (const ulonglong2*)c->d_kg_off, accq));
+        // 3. exact integer first-Add on the tensor cores: C[Mp][8 WQ] = A . Bt (rows padded to 16)
+        const int Mp = (rows + 15) / 16 * 16;
+        const int8_t* A = coef;
+        int8_t* Apad = nullptr;
+        if (Mp != rows) {
+            RET(scratch(c, &Apad, (size_t)Mp * Kp));
+            CK(cudaMemsetAsync(Apad, 0, (size_t)Mp * Kp, c->stream));
+            CK(cudaMemcpyAsync(Apad, coef, (size_t)rows * Kp, cudaMemcpyDeviceToDevice, c->stream));
+            A = Apad;
+        }
+        int32_t* C;
+        RET(scratch(c, &C, (size_t)8 * WQ * Mp));
+        RET(lt_gemm_i8(c, A, Kp, Bt, Kp, C, Mp, Mp, 8 * WQ, Kp, 0));
+        release(c, Bt);
+        release(c, Apad);
+        // 4. recombine bytes -> words mod q_j over QP
+        if (post) {
+            KLAUNCH(c, "k_kg_recombine_post", k_kg_recombine_post<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
+                                                  c->dc, C, rowsum, Mr, nb, Mp, (const ulonglong2*)c->d_kg_off,
+                                                  (const ulonglong2*)masks, accq));
+        } else {
+            KLAUNCH(c, "k_kg_recombine", k_kg_recombine<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
+                                             c->dc, C, rowsum, Mr, Mp, (const ulonglong2*)c->d_kg_off, accq));
+        }
+        release(c, C);
     }
-    release(c, C);
     // 5. one ModDown per accumulator (straight into outs when there is no second-Perm)
     u64 *acc = outs, *rr;
     if (c_n > 1) RET(scratch(c, &acc, (size_t)Mr * W));

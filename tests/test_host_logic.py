@@ -315,7 +315,7 @@ def test_kg2_post_coefficients_are_a_column_regrouping():
         A, _, K = kg2_coefficients(t, c_n, pair)
         B, rs = kg2_post_coefficients(A, K, nb)
         Kq = K // nb
-        assert B.shape == (A.shape[0] * nb, (Kq + 15) // 16 * 16)
+        assert B.shape == (A.shape[0] * nb, (Kq + 31) // 32 * 32)
         assert np.array_equal(rs, B.astype(np.int64).sum(axis=1))
         for m in range(A.shape[0]):
             for beta in range(nb):
