@@ -918,24 +918,27 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase)
 __device__ __forceinline__ uint32_t kg_tc_off(int r, int c, int Kp) { return (r & 7) * 16 + (r >> 3) * 8 * Kp + c * 128; }
 
 #define KG_TC_N 256
-__global__ void __launch_bounds__(128, 1) k_kg_tc(DevCtx c, const int8_t* __restrict__ A, const int32_t* __restrict__ rowsum,
-                                                 int rows_real, int nb, int Mr, const int8_t* __restrict__ Bt, int Kp,
-                                                 int ntiles, const ulonglong2* __restrict__ off,
-                                                 const ulonglong2* __restrict__ masks, u64* __restrict__ accq)
+#define KG_TC_THREADS 512
+// 16 warps: warp w reads TMEM lanes 32 (w % 4) (its 32 rows) for the 8 QP words 8 (w / 4) .. + 7 of
+// the tile.  Two CTAs per SM overlap one CTA's tile load + MMA with the other's epilogue.
+__global__ void __launch_bounds__(KG_TC_THREADS, 2) k_kg_tc(DevCtx c, const int8_t* __restrict__ A,
+                                                           const int32_t* __restrict__ rowsum, int rows_real, int nb,
+                                                           int Mr, const int8_t* __restrict__ Bt, int Kp, int ntiles,
+                                                           const ulonglong2* __restrict__ off,
+                                                           const ulonglong2* __restrict__ masks, u64* __restrict__ accq)
 {
     extern __shared__ __align__(128) uint8_t kg_sm[];
-    uint8_t* sA = kg_sm;                              // 128 x Kp
-    uint8_t* sB = kg_sm + 128 * Kp;                   // 256 x Kp
+    uint8_t* sA = kg_sm;                                              // 128 x Kp
+    uint8_t* sB = kg_sm + 128 * Kp;                                   // 256 x Kp
+    ulonglong2* sMask = (ulonglong2*)(kg_sm + 384 * Kp);              // [nb][32]
     __shared__ uint64_t mbar;
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rb = blockIdx.x;
-    const int kc = Kp / 16;                           // 16-byte chunks per row
-    // A block -> shared memory (constant for the CTA)
-    for (int q = tid; q < 128 * (kc / 2); q += 128) {
-        const int r = q % 128, c2 = q / 128;          // rows fastest: 32-byte global reads, conflict-free stores
-        const int R = rb * 128 + r;
-        const uint4* src = (const uint4*)(A + (long long)R * Kp + c2 * 32);
+    const int kc2 = Kp / 32;                                          // 32-byte pieces per row
+    for (int q = tid; q < 128 * kc2; q += KG_TC_THREADS) {            // A block -> smem (once)
+        const int r = q % 128, c2 = q / 128;
+        const uint4* src = (const uint4*)(A + (long long)(rb * 128 + r) * Kp + c2 * 32);
         const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
         *(uint4*)(sA + kg_tc_off(r, 2 * c2, Kp)) = v0;
         *(uint4*)(sA + kg_tc_off(r, 2 * c2 + 1, Kp)) = v1;
@@ -956,24 +959,27 @@ __global__ void __launch_bounds__(128, 1) k_kg_tc(DevCtx c, const int8_t* __rest
     const uint32_t tmem = tmem_base_sh;
     const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(KG_TC_N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t aaddr = smem_u32(sA), baddr = smem_u32(sB);
-    // epilogue constants of this thread's row
-    const int r = warp * 32 + lane, R = rb * 128 + r;
+    const int lg = warp & 3, cq = warp >> 2;                          // TMEM lane group, word quarter
+    const int r = lg * 32 + lane, R = rb * 128 + r;
     const bool row_ok = R < rows_real;
     const int m = R / nb, beta = R - m * nb;
     const long long bias = row_ok ? 128LL * rowsum[R] : 0;
-    const long long MN = (long long)c.M * c.N, WQ = 2 * MN;
+    const int MN = c.M * c.N;
+    const long long WQ = 2LL * MN;
     uint32_t phase = 0;
     for (int tile = blockIdx.y; tile < ntiles; tile += gridDim.y) {
         const long long pos0 = (long long)tile * (KG_TC_N / 8);
-        // B tile: rows 8 pos0 .. 8 pos0 + 255 of Bt (contiguous) -> shared memory
+        const int jl0 = (int)(pos0 % MN);
         const int8_t* gB = Bt + pos0 * 8 * Kp;
-        for (int q = tid; q < KG_TC_N * (kc / 2); q += 128) {
+        for (int q = tid; q < KG_TC_N * kc2; q += KG_TC_THREADS) {
             const int rr = q % KG_TC_N, c2 = q / KG_TC_N;
             const uint4* src = (const uint4*)(gB + (long long)rr * Kp + c2 * 32);
             const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
             *(uint4*)(sB + kg_tc_off(rr, 2 * c2, Kp)) = v0;
             *(uint4*)(sB + kg_tc_off(rr, 2 * c2 + 1, Kp)) = v1;
         }
+        for (int q = tid; q < nb * 32; q += KG_TC_THREADS)            // the tile's band masks
+            sMask[q] = __ldg(masks + (long long)(q >> 5) * MN + jl0 + (q & 31));
         asm volatile("fence.proxy.async.shared::cta;");
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();
@@ -994,39 +1000,49 @@ __global__ void __launch_bounds__(128, 1) k_kg_tc(DevCtx c, const int8_t* __rest
         }
         phase ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;");
-        // epilogue: 32 QP words per row
-        const int jq = (int)((pos0 % MN) / c.N);        // the tile never straddles a prime (N % 32 == 0)
+        const int jq = jl0 / c.N;                                     // a tile never straddles a prime
         const ModC md = c.mod[jq];
         const ulonglong2 o = off[jq];
-        u64 keep[4];
-        for (int p = 0; p < KG_TC_N / 8; p++) {
-            uint32_t x[8];
-            const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(8 * p);
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
-                         : "r"(taddr));
+#pragma unroll 1
+        for (int h = 0; h < 2; h++) {                                 // 2 x 4 words per warp
+            const int p0 = cq * 8 + h * 4;
+            uint32_t x[32];
+            const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(8 * p0);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
+                  "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15]),
+                  "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]), "=r"(x[21]), "=r"(x[22]), "=r"(x[23]),
+                  "=r"(x[24]), "=r"(x[25]), "=r"(x[26]), "=r"(x[27]), "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
+                : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const long long pos = pos0 + p;
-            u64 v = 0;
-            if (row_ok) {
-                __int128 t = 0;
+            u64 v[4];
 #pragma unroll
-                for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)(int32_t)x[b] + bias);
-                unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
-                const u64 w = mont_mul(csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q), md.r2, md);
-                const ulonglong2 mk = __ldg(masks + (long long)beta * MN + (pos % MN));
-                v = csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q);
+            for (int w4 = 0; w4 < 4; w4++) {
+                v[w4] = 0;
+                if (row_ok) {
+                    __int128 t = 0;
+#pragma unroll
+                    for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)(int32_t)x[w4 * 8 + b] + bias);
+                    unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
+                    const u64 w = mont_mul(csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q), md.r2, md);
+                    const ulonglong2 mk = sMask[beta * 32 + p0 + w4];
+                    v[w4] = csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q);
+                }
             }
-            for (int sh = 1; sh < nb; sh <<= 1) v = add_mod(v, __shfl_xor_sync(0xffffffffu, v, sh), md.q);
-            keep[p & 3] = v;
-            if ((p & 3) == 3 && beta == 0 && row_ok && m < Mr) {
-                u64* dst = accq + (long long)m * WQ + pos - 3;
-                *(ulonglong2*)dst = make_ulonglong2(keep[0], keep[1]);
-                *(ulonglong2*)(dst + 2) = make_ulonglong2(keep[2], keep[3]);
+            for (int sh = 1; sh < nb; sh <<= 1) {
+#pragma unroll
+                for (int w4 = 0; w4 < 4; w4++) v[w4] = add_mod(v[w4], __shfl_xor_sync(0xffffffffu, v[w4], sh), md.q);
+            }
+            if (beta == 0 && row_ok && m < Mr) {
+                u64* dst = accq + (long long)m * WQ + pos0 + p0;
+                *(ulonglong2*)dst = make_ulonglong2(v[0], v[1]);
+                *(ulonglong2*)(dst + 2) = make_ulonglong2(v[2], v[3]);
             }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();   // TMEM drained and shared B tile free before the next tile
+        __syncthreads();   // TMEM drained and shared tiles free before the next tile
         asm volatile("tcgen05.fence::after_thread_sync;");
     }
     __syncthreads();

@@ -1441,7 +1441,7 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     u64* accq;
     RET(scratch(c, &accq, (size_t)Mr * WQ));
     // fused tcgen05 path: post-mask form, bands within a warp, K in 32-byte steps, A + B tiles in smem
-    const bool tc = post && nb <= 32 && (32 % nb) == 0 && Kp % 32 == 0 && 384LL * Kp <= kMaxDynSmem &&
+    const bool tc = post && nb <= 32 && (32 % nb) == 0 && Kp % 32 == 0 && 384LL * Kp + 512LL * nb <= kMaxDynSmem &&
                     (c->dc.N % 32) == 0 && getenv("GALA_KG_NO_TC") == nullptr;
     if (tc) {
         // 3+4. first-Add on the tensor cores with the byte recombination and band masks in the epilogue
@@ -1455,7 +1455,7 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         int gy = (2 * c->num_sms + rbs - 1) / rbs;
         if (gy > ntiles) gy = ntiles;
         dim3 grid((unsigned)rbs, (unsigned)gy);
-        KLAUNCH(c, "k_kg_tc", k_kg_tc<<<grid, 128, (size_t)384 * Kp, c->stream>>>(
+        KLAUNCH(c, "k_kg_tc", k_kg_tc<<<grid, KG_TC_THREADS, (size_t)384 * Kp + 512 * nb, c->stream>>>(
                                   c->dc, Apad, rowsum, rows, nb, Mr, Bt, Kp, ntiles, (const ulonglong2*)c->d_kg_off,
                                   (const ulonglong2*)masks, accq));
         release(c, Apad);
