@@ -744,7 +744,7 @@ template <int L>
 __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__ Dblk, const u64* __restrict__ X,
                                                const u64* const* __restrict__ keys, const unsigned* __restrict__ gal,
                                                const ulonglong2* __restrict__ masks, const ulonglong2* __restrict__ pconst,
-                                               int k, int nb, int n_ib, int Kp, int8_t* __restrict__ Bt)
+                                               int k, int nb, int n_ib, int Kp, int8_t* __restrict__ Bt, int canon)
 {
     __shared__ u64 sm[KG_PT * KG_KT];
     constexpr int M = L + 1;
@@ -819,6 +819,12 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
         bytes4x4(hi[4 * q4], hi[4 * q4 + 1], hi[4 * q4 + 2], hi[4 * q4 + 3], o);
 #pragma unroll
         for (int b = 0; b < 4; b++) pl[4 + b][q4] = o[b];
+    }
+    if (canon) {   // tcgen05 tile layout: [tile = pos / 32][16-byte K chunk][256 rows (pos % 32, b)][16]
+        int8_t* o = Bt + ((((long long)(pos >> 5) * (Kp >> 4) + (K0 >> 4) + ch) * 256) + 8 * (pos & 31)) * 16;
+#pragma unroll
+        for (int b = 0; b < 8; b++) *(uint4*)(o + b * 16) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
+        return;
     }
     int8_t* o = Bt + (long long)pos * 8 * Kp + K0 + ch * 16;
 #pragma unroll
@@ -918,135 +924,232 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase)
 __device__ __forceinline__ uint32_t kg_tc_off(int r, int c, int Kp) { return (r & 7) * 16 + (r >> 3) * 8 * Kp + c * 128; }
 
 #define KG_TC_N 256
-#define KG_TC_THREADS 512
-// 16 warps: warp w reads TMEM lanes 32 (w % 4) (its 32 rows) for the 8 QP words 8 (w / 4) .. + 7 of
-// the tile.  Two CTAs per SM overlap one CTA's tile load + MMA with the other's epilogue.
-__global__ void __launch_bounds__(KG_TC_THREADS, 2) k_kg_tc(DevCtx c, const int8_t* __restrict__ A,
-                                                           const int32_t* __restrict__ rowsum, int rows_real, int nb,
-                                                           int Mr, const int8_t* __restrict__ Bt, int Kp, int ntiles,
-                                                           const ulonglong2* __restrict__ off,
+#define KG_TC_KCS 4          // 16-byte K chunks per pipeline stage (two K = 32 MMAs)
+#define KG_TC_STAGES 4
+#define KG_TC_EPI_WARPS 16
+#define KG_TC_THREADS ((2 + KG_TC_EPI_WARPS) * 32)
+// Warp-specialized persistent kernel (one CTA per SM, 512 TMEM columns = two 128 x 256 int32
+// accumulators):
+//   warp 0 (one lane): producer -- per stage one cp.async.bulk of the A chunks ([rb][chunk][128][16])
+//                      and one of the B chunks ([tile][chunk][256][16]), completing on full[s];
+//   warp 1 (one lane): MMA issuer -- waits full[s], issues tcgen05.mma.kind::i8 (M 128, N 256, K 32)
+//                      from SWIZZLE_NONE K-major descriptors, commits empty[s]; after the last
+//                      stage of a job commits tfull[acc];
+//   warps 2..17:       epilogue -- stage the job's band masks in shared memory, wait tfull[acc],
+//                      read TMEM (warp w: lanes 32 (w % 4), 8 words), rebuild each word mod q,
+//                      multiply by the band mask, sum the nb bands with shuffles, store; arrive
+//                      tempty[acc].
+// Jobs = (tile, row block) pairs, row block fastest (consecutive jobs share the B tile in L2).
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity)
+{
+    while (!mbar_try_wait(smem_u32(b), parity)) {
+    }
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* b)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8_t* __restrict__ Acan,
+                                                           const int32_t* __restrict__ rowsum, int rows_real, int rbs,
+                                                           int nb, int Mr, const int8_t* __restrict__ Bcan, int Kp,
+                                                           int ntiles, const ulonglong2* __restrict__ off,
                                                            const ulonglong2* __restrict__ masks, u64* __restrict__ accq)
 {
     extern __shared__ __align__(128) uint8_t kg_sm[];
-    uint8_t* sA = kg_sm;                                              // 128 x Kp
-    uint8_t* sB = kg_sm + 128 * Kp;                                   // 256 x Kp
-    ulonglong2* sMask = (ulonglong2*)(kg_sm + 384 * Kp);              // [nb][32]
-    __shared__ uint64_t mbar;
+    constexpr int STAGE_BYTES = KG_TC_KCS * (128 + KG_TC_N) * 16;
+    uint8_t* ring = kg_sm;                                                   // [STAGES][A chunks | B chunks]
+    ulonglong2* sMask = (ulonglong2*)(kg_sm + KG_TC_STAGES * STAGE_BYTES);  // [2][nb][32]
+    __shared__ uint64_t full[KG_TC_STAGES], empty[KG_TC_STAGES], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int rb = blockIdx.x;
-    const int kc2 = Kp / 32;                                          // 32-byte pieces per row
-    for (int q = tid; q < 128 * kc2; q += KG_TC_THREADS) {            // A block -> smem (once)
-        const int r = q % 128, c2 = q / 128;
-        const uint4* src = (const uint4*)(A + (long long)(rb * 128 + r) * Kp + c2 * 32);
-        const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
-        *(uint4*)(sA + kg_tc_off(r, 2 * c2, Kp)) = v0;
-        *(uint4*)(sA + kg_tc_off(r, 2 * c2 + 1, Kp)) = v1;
-    }
+    const int KC = Kp / 16, nst = (KC + KG_TC_KCS - 1) / KG_TC_KCS;
+    const long long jobs = (long long)ntiles * rbs;
+    const long long per = (jobs + gridDim.x - 1) / gridDim.x;
+    const long long j0 = blockIdx.x * per, j1 = j0 + per < jobs ? j0 + per : jobs;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
-                     "r"(KG_TC_N));
+                     "r"(2 * KG_TC_N));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    if (tid == 32) {
+        for (int i = 0; i < KG_TC_STAGES; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], KG_TC_EPI_WARPS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
-    asm volatile("fence.proxy.async.shared::cta;");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base_sh;
-    const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(KG_TC_N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    const uint32_t aaddr = smem_u32(sA), baddr = smem_u32(sB);
-    const int lg = warp & 3, cq = warp >> 2;                          // TMEM lane group, word quarter
-    const int r = lg * 32 + lane, R = rb * 128 + r;
-    const bool row_ok = R < rows_real;
-    const int m = R / nb, beta = R - m * nb;
-    const long long bias = row_ok ? 128LL * rowsum[R] : 0;
-    const int MN = c.M * c.N;
-    const long long WQ = 2LL * MN;
-    uint32_t phase = 0;
-    for (int tile = blockIdx.y; tile < ntiles; tile += gridDim.y) {
-        const long long pos0 = (long long)tile * (KG_TC_N / 8);
-        const int jl0 = (int)(pos0 % MN);
-        const int8_t* gB = Bt + pos0 * 8 * Kp;
-        for (int q = tid; q < KG_TC_N * kc2; q += KG_TC_THREADS) {
-            const int rr = q % KG_TC_N, c2 = q / KG_TC_N;
-            const uint4* src = (const uint4*)(gB + (long long)rr * Kp + c2 * 32);
-            const uint4 v0 = __ldg(src), v1 = __ldg(src + 1);
-            *(uint4*)(sB + kg_tc_off(rr, 2 * c2, Kp)) = v0;
-            *(uint4*)(sB + kg_tc_off(rr, 2 * c2 + 1, Kp)) = v1;
-        }
-        for (int q = tid; q < nb * 32; q += KG_TC_THREADS)            // the tile's band masks
-            sMask[q] = __ldg(masks + (long long)(q >> 5) * MN + jl0 + (q & 31));
-        asm volatile("fence.proxy.async.shared::cta;");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (tid == 0) {
-            for (int ks = 0; ks < Kp / 32; ks++) {
-                const uint64_t ad = umma_desc_kmajor(aaddr + ks * 256, 128, 8 * Kp);
-                const uint64_t bd = umma_desc_kmajor(baddr + ks * 256, 128, 8 * Kp);
-                asm volatile(
-                    "{\n\t.reg .pred p;\n\t"
-                    "setp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                    ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
-            }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&mbar)));
-        }
-        while (!mbar_try_wait(smem_u32(&mbar), phase)) {
-        }
-        phase ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const int jq = jl0 / c.N;                                     // a tile never straddles a prime
-        const ModC md = c.mod[jq];
-        const ulonglong2 o = off[jq];
-#pragma unroll 1
-        for (int h = 0; h < 2; h++) {                                 // 2 x 4 words per warp
-            const int p0 = cq * 8 + h * 4;
-            uint32_t x[32];
-            const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(8 * p0);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-                "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-                : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
-                  "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15]),
-                  "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]), "=r"(x[21]), "=r"(x[22]), "=r"(x[23]),
-                  "=r"(x[24]), "=r"(x[25]), "=r"(x[26]), "=r"(x[27]), "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            u64 v[4];
-#pragma unroll
-            for (int w4 = 0; w4 < 4; w4++) {
-                v[w4] = 0;
-                if (row_ok) {
-                    __int128 t = 0;
-#pragma unroll
-                    for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)(int32_t)x[w4 * 8 + b] + bias);
-                    unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
-                    const u64 w = mont_mul(csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q), md.r2, md);
-                    const ulonglong2 mk = sMask[beta * 32 + p0 + w4];
-                    v[w4] = csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q);
+    if (warp == 0) {
+        if (lane == 0) {   // producer
+            int s = 0;
+            uint32_t ph = 0;
+            for (long long jb = j0; jb < j1; jb++) {
+                const int rb = (int)(jb % rbs);
+                const long long tile = jb / rbs;
+                for (int g = 0; g < nst; g++) {
+                    const int ch0 = g * KG_TC_KCS, n = KC - ch0 < KG_TC_KCS ? KC - ch0 : KG_TC_KCS;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = ring + s * STAGE_BYTES;
+                    mbar_expect_tx(&full[s], (uint32_t)(n * (128 + KG_TC_N) * 16));
+                    bulk_g2s(st, Acan + ((long long)rb * KC + ch0) * 128 * 16, n * 128 * 16, &full[s]);
+                    bulk_g2s(st + n * 128 * 16, Bcan + (tile * KC + ch0) * KG_TC_N * 16, n * KG_TC_N * 16, &full[s]);
+                    if (++s == KG_TC_STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
             }
-            for (int sh = 1; sh < nb; sh <<= 1) {
-#pragma unroll
-                for (int w4 = 0; w4 < 4; w4++) v[w4] = add_mod(v[w4], __shfl_xor_sync(0xffffffffu, v[w4], sh), md.q);
-            }
-            if (beta == 0 && row_ok && m < Mr) {
-                u64* dst = accq + (long long)m * WQ + pos0 + p0;
-                *(ulonglong2*)dst = make_ulonglong2(v[0], v[1]);
-                *(ulonglong2*)(dst + 2) = make_ulonglong2(v[2], v[3]);
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // MMA issuer
+            const uint32_t idesc =
+                (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(KG_TC_N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (long long jb = j0; jb < j1; jb++, it++) {
+                const int acc = it & 1;
+                const uint32_t tph = (uint32_t)((it >> 1) & 1);
+                mbar_wait(&tempty[acc], tph ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(acc * KG_TC_N);
+                for (int g = 0; g < nst; g++) {
+                    const int ch0 = g * KG_TC_KCS, n = KC - ch0 < KG_TC_KCS ? KC - ch0 : KG_TC_KCS;
+                    mbar_wait(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa = smem_u32(ring + s * STAGE_BYTES), sb = sa + n * 128 * 16;
+                    for (int kk = 0; kk < n / 2; kk++) {
+                        const uint64_t ad = umma_desc_kmajor(sa + kk * 2 * 128 * 16, 128 * 16, 128);
+                        const uint64_t bd = umma_desc_kmajor(sb + kk * 2 * KG_TC_N * 16, KG_TC_N * 16, 128);
+                        const uint32_t accum = (g > 0 || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\t"
+                            "setp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                            ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+                    }
+                    umma_commit(&empty[s]);
+                    if (++s == KG_TC_STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
             }
         }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();   // TMEM drained and shared tiles free before the next tile
-        asm volatile("tcgen05.fence::after_thread_sync;");
+    } else {   // epilogue warps
+        const int ew = warp - 2, et = tid - 64;
+        const int lg = warp & 3, cq = ew >> 2;                       // TMEM lane group (warp % 4), word quarter
+        const int r = lg * 32 + lane;
+        const int MN = c.M * c.N;
+        const long long WQ = 2LL * MN;
+        int it = 0;
+        for (long long jb = j0; jb < j1; jb++, it++) {
+            const int acc = it & 1;
+            const int rb = (int)(jb % rbs);
+            const long long tile = jb / rbs;
+            const long long pos0 = tile * (KG_TC_N / 8);
+            const int jl0 = (int)(pos0 % MN);
+            ulonglong2* sm = sMask + acc * nb * 32;
+            for (int q = et; q < nb * 32; q += KG_TC_EPI_WARPS * 32)
+                sm[q] = __ldg(masks + (long long)(q >> 5) * MN + jl0 + (q & 31));
+            asm volatile("bar.sync 1, %0;" ::"n"(KG_TC_EPI_WARPS * 32));
+            const int R = rb * 128 + r;
+            const bool row_ok = R < rows_real;
+            const int m = R / nb, beta = R - m * nb;
+            const long long bias = row_ok ? 128LL * rowsum[R] : 0;
+            const int jq = jl0 / c.N;                                // a tile never straddles a prime
+            const ModC md = c.mod[jq];
+            const ulonglong2 o = off[jq];
+            mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+            for (int h = 0; h < 2; h++) {
+                const int p0 = cq * 8 + h * 4;
+                uint32_t x[32];
+                const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * KG_TC_N + 8 * p0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                    "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                    : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
+                      "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15]),
+                      "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]), "=r"(x[21]), "=r"(x[22]), "=r"(x[23]),
+                      "=r"(x[24]), "=r"(x[25]), "=r"(x[26]), "=r"(x[27]), "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (h == 1) {   // this warp's TMEM reads of the job are done
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                }
+                u64 v[4];
+#pragma unroll
+                for (int w4 = 0; w4 < 4; w4++) {
+                    v[w4] = 0;
+                    if (row_ok) {
+                        __int128 t = 0;
+#pragma unroll
+                        for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)(int32_t)x[w4 * 8 + b] + bias);
+                        unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
+                        const u64 w = mont_mul(csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q), md.r2, md);
+                        const ulonglong2 mk = sm[beta * 32 + p0 + w4];
+                        v[w4] = csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q);
+                    }
+                }
+                for (int sh = 1; sh < nb; sh <<= 1) {
+#pragma unroll
+                    for (int w4 = 0; w4 < 4; w4++) v[w4] = add_mod(v[w4], __shfl_xor_sync(0xffffffffu, v[w4], sh), md.q);
+                }
+                if (beta == 0 && row_ok && m < Mr) {
+                    u64* dst = accq + (long long)m * WQ + pos0 + p0;
+                    *(ulonglong2*)dst = make_ulonglong2(v[0], v[1]);
+                    *(ulonglong2*)(dst + 2) = make_ulonglong2(v[2], v[3]);
+                }
+            }
+            // the mask buffer of this accumulator is rewritten two jobs later: all epilogue warps
+            // are past it once they pass the next job's bar.sync
+        }
     }
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(KG_TC_N));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * KG_TC_N));
+}
+
+// [rows_p][Kp] row-major -> [rows_p / 128][Kp / 16][128][16] (tcgen05 K-major core-matrix order)
+__global__ void k_kg_tc_layout_a(const int8_t* __restrict__ A, int rows, int rows_p, int Kp, int8_t* __restrict__ out)
+{
+    const int KC = Kp / 16;
+    const long long total = (long long)rows_p * KC;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int r = (int)(e % rows_p), ch = (int)(e / rows_p);
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < rows) v = *(const uint4*)(A + (long long)r * Kp + ch * 16);
+        *(uint4*)(out + (((long long)(r >> 7) * KC + ch) * 128 + (r & 127)) * 16) = v;
+    }
 }
 
 // ---------------------------------------------------------------------------

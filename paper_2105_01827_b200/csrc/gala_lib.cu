@@ -19,7 +19,6 @@
 
 #include "gala_kernels.cuh"
 
-static const int kMaxDynSmem = 220 * 1024;   // k_kg_tc: 384 Kp bytes of A + B tiles
 #include "../../include/gala_b200.h"
 
 typedef unsigned __int128 u128;
@@ -663,7 +662,8 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_ntt_inv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_ntt_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_moddown, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CKC(cudaFuncSetAttribute(k_kg_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    CKC(cudaFuncSetAttribute(k_kg_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             KG_TC_STAGES * KG_TC_KCS * (128 + KG_TC_N) * 16 + 2 * 512 * 32));
     {
         int dev = 0, sms = 0;
         cudaGetDevice(&dev);
@@ -1416,6 +1416,10 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(n_ib * L * L), nt, c->smem_ntt, c->stream>>>(
                                         c->dc, (const TermDesc*)d_blob, d_gal, blk_words));
     }
+    // fused tcgen05 path (post-mask form, bands within a warp, K in 32-byte steps): the byte planes are
+    // written in the tensor-core tile order so every pipeline stage is one bulk copy
+    const bool tc = post && nb <= 32 && (32 % nb) == 0 && Kp % 32 == 0 && (c->dc.N % 32) == 0 &&
+                    getenv("GALA_KG_NO_TC") == nullptr;
     // 2. fused key switch (no ModDown) + band masks -> biased bytes, K-contiguous: Bt[8 WQ][Kp]
     int8_t* Bt;
     RET(scratch(c, &Bt, (size_t)8 * WQ * Kp));
@@ -1426,7 +1430,7 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
 #define KG_ZY(LL)                                                                                                  \
     KLAUNCH(c, "k_kg_zy", k_kg_zy<LL><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1,                \
                                                                    post ? nullptr : (const ulonglong2*)masks, pm, k,  \
-                                                                   nb_y, n_ib, Kp, Bt))
+                                                                   nb_y, n_ib, Kp, Bt, tc ? 1 : 0))
         switch (L) {
             case 1: KG_ZY(1); break;
             case 2: KG_ZY(2); break;
@@ -1440,25 +1444,22 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     release(c, d_blob);
     u64* accq;
     RET(scratch(c, &accq, (size_t)Mr * WQ));
-    // fused tcgen05 path: post-mask form, bands within a warp, K in 32-byte steps, A + B tiles in smem
-    const bool tc = post && nb <= 32 && (32 % nb) == 0 && Kp % 32 == 0 && 384LL * Kp + 512LL * nb <= kMaxDynSmem &&
-                    (c->dc.N % 32) == 0 && getenv("GALA_KG_NO_TC") == nullptr;
     if (tc) {
         // 3+4. first-Add on the tensor cores with the byte recombination and band masks in the epilogue
         const int rows_p = (rows + 127) / 128 * 128;
-        int8_t* Apad;
-        RET(scratch(c, &Apad, (size_t)rows_p * Kp));
-        CK(cudaMemsetAsync(Apad, 0, (size_t)rows_p * Kp, c->stream));
-        CK(cudaMemcpyAsync(Apad, coef, (size_t)rows * Kp, cudaMemcpyDeviceToDevice, c->stream));
+        int8_t* Acan;
+        RET(scratch(c, &Acan, (size_t)rows_p * Kp));
+        KLAUNCH(c, "k_kg_tc_layout_a", k_kg_tc_layout_a<<<grid_for((long long)rows_p * Kp / 16, 256), 256, 0, c->stream>>>(
+                                           coef, rows, rows_p, Kp, Acan));
         const int ntiles = (int)(8 * WQ / KG_TC_N);
         const int rbs = rows_p / 128;
-        int gy = (2 * c->num_sms + rbs - 1) / rbs;
-        if (gy > ntiles) gy = ntiles;
-        dim3 grid((unsigned)rbs, (unsigned)gy);
-        KLAUNCH(c, "k_kg_tc", k_kg_tc<<<grid, KG_TC_THREADS, (size_t)384 * Kp + 512 * nb, c->stream>>>(
-                                  c->dc, Apad, rowsum, rows, nb, Mr, Bt, Kp, ntiles, (const ulonglong2*)c->d_kg_off,
+        long long jobs = (long long)ntiles * rbs;
+        const int grid = (int)(jobs < c->num_sms ? jobs : c->num_sms);
+        const size_t smem = (size_t)KG_TC_STAGES * KG_TC_KCS * (128 + KG_TC_N) * 16 + 2 * 512 * (size_t)nb;
+        KLAUNCH(c, "k_kg_tc", k_kg_tc<<<grid, KG_TC_THREADS, smem, c->stream>>>(
+                                  c->dc, Acan, rowsum, rows, rbs, nb, Mr, Bt, Kp, ntiles, (const ulonglong2*)c->d_kg_off,
                                   (const ulonglong2*)masks, accq));
-        release(c, Apad);
+        release(c, Acan);
         release(c, Bt);
     } else {
         // 3. exact integer first-Add on the tensor cores: C[Mp][8 WQ] = A . Bt (rows padded to 16)
