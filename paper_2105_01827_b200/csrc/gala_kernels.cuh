@@ -718,14 +718,18 @@ __device__ __forceinline__ int kg_swz(int pp, int kk) { return pp * KG_KT + (kk 
 
 // Montgomery-form operands [count][M][N] -> Shoup pairs (w, floor(w 2^64 / q)).  With w_m = w 2^64
 // mod q: w = REDC(w_m) and w 2^64 = q wsh + w_m, so wsh = (w 2^64 - w_m) / q = w_m (-q^-1) mod 2^64.
-__global__ void k_mont_to_shoup(DevCtx c, const u64* __restrict__ in, long long count, ulonglong2* __restrict__ out)
+// keep_mont: Shoup pairs of the Montgomery value itself, (w_m, floor(w_m 2^64 / q)) -- multiplying a
+// REDC output (x 2^-64) by w_m = w 2^64 gives x w directly (the post-mask epilogues use this).
+__global__ void k_mont_to_shoup(DevCtx c, const u64* __restrict__ in, long long count, int keep_mont,
+                                ulonglong2* __restrict__ out)
 {
     const int N = c.N, M = c.M;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count * M * N;
          e += (long long)gridDim.x * blockDim.x) {
         const ModC md = c.mod[(int)((e / N) % M)];
         const u64 wm = in[e];
-        out[e] = make_ulonglong2(csub(redc_lazy(0, wm, md), md.q), wm * md.qinv_neg);
+        if (keep_mont) out[e] = make_ulonglong2(wm, mont_mul(wm, md.r2, md) * md.qinv_neg);
+        else out[e] = make_ulonglong2(csub(redc_lazy(0, wm, md), md.q), wm * md.qinv_neg);
     }
 }
 
@@ -831,6 +835,21 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
     for (int b = 0; b < 8; b++) *(uint4*)(o + (long long)b * Kp) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
 }
 
+// sum_b (x_b + bias) 256^b (signed, |.| < 2^90) made non-negative with off (a multiple of q >= 2^90)
+// and Montgomery-reduced once: returns (that sum) 2^-64 mod q.  Two 64-bit halves instead of a
+// 128-bit shift chain.
+__device__ __forceinline__ u64 kg_rec_redc(const uint32_t* x, long long bias, ulonglong2 off, const ModC& md)
+{
+    const long long b4 = bias * 0x01010101LL;
+    const long long lo = (long long)(int32_t)x[0] + ((long long)(int32_t)x[1] << 8) + ((long long)(int32_t)x[2] << 16) +
+                         ((long long)(int32_t)x[3] << 24) + b4;
+    const long long hi = (long long)(int32_t)x[4] + ((long long)(int32_t)x[5] << 8) + ((long long)(int32_t)x[6] << 16) +
+                         ((long long)(int32_t)x[7] << 24) + b4;
+    const __int128 t = ((__int128)hi << 32) + (__int128)lo + (((__int128)off.x << 64) | (__int128)off.y);
+    const unsigned __int128 u = (unsigned __int128)t;
+    return csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q);
+}
+
 // One word of the integer first-Add back from its byte planes: (sum_b (C[8 pos + b][m] + 128 rowsum)
 // 256^b) mod q.  C is the int32 GEMM output (column-major, leading dimension ld).  The signed
 // 128-bit total is made non-negative with a multiple of q (off >= 2^90) and reduced exactly with
@@ -875,9 +894,12 @@ __global__ void k_kg_recombine_post(DevCtx c, const int32_t* __restrict__ C, con
         const int j = (int)(jl / c.N);
         const ModC md = c.mod[j];
         u64 a = 0;
-        for (int beta = 0; beta < nb; beta++) {
+        for (int beta = 0; beta < nb; beta++) {   // masks are Montgomery-form Shoup pairs
             const int r = m * nb + beta;
-            const u64 w = kg_rec_word(C, pos, Mp, r, 128LL * rowsum[r], off[j], md);
+            uint32_t x[8];
+#pragma unroll
+            for (int b = 0; b < 8; b++) x[b] = (uint32_t)C[(8 * pos + b) * Mp + r];
+            const u64 w = kg_rec_redc(x, 128LL * rowsum[r], off[j], md);
             const ulonglong2 mk = __ldg(masks + (long long)beta * MN + jl);
             a = add_mod(a, csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q), md.q);
         }
@@ -1112,23 +1134,36 @@ __global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8
                 for (int w4 = 0; w4 < 4; w4++) {
                     v[w4] = 0;
                     if (row_ok) {
-                        __int128 t = 0;
-#pragma unroll
-                        for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)(int32_t)x[w4 * 8 + b] + bias);
-                        unsigned __int128 u = (unsigned __int128)(t + (((__int128)o.x << 64) | (__int128)o.y));
-                        const u64 w = mont_mul(csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q), md.r2, md);
-                        const ulonglong2 mk = sm[beta * 32 + p0 + w4];
+                        const u64 w = kg_rec_redc(x + 8 * w4, bias, o, md);
+                        const ulonglong2 mk = sm[beta * 32 + p0 + w4];   // Montgomery-form mask
                         v[w4] = csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q);
                     }
                 }
-                for (int sh = 1; sh < nb; sh <<= 1) {
-#pragma unroll
-                    for (int w4 = 0; w4 < 4; w4++) v[w4] = add_mod(v[w4], __shfl_xor_sync(0xffffffffu, v[w4], sh), md.q);
-                }
-                if (beta == 0 && row_ok && m < Mr) {
-                    u64* dst = accq + (long long)m * WQ + pos0 + p0;
-                    *(ulonglong2*)dst = make_ulonglong2(v[0], v[1]);
-                    *(ulonglong2*)(dst + 2) = make_ulonglong2(v[2], v[3]);
+                // sum the nb band rows (lanes beta = 0..nb-1 of the group) as a reduce-scatter over
+                // the 4 words: the first two rounds halve the words each lane carries
+                u64* dstrow = accq + (long long)m * WQ + pos0 + p0;
+                const bool wr = row_ok && m < Mr;
+                if (nb == 1) {
+                    if (wr) {
+                        *(ulonglong2*)dstrow = make_ulonglong2(v[0], v[1]);
+                        *(ulonglong2*)(dstrow + 2) = make_ulonglong2(v[2], v[3]);
+                    }
+                } else {
+                    const int sa = nb >> 1;
+                    const bool ba = (beta & sa) != 0;
+                    const u64 s0 = ba ? v[0] : v[2], s1 = ba ? v[1] : v[3];
+                    const u64 r0 = __shfl_xor_sync(0xffffffffu, s0, sa), r1 = __shfl_xor_sync(0xffffffffu, s1, sa);
+                    const u64 w0 = add_mod(ba ? v[2] : v[0], r0, md.q), w1 = add_mod(ba ? v[3] : v[1], r1, md.q);
+                    if (nb == 2) {      // lane beta holds words 2 beta, 2 beta + 1
+                        if (wr) *(ulonglong2*)(dstrow + (ba ? 2 : 0)) = make_ulonglong2(w0, w1);
+                    } else {
+                        const int sb = nb >> 2;
+                        const bool bb = (beta & sb) != 0;
+                        const u64 rr = __shfl_xor_sync(0xffffffffu, bb ? w0 : w1, sb);
+                        u64 z = add_mod(bb ? w1 : w0, rr, md.q);
+                        for (int sh = nb >> 3; sh >= 1; sh >>= 1) z = add_mod(z, __shfl_xor_sync(0xffffffffu, z, sh), md.q);
+                        if (wr && (beta & (sb - 1)) == 0) dstrow[(ba ? 2 : 0) + (bb ? 1 : 0)] = z;
+                    }
                 }
             }
             // the mask buffer of this accumulator is rewritten two jobs later: all epilogue warps

@@ -1273,7 +1273,7 @@ int gala_kg2_encode_masks(gala_ctx* c, int k_h, int k_w, int u_w, int u_h, int p
                                    c->dc, slots + (long long)first * N, mont + (long long)first * M * N));
     }
     KLAUNCH(c, "k_mont_to_shoup", k_mont_to_shoup<<<grid_for((long long)count * M * N, 256), 256, 0, c->stream>>>(
-                                      c->dc, mont, count, (ulonglong2*)masks));
+                                      c->dc, mont, count, band_only ? 1 : 0, (ulonglong2*)masks));
     release(c, slots);
     release(c, mont);
     (void)L;
