@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--baby", type=int, default=0, help="BSGS baby-step count (0: library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tensor-cores", action="store_true", help="CUDA-core baby-step sums (k_gala_mac2)")
     ap.add_argument("--profile-only", action="store_true", help="run one profiled step and print the breakdown")
     return ap.parse_args()
 
@@ -167,7 +168,7 @@ def run_ours(args):
 
     params = HEParams(n=SLOTS, p=P, rns_limbs=3, device=local, seed=7)
     t_setup = time.perf_counter()
-    layer = GalaFC(weights(), params, baby=args.baby or None)
+    layer = GalaFC(weights(), params, baby=args.baby or None, tensor_cores=not args.no_tensor_cores)
     ctx = layer.ctx
     N, L, T, baby = ctx.N, ctx.L, layer.T, layer.baby
     B = args.batch
@@ -247,6 +248,13 @@ def run_ours(args):
 
     def e2e_step():
         # one C-ABI call per step: H2D of B canonical ciphertexts + masks, fused layers, D2H of masked words
+        if layer.schedule == 2 and layer.wcan[0] is not None:
+            _lib.check(ctx.lib.gala_mv_gala2_batch_tc_host(h, ctypes.c_void_p(host_ct.data_ptr()), B,
+                                                           ctypes.c_void_p(pts.data_ptr()),
+                                                           ctypes.c_void_p(layer.wcan[0].data_ptr()), T, baby,
+                                                           ctypes.c_void_p(host_r.data_ptr()),
+                                                           ctypes.c_void_p(host_out.data_ptr())))
+            return
         host_fn = ctx.lib.gala_mv_gala2_batch_host if layer.schedule == 2 else ctx.lib.gala_mv_gala_batch_host
         _lib.check(host_fn(h, ctypes.c_void_p(host_ct.data_ptr()), B,
                                                    ctypes.c_void_p(pts.data_ptr()), T, baby,
@@ -322,6 +330,7 @@ def run_ours(args):
         "data": "synthetic (seeded int8 weights mapped to Z_p, uniform Z_p inputs)",
         "config": {"workload": WORKLOAD, "layer": "GALA FC 1024x4096 (2 paired MvTasks of 512x4096, T=512)",
                    "gala_schedule": layer.schedule,
+                   "baby_step_sums": "tcgen05 int8 MMA" if layer.wcan[0] is not None and B <= 32 else "CUDA cores",
                    "N": N, "L": L, "special_primes": 1, "p": P, "bsgs_baby": baby, "batch_per_gpu": B,
                    "parallelism": f"replicas x{world} (independent inputs per GPU)",
                    "l2": "flushed (256 MB write) before every timed step"},

@@ -118,6 +118,20 @@ int gala_mv_gala_host(gala_ctx *ctx, const uint64_t *ct_host, const uint64_t *pt
 int gala_mv_gala_batch_host(gala_ctx *ctx, const uint64_t *cts_host, int B, const uint64_t *pts_dev, int T,
                             int baby, const uint32_t *r_slots_host, uint64_t *masked_host);
 
+/* GALA schedule 2 with the baby-step sums on the int8 tensor cores (tcgen05): the weights' byte
+ * convolution (Toeplitz) expansion, built once per layer by gala_fc_tc_weights into wcan_dev
+ * (gala_fc_tc_weight_bytes bytes: 64 KB per QP position), is the MMA B operand; E_jj is packed
+ * per position as the A operand.  Same words as gala_mv_gala2_batch (exact modular arithmetic).
+ * Needs B <= 32, T/baby <= 8 and baby <= 64; otherwise the CUDA-core path runs. */
+size_t gala_fc_tc_weight_bytes(gala_ctx *ctx);
+int gala_fc_tc_weights(gala_ctx *ctx, const uint64_t *pts2_dev, int T, int baby, uint8_t *wcan_dev);
+int gala_mv_gala2_batch_tc(gala_ctx *ctx, const uint64_t *cts_dev, int B, const uint64_t *pts2_dev,
+                           const uint8_t *wcan_dev, int T, int baby, const uint32_t *r_slots_dev,
+                           uint64_t *outs_dev, uint64_t *masked_dev);
+int gala_mv_gala2_batch_tc_host(gala_ctx *ctx, const uint64_t *cts_host, int B, const uint64_t *pts2_dev,
+                                const uint8_t *wcan_dev, int T, int baby, const uint32_t *r_slots_host,
+                                uint64_t *masked_host);
+
 /* Fused kernel-grouping convolution (mimo_kernel_grouping, conv.py:268-293):
  * cts_dev [n_ib][2][L][N]; pts_dev [n_obp][n_ib][c_n][k][L][N];
  * tap_steps_host [k] (rotation per tap, conv.py:84-91); out [n_obp][2][L][N] */

@@ -437,17 +437,34 @@ class Context:
         self.call("gala_encode_gala_weights", ctypes.c_void_p(_ptr(d_sl)), T, int(baby), ctypes.c_void_p(_ptr(pts2)))
         return pts2
 
-    def mv_gala2_batch(self, cts, pts2, T: int, d_r=None, baby: int | None = None, outs=None, masked=None):
+    def mv_gala2_batch(self, cts, pts2, T: int, d_r=None, baby: int | None = None, outs=None, masked=None,
+                       wcan=None):
+        """Schedule 2; with ``wcan`` (``fc_tc_weights``) the baby-step sums run on the tensor cores."""
         b, steps = self.bsgs_steps(T, baby)
         self.ensure_keys(steps)
         B = cts.shape[0]
         outs = self.empty_ct(B) if outs is None else outs
         if d_r is not None and masked is None:
             masked = self.empty_ct(B)
-        self.call("gala_mv_gala2_batch", ctypes.c_void_p(_ptr(cts)), int(B), ctypes.c_void_p(_ptr(pts2)), int(T),
-                  int(b), ctypes.c_void_p(_ptr(d_r)) if d_r is not None else None, ctypes.c_void_p(_ptr(outs)),
-                  ctypes.c_void_p(_ptr(masked)) if masked is not None else None)
+        common = (ctypes.c_void_p(_ptr(cts)), int(B), ctypes.c_void_p(_ptr(pts2)))
+        tail = (int(T), int(b), ctypes.c_void_p(_ptr(d_r)) if d_r is not None else None, ctypes.c_void_p(_ptr(outs)),
+                ctypes.c_void_p(_ptr(masked)) if masked is not None else None)
+        if wcan is not None:
+            self.call("gala_mv_gala2_batch_tc", *common, ctypes.c_void_p(_ptr(wcan)), *tail)
+        else:
+            self.call("gala_mv_gala2_batch", *common, *tail)
         return outs, masked
+
+    def fc_tc_supported(self, T: int, baby: int) -> bool:
+        return T % baby == 0 and T // baby <= 8 and baby <= 64 and self.N % 32 == 0
+
+    def fc_tc_weights(self, pts2, T: int, baby: int):
+        """Byte-convolution expansion of schedule-2 weights for the tensor-core baby-step sums."""
+        torch = _torch()
+        nbytes = int(self.lib.gala_fc_tc_weight_bytes(self._bind()))
+        wcan = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.call("gala_fc_tc_weights", ctypes.c_void_p(_ptr(pts2)), int(T), int(baby), ctypes.c_void_p(_ptr(wcan)))
+        return wcan
 
     def conv_kg(self, cts, pts, tap_steps, band_step: int):
         """cts [n_ib][2][L][N]; pts [n_obp][n_ib][c_n][k][L][N] -> [n_obp][2][L][N]."""

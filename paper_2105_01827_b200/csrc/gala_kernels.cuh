@@ -1188,6 +1188,256 @@ __global__ void k_kg_tc_layout_a(const int8_t* __restrict__ A, int rows, int row
 }
 
 // ---------------------------------------------------------------------------
+// GALA schedule 2 on the tensor cores.  Per QP position p = (j, k) the baby-step sums are a small
+// integer matrix product over the baby rotations jj:
+//   Out[(s, bi)][g] = sum_jj X_s[bi][jj] w[g][jj],   X_0 = E_c0, X_1 = E_c1, X_2 = sigma_jj(c0)
+// With 8-byte operands X = sum_a 256^a X_a, w = sum_b 256^b w_b:
+//   Out = sum_s' 256^s' D_s',  D[(s, bi)][(g, s')] = sum_(jj, a) X_a[(s, bi)][jj] * w_(s' - a)[g][jj]
+// -- one int8 MMA per position with A = the bytes of X in their natural little-endian order
+// (K = (jj, a)), and B = the byte-convolution (Toeplitz) expansion of the weights (column
+// (g, s'), 0 <= s' < 15).  D < 63 * 8 * 255^2 < 2^25 is exact in int32 and sum_s' 256^s' D_s' is
+// the exact integer sum_jj X w < 2^126, reduced once mod q (w is in Montgomery form, so the REDC
+// yields sum X w mod q).  Operands are stored in the tcgen05 SWIZZLE_NONE K-major core-matrix
+// order: 16-byte chunk (row r, chunk kc) at (r / 8) 4096 + kc 128 + (r % 8) 16.
+//   Ecan: per position 12 row groups (rows s 32 + bi, s < 3, bi < 32) = 48 KB
+//   Wcan: per position 16 row groups (rows g 16 + s', g < 8) = 64 KB (built once per layer)
+#define GTC_A_BYTES (12 * 4096)
+#define GTC_B_BYTES (16 * 4096)
+__device__ __forceinline__ u64 bswap64(u64 w)
+{
+    const uint32_t lo = (uint32_t)w, hi = (uint32_t)(w >> 32);
+    return ((u64)__byte_perm(lo, 0, 0x0123) << 32) | (u64)__byte_perm(hi, 0, 0x0123);
+}
+
+// Wcan[p][(g, s')][(jj', a)] = byte (s' - a) of w[g b + jj' + 1][p]  (0 outside [0, 7] or jj' + 1 >= b)
+__global__ void k_gala_wcan(DevCtx c, const u64* __restrict__ pts2, int baby, int G, uint8_t* __restrict__ Wcan)
+{
+    const long long MN = (long long)c.M * c.N;
+    const long long total = MN * 128 * 32;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int kc = (int)(e & 31), n = (int)((e >> 5) & 127);
+        const long long p = e >> 12;
+        const int g = n >> 4, sp = n & 15;
+        u64 t[2];
+#pragma unroll
+        for (int jw = 0; jw < 2; jw++) {
+            const int jj = 2 * kc + jw + 1;
+            const u64 w = (g < G && jj < baby) ? __ldg(pts2 + (long long)(g * baby + jj) * MN + p) : 0;
+            const u64 rev = bswap64(w);
+            t[jw] = sp <= 7 ? rev >> (8 * (7 - sp)) : (sp == 15 ? 0 : rev << (8 * (sp - 7)));
+        }
+        *(ulonglong2*)(Wcan + p * GTC_B_BYTES + (n >> 3) * 4096 + kc * 128 + (n & 7) * 16) = make_ulonglong2(t[0], t[1]);
+    }
+}
+
+// E_jj, sigma_jj(c0) for every (input, baby rotation), written as Ecan (k_gala_e's math).  grid (N / 32,
+// 32 chunks, M), 256 threads: thread (position kk, 4 inputs) computes the two rotations of chunk kc.
+template <int L>
+__global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restrict__ Dblk, const u64* const* __restrict__ keys,
+                                                    const unsigned* __restrict__ gal, int baby, int B, uint8_t* __restrict__ Ecan)
+{
+    __shared__ u64 sm[32][96][2];
+    constexpr int M = L + 1;
+    const int N = c.N, logN = c.logN;
+    const int j = blockIdx.z, kc = blockIdx.y, k0 = blockIdx.x * 32;
+    const int kk = threadIdx.x & 31, bg = threadIdx.x >> 5;
+    const int k = k0 + kk;
+    const ModC md = c.mod[j];
+    const long long NN = N, MN = (long long)M * N, bw = (long long)(L * M + L) * N;
+#pragma unroll
+    for (int jw = 0; jw < 2; jw++) {
+        const int jj = 2 * kc + jw + 1;
+        const bool valid = jj < baby;
+        u64 ka[L], kb[L];
+        int src = 0;
+        if (valid) {
+            const u64* key = keys[jj];
+            src = auto_src(k, gal[jj], logN);
+#pragma unroll
+            for (int i = 0; i < L; i++) {
+                ka[i] = __ldg(key + (((long long)i * 2 + 0) * M + j) * NN + k);
+                kb[i] = __ldg(key + (((long long)i * 2 + 1) * M + j) * NN + k);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int bi = bg * 4 + q;
+            u64 e0 = 0, e1 = 0, r0 = 0;
+            if (valid && bi < B) {
+                const u64* D = Dblk + (long long)bi * bw;
+                Acc128 s0, s1;
+#pragma unroll
+                for (int i = 0; i < L; i++) {
+                    const u64 d = __ldg(D + ((long long)i * M + j) * NN + src);
+                    s0.mac(d, ka[i]);
+                    s1.mac(d, kb[i]);
+                }
+                e0 = s0.reduce(md);
+                e1 = s1.reduce(md);
+                if (j < L) r0 = __ldg(D + ((long long)L * M + j) * NN + src);
+            }
+            sm[kk][bi][jw] = e0;
+            sm[kk][32 + bi][jw] = e1;
+            sm[kk][64 + bi][jw] = r0;
+        }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 32 * 96; idx += 256) {
+        const int kk2 = idx / 96, r = idx - kk2 * 96;
+        const long long p = (long long)j * N + k0 + kk2;
+        *(ulonglong2*)(Ecan + p * GTC_A_BYTES + (r >> 3) * 4096 + kc * 128 + (r & 7) * 16) =
+            make_ulonglong2(sm[kk2][r][0], sm[kk2][r][1]);
+    }
+}
+
+// The baby-step sums of every (input, group) at every position on the tensor cores.  Warp-specialized
+// persistent kernel, one CTA per SM: warp 0 lane 0 bulk-copies each position's A (Ecan) and B (Wcan)
+// tiles into a 2-stage ring; warp 1 lane 0 issues 16 tcgen05.mma.kind::i8 (M 128, N 128, K 32,
+// unsigned bytes) into one of two TMEM accumulators; warps 2..5 (TMEM lane group s = warp % 4 ->
+// stream s, lane = input) rebuild each (input, stream, group) sum from its 15 byte-shifted columns,
+// reduce it mod q once and write U / Cacc (adding the step-0 member for stream 2).
+#define GTC_THREADS 192
+template <int L>
+__global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint8_t* __restrict__ Ecan,
+                                                          const uint8_t* __restrict__ Wcan, const u64* __restrict__ X,
+                                                          const u64* __restrict__ pts2, int baby, int G, int B,
+                                                          u64* __restrict__ U, u64* __restrict__ Cacc)
+{
+    extern __shared__ __align__(128) uint8_t gtc_sm[];
+    constexpr int M = L + 1;
+    constexpr int STAGE = GTC_A_BYTES + GTC_B_BYTES;
+    __shared__ uint64_t full[2], empty[2], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base_sh;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int N = c.N;
+    const long long MN = (long long)M * N, npos = MN;
+    const long long per = (npos + gridDim.x - 1) / gridDim.x;
+    const long long p0 = blockIdx.x * per, p1 = p0 + per < npos ? p0 + per : npos;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base_sh;
+    if (warp == 0) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (long long p = p0; p < p1; p++) {
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t* st = gtc_sm + s * STAGE;
+                mbar_expect_tx(&full[s], (uint32_t)STAGE);
+                bulk_g2s(st, Ecan + p * GTC_A_BYTES, GTC_A_BYTES, &full[s]);
+                bulk_g2s(st + GTC_A_BYTES, Wcan + p * GTC_B_BYTES, GTC_B_BYTES, &full[s]);
+                if (++s == 2) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (long long p = p0; p < p1; p++, it++) {
+                const int acc = it & 1;
+                mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
+                mbar_wait(&full[s], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sa = smem_u32(gtc_sm + s * STAGE), sb = sa + GTC_A_BYTES;
+                const uint32_t d = tmem + (uint32_t)(acc * 128);
+#pragma unroll 1
+                for (int ks = 0; ks < 16; ks++) {
+                    const uint64_t ad = umma_desc_kmajor(sa + ks * 256, 128, 4096);
+                    const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\t"
+                        "setp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                        ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
+                }
+                umma_commit(&empty[s]);
+                umma_commit(&tfull[acc]);
+                if (++s == 2) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else {   // epilogue: TMEM lane group lg = warp % 4 holds rows 32 lg .. (stream s = lg, input = lane)
+        const int lg = warp & 3, sidx = lg, bi = lane;
+        const long long W = 2LL * L * N;
+        int it = 0;
+        for (long long p = p0; p < p1; p++, it++) {
+            const int acc = it & 1;
+            const int j = (int)(p / N), k = (int)(p - (long long)j * N);
+            const ModC md = c.mod[j];
+            const u64 q = md.q;
+            mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const bool active = sidx < 2 || (sidx == 2 && j < L);
+            u64 xc0 = 0, xc1 = 0;
+            if (sidx == 2 && active && bi < B) {
+                xc0 = __ldg(X + (long long)bi * W + (long long)j * N + k);
+                xc1 = __ldg(X + (long long)bi * W + (long long)(L + j) * N + k);
+            }
+            for (int g = 0; g < G; g++) {
+                uint32_t x[16];
+                const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + g * 16);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                    "%14, %15}, [%16];"
+                    : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
+                      "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (!active || bi >= B) continue;
+                // sum_s' 256^s' D_s' (exact, < 2^126): three 40-bit-spaced partial sums below 2^58
+                u64 lo5 = 0, mi5 = 0, hi5 = 0;
+#pragma unroll
+                for (int t = 0; t < 5; t++) {
+                    lo5 += (u64)x[t] << (8 * t);
+                    mi5 += (u64)x[5 + t] << (8 * t);
+                    hi5 += (u64)x[10 + t] << (8 * t);
+                }
+                u64 lo = lo5 + (mi5 << 40);
+                u64 hi = (mi5 >> 24) + (hi5 << 16) + (lo < lo5 ? 1ull : 0ull);
+                if (hi >= 2 * q) hi -= 2 * q;
+                if (hi >= 2 * q) hi -= 2 * q;
+                if (hi >= q) hi -= q;
+                const u64 v = csub(redc_lazy(hi, lo, md), q);   // sum_jj X w   (w Montgomery)
+                const long long z = (long long)bi * G + g;
+                if (sidx < 2) {
+                    U[((z * 2 + sidx) * M + j) * (long long)N + k] = v;
+                } else {
+                    const u64 w0 = __ldg(pts2 + (long long)(g * baby) * MN + p);   // step-0 member
+                    Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = add_mod(v, mont_mul(xc0, w0, md), q);
+                    Cacc[((z * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, w0, md);
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// ---------------------------------------------------------------------------
 // encoding.  MODE 0: plaintext operand (centred lift, Montgomery);
 //            MODE 1: Delta * m (plain), for encrypt / subtract_plain
 // one CTA per (vector b, prime j); each CTA recomputes the mod-p INTT (cheap,

@@ -662,6 +662,10 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_ntt_inv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_ntt_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_moddown, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_gala_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (GTC_A_BYTES + GTC_B_BYTES)));
+    CKC(cudaFuncSetAttribute(k_gala_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (GTC_A_BYTES + GTC_B_BYTES)));
+    CKC(cudaFuncSetAttribute(k_gala_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (GTC_A_BYTES + GTC_B_BYTES)));
+    CKC(cudaFuncSetAttribute(k_gala_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (GTC_A_BYTES + GTC_B_BYTES)));
     CKC(cudaFuncSetAttribute(k_kg_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              KG_TC_STAGES * KG_TC_KCS * (128 + KG_TC_N) * 16 + 2 * 512 * 32));
     {
@@ -958,8 +962,8 @@ int gala_encode_gala_weights(gala_ctx* c, const uint32_t* slots, int T, int baby
     return GALA_OK;
 }
 
-int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2, int T, int baby,
-                        const uint32_t* r, uint64_t* outs, uint64_t* masked)
+static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2, const uint8_t* wcan, int T, int baby,
+                   const uint32_t* r, uint64_t* outs, uint64_t* masked)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     if (T <= 0 || B <= 0) return set_err(GALA_ERR_DIM, "T and B must be positive");
@@ -1026,13 +1030,34 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
     // 2. stage A: E_jj = sum_i sigma_jj(D_i) ksk_jj[i] per input and baby rotation (shared by all groups);
     //    stage B: per (input, group) U = sum_jj w_t E_jj, C0 = sum_jj w_t sigma_jj(c0) (+ step-0 member)
     const int Z = B * G;
-    u64 *E, *R0, *U, *Cacc, *rr, *inner;
-    RET(scratch(c, &E, (size_t)B * (baby - 1) * 2 * MN));
-    RET(scratch(c, &R0, (size_t)B * (baby - 1) * L * N));
+    u64 *E = nullptr, *R0 = nullptr, *U, *Cacc, *rr, *inner;
     RET(scratch(c, &U, (size_t)Z * 2 * M * N));
     RET(scratch(c, &Cacc, (size_t)Z * 2 * L * N));
     RET(scratch(c, &rr, (size_t)Z * 2 * N));
     RET(scratch(c, &inner, (size_t)Z * W));
+    const bool tc = wcan != nullptr && B <= 32 && G <= 8 && baby <= 64 && (N % 32) == 0 && getenv("GALA_FC_NO_TC") == nullptr;
+    if (tc) {
+        // tensor-core baby-step sums: E packed as int8 MMA operands, weights as their byte-convolution
+        uint8_t* Ecan;
+        RET(scratch(c, &Ecan, (size_t)MN * GTC_A_BYTES));
+        const u64* const* dk = (const u64* const*)(d_blob + o_keys);
+        dim3 ge((unsigned)(N / 32), 32, (unsigned)M);
+#define GALA_ECAN(LL) KLAUNCH(c, "k_gala_e", (k_gala_e_can<LL><<<ge, 256, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, B, Ecan)))
+#define GALA_TC(LL)                                                                                        \
+    KLAUNCH(c, "k_gala_tc", (k_gala_tc<LL><<<c->num_sms, GTC_THREADS, 2 * (GTC_A_BYTES + GTC_B_BYTES), c->stream>>>( \
+                                c->dc, Ecan, wcan, cts, pts2, baby, G, B, U, Cacc)))
+        switch (L) {
+            case 1: GALA_ECAN(1); GALA_TC(1); break;
+            case 2: GALA_ECAN(2); GALA_TC(2); break;
+            case 3: GALA_ECAN(3); GALA_TC(3); break;
+            default: GALA_ECAN(4); GALA_TC(4); break;
+        }
+#undef GALA_ECAN
+#undef GALA_TC
+        release(c, Ecan);
+    } else {
+    RET(scratch(c, &E, (size_t)B * (baby - 1) * 2 * MN));
+    RET(scratch(c, &R0, (size_t)B * (baby - 1) * L * N));
     {
         const int th = N < 256 ? N : 256;
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
@@ -1061,6 +1086,7 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
     }
     release(c, E);
     release(c, R0);
+    }
     // 3. one ModDown per (input, group) -> inner[b][g]
     RET(launch_inv<false>(c, U + (long long)L * N, rr, Z * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
@@ -1091,8 +1117,32 @@ int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t*
     return GALA_OK;
 }
 
+int gala_mv_gala2_batch(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2, int T, int baby,
+                        const uint32_t* r, uint64_t* outs, uint64_t* masked)
+{
+    return mv2_run(c, cts, B, pts2, nullptr, T, baby, r, outs, masked);
+}
+
+int gala_mv_gala2_batch_tc(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2, const uint8_t* wcan, int T,
+                           int baby, const uint32_t* r, uint64_t* outs, uint64_t* masked)
+{
+    return mv2_run(c, cts, B, pts2, wcan, T, baby, r, outs, masked);
+}
+
+size_t gala_fc_tc_weight_bytes(gala_ctx* c) { return (size_t)c->dc.M * c->dc.N * GTC_B_BYTES; }
+
+int gala_fc_tc_weights(gala_ctx* c, const uint64_t* pts2, int T, int baby, uint8_t* wcan)
+{
+    if (baby <= 0 || T % baby) return set_err(GALA_ERR_PARAM, "baby %d must divide T=%d", baby, T);
+    const int G = T / baby;
+    if (G > 8 || baby > 64) return set_err(GALA_ERR_PARAM, "tensor-core FC path needs T/baby <= 8 and baby <= 64");
+    const long long total = (long long)c->dc.M * c->dc.N * 128 * 32;
+    KLAUNCH(c, "k_gala_wcan", k_gala_wcan<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, pts2, baby, G, wcan));
+    return GALA_OK;
+}
+
 static int mv_batch_host(gala_ctx* c, int schedule, const uint64_t* cts_host, int B, const uint64_t* pts, int T,
-                         int baby, const uint32_t* r_host, uint64_t* masked_host)
+                         int baby, const uint32_t* r_host, uint64_t* masked_host, const uint8_t* wcan = nullptr)
 {
     const int N = c->dc.N, L = c->dc.L;
     const long long W = 2LL * L * N;
@@ -1106,7 +1156,7 @@ static int mv_batch_host(gala_ctx* c, int schedule, const uint64_t* cts_host, in
     CK(cudaMemcpyAsync(coef, cts_host, sizeof(u64) * B * W, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(r, r_host, sizeof(uint32_t) * B * N, cudaMemcpyHostToDevice, c->stream));
     RET(gala_ct_import(c, coef, ct, B));
-    if (schedule == 2) RET(gala_mv_gala2_batch(c, ct, B, pts, T, baby, r, out, masked));
+    if (schedule == 2) RET(mv2_run(c, ct, B, pts, wcan, T, baby, r, out, masked));
     else RET(gala_mv_gala_batch(c, ct, B, pts, T, baby, r, out, masked));
     RET(gala_ct_export(c, masked, coef, B));
     CK(cudaMemcpyAsync(masked_host, coef, sizeof(u64) * B * W, cudaMemcpyDeviceToHost, c->stream));
@@ -1129,6 +1179,12 @@ int gala_mv_gala2_batch_host(gala_ctx* c, const uint64_t* cts_host, int B, const
                              const uint32_t* r_host, uint64_t* masked_host)
 {
     return mv_batch_host(c, 2, cts_host, B, pts2, T, baby, r_host, masked_host);
+}
+
+int gala_mv_gala2_batch_tc_host(gala_ctx* c, const uint64_t* cts_host, int B, const uint64_t* pts2, const uint8_t* wcan,
+                                int T, int baby, const uint32_t* r_host, uint64_t* masked_host)
+{
+    return mv_batch_host(c, 2, cts_host, B, pts2, T, baby, r_host, masked_host, wcan);
 }
 
 int gala_mv_gala_host(gala_ctx* c, const uint64_t* ct_host, const uint64_t* pts, int T, int baby,

@@ -300,7 +300,8 @@ class GalaFC:
     and returns the masked output ciphertexts plus the server's folded shares.
     """
 
-    def __init__(self, w, params: HEParams, pair_rows: bool = True, baby: int | None = None):
+    def __init__(self, w, params: HEParams, pair_rows: bool = True, baby: int | None = None,
+                 tensor_cores: bool = True):
         self.params = params
         self.ctx = context(params)
         w = np.asarray(w, dtype=np.int64) % params.p
@@ -333,6 +334,10 @@ class GalaFC:
         for blk in self.blocks:    # resident encoded weights, in the layout of the chosen schedule
             blk[1] = (self.ctx.encode_gala_weights(blk[1], self.baby) if self.schedule == 2
                       else self.ctx.encode_plain(blk[1]))
+        # tensor-core baby-step sums (schedule 2): the weights' byte-convolution expansion, per block
+        self.wcan = [None] * len(self.blocks)
+        if tensor_cores and self.schedule == 2 and self.ctx.fc_tc_supported(self.T, self.baby):
+            self.wcan = [self.ctx.fc_tc_weights(blk[1], self.T, self.baby) for blk in self.blocks]
         self.ctx.ensure_keys(self.steps)
 
     def encrypt_input(self, x) -> list:
@@ -355,16 +360,19 @@ class GalaFC:
     def forward_device(self, cts, masks) -> list:
         """Server side, device only: masked output ciphertexts (one per block)."""
         outs = []
-        for (tasks, pts, T), ct, rs in zip(self.blocks, cts, masks):
+        for bidx, ((tasks, pts, T), ct, rs) in enumerate(zip(self.blocks, cts, masks)):
             phys_r = self.ctx.physical(rs[0].slots, rs[1].slots if self.paired else None)
-            _, masked = self.run_batch(ct.unsqueeze(0), pts, self.ctx.to_device_u32(phys_r[None, :]))
+            _, masked = self.run_batch(ct.unsqueeze(0), pts, self.ctx.to_device_u32(phys_r[None, :]), block=bidx)
             outs.append(masked[0])
         return outs
 
-    def run_batch(self, cts, pts, d_r, outs=None, masked=None):
+    def run_batch(self, cts, pts, d_r, outs=None, masked=None, block: int | None = None):
         """Fused layer over a batch of inputs (cts [B][2][L][N], d_r [B][N]) for one column block."""
         if self.schedule == 2:
-            return self.ctx.mv_gala2_batch(cts, pts, self.T, d_r, self.baby, outs=outs, masked=masked)
+            if block is None:   # locate the block by its weights tensor
+                block = next((i for i, b in enumerate(self.blocks) if b[1] is pts), None)
+            wcan = self.wcan[block] if block is not None else None
+            return self.ctx.mv_gala2_batch(cts, pts, self.T, d_r, self.baby, outs=outs, masked=masked, wcan=wcan)
         return self.ctx.mv_gala_batch(cts, pts, self.T, d_r, self.baby, outs=outs, masked=masked)
 
     def server_shares(self, masks) -> np.ndarray:

@@ -242,3 +242,31 @@ def test_conv_kg2_kernel_sizes(tw, ksz, post):
                             torch.from_numpy(rowsum).to(dev), ksz * ksz, pair * c_n, taps, u_w * u_h, c_n, post=post)
     c_out = tw.cpu.conv_kg2(np.stack([c for _, c in xs]), kern, u_w, u_h, pair, band_only=post)
     assert np.array_equal(tw.gpu.export_words(g_out), c_out)
+
+
+@pytest.mark.parametrize("T", [2, 4, 8, 16])
+def test_mv_gala2_tensor_core_words(tw, T):
+    """Tensor-core baby-step sums (byte-convolution int8 MMA) == CUDA-core schedule 2 == oracle o_mv_gala2."""
+    import torch
+
+    n = tw.bfv.n
+    if T > n or tw.N % 32:
+        pytest.skip("shape")
+    b, steps = tw.gpu.bsgs_steps(T)
+    if not tw.gpu.fc_tc_supported(T, b):
+        pytest.skip("tensor-core path not applicable")
+    tw.keys_for(steps)
+    pts = tw.slots(T)
+    pts2 = tw.gpu.encode_gala_weights(pts, b)
+    wcan = tw.gpu.fc_tc_weights(pts2, T, b)
+    xs = [tw.encrypt(tw.slots()) for _ in range(3)]
+    rs = tw.slots(3)
+    cts = torch.stack([g for g, _ in xs])
+    d_r = tw.gpu.to_device_u32(rs)
+    outs, masked = tw.gpu.mv_gala2_batch(cts, pts2, T, d_r, b, wcan=wcan)
+    outs1, masked1 = tw.gpu.mv_gala2_batch(cts, pts2, T, d_r, b)
+    assert np.array_equal(tw.gpu.export_words(outs), tw.gpu.export_words(outs1))
+    for i, (g, c) in enumerate(xs):
+        c_out, c_masked = tw.cpu.mv_gala(c, pts, rs[i], baby=b, schedule=2)
+        assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
+        assert np.array_equal(tw.gpu.export_words(masked[i]), c_masked)
