@@ -118,10 +118,10 @@ int gala_mv_gala_host(gala_ctx *ctx, const uint64_t *ct_host, const uint64_t *pt
 int gala_mv_gala_batch_host(gala_ctx *ctx, const uint64_t *cts_host, int B, const uint64_t *pts_dev, int T,
                             int baby, const uint32_t *r_slots_host, uint64_t *masked_host);
 
-/* GALA schedule 2 with the baby-step sums on the int8 tensor cores (tcgen05): the weights' byte
- * convolution (Toeplitz) expansion, built once per layer by gala_fc_tc_weights into wcan_dev
- * (gala_fc_tc_weight_bytes bytes: 64 KB per QP position), is the MMA B operand; E_jj is packed
- * per position as the A operand.  Same words as gala_mv_gala2_batch (exact modular arithmetic).
+/* GALA schedule 2 with the baby-step sums on the int8 tensor cores (tcgen05): per QP position the
+ * weights' byte-convolution (Toeplitz) expansion is the MMA B operand (built in shared memory from
+ * the position-major weights gala_fc_tc_weights writes to wcan_dev, gala_fc_tc_weight_bytes bytes =
+ * 4 KB per position) and E_jj, packed per position, the A operand.  Same words as gala_mv_gala2_batch (exact modular arithmetic).
  * Needs B <= 32, T/baby <= 8 and baby <= 64; otherwise the CUDA-core path runs. */
 size_t gala_fc_tc_weight_bytes(gala_ctx *ctx);
 int gala_fc_tc_weights(gala_ctx *ctx, const uint64_t *pts2_dev, int T, int baby, uint8_t *wcan_dev);

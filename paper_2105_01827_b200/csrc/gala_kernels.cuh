@@ -1200,7 +1200,7 @@ __global__ void k_kg_tc_layout_a(const int8_t* __restrict__ A, int rows, int row
 // yields sum X w mod q).  Operands are stored in the tcgen05 SWIZZLE_NONE K-major core-matrix
 // order: 16-byte chunk (row r, chunk kc) at (r / 8) 4096 + kc 128 + (r % 8) 16.
 //   Ecan: per position 12 row groups (rows s 32 + bi, s < 3, bi < 32) = 48 KB
-//   Wcan: per position 16 row groups (rows g 16 + s', g < 8) = 64 KB (built once per layer)
+//   B tile: per position 16 row groups (rows g 16 + s', g < 8) = 64 KB, expanded in shared memory
 #define GTC_A_BYTES (12 * 4096)
 #define GTC_B_BYTES (16 * 4096)
 __device__ __forceinline__ u64 bswap64(u64 w)
@@ -1209,24 +1209,17 @@ __device__ __forceinline__ u64 bswap64(u64 w)
     return ((u64)__byte_perm(lo, 0, 0x0123) << 32) | (u64)__byte_perm(hi, 0, 0x0123);
 }
 
-// Wcan[p][(g, s')][(jj', a)] = byte (s' - a) of w[g b + jj' + 1][p]  (0 outside [0, 7] or jj' + 1 >= b)
-__global__ void k_gala_wcan(DevCtx c, const u64* __restrict__ pts2, int baby, int G, uint8_t* __restrict__ Wcan)
+// wT[p][g][jj] = w[g b + jj][p] (Montgomery words, 0 for g >= G or jj >= b): the 4 KB of weights one
+// position's byte-convolution tile is built from (in shared memory, by k_gala_tc's expander warps)
+#define GTC_W_BYTES (8 * 64 * 8)
+__global__ void k_gala_wt(DevCtx c, const u64* __restrict__ pts2, int baby, int G, u64* __restrict__ wT)
 {
     const long long MN = (long long)c.M * c.N;
-    const long long total = MN * 128 * 32;
+    const long long total = MN * 512;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-        const int kc = (int)(e & 31), n = (int)((e >> 5) & 127);
-        const long long p = e >> 12;
-        const int g = n >> 4, sp = n & 15;
-        u64 t[2];
-#pragma unroll
-        for (int jw = 0; jw < 2; jw++) {
-            const int jj = 2 * kc + jw + 1;
-            const u64 w = (g < G && jj < baby) ? __ldg(pts2 + (long long)(g * baby + jj) * MN + p) : 0;
-            const u64 rev = bswap64(w);
-            t[jw] = sp <= 7 ? rev >> (8 * (7 - sp)) : (sp == 15 ? 0 : rev << (8 * (sp - 7)));
-        }
-        *(ulonglong2*)(Wcan + p * GTC_B_BYTES + (n >> 3) * 4096 + kc * 128 + (n & 7) * 16) = make_ulonglong2(t[0], t[1]);
+        const int jj = (int)(e & 63), g = (int)((e >> 6) & 7);
+        const long long p = e >> 9;
+        wT[e] = (g < G && jj < baby) ? __ldg(pts2 + (long long)(g * baby + jj) * MN + p) : 0;
     }
 }
 
@@ -1291,28 +1284,36 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
 }
 
 // The baby-step sums of every (input, group) at every position on the tensor cores.  Warp-specialized
-// persistent kernel, one CTA per SM: warp 0 lane 0 bulk-copies each position's A (Ecan) and B (Wcan)
-// tiles into a 2-stage ring; warp 1 lane 0 issues 16 tcgen05.mma.kind::i8 (M 128, N 128, K 32,
-// unsigned bytes) into one of two TMEM accumulators; warps 2..5 (TMEM lane group s = warp % 4 ->
-// stream s, lane = input) rebuild each (input, stream, group) sum from its 15 byte-shifted columns,
-// reduce it mod q once and write U / Cacc (adding the step-0 member for stream 2).
-#define GTC_THREADS 192
+// persistent kernel, one CTA per SM:
+//   warp 0 lane 0  producer: per position one cp.async.bulk of the A tile (Ecan, 48 KB) and one of the
+//                  raw weights (wT, 4 KB) into a 2-stage ring (full / empty mbarriers);
+//   warps 6..9     expanders: build the position's byte-convolution B tile (64 KB, single buffer) from
+//                  the raw weights (byte reversal + funnel shift per 8-byte window), fence the generic
+//                  -> async proxy, arrive bfull;
+//   warp 1 lane 0  MMA: 16 tcgen05.mma.kind::i8 (M 128, N 128, K 32, unsigned bytes) into one of two
+//                  TMEM accumulators; commits empty[s], bempty and tfull[acc];
+//   warps 2..5     epilogue (TMEM lane group s = warp % 4 -> stream s, lane = input): rebuild each
+//                  (input, stream, group) sum from its 15 byte-shifted columns, reduce once mod q,
+//                  write U / Cacc (plus the step-0 member for stream 2).
+#define GTC_THREADS 320
+#define GTC_STAGE (GTC_A_BYTES + GTC_W_BYTES)
+#define GTC_SMEM (2 * GTC_STAGE + GTC_B_BYTES)
 template <int L>
 __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint8_t* __restrict__ Ecan,
-                                                          const uint8_t* __restrict__ Wcan, const u64* __restrict__ X,
+                                                          const u64* __restrict__ wT, const u64* __restrict__ X,
                                                           const u64* __restrict__ pts2, int baby, int G, int B,
                                                           u64* __restrict__ U, u64* __restrict__ Cacc)
 {
     extern __shared__ __align__(128) uint8_t gtc_sm[];
     constexpr int M = L + 1;
-    constexpr int STAGE = GTC_A_BYTES + GTC_B_BYTES;
-    __shared__ uint64_t full[2], empty[2], tfull[2], tempty[2];
+    __shared__ uint64_t full[2], empty[2], tfull[2], tempty[2], bfull, bempty;
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = c.N;
     const long long MN = (long long)M * N, npos = MN;
     const long long per = (npos + gridDim.x - 1) / gridDim.x;
     const long long p0 = blockIdx.x * per, p1 = p0 + per < npos ? p0 + per : npos;
+    uint8_t* sBt = gtc_sm + 2 * GTC_STAGE;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -1324,6 +1325,8 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
+        mbar_init(&bfull, 4);
+        mbar_init(&bempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1336,10 +1339,10 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             uint32_t ph = 0;
             for (long long p = p0; p < p1; p++) {
                 mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* st = gtc_sm + s * STAGE;
-                mbar_expect_tx(&full[s], (uint32_t)STAGE);
+                uint8_t* st = gtc_sm + s * GTC_STAGE;
+                mbar_expect_tx(&full[s], (uint32_t)GTC_STAGE);
                 bulk_g2s(st, Ecan + p * GTC_A_BYTES, GTC_A_BYTES, &full[s]);
-                bulk_g2s(st + GTC_A_BYTES, Wcan + p * GTC_B_BYTES, GTC_B_BYTES, &full[s]);
+                bulk_g2s(st + GTC_A_BYTES, wT + p * 512, GTC_W_BYTES, &full[s]);
                 if (++s == 2) {
                     s = 0;
                     ph ^= 1;
@@ -1348,7 +1351,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -1356,8 +1359,9 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 const int acc = it & 1;
                 mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
                 mbar_wait(&full[s], ph);
+                mbar_wait(&bfull, (uint32_t)(it & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t sa = smem_u32(gtc_sm + s * STAGE), sb = sa + GTC_A_BYTES;
+                const uint32_t sa = smem_u32(gtc_sm + s * GTC_STAGE), sb = smem_u32(sBt);
                 const uint32_t d = tmem + (uint32_t)(acc * 128);
 #pragma unroll 1
                 for (int ks = 0; ks < 16; ks++) {
@@ -1370,11 +1374,39 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                         ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
                 }
                 umma_commit(&empty[s]);
+                umma_commit(&bempty);
                 umma_commit(&tfull[acc]);
                 if (++s == 2) {
                     s = 0;
                     ph ^= 1;
                 }
+            }
+        }
+    } else if (warp >= 6) {   // expanders: B row n = (g, s') per thread, all 32 K chunks
+        const int n = tid - 6 * 32, g = n >> 4, sp = n & 15;
+        const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? 8 * (sp - 7) : 0;
+        uint8_t* rowbase = sBt + (n >> 3) * 4096 + (n & 7) * 16;
+        int s = 0;
+        uint32_t ph = 0;
+        int it = 0;
+        for (long long p = p0; p < p1; p++, it++) {
+            mbar_wait(&full[s], ph);
+            mbar_wait(&bempty, (uint32_t)((it & 1) ^ 1));
+            const u64* raw = (const u64*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES) + g * 64;
+#pragma unroll 4
+            for (int kc = 0; kc < 32; kc++) {
+                // chunk kc holds jj' = 2 kc, 2 kc + 1, i.e. baby rotations jj = 2 kc + 1, 2 kc + 2
+                const u64 r0 = bswap64(raw[2 * kc + 1]), r1 = kc < 31 ? bswap64(raw[2 * kc + 2]) : 0ull;
+                const u64 t0 = sp == 15 ? 0ull : (sp <= 7 ? r0 >> sh_r : r0 << sh_l);
+                const u64 t1 = sp == 15 ? 0ull : (sp <= 7 ? r1 >> sh_r : r1 << sh_l);
+                *(ulonglong2*)(rowbase + kc * 128) = make_ulonglong2(t0, t1);
+            }
+            asm volatile("fence.proxy.async.shared::cta;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bfull);
+            if (++s == 2) {
+                s = 0;
+                ph ^= 1;
             }
         }
     } else {   // epilogue: TMEM lane group lg = warp % 4 holds rows 32 lg .. (stream s = lg, input = lane)
@@ -1423,7 +1455,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 if (sidx < 2) {
                     U[((z * 2 + sidx) * M + j) * (long long)N + k] = v;
                 } else {
-                    const u64 w0 = __ldg(pts2 + (long long)(g * baby) * MN + p);   // step-0 member
+                    const u64 w0 = __ldg(wT + p * 512 + g * 64);   // step-0 member weight
                     Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = add_mod(v, mont_mul(xc0, w0, md), q);
                     Cacc[((z * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, w0, md);
                 }

@@ -662,10 +662,10 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_ntt_inv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_ntt_inv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_moddown, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CKC(cudaFuncSetAttribute(k_gala_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (GTC_A_BYTES + GTC_B_BYTES)));
-    CKC(cudaFuncSetAttribute(k_gala_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (GTC_A_BYTES + GTC_B_BYTES)));
-    CKC(cudaFuncSetAttribute(k_gala_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (GTC_A_BYTES + GTC_B_BYTES)));
-    CKC(cudaFuncSetAttribute(k_gala_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (GTC_A_BYTES + GTC_B_BYTES)));
+    CKC(cudaFuncSetAttribute(k_gala_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_kg_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              KG_TC_STAGES * KG_TC_KCS * (128 + KG_TC_N) * 16 + 2 * 512 * 32));
     {
@@ -1044,8 +1044,8 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
         dim3 ge((unsigned)(N / 32), 32, (unsigned)M);
 #define GALA_ECAN(LL) KLAUNCH(c, "k_gala_e", (k_gala_e_can<LL><<<ge, 256, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, B, Ecan)))
 #define GALA_TC(LL)                                                                                        \
-    KLAUNCH(c, "k_gala_tc", (k_gala_tc<LL><<<c->num_sms, GTC_THREADS, 2 * (GTC_A_BYTES + GTC_B_BYTES), c->stream>>>( \
-                                c->dc, Ecan, wcan, cts, pts2, baby, G, B, U, Cacc)))
+    KLAUNCH(c, "k_gala_tc", (k_gala_tc<LL><<<c->num_sms, GTC_THREADS, GTC_SMEM, c->stream>>>(                   \
+                                c->dc, Ecan, (const u64*)wcan, cts, pts2, baby, G, B, U, Cacc)))
         switch (L) {
             case 1: GALA_ECAN(1); GALA_TC(1); break;
             case 2: GALA_ECAN(2); GALA_TC(2); break;
@@ -1129,15 +1129,15 @@ int gala_mv_gala2_batch_tc(gala_ctx* c, const uint64_t* cts, int B, const uint64
     return mv2_run(c, cts, B, pts2, wcan, T, baby, r, outs, masked);
 }
 
-size_t gala_fc_tc_weight_bytes(gala_ctx* c) { return (size_t)c->dc.M * c->dc.N * GTC_B_BYTES; }
+size_t gala_fc_tc_weight_bytes(gala_ctx* c) { return (size_t)c->dc.M * c->dc.N * GTC_W_BYTES; }
 
 int gala_fc_tc_weights(gala_ctx* c, const uint64_t* pts2, int T, int baby, uint8_t* wcan)
 {
     if (baby <= 0 || T % baby) return set_err(GALA_ERR_PARAM, "baby %d must divide T=%d", baby, T);
     const int G = T / baby;
     if (G > 8 || baby > 64) return set_err(GALA_ERR_PARAM, "tensor-core FC path needs T/baby <= 8 and baby <= 64");
-    const long long total = (long long)c->dc.M * c->dc.N * 128 * 32;
-    KLAUNCH(c, "k_gala_wcan", k_gala_wcan<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, pts2, baby, G, wcan));
+    const long long total = (long long)c->dc.M * c->dc.N * 512;
+    KLAUNCH(c, "k_gala_wt", k_gala_wt<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, pts2, baby, G, (u64*)wcan));
     return GALA_OK;
 }
 
