@@ -1286,7 +1286,7 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
 // The baby-step sums of every (input, group) at every position on the tensor cores.  Warp-specialized
 // persistent kernel, one CTA per SM:
 //   warp 0 lane 0  producer: per position one cp.async.bulk of the A tile (Ecan, 48 KB) and one of the
-//                  raw weights (wT, 4 KB) into a 2-stage ring (full / empty mbarriers);
+//                  raw weights (wT, 4 KB) into a 3-stage ring (full / empty mbarriers);
 //   warps 6..9     expanders: build the position's byte-convolution B tile (64 KB, single buffer) from
 //                  the raw weights (byte reversal + funnel shift per 8-byte window), fence the generic
 //                  -> async proxy, arrive bfull;
@@ -1296,8 +1296,9 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
 //                  (input, stream, group) sum from its 15 byte-shifted columns, reduce once mod q,
 //                  write U / Cacc (plus the step-0 member for stream 2).
 #define GTC_THREADS 320
+#define GTC_NST 3
 #define GTC_STAGE (GTC_A_BYTES + GTC_W_BYTES)
-#define GTC_SMEM (2 * GTC_STAGE + GTC_B_BYTES)
+#define GTC_SMEM (GTC_NST * GTC_STAGE + GTC_B_BYTES)
 template <int L>
 __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint8_t* __restrict__ Ecan,
                                                           const u64* __restrict__ wT, const u64* __restrict__ X,
@@ -1306,22 +1307,24 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
 {
     extern __shared__ __align__(128) uint8_t gtc_sm[];
     constexpr int M = L + 1;
-    __shared__ uint64_t full[2], empty[2], tfull[2], tempty[2], bfull, bempty;
+    __shared__ uint64_t full[GTC_NST], empty[GTC_NST], tfull[2], tempty[2], bfull, bempty;
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = c.N;
     const long long MN = (long long)M * N, npos = MN;
     const long long per = (npos + gridDim.x - 1) / gridDim.x;
     const long long p0 = blockIdx.x * per, p1 = p0 + per < npos ? p0 + per : npos;
-    uint8_t* sBt = gtc_sm + 2 * GTC_STAGE;
+    uint8_t* sBt = gtc_sm + GTC_NST * GTC_STAGE;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        for (int i = 0; i < 2; i++) {
+        for (int i = 0; i < GTC_NST; i++) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
@@ -1343,7 +1346,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 mbar_expect_tx(&full[s], (uint32_t)GTC_STAGE);
                 bulk_g2s(st, Ecan + p * GTC_A_BYTES, GTC_A_BYTES, &full[s]);
                 bulk_g2s(st + GTC_A_BYTES, wT + p * 512, GTC_W_BYTES, &full[s]);
-                if (++s == 2) {
+                if (++s == GTC_NST) {
                     s = 0;
                     ph ^= 1;
                 }
@@ -1376,7 +1379,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 umma_commit(&empty[s]);
                 umma_commit(&bempty);
                 umma_commit(&tfull[acc]);
-                if (++s == 2) {
+                if (++s == GTC_NST) {
                     s = 0;
                     ph ^= 1;
                 }
@@ -1404,7 +1407,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             asm volatile("fence.proxy.async.shared::cta;");
             __syncwarp();
             if (lane == 0) mbar_arrive(&bfull);
-            if (++s == 2) {
+            if (++s == GTC_NST) {
                 s = 0;
                 ph ^= 1;
             }
@@ -1418,14 +1421,18 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             const int j = (int)(p / N), k = (int)(p - (long long)j * N);
             const ModC md = c.mod[j];
             const u64 q = md.q;
-            mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;");
             const bool active = sidx < 2 || (sidx == 2 && j < L);
-            u64 xc0 = 0, xc1 = 0;
+            // step-0 operands issued before the accumulator wait, so their latency hides behind the MMA
+            u64 xc0 = 0, xc1 = 0, w0[8];
             if (sidx == 2 && active && bi < B) {
                 xc0 = __ldg(X + (long long)bi * W + (long long)j * N + k);
                 xc1 = __ldg(X + (long long)bi * W + (long long)(L + j) * N + k);
+#pragma unroll
+                for (int g = 0; g < 8; g++) w0[g] = g < G ? __ldg(wT + p * 512 + g * 64) : 0;
             }
+            mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
             for (int g = 0; g < G; g++) {
                 uint32_t x[16];
                 const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + g * 16);
@@ -1454,10 +1461,12 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 const long long z = (long long)bi * G + g;
                 if (sidx < 2) {
                     U[((z * 2 + sidx) * M + j) * (long long)N + k] = v;
-                } else {
-                    const u64 w0 = __ldg(wT + p * 512 + g * 64);   // step-0 member weight
-                    Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = add_mod(v, mont_mul(xc0, w0, md), q);
-                    Cacc[((z * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, w0, md);
+                } else {   // step-0 member weight w0[g]
+                    u64 wg = w0[0];
+#pragma unroll
+                    for (int t = 1; t < 8; t++) wg = g == t ? w0[t] : wg;
+                    Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = add_mod(v, mont_mul(xc0, wg, md), q);
+                    Cacc[((z * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, wg, md);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
