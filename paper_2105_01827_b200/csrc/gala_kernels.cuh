@@ -1287,18 +1287,20 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
 // persistent kernel, one CTA per SM:
 //   warp 0 lane 0  producer: per position one cp.async.bulk of the A tile (Ecan, 48 KB) and one of the
 //                  raw weights (wT, 4 KB) into a 3-stage ring (full / empty mbarriers);
-//   warps 6..9     expanders: build the position's byte-convolution B tile (64 KB, single buffer) from
-//                  the raw weights (byte reversal + funnel shift per 8-byte window), fence the generic
-//                  -> async proxy, arrive bfull;
-//   warp 1 lane 0  MMA: 16 tcgen05.mma.kind::i8 (M 128, N 128, K 32, unsigned bytes) into one of two
-//                  TMEM accumulators; commits empty[s], bempty and tfull[acc];
+//   warps 6..13    expanders: build the position's byte-convolution B tile in two halves (groups
+//                  0-3, 4-7; 32 KB each, double-buffered) from the raw weights (byte reversal +
+//                  shift per 8-byte window), fence the generic -> async proxy, arrive bfull[h];
+//   warp 1 lane 0  MMA: per half 16 tcgen05.mma.kind::i8 (M 128, N 64, K 32, unsigned bytes) into
+//                  columns 64 h of one of two TMEM accumulators (the next half's expansion overlaps);
+//                  commits bempty[h], then empty[s] and tfull[acc];
 //   warps 2..5     epilogue (TMEM lane group s = warp % 4 -> stream s, lane = input): rebuild each
 //                  (input, stream, group) sum from its 15 byte-shifted columns, reduce once mod q,
 //                  write U / Cacc (plus the step-0 member for stream 2).
-#define GTC_THREADS 320
+#define GTC_THREADS 448
 #define GTC_NST 3
 #define GTC_STAGE (GTC_A_BYTES + GTC_W_BYTES)
-#define GTC_SMEM (GTC_NST * GTC_STAGE + GTC_B_BYTES)
+#define GTC_BH_BYTES (8 * 4096)
+#define GTC_SMEM (GTC_NST * GTC_STAGE + 2 * GTC_BH_BYTES)
 template <int L>
 __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint8_t* __restrict__ Ecan,
                                                           const u64* __restrict__ wT, const u64* __restrict__ X,
@@ -1307,14 +1309,14 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
 {
     extern __shared__ __align__(128) uint8_t gtc_sm[];
     constexpr int M = L + 1;
-    __shared__ uint64_t full[GTC_NST], empty[GTC_NST], tfull[2], tempty[2], bfull, bempty;
+    __shared__ uint64_t full[GTC_NST], empty[GTC_NST], tfull[2], tempty[2], bfull[2], bempty[2];
     __shared__ uint32_t tmem_base_sh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = c.N;
     const long long MN = (long long)M * N, npos = MN;
     const long long per = (npos + gridDim.x - 1) / gridDim.x;
     const long long p0 = blockIdx.x * per, p1 = p0 + per < npos ? p0 + per : npos;
-    uint8_t* sBt = gtc_sm + GTC_NST * GTC_STAGE;
+    uint8_t* sBh = gtc_sm + GTC_NST * GTC_STAGE;   // [2][32 KB]
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -1327,9 +1329,9 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
         for (int i = 0; i < 2; i++) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
+            mbar_init(&bfull[i], 8);
+            mbar_init(&bempty[i], 1);
         }
-        mbar_init(&bfull, 4);
-        mbar_init(&bempty, 1);
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1354,7 +1356,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -1362,22 +1364,25 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 const int acc = it & 1;
                 mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
                 mbar_wait(&full[s], ph);
-                mbar_wait(&bfull, (uint32_t)(it & 1));
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t sa = smem_u32(gtc_sm + s * GTC_STAGE), sb = smem_u32(sBt);
-                const uint32_t d = tmem + (uint32_t)(acc * 128);
+                const uint32_t sa = smem_u32(gtc_sm + s * GTC_STAGE);
+                for (int h = 0; h < 2; h++) {
+                    mbar_wait(&bfull[h], (uint32_t)(it & 1));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sb = smem_u32(sBh + h * GTC_BH_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(acc * 128 + h * 64);
 #pragma unroll 1
-                for (int ks = 0; ks < 16; ks++) {
-                    const uint64_t ad = umma_desc_kmajor(sa + ks * 256, 128, 4096);
-                    const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\t"
-                        "setp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                        ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
+                    for (int ks = 0; ks < 16; ks++) {
+                        const uint64_t ad = umma_desc_kmajor(sa + ks * 256, 128, 4096);
+                        const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\t"
+                            "setp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                            ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
+                    }
+                    umma_commit(&bempty[h]);
                 }
                 umma_commit(&empty[s]);
-                umma_commit(&bempty);
                 umma_commit(&tfull[acc]);
                 if (++s == GTC_NST) {
                     s = 0;
@@ -1385,28 +1390,33 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 }
             }
         }
-    } else if (warp >= 6) {   // expanders: B row n = (g, s') per thread, all 32 K chunks
-        const int n = tid - 6 * 32, g = n >> 4, sp = n & 15;
+    } else if (warp >= 6) {   // 8 expander warps: thread -> B row n (of 64 in the half) x 8 K chunks
+        const int et = tid - 6 * 32;
+        const int n = et & 63, kq = et >> 6;
+        const int gl = n >> 4, sp = n & 15;
         const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? 8 * (sp - 7) : 0;
-        uint8_t* rowbase = sBt + (n >> 3) * 4096 + (n & 7) * 16;
         int s = 0;
         uint32_t ph = 0;
         int it = 0;
         for (long long p = p0; p < p1; p++, it++) {
             mbar_wait(&full[s], ph);
-            mbar_wait(&bempty, (uint32_t)((it & 1) ^ 1));
-            const u64* raw = (const u64*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES) + g * 64;
-#pragma unroll 4
-            for (int kc = 0; kc < 32; kc++) {
-                // chunk kc holds jj' = 2 kc, 2 kc + 1, i.e. baby rotations jj = 2 kc + 1, 2 kc + 2
-                const u64 r0 = bswap64(raw[2 * kc + 1]), r1 = kc < 31 ? bswap64(raw[2 * kc + 2]) : 0ull;
-                const u64 t0 = sp == 15 ? 0ull : (sp <= 7 ? r0 >> sh_r : r0 << sh_l);
-                const u64 t1 = sp == 15 ? 0ull : (sp <= 7 ? r1 >> sh_r : r1 << sh_l);
-                *(ulonglong2*)(rowbase + kc * 128) = make_ulonglong2(t0, t1);
+            for (int h = 0; h < 2; h++) {
+                mbar_wait(&bempty[h], (uint32_t)((it & 1) ^ 1));
+                const u64* raw = (const u64*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES) + (4 * h + gl) * 64;
+                uint8_t* rowbase = sBh + h * GTC_BH_BYTES + (n >> 3) * 4096 + (n & 7) * 16;
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int kc = kq * 8 + i;
+                    // chunk kc holds jj' = 2 kc, 2 kc + 1, i.e. baby rotations jj = 2 kc + 1, 2 kc + 2
+                    const u64 r0 = bswap64(raw[2 * kc + 1]), r1 = kc < 31 ? bswap64(raw[2 * kc + 2]) : 0ull;
+                    const u64 t0 = sp == 15 ? 0ull : (sp <= 7 ? r0 >> sh_r : r0 << sh_l);
+                    const u64 t1 = sp == 15 ? 0ull : (sp <= 7 ? r1 >> sh_r : r1 << sh_l);
+                    *(ulonglong2*)(rowbase + kc * 128) = make_ulonglong2(t0, t1);
+                }
+                asm volatile("fence.proxy.async.shared::cta;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bfull[h]);
             }
-            asm volatile("fence.proxy.async.shared::cta;");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bfull);
             if (++s == GTC_NST) {
                 s = 0;
                 ph ^= 1;
