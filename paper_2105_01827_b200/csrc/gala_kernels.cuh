@@ -1287,15 +1287,16 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
 // persistent kernel, one CTA per SM:
 //   warp 0 lane 0  producer: per position one cp.async.bulk of the A tile (Ecan, 48 KB) and one of the
 //                  raw weights (wT, 4 KB) into a 3-stage ring (full / empty mbarriers);
-//   warps 6..13    expanders: build the position's byte-convolution B tile in two halves (groups
+//   warps 10..13   expanders: build the position's byte-convolution B tile in two halves (groups
 //                  0-3, 4-7; 32 KB each, double-buffered) from the raw weights (byte reversal +
 //                  shift per 8-byte window), fence the generic -> async proxy, arrive bfull[h];
 //   warp 1 lane 0  MMA: per half 16 tcgen05.mma.kind::i8 (M 128, N 64, K 32, unsigned bytes) into
 //                  columns 64 h of one of two TMEM accumulators (the next half's expansion overlaps);
 //                  commits bempty[h], then empty[s] and tfull[acc];
-//   warps 2..5     epilogue (TMEM lane group s = warp % 4 -> stream s, lane = input): rebuild each
-//                  (input, stream, group) sum from its 15 byte-shifted columns, reduce once mod q,
-//                  write U / Cacc (plus the step-0 member for stream 2).
+//   warps 2..9     epilogue (TMEM lane group s = warp % 4 -> stream s, lane = input; groups 4 gh ..
+//                  4 gh + 3 with gh = (warp - 2) / 4, one 64-column TMEM load per position): rebuild
+//                  each (input, stream, group) sum from its 15 byte-shifted columns, reduce once mod
+//                  q, write U / Cacc (plus the step-0 member for stream 2).
 #define GTC_THREADS 448
 #define GTC_NST 3
 #define GTC_STAGE (GTC_A_BYTES + GTC_W_BYTES)
@@ -1328,8 +1329,8 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
         }
         for (int i = 0; i < 2; i++) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4);
-            mbar_init(&bfull[i], 8);
+            mbar_init(&tempty[i], 8);
+            mbar_init(&bfull[i], 4);
             mbar_init(&bempty[i], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
@@ -1390,8 +1391,8 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 }
             }
         }
-    } else if (warp >= 6) {   // 8 expander warps: thread -> B row n (of 64 in the half) x 8 K chunks
-        const int et = tid - 6 * 32;
+    } else if (warp >= 10) {   // 4 expander warps: thread -> B row n (of 64 in the half) x 16 K chunks
+        const int et = tid - 10 * 32;
         const int n = et & 63, kq = et >> 6;
         const int gl = n >> 4, sp = n & 15;
         const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? 8 * (sp - 7) : 0;
@@ -1404,9 +1405,9 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 mbar_wait(&bempty[h], (uint32_t)((it & 1) ^ 1));
                 const u64* raw = (const u64*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES) + (4 * h + gl) * 64;
                 uint8_t* rowbase = sBh + h * GTC_BH_BYTES + (n >> 3) * 4096 + (n & 7) * 16;
-#pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    const int kc = kq * 8 + i;
+#pragma unroll 4
+                for (int i = 0; i < 16; i++) {
+                    const int kc = kq * 16 + i;
                     // chunk kc holds jj' = 2 kc, 2 kc + 1, i.e. baby rotations jj = 2 kc + 1, 2 kc + 2
                     const u64 r0 = bswap64(raw[2 * kc + 1]), r1 = kc < 31 ? bswap64(raw[2 * kc + 2]) : 0ull;
                     const u64 t0 = sp == 15 ? 0ull : (sp <= 7 ? r0 >> sh_r : r0 << sh_l);
@@ -1423,7 +1424,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             }
         }
     } else {   // epilogue: TMEM lane group lg = warp % 4 holds rows 32 lg .. (stream s = lg, input = lane)
-        const int lg = warp & 3, sidx = lg, bi = lane;
+        const int lg = warp & 3, sidx = lg, bi = lane, gh = (warp - 2) >> 2;
         const long long W = 2LL * L * N;
         int it = 0;
         for (long long p = p0; p < p1; p++, it++) {
@@ -1431,57 +1432,66 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             const int j = (int)(p / N), k = (int)(p - (long long)j * N);
             const ModC md = c.mod[j];
             const u64 q = md.q;
-            const bool active = sidx < 2 || (sidx == 2 && j < L);
+            const bool active = (sidx < 2 || (sidx == 2 && j < L)) && bi < B;
             // step-0 operands issued before the accumulator wait, so their latency hides behind the MMA
-            u64 xc0 = 0, xc1 = 0, w0[8];
-            if (sidx == 2 && active && bi < B) {
+            u64 xc0 = 0, xc1 = 0, w0[4];
+            if (sidx == 2 && active) {
                 xc0 = __ldg(X + (long long)bi * W + (long long)j * N + k);
                 xc1 = __ldg(X + (long long)bi * W + (long long)(L + j) * N + k);
 #pragma unroll
-                for (int g = 0; g < 8; g++) w0[g] = g < G ? __ldg(wT + p * 512 + g * 64) : 0;
+                for (int t = 0; t < 4; t++) w0[t] = 4 * gh + t < G ? __ldg(wT + p * 512 + (4 * gh + t) * 64) : 0;
             }
             mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll 1
-            for (int g = 0; g < G; g++) {
-                uint32_t x[16];
-                const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + g * 16);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-                    "%14, %15}, [%16];"
-                    : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
-                      "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (!active || bi >= B) continue;
-                // sum_s' 256^s' D_s' (exact, < 2^126): three 40-bit-spaced partial sums below 2^58
-                u64 lo5 = 0, mi5 = 0, hi5 = 0;
-#pragma unroll
-                for (int t = 0; t < 5; t++) {
-                    lo5 += (u64)x[t] << (8 * t);
-                    mi5 += (u64)x[5 + t] << (8 * t);
-                    hi5 += (u64)x[10 + t] << (8 * t);
-                }
-                u64 lo = lo5 + (mi5 << 40);
-                u64 hi = (mi5 >> 24) + (hi5 << 16) + (lo < lo5 ? 1ull : 0ull);
-                if (hi >= 2 * q) hi -= 2 * q;
-                if (hi >= 2 * q) hi -= 2 * q;
-                if (hi >= q) hi -= q;
-                const u64 v = csub(redc_lazy(hi, lo, md), q);   // sum_jj X w   (w Montgomery)
-                const long long z = (long long)bi * G + g;
-                if (sidx < 2) {
-                    U[((z * 2 + sidx) * M + j) * (long long)N + k] = v;
-                } else {   // step-0 member weight w0[g]
-                    u64 wg = w0[0];
-#pragma unroll
-                    for (int t = 1; t < 8; t++) wg = g == t ? w0[t] : wg;
-                    Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = add_mod(v, mont_mul(xc0, wg, md), q);
-                    Cacc[((z * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, wg, md);
-                }
-            }
+            uint32_t x[64];
+            const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + gh * 64);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+                "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, "
+                "%37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, "
+                "%59, %60, %61, %62, %63}, [%64];"
+                : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
+                  "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15]),
+                  "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]), "=r"(x[21]), "=r"(x[22]), "=r"(x[23]),
+                  "=r"(x[24]), "=r"(x[25]), "=r"(x[26]), "=r"(x[27]), "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31]),
+                  "=r"(x[32]), "=r"(x[33]), "=r"(x[34]), "=r"(x[35]), "=r"(x[36]), "=r"(x[37]), "=r"(x[38]), "=r"(x[39]),
+                  "=r"(x[40]), "=r"(x[41]), "=r"(x[42]), "=r"(x[43]), "=r"(x[44]), "=r"(x[45]), "=r"(x[46]), "=r"(x[47]),
+                  "=r"(x[48]), "=r"(x[49]), "=r"(x[50]), "=r"(x[51]), "=r"(x[52]), "=r"(x[53]), "=r"(x[54]), "=r"(x[55]),
+                  "=r"(x[56]), "=r"(x[57]), "=r"(x[58]), "=r"(x[59]), "=r"(x[60]), "=r"(x[61]), "=r"(x[62]), "=r"(x[63])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) mbar_arrive(&tempty[acc]);   // this warp's accumulator columns are in registers
+            if (active) {
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    const int g = 4 * gh + t;
+                    if (g >= G) break;
+                    const uint32_t* xg = x + 16 * t;
+                    // sum_s' 256^s' D_s' (exact, < 2^126): three 40-bit-spaced partial sums below 2^58
+                    u64 lo5 = 0, mi5 = 0, hi5 = 0;
+#pragma unroll
+                    for (int u = 0; u < 5; u++) {
+                        lo5 += (u64)xg[u] << (8 * u);
+                        mi5 += (u64)xg[5 + u] << (8 * u);
+                        hi5 += (u64)xg[10 + u] << (8 * u);
+                    }
+                    u64 lo = lo5 + (mi5 << 40);
+                    u64 hi = (mi5 >> 24) + (hi5 << 16) + (lo < lo5 ? 1ull : 0ull);
+                    if (hi >= 2 * q) hi -= 2 * q;
+                    if (hi >= 2 * q) hi -= 2 * q;
+                    if (hi >= q) hi -= q;
+                    const u64 v = csub(redc_lazy(hi, lo, md), q);   // sum_jj X w   (w Montgomery)
+                    const long long z = (long long)bi * G + g;
+                    if (sidx < 2) {
+                        U[((z * 2 + sidx) * M + j) * (long long)N + k] = v;
+                    } else {
+                        Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = add_mod(v, mont_mul(xc0, w0[t], md), q);
+                        Cacc[((z * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, w0[t], md);
+                    }
+                }
+            }
         }
     }
     __syncthreads();
