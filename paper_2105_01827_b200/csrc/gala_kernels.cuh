@@ -1199,7 +1199,8 @@ __global__ void k_kg_tc_layout_a(const int8_t* __restrict__ A, int rows, int row
 // the exact integer sum_jj X w < 2^126, reduced once mod q (w is in Montgomery form, so the REDC
 // yields sum X w mod q).  Operands are stored in the tcgen05 SWIZZLE_NONE K-major core-matrix
 // order: 16-byte chunk (row r, chunk kc) at (r / 8) 4096 + kc 128 + (r % 8) 16.
-//   Ecan: per position 12 row groups (rows s 32 + bi, s < 3, bi < 32) = 48 KB
+//   Ecan: chunk-major [kc][p][96 rows (s 32 + bi)][16 B] (48 KB per position); in shared memory the A
+//         tile is [kc][row group][8][16 B] (LBO 1536, SBO 128), one 1.5 KB bulk copy per chunk
 //   B tile: per position 16 row groups (rows g 16 + s', g < 8) = 64 KB, expanded in shared memory
 #define GTC_A_BYTES (12 * 4096)
 #define GTC_B_BYTES (16 * 4096)
@@ -1275,12 +1276,10 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
         }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < 32 * 96; idx += 256) {
-        const int kk2 = idx / 96, r = idx - kk2 * 96;
-        const long long p = (long long)j * N + k0 + kk2;
-        *(ulonglong2*)(Ecan + p * GTC_A_BYTES + (r >> 3) * 4096 + kc * 128 + (r & 7) * 16) =
-            make_ulonglong2(sm[kk2][r][0], sm[kk2][r][1]);
-    }
+    // chunk-major layout Ecan[kc][p][row 0..95][16 B]: the block's 32 positions are one contiguous 48 KB run
+    uint8_t* dst = Ecan + ((long long)kc * MN + (long long)j * N + k0) * (96 * 16);
+    for (int idx = threadIdx.x; idx < 32 * 96; idx += 256)
+        *(ulonglong2*)(dst + (long long)idx * 16) = *(const ulonglong2*)&sm[idx / 96][idx % 96][0];
 }
 
 // The baby-step sums of every (input, group) at every position on the tensor cores.  Warp-specialized
@@ -1347,7 +1346,8 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* st = gtc_sm + s * GTC_STAGE;
                 mbar_expect_tx(&full[s], (uint32_t)GTC_STAGE);
-                bulk_g2s(st, Ecan + p * GTC_A_BYTES, GTC_A_BYTES, &full[s]);
+                for (int kc = 0; kc < 32; kc++)
+                    bulk_g2s(st + kc * 1536, Ecan + ((long long)kc * npos + p) * 1536, 1536, &full[s]);
                 bulk_g2s(st + GTC_A_BYTES, wT + p * 512, GTC_W_BYTES, &full[s]);
                 if (++s == GTC_NST) {
                     s = 0;
@@ -1373,7 +1373,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                     const uint32_t d = tmem + (uint32_t)(acc * 128 + h * 64);
 #pragma unroll 1
                     for (int ks = 0; ks < 16; ks++) {
-                        const uint64_t ad = umma_desc_kmajor(sa + ks * 256, 128, 4096);
+                        const uint64_t ad = umma_desc_kmajor(sa + ks * 2 * 1536, 1536, 128);
                         const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
                         asm volatile(
                             "{\n\t.reg .pred p;\n\t"
