@@ -396,7 +396,9 @@ def run_ours(args):
         "kernel_breakdown_ms_per_step": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
         "e2e": {"value": round(e2e_value, 3), "unit": "layers/s",
                 "h2d_bytes_per_step": B * (ct_bytes + N * 4), "d2h_bytes_per_step": B * ct_bytes,
-                "path": f"gala_mv_gala{layer.schedule if layer.schedule == 2 else ''}_batch_host (C-ABI, pinned host buffers, canonical words, one call per step)"},
+                "path": ("gala_mv_gala2_batch_tc_host" if tc_on else
+                         f"gala_mv_gala{layer.schedule if layer.schedule == 2 else ''}_batch_host")
+                        + " (C-ABI, pinned host buffers, canonical words, one call per step)"},
         "gpu_launches": int(launches),
         "setup_s": round(setup_s, 2),
         "clocks": clk.summary(),

@@ -1270,16 +1270,19 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
                 e1 = s1.reduce(md);
                 if (j < L) r0 = __ldg(D + ((long long)L * M + j) * NN + src);
             }
-            sm[kk][bi][jw] = e0;
-            sm[kk][32 + bi][jw] = e1;
-            sm[kk][64 + bi][jw] = r0;
+            // row r of position kk lives at (r + kk) % 96: the 32 positions of a warp hit distinct banks
+            sm[kk][(bi + kk) % 96][jw] = e0;
+            sm[kk][(32 + bi + kk) % 96][jw] = e1;
+            sm[kk][(64 + bi + kk) % 96][jw] = r0;
         }
     }
     __syncthreads();
     // chunk-major layout Ecan[kc][p][row 0..95][16 B]: the block's 32 positions are one contiguous 48 KB run
     uint8_t* dst = Ecan + ((long long)kc * MN + (long long)j * N + k0) * (96 * 16);
-    for (int idx = threadIdx.x; idx < 32 * 96; idx += 256)
-        *(ulonglong2*)(dst + (long long)idx * 16) = *(const ulonglong2*)&sm[idx / 96][idx % 96][0];
+    for (int idx = threadIdx.x; idx < 32 * 96; idx += 256) {
+        const int kk2 = idx / 96, r = idx - kk2 * 96;
+        *(ulonglong2*)(dst + (long long)idx * 16) = *(const ulonglong2*)&sm[kk2][(r + kk2) % 96][0];
+    }
 }
 
 // The baby-step sums of every (input, group) at every position on the tensor cores.  Warp-specialized
