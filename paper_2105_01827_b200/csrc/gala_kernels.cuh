@@ -1210,17 +1210,29 @@ __device__ __forceinline__ u64 bswap64(u64 w)
     return ((u64)__byte_perm(lo, 0, 0x0123) << 32) | (u64)__byte_perm(hi, 0, 0x0123);
 }
 
-// wT[p][g][jj] = w[g b + jj][p] (Montgomery words, 0 for g >= G or jj >= b): the 4 KB of weights one
-// position's byte-convolution tile is built from (in shared memory, by k_gala_tc's expander warps)
-#define GTC_W_BYTES (8 * 64 * 8)
+// Per position p, the weights one byte-convolution tile is built from (in shared memory, by k_gala_tc's
+// expander warps): wT[p] = { bswap64(w[g b + jj' + 1][p]) for g < 8, jj' < 64 ;  w[g b][p] for g < 8 }
+// (Montgomery words, 0 outside g < G, jj' + 1 < b): byte-reversed so an 8-byte window of the
+// convolution is one shift, shifted by one rotation so chunk kc's two words are 16-byte aligned,
+// followed by the step-0 weights.  4160 bytes per position.
+#define GTC_W_WORDS (8 * 64 + 8)
+#define GTC_W_BYTES (GTC_W_WORDS * 8)
 __global__ void k_gala_wt(DevCtx c, const u64* __restrict__ pts2, int baby, int G, u64* __restrict__ wT)
 {
     const long long MN = (long long)c.M * c.N;
-    const long long total = MN * 512;
+    const long long total = MN * GTC_W_WORDS;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-        const int jj = (int)(e & 63), g = (int)((e >> 6) & 7);
-        const long long p = e >> 9;
-        wT[e] = (g < G && jj < baby) ? __ldg(pts2 + (long long)(g * baby + jj) * MN + p) : 0;
+        const int i = (int)(e % GTC_W_WORDS);
+        const long long p = e / GTC_W_WORDS;
+        u64 v = 0;
+        if (i < 512) {
+            const int g = i >> 6, jj = (i & 63) + 1;
+            if (g < G && jj < baby) v = bswap64(__ldg(pts2 + (long long)(g * baby + jj) * MN + p));
+        } else {
+            const int g = i - 512;
+            if (g < G) v = __ldg(pts2 + (long long)(g * baby) * MN + p);
+        }
+        wT[e] = v;
     }
 }
 
@@ -1299,7 +1311,7 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
 //                  4 gh + 3 with gh = (warp - 2) / 4, one 64-column TMEM load per position): rebuild
 //                  each (input, stream, group) sum from its 15 byte-shifted columns, reduce once mod
 //                  q, write U / Cacc (plus the step-0 member for stream 2).
-#define GTC_THREADS 448
+#define GTC_THREADS 576
 #define GTC_NST 3
 #define GTC_STAGE (GTC_A_BYTES + GTC_W_BYTES)
 #define GTC_BH_BYTES (8 * 4096)
@@ -1332,7 +1344,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
         for (int i = 0; i < 2; i++) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 8);
-            mbar_init(&bfull[i], 4);
+            mbar_init(&bfull[i], 8);
             mbar_init(&bempty[i], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
@@ -1351,7 +1363,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 mbar_expect_tx(&full[s], (uint32_t)GTC_STAGE);
                 for (int kc = 0; kc < 32; kc++)
                     bulk_g2s(st + kc * 1536, Ecan + ((long long)kc * npos + p) * 1536, 1536, &full[s]);
-                bulk_g2s(st + GTC_A_BYTES, wT + p * 512, GTC_W_BYTES, &full[s]);
+                bulk_g2s(st + GTC_A_BYTES, wT + p * GTC_W_WORDS, GTC_W_BYTES, &full[s]);
                 if (++s == GTC_NST) {
                     s = 0;
                     ph ^= 1;
@@ -1394,11 +1406,14 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 }
             }
         }
-    } else if (warp >= 10) {   // 4 expander warps: thread -> B row n (of 64 in the half) x 16 K chunks
+    } else if (warp >= 10) {   // 8 expander warps: thread -> B row n (of 64 in the half) x 8 K chunks
         const int et = tid - 10 * 32;
         const int n = et & 63, kq = et >> 6;
         const int gl = n >> 4, sp = n & 15;
-        const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? 8 * (sp - 7) : 0;
+        // byte-reversed word r: window for shift s' is (r >> 8 (7 - s')) for s' <= 7, (r << 8 (s' - 7)) above;
+        // s' = 15 is all zero
+        const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? (sp == 15 ? 0 : 8 * (sp - 7)) : 0;
+        const u64 keep = sp == 15 ? 0ull : ~0ull;
         int s = 0;
         uint32_t ph = 0;
         int it = 0;
@@ -1406,15 +1421,13 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             mbar_wait(&full[s], ph);
             for (int h = 0; h < 2; h++) {
                 mbar_wait(&bempty[h], (uint32_t)((it & 1) ^ 1));
-                const u64* raw = (const u64*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES) + (4 * h + gl) * 64;
+                const ulonglong2* raw = (const ulonglong2*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES) + (4 * h + gl) * 32;
                 uint8_t* rowbase = sBh + h * GTC_BH_BYTES + (n >> 3) * 4096 + (n & 7) * 16;
-#pragma unroll 4
-                for (int i = 0; i < 16; i++) {
-                    const int kc = kq * 16 + i;
-                    // chunk kc holds jj' = 2 kc, 2 kc + 1, i.e. baby rotations jj = 2 kc + 1, 2 kc + 2
-                    const u64 r0 = bswap64(raw[2 * kc + 1]), r1 = kc < 31 ? bswap64(raw[2 * kc + 2]) : 0ull;
-                    const u64 t0 = sp == 15 ? 0ull : (sp <= 7 ? r0 >> sh_r : r0 << sh_l);
-                    const u64 t1 = sp == 15 ? 0ull : (sp <= 7 ? r1 >> sh_r : r1 << sh_l);
+#pragma unroll
+                for (int i = 0; i < 8; i++) {
+                    const int kc = kq * 8 + i;
+                    const ulonglong2 r = raw[kc];   // rotations jj = 2 kc + 1, 2 kc + 2 (byte-reversed)
+                    const u64 t0 = ((r.x >> sh_r) << sh_l) & keep, t1 = ((r.y >> sh_r) << sh_l) & keep;
                     *(ulonglong2*)(rowbase + kc * 128) = make_ulonglong2(t0, t1);
                 }
                 asm volatile("fence.proxy.async.shared::cta;");
@@ -1442,7 +1455,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 xc0 = __ldg(X + (long long)bi * W + (long long)j * N + k);
                 xc1 = __ldg(X + (long long)bi * W + (long long)(L + j) * N + k);
 #pragma unroll
-                for (int t = 0; t < 4; t++) w0[t] = 4 * gh + t < G ? __ldg(wT + p * 512 + (4 * gh + t) * 64) : 0;
+                for (int t = 0; t < 4; t++) w0[t] = __ldg(wT + p * GTC_W_WORDS + 512 + 4 * gh + t);
             }
             mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");

@@ -1136,7 +1136,7 @@ int gala_fc_tc_weights(gala_ctx* c, const uint64_t* pts2, int T, int baby, uint8
     if (baby <= 0 || T % baby) return set_err(GALA_ERR_PARAM, "baby %d must divide T=%d", baby, T);
     const int G = T / baby;
     if (G > 8 || baby > 64) return set_err(GALA_ERR_PARAM, "tensor-core FC path needs T/baby <= 8 and baby <= 64");
-    const long long total = (long long)c->dc.M * c->dc.N * 512;
+    const long long total = (long long)c->dc.M * c->dc.N * GTC_W_WORDS;
     KLAUNCH(c, "k_gala_wt", k_gala_wt<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, pts2, baby, G, (u64*)wcan));
     return GALA_OK;
 }
