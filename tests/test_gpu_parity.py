@@ -259,14 +259,17 @@ def test_mv_gala2_tensor_core_words(tw, T):
     pts = tw.slots(T)
     pts2 = tw.gpu.encode_gala_weights(pts, b)
     wcan = tw.gpu.fc_tc_weights(pts2, T, b)
-    xs = [tw.encrypt(tw.slots()) for _ in range(3)]
-    rs = tw.slots(3)
+    nb = 17                                   # the tensor-core path runs for 16 <= B <= 32 inputs
+    xs = [tw.encrypt(tw.slots()) for _ in range(nb)]
+    rs = tw.slots(nb)
     cts = torch.stack([g for g, _ in xs])
     d_r = tw.gpu.to_device_u32(rs)
     outs, masked = tw.gpu.mv_gala2_batch(cts, pts2, T, d_r, b, wcan=wcan)
     outs1, masked1 = tw.gpu.mv_gala2_batch(cts, pts2, T, d_r, b)
     assert np.array_equal(tw.gpu.export_words(outs), tw.gpu.export_words(outs1))
-    for i, (g, c) in enumerate(xs):
+    assert np.array_equal(tw.gpu.export_words(masked), tw.gpu.export_words(masked1))
+    for i in (0, nb - 1):
+        g, c = xs[i]
         c_out, c_masked = tw.cpu.mv_gala(c, pts, rs[i], baby=b, schedule=2)
         assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
         assert np.array_equal(tw.gpu.export_words(masked[i]), c_masked)
