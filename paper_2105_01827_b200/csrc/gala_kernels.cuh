@@ -1283,17 +1283,18 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
                 if (j < L) r0 = __ldg(D + ((long long)L * M + j) * NN + src);
             }
             // row r of position kk lives at (r + kk) % 96: the 32 positions of a warp hit distinct banks
-            sm[kk][(bi + kk) % 96][jw] = e0;
-            sm[kk][(32 + bi + kk) % 96][jw] = e1;
-            sm[kk][(64 + bi + kk) % 96][jw] = r0;
+            const int r2 = 64 + bi + kk;
+            sm[kk][bi + kk][jw] = e0;
+            sm[kk][32 + bi + kk][jw] = e1;
+            sm[kk][r2 >= 96 ? r2 - 96 : r2][jw] = r0;
         }
     }
     __syncthreads();
     // chunk-major layout Ecan[kc][p][row 0..95][16 B]: the block's 32 positions are one contiguous 48 KB run
     uint8_t* dst = Ecan + ((long long)kc * MN + (long long)j * N + k0) * (96 * 16);
     for (int idx = threadIdx.x; idx < 32 * 96; idx += 256) {
-        const int kk2 = idx / 96, r = idx - kk2 * 96;
-        *(ulonglong2*)(dst + (long long)idx * 16) = *(const ulonglong2*)&sm[kk2][(r + kk2) % 96][0];
+        const int kk2 = idx / 96, r = idx - kk2 * 96, rr = r + kk2;
+        *(ulonglong2*)(dst + (long long)idx * 16) = *(const ulonglong2*)&sm[kk2][rr >= 96 ? rr - 96 : rr][0];
     }
 }
 
