@@ -152,6 +152,14 @@ def modmul_model(N, L, T, baby, schedule):
     return per_kernel, total
 
 
+def ks_modmuls_one(N, L):
+    """one full Perm, hybrid key switching, K = 1, D = L digits."""
+    from paper_2105_01827_b200.analytics import ntt_modmuls
+
+    h, K, D = ntt_modmuls(N), 1, L
+    return (L + D * (L + K - 1) + 2 * K + 2 * L) * h + (2 * D * (L + K) + 2 * L) * N
+
+
 def hbm_model(N, L, T, baby, B, tc):
     """Algorithmic DRAM bytes per launch of the schedule-2 baby-step kernels (batch of B inputs)."""
     M, G = L + 1, T // baby
@@ -302,6 +310,22 @@ def run_ours(args):
         e2e_ms = float(t.item())
     e2e_value = layers / (e2e_ms / 1e3)
 
+    # raw key-switch probe: hoisted full rotations of the batch's inputs, 8 steps each
+    ks_steps = [1, 2, 3, 5, 8, 13, 21, 34]
+    rot_outs = ctx.rotate_batch(cts_b, ks_steps)
+    torch.cuda.synchronize()
+    ks_ms = []
+    for _ in range(5):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        ctx.rotate_batch(cts_b, ks_steps)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        ks_ms.append(a0.elapsed_time(a1))
+    ks_ms_med = float(np.median(ks_ms))
+    ks_rot_per_s = B * len(ks_steps) / (ks_ms_med / 1e3)
+    del rot_outs
+
     # roofline: integer-multiply bound (modmul count) -- peak measured live with the library's own modmul
     peak_modmul = ctx.bench_modmul()
     per_kernel, layer_modmuls = modmul_model(N, L, T, baby, layer.schedule)
@@ -376,6 +400,12 @@ def run_ours(args):
                    "parallelism": f"replicas x{world} (independent inputs per GPU)",
                    "l2": "flushed (256 MB write) before every timed step"},
         "rotations_per_s": round(value * (T - 1), 1),
+        "ks_probe": {"rotations_per_s": round(ks_rot_per_s, 1), "batch": B, "steps_per_input": len(ks_steps),
+                     "ms": round(ks_ms_med, 4),
+                     "modmuls_per_rotation": ks_modmuls_one(N, L),
+                     "achieved_gmodmul_s": round(ks_rot_per_s * ks_modmuls_one(N, L) / 1e9, 1),
+                     "note": "hoisted full key switches (one decomposition per input, one ModDown per output), "
+                             "gala_rotate_batch; SURVEY 8(d) count per rotation"},
         "roofline": {
             "bound": bound,
             "kernel": dom_name,

@@ -132,6 +132,11 @@ int gala_mv_gala2_batch_tc_host(gala_ctx *ctx, const uint64_t *cts_host, int B, 
                                 const uint8_t *wcan_dev, int T, int baby, const uint32_t *r_slots_host,
                                 uint64_t *masked_host);
 
+/* Batched hoisted rotations (the raw key-switch throughput probe; he_decperm + he_hstperm,
+ * backend.py:279-294, for many inputs at once): cts_dev [B][2][L][N], steps_host [S] (non-zero),
+ * outs_dev [B][S][2][L][N]; each output equals gala_rotate(input, step). */
+int gala_rotate_batch(gala_ctx *ctx, const uint64_t *cts_dev, int B, const int *steps_host, int S, uint64_t *outs_dev);
+
 /* Fused kernel-grouping convolution (mimo_kernel_grouping, conv.py:268-293):
  * cts_dev [n_ib][2][L][N]; pts_dev [n_obp][n_ib][c_n][k][L][N];
  * tap_steps_host [k] (rotation per tap, conv.py:84-91); out [n_obp][2][L][N] */

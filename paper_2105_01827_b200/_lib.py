@@ -59,6 +59,7 @@ SIGNATURES = [
     ("gala_mv_gala_batch_host", i32, [vp, vp, i32, vp, i32, i32, vp, vp]),
     ("gala_conv_kg", i32, [vp, vp, i32, vp, i32, i32, i32, vp, i32, vp]),
     ("gala_kg_encode_weights", i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, vp]),
+    ("gala_rotate_batch", i32, [vp, vp, i32, vp, i32, vp]),
     ("gala_fc_tc_weight_bytes", ctypes.c_size_t, [vp]),
     ("gala_fc_tc_weights", i32, [vp, vp, i32, i32, vp]),
     ("gala_mv_gala2_batch_tc", i32, [vp, vp, i32, vp, vp, i32, i32, vp, vp, vp]),

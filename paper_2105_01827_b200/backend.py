@@ -376,6 +376,17 @@ class Context:
                   ctypes.c_void_p(_ptr(out)))
         return out
 
+    def rotate_batch(self, cts, steps):
+        """cts [B][2][L][N] -> [B][S][2][L][N]: every input rotated by every (non-zero) step, hoisted."""
+        torch = _torch()
+        steps = [int(s) for s in steps]
+        self.ensure_keys(steps)
+        B, S = cts.shape[0], len(steps)
+        outs = torch.empty((B, S) + tuple(cts.shape[1:]), dtype=torch.int64, device=self.device)
+        st = (ctypes.c_int * S)(*steps)
+        self.call("gala_rotate_batch", ctypes.c_void_p(_ptr(cts)), int(B), st, int(S), ctypes.c_void_p(_ptr(outs)))
+        return outs
+
     def bsgs_steps(self, T: int, baby: int | None = None):
         b = baby or int(self.lib.gala_bsgs_baby(int(T)))
         G = T // b

@@ -877,6 +877,35 @@ int gala_rotate_hoisted(gala_ctx* c, const uint64_t* ct, const uint64_t* digits,
     return rotate_engine(c, {t}, {{{0, 0}}}, {out});
 }
 
+// Batched hoisted rotations: every input decomposed once, rotated by every step (one full key switch
+// with its own ModDown per output).  outs [B][S][2][L][N].  Same words as gala_rotate per (input, step).
+int gala_rotate_batch(gala_ctx* c, const uint64_t* cts, int B, const int* steps_host, int S, uint64_t* outs)
+{
+    const int N = c->dc.N, L = c->dc.L;
+    const long long W = 2LL * L * N;
+    if (B <= 0 || S <= 0) return set_err(GALA_ERR_DIM, "empty rotation batch");
+    std::vector<int> st(S);
+    for (int i = 0; i < S; i++) {
+        st[i] = norm_step(c, steps_host[i]);
+        if (st[i] == 0) return set_err(GALA_ERR_PARAM, "step %d is the identity", steps_host[i]);
+        if (!key_for(c, st[i])) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", st[i]);
+    }
+    std::vector<EngTerm> terms(B);
+    std::vector<std::vector<EngMember>> groups;
+    std::vector<u64*> o;
+    for (int b = 0; b < B; b++) {
+        terms[b].X = cts + b * W;
+        terms[b].pt = nullptr;
+        terms[b].ntt_block = nullptr;
+        terms[b].steps = st;
+        for (int i = 0; i < S; i++) {
+            groups.push_back({{b, i}});
+            o.push_back(outs + ((long long)b * S + i) * W);
+        }
+    }
+    return rotate_engine(c, terms, groups, o);
+}
+
 int gala_rotate(gala_ctx* c, const uint64_t* ct, int step, uint64_t* out)
 {
     const int N = c->dc.N, L = c->dc.L;

@@ -273,3 +273,20 @@ def test_mv_gala2_tensor_core_words(tw, T):
         c_out, c_masked = tw.cpu.mv_gala(c, pts, rs[i], baby=b, schedule=2)
         assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
         assert np.array_equal(tw.gpu.export_words(masked[i]), c_masked)
+
+
+def test_rotate_batch_words(tw):
+    """Batched hoisted rotations == per-input rotations == oracle."""
+    import torch
+
+    n = tw.bfv.n
+    steps = sorted({1 % n, 3 % n, (n - 1) % n} - {0})
+    if not steps:
+        pytest.skip("tiny")
+    tw.keys_for(steps)
+    xs = [tw.encrypt(tw.slots()) for _ in range(3)]
+    outs = tw.gpu.rotate_batch(torch.stack([g for g, _ in xs]), steps)
+    for b, (g, c) in enumerate(xs):
+        want = tw.cpu.rotate_hoisted(c, steps)
+        for i in range(len(steps)):
+            assert np.array_equal(tw.gpu.export_words(outs[b, i]), want[i])
