@@ -762,35 +762,44 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
         const u64 q = md.q;
         const ulonglong2 pc = pconst[j < M ? j : 0];   // P mod q_j, Shoup companion
         const int gpt = KG_KT / nb, g0 = K0 / nb, G = n_ib * k;
-        const long long bw = (long long)(L * M + L) * N;
+        const int bw = (L * M + L) * N;                  // words per identity block (< 2^31)
+        const u64* Dj = Dblk + (long long)j * N;
+        const u64* Xj = X + (long long)comp * L * N + jl;
+        const int koff = (comp * M + j) * N + i;
+        // (ib, t) of g = g0 + gl, advanced incrementally (gl steps by 8): no division in the loop
+        int gfirst = g0 + w;
+        int ib = gfirst / k, t = gfirst - ib * k;
         for (int gl = w; gl < gpt; gl += 8) {
             const int g = g0 + gl;
             const bool valid = g < G && pos < P2;
+            const int tt = t;
             u64 z = 0;
-            int t = 0;
             if (valid) {
-                const int ib = g / k;
-                t = g - ib * k;
-                const u64* key = keys[t];
+                const u64* key = keys[tt];
                 if (key == nullptr) {
-                    if (j < L) z = csub(shoup_lazy_sf(__ldg(X + ((long long)ib * 2 + comp) * L * N + jl), pc.x, pc.y, q), q);
+                    if (j < L) z = csub(shoup_lazy_sf(__ldg(Xj + (long long)ib * 2 * L * N), pc.x, pc.y, q), q);
                 } else {
-                    const int src = auto_src(i, gal[t], logN);
-                    const u64* D = Dblk + ib * bw + (long long)j * N + src;
-                    const u64* kp = key + ((long long)comp * M + j) * N + i;
+                    const int src = auto_src(i, gal[tt], logN);
+                    const u64* D = Dj + (long long)ib * bw + src;
+                    const u64* kp = key + koff;
                     Acc128 s;
 #pragma unroll
-                    for (int l = 0; l < L; l++) s.mac(__ldg(D + (long long)l * MN), __ldg(kp + (long long)l * 2 * MN));
+                    for (int l = 0; l < L; l++) s.mac(__ldg(D + l * MN), __ldg(kp + l * 2 * MN));
                     z = s.reduce(md);
                     if (comp == 0 && j < L)
-                        z = add_mod(z, csub(shoup_lazy_sf(__ldg(D + (long long)L * MN), pc.x, pc.y, q), q), q);
+                        z = add_mod(z, csub(shoup_lazy_sf(__ldg(D + L * MN), pc.x, pc.y, q), q), q);
                 }
+            }
+            t += 8;
+            while (t >= k) {
+                t -= k;
+                ib++;
             }
             if (masks == nullptr) {            // post-mask form: the GEMM takes Z itself (nb == 1)
                 sm[kg_swz(pp, gl)] = z ^ 0x8080808080808080ull;
                 continue;
             }
-            const ulonglong2* mk = masks + (long long)t * nb * MN + jl;
+            const ulonglong2* mk = masks + (long long)tt * nb * MN + jl;
             for (int beta = 0; beta < nb; beta++) {
                 u64 v = 0;
                 if (valid) {
