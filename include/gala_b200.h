@@ -143,6 +143,16 @@ int gala_rotate_batch(gala_ctx *ctx, const uint64_t *cts_dev, int B, const int *
 int gala_conv_kg(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *pts_dev, int n_obp,
                  int c_n, int k, const int *tap_steps_host, int band_step, uint64_t *outs_dev);
 
+/* Schedule-1 first-Add on the int8 tensor cores: per Q position one byte-convolution MMA of the
+ * plaintext bytes (A, position-major ptcan_dev written once by gala_kg1_tc_weights from the
+ * gala_kg_encode_weights plaintexts; gala_kg1_tc_bytes bytes, 0 if the shape is unsupported:
+ * n_obp c_n <= 512 rows, n_ib k <= 1024 words) with the rotated inputs' byte-shift expansion (B).
+ * Same words as gala_conv_kg. */
+size_t gala_kg1_tc_bytes(gala_ctx *ctx, int n_ib, int n_obp, int c_n, int k);
+int gala_kg1_tc_weights(gala_ctx *ctx, const uint64_t *pts_dev, int n_obp, int n_ib, int c_n, int k, uint64_t *ptcan_dev);
+int gala_conv_kg_tc(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *ptcan_dev, int n_obp, int c_n, int k,
+                    const int *tap_steps_host, int band_step, uint64_t *outs_dev);
+
 /* On-GPU kernel-grouping weight encoding (coef_vectors, conv.py:220-235, in the physical
  * two-row form): kernels_dev int32 [c_o][c_i][k_h][k_w] (values mod p) -> pts_dev
  * [n_obp][n_ib][c_n][k_h k_w][L][N] ready for gala_conv_kg.  pair = 2 puts output blocks

@@ -487,6 +487,26 @@ class Context:
                   int(c_n), int(k), st, int(band_step), ctypes.c_void_p(_ptr(outs)))
         return outs
 
+    def kg1_tc_weights(self, pts, n_obp: int, n_ib: int, c_n: int, k: int):
+        """Position-major copy of schedule-1 KG plaintexts for the tensor-core first-Add (None: unsupported)."""
+        torch = _torch()
+        nbytes = int(self.lib.gala_kg1_tc_bytes(self._bind(), int(n_ib), int(n_obp), int(c_n), int(k)))
+        if nbytes == 0:
+            return None
+        out = torch.empty(nbytes // 8, dtype=torch.int64, device=self.device)
+        self.call("gala_kg1_tc_weights", ctypes.c_void_p(_ptr(pts)), int(n_obp), int(n_ib), int(c_n), int(k),
+                  ctypes.c_void_p(_ptr(out)))
+        return out
+
+    def conv_kg_tc(self, cts, ptcan, n_obp: int, n_ib: int, c_n: int, k: int, tap_steps, band_step: int):
+        """Schedule 1 with the first-Add on the tensor cores; same words as conv_kg."""
+        self.ensure_keys(list(tap_steps) + [d * band_step for d in range(1, c_n)])
+        outs = self.empty_ct(n_obp)
+        st = (ctypes.c_int * k)(*[int(s) for s in tap_steps])
+        self.call("gala_conv_kg_tc", ctypes.c_void_p(_ptr(cts)), int(n_ib), ctypes.c_void_p(_ptr(ptcan)), int(n_obp),
+                  int(c_n), int(k), st, int(band_step), ctypes.c_void_p(_ptr(outs)))
+        return outs
+
     def conv_kg2(self, cts, masks, coef, rowsum, k: int, nb: int, tap_steps, band_step: int, c_n: int,
                  post: bool = False):
         """Schedule 2: cts [n_ib][2][L][N] -> [Mr/c_n][2][L][N].  Pre-mask: masks [k][nb][M][N][2],

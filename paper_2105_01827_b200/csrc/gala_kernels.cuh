@@ -1525,6 +1525,252 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
 }
 
 // ---------------------------------------------------------------------------
+// Conv schedule 1 first-Add on the tensor cores.  Per Q position p = (j, x):
+//   acc[r][comp] = sum_w R[comp][w] pt[r][w]      (r = o c_n + d, w = ib k + tap)
+// with 8-byte operands is, as in k_gala_tc, one int8 byte-convolution MMA per position:
+//   D[r][(comp, s')] = sum_(w, a) pt_a[r][w] R_(s' - a)[comp][w],   acc = sum_s' 256^s' D_s'
+// A = the plaintext bytes (streamed from HBM in K-chunk stages: PTcan[p][kc][Rp rows][16 B]),
+// B = the byte-convolution expansion of the position's rotated inputs (32 rows (comp, s')), built
+// in shared memory from Rt[p][comp][w].  The exact sum can exceed 2^128, so the rebuild folds three
+// 40-bit-spaced partial sums with 2^40 and 2^80 mod q before one REDC (pt is Montgomery: the REDC
+// yields sum R pt mod q; K <= 1024 words keeps every partial below 2^64 and the fold below 2^124).
+// Same words as k_kg_accumulate.
+#define KG1_GK 8            // 16-byte K chunks per A stage
+#define KG1_NST 4
+#define KG1_THREADS 320     // warp 0 producer, 1 MMA, 2..5 epilogue, 6..9 expanders
+
+// pts [n_obp][n_ib][c_n][k][L][N] (Montgomery) -> PTcan [p][KC][Rp][16 B], row r = o c_n + d, word w = ib k + t
+__global__ void k_kg1_pt_can(DevCtx c, const u64* __restrict__ pts, int n_obp, int n_ib, int c_n, int k, int Rp, int KC,
+                             u64* __restrict__ out)
+{
+    const int N = c.N, L = c.L;
+    const long long P = (long long)L * N, LN = (long long)L * N;
+    const long long per_p = (long long)KC * Rp * 2;            // words per position
+    const long long total = P * per_p;
+    const int Kw = n_ib * k, Mr = n_obp * c_n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long p = e / per_p;
+        const int rem = (int)(e - p * per_p);
+        const int kc = rem / (Rp * 2), r = (rem / 2) % Rp, half = rem & 1;
+        const int w = 2 * kc + half;
+        u64 v = 0;
+        if (r < Mr && w < Kw) {
+            const int o = r / c_n, d = r - o * c_n, ib = w / k, t = w - ib * k;
+            v = __ldg(pts + ((((long long)o * n_ib + ib) * c_n + d) * k + t) * LN + p);
+        }
+        out[e] = v;
+    }
+}
+
+// R [ib][t][2][L][N] -> Rt[p][comp][Kwp] (byte-reversed for the expansion; zero padding)
+__global__ void k_kg1_rt(DevCtx c, const u64* __restrict__ R, int Kw, int Kwp, u64* __restrict__ Rt)
+{
+    const int N = c.N, L = c.L;
+    const long long LN = (long long)L * N, W = 2 * LN;
+    const long long total = LN * 2 * Kwp;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int w = (int)(e % Kwp);
+        const long long pc = e / Kwp;
+        const int comp = (int)(pc & 1);
+        const long long p = pc >> 1;
+        Rt[e] = w < Kw ? bswap64(__ldg(R + (long long)w * W + comp * LN + p)) : 0ull;
+    }
+}
+
+template <int MT>
+__global__ void __launch_bounds__(KG1_THREADS, 1) k_kg1_tc(DevCtx c, const uint8_t* __restrict__ PTcan,
+                                                          const u64* __restrict__ Rt, int Mr, int Kwp,
+                                                          u64* __restrict__ acc)
+{
+    extern __shared__ __align__(128) uint8_t k1_sm[];
+    constexpr int Rp = MT * 128;
+    constexpr int STAGE = KG1_GK * Rp * 16;
+    const int KC = Kwp / 2, nst = KC / KG1_GK;
+    const int BBYTES = KC * 32 * 16, RAW = 2 * Kwp * 8;
+    uint8_t* ring = k1_sm;                                   // [KG1_NST][STAGE]
+    uint8_t* sB = k1_sm + KG1_NST * STAGE;                   // [2][BBYTES]
+    uint8_t* sRaw = sB + 2 * BBYTES;                         // [2][RAW]
+    __shared__ uint64_t full[KG1_NST], empty[KG1_NST], rfull[2], rempty[2], bfull[2], bempty[2], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base_sh;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int N = c.N, L = c.L;
+    const long long P = (long long)L * N;
+    const long long per = (P + gridDim.x - 1) / gridDim.x;
+    const long long p0 = blockIdx.x * per, p1 = p0 + per < P ? p0 + per : P;
+    constexpr uint32_t TCOLS = 2 * MT * 32 <= 32 ? 32 : (2 * MT * 32 <= 64 ? 64 : (2 * MT * 32 <= 128 ? 128 : 256));
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(TCOLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < KG1_NST; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&rfull[i], 1);
+            mbar_init(&rempty[i], 4);
+            mbar_init(&bfull[i], 4);
+            mbar_init(&bempty[i], 1);
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base_sh;
+    if (warp == 0) {
+        if (lane == 0) {   // producer: raw rotated inputs per position, plaintext K-chunk stages
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (long long p = p0; p < p1; p++, it++) {
+                const int b = it & 1;
+                mbar_wait(&rempty[b], (uint32_t)(((it >> 1) & 1) ^ 1));
+                mbar_expect_tx(&rfull[b], (uint32_t)RAW);
+                bulk_g2s(sRaw + b * RAW, Rt + p * 2 * Kwp, RAW, &rfull[b]);
+                for (int g = 0; g < nst; g++) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_expect_tx(&full[s], (uint32_t)STAGE);
+                    bulk_g2s(ring + s * STAGE, PTcan + (p * KC + (long long)g * KG1_GK) * Rp * 16, STAGE, &full[s]);
+                    if (++s == KG1_NST) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // MMA issuer
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(32 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (long long p = p0; p < p1; p++, it++) {
+                const int a = it & 1;
+                mbar_wait(&tempty[a], (uint32_t)(((it >> 1) & 1) ^ 1));
+                mbar_wait(&bfull[a], (uint32_t)((it >> 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sb = smem_u32(sB + a * BBYTES);
+                for (int g = 0; g < nst; g++) {
+                    mbar_wait(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t sa = smem_u32(ring + s * STAGE);
+#pragma unroll
+                    for (int mt = 0; mt < MT; mt++) {
+                        const uint32_t d = tmem + (uint32_t)((a * MT + mt) * 32);
+#pragma unroll
+                        for (int kk = 0; kk < KG1_GK / 2; kk++) {
+                            const uint64_t ad = umma_desc_kmajor(sa + kk * 2 * Rp * 16 + mt * 128 * 16, Rp * 16, 128);
+                            const uint64_t bd = umma_desc_kmajor(sb + (g * KG1_GK + kk * 2) * 512, 512, 128);
+                            const uint32_t accum = (g > 0 || kk > 0) ? 1u : 0u;
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\t"
+                                "setp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                                ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+                        }
+                    }
+                    umma_commit(&empty[s]);
+                    if (++s == KG1_NST) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit(&bempty[a]);
+                umma_commit(&tfull[a]);
+            }
+        }
+    } else if (warp >= 6) {   // expanders: B row n = (comp, s'), thread -> (row, chunk subset)
+        const int et = tid - 6 * 32;
+        const int n = et & 31, part = et >> 5;                  // 4 parts over the K chunks
+        const int comp = n >> 4, sp = n & 15;
+        const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? (sp == 15 ? 0 : 8 * (sp - 7)) : 0;
+        const u64 keep = sp == 15 ? 0ull : ~0ull;
+        int it = 0;
+        for (long long p = p0; p < p1; p++, it++) {
+            const int b = it & 1;
+            mbar_wait(&rfull[b], (uint32_t)((it >> 1) & 1));
+            mbar_wait(&bempty[b], (uint32_t)(((it >> 1) & 1) ^ 1));
+            const ulonglong2* raw = (const ulonglong2*)(sRaw + b * RAW) + comp * (Kwp / 2);
+            uint8_t* rowbase = sB + b * BBYTES + (n >> 3) * 128 + (n & 7) * 16;
+            for (int kc = part; kc < KC; kc += 4) {
+                const ulonglong2 r = raw[kc];                   // words w = 2 kc, 2 kc + 1 (byte-reversed)
+                const u64 t0 = ((r.x >> sh_r) << sh_l) & keep, t1 = ((r.y >> sh_r) << sh_l) & keep;
+                *(ulonglong2*)(rowbase + kc * 512) = make_ulonglong2(t0, t1);
+            }
+            asm volatile("fence.proxy.async.shared::cta;");
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&bfull[b]);
+                mbar_arrive(&rempty[b]);
+            }
+        }
+    } else {   // epilogue: lane group lg = warp % 4 -> rows 32 lg + lane of every M tile
+        const int lg = warp & 3;
+        const long long LN = (long long)L * N;
+        int it = 0;
+        for (long long p = p0; p < p1; p++, it++) {
+            const int a = it & 1;
+            const int j = (int)(p / N);
+            const ModC md = c.mod[j];
+            const u64 q = md.q;
+            const u64 c40 = (u64)(((unsigned __int128)1 << 40) % q), c80 = (u64)((((unsigned __int128)c40) << 40) % q);
+            mbar_wait(&tfull[a], (uint32_t)((it >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            uint32_t x[MT][32];
+#pragma unroll
+            for (int mt = 0; mt < MT; mt++) {
+                const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)((a * MT + mt) * 32);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                    "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                    : "=r"(x[mt][0]), "=r"(x[mt][1]), "=r"(x[mt][2]), "=r"(x[mt][3]), "=r"(x[mt][4]), "=r"(x[mt][5]),
+                      "=r"(x[mt][6]), "=r"(x[mt][7]), "=r"(x[mt][8]), "=r"(x[mt][9]), "=r"(x[mt][10]), "=r"(x[mt][11]),
+                      "=r"(x[mt][12]), "=r"(x[mt][13]), "=r"(x[mt][14]), "=r"(x[mt][15]), "=r"(x[mt][16]), "=r"(x[mt][17]),
+                      "=r"(x[mt][18]), "=r"(x[mt][19]), "=r"(x[mt][20]), "=r"(x[mt][21]), "=r"(x[mt][22]), "=r"(x[mt][23]),
+                      "=r"(x[mt][24]), "=r"(x[mt][25]), "=r"(x[mt][26]), "=r"(x[mt][27]), "=r"(x[mt][28]), "=r"(x[mt][29]),
+                      "=r"(x[mt][30]), "=r"(x[mt][31])
+                    : "r"(taddr));
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+#pragma unroll
+            for (int mt = 0; mt < MT; mt++) {
+                const int r = mt * 128 + lg * 32 + lane;
+                if (r >= Mr) continue;
+#pragma unroll
+                for (int comp = 0; comp < 2; comp++) {
+                    const uint32_t* xs = x[mt] + comp * 16;
+                    u64 lo5 = 0, mi5 = 0, hi5 = 0;
+#pragma unroll
+                    for (int u = 0; u < 5; u++) {
+                        lo5 += (u64)xs[u] << (8 * u);
+                        mi5 += (u64)xs[5 + u] << (8 * u);
+                        hi5 += (u64)xs[10 + u] << (8 * u);
+                    }
+                    // lo5 + mi5 2^40 + hi5 2^80 == sum R pt (mod q); fold with the constants (< 2^120)
+                    Acc128 t;
+                    t.mac(mi5, c40);
+                    t.mac(hi5, c80);
+                    t.lo += lo5;
+                    t.hi += t.lo < lo5 ? 1ull : 0ull;
+                    if (t.hi >= q) t.hi -= q;                       // t < 2^124 (Kwp <= 1024): hi < 2^60
+                    const u64 v = csub(redc_lazy(t.hi, t.lo, md), q);
+                    acc[((long long)r * 2 + comp) * LN + p] = v;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TCOLS));
+}
+
+// ---------------------------------------------------------------------------
 // encoding.  MODE 0: plaintext operand (centred lift, Montgomery);
 //            MODE 1: Delta * m (plain), for encrypt / subtract_plain
 // one CTA per (vector b, prime j); each CTA recomputes the mod-p INTT (cheap,

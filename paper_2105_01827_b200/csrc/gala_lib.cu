@@ -666,6 +666,9 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_gala_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_kg1_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CKC(cudaFuncSetAttribute(k_kg1_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CKC(cudaFuncSetAttribute(k_kg1_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CKC(cudaFuncSetAttribute(k_kg_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              KG_TC_STAGES * KG_TC_KCS * (128 + KG_TC_N) * 16 + 2 * 512 * 32));
     {
@@ -1225,8 +1228,56 @@ int gala_mv_gala_host(gala_ctx* c, const uint64_t* ct_host, const uint64_t* pts,
     return gala_mv_gala_batch_host(c, ct_host, 1, pts, T, baby, r_host, masked_host);
 }
 
+// schedule-1 plaintexts on the tensor cores: tile geometry
+static void kg1_geom(int n_ib, int n_obp, int c_n, int k, int* Rp, int* Kwp, int* MT)
+{
+    const int Mr = n_obp * c_n, Kw = n_ib * k;
+    *MT = (Mr + 127) / 128;
+    *Rp = *MT * 128;
+    *Kwp = (Kw + 15) / 16 * 16;
+}
+
+static size_t kg1_smem(int MT, int Kwp)
+{
+    return (size_t)KG1_NST * KG1_GK * MT * 128 * 16 + 2 * (size_t)(Kwp / 2) * 512 + 2 * (size_t)Kwp * 16;
+}
+
+size_t gala_kg1_tc_bytes(gala_ctx* c, int n_ib, int n_obp, int c_n, int k)
+{
+    int Rp, Kwp, MT;
+    kg1_geom(n_ib, n_obp, c_n, k, &Rp, &Kwp, &MT);
+    if ((MT != 1 && MT != 2 && MT != 4) || Kwp > 1024 || kg1_smem(MT, Kwp) > 220 * 1024 || c->dc.N % 32) return 0;
+    return (size_t)c->dc.L * c->dc.N * Kwp * Rp * 8;
+}
+
+int gala_kg1_tc_weights(gala_ctx* c, const uint64_t* pts, int n_obp, int n_ib, int c_n, int k, uint64_t* ptcan)
+{
+    int Rp, Kwp, MT;
+    kg1_geom(n_ib, n_obp, c_n, k, &Rp, &Kwp, &MT);
+    if (gala_kg1_tc_bytes(c, n_ib, n_obp, c_n, k) == 0) return set_err(GALA_ERR_PARAM, "layer shape not supported on the tensor-core path");
+    const long long total = (long long)c->dc.L * c->dc.N * (Kwp / 2) * Rp * 2;
+    KLAUNCH(c, "k_kg1_pt_can", k_kg1_pt_can<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, pts, n_obp, n_ib, c_n, k, Rp,
+                                                                                     Kwp / 2, ptcan));
+    return GALA_OK;
+}
+
+static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts, const uint64_t* ptcan, int n_obp,
+                       int c_n, int k, const int* tap_steps, int band_step, uint64_t* outs);
+
 int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts, int n_obp, int c_n, int k,
                  const int* tap_steps, int band_step, uint64_t* outs)
+{
+    return conv_kg_run(c, cts, n_ib, pts, nullptr, n_obp, c_n, k, tap_steps, band_step, outs);
+}
+
+int gala_conv_kg_tc(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* ptcan, int n_obp, int c_n, int k,
+                    const int* tap_steps, int band_step, uint64_t* outs)
+{
+    return conv_kg_run(c, cts, n_ib, nullptr, ptcan, n_obp, c_n, k, tap_steps, band_step, outs);
+}
+
+static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts, const uint64_t* ptcan, int n_obp,
+                       int c_n, int k, const int* tap_steps, int band_step, uint64_t* outs)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const long long W = 2LL * L * N;
@@ -1271,6 +1322,26 @@ int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts
     // first-Add: acc[o][d] over all input blocks and taps
     u64* acc;
     RET(scratch(c, &acc, (size_t)n_obp * c_n * W));
+    if (ptcan) {   // on the tensor cores: position-major plaintext bytes x byte-convolution of R
+        int Rp, Kwp, MT;
+        kg1_geom(n_ib, n_obp, c_n, k, &Rp, &Kwp, &MT);
+        if (gala_kg1_tc_bytes(c, n_ib, n_obp, c_n, k) == 0) return set_err(GALA_ERR_PARAM, "layer shape not supported on the tensor-core path");
+        u64* Rt;
+        RET(scratch(c, &Rt, (size_t)L * N * 2 * Kwp));
+        KLAUNCH(c, "k_kg1_rt", k_kg1_rt<<<grid_for((long long)L * N * 2 * Kwp, 256), 256, 0, c->stream>>>(c->dc, R, n_ib * k, Kwp, Rt));
+        release(c, R);
+        const size_t smem = kg1_smem(MT, Kwp);
+        const int grid1 = c->num_sms;
+#define KG1(MTV) KLAUNCH(c, "k_kg1_tc", (k_kg1_tc<MTV><<<grid1, KG1_THREADS, smem, c->stream>>>(c->dc, (const uint8_t*)ptcan, Rt, n_obp * c_n, Kwp, acc)))
+        if (MT == 1) KG1(1);
+        else if (MT == 2) KG1(2);
+        else KG1(4);
+#undef KG1
+        release(c, Rt);
+        RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, n_obp, c_n, band_step, outs, 0));
+        release(c, acc);
+        return GALA_OK;
+    }
     const int th = N < 256 ? N : 256;
     dim3 grid((N + th - 1) / th, L, n_obp * c_n);
     // input-block chunks whose rotated inputs (k * W words each) fit comfortably in L2 (~48 MB)

@@ -335,7 +335,7 @@ def test_gpu_weight_encoding_equals_host_encoding(u, c_i, k, c_o, n):
     rng = np.random.default_rng(u + c_i)
     task = ConvTask(u, u, c_i, k, k, c_o, rng.integers(0, P, (c_o, c_i, k, k)), params)
     for pair in (True, False):
-        a = KernelGroupingConv(task, pair_rows=pair)
+        a = KernelGroupingConv(task, pair_rows=pair, schedule=1, drop_plaintexts=False)
         b = KernelGroupingConv(task, pair_rows=pair, host_encode=True)
         assert bool((a.pts == b.pts).all())
 

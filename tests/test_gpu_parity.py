@@ -79,6 +79,7 @@ def test_mv_gala_words(tw, T):
 
 
 def test_conv_kg_words(tw):
+    """Schedule 1 (CUDA-core and tensor-core first-Add) == oracle o_conv_kg."""
     n = tw.bfv.n
     if n < 16:
         pytest.skip("tiny")
@@ -96,6 +97,11 @@ def test_conv_kg_words(tw):
     g_out = tw.gpu.conv_kg(g_in, d_pts, tap_steps, band)
     c_out = tw.cpu.conv_kg(c_in, pts, tap_steps, band)
     assert np.array_equal(tw.gpu.export_words(g_out), c_out)
+    # the same first-Add on the tensor cores (byte-convolution int8 MMA per position)
+    ptcan = tw.gpu.kg1_tc_weights(d_pts, n_obp, n_ib, c_n, k)
+    if ptcan is not None:
+        t_out = tw.gpu.conv_kg_tc(g_in, ptcan, n_obp, n_ib, c_n, k, tap_steps, band)
+        assert np.array_equal(tw.gpu.export_words(t_out), c_out)
 
 
 def test_mv_gala_batch_words(tw):
