@@ -184,6 +184,12 @@ int gala_conv_kg2_post(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const u
                        const int8_t *coef_dev, const int32_t *rowsum_dev, int Mr, int Kp, const int *tap_steps_host,
                        int band_step, int c_n, uint64_t *outs_dev);
 
+/* The same for nbatch independent images sharing the weights (e.g. a layer's halo tiles):
+ * cts_dev [nbatch][n_ib][2][L][N] -> outs_dev [nbatch][Mr / c_n][2][L][N]; one pass of launches. */
+int gala_conv_kg2_post_batch(gala_ctx *ctx, const uint64_t *cts_dev, int nbatch, int n_ib, const uint64_t *masks_dev,
+                             int k, int nb, const int8_t *coef_dev, const int32_t *rowsum_dev, int Mr, int Kp,
+                             const int *tap_steps_host, int band_step, int c_n, uint64_t *outs_dev);
+
 /* canonical word import/export of `count` ciphertexts */
 int gala_ct_export(gala_ctx *ctx, const uint64_t *ct_dev, uint64_t *coef_dev, int count);
 int gala_ct_import(gala_ctx *ctx, const uint64_t *coef_dev, uint64_t *ct_dev, int count);

@@ -70,6 +70,7 @@ SIGNATURES = [
     ("gala_kg2_encode_masks", i32, [vp, i32, i32, i32, i32, i32, i32, vp]),
     ("gala_conv_kg2", i32, [vp, vp, i32, vp, i32, i32, vp, vp, i32, i32, vp, i32, i32, vp]),
     ("gala_conv_kg2_post", i32, [vp, vp, i32, vp, i32, i32, vp, vp, i32, i32, vp, i32, i32, vp]),
+    ("gala_conv_kg2_post_batch", i32, [vp, vp, i32, i32, vp, i32, i32, vp, vp, i32, i32, vp, i32, i32, vp]),
     ("gala_ct_export", i32, [vp, vp, vp, i32]),
     ("gala_ct_import", i32, [vp, vp, vp, i32]),
     ("gala_pt_export", i32, [vp, vp, vp, i32]),

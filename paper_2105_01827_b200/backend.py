@@ -523,6 +523,21 @@ class Context:
                   ctypes.c_void_p(_ptr(outs)))
         return outs
 
+    def conv_kg2_batch(self, cts_batch, masks, coef, rowsum, k: int, nb: int, tap_steps, band_step: int, c_n: int):
+        """Post-mask schedule 2 over B images sharing the weights: [B][n_ib][2][L][N] -> [B][Mr/c_n][2][L][N]."""
+        torch = _torch()
+        nbatch, n_ib = cts_batch.shape[0], cts_batch.shape[1]
+        rows, Kp = coef.shape
+        Mr = rows // nb
+        self.ensure_keys(list(tap_steps) + [d * band_step for d in range(1, c_n)])
+        outs = torch.empty((nbatch, Mr // c_n, 2, self.L, self.N), dtype=torch.int64, device=self.device)
+        st = (ctypes.c_int * k)(*[int(s) for s in tap_steps])
+        self.call("gala_conv_kg2_post_batch", ctypes.c_void_p(_ptr(cts_batch)), int(nbatch), int(n_ib),
+                  ctypes.c_void_p(_ptr(masks)), int(k), int(nb), ctypes.c_void_p(_ptr(coef)),
+                  ctypes.c_void_p(_ptr(rowsum)), int(Mr), int(Kp), st, int(band_step), int(c_n),
+                  ctypes.c_void_p(_ptr(outs)))
+        return outs
+
     def kg2_encode_masks(self, k_h: int, k_w: int, u_w: int, u_h: int, pair: int, band_only: bool = False):
         torch = _torch()
         c_n = self.params.n // (u_w * u_h)

@@ -754,6 +754,11 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
     constexpr int M = L + 1;
     const int N = c.N, logN = c.logN, MN = M * N, P2 = 2 * MN;
     const int pos0 = blockIdx.x * KG_PT, K0 = blockIdx.y * KG_KT;
+    // batch element blockIdx.z: its inputs follow the previous elements' (n_ib each), its byte planes
+    // continue the tile order (canon only)
+    Dblk += (long long)blockIdx.z * n_ib * ((L * M + L) * (long long)N);
+    X += (long long)blockIdx.z * n_ib * 2 * L * (long long)N;
+    Bt += (long long)blockIdx.z * 8 * P2 * (long long)Kp;
     {
         const int pp = threadIdx.x & 31, w = threadIdx.x >> 5;
         const int pos = pos0 + pp;
@@ -1002,7 +1007,8 @@ __global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8
                                                            const int32_t* __restrict__ rowsum, int rows_real, int rbs,
                                                            int nb, int Mr, const int8_t* __restrict__ Bcan, int Kp,
                                                            int ntiles, const ulonglong2* __restrict__ off,
-                                                           const ulonglong2* __restrict__ masks, u64* __restrict__ accq)
+                                                           const ulonglong2* __restrict__ masks, u64* __restrict__ accq,
+                                                           int tiles_per_batch)
 {
     extern __shared__ __align__(128) uint8_t kg_sm[];
     constexpr int STAGE_BYTES = KG_TC_KCS * (128 + KG_TC_N) * 16;
@@ -1104,7 +1110,8 @@ __global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8
             const int acc = it & 1;
             const int rb = (int)(jb % rbs);
             const long long tile = jb / rbs;
-            const long long pos0 = tile * (KG_TC_N / 8);
+            const long long bat = tile / tiles_per_batch;                 // batch element of this tile
+            const long long pos0 = (tile - bat * tiles_per_batch) * (KG_TC_N / 8);
             const int jl0 = (int)(pos0 % MN);
             ulonglong2* sm = sMask + acc * nb * 32;
             for (int q = et; q < nb * 32; q += KG_TC_EPI_WARPS * 32)
@@ -1150,7 +1157,7 @@ __global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8
                 }
                 // sum the nb band rows (lanes beta = 0..nb-1 of the group) as a reduce-scatter over
                 // the 4 words: the first two rounds halve the words each lane carries
-                u64* dstrow = accq + (long long)m * WQ + pos0 + p0;
+                u64* dstrow = accq + (bat * Mr + m) * WQ + pos0 + p0;
                 const bool wr = row_ok && m < Mr;
                 if (nb == 1) {
                     if (wr) {

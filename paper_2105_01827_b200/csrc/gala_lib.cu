@@ -1497,9 +1497,11 @@ static unsigned __int128 kg_offset(u64 q)
     return (two90 / q + 1) * q;
 }
 
+// nbatch independent images (e.g. the halo tiles of one layer) share the weights and every launch:
+// cts [nbatch][n_ib][2][L][N] -> outs [nbatch][Mr / c_n][2][L][N] (fused tcgen05 path only for nbatch > 1)
 static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, const uint64_t* masks, int k, int nb,
                         const int8_t* coef, const int32_t* rowsum, int Mr, int Kp, const int* tap_steps, int band_step,
-                        int c_n, uint64_t* outs)
+                        int c_n, uint64_t* outs, int nbatch = 1)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const long long W = 2LL * L * N, WQ = 2LL * M * N;
@@ -1539,11 +1541,12 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     if (KG_KT % nb_y) return set_err(GALA_ERR_DIM, "band count %d must divide %d", nb, KG_KT);
     // 1. one decomposition per input: identity digit block [(L M + L)][N]
     const long long blk_words = (long long)(L * M + L) * N;
+    const int n_in = nbatch * n_ib;          // decomposed inputs over the whole batch
     u64 *dig, *Dblk;
-    RET(scratch(c, &dig, (size_t)n_ib * L * N));
-    RET(scratch(c, &Dblk, (size_t)n_ib * blk_words));
-    std::vector<TermDesc> td(n_ib);
-    for (int b = 0; b < n_ib; b++) {
+    RET(scratch(c, &dig, (size_t)n_in * L * N));
+    RET(scratch(c, &Dblk, (size_t)n_in * blk_words));
+    std::vector<TermDesc> td(n_in);
+    for (int b = 0; b < n_in; b++) {
         td[b].X = cts + b * W;
         td[b].pt = nullptr;
         td[b].dig = dig + (long long)b * L * N;
@@ -1570,20 +1573,21 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     const int nt = ntt_threads(N);
     const unsigned* d_gal = (const unsigned*)(d_blob + o_gal);
     if (any_rot) {
-        KLAUNCH(c, "k_digits_intt", k_digits_intt<<<(unsigned)(n_ib * L), nt, c->smem_ntt, c->stream>>>(
+        KLAUNCH(c, "k_digits_intt", k_digits_intt<<<(unsigned)(n_in * L), nt, c->smem_ntt, c->stream>>>(
                                         c->dc, (const TermDesc*)d_blob, d_gal, blk_words));
-        KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(n_ib * L * L), nt, c->smem_ntt, c->stream>>>(
+        KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(n_in * L * L), nt, c->smem_ntt, c->stream>>>(
                                         c->dc, (const TermDesc*)d_blob, d_gal, blk_words));
     }
     // fused tcgen05 path (post-mask form, bands within a warp, K in 32-byte steps): the byte planes are
     // written in the tensor-core tile order so every pipeline stage is one bulk copy
     const bool tc = post && nb <= 32 && (32 % nb) == 0 && Kp % 32 == 0 && (c->dc.N % 32) == 0 &&
                     getenv("GALA_KG_NO_TC") == nullptr;
+    if (nbatch > 1 && !tc) return set_err(GALA_ERR_PARAM, "batched convolution needs the fused tensor-core post-mask path");
     // 2. fused key switch (no ModDown) + band masks -> biased bytes, K-contiguous: Bt[8 WQ][Kp]
     int8_t* Bt;
-    RET(scratch(c, &Bt, (size_t)8 * WQ * Kp));
+    RET(scratch(c, &Bt, (size_t)8 * WQ * Kp * nbatch));
     {
-        dim3 grid((unsigned)((WQ + KG_PT - 1) / KG_PT), (unsigned)((Kp + KG_KT - 1) / KG_KT));
+        dim3 grid((unsigned)((WQ + KG_PT - 1) / KG_PT), (unsigned)((Kp + KG_KT - 1) / KG_KT), (unsigned)nbatch);
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
         const ulonglong2* pm = (const ulonglong2*)(c->d_kg_off + 2 * GALA_MAXM);
 #define KG_ZY(LL)                                                                                                  \
@@ -1602,7 +1606,7 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     release(c, Dblk);
     release(c, d_blob);
     u64* accq;
-    RET(scratch(c, &accq, (size_t)Mr * WQ));
+    RET(scratch(c, &accq, (size_t)nbatch * Mr * WQ));
     if (tc) {
         // 3+4. first-Add on the tensor cores with the byte recombination and band masks in the epilogue
         const int rows_p = (rows + 127) / 128 * 128;
@@ -1610,14 +1614,14 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         RET(scratch(c, &Acan, (size_t)rows_p * Kp));
         KLAUNCH(c, "k_kg_tc_layout_a", k_kg_tc_layout_a<<<grid_for((long long)rows_p * Kp / 16, 256), 256, 0, c->stream>>>(
                                            coef, rows, rows_p, Kp, Acan));
-        const int ntiles = (int)(8 * WQ / KG_TC_N);
+        const int ntiles = (int)(8 * WQ / KG_TC_N) * nbatch;
         const int rbs = rows_p / 128;
         long long jobs = (long long)ntiles * rbs;
         const int grid = (int)(jobs < c->num_sms ? jobs : c->num_sms);
         const size_t smem = (size_t)KG_TC_STAGES * KG_TC_KCS * (128 + KG_TC_N) * 16 + 2 * 512 * (size_t)nb;
         KLAUNCH(c, "k_kg_tc", k_kg_tc<<<grid, KG_TC_THREADS, smem, c->stream>>>(
                                   c->dc, Acan, rowsum, rows, rbs, nb, Mr, Bt, Kp, ntiles, (const ulonglong2*)c->d_kg_off,
-                                  (const ulonglong2*)masks, accq));
+                                  (const ulonglong2*)masks, accq, (int)(8 * WQ / KG_TC_N)));
         release(c, Acan);
         release(c, Bt);
     } else {
@@ -1648,10 +1652,11 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         release(c, C);
     }
     // 5. one ModDown per accumulator (straight into outs when there is no second-Perm)
+    const int Mb = Mr * nbatch;              // accumulators over the batch
     u64 *acc = outs, *rr;
-    if (c_n > 1) RET(scratch(c, &acc, (size_t)Mr * W));
-    RET(scratch(c, &rr, (size_t)Mr * 2 * N));
-    RET(launch_inv<false>(c, accq + (long long)L * N, rr, Mr * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
+    if (c_n > 1) RET(scratch(c, &acc, (size_t)Mb * W));
+    RET(scratch(c, &rr, (size_t)Mb * 2 * N));
+    RET(launch_inv<false>(c, accq + (long long)L * N, rr, Mb * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
     MdArgs a;
     a.r = rr;
@@ -1662,12 +1667,13 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     a.out = acc;
     a.out_is = W;
     a.outs = nullptr;
-    KLAUNCH(c, "k_moddown", k_moddown<<<Mr * 2 * L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, a));
+    KLAUNCH(c, "k_moddown", k_moddown<<<Mb * 2 * L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, a));
     release(c, rr);
     release(c, accq);
     // 6. second-Perm: out[o] = sum_d rot_{d * band}(acc[o][d]), one lazy ModDown per o
     if (c_n > 1) {
-        RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, Mr / c_n, c_n, band_step, outs, 0));
+        RET(rotate_sum_regular(c, acc, W, (long long)Mr * W, nullptr, nbatch, Mr / c_n, c_n, band_step, outs,
+                               (long long)(Mr / c_n) * W));
         release(c, acc);
     }
     return GALA_OK;
@@ -1685,6 +1691,14 @@ int gala_conv_kg2_post(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_
                        int c_n, uint64_t* outs)
 {
     return conv_kg2_run(c, true, cts, n_ib, masks, k, nb, coef, rowsum, Mr, Kp, tap_steps, band_step, c_n, outs);
+}
+
+int gala_conv_kg2_post_batch(gala_ctx* c, const uint64_t* cts, int nbatch, int n_ib, const uint64_t* masks, int k, int nb,
+                             const int8_t* coef, const int32_t* rowsum, int Mr, int Kp, const int* tap_steps,
+                             int band_step, int c_n, uint64_t* outs)
+{
+    if (nbatch <= 0) return set_err(GALA_ERR_DIM, "empty batch");
+    return conv_kg2_run(c, true, cts, n_ib, masks, k, nb, coef, rowsum, Mr, Kp, tap_steps, band_step, c_n, outs, nbatch);
 }
 
 int gala_ct_export(gala_ctx* c, const uint64_t* ct, uint64_t* coef, int count)

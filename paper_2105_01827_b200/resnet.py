@@ -130,6 +130,11 @@ class ConvLayer:
         return out
 
     def forward_device(self, enc_frames):
+        if len(enc_frames) > 1 and self.kg.batchable:   # halo tiles share every launch
+            import torch
+
+            outs = self.kg.forward_device_batch(torch.stack([cts for _, _, cts in enc_frames]))
+            return [(oy, ox, outs[i]) for i, (oy, ox, _) in enumerate(enc_frames)]
         return [(oy, ox, self.kg.forward_device(cts)) for oy, ox, cts in enc_frames]
 
     def decrypt_output(self, outs) -> np.ndarray:

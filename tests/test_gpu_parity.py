@@ -296,3 +296,35 @@ def test_rotate_batch_words(tw):
         want = tw.cpu.rotate_hoisted(c, steps)
         for i in range(len(steps)):
             assert np.array_equal(tw.gpu.export_words(outs[b, i]), want[i])
+
+
+def test_conv_kg2_post_batch_words(tw):
+    """Batched post-mask convolution (several images in one pass) == per-image calls == oracle."""
+    import torch
+
+    from paper_2105_01827_b200.conv import ConvTask, kg2_coefficients, kg2_post_coefficients
+
+    n = tw.bfv.n
+    if n not in KG2_GEOM:
+        pytest.skip("no geometry for this ring")
+    u_w, u_h = KG2_GEOM[n]
+    c_n = n // (u_w * u_h)
+    c_i, c_o, pair, nimg = 2 * c_n, 2 * c_n, 2, 3
+    kern = tw.rng.integers(-128, 128, (c_o, c_i, 3, 3))
+    task = ConvTask(u_w, u_h, c_i, 3, 3, c_o, kern, tw.params)
+    taps = [rot for _, _, rot in task.offsets()]
+    tw.keys_for(taps + [d * u_w * u_h for d in range(1, c_n)])
+    A, _, K = kg2_coefficients(task, c_n, pair)
+    B, rowsum = kg2_post_coefficients(A, K, pair * c_n)
+    masks = tw.gpu.kg2_encode_masks(3, 3, u_w, u_h, pair, band_only=True)
+    dev = tw.gpu.device
+    dB, drs = torch.from_numpy(B).to(dev), torch.from_numpy(rowsum).to(dev)
+    imgs = []
+    for _ in range(nimg):
+        x = tw.rng.integers(0, P, (c_i, u_h, u_w))
+        imgs.append([tw.encrypt(np.concatenate([b, b]).astype(np.uint32)) for b in x.reshape(c_i // c_n, -1)])
+    g_batch = torch.stack([torch.stack([g for g, _ in im]) for im in imgs])
+    outs = tw.gpu.conv_kg2_batch(g_batch, masks, dB, drs, 9, pair * c_n, taps, u_w * u_h, c_n)
+    for i, im in enumerate(imgs):
+        c_out = tw.cpu.conv_kg2(np.stack([c for _, c in im]), kern, u_w, u_h, pair, band_only=True)
+        assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
