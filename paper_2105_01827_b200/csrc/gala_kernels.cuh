@@ -1343,6 +1343,10 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
     constexpr int M = L + 1;
     __shared__ uint64_t full[GTC_NST], empty[GTC_NST], tfull[2], tempty[2], bfull[2], bempty[2];
     __shared__ uint32_t tmem_base_sh;
+    // step-0 weights w[g b][p] of the last 4 positions: copied from the raw stage by the expanders (before
+    // the position's MMA), read by the epilogue (before it releases the accumulator).  Position p + 4's
+    // copy waits on MMA p + 3, which waited on the epilogue of p + 1: the epilogue of p is done.
+    __shared__ u64 s_w0[4][8];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = c.N;
     const long long MN = (long long)M * N, npos = MN;
@@ -1438,6 +1442,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             mbar_wait(&full[s], ph);
             for (int h = 0; h < 2; h++) {
                 mbar_wait(&bempty[h], (uint32_t)((it & 1) ^ 1));
+                if (h == 0 && et < 8) s_w0[it & 3][et] = ((const u64*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES))[512 + et];
                 const ulonglong2* raw = (const ulonglong2*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES) + (4 * h + gl) * 32;
                 uint8_t* rowbase = sBh + h * GTC_BH_BYTES + (n >> 3) * 4096 + (n & 7) * 16;
 #pragma unroll
@@ -1466,16 +1471,17 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             const ModC md = c.mod[j];
             const u64 q = md.q;
             const bool active = (sidx < 2 || (sidx == 2 && j < L)) && bi < B;
-            // step-0 operands issued before the accumulator wait, so their latency hides behind the MMA
+            // step-0 operands: x issued before the accumulator wait (its latency hides behind the MMA), the
+            // weights from the shared ring the expanders filled before this position's MMA
             u64 xc0 = 0, xc1 = 0, w0[4];
             if (sidx == 2 && active) {
                 xc0 = __ldg(X + (long long)bi * W + (long long)j * N + k);
                 xc1 = __ldg(X + (long long)bi * W + (long long)(L + j) * N + k);
-#pragma unroll
-                for (int t = 0; t < 4; t++) w0[t] = __ldg(wT + p * GTC_W_WORDS + 512 + 4 * gh + t);
             }
             mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int t = 0; t < 4; t++) w0[t] = s_w0[it & 3][4 * gh + t];
             uint32_t x[64];
             const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + gh * 64);
             asm volatile(
