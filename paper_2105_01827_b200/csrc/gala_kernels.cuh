@@ -1227,10 +1227,11 @@ __device__ __forceinline__ u64 bswap64(u64 w)
 }
 
 // Per position p, the weights one byte-convolution tile is built from (in shared memory, by k_gala_tc's
-// expander warps): wT[p] = { bswap64(w[g b + jj' + 1][p]) for g < 8, jj' < 64 ;  w[g b][p] for g < 8 }
-// (Montgomery words, 0 outside g < G, jj' + 1 < b): byte-reversed so an 8-byte window of the
-// convolution is one shift, shifted by one rotation so chunk kc's two words are 16-byte aligned,
-// followed by the step-0 weights.  4160 bytes per position.
+// expander warps): wT[p] = { bswap64(w[g b + jj][p]) for g < 8, jj < 64 ;  w[g b][p] for g < 8 }
+// (Montgomery words, 0 outside g < G, jj < b): byte-reversed so an 8-byte window of the convolution is
+// one shift, followed by the step-0 weights again (plain) for the step-0 product of the c1 stream.
+// The jj = 0 column carries the step-0 member of the c0 stream into the MMA (its E rows are zero).
+// 4160 bytes per position.
 #define GTC_W_WORDS (8 * 64 + 8)
 #define GTC_W_BYTES (GTC_W_WORDS * 8)
 __global__ void k_gala_wt(DevCtx c, const u64* __restrict__ pts2, int baby, int G, u64* __restrict__ wT)
@@ -1242,7 +1243,7 @@ __global__ void k_gala_wt(DevCtx c, const u64* __restrict__ pts2, int baby, int 
         const long long p = e / GTC_W_WORDS;
         u64 v = 0;
         if (i < 512) {
-            const int g = i >> 6, jj = (i & 63) + 1;
+            const int g = i >> 6, jj = i & 63;
             if (g < G && jj < baby) v = bswap64(__ldg(pts2 + (long long)(g * baby + jj) * MN + p));
         } else {
             const int g = i - 512;
@@ -1252,7 +1253,8 @@ __global__ void k_gala_wt(DevCtx c, const u64* __restrict__ pts2, int baby, int 
     }
 }
 
-// E_jj, sigma_jj(c0) for every (input, baby rotation), written as Ecan (k_gala_e's math).  grid (N / 32,
+// E_jj, sigma_jj(c0) for every (input, baby rotation jj = 0 .. 63), written as Ecan (k_gala_e's math;
+// E_0 = 0 and sigma_0(c0) = c0 so the step-0 member of the c0 stream rides in the MMA).  grid (N / 32,
 // 32 chunks, M), 256 threads: thread (position kk, 4 inputs) computes the two rotations of chunk kc.
 template <int L>
 __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restrict__ Dblk, const u64* const* __restrict__ keys,
@@ -1268,10 +1270,10 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
     const long long NN = N, MN = (long long)M * N, bw = (long long)(L * M + L) * N;
 #pragma unroll
     for (int jw = 0; jw < 2; jw++) {
-        const int jj = 2 * kc + jw + 1;
-        const bool valid = jj < baby;
+        const int jj = 2 * kc + jw;               // jj = 0: E = 0 (no key switch), sigma_0(c0) = c0
+        const bool valid = jj >= 1 && jj < baby;
         u64 ka[L], kb[L];
-        int src = 0;
+        int src = k;
         if (valid) {
             const u64* key = keys[jj];
             src = auto_src(k, gal[jj], logN);
@@ -1285,6 +1287,7 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
         for (int q = 0; q < 4; q++) {
             const int bi = bg * 4 + q;
             u64 e0 = 0, e1 = 0, r0 = 0;
+            if (jj == 0 && bi < B && j < L) r0 = __ldg(Dblk + (long long)bi * bw + ((long long)L * M + j) * NN + k);
             if (valid && bi < B) {
                 const u64* D = Dblk + (long long)bi * bw;
                 Acc128 s0, s1;
@@ -1448,7 +1451,7 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
 #pragma unroll
                 for (int i = 0; i < 8; i++) {
                     const int kc = kq * 8 + i;
-                    const ulonglong2 r = raw[kc];   // rotations jj = 2 kc + 1, 2 kc + 2 (byte-reversed)
+                    const ulonglong2 r = raw[kc];   // rotations jj = 2 kc, 2 kc + 1 (byte-reversed)
                     const u64 t0 = ((r.x >> sh_r) << sh_l) & keep, t1 = ((r.y >> sh_r) << sh_l) & keep;
                     *(ulonglong2*)(rowbase + kc * 128) = make_ulonglong2(t0, t1);
                 }
@@ -1470,14 +1473,11 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             const int j = (int)(p / N), k = (int)(p - (long long)j * N);
             const ModC md = c.mod[j];
             const u64 q = md.q;
-            const bool active = (sidx < 2 || (sidx == 2 && j < L)) && bi < B;
-            // step-0 operands: x issued before the accumulator wait (its latency hides behind the MMA), the
-            // weights from the shared ring the expanders filled before this position's MMA
-            u64 xc0 = 0, xc1 = 0, w0[4];
-            if (sidx == 2 && active) {
-                xc0 = __ldg(X + (long long)bi * W + (long long)j * N + k);
-                xc1 = __ldg(X + (long long)bi * W + (long long)(L + j) * N + k);
-            }
+            const bool active = (sidx < 2 || j < L) && bi < B;
+            // lane groups 0..2: the MMA rows (U c0, U c1, Cacc c0 incl. its step-0 member); lane group 3
+            // (no MMA rows): the step-0 product of the c1 stream, x.c1 (.) w[g b], on the CUDA cores
+            u64 xc1 = 0, w0[4];
+            if (sidx == 3 && active) xc1 = __ldg(X + (long long)bi * W + (long long)(L + j) * N + k);
             mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
@@ -1502,7 +1502,13 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);   // this warp's accumulator columns are in registers
-            if (active) {
+            if (active && sidx == 3) {
+#pragma unroll
+                for (int t = 0; t < 4; t++) {
+                    const int g = 4 * gh + t;
+                    if (g < G) Cacc[((((long long)bi * G + g) * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, w0[t], md);
+                }
+            } else if (active) {
 #pragma unroll
                 for (int t = 0; t < 4; t++) {
                     const int g = 4 * gh + t;
@@ -1523,12 +1529,8 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                     if (hi >= q) hi -= q;
                     const u64 v = csub(redc_lazy(hi, lo, md), q);   // sum_jj X w   (w Montgomery)
                     const long long z = (long long)bi * G + g;
-                    if (sidx < 2) {
-                        U[((z * 2 + sidx) * M + j) * (long long)N + k] = v;
-                    } else {
-                        Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = add_mod(v, mont_mul(xc0, w0[t], md), q);
-                        Cacc[((z * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, w0[t], md);
-                    }
+                    if (sidx < 2) U[((z * 2 + sidx) * M + j) * (long long)N + k] = v;
+                    else Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = v;
                 }
             }
         }
