@@ -91,6 +91,79 @@ struct Acc128 {
     __device__ __forceinline__ u64 reduce(const ModC& m) const { return csub(redc_lazy(hi, lo, m), m.q); }
 };
 
+// REDC for the special-form primes q = a 2^32 + 1 (every ciphertext and special prime; gala_create
+// checks): -q^-1 = a 2^32 - 1 mod 2^64, so m = lo (-q^-1) is one 32-bit multiply, and hi64(m q) =
+// m1 a + ((m0 a + m1) >> 32) is two 32x32 wide products.  Same result as redc_lazy, in [0, 2q).
+__device__ __forceinline__ u64 redc_sf_lazy(u64 hi, u64 lo, u64 q)
+{
+    const uint32_t a = (uint32_t)(q >> 32);
+    const u64 mm = ((u64)((uint32_t)lo * a) << 32) - lo;
+    const uint32_t m0 = (uint32_t)mm, m1 = (uint32_t)(mm >> 32);
+    const u64 t = (u64)m1 * a + (((u64)m0 * a + m1) >> 32);
+    return hi + t + (lo != 0ull ? 1ull : 0ull);
+}
+
+// 128-bit sum of products of canonical residues built from 32x32 -> 64 partial products, each
+// accumulated in its own register by one IMAD.WIDE.U32 (the a0 b0 partials through a carry chain).
+// Bound: the cross sums stay below 2^64 for up to 4 terms of residues < 2^60 (or 1 term < 2^62).
+// set() starts the sum with its first product (no adds of zero).
+struct AccPP {
+    u64 s00, s01, s11;
+    uint32_t c00;
+    __device__ __forceinline__ void set(u64 a, u64 b)
+    {
+        const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+        s00 = (u64)a0 * b0;
+        c00 = 0;
+        s01 = (u64)a0 * b1;
+        s01 += (u64)a1 * b0;
+        s11 = (u64)a1 * b1;
+    }
+    __device__ __forceinline__ void mac(u64 a, u64 b)
+    {
+        const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+        asm("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %2, %3;\n\tadd.cc.u64 %0, %0, t;\n\taddc.u32 %1, %1, 0;\n\t}"
+            : "+l"(s00), "+r"(c00)
+            : "r"(a0), "r"(b0));
+        s01 += (u64)a0 * b1;
+        s01 += (u64)a1 * b0;
+        s11 += (u64)a1 * b1;
+    }
+    // (sum) 2^-64 mod q, canonical, for a special-form q = a 2^32 + 1 (see redc_sf_lazy)
+    __device__ __forceinline__ u64 reduce_sf(u64 q) const
+    {
+        uint32_t r0, r1;
+        asm("{\n\t.reg .u32 lo0, lo1, h0, h1, t, m0, m1, th, u0, u1, nz, a;\n\t.reg .pred p;\n\t"
+            "mov.b64 {lo0, t}, %2;\n\t"
+            "mov.b64 {u0, u1}, %3;\n\t"
+            "add.cc.u32 lo1, t, u0;\n\t"            // lo = s00 + (s01 << 32)
+            "mov.b64 {h0, h1}, %4;\n\t"
+            "addc.cc.u32 h0, h0, u1;\n\t"           // hi = s11 + (s01 >> 32) + carry + c00
+            "addc.u32 h1, h1, 0;\n\t"
+            "add.cc.u32 h0, h0, %5;\n\t"
+            "addc.u32 h1, h1, 0;\n\t"
+            "mov.b64 {t, a}, %6;\n\t"               // a = q >> 32
+            "mul.lo.u32 t, lo0, a;\n\t"             // m = lo (a 2^32 - 1) mod 2^64
+            "sub.cc.u32 m0, 0, lo0;\n\t"
+            "subc.u32 m1, t, lo1;\n\t"
+            "mad.lo.cc.u32 t, m0, a, m1;\n\t"       // th = (m0 a + m1) >> 32
+            "madc.hi.u32 th, m0, a, 0;\n\t"
+            "mad.lo.cc.u32 u0, m1, a, th;\n\t"      // hi64(m q) = m1 a + th
+            "madc.hi.u32 u1, m1, a, 0;\n\t"
+            "or.b32 t, lo0, lo1;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "selp.u32 nz, 1, 0, p;\n\t"
+            "add.cc.u32 h0, h0, u0;\n\t"
+            "addc.u32 h1, h1, u1;\n\t"
+            "add.cc.u32 %0, h0, nz;\n\t"
+            "addc.u32 %1, h1, 0;\n\t"
+            "}"
+            : "=r"(r0), "=r"(r1)
+            : "l"(s00), "l"(s01), "l"(s11), "r"(c00), "l"(q));
+        return csub(((u64)r1 << 32) | r0, q);
+    }
+};
+
 // streaming (evict-first) global accesses for polynomial data, so the twiddle
 // tables keep their L1 residency
 __device__ __forceinline__ u64 ld_cs(const u64* p) { return (u64)__ldcs((const unsigned long long*)p); }

@@ -1283,23 +1283,30 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
                 kb[i] = __ldg(key + (((long long)i * 2 + 1) * M + j) * NN + k);
             }
         }
+        // pointer walk (64-bit adds) instead of per-load index products
+        const u64* Dq = Dblk + (long long)(bg * 4) * bw + (long long)j * NN + src;
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < 4; q++, Dq += bw) {
             const int bi = bg * 4 + q;
             u64 e0 = 0, e1 = 0, r0 = 0;
-            if (jj == 0 && bi < B && j < L) r0 = __ldg(Dblk + (long long)bi * bw + ((long long)L * M + j) * NN + k);
+            if (jj == 0 && bi < B && j < L) r0 = __ldg(Dq + (long long)L * MN);
             if (valid && bi < B) {
-                const u64* D = Dblk + (long long)bi * bw;
-                Acc128 s0, s1;
+                AccPP s0, s1;
+                const u64* Di = Dq;
 #pragma unroll
-                for (int i = 0; i < L; i++) {
-                    const u64 d = __ldg(D + ((long long)i * M + j) * NN + src);
-                    s0.mac(d, ka[i]);
-                    s1.mac(d, kb[i]);
+                for (int i = 0; i < L; i++, Di += MN) {
+                    const u64 d = __ldg(Di);
+                    if (i == 0) {
+                        s0.set(d, ka[i]);
+                        s1.set(d, kb[i]);
+                    } else {
+                        s0.mac(d, ka[i]);
+                        s1.mac(d, kb[i]);
+                    }
                 }
-                e0 = s0.reduce(md);
-                e1 = s1.reduce(md);
-                if (j < L) r0 = __ldg(D + ((long long)L * M + j) * NN + src);
+                e0 = s0.reduce_sf(md.q);
+                e1 = s1.reduce_sf(md.q);
+                if (j < L) r0 = __ldg(Di);
             }
             // row r of position kk lives at (r + kk) % 96: the 32 positions of a warp hit distinct banks
             const int r2 = 64 + bi + kk;
