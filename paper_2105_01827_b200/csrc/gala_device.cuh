@@ -68,13 +68,38 @@ __device__ __forceinline__ u64 shoup_lz(u64 x, u64 w, u64 wsh, u64 q)
     return shoup_lazy(x, w, wsh, q);
 }
 
-// Montgomery REDC of hi:lo < q 2^64: returns (hi:lo) 2^-64 mod q in [0, 2q)
-__device__ __forceinline__ u64 redc_lazy(u64 hi, u64 lo, const ModC& m)
+// Montgomery REDC of hi:lo < q 2^64 for a special-form q = a 2^32 + 1 (every prime REDC sees;
+// gala_create rejects others): returns (hi:lo) 2^-64 mod q in [0, 2q).  -q^-1 = a 2^32 - 1 mod 2^64,
+// so m = lo (-q^-1) is one 32-bit multiply, and hi64(m q) = m1 a + ((m0 a + m1) >> 32) is two
+// 32x32 wide products; the carry of lo + lo64(m q) is (lo != 0).
+__device__ __forceinline__ u64 redc_sf_lazy(u64 hi, u64 lo, u64 q)
 {
-    u64 mm = lo * m.qinv_neg;
-    u64 t = __umul64hi(mm, m.q);
-    return hi + t + (lo != 0ull ? 1ull : 0ull);
+    u64 r;
+    asm("{\n\t.reg .u32 lo0, lo1, h0, h1, t, m0, m1, th, u0, u1, nz, a;\n\t.reg .pred p;\n\t"
+        "mov.b64 {lo0, lo1}, %1;\n\t"
+        "mov.b64 {h0, h1}, %2;\n\t"
+        "mov.b64 {t, a}, %3;\n\t"
+        "mul.lo.u32 t, lo0, a;\n\t"
+        "sub.cc.u32 m0, 0, lo0;\n\t"
+        "subc.u32 m1, t, lo1;\n\t"
+        "mad.lo.cc.u32 t, m0, a, m1;\n\t"
+        "madc.hi.u32 th, m0, a, 0;\n\t"
+        "mad.lo.cc.u32 u0, m1, a, th;\n\t"
+        "madc.hi.u32 u1, m1, a, 0;\n\t"
+        "or.b32 t, lo0, lo1;\n\t"
+        "setp.ne.u32 p, t, 0;\n\t"
+        "selp.u32 nz, 1, 0, p;\n\t"
+        "add.cc.u32 h0, h0, u0;\n\t"
+        "addc.u32 h1, h1, u1;\n\t"
+        "add.cc.u32 h0, h0, nz;\n\t"
+        "addc.u32 h1, h1, 0;\n\t"
+        "mov.b64 %0, {h0, h1};\n\t"
+        "}"
+        : "=l"(r)
+        : "l"(lo), "l"(hi), "l"(q));
+    return r;
 }
+__device__ __forceinline__ u64 redc_lazy(u64 hi, u64 lo, const ModC& m) { return redc_sf_lazy(hi, lo, m.q); }
 __device__ __forceinline__ u64 mont_mul(u64 a, u64 b, const ModC& m)
 {
     return csub(redc_lazy(__umul64hi(a, b), a * b, m), m.q);
@@ -91,32 +116,26 @@ struct Acc128 {
     __device__ __forceinline__ u64 reduce(const ModC& m) const { return csub(redc_lazy(hi, lo, m), m.q); }
 };
 
-// REDC for the special-form primes q = a 2^32 + 1 (every ciphertext and special prime; gala_create
-// checks): -q^-1 = a 2^32 - 1 mod 2^64, so m = lo (-q^-1) is one 32-bit multiply, and hi64(m q) =
-// m1 a + ((m0 a + m1) >> 32) is two 32x32 wide products.  Same result as redc_lazy, in [0, 2q).
-__device__ __forceinline__ u64 redc_sf_lazy(u64 hi, u64 lo, u64 q)
-{
-    const uint32_t a = (uint32_t)(q >> 32);
-    const u64 mm = ((u64)((uint32_t)lo * a) << 32) - lo;
-    const uint32_t m0 = (uint32_t)mm, m1 = (uint32_t)(mm >> 32);
-    const u64 t = (u64)m1 * a + (((u64)m0 * a + m1) >> 32);
-    return hi + t + (lo != 0ull ? 1ull : 0ull);
-}
-
-// 128-bit sum of products of canonical residues built from 32x32 -> 64 partial products, each
-// accumulated in its own register by one IMAD.WIDE.U32 (the a0 b0 partials through a carry chain).
-// Bound: the cross sums stay below 2^64 for up to 4 terms of residues < 2^60 (or 1 term < 2^62).
-// set() starts the sum with its first product (no adds of zero).
+// 128-bit sum of products built from 32x32 -> 64 partial products, each accumulated in its own
+// register by one IMAD.WIDE.U32 (the a0 b0 partials through a carry chain).  Valid wherever Acc128
+// is: for k products of operands below A, B (both >= q) with k A B < q 2^64, the cross sums stay
+// below k B < 2^64 and k A < 2^64.  set() starts the sum with its first product.  MERGE keeps the
+// two cross sums in one register: only for 2 k max(A, B) < 2^64 (e.g. up to 4 canonical products
+// with q < 2^60, or 1 with q < 2^62).
+template <bool MERGE = false>
 struct AccPP {
-    u64 s00, s01, s11;
+    u64 s00, s01, s10, s11;
     uint32_t c00;
+    __device__ __forceinline__ AccPP() {}
+    __device__ __forceinline__ void clear() { s00 = s01 = s10 = s11 = 0; c00 = 0; }
     __device__ __forceinline__ void set(u64 a, u64 b)
     {
         const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
         s00 = (u64)a0 * b0;
         c00 = 0;
         s01 = (u64)a0 * b1;
-        s01 += (u64)a1 * b0;
+        if (MERGE) s01 += (u64)a1 * b0;
+        else s10 = (u64)a1 * b0;
         s11 = (u64)a1 * b1;
     }
     __device__ __forceinline__ void mac(u64 a, u64 b)
@@ -126,41 +145,54 @@ struct AccPP {
             : "+l"(s00), "+r"(c00)
             : "r"(a0), "r"(b0));
         s01 += (u64)a0 * b1;
-        s01 += (u64)a1 * b0;
+        if (MERGE) s01 += (u64)a1 * b0;
+        else s10 += (u64)a1 * b0;
         s11 += (u64)a1 * b1;
     }
-    // (sum) 2^-64 mod q, canonical, for a special-form q = a 2^32 + 1 (see redc_sf_lazy)
+    // the 128-bit sum as hi:lo
+    __device__ __forceinline__ void value(u64& hi, u64& lo) const
+    {
+        if (MERGE) {
+            asm("{\n\t.reg .u32 x0, x1, l0, l1, h0, h1;\n\t"
+                "mov.b64 {x0, x1}, %3;\n\t"
+                "mov.b64 {l0, l1}, %2;\n\t"
+                "mov.b64 {h0, h1}, %4;\n\t"
+                "add.cc.u32 l1, l1, x0;\n\t"
+                "addc.cc.u32 h0, h0, x1;\n\t"
+                "addc.u32 h1, h1, 0;\n\t"
+                "add.cc.u32 h0, h0, %5;\n\t"
+                "addc.u32 h1, h1, 0;\n\t"
+                "mov.b64 %0, {h0, h1};\n\t"
+                "mov.b64 %1, {l0, l1};\n\t"
+                "}"
+                : "=l"(hi), "=l"(lo)
+                : "l"(s00), "l"(s01), "l"(s11), "r"(c00));
+            return;
+        }
+        asm("{\n\t.reg .u32 x0, x1, y0, y1, m0, m1, m2, l0, l1, h0, h1;\n\t"
+            "mov.b64 {x0, x1}, %3;\n\t"
+            "mov.b64 {y0, y1}, %4;\n\t"
+            "add.cc.u32 m0, x0, y0;\n\t"            // mid = s01 + s10 (65 bits)
+            "addc.cc.u32 m1, x1, y1;\n\t"
+            "addc.u32 m2, 0, 0;\n\t"
+            "mov.b64 {l0, l1}, %2;\n\t"
+            "mov.b64 {h0, h1}, %5;\n\t"
+            "add.cc.u32 l1, l1, m0;\n\t"            // lo = s00 + (mid << 32)
+            "addc.cc.u32 h0, h0, m1;\n\t"           // hi = s11 + (mid >> 32) + carries + c00
+            "addc.u32 h1, h1, m2;\n\t"
+            "add.cc.u32 h0, h0, %6;\n\t"
+            "addc.u32 h1, h1, 0;\n\t"
+            "mov.b64 %0, {h0, h1};\n\t"
+            "mov.b64 %1, {l0, l1};\n\t"
+            "}"
+            : "=l"(hi), "=l"(lo)
+            : "l"(s00), "l"(s01), "l"(s10), "l"(s11), "r"(c00));
+    }
     __device__ __forceinline__ u64 reduce_sf(u64 q) const
     {
-        uint32_t r0, r1;
-        asm("{\n\t.reg .u32 lo0, lo1, h0, h1, t, m0, m1, th, u0, u1, nz, a;\n\t.reg .pred p;\n\t"
-            "mov.b64 {lo0, t}, %2;\n\t"
-            "mov.b64 {u0, u1}, %3;\n\t"
-            "add.cc.u32 lo1, t, u0;\n\t"            // lo = s00 + (s01 << 32)
-            "mov.b64 {h0, h1}, %4;\n\t"
-            "addc.cc.u32 h0, h0, u1;\n\t"           // hi = s11 + (s01 >> 32) + carry + c00
-            "addc.u32 h1, h1, 0;\n\t"
-            "add.cc.u32 h0, h0, %5;\n\t"
-            "addc.u32 h1, h1, 0;\n\t"
-            "mov.b64 {t, a}, %6;\n\t"               // a = q >> 32
-            "mul.lo.u32 t, lo0, a;\n\t"             // m = lo (a 2^32 - 1) mod 2^64
-            "sub.cc.u32 m0, 0, lo0;\n\t"
-            "subc.u32 m1, t, lo1;\n\t"
-            "mad.lo.cc.u32 t, m0, a, m1;\n\t"       // th = (m0 a + m1) >> 32
-            "madc.hi.u32 th, m0, a, 0;\n\t"
-            "mad.lo.cc.u32 u0, m1, a, th;\n\t"      // hi64(m q) = m1 a + th
-            "madc.hi.u32 u1, m1, a, 0;\n\t"
-            "or.b32 t, lo0, lo1;\n\t"
-            "setp.ne.u32 p, t, 0;\n\t"
-            "selp.u32 nz, 1, 0, p;\n\t"
-            "add.cc.u32 h0, h0, u0;\n\t"
-            "addc.u32 h1, h1, u1;\n\t"
-            "add.cc.u32 %0, h0, nz;\n\t"
-            "addc.u32 %1, h1, 0;\n\t"
-            "}"
-            : "=r"(r0), "=r"(r1)
-            : "l"(s00), "l"(s01), "l"(s11), "r"(c00), "l"(q));
-        return csub(((u64)r1 << 32) | r0, q);
+        u64 hi, lo;
+        value(hi, lo);
+        return csub(redc_sf_lazy(hi, lo, q), q);
     }
 };
 

@@ -282,7 +282,9 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
             a1 = add_mod(a1, x1, q);
         }
     }
-    Acc128 s0, s1;
+    AccPP<> s0, s1;
+    s0.clear();
+    s1.clear();
     int pending = 0;
     constexpr int LMAX = L;
     u64 dv[LMAX], kb[LMAX], ka[LMAX], cv = 0;
@@ -304,10 +306,10 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
         for (int i = 0; i < LMAX; i++) { d[i] = dv[i]; b[i] = kb[i]; a[i] = ka[i]; }
         if (it + 1 < hi) fetch(mem[it + 1]);      // prefetch the next member
         if (pending + L > lazy) {
-            u0 = add_mod(u0, s0.reduce(md), q);
-            u1 = add_mod(u1, s1.reduce(md), q);
-            s0 = Acc128();
-            s1 = Acc128();
+            u0 = add_mod(u0, s0.reduce_sf(q), q);
+            u1 = add_mod(u1, s1.reduce_sf(q), q);
+            s0.clear();
+            s1.clear();
             pending = 0;
         }
 #pragma unroll
@@ -320,8 +322,8 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
         pending += L;
         if (j < L) a0 = add_mod(a0, cc, q);
     }
-    u0 = add_mod(u0, s0.reduce(md), q);
-    u1 = add_mod(u1, s1.reduce(md), q);
+    u0 = add_mod(u0, s0.reduce_sf(q), q);
+    u1 = add_mod(u1, s1.reduce_sf(q), q);
     U[(((long long)g * 2 + 0) * M + j) * NN + k] = u0;
     U[(((long long)g * 2 + 1) * M + j) * NN + k] = u1;
     if (j < L) {
@@ -787,10 +789,13 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
                     const int src = auto_src(i, gal[tt], logN);
                     const u64* D = Dj + (long long)ib * bw + src;
                     const u64* kp = key + koff;
-                    Acc128 s;
+                    AccPP<true> s;   // L <= 4 canonical products
 #pragma unroll
-                    for (int l = 0; l < L; l++) s.mac(__ldg(D + l * MN), __ldg(kp + l * 2 * MN));
-                    z = s.reduce(md);
+                    for (int l = 0; l < L; l++) {
+                        if (l == 0) s.set(__ldg(D), __ldg(kp));
+                        else s.mac(__ldg(D + l * MN), __ldg(kp + l * 2 * MN));
+                    }
+                    z = s.reduce_sf(q);
                     if (comp == 0 && j < L)
                         z = add_mod(z, csub(shoup_lazy_sf(__ldg(D + L * MN), pc.x, pc.y, q), q), q);
                 }
@@ -1291,7 +1296,7 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
             u64 e0 = 0, e1 = 0, r0 = 0;
             if (jj == 0 && bi < B && j < L) r0 = __ldg(Dq + (long long)L * MN);
             if (valid && bi < B) {
-                AccPP s0, s1;
+                AccPP<true> s0, s1;   // L <= 4 canonical products per sum: merged cross sums fit
                 const u64* Di = Dq;
 #pragma unroll
                 for (int i = 0; i < L; i++, Di += MN) {
