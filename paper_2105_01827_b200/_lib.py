@@ -13,7 +13,7 @@ import os
 from .errors import DimensionError, GalaError, ParameterError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libgala_b200.so")
+LIB_PATH = os.environ.get("GALA_LIB_PATH") or os.path.join(_HERE, "_lib", "libgala_b200.so")   # override: experiments
 
 GALA_OK = 0
 GALA_ERR_PARAM = -1

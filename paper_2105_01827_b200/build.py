@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, SRC, *LINK]
+    extra = os.environ.get("GALA_NVCC_EXTRA", "").split()   # experiments only (e.g. -DGTC_PROF)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", OUT, SRC, *LINK]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)

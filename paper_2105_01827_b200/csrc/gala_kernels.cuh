@@ -1336,18 +1336,34 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
 //   warps 10..13   expanders: build the position's byte-convolution B tile in two halves (groups
 //                  0-3, 4-7; 32 KB each, double-buffered) from the raw weights (byte reversal +
 //                  shift per 8-byte window), fence the generic -> async proxy, arrive bfull[h];
-//   warp 1 lane 0  MMA: per half 16 tcgen05.mma.kind::i8 (M 128, N 64, K 32, unsigned bytes) into
-//                  columns 64 h of one of two TMEM accumulators (the next half's expansion overlaps);
-//                  commits bempty[h], then empty[s] and tfull[acc];
+//   warp 1 lane 0  MMA: once both halves are built, 16 tcgen05.mma.kind::i8 (M 128, N 128, K 32,
+//                  unsigned bytes) into one of two TMEM accumulators (N 128 reads the A tile from
+//                  shared memory once per position, not once per half); commits bempty[0..1], then
+//                  empty[s] and tfull[acc];
 //   warps 2..9     epilogue (TMEM lane group s = warp % 4 -> stream s, lane = input; groups 4 gh ..
 //                  4 gh + 3 with gh = (warp - 2) / 4, one 64-column TMEM load per position): rebuild
 //                  each (input, stream, group) sum from its 15 byte-shifted columns, reduce once mod
 //                  q, write U / Cacc (plus the step-0 member for stream 2).
 #define GTC_THREADS 576
-#define GTC_NST 3
-#define GTC_STAGE (GTC_A_BYTES + GTC_W_BYTES)
-#define GTC_BH_BYTES (8 * 4096)
-#define GTC_SMEM (GTC_NST * GTC_STAGE + 2 * GTC_BH_BYTES)
+#define GTC_NST 2
+#define GTC_STAGE GTC_A_BYTES
+#define GTC_BB_BYTES (16 * 4096)   // 128 B rows (8 groups x 16 shifts; shift 15 is never read)
+// + 512 B: the M 128 A read of the last stage runs past its 96 rows (rows 96..127 are don't-care)
+#define GTC_SMEM (2 * GTC_BB_BYTES + GTC_NST * GTC_STAGE + 512)
+#ifdef GTC_PROF
+__device__ unsigned long long g_gtc_prof[1024][16];
+#define GP_DECL long long gp_[16] = {0}; const long long gp_t0 = clock64();
+#define GP_WAIT(slot, stmt) { const long long t_ = clock64(); stmt; gp_[slot] += clock64() - t_; }
+#define GP_MARK(v) const long long v = clock64();
+#define GP_ADD(slot, v) gp_[slot] += clock64() - v;
+#define GP_FLUSH(first) if (lane == 0) { for (int i_ = 0; i_ < 16; i_++) if (gp_[i_] && i_ != 10 && i_ != 11) g_gtc_prof[blockIdx.x][i_] = gp_[i_]; if (first) { g_gtc_prof[blockIdx.x][10] = clock64() - gp_t0; g_gtc_prof[blockIdx.x][11] = p1 - p0; } }
+#else
+#define GP_DECL
+#define GP_WAIT(slot, stmt) stmt;
+#define GP_MARK(v)
+#define GP_ADD(slot, v)
+#define GP_FLUSH(first)
+#endif
 template <int L>
 __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint8_t* __restrict__ Ecan,
                                                           const u64* __restrict__ wT, const u64* __restrict__ X,
@@ -1365,9 +1381,12 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int N = c.N;
     const long long MN = (long long)M * N, npos = MN;
-    const long long per = (npos + gridDim.x - 1) / gridDim.x;
+    // whole blocks of 4 positions per CTA: the epilogue writes 4 consecutive words (one sector) per output
+    const long long per = ((npos + gridDim.x - 1) / gridDim.x + 3) & ~3LL;
     const long long p0 = blockIdx.x * per, p1 = p0 + per < npos ? p0 + per : npos;
-    uint8_t* sBh = gtc_sm + GTC_NST * GTC_STAGE;   // [2][32 KB]
+    // [B buffer 0][B buffer 1][A stages]
+    uint8_t* sB = gtc_sm;
+    uint8_t* sSt = gtc_sm + 2 * GTC_BB_BYTES;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -1389,17 +1408,17 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base_sh;
+    GP_DECL
     if (warp == 0) {
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
             for (long long p = p0; p < p1; p++) {
-                mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* st = gtc_sm + s * GTC_STAGE;
+                GP_WAIT(0, mbar_wait(&empty[s], ph ^ 1));
+                uint8_t* st = sSt + s * GTC_STAGE;
                 mbar_expect_tx(&full[s], (uint32_t)GTC_STAGE);
                 for (int kc = 0; kc < 32; kc++)
                     bulk_g2s(st + kc * 1536, Ecan + ((long long)kc * npos + p) * 1536, 1536, &full[s]);
-                bulk_g2s(st + GTC_A_BYTES, wT + p * GTC_W_WORDS, GTC_W_BYTES, &full[s]);
                 if (++s == GTC_NST) {
                     s = 0;
                     ph ^= 1;
@@ -1408,32 +1427,31 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t idesc = (2u << 4) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            // M 128, N 128 (both B halves: 8 groups x 16 shifts), s32 accumulate, unsigned bytes
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
             for (long long p = p0; p < p1; p++, it++) {
                 const int acc = it & 1;
-                mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
-                mbar_wait(&full[s], ph);
-                const uint32_t sa = smem_u32(gtc_sm + s * GTC_STAGE);
-                for (int h = 0; h < 2; h++) {
-                    mbar_wait(&bfull[h], (uint32_t)(it & 1));
-                    asm volatile("tcgen05.fence::after_thread_sync;");
-                    const uint32_t sb = smem_u32(sBh + h * GTC_BH_BYTES);
-                    const uint32_t d = tmem + (uint32_t)(acc * 128 + h * 64);
+                GP_WAIT(1, mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1)));
+                GP_WAIT(2, mbar_wait(&full[s], ph));
+                const uint32_t sa = smem_u32(sSt + s * GTC_STAGE);
+                GP_WAIT(3, mbar_wait(&bfull[acc], (uint32_t)((it >> 1) & 1)));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sb = smem_u32(sB + acc * GTC_BB_BYTES);
+                const uint32_t d = tmem + (uint32_t)(acc * 128);
 #pragma unroll 1
-                    for (int ks = 0; ks < 16; ks++) {
-                        const uint64_t ad = umma_desc_kmajor(sa + ks * 2 * 1536, 1536, 128);
-                        const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
-                        asm volatile(
-                            "{\n\t.reg .pred p;\n\t"
-                            "setp.ne.b32 p, %4, 0;\n\t"
-                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                            ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
-                    }
-                    umma_commit(&bempty[h]);
+                for (int ks = 0; ks < 16; ks++) {
+                    const uint64_t ad = umma_desc_kmajor(sa + ks * 2 * 1536, 1536, 128);
+                    const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\t"
+                        "setp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                        ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
                 }
+                umma_commit(&bempty[acc]);
                 umma_commit(&empty[s]);
                 umma_commit(&tfull[acc]);
                 if (++s == GTC_NST) {
@@ -1442,111 +1460,142 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 }
             }
         }
-    } else if (warp >= 10) {   // 8 expander warps: thread -> B row n (of 64 in the half) x 8 K chunks
+    } else if (warp >= 10) {   // 8 expander warps: thread -> B row n = 16 g + s' x one K half
         const int et = tid - 10 * 32;
-        const int n = et & 63, kq = et >> 6;
-        const int gl = n >> 4, sp = n & 15;
-        // byte-reversed word r: window for shift s' is (r >> 8 (7 - s')) for s' <= 7, (r << 8 (s' - 7)) above;
-        // s' = 15 is all zero
-        const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? (sp == 15 ? 0 : 8 * (sp - 7)) : 0;
-        const u64 keep = sp == 15 ? 0ull : ~0ull;
-        int s = 0;
-        uint32_t ph = 0;
+        const int n = et >> 1, kh = et & 1;
+        const int g = n >> 4, sp = n & 15;
+        const bool act = sp < 15;                 // row s' = 15 (column never read) is left as is
+        // byte-reversed word r: window for shift s' is (r >> 8 (7 - s')) for s' <= 7, (r << 8 (s' - 7)) above
+        const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? 8 * (sp - 7) : 0;
+        // the raw weights come from global memory straight into registers, one position ahead: the
+        // expansion waits only for its B buffer, not for the position's A tile
+        ulonglong2 r[16];
+        u64 w0n = 0;
+        auto load_raw = [&](long long pp) {
+            if (pp >= p1) return;
+            const ulonglong2* src = (const ulonglong2*)(wT + pp * GTC_W_WORDS) + g * 32 + kh * 16;
+            if (act) {
+#pragma unroll
+                for (int i = 0; i < 16; i++) r[i] = __ldg(src + i);
+            }
+            if (et < 8) w0n = __ldg(wT + pp * GTC_W_WORDS + 512 + et);
+        };
+        load_raw(p0);
         int it = 0;
         for (long long p = p0; p < p1; p++, it++) {
-            mbar_wait(&full[s], ph);
-            for (int h = 0; h < 2; h++) {
-                mbar_wait(&bempty[h], (uint32_t)((it & 1) ^ 1));
-                if (h == 0 && et < 8) s_w0[it & 3][et] = ((const u64*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES))[512 + et];
-                const ulonglong2* raw = (const ulonglong2*)(gtc_sm + s * GTC_STAGE + GTC_A_BYTES) + (4 * h + gl) * 32;
-                uint8_t* rowbase = sBh + h * GTC_BH_BYTES + (n >> 3) * 4096 + (n & 7) * 16;
+            const int b = it & 1;
+            GP_WAIT(6, mbar_wait(&bempty[b], (uint32_t)(((it >> 1) & 1) ^ 1)));
+            GP_MARK(ex0)
+            if (et < 8) s_w0[it & 3][et] = w0n;
+            if (act) {
+                uint8_t* rowbase = sB + b * GTC_BB_BYTES + (n >> 3) * 4096 + (n & 7) * 16 + kh * 16 * 128;
 #pragma unroll
-                for (int i = 0; i < 8; i++) {
-                    const int kc = kq * 8 + i;
-                    const ulonglong2 r = raw[kc];   // rotations jj = 2 kc, 2 kc + 1 (byte-reversed)
-                    const u64 t0 = ((r.x >> sh_r) << sh_l) & keep, t1 = ((r.y >> sh_r) << sh_l) & keep;
-                    *(ulonglong2*)(rowbase + kc * 128) = make_ulonglong2(t0, t1);
-                }
-                asm volatile("fence.proxy.async.shared::cta;");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bfull[h]);
+                for (int i = 0; i < 16; i++)   // rotations jj = 2 kc, 2 kc + 1 (byte-reversed), kc = 16 kh + i
+                    *(ulonglong2*)(rowbase + i * 128) = make_ulonglong2((r[i].x >> sh_r) << sh_l, (r[i].y >> sh_r) << sh_l);
             }
-            if (++s == GTC_NST) {
-                s = 0;
-                ph ^= 1;
-            }
+            load_raw(p + 1);
+            asm volatile("fence.proxy.async.shared::cta;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bfull[b]);
+            GP_ADD(7, ex0)
         }
     } else {   // epilogue: TMEM lane group lg = warp % 4 holds rows 32 lg .. (stream s = lg, input = lane)
         const int lg = warp & 3, sidx = lg, bi = lane, gh = (warp - 2) >> 2;
         const long long W = 2LL * L * N;
-        int it = 0;
-        for (long long p = p0; p < p1; p++, it++) {
-            const int acc = it & 1;
-            const int j = (int)(p / N), k = (int)(p - (long long)j * N);
-            const ModC md = c.mod[j];
+        const long long gstride = sidx < 2 ? 2LL * M * N : 2LL * L * N;   // words between groups g, g + 1
+        // sum_s' 256^s' D_s' of one group's 15 columns (exact, < 2^126) reduced mod q: three 40-bit-spaced
+        // partial sums below 2^58, folded, one REDC (w Montgomery: the result is sum_jj X w mod q)
+        auto rebuild = [&](const uint32_t* xg, const ModC& md) -> u64 {
             const u64 q = md.q;
+            u64 lo5 = 0, mi5 = 0, hi5 = 0;
+#pragma unroll
+            for (int u = 0; u < 5; u++) {
+                lo5 += (u64)xg[u] << (8 * u);
+                mi5 += (u64)xg[5 + u] << (8 * u);
+                hi5 += (u64)xg[10 + u] << (8 * u);
+            }
+            const u64 lo = lo5 + (mi5 << 40);
+            u64 hi = (mi5 >> 24) + (hi5 << 16) + (lo < lo5 ? 1ull : 0ull);
+            if (hi >= 2 * q) hi -= 2 * q;
+            if (hi >= 2 * q) hi -= 2 * q;
+            if (hi >= q) hi -= q;
+            return csub(redc_lazy(hi, lo, md), q);
+        };
+        int it = 0;
+        // blocks of 4 positions p = j N + k .. k + 3 (same prime: N % 4 == 0); one 32-byte store per output
+        int j = (int)(p0 / N), k = (int)(p0 - (long long)j * N);
+        for (long long p = p0; p < p1; p += 4) {
+            const ModC md = c.mod[j];
             const bool active = (sidx < 2 || j < L) && bi < B;
-            // lane groups 0..2: the MMA rows (U c0, U c1, Cacc c0 incl. its step-0 member); lane group 3
-            // (no MMA rows): the step-0 product of the c1 stream, x.c1 (.) w[g b], on the CUDA cores
-            u64 xc1 = 0, w0[4];
-            if (sidx == 3 && active) xc1 = __ldg(X + (long long)bi * W + (long long)(L + j) * N + k);
-            mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
-            asm volatile("tcgen05.fence::after_thread_sync;");
+            const long long z0 = (long long)bi * G + 4 * gh;
+            u64* out0 = sidx == 3 ? Cacc + ((z0 * 2 + 1) * L + j) * (long long)N + k
+                      : sidx < 2  ? U + ((z0 * 2 + sidx) * M + j) * (long long)N + k
+                                  : Cacc + ((z0 * 2 + 0) * L + j) * (long long)N + k;
+            // lane group 3 (no MMA rows): the step-0 product of the c1 stream, x.c1 (.) w[g b], on the CUDA cores
+            ulonglong2 xa = make_ulonglong2(0, 0), xb = make_ulonglong2(0, 0);
+            if (sidx == 3 && active) {
+                const ulonglong2* xs = (const ulonglong2*)(X + (long long)bi * W + (long long)(L + j) * N + k);
+                xa = __ldg(xs);
+                xb = __ldg(xs + 1);
+            }
+            u64 res[4][4];
 #pragma unroll
-            for (int t = 0; t < 4; t++) w0[t] = s_w0[it & 3][4 * gh + t];
-            uint32_t x[64];
-            const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + gh * 64);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-                "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, "
-                "%37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, "
-                "%59, %60, %61, %62, %63}, [%64];"
-                : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]),
-                  "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15]),
-                  "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]), "=r"(x[21]), "=r"(x[22]), "=r"(x[23]),
-                  "=r"(x[24]), "=r"(x[25]), "=r"(x[26]), "=r"(x[27]), "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31]),
-                  "=r"(x[32]), "=r"(x[33]), "=r"(x[34]), "=r"(x[35]), "=r"(x[36]), "=r"(x[37]), "=r"(x[38]), "=r"(x[39]),
-                  "=r"(x[40]), "=r"(x[41]), "=r"(x[42]), "=r"(x[43]), "=r"(x[44]), "=r"(x[45]), "=r"(x[46]), "=r"(x[47]),
-                  "=r"(x[48]), "=r"(x[49]), "=r"(x[50]), "=r"(x[51]), "=r"(x[52]), "=r"(x[53]), "=r"(x[54]), "=r"(x[55]),
-                  "=r"(x[56]), "=r"(x[57]), "=r"(x[58]), "=r"(x[59]), "=r"(x[60]), "=r"(x[61]), "=r"(x[62]), "=r"(x[63])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);   // this warp's accumulator columns are in registers
-            if (active && sidx == 3) {
+            for (int pi = 0; pi < 4; pi++, it++) {
+                const int acc = it & 1;
+                GP_WAIT(8, mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1)));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                u64 w0[4];
 #pragma unroll
-                for (int t = 0; t < 4; t++) {
-                    const int g = 4 * gh + t;
-                    if (g < G) Cacc[((((long long)bi * G + g) * 2 + 1) * L + j) * (long long)N + k] = mont_mul(xc1, w0[t], md);
-                }
-            } else if (active) {
+                for (int t = 0; t < 4; t++) w0[t] = s_w0[it & 3][4 * gh + t];
+                if (sidx == 3) {
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    const u64 xc1 = pi == 0 ? xa.x : pi == 1 ? xa.y : pi == 2 ? xb.x : xb.y;
 #pragma unroll
-                for (int t = 0; t < 4; t++) {
-                    const int g = 4 * gh + t;
-                    if (g >= G) break;
-                    const uint32_t* xg = x + 16 * t;
-                    // sum_s' 256^s' D_s' (exact, < 2^126): three 40-bit-spaced partial sums below 2^58
-                    u64 lo5 = 0, mi5 = 0, hi5 = 0;
+                    for (int t = 0; t < 4; t++) res[pi][t] = mont_mul(xc1, w0[t], md);
+                } else {
+                    uint32_t x[32];
+                    const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + gh * 64);
 #pragma unroll
-                    for (int u = 0; u < 5; u++) {
-                        lo5 += (u64)xg[u] << (8 * u);
-                        mi5 += (u64)xg[5 + u] << (8 * u);
-                        hi5 += (u64)xg[10 + u] << (8 * u);
+                    for (int hf = 0; hf < 2; hf++) {   // groups 2 hf, 2 hf + 1: columns 16 t .. 16 t + 14
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+                            "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+                            "%30, %31}, [%32];"
+                            : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),
+                              "=r"(x[7]), "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]),
+                              "=r"(x[14]), "=r"(x[15]), "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]),
+                              "=r"(x[21]), "=r"(x[22]), "=r"(x[23]), "=r"(x[24]), "=r"(x[25]), "=r"(x[26]), "=r"(x[27]),
+                              "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
+                            : "r"(taddr + 32 * hf));
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (hf == 1) {   // the accumulator columns of this warp are in registers
+                            asm volatile("tcgen05.fence::before_thread_sync;");
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&tempty[acc]);
+                        }
+                        res[pi][2 * hf] = rebuild(x, md);
+                        res[pi][2 * hf + 1] = rebuild(x + 16, md);
                     }
-                    u64 lo = lo5 + (mi5 << 40);
-                    u64 hi = (mi5 >> 24) + (hi5 << 16) + (lo < lo5 ? 1ull : 0ull);
-                    if (hi >= 2 * q) hi -= 2 * q;
-                    if (hi >= 2 * q) hi -= 2 * q;
-                    if (hi >= q) hi -= q;
-                    const u64 v = csub(redc_lazy(hi, lo, md), q);   // sum_jj X w   (w Montgomery)
-                    const long long z = (long long)bi * G + g;
-                    if (sidx < 2) U[((z * 2 + sidx) * M + j) * (long long)N + k] = v;
-                    else Cacc[((z * 2 + 0) * L + j) * (long long)N + k] = v;
                 }
+            }
+            if (active) {
+#pragma unroll
+                for (int t = 0; t < 4; t++)
+                    if (4 * gh + t < G)
+                        asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(out0 + t * gstride),
+                                     "l"(res[0][t]), "l"(res[1][t]), "l"(res[2][t]), "l"(res[3][t])
+                                     : "memory");
+            }
+            k += 4;
+            if (k == N) {
+                k = 0;
+                j++;
             }
         }
     }
+    if (warp == 0 || warp == 1 || warp == 2 || warp == 10) GP_FLUSH(warp == 0)
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }

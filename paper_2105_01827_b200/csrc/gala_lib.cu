@@ -1782,3 +1782,11 @@ int gala_bench_modmul(gala_ctx* c, int blocks, int iters, double* modmul_per_s)
 }
 
 } // extern "C"
+
+#ifdef GTC_PROF
+extern "C" int gala_debug_gtc_prof(unsigned long long* out, int rows)
+{
+    return (int)cudaMemcpyFromSymbol(out, g_gtc_prof, (size_t)rows * 16 * sizeof(unsigned long long));
+}
+#endif
+
