@@ -418,7 +418,9 @@ def run_ours(args):
             "kernel_share_of_step": round(dom["ms"] / step_ms_prof, 4) if step_ms_prof else None,
             "roofs": roofs,
             "layer": {"achieved": round(layer_achieved / 1e9, 2), "frac": round(layer_achieved / peak_modmul, 4),
-                      "modmuls_per_layer": layer_modmuls},
+                      "modmuls_per_layer": layer_modmuls,
+                      "note": "modmul-equivalents of the whole layer against the CUDA-core roof; the baby-step "
+                              "products run on the int8 tensor cores, so this can exceed 1"},
             "hbm": {"algorithmic_bytes_per_layer": int(layer_bytes),
                     "achieved_gbs": round(layer_bytes * layers / world / (total_ms / 1e3) / 1e9, 2),
                     "peak_gbs": hbm_peak},

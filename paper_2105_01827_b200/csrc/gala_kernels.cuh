@@ -1271,8 +1271,10 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
     const int j = blockIdx.z, kc = blockIdx.y, k0 = blockIdx.x * 32;
     const int kk = threadIdx.x & 31, bg = threadIdx.x >> 5;
     const int k = k0 + kk;
-    const ModC md = c.mod[j];
-    const long long NN = N, MN = (long long)M * N, bw = (long long)(L * M + L) * N;
+    const u64 q = c.mod[j].q;
+    // 32-bit word offsets (the digit blocks of a batch and a key are < 2^31 words): address arithmetic
+    // stays on the integer ALU instead of 64-bit multiply-adds
+    const uint32_t MN = (uint32_t)M * N, bw = (uint32_t)(L * M + L) * N;
 #pragma unroll
     for (int jw = 0; jw < 2; jw++) {
         const int jj = 2 * kc + jw;               // jj = 0: E = 0 (no key switch), sigma_0(c0) = c0
@@ -1280,27 +1282,28 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
         u64 ka[L], kb[L];
         int src = k;
         if (valid) {
-            const u64* key = keys[jj];
+            const u64* key = keys[jj] + ((uint32_t)j * N + k);
             src = auto_src(k, gal[jj], logN);
 #pragma unroll
             for (int i = 0; i < L; i++) {
-                ka[i] = __ldg(key + (((long long)i * 2 + 0) * M + j) * NN + k);
-                kb[i] = __ldg(key + (((long long)i * 2 + 1) * M + j) * NN + k);
+                ka[i] = __ldg(key + (uint32_t)(2 * i) * MN);
+                kb[i] = __ldg(key + (uint32_t)(2 * i + 1) * MN);
             }
         }
-        // pointer walk (64-bit adds) instead of per-load index products
-        const u64* Dq = Dblk + (long long)(bg * 4) * bw + (long long)j * NN + src;
+        uint32_t o = (uint32_t)(bg * 4) * bw + (uint32_t)j * N + src;
 #pragma unroll
-        for (int q = 0; q < 4; q++, Dq += bw) {
-            const int bi = bg * 4 + q;
-            u64 e0 = 0, e1 = 0, r0 = 0;
-            if (jj == 0 && bi < B && j < L) r0 = __ldg(Dq + (long long)L * MN);
+        for (int qi = 0; qi < 4; qi++, o += bw) {
+            const int bi = bg * 4 + qi;
+            const int r2 = 64 + bi + kk;
+            // row r of position kk lives at (r + kk) % 96: the 32 positions of a warp hit distinct banks
+            u64* s_e0 = &sm[kk][bi + kk][jw];
+            u64* s_e1 = &sm[kk][32 + bi + kk][jw];
+            u64* s_r0 = &sm[kk][r2 >= 96 ? r2 - 96 : r2][jw];
             if (valid && bi < B) {
                 AccPP<true> s0, s1;   // L <= 4 canonical products per sum: merged cross sums fit
-                const u64* Di = Dq;
 #pragma unroll
-                for (int i = 0; i < L; i++, Di += MN) {
-                    const u64 d = __ldg(Di);
+                for (int i = 0; i < L; i++) {
+                    const u64 d = __ldg(Dblk + (o + (uint32_t)i * MN));
                     if (i == 0) {
                         s0.set(d, ka[i]);
                         s1.set(d, kb[i]);
@@ -1309,15 +1312,14 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
                         s1.mac(d, kb[i]);
                     }
                 }
-                e0 = s0.reduce_sf(md.q);
-                e1 = s1.reduce_sf(md.q);
-                if (j < L) r0 = __ldg(Di);
+                *s_e0 = s0.reduce_sf(q);
+                *s_e1 = s1.reduce_sf(q);
+                *s_r0 = j < L ? __ldg(Dblk + (o + (uint32_t)L * MN)) : 0ull;
+            } else {
+                *s_e0 = 0;
+                *s_e1 = 0;
+                *s_r0 = (jj == 0 && bi < B && j < L) ? __ldg(Dblk + (o + (uint32_t)L * MN)) : 0ull;
             }
-            // row r of position kk lives at (r + kk) % 96: the 32 positions of a warp hit distinct banks
-            const int r2 = 64 + bi + kk;
-            sm[kk][bi + kk][jw] = e0;
-            sm[kk][32 + bi + kk][jw] = e1;
-            sm[kk][r2 >= 96 ? r2 - 96 : r2][jw] = r0;
         }
     }
     __syncthreads();
@@ -2014,7 +2016,7 @@ __global__ void __launch_bounds__(256) k_bench_modmul(u64 q, u64 w, u64 wsh, int
     for (int it = 0; it < iters; it++) {
 #pragma unroll
         for (int i = 0; i < 8; i++) {
-            u64 v = shoup_lazy(x[i], w, wsh, q);
+            u64 v = shoup_lazy_sf(x[i], w, wsh, q);   // the cheapest modmul flavour the library uses
             x[i] = v >= q2 ? v - q2 : v;
         }
     }
