@@ -238,6 +238,66 @@ __global__ void __launch_bounds__(512, 2) v_g(const u64* in, u64* out, const ulo
     for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
 }
 
+// M: Montgomery-form twiddles (8 B each; w 2^64 mod q) and the special-form REDC: the product from four
+// 32x32 partials, then redc_sf_lazy; same [0, 2q) lazy bound as Shoup
+__device__ __forceinline__ u64 mont_lazy_pp(u64 x, u64 wm, u64 q)
+{
+    AccPP<> a;
+    a.set(x, wm);
+    u64 hi, lo;
+    a.value(hi, lo);
+    return redc_sf_lazy(hi, lo, q);
+}
+template <int R>
+__device__ __forceinline__ void fwd_pass_m(u64* s, const u64* __restrict__ tw, u64 q, int logN, int s0)
+{
+    const int N = 1 << logN;
+    const int G = N >> R;
+    const int lt = logN - s0 - R;
+    const int t_end = 1 << lt;
+    const u64 q2 = 2 * q;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const int blk = g >> lt, off = g & (t_end - 1);
+        const int base = (blk << (logN - s0)) + off;
+        u64 x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) x[k] = s[pad(base + (k << lt))];
+#pragma unroll
+        for (int l = 0; l < R; l++) {
+            const int m = 1 << (s0 + l);
+            const int half = 1 << (R - 1 - l);
+#pragma unroll
+            for (int k = 0; k < (1 << R); k++) {
+                if (k & half) continue;
+                const u64 w = __ldg(&tw[m + (blk << l) + (k >> (R - l))]);
+                u64 U = x[k];
+                U = U >= q2 ? U - q2 : U;
+                u64 V = mont_lazy_pp(x[k + half], w, q);
+                x[k] = U + V;
+                x[k + half] = U - V + q2;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) s[pad(base + (k << lt))] = x[k];
+    }
+}
+__global__ void __launch_bounds__(512, 2) v_m(const u64* in, u64* out, const u64* tw, u64 q, int logN)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    const u64* src = in + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(i)] = src[i];
+    __syncthreads();
+    fwd_pass_m<1>(sm, tw, q, logN, 0);
+    __syncthreads();
+    for (int s0 = 1; s0 < logN; s0 += 3) {
+        fwd_pass_m<3>(sm, tw, q, logN, s0);
+        __syncthreads();
+    }
+    u64* dst = out + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
+}
+
 int main()
 {
     const int logN = 13, N = 1 << logN;
@@ -319,6 +379,17 @@ int main()
     run("G prod plan generic", [&] { v_g<false><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
     CKE(cudaFuncSetAttribute(v_g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     run("G prod plan SF", [&] { v_g<true><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    {
+        std::vector<u64> twm(N);
+        for (int k = 0; k < N; k++) twm[k] = (u64)((((u128)tw[k].x) << 64) % q);
+        u64* dtwm;
+        CKE(cudaMalloc(&dtwm, N * 8));
+        CKE(cudaMemcpy(dtwm, twm.data(), N * 8, cudaMemcpyHostToDevice));
+        CKE(cudaFuncSetAttribute(v_m, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        run("M montgomery tw + sf REDC", [&] { v_m<<<P, 512, smem>>>(din, dout, dtwm, q, logN); }, false);
+        CKE(cudaFuncSetAttribute(v_g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        run("G prod plan SF (again)", [&] { v_g<true><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    }
     CKE(cudaFuncSetAttribute(v_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     run("K SF + pass-level folds", [&] { v_k<true><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
     CKE(cudaFuncSetAttribute(v_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
