@@ -298,6 +298,70 @@ __global__ void __launch_bounds__(512, 2) v_m(const u64* in, u64* out, const u64
     for (int i = threadIdx.x; i < N; i += blockDim.x) dst[i] = csub(csub(sm[pad(i)], 2 * q), q);
 }
 
+// A: approximate Shoup quotient (three of the four 32x32 partials of x w'; the quotient is at most 2
+// short, so the product lands in [0, 4q)) with q < 2^60 and 6q lazy bounds through the pass
+__device__ __forceinline__ u64 shoup_approx_sf(u64 x, u64 w, u64 wsh, u64 q)
+{
+    const uint32_t x0 = (uint32_t)x, x1 = (uint32_t)(x >> 32), s0 = (uint32_t)wsh, s1 = (uint32_t)(wsh >> 32);
+    const u64 qh = (u64)x1 * s1 + (((u64)x0 * s1) >> 32) + (((u64)x1 * s0) >> 32);
+    const uint32_t a = (uint32_t)(q >> 32);
+    const u64 hq = qh + ((u64)((uint32_t)qh * a) << 32);
+    return x * w - hq;
+}
+template <int R>
+__device__ __forceinline__ void fwd_pass_a(u64* s, const ulonglong2* __restrict__ tw, u64 q, int logN, int s0)
+{
+    const int N = 1 << logN;
+    const int G = N >> R;
+    const int lt = logN - s0 - R;
+    const int t_end = 1 << lt;
+    const u64 q2 = 2 * q, q4 = 4 * q;
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        const int blk = g >> lt, off = g & (t_end - 1);
+        const int base = (blk << (logN - s0)) + off;
+        u64 x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) x[k] = s[pad(base + (k << lt))];
+#pragma unroll
+        for (int l = 0; l < R; l++) {
+            const int m = 1 << (s0 + l);
+            const int half = 1 << (R - 1 - l);
+#pragma unroll
+            for (int k = 0; k < (1 << R); k++) {
+                if (k & half) continue;
+                const ulonglong2 w = __ldg(&tw[m + (blk << l) + (k >> (R - l))]);
+                u64 U = x[k];                       // < 6q
+                U = U >= q4 ? U - q4 : U;
+                U = U >= q2 ? U - q2 : U;           // [0, 2q)
+                u64 V = shoup_approx_sf(x[k + half], w.x, w.y, q);   // [0, 4q)
+                x[k] = U + V;                       // [0, 6q)
+                x[k + half] = U - V + q4;           // (0, 6q)
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << R); k++) s[pad(base + (k << lt))] = x[k];
+    }
+}
+__global__ void __launch_bounds__(512, 2) v_a(const u64* in, u64* out, const ulonglong2* tw, u64 q, int logN)
+{
+    extern __shared__ u64 sm[];
+    const int N = 1 << logN;
+    const u64* src = in + (long long)blockIdx.x * N;
+    fwd_first_pass<1, true>([=](int i) { return src[i]; }, sm, tw, q, logN);
+    __syncthreads();
+    for (int s0 = 1; s0 < logN; s0 += 3) {
+        fwd_pass_a<3>(sm, tw, q, logN, s0);
+        __syncthreads();
+    }
+    u64* dst = out + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        u64 v = sm[pad(i)];
+        v = v >= 4 * q ? v - 4 * q : v;
+        v = v >= 2 * q ? v - 2 * q : v;
+        dst[i] = v >= q ? v - q : v;
+    }
+}
+
 int main()
 {
     const int logN = 13, N = 1 << logN;
@@ -390,6 +454,9 @@ int main()
         CKE(cudaFuncSetAttribute(v_g<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         run("G prod plan SF (again)", [&] { v_g<true><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
     }
+    CKE(cudaFuncSetAttribute(v_a, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    run("A approx Shoup, 6q bounds", [&] { v_a<<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
+    run("A approx Shoup, 6q bounds", [&] { v_a<<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
     CKE(cudaFuncSetAttribute(v_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     run("K SF + pass-level folds", [&] { v_k<true><<<P, 512, smem>>>(din, dout, dtw, q, logN); }, false);
     CKE(cudaFuncSetAttribute(v_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
