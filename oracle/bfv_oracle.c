@@ -761,7 +761,9 @@ static void encode_pt_ntt_qp(const octx *c, const uint32_t *slots, u64 *pt)
  *   d'_i = d_i * p_t   (integer polynomials; sum_i d'_i g_i = c1 p_t mod Q)
  * so  KSraw(sigma_j, x (.) p_t) = sum_i sigma_j(D_i (.) P_t) * ksk_j[i]  over QP,
  * with P_t the centred lift of p_t in every prime of QP.  Giant steps rotate
- * the group sums with their own decompositions (as in o_mv_gala).
+ * the group sums with their own decompositions; only the c1 of a group sum is
+ * brought down to Q (it must be decomposed), its c0 is rotated in QP and summed,
+ * and one final ModDown covers those sums and the giant-step key switches.
  */
 int o_mv_gala2(void *h, const u64 *ct, const uint32_t *pts, int T, int baby, const uint32_t *r, u64 *out,
                u64 *masked)
@@ -770,23 +772,26 @@ int o_mv_gala2(void *h, const u64 *ct, const uint32_t *pts, int T, int baby, con
     int N = c->N, L = c->L, M = c->M, n = N / 2;
     if (baby <= 0) baby = o_bsgs_baby(T);
     if (T % baby) return -4;
+    if (T > n) return -4;
     int G = T / baby;
-    size_t W = 2 * (size_t)L * N, UW = 2 * (size_t)M * N;
+    size_t W = 2 * (size_t)L * N, UW = 2 * (size_t)M * N, LN = (size_t)L * N;
     u64 *ctn = malloc(sizeof(u64) * W);
     ct_to_ntt(c, ct, ctn);
     u64 *D = malloc(sizeof(u64) * (size_t)L * M * N);
-    decompose(c, ctn + (size_t)L * N, D);
-    u64 *inner = malloc(sizeof(u64) * W * (size_t)G);
+    decompose(c, ctn + LN, D);
+    /* per group g: U_g (QP, both components), C0_g (Q: c0 rotation sums), C1_g (Q: step-0 c1 product) */
+    u64 *Ug = calloc(UW * (size_t)G, sizeof(u64));
+    u64 *C0g = calloc(LN * (size_t)G, sizeof(u64));
+    u64 *C1g = calloc(LN * (size_t)G, sizeof(u64));
     int rc = 0;
     for (int j = 1; j < baby; j++) if (!c->ksk[j % n]) rc = -2;
-    if (rc) { free(ctn); free(D); free(inner); return rc; }
+    for (int g = 1; g < G; g++) if (!c->ksk[(g * baby) % n]) rc = -2;
+    if (rc) { free(ctn); free(D); free(Ug); free(C0g); free(C1g); return rc; }
 #pragma omp parallel for schedule(dynamic)
     for (int g = 0; g < G; g++) {
-        u64 *U = calloc(UW, sizeof(u64));
-        u64 *C0 = calloc((size_t)L * N, sizeof(u64));
+        u64 *U = Ug + (size_t)g * UW, *C0 = C0g + (size_t)g * LN, *C1 = C1g + (size_t)g * LN;
         u64 *P = malloc(sizeof(u64) * (size_t)M * N);
         u64 *X = malloc(sizeof(u64) * N), *Y = malloc(sizeof(u64) * N);
-        u64 *res = inner + (size_t)g * W;
         for (int jj = 0; jj < baby; jj++) {
             int t = g * baby + jj;
             encode_pt_ntt_qp(c, pts + (size_t)t * N, P);
@@ -796,7 +801,7 @@ int o_mv_gala2(void *h, const u64 *ct, const uint32_t *pts, int T, int baby, con
                     for (int k = 0; k < N; k++) {
                         C0[(size_t)j * N + k] = addmod(C0[(size_t)j * N + k],
                                                        mulmod(ctn[(size_t)j * N + k], P[(size_t)j * N + k], q), q);
-                        res[((size_t)L + j) * N + k] = mulmod(ctn[((size_t)L + j) * N + k], P[(size_t)j * N + k], q);
+                        C1[(size_t)j * N + k] = mulmod(ctn[((size_t)L + j) * N + k], P[(size_t)j * N + k], q);
                     }
                 }
                 continue;
@@ -822,28 +827,75 @@ int o_mv_gala2(void *h, const u64 *ct, const uint32_t *pts, int T, int baby, con
                 for (int k = 0; k < N; k++) C0[(size_t)j * N + k] = addmod(C0[(size_t)j * N + k], Y[k], q);
             }
         }
-        u64 *md = malloc(sizeof(u64) * (size_t)L * N);
-        moddown(c, U, md);
-        for (size_t i = 0; i < (size_t)L * N; i++) {
-            u64 q = c->t[i / N].q;
-            res[i] = addmod(C0[i], md[i], q);
-        }
-        moddown(c, U + (size_t)M * N, md);
-        for (size_t i = 0; i < (size_t)L * N; i++) {
-            u64 q = c->t[i / N].q;
-            res[(size_t)L * N + i] = addmod(res[(size_t)L * N + i], md[i], q);
-        }
-        free(U); free(C0); free(P); free(X); free(Y); free(md);
+        free(P); free(X); free(Y);
     }
-    u64 *resn = malloc(sizeof(u64) * W);
-    int *steps = malloc(sizeof(int) * (size_t)G);
-    for (int g = 0; g < G; g++) steps[g] = g * baby;
-    rc = rotate_sum_lazy(c, inner, steps, G, resn);
+    /* giant steps, c0 ModDown deferred: S.c0 = sum_g sigma_g(U_g.c0), S.c1 = U_0.c1 (QP);
+     * Qadd.c0 = sum_g sigma_g(C0_g), Qadd.c1 = C1_0 (Q); group g >= 1: c1' = C1_g + ModDown(U_g.c1)
+     * is key-switched for the rotation by g b into Uks (QP).  out = ModDown(S + Uks) + Qadd. */
+    u64 *S = calloc(UW, sizeof(u64)), *Uks = calloc(UW, sizeof(u64)), *Qadd = calloc(W, sizeof(u64));
+    u64 *perm = malloc(sizeof(u64) * N);
+    for (int g = 0; g < G; g++) {
+        const u64 *U = Ug + (size_t)g * UW;
+        u64 ge = g ? galois((g * baby) % n, N) : 1;
+        for (int j = 0; j < M; j++) {
+            u64 q = c->t[j].q;
+            if (g) automorph_ntt(U + (size_t)j * N, perm, N, ge);
+            else memcpy(perm, U + (size_t)j * N, sizeof(u64) * N);
+            for (int k = 0; k < N; k++) S[(size_t)j * N + k] = addmod(S[(size_t)j * N + k], perm[k], q);
+        }
+        for (int j = 0; j < L; j++) {
+            u64 q = c->t[j].q;
+            const u64 *C0 = C0g + (size_t)g * LN + (size_t)j * N;
+            if (g) automorph_ntt(C0, perm, N, ge);
+            else memcpy(perm, C0, sizeof(u64) * N);
+            for (int k = 0; k < N; k++) Qadd[(size_t)j * N + k] = addmod(Qadd[(size_t)j * N + k], perm[k], q);
+        }
+    }
+    memcpy(S + (size_t)M * N, Ug + (size_t)M * N, sizeof(u64) * (size_t)M * N);
+    memcpy(Qadd + LN, C1g, sizeof(u64) * LN);
+    int *rcs = calloc((size_t)G, sizeof(int));
+    u64 *Ut = calloc(UW * (size_t)G, sizeof(u64));
+#pragma omp parallel for schedule(dynamic)
+    for (int g = 1; g < G; g++) {
+        u64 *c1p = malloc(sizeof(u64) * LN), *Dg = malloc(sizeof(u64) * (size_t)L * M * N);
+        moddown(c, Ug + (size_t)g * UW + (size_t)M * N, c1p);
+        for (size_t i = 0; i < LN; i++) {
+            u64 q = c->t[i / N].q;
+            c1p[i] = addmod(c1p[i], C1g[(size_t)g * LN + i], q);
+        }
+        decompose(c, c1p, Dg);
+        rcs[g] = ks_accumulate(c, g * baby, Dg, Ut + (size_t)g * UW);
+        free(c1p); free(Dg);
+    }
+    for (int g = 1; g < G; g++) {
+        if (rcs[g]) rc = rcs[g];
+        for (int j = 0; j < M; j++) {
+            u64 q = c->t[j].q;
+            for (int comp = 0; comp < 2; comp++) {
+                u64 *u = Uks + ((size_t)comp * M + j) * N;
+                const u64 *v = Ut + (size_t)g * UW + ((size_t)comp * M + j) * N;
+                for (int k = 0; k < N; k++) u[k] = addmod(u[k], v[k], q);
+            }
+        }
+    }
     if (!rc) {
+        u64 *resn = malloc(sizeof(u64) * W), *md = malloc(sizeof(u64) * LN);
+        for (size_t i = 0; i < UW; i++) {
+            u64 q = c->t[(i / N) % M].q;
+            S[i] = addmod(S[i], Uks[i], q);
+        }
+        for (int comp = 0; comp < 2; comp++) {
+            moddown(c, S + (size_t)comp * M * N, md);
+            for (size_t i = 0; i < LN; i++) {
+                u64 q = c->t[i / N].q;
+                resn[(size_t)comp * LN + i] = addmod(md[i], Qadd[(size_t)comp * LN + i], q);
+            }
+        }
         ct_from_ntt(c, resn, out);
         if (r && masked) o_sub_plain(c, out, r, masked);
+        free(resn); free(md);
     }
-    free(ctn); free(D); free(inner); free(resn); free(steps);
+    free(ctn); free(D); free(Ug); free(C0g); free(C1g); free(S); free(Uks); free(Qadd); free(perm); free(rcs); free(Ut);
     return rc;
 }
 

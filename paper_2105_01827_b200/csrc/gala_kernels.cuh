@@ -101,17 +101,22 @@ struct MdArgs {
     u64* out;          // [G] stride out_is, [2][L][N]   (used when outs == null)
     long long out_is;
     u64* const* outs;  // optional per-group output pointers
+    int comps;         // components per item (0 = 2); 1: only component comp0
+    int comp0;
+    int skip_per;      // > 0: item x reads source item (x / (skip_per - 1)) skip_per + 1 + x % (skip_per - 1)
 };
 
 __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
 {
     extern __shared__ u64 sm[];
     const int L = c.L, M = c.M, N = c.N;
-    const int g = blockIdx.x / (2 * L), w = blockIdx.x % (2 * L);
-    const int comp = w / L, j = w % L;
+    const int comps = a.comps ? a.comps : 2;
+    const int x = blockIdx.x / (comps * L), w = blockIdx.x % (comps * L);
+    const int comp = a.comp0 + w / L, j = w % L;
+    const long long g = a.skip_per > 0 ? (long long)(x / (a.skip_per - 1)) * a.skip_per + 1 + x % (a.skip_per - 1) : x;
     const ModC md = c.mod[j];
     const u64 q = md.q, P = c.mod[L].q, halfP = P >> 1;
-    const u64* r = a.r + ((long long)g * 2 + comp) * N;
+    const u64* r = a.r + ((long long)x * comps + (comp - a.comp0)) * N;
     // centred lift of v in [0, P) into [0, 2q): |v - P| < P/2 < q_j (asserted at context creation)
     ntt_fwd_g([=](int i) {
         const u64 v = r[i];
@@ -120,7 +125,7 @@ __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
     const u64* U = a.U + (((long long)g * 2 + comp) * M + j) * N;
     const u64* add = comp == 0 ? a.add0 : a.add1;
     if (add) add += (long long)g * a.add_is + (long long)j * N;
-    u64* out = (a.outs ? a.outs[g] : a.out + (long long)g * a.out_is) + ((long long)comp * L + j) * N;
+    u64* out = (a.outs ? a.outs[x] : a.out + (long long)x * a.out_is) + ((long long)comp * L + j) * N;
     const u64 pinv = c.pinv_mont[j];
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         u64 R = csub(csub(sm[pad(i)], 2 * q), q);
@@ -147,6 +152,7 @@ struct TermDesc {
     u64* dig;          // [L][N] digit coefficients (scratch)
     u64* blk;          // first permuted block [(L*M + L)][N]; rotation r at blk + r * blk_words
     int rot_off, rot_cnt;
+    int c0_zero;       // the term's c0 is zero: no sigma-copies of it (its block slots are not read)
 };
 
 __device__ __forceinline__ u64 src_limb(const DevCtx& c, const TermDesc& t, int comp, int j, int k)
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(512, 2) k_digits_intt(DevCtx c, const TermDesc
     const int ti = blockIdx.x / L, i = blockIdx.x % L;
     const TermDesc t = terms[ti];
     const u64 q = c.mod[i].q;
-    if (t.blk) {
+    if (t.blk && !t.c0_zero) {
         for (int k = threadIdx.x; k < N; k += blockDim.x) sm[pad(k)] = src_limb(c, t, 0, i, k);
         __syncthreads();
         write_perm(c, sm, t, galois, blk_words, L * M + i);
@@ -244,6 +250,7 @@ struct MacMember {
     const u64* key;    // [L][2][M][N]
     const u64* X;      // step-0 member source
     const u64* pt;
+    int no_c0;         // rotated member whose c0 is zero (block c0 slots not written)
 };
 
 // grid (N / blockDim, M, G); U [G][2][M][N]; Cacc [G][2][L][N].
@@ -255,7 +262,8 @@ struct MacMember {
 template <int L>
 __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __restrict__ mem,
                                                 const int* __restrict__ group_off, u64* __restrict__ U,
-                                                u64* __restrict__ Cacc)
+                                                u64* __restrict__ Cacc, const u64* __restrict__ qp_add,
+                                                const u64* __restrict__ q_add)
 {
     const int N = c.N, M = L + 1;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -265,7 +273,16 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
     const u64 q = md.q;
     const int lazy = c.lazy[j];
     const long long NN = N;
+    // optional addends: QP [G][2][M][N] into U (before the ModDown), Q [G][2][L][N] into the c0/c1 sums
     u64 u0 = 0, u1 = 0, a0 = 0, a1 = 0;
+    if (qp_add) {
+        u0 = qp_add[(((long long)g * 2 + 0) * M + j) * NN + k];
+        u1 = qp_add[(((long long)g * 2 + 1) * M + j) * NN + k];
+    }
+    if (q_add && j < L) {
+        a0 = q_add[(((long long)g * 2 + 0) * L + j) * NN + k];
+        a1 = q_add[(((long long)g * 2 + 1) * L + j) * NN + k];
+    }
     int it = group_off[g];
     const int hi = group_off[g + 1];
     for (; it < hi; it++) {                       // step-0 members
@@ -297,7 +314,7 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
                 ka[i] = __ldg(&m.key[(((long long)i * 2 + 1) * M + j) * NN + k]);
             }
         }
-        if (j < L) cv = __ldcs((const unsigned long long*)(m.blk + ((long long)L * M + j) * NN + k));
+        cv = (j < L && !m.no_c0) ? __ldcs((const unsigned long long*)(m.blk + ((long long)L * M + j) * NN + k)) : 0ull;
     };
     if (it < hi) fetch(mem[it]);
     for (; it < hi; it++) {
@@ -329,6 +346,41 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
     if (j < L) {
         Cacc[(((long long)g * 2 + 0) * L + j) * NN + k] = a0;
         Cacc[(((long long)g * 2 + 1) * L + j) * NN + k] = a1;
+    }
+}
+
+// GALA schedule 2, giant steps with the c0 ModDown deferred: per input b (groups z = b G + g)
+//   S[b].c0 = sum_g sigma_g(U_z.c0)            (QP)      Qadd[b].c0 = sum_g sigma_g(C_z.c0)      (Q)
+//   S[b].c1 = sum_{g: step 0} U_z.c1           (QP)      Qadd[b].c1 = sum_{g: step 0} C_z.c1     (Q)
+// (sigma_g = the automorphism of the giant step g b; identity for step 0).  The final ModDown of S plus
+// the giant-step key switches, plus Qadd, is the layer output.  grid (N / 256, M, B)
+__global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __restrict__ Cacc,
+                           const unsigned* __restrict__ gal, int G, u64* __restrict__ S, u64* __restrict__ Qadd)
+{
+    const int N = c.N, L = c.L, M = c.M;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, b = blockIdx.z;
+    if (k >= N) return;
+    const u64 q = c.mod[j].q;
+    const long long NN = N;
+    u64 s0 = 0, s1 = 0, c0 = 0, c1 = 0;
+#pragma unroll 1
+    for (int g = 0; g < G; g++) {
+        const long long z = (long long)b * G + g;
+        const unsigned ge = gal[g];
+        const int src = ge == 1u ? k : auto_src(k, ge, c.logN);
+        s0 = add_mod(s0, __ldg(U + ((z * 2 + 0) * M + j) * NN + src), q);
+        if (j < L) c0 = add_mod(c0, __ldg(Cacc + ((z * 2 + 0) * L + j) * NN + src), q);
+        if (ge == 1u) {
+            s1 = add_mod(s1, __ldg(U + ((z * 2 + 1) * M + j) * NN + k), q);
+            if (j < L) c1 = add_mod(c1, __ldg(Cacc + ((z * 2 + 1) * L + j) * NN + k), q);
+        }
+    }
+    S[(((long long)b * 2 + 0) * M + j) * NN + k] = s0;
+    S[(((long long)b * 2 + 1) * M + j) * NN + k] = s1;
+    if (j < L) {
+        Qadd[(((long long)b * 2 + 0) * L + j) * NN + k] = c0;
+        Qadd[(((long long)b * 2 + 1) * L + j) * NN + k] = c1;
     }
 }
 

@@ -246,6 +246,7 @@ struct EngTerm {
     const u64* pt;
     std::vector<int> steps;   // nonzero rotation steps of this term
     const u64* ntt_block;     // optional: precomputed identity block (hoisted DecPerm)
+    bool c0_zero = false;     // X.c0 is zero: skip its sigma-copies and sums
 };
 struct EngMember {
     int term;
@@ -254,8 +255,11 @@ struct EngMember {
 
 static const u64* key_for(gala_ctx* c, int step);
 
+// qp_add [G][2][M][N] (optional) is added to each group's key-switch sum before its ModDown, q_add
+// [G][2][L][N] (optional) after it.
 static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
-                         const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs)
+                         const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs,
+                         const u64* qp_add = nullptr, const u64* q_add = nullptr)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const int G = (int)groups.size();
@@ -281,9 +285,10 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     int di = 0;
     for (size_t t = 0; t < terms.size(); t++) {
         if (terms[t].steps.empty()) continue;
-        TermDesc d;
+        TermDesc d{};
         d.X = terms[t].X;
         d.pt = terms[t].pt;
+        d.c0_zero = terms[t].c0_zero ? 1 : 0;
         d.dig = terms[t].ntt_block ? nullptr : dig + (long long)(di++) * L * N;
         d.blk = blk + (long long)term_rot_base[t] * blk_words;
         d.rot_off = (int)gal.size();
@@ -303,7 +308,7 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         std::vector<EngMember> g(g0);   // k_ks_mac expects the step-0 members first
         std::stable_partition(g.begin(), g.end(), [](const EngMember& m) { return m.rot < 0; });
         for (auto& m : g) {
-            MacMember mm;
+            MacMember mm{};
             const EngTerm& T = terms[m.term];
             if (m.rot < 0) {
                 mm.blk = nullptr;
@@ -315,6 +320,7 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
                 mm.key = key_for(c, T.steps[m.rot]);
                 mm.X = nullptr;
                 mm.pt = nullptr;
+                mm.no_c0 = T.c0_zero ? 1 : 0;
             }
             mem.push_back(mm);
         }
@@ -361,15 +367,15 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         const MacMember* dm = (const MacMember*)(d_blob + o_mem);
         const int* doff = (const int*)(d_blob + o_off);
         switch (L) {
-            case 1: KLAUNCH(c, "k_ks_mac", k_ks_mac<1><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
-            case 2: KLAUNCH(c, "k_ks_mac", k_ks_mac<2><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
-            case 3: KLAUNCH(c, "k_ks_mac", k_ks_mac<3><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
-            default: KLAUNCH(c, "k_ks_mac", k_ks_mac<4><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc)); break;
+            case 1: KLAUNCH(c, "k_ks_mac", k_ks_mac<1><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc, qp_add, q_add)); break;
+            case 2: KLAUNCH(c, "k_ks_mac", k_ks_mac<2><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc, qp_add, q_add)); break;
+            case 3: KLAUNCH(c, "k_ks_mac", k_ks_mac<3><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc, qp_add, q_add)); break;
+            default: KLAUNCH(c, "k_ks_mac", k_ks_mac<4><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc, qp_add, q_add)); break;
         }
     }
     RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
-    MdArgs a;
+    MdArgs a{};
     a.r = r;
     a.U = U;
     a.add0 = Cacc;
@@ -839,7 +845,7 @@ int gala_decompose(gala_ctx* c, const uint64_t* ct, uint64_t* digits)
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     u64* dig;
     RET(scratch(c, &dig, (size_t)L * N));
-    TermDesc d;
+    TermDesc d{};
     d.X = ct;
     d.pt = nullptr;
     d.dig = dig;
@@ -847,7 +853,7 @@ int gala_decompose(gala_ctx* c, const uint64_t* ct, uint64_t* digits)
     d.rot_off = 0;
     d.rot_cnt = 1;
     struct {
-        TermDesc t;
+        TermDesc t{};
         unsigned g;
     } b = {d, 1u};
     char* d_blob;
@@ -1002,6 +1008,7 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     if (baby <= 0) baby = gala_bsgs_baby(T);
     if (T % baby) return set_err(GALA_ERR_PARAM, "baby step %d does not divide T=%d", baby, T);
     const int G = T / baby;
+    if ((long long)T > N / 2) return set_err(GALA_ERR_DIM, "T=%d exceeds the %d slots of a row", T, N / 2);
     const long long W = 2LL * L * N, MN = (long long)M * N;
     const long long blk_words = (long long)(L * M + L) * N;
     for (int j = 1; j < baby; j++)
@@ -1062,11 +1069,10 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     // 2. stage A: E_jj = sum_i sigma_jj(D_i) ksk_jj[i] per input and baby rotation (shared by all groups);
     //    stage B: per (input, group) U = sum_jj w_t E_jj, C0 = sum_jj w_t sigma_jj(c0) (+ step-0 member)
     const int Z = B * G;
-    u64 *E = nullptr, *R0 = nullptr, *U, *Cacc, *rr, *inner;
+    u64 *E = nullptr, *R0 = nullptr, *U, *Cacc, *rr;
     RET(scratch(c, &U, (size_t)Z * 2 * M * N));
     RET(scratch(c, &Cacc, (size_t)Z * 2 * L * N));
     RET(scratch(c, &rr, (size_t)Z * 2 * N));
-    RET(scratch(c, &inner, (size_t)Z * W));
     // the tensor-core tile always spans 32 input rows: it pays off from about half a tile of inputs
     // (config 2 at B = 8: 0.139 ms/layer vs 0.097 on the CUDA cores; B = 32: 0.044 vs 0.088)
     const bool tc = wcan != nullptr && B >= 16 && B <= 32 && G <= 8 && baby <= 64 && (N % 32) == 0 &&
@@ -1122,32 +1128,74 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     release(c, E);
     release(c, R0);
     }
-    // 3. one ModDown per (input, group) -> inner[b][g]
-    RET(launch_inv<false>(c, U + (long long)L * N, rr, Z * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
-                          "k_ntt_inv[moddown]"));
-    MdArgs a;
-    a.r = rr;
-    a.U = U;
-    a.add0 = Cacc;
-    a.add1 = Cacc + (long long)L * N;
-    a.add_is = 2LL * L * N;
-    a.out = inner;
-    a.out_is = W;
-    a.outs = nullptr;
-    KLAUNCH(c, "k_moddown", k_moddown<<<Z * 2 * L, nt, c->smem_ntt, c->stream>>>(c->dc, a));
+    release(c, dig);
+    release(c, Dblk);
+    // 3. giant steps with the c0 ModDown deferred.  Group g's sum (U_z in QP, C_z in Q; z = b G + g) is
+    //    rotated by g b.  Only its c1 needs a ModDown (to be decomposed for the key switch); its c0 is
+    //    rotated in QP and summed: S.c0 = sum_g sigma_g(U_z.c0), S.c1 = U_{b,0}.c1, and one final
+    //    ModDown of S + the key-switch sums gives the layer (oracle: o_mv_gala2).
+    std::vector<unsigned> ggal(G, 1u);
+    for (int g = 1; g < G; g++) ggal[g] = galois_of(c, g * baby);
+    unsigned* d_ggal;
+    RET(upload(c, ggal.data(), ggal.size() * sizeof(unsigned), (void**)&d_ggal));
+    u64 *S, *Qadd;
+    RET(scratch(c, &S, (size_t)B * 2 * M * N));
+    RET(scratch(c, &Qadd, (size_t)B * 2 * L * N));
+    {
+        const int th = N < 256 ? N : 256;
+        dim3 gq((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)B);
+        KLAUNCH(c, "k_giant_qp", k_giant_qp<<<gq, th, 0, c->stream>>>(c->dc, U, Cacc, d_ggal, G, S, Qadd));
+    }
+    const int Zi = B * (G - 1);
+    u64* inner = nullptr;
+    if (Zi > 0) {
+        // inner ModDown of c1 for the groups g >= 1 (item x -> z = (x / (G-1)) G + 1 + x % (G-1))
+        RET(scratch(c, &inner, (size_t)Zi * W));
+        RET(launch_inv<false>(c, U + (long long)(M + L) * N, rr, Zi, pm_make(1, 1, L, 0, 2LL * M * N, N, G),
+                              "k_ntt_inv[moddown]"));
+        MdArgs a{};
+        a.r = rr;
+        a.U = U;
+        a.add0 = Cacc;
+        a.add1 = Cacc + (long long)L * N;
+        a.add_is = 2LL * L * N;
+        a.out = inner;
+        a.out_is = W;
+        a.outs = nullptr;
+        a.comps = 1;
+        a.comp0 = 1;
+        a.skip_per = G;
+        KLAUNCH(c, "k_moddown", k_moddown<<<Zi * L, nt, c->smem_ntt, c->stream>>>(c->dc, a));
+    }
     release(c, U);
     release(c, Cacc);
     release(c, rr);
-    release(c, dig);
-    release(c, Dblk);
     release(c, d_blob);
-    // 4. giant steps (each group sum has its own decomposition), one lazy ModDown per input
-    if (G > 1) {
-        RET(rotate_sum_regular(c, inner, W, (long long)G * W, nullptr, B, 1, G, baby, outs, W));
-    } else {
-        CK(cudaMemcpyAsync(outs, inner, sizeof(u64) * B * W, cudaMemcpyDeviceToDevice, c->stream));
+    // 4. per input: the G-1 giant-step key switches of (0, c1') plus S before one lazy ModDown, plus Qadd
+    {
+        std::vector<EngTerm> terms;
+        std::vector<std::vector<EngMember>> groups((size_t)B);
+        std::vector<u64*> eouts;
+        terms.reserve((size_t)Zi);
+        for (int b = 0; b < B; b++) {
+            for (int g = 1; g < G; g++) {
+                EngTerm t;
+                t.X = inner + ((long long)b * (G - 1) + (g - 1)) * W;
+                t.pt = nullptr;
+                t.ntt_block = nullptr;
+                t.c0_zero = true;
+                t.steps.push_back(norm_step(c, g * baby));
+                terms.push_back(t);
+                groups[(size_t)b].push_back({(int)terms.size() - 1, 0});
+            }
+            eouts.push_back(outs + (long long)b * W);
+        }
+        RET(rotate_engine(c, terms, groups, eouts, S, Qadd));
     }
     release(c, inner);
+    release(c, S);
+    release(c, Qadd);
+    release(c, d_ggal);
     if (DM) RET(mask_finish(c, outs, DM, B, masked));
     return GALA_OK;
 }
@@ -1658,7 +1706,7 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     RET(scratch(c, &rr, (size_t)Mb * 2 * N));
     RET(launch_inv<false>(c, accq + (long long)L * N, rr, Mb * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
-    MdArgs a;
+    MdArgs a{};
     a.r = rr;
     a.U = accq;
     a.add0 = nullptr;

@@ -49,8 +49,11 @@ MV = load("mv_gala.npz")
 MV_CASES = list(range(int(MV["count"][0])))
 
 
+@pytest.mark.parametrize("schedule", [1, 2])
 @pytest.mark.parametrize("idx", MV_CASES)
-def test_oracle_mv_gala_matches_reference_payload(idx):
+def test_oracle_mv_gala_matches_reference_payload(idx, schedule):
+    """Both oracle schedules (1: per-term key switches, as the reference; 2: digits hoisted across the
+    plaintext product, deferred c0 ModDown) decrypt to the reference's payload and shares."""
     n, n_o, n_i, seed, rseed = (int(v) for v in MV[f"c{idx}_dims"])
     if n > 1024 and idx % 2:
         pytest.skip("large cases: every other one on CPU")
@@ -66,7 +69,7 @@ def test_oracle_mv_gala_matches_reference_payload(idx):
     ct = enc(o, bfv, rng, np.concatenate([xs, xs]).astype(np.uint32))
     r = np.random.default_rng(rseed).integers(0, P, n, dtype=np.int64)
     out, masked = o.mv_gala(ct, np.concatenate([slots, slots], axis=1).astype(np.uint32),
-                            np.concatenate([r, r]).astype(np.uint32))
+                            np.concatenate([r, r]).astype(np.uint32), schedule=schedule)
     dec = o.decrypt(out).astype(np.int64)
     assert np.array_equal(dec[:n], MV[f"c{idx}_payload"].astype(np.int64))
     assert np.array_equal(dec[n:], MV[f"c{idx}_payload"].astype(np.int64))
