@@ -110,7 +110,7 @@ if __name__ == "__main__":
         if w == "cfg1":
             r = fc("cfg1", 2048, 1, 16, 2048, 64)
         elif w == "cfg2":
-            r = fc("cfg2", 4096, 3, 1024, 4096, 8)
+            r = fc("cfg2", 4096, 3, 1024, 4096, 32)
         elif w == "cfg3":
             r = conv("cfg3", 2048, 1, 16, 16, 64, 64, 3)
         elif w == "cfg4":
