@@ -1321,14 +1321,15 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
     constexpr int M = L + 1;
     const int N = c.N, logN = c.logN;
     const int j = blockIdx.z, kc = blockIdx.y, k0 = blockIdx.x * 32;
-    const int kk = threadIdx.x & 31, bg = threadIdx.x >> 5;
+    // warp w: rotation jj = 2 kc + (w >> 2), inputs 8 (w & 3) .. + 7 (the key limbs are loaded once
+    // per thread and reused by 8 inputs)
+    const int kk = threadIdx.x & 31, jw = threadIdx.x >> 7, bg = (threadIdx.x >> 5) & 3;
     const int k = k0 + kk;
     const u64 q = c.mod[j].q;
     // 32-bit word offsets (the digit blocks of a batch and a key are < 2^31 words): address arithmetic
     // stays on the integer ALU instead of 64-bit multiply-adds
     const uint32_t MN = (uint32_t)M * N, bw = (uint32_t)(L * M + L) * N;
-#pragma unroll
-    for (int jw = 0; jw < 2; jw++) {
+    {
         const int jj = 2 * kc + jw;               // jj = 0: E = 0 (no key switch), sigma_0(c0) = c0
         const bool valid = jj >= 1 && jj < baby;
         u64 ka[L], kb[L];
@@ -1342,10 +1343,10 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
                 kb[i] = __ldg(key + (uint32_t)(2 * i + 1) * MN);
             }
         }
-        uint32_t o = (uint32_t)(bg * 4) * bw + (uint32_t)j * N + src;
+        uint32_t o = (uint32_t)(bg * 8) * bw + (uint32_t)j * N + src;
 #pragma unroll
-        for (int qi = 0; qi < 4; qi++, o += bw) {
-            const int bi = bg * 4 + qi;
+        for (int qi = 0; qi < 8; qi++, o += bw) {
+            const int bi = bg * 8 + qi;
             const int r2 = 64 + bi + kk;
             // row r of position kk lives at (r + kk) % 96: the 32 positions of a warp hit distinct banks
             u64* s_e0 = &sm[kk][bi + kk][jw];
