@@ -101,9 +101,11 @@ int gala_bsgs_baby(int T);
 /* GALA schedule 2 (the production schedule when the noise budget allows; see
  * DESIGN.md): one gadget decomposition of each input's c1, digits hoisted
  * across the plaintext product (sum_i (d_i p_t) g_i = c1 p_t mod Q), so the
- * T-1 baby-step key switches need no NTTs.  Plaintexts come from
- * gala_encode_gala_weights: slots [T][N] -> pts2 [T][L+1][N] (every prime of
- * QP, pre-permuted by sigma_{t mod baby}).  Matches oracle o_mv_gala2. */
+ * T-1 baby-step key switches need no NTTs.  The giant steps bring only the c1
+ * of a group sum down to Q; the c0 parts are rotated in QP and share the final
+ * ModDown.  Plaintexts come from gala_encode_gala_weights: slots [T][N] -> pts2
+ * [T][L+1][N] (every prime of QP, pre-permuted by sigma_{t mod baby}).
+ * T <= N/2.  Matches oracle o_mv_gala2. */
 int gala_encode_gala_weights(gala_ctx *ctx, const uint32_t *slots_dev, int T, int baby, uint64_t *pts2_dev);
 int gala_mv_gala2_batch(gala_ctx *ctx, const uint64_t *cts_dev, int B, const uint64_t *pts2_dev, int T, int baby,
                         const uint32_t *r_slots_dev, uint64_t *outs_dev, uint64_t *masked_dev);
