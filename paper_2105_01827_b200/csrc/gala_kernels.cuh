@@ -349,6 +349,36 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
     }
 }
 
+// U[g] = sum of the chunk sums Uv[v], v in [vstart[g], vstart[g] + vcount[g]) (and Cacc likewise):
+// groups k_ks_mac split into several grid slices.  grid (N / 256, M, G)
+__global__ void k_fold_groups(DevCtx c, const u64* __restrict__ Uv, const u64* __restrict__ Cv,
+                              const int* __restrict__ vstart, const int* __restrict__ vcount, u64* __restrict__ U,
+                              u64* __restrict__ Cacc)
+{
+    const int N = c.N, L = c.L, M = c.M;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, g = blockIdx.z;
+    if (k >= N) return;
+    const u64 q = c.mod[j].q;
+    const long long NN = N;
+    const int v0 = vstart[g], nv = vcount[g];
+    u64 u0 = 0, u1 = 0, a0 = 0, a1 = 0;
+    for (int v = v0; v < v0 + nv; v++) {
+        u0 = add_mod(u0, Uv[(((long long)v * 2 + 0) * M + j) * NN + k], q);
+        u1 = add_mod(u1, Uv[(((long long)v * 2 + 1) * M + j) * NN + k], q);
+        if (j < L) {
+            a0 = add_mod(a0, Cv[(((long long)v * 2 + 0) * L + j) * NN + k], q);
+            a1 = add_mod(a1, Cv[(((long long)v * 2 + 1) * L + j) * NN + k], q);
+        }
+    }
+    U[(((long long)g * 2 + 0) * M + j) * NN + k] = u0;
+    U[(((long long)g * 2 + 1) * M + j) * NN + k] = u1;
+    if (j < L) {
+        Cacc[(((long long)g * 2 + 0) * L + j) * NN + k] = a0;
+        Cacc[(((long long)g * 2 + 1) * L + j) * NN + k] = a1;
+    }
+}
+
 // GALA schedule 2, giant steps with the c0 ModDown deferred: per input b (groups z = b G + g)
 //   S[b].c0 = sum_g sigma_g(U_z.c0)            (QP)      Qadd[b].c0 = sum_g sigma_g(C_z.c0)      (Q)
 //   S[b].c1 = sum_{g: step 0} U_z.c1           (QP)      Qadd[b].c1 = sum_{g: step 0} C_z.c1     (Q)

@@ -303,12 +303,32 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     }
     std::vector<MacMember> mem;
     std::vector<int> off;
+    // long groups (the conv second-Perm sums c_n - 1 rotations) are split into chunks of at most
+    // kChunk rotated members, one k_ks_mac grid slice each, and the chunk sums folded afterwards:
+    // each thread's serial member loop stays short
+    const int kChunk = 16;
+    const bool can_split = qp_add == nullptr && q_add == nullptr;
+    std::vector<int> vstart, vcount;   // real group -> its virtual groups
     for (auto& g0 : groups) {
-        off.push_back((int)mem.size());
         std::vector<EngMember> g(g0);   // k_ks_mac expects the step-0 members first
         std::stable_partition(g.begin(), g.end(), [](const EngMember& m) { return m.rot < 0; });
-        for (auto& m : g) {
-            MacMember mm{};
+        int n0 = 0;
+        while (n0 < (int)g.size() && g[n0].rot < 0) n0++;
+        const int nrot = (int)g.size() - n0;
+        const int S = can_split && nrot > 2 * kChunk ? (nrot + kChunk - 1) / kChunk : 1;
+        vstart.push_back((int)off.size());
+        vcount.push_back(S);
+        int mi = 0;
+        for (int sidx = 0; sidx < S; sidx++) {
+            off.push_back((int)mem.size());
+            // chunk 0 takes the step-0 members; rotated members are dealt evenly
+            const int r_lo = (int)((long long)nrot * sidx / S), r_hi = (int)((long long)nrot * (sidx + 1) / S);
+            const int hi = n0 + r_hi;
+            if (sidx == 0) mi = 0;
+            else mi = n0 + r_lo;
+            for (; mi < hi; mi++) {
+                const EngMember& m = g[mi];
+                MacMember mm{};
             const EngTerm& T = terms[m.term];
             if (m.rot < 0) {
                 mm.blk = nullptr;
@@ -323,9 +343,11 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
                 mm.no_c0 = T.c0_zero ? 1 : 0;
             }
             mem.push_back(mm);
+            }
         }
     }
     off.push_back((int)mem.size());
+    const int V = (int)off.size() - 1;   // virtual groups
     // one descriptor blob
     auto align = [](size_t x) { return (x + 15) & ~(size_t)15; };
     size_t o_td = 0, o_th = align(o_td + td.size() * sizeof(TermDesc));
@@ -357,21 +379,38 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
                                                   c->stream>>>(c->dc, (const TermDesc*)(d_blob + o_th),
                                                                (const unsigned*)(d_blob + o_gal), blk_words));
     }
-    u64 *U, *Cacc, *r;
+    u64 *U, *Cacc, *r, *Uv = nullptr, *Cv = nullptr;
     RET(scratch(c, &U, (size_t)G * 2 * M * N));
     RET(scratch(c, &Cacc, (size_t)G * 2 * L * N));
     RET(scratch(c, &r, (size_t)G * 2 * N));
+    if (V > G) {
+        RET(scratch(c, &Uv, (size_t)V * 2 * M * N));
+        RET(scratch(c, &Cv, (size_t)V * 2 * L * N));
+    }
     const int th = N < 256 ? N : 256;
-    dim3 grid((N + th - 1) / th, M, G);
+    dim3 grid((N + th - 1) / th, M, V);
     {
+        u64* const Uo = V > G ? Uv : U;
+        u64* const Co = V > G ? Cv : Cacc;
         const MacMember* dm = (const MacMember*)(d_blob + o_mem);
         const int* doff = (const int*)(d_blob + o_off);
         switch (L) {
-            case 1: KLAUNCH(c, "k_ks_mac", k_ks_mac<1><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc, qp_add, q_add)); break;
-            case 2: KLAUNCH(c, "k_ks_mac", k_ks_mac<2><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc, qp_add, q_add)); break;
-            case 3: KLAUNCH(c, "k_ks_mac", k_ks_mac<3><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc, qp_add, q_add)); break;
-            default: KLAUNCH(c, "k_ks_mac", k_ks_mac<4><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, U, Cacc, qp_add, q_add)); break;
+            case 1: KLAUNCH(c, "k_ks_mac", k_ks_mac<1><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add)); break;
+            case 2: KLAUNCH(c, "k_ks_mac", k_ks_mac<2><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add)); break;
+            case 3: KLAUNCH(c, "k_ks_mac", k_ks_mac<3><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add)); break;
+            default: KLAUNCH(c, "k_ks_mac", k_ks_mac<4><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add)); break;
         }
+    }
+    if (V > G) {   // fold the chunk sums of every split group
+        int* d_vsc;
+        std::vector<int> vsc(vstart);
+        vsc.insert(vsc.end(), vcount.begin(), vcount.end());
+        RET(upload(c, vsc.data(), vsc.size() * sizeof(int), (void**)&d_vsc));
+        KLAUNCH(c, "k_fold_groups", k_fold_groups<<<dim3((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)G), th, 0,
+                                                    c->stream>>>(c->dc, Uv, Cv, d_vsc, d_vsc + G, U, Cacc));
+        release(c, d_vsc);
+        release(c, Uv);
+        release(c, Cv);
     }
     RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));

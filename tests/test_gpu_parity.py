@@ -104,6 +104,28 @@ def test_conv_kg_words(tw):
         assert np.array_equal(tw.gpu.export_words(t_out), c_out)
 
 
+def test_conv_kg_long_second_perm_words(tw):
+    """A second-Perm of 39 rotations: the engine splits the group's key MACs into chunks (k_ks_mac
+    slices + k_fold_groups); words == oracle."""
+    n = tw.bfv.n
+    if n < 256:
+        pytest.skip("needs 40 distinct band steps")
+    band = n // 64
+    c_n, k, n_ib, n_obp = 40, 2, 1, 1
+    tap_steps = [0, 1]
+    tw.keys_for(tap_steps + [d * band for d in range(1, c_n)])
+    xs = [tw.encrypt(tw.slots()) for _ in range(n_ib)]
+    pts = tw.slots(n_obp * n_ib * c_n * k).reshape(n_obp, n_ib, c_n, k, tw.N)
+    import torch
+
+    g_in = torch.stack([g for g, _ in xs])
+    c_in = np.stack([c for _, c in xs])
+    d_pts = tw.gpu.encode_plain(pts.reshape(-1, tw.N)).view(n_obp, n_ib, c_n, k, tw.L, tw.N)
+    g_out = tw.gpu.conv_kg(g_in, d_pts, tap_steps, band)
+    c_out = tw.cpu.conv_kg(c_in, pts, tap_steps, band)
+    assert np.array_equal(tw.gpu.export_words(g_out), c_out)
+
+
 def test_mv_gala_batch_words(tw):
     """Batched entry point == per-input fused calls == oracle."""
     import torch
