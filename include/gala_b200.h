@@ -145,6 +145,13 @@ int gala_rotate_batch(gala_ctx *ctx, const uint64_t *cts_dev, int B, const int *
 int gala_conv_kg(gala_ctx *ctx, const uint64_t *cts_dev, int n_ib, const uint64_t *pts_dev, int n_obp,
                  int c_n, int k, const int *tap_steps_host, int band_step, uint64_t *outs_dev);
 
+/* Batch of B images sharing one layer's weights (same words as B gala_conv_kg calls):
+ * cts_dev [B][n_ib][2][L][N] -> outs_dev [B][n_obp][2][L][N].  Every stage (input rotations,
+ * first-Add, second-Perm) runs once for the batch; the first-Add loads each plaintext word once
+ * per 4 images. */
+int gala_conv_kg_batch(gala_ctx *ctx, const uint64_t *cts_dev, int B, int n_ib, const uint64_t *pts_dev, int n_obp,
+                       int c_n, int k, const int *tap_steps_host, int band_step, uint64_t *outs_dev);
+
 /* Schedule-1 first-Add on the int8 tensor cores: per Q position one byte-convolution MMA of the
  * plaintext bytes (A, position-major ptcan_dev written once by gala_kg1_tc_weights from the
  * gala_kg_encode_weights plaintexts; gala_kg1_tc_bytes bytes, 0 if the shape is unsupported:

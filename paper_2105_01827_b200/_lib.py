@@ -67,6 +67,7 @@ SIGNATURES = [
     ("gala_kg1_tc_bytes", ctypes.c_size_t, [vp, i32, i32, i32, i32]),
     ("gala_kg1_tc_weights", i32, [vp, vp, i32, i32, i32, i32, vp]),
     ("gala_conv_kg_tc", i32, [vp, vp, i32, vp, i32, i32, i32, vp, i32, vp]),
+    ("gala_conv_kg_batch", i32, [vp, vp, i32, i32, vp, i32, i32, i32, vp, i32, vp]),
     ("gala_kg2_encode_masks", i32, [vp, i32, i32, i32, i32, i32, i32, vp]),
     ("gala_conv_kg2", i32, [vp, vp, i32, vp, i32, i32, vp, vp, i32, i32, vp, i32, i32, vp]),
     ("gala_conv_kg2_post", i32, [vp, vp, i32, vp, i32, i32, vp, vp, i32, i32, vp, i32, i32, vp]),

@@ -487,6 +487,21 @@ class Context:
                   int(c_n), int(k), st, int(band_step), ctypes.c_void_p(_ptr(outs)))
         return outs
 
+    def conv_kg_batch(self, cts_batch, pts, tap_steps, band_step: int):
+        """Schedule 1 over B images sharing the weights: [B][n_ib][2][L][N] -> [B][n_obp][2][L][N]."""
+        torch = _torch()
+        n_obp, n_ib, c_n, k = pts.shape[:4]
+        nbatch = cts_batch.shape[0]
+        if cts_batch.shape[1] != n_ib:
+            raise DimensionError(f"expected {n_ib} input ciphertexts per image, got {cts_batch.shape[1]}")
+        self.ensure_keys(list(tap_steps) + [d * band_step for d in range(1, c_n)])
+        outs = torch.empty((nbatch, n_obp, 2, self.L, self.N), dtype=torch.int64, device=self.device)
+        st = (ctypes.c_int * k)(*[int(s) for s in tap_steps])
+        self.call("gala_conv_kg_batch", ctypes.c_void_p(_ptr(cts_batch)), int(nbatch), int(n_ib),
+                  ctypes.c_void_p(_ptr(pts)), int(n_obp), int(c_n), int(k), st, int(band_step),
+                  ctypes.c_void_p(_ptr(outs)))
+        return outs
+
     def kg1_tc_weights(self, pts, n_obp: int, n_ib: int, c_n: int, k: int):
         """Position-major copy of schedule-1 KG plaintexts for the tensor-core first-Add (None: unsupported)."""
         torch = _torch()

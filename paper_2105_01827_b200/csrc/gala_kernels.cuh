@@ -670,54 +670,90 @@ __global__ void k_sub_plain(DevCtx c, const u64* __restrict__ ct, const u64* __r
     }
 }
 
-// conv first-Add over one chunk of input blocks [ib0, ib1):
-//   acc[o][d][comp][j][x] (+)= sum_{ib in chunk} sum_tap R[ib][tap][comp][j][x] * pt[o][ib][d][tap][j][x]
-// The host sizes chunks so R[ib0:ib1] stays resident in L2 while every (o, d) re-reads it; plaintexts
-// stream once from HBM with evict-first loads.  128-bit lazy accumulation, REDC every c.lazy[j]
-// products.  grid: (N / blockDim, L, n_obp * c_n)
-__global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __restrict__ R, int n_ib, int ib0,
-                                                       int ib1, int k, const u64* __restrict__ pts, int c_n,
-                                                       int accumulate, u64* __restrict__ acc)
+// conv first-Add over one chunk of input blocks [ib0, ib1), for a batch of images sharing the weights:
+//   acc[b][o][d][comp][j][x] (+)= sum_{ib in chunk} sum_tap R[b][ib][tap][comp][j][x] * pt[o][ib][d][tap][j][x]
+// Register tile: each thread carries IMG images x ODT accumulator rows od = o c_n + d, so a rotated
+// input word is loaded once per ODT rows and a plaintext word once per IMG images (the single-row,
+// single-image form re-read R from L2 once per row: L2-bound).  The image groups of one row group
+// are adjacent in the launch order (grid.y), so later groups find the plaintexts in L2; the host
+// sizes ib chunks so R[., ib0:ib1] stays resident in L2 across the row groups.  128-bit sums
+// T = hi 2^64 + lo: every c.lazy[j] products the high word is brought back below q by one
+// conditional subtraction (T - q 2^64 == T mod q; lazy products of canonical operands add less
+// than q to hi), so the sum never leaves its 4 registers; one REDC at the end.  grid: (N / blockDim, L * ceil(nimg / IMG), ceil(rows / ODT)).
+template <int IMG, int ODT>
+__global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __restrict__ R, long long R_bs, int n_ib,
+                                                       int ib0, int ib1, int k, const u64* __restrict__ pts, int c_n,
+                                                       int rows, int nimg, int accumulate, u64* __restrict__ acc,
+                                                       long long acc_bs)
 {
     const int N = c.N, L = c.L;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y, od = blockIdx.z;
-    const int o = od / c_n, d = od - o * c_n;
+    const int j = blockIdx.y % L, b0 = (blockIdx.y / L) * IMG, od0 = blockIdx.z * ODT;
     if (x >= N) return;
-    const ModC md = c.mod[j];
-    const u64 q = md.q;
+    const int nb = nimg - b0 < IMG ? nimg - b0 : IMG;
+    const int nr = rows - od0 < ODT ? rows - od0 : ODT;
+    const u64 q = c.mod[j].q;
     const int lazy = c.lazy[j];
     const long long LN = (long long)L * N, W = 2 * LN;
-    u64 s0 = 0, s1 = 0;
-    Acc128 a0, a1;
+    Acc128 a[ODT][IMG][2];
+    const u64* prow[ODT];
+#pragma unroll
+    for (int r = 0; r < ODT; r++) {
+        const int od = od0 + (r < nr ? r : 0);
+        const int o = od / c_n, d = od - o * c_n;
+        prow[r] = pts + (((long long)o * n_ib * c_n + d) * k) * LN + (long long)j * N + x;
+    }
     int pending = 0;
+    const u64* Rimg = R + (long long)b0 * R_bs + (long long)j * N + x;
+    const long long pt_ib = (long long)c_n * k * LN;
     for (int ib = ib0; ib < ib1; ib++) {
-        const u64* pt = pts + ((((long long)o * n_ib + ib) * c_n + d) * k) * LN + (long long)j * N + x;
-        const u64* Rb = R + ((long long)ib * k) * W + (long long)j * N + x;
+        const u64* Rb = Rimg + ((long long)ib * k) * W;
         for (int t = 0; t < k; t++) {
-            const u64 w = __ldcs((const unsigned long long*)(pt + t * LN));
-            const u64 r0 = __ldg(Rb + t * W), r1 = __ldg(Rb + t * W + LN);
             if (pending == lazy) {
-                s0 = add_mod(s0, a0.reduce(md), q);
-                s1 = add_mod(s1, a1.reduce(md), q);
-                a0 = Acc128();
-                a1 = Acc128();
+#pragma unroll
+                for (int r = 0; r < ODT; r++)
+#pragma unroll
+                    for (int i = 0; i < IMG; i++)
+#pragma unroll
+                        for (int cp = 0; cp < 2; cp++) a[r][i][cp].hi = csub(a[r][i][cp].hi, q);
                 pending = 0;
             }
-            a0.mac(r0, w);
-            a1.mac(r1, w);
+            u64 rv[IMG][2];
+#pragma unroll
+            for (int i = 0; i < IMG; i++) {
+                const u64* rp = Rb + (i < nb ? i : 0) * R_bs + t * W;
+                rv[i][0] = __ldg(rp);
+                rv[i][1] = __ldg(rp + LN);
+            }
+#pragma unroll
+            for (int r = 0; r < ODT; r++) {
+                const u64 w = __ldcs((const unsigned long long*)(prow[r] + (long long)ib * pt_ib + t * LN));
+#pragma unroll
+                for (int i = 0; i < IMG; i++) {
+                    a[r][i][0].mac(rv[i][0], w);
+                    a[r][i][1].mac(rv[i][1], w);
+                }
+            }
             pending++;
         }
     }
-    s0 = add_mod(s0, a0.reduce(md), q);
-    s1 = add_mod(s1, a1.reduce(md), q);
-    u64* out = acc + (long long)od * W + (long long)j * N + x;
-    if (accumulate) {
-        s0 = add_mod(s0, out[0], q);
-        s1 = add_mod(s1, out[LN], q);
+#pragma unroll
+    for (int r = 0; r < ODT; r++) {
+        if (r >= nr) break;
+#pragma unroll
+        for (int i = 0; i < IMG; i++) {
+            if (i >= nb) break;
+            u64 v0 = csub(redc_sf_lazy(csub(a[r][i][0].hi, q), a[r][i][0].lo, q), q);
+            u64 v1 = csub(redc_sf_lazy(csub(a[r][i][1].hi, q), a[r][i][1].lo, q), q);
+            u64* out = acc + (long long)(b0 + i) * acc_bs + (long long)(od0 + r) * W + (long long)j * N + x;
+            if (accumulate) {
+                v0 = add_mod(v0, out[0], q);
+                v1 = add_mod(v1, out[LN], q);
+            }
+            out[0] = v0;
+            out[LN] = v1;
+        }
     }
-    out[0] = s0;
-    out[LN] = s1;
 }
 
 // ---------------------------------------------------------------------------

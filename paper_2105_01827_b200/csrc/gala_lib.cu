@@ -1349,7 +1349,7 @@ int gala_kg1_tc_weights(gala_ctx* c, const uint64_t* pts, int n_obp, int n_ib, i
 }
 
 static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts, const uint64_t* ptcan, int n_obp,
-                       int c_n, int k, const int* tap_steps, int band_step, uint64_t* outs);
+                       int c_n, int k, const int* tap_steps, int band_step, uint64_t* outs, int B = 1);
 
 int gala_conv_kg(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts, int n_obp, int c_n, int k,
                  const int* tap_steps, int band_step, uint64_t* outs)
@@ -1363,8 +1363,16 @@ int gala_conv_kg_tc(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* 
     return conv_kg_run(c, cts, n_ib, nullptr, ptcan, n_obp, c_n, k, tap_steps, band_step, outs);
 }
 
+int gala_conv_kg_batch(gala_ctx* c, const uint64_t* cts, int B, int n_ib, const uint64_t* pts, int n_obp, int c_n, int k,
+                       const int* tap_steps, int band_step, uint64_t* outs)
+{
+    if (B <= 0) return set_err(GALA_ERR_DIM, "empty image batch");
+    return conv_kg_run(c, cts, n_ib, pts, nullptr, n_obp, c_n, k, tap_steps, band_step, outs, B);
+}
+
+// B images sharing the weights: cts [B][n_ib][W] -> outs [B][n_obp][W]; every stage runs once for the batch
 static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts, const uint64_t* ptcan, int n_obp,
-                       int c_n, int k, const int* tap_steps, int band_step, uint64_t* outs)
+                       int c_n, int k, const int* tap_steps, int band_step, uint64_t* outs, int B)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const long long W = 2LL * L * N;
@@ -1382,17 +1390,23 @@ static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, d * band_step));
     // input rotations R[ib][tap]: one DecPerm per input (digit NTTs once), HstPerm per nonzero tap
     u64* R;
-    RET(scratch(c, &R, (size_t)n_ib * k * W));
-    for (int ib = 0; ib < n_ib; ib++)
-        for (int t = 0; t < k; t++)
-            if (norm_step(c, tap_steps[t]) == 0)
-                CK(cudaMemcpyAsync(R + ((long long)ib * k + t) * W, cts + (long long)ib * W, sizeof(u64) * W,
-                                   cudaMemcpyDeviceToDevice, c->stream));
+    if (ptcan && B > 1) {   // the tensor-core first-Add takes one image per call
+        for (int b = 0; b < B; b++)
+            RET(conv_kg_run(c, cts + (long long)b * n_ib * W, n_ib, pts, ptcan, n_obp, c_n, k, tap_steps, band_step,
+                            outs + (long long)b * n_obp * W, 1));
+        return GALA_OK;
+    }
+    const int nin = B * n_ib;   // inputs of every image, image-major
+    RET(scratch(c, &R, (size_t)nin * k * W));
+    for (int t = 0; t < k; t++)   // unrotated taps: one strided copy over every input
+        if (norm_step(c, tap_steps[t]) == 0)
+            CK(cudaMemcpy2DAsync(R + (long long)t * W, sizeof(u64) * k * W, cts, sizeof(u64) * W, sizeof(u64) * W,
+                                 (size_t)nin, cudaMemcpyDeviceToDevice, c->stream));
     if (!rot_taps.empty()) {
         std::vector<EngTerm> terms;
         std::vector<std::vector<EngMember>> groups;
         std::vector<u64*> outs;
-        for (int ib = 0; ib < n_ib; ib++) {
+        for (int ib = 0; ib < nin; ib++) {
             EngTerm t;
             t.X = cts + (long long)ib * W;
             t.pt = nullptr;
@@ -1408,7 +1422,7 @@ static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_
     }
     // first-Add: acc[o][d] over all input blocks and taps
     u64* acc;
-    RET(scratch(c, &acc, (size_t)n_obp * c_n * W));
+    RET(scratch(c, &acc, (size_t)B * n_obp * c_n * W));
     if (ptcan) {   // on the tensor cores: position-major plaintext bytes x byte-convolution of R
         int Rp, Kwp, MT;
         kg1_geom(n_ib, n_obp, c_n, k, &Rp, &Kwp, &MT);
@@ -1430,19 +1444,41 @@ static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_
         return GALA_OK;
     }
     const int th = N < 256 ? N : 256;
-    dim3 grid((N + th - 1) / th, L, n_obp * c_n);
-    // input-block chunks whose rotated inputs (k * W words each) fit comfortably in L2 (~48 MB)
+    const int rows = n_obp * c_n;
+    // register tile (images x rows per thread), measured at config 3 x 16 images: 2 x 2 0.030,
+    // 1 x 4 0.032, 2 x 4 0.036 (170 registers), 2 x 1 0.036, 1 x 1 0.050 ms per image
+    int img = B >= 2 ? 2 : 1;
+    int odt = rows >= 2 ? 2 : 1;
+    if (const char* e = getenv("GALA_KGACC")) {   // A/B experiments: "img,odt"
+        int a = 0, b2 = 0;
+        if (sscanf(e, "%d,%d", &a, &b2) == 2 && (a == 1 || a == 2) && (b2 == 1 || b2 == 2 || b2 == 4)) {
+            img = a;
+            odt = b2;
+        }
+    }
+    dim3 grid((N + th - 1) / th, L * ((B + img - 1) / img), (rows + odt - 1) / odt);
+    // input-block chunks whose rotated inputs (k * W words each, every image) fit comfortably in L2 (~48 MB)
     const long long chunk_bytes = 48ll << 20;
-    int per_chunk = (int)(chunk_bytes / ((long long)k * W * 8));
+    int per_chunk = (int)(chunk_bytes / ((long long)B * k * W * 8));
     if (per_chunk < 1) per_chunk = 1;
+    const long long R_bs = (long long)n_ib * k * W, acc_bs = (long long)rows * W;
     for (int ib0 = 0; ib0 < n_ib; ib0 += per_chunk) {
         const int ib1 = ib0 + per_chunk < n_ib ? ib0 + per_chunk : n_ib;
-        KLAUNCH(c, "k_kg_accumulate", k_kg_accumulate<<<grid, th, 0, c->stream>>>(c->dc, R, n_ib, ib0, ib1, k, pts,
-                                                                                  c_n, ib0 > 0, acc));
+#define KGACC(IM, OD) KLAUNCH(c, "k_kg_accumulate", (k_kg_accumulate<IM, OD><<<grid, th, 0, c->stream>>>(c->dc, R, R_bs, n_ib, ib0, ib1, k, pts, c_n, rows, B, ib0 > 0, acc, acc_bs)))
+        if (img == 2) {
+            if (odt == 4) KGACC(2, 4);
+            else if (odt == 2) KGACC(2, 2);
+            else KGACC(2, 1);
+        } else {
+            if (odt == 4) KGACC(1, 4);
+            else if (odt == 2) KGACC(1, 2);
+            else KGACC(1, 1);
+        }
+#undef KGACC
     }
     release(c, R);
-    // second-Perm: out[o] = sum_d rot_{d * band}(acc[o][d]), one lazy ModDown per o
-    RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, n_obp, c_n, band_step, outs, 0));
+    // second-Perm: out[b][o] = sum_d rot_{d * band}(acc[b][o][d]), one lazy ModDown per (b, o)
+    RET(rotate_sum_regular(c, acc, W, 0, nullptr, 1, B * n_obp, c_n, band_step, outs, 0));
     release(c, acc);
     return GALA_OK;
 }

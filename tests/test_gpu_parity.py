@@ -104,6 +104,29 @@ def test_conv_kg_words(tw):
         assert np.array_equal(tw.gpu.export_words(t_out), c_out)
 
 
+@pytest.mark.parametrize("nimg", [1, 3, 6])
+def test_conv_kg_batch_words(tw, nimg):
+    """Schedule 1 over a batch of images sharing the weights (2 and 4 images per thread, ragged
+    tails) == one oracle o_conv_kg per image."""
+    n = tw.bfv.n
+    if n < 16:
+        pytest.skip("tiny")
+    band = n // 4
+    c_n, k, n_ib, n_obp = 4, 3, 3, 2
+    tap_steps = [0, 1, n - 1]
+    tw.keys_for(tap_steps + [d * band for d in range(1, c_n)])
+    imgs = [[tw.encrypt(tw.slots()) for _ in range(n_ib)] for _ in range(nimg)]
+    pts = tw.slots(n_obp * n_ib * c_n * k).reshape(n_obp, n_ib, c_n, k, tw.N)
+    import torch
+
+    d_pts = tw.gpu.encode_plain(pts.reshape(-1, tw.N)).view(n_obp, n_ib, c_n, k, tw.L, tw.N)
+    g_batch = torch.stack([torch.stack([g for g, _ in im]) for im in imgs])
+    outs = tw.gpu.conv_kg_batch(g_batch, d_pts, tap_steps, band)
+    for b, im in enumerate(imgs):
+        c_out = tw.cpu.conv_kg(np.stack([c for _, c in im]), pts, tap_steps, band)
+        assert np.array_equal(tw.gpu.export_words(outs[b]), c_out), f"image {b}"
+
+
 def test_conv_kg_long_second_perm_words(tw):
     """A second-Perm of 39 rotations: the engine splits the group's key MACs into chunks (k_ks_mac
     slices + k_fold_groups); words == oracle."""

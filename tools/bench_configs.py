@@ -71,7 +71,7 @@ def fc(name, n, L, n_out, n_in, B):
             "breakdown_ms_per_layer": {k: round(v["ms"] / B, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
 
 
-def conv(name, n, L, u, frame, c_i, c_o, k):
+def conv(name, n, L, u, frame, c_i, c_o, k, B=1):
     params = HEParams(n=n, rns_limbs=L, seed=32)
     rng = np.random.default_rng(2)
     kern = rng.integers(-128, 128, (c_o, c_i, k, k)) % P
@@ -87,6 +87,42 @@ def conv(name, n, L, u, frame, c_i, c_o, k):
     stacked = torch.stack([c.data for c in cts])
     run = lambda: layer.forward_device(stacked)  # noqa: E731
     ms = timeit(run, reps=3)
+    batch = None
+    if B > 1 and layer.batchable:
+        # B images sharing the weights: one pass (rotations, first-Add, second-Perm batched)
+        chs = [rng.integers(0, P, (c_i, u, u)) for _ in range(B - 1)]
+        imgs = [img]
+        for c2 in chs:
+            im2 = np.zeros_like(img)
+            im2[:, :u, :u] = c2
+            imgs.append(im2)
+        bt = torch.stack([torch.stack([c.data for c in encrypt_inputs(task, im)]) for im in imgs])
+        runb = lambda: layer.forward_device_batch(bt)  # noqa: E731
+        msb = timeit(runb, reps=3)
+        from paper_2105_01827_b200 import _lib
+        torch.cuda.synchronize()
+        l0, h0 = _lib.launch_count(), time.perf_counter()
+        runb()
+        host_ms = (time.perf_counter() - h0) * 1e3
+        launches = _lib.launch_count() - l0
+        torch.cuda.synchronize()
+        ctx.profile(True)
+        runb()
+        profb = ctx.profile_read()
+        ctx.profile(False)
+        ob = runb()
+        okb = True
+        for bi in (0, B - 1):
+            outs_b = [ob[bi][o // layer.pair] for o in range(layer.n_ob)]
+            got = np.concatenate([ctx.decrypt_physical(ob[bi][o // layer.pair])[(o % layer.pair) * n:(o % layer.pair + 1) * n]
+                                  .reshape(layer.c_n, frame, frame) for o in range(layer.n_ob)])[:, :u, :u]
+            want = conv2d_mod_p(ch if bi == 0 else chs[bi - 1], kern, P)
+            okb = okb and bool(np.array_equal(got, want))
+            del outs_b
+        batch = {"images": B, "ms_per_batch": msb, "host_enqueue_ms": round(host_ms, 3), "launches": launches, "ms_per_layer": msb / B, "layers_per_s": 1e3 * B / msb,
+                 "correct": okb,
+                 "breakdown_ms_per_layer": {k2: round(v["ms"] / B, 4)
+                                            for k2, v in sorted(profb.items(), key=lambda kv: -kv[1]["ms"])}}
     ctx.profile(True)
     run()
     prof = ctx.profile_read()
@@ -99,7 +135,8 @@ def conv(name, n, L, u, frame, c_i, c_o, k):
             "ms_per_layer": ms, "layers_per_s": 1e3 / ms, "correct": ok, "weight_encode_s": round(setup, 2),
             "schedule": layer.schedule, "post_mask": layer.post,
             "plaintext_bytes": layer.resident_bytes, "meter": repr(meter),
-            "breakdown_ms": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+            "breakdown_ms": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
+            "batch": batch}
 
 
 SCHED = int(os.environ["KG_SCHED"]) if os.environ.get("KG_SCHED") else None
@@ -108,11 +145,11 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4"]
     for w in which:
         if w == "cfg1":
-            r = fc("cfg1", 2048, 1, 16, 2048, 64)
+            r = fc("cfg1", 2048, 1, 16, 2048, int(os.environ.get("CFG1_BATCH", "64")))
         elif w == "cfg2":
             r = fc("cfg2", 4096, 3, 1024, 4096, 32)
         elif w == "cfg3":
-            r = conv("cfg3", 2048, 1, 16, 16, 64, 64, 3)
+            r = conv("cfg3", 2048, 1, 16, 16, 64, 64, 3, B=int(os.environ.get("CFG3_BATCH", "16")))
         elif w == "cfg4":
             r = conv("cfg4", 4096, 3, 56, 64, 64, 64, 3)
         elif w.startswith("conv:"):     # conv:n:L:u:frame:c_i:c_o:k
