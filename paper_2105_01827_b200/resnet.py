@@ -193,25 +193,28 @@ class FCLayer:
 class ResNet18Linear:
     """All ResNet-18 linear layers with resident encoded weights on one GPU."""
 
-    def __init__(self, params: HEParams | None = None, seed: int = 2105, layers=None):
+    def __init__(self, params: HEParams | None = None, seed: int = 2105, layers=None, only=None):
+        """``only``: indices of the layers this process serves (multi-GPU layer partition,
+        `sharding.partition_layers`); the others get weights drawn (same stream) but no GPU state."""
         self.params = params or HEParams(n=4096, rns_limbs=3, seed=5)
         self.specs = layers or resnet18_224()
         rng = np.random.default_rng(seed)
         p = self.params.p
+        keep = set(range(len(self.specs))) if only is None else set(only)
         self.weights, self.layers = [], []
-        for spec in self.specs:
+        for i, spec in enumerate(self.specs):
             if spec.kind == "fc":
                 w = rng.integers(-128, 128, (spec.c_out, spec.c_in)) % p
-                self.layers.append(FCLayer(spec, w, self.params))
+                self.layers.append(FCLayer(spec, w, self.params) if i in keep else None)
             else:
                 w = rng.integers(-128, 128, (spec.c_out, spec.c_in, spec.k, spec.k)) % p
-                self.layers.append(ConvLayer(spec, w, self.params))
+                self.layers.append(ConvLayer(spec, w, self.params) if i in keep else None)
             self.weights.append(w)
         self.ctx = context(self.params)
 
     @property
     def plaintext_bytes(self) -> int:
-        return sum(l.plaintext_bytes for l in self.layers)
+        return sum(l.plaintext_bytes for l in self.layers if l is not None)
 
     def random_input(self, i: int, rng) -> np.ndarray:
         spec = self.specs[i]
@@ -219,3 +222,14 @@ class ResNet18Linear:
         if spec.kind == "fc":
             return rng.integers(0, p, spec.c_in)
         return rng.integers(0, p, (spec.c_in, spec.size, spec.size))
+
+
+def layer_costs(specs, measured: dict | None = None) -> list[float]:
+    """Per-layer cost estimates for the multi-GPU layer partition: measured ms per layer name
+    where known (e.g. `profiles/r1_resnet18_224.jsonl`), else the plaintext MAC count
+    c_in c_out k^2 s^2 / stride^2 scaled to the same unit."""
+    measured = measured or {}
+    macs = [sp.c_in * sp.c_out * sp.k * sp.k * sp.out_size * sp.out_size for sp in specs]
+    known = [(measured[sp.name], m) for sp, m in zip(specs, macs) if sp.name in measured]
+    scale = sum(ms for ms, _ in known) / max(1, sum(m for _, m in known)) if known else 1.0
+    return [float(measured.get(sp.name, m * scale)) for sp, m in zip(specs, macs)]

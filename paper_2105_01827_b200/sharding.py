@@ -1,12 +1,29 @@
-"""Multi-GPU partitioning of independent GALA layer invocations.
+"""Multi-GPU partitioning of independent GALA ciphertext work.
 
-The GALA dot product has no cross-ciphertext exchange step: independent
-inputs (and independent output-channel groups of a convolution) are
-partitioned across ranks, one process per GPU, with no data-path collective
-("replicas", weak scaling).  The only collectives are control-plane: the
-max-over-ranks of the timed region and gathering small per-rank results.
+The GALA linear layers have no cross-ciphertext exchange inside a layer's output
+blocks: each output ciphertext of a kernel-grouping convolution depends only on
+the (shared) input ciphertexts and its own block of kernels (`conv.py:268-293`),
+and independent layers / inputs share nothing at all.  So work is partitioned
+across ranks, one process per GPU:
+
+* **inputs / layers** (configs 1, 2, 5): replicas, or a cost-balanced assignment
+  of whole layers to ranks (`partition_layers`); no data-path collective;
+* **output blocks of one convolution** (configs 3, 4, 5): `ShardedKernelGroupingConv`
+  broadcasts the input ciphertexts from the source rank, every rank runs the fused
+  layer on its contiguous range of physical output ciphertexts, and only the final
+  output ciphertexts are gathered to the destination rank (NCCL over NVLink on
+  GPUs, gloo on CPU).  The words of every output block equal the single-GPU
+  layer's words for that block: the sub-layer is the same computation restricted
+  to its kernels (`tests/test_multiprocess.py`).
+
+The control-plane collectives are the max-over-ranks of the timed region and small
+per-rank result objects.
 """
 from __future__ import annotations
+
+import heapq
+
+import numpy as np
 
 
 def shard_range(n_items: int, world: int, rank: int) -> range:
@@ -18,12 +35,45 @@ def shard_range(n_items: int, world: int, rank: int) -> range:
     return range(lo, lo + base + (1 if rank < extra else 0))
 
 
+def partition_layers(costs, world: int) -> list[list[int]]:
+    """Longest-processing-time assignment of independent layers to `world` ranks.
+
+    Returns, per rank, the layer indices in ascending order.  Deterministic (ties by
+    index), so every rank computes the same assignment without communicating.
+    """
+    if world <= 0:
+        raise ValueError("bad world")
+    order = sorted(range(len(costs)), key=lambda i: (-float(costs[i]), i))
+    heap = [(0.0, r) for r in range(world)]
+    out: list[list[int]] = [[] for _ in range(world)]
+    for i in order:
+        load, r = heapq.heappop(heap)
+        out[r].append(i)
+        heapq.heappush(heap, (load + float(costs[i]), r))
+    return [sorted(v) for v in out]
+
+
+def _dist():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist
+    return None
+
+
+def world_rank(group=None) -> tuple[int, int]:
+    dist = _dist()
+    if dist is None:
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Maximum of a per-rank scalar (elapsed time) across the process group."""
     import torch
-    import torch.distributed as dist
 
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    dist = _dist()
+    if dist is None or dist.get_world_size() == 1:
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -32,10 +82,104 @@ def max_over_ranks(value: float, device=None) -> float:
 
 def gather_objects(obj):
     """All ranks' small result objects (e.g. output shares) on every rank."""
-    import torch.distributed as dist
-
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    dist = _dist()
+    if dist is None or dist.get_world_size() == 1:
         return [obj]
     out = [None] * dist.get_world_size()
     dist.all_gather_object(out, obj)
     return out
+
+
+def gather_blocks(local, sizes, dst: int = 0, group=None):
+    """Gather per-rank ciphertext blocks [n_r][...] to `dst` -> [sum n_r][...] (None elsewhere).
+
+    Blocks are padded to the largest shard so one fixed-size `gather` moves them; only
+    `dst` receives data (the final result ciphertexts).
+    """
+    import torch
+
+    dist = _dist()
+    world, rank = world_rank(group)
+    if dist is None or world == 1:
+        return local
+    m = max(sizes)
+    if local.shape[0] < m:
+        pad = torch.zeros((m - local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        local = torch.cat([local, pad])
+    bufs = [torch.empty_like(local) for _ in range(world)] if rank == dst else None
+    dist.gather(local.contiguous(), bufs, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([b[:n] for b, n in zip(bufs, sizes)])
+
+
+def sub_conv_task(task, obp: range, pair: int):
+    """The ConvTask of physical output ciphertexts `obp` (output channels of blocks
+    pair*obp.start .. pair*obp.stop, each block c_n channels)."""
+    from .conv import ConvTask
+
+    c_n = task.channels_per_ct
+    lo = obp.start * pair * c_n
+    hi = min(task.c_o, obp.stop * pair * c_n)
+    return ConvTask(task.u_w, task.u_h, task.c_i, task.k_w, task.k_h, hi - lo, np.asarray(task.kernels)[lo:hi],
+                    task.params)
+
+
+class ShardedKernelGroupingConv:
+    """`KernelGroupingConv` with its physical output ciphertexts partitioned across ranks.
+
+    Every rank holds the encoded weights of its own output blocks only (HBM per GPU
+    falls with the world size).  `forward_device` takes the physical inputs on the
+    source rank (any tensor of the right shape elsewhere), broadcasts them, runs the
+    local fused layer and gathers the outputs on `dst`.  ``layer_factory(sub_task)``
+    builds the per-rank layer (default `KernelGroupingConv(sub_task, **kw)`).
+    """
+
+    def __init__(self, task, group=None, layer_factory=None, pair_rows: bool = True, **kw):
+        self.task, self.group = task, group
+        self.world, self.rank = world_rank(group)
+        c_n = task.channels_per_ct
+        self.pair = 2 if pair_rows else 1
+        n_ob = task.c_o // c_n
+        self.n_obp = (n_ob + self.pair - 1) // self.pair
+        self.shards = [shard_range(self.n_obp, self.world, r) for r in range(self.world)]
+        self.sizes = [len(s) for s in self.shards]
+        mine = self.shards[self.rank]
+        self.sub_task = sub_conv_task(task, mine, self.pair) if len(mine) else None
+        if layer_factory is None:
+            from .conv import KernelGroupingConv
+
+            def layer_factory(t):
+                return KernelGroupingConv(t, pair_rows=pair_rows, **kw)
+        self.local = layer_factory(self.sub_task) if self.sub_task is not None else None
+
+    def forward_device(self, cts_phys, src: int = 0, dst: int = 0):
+        """[n_ib][2][L][N] on `src` -> [n_obp][2][L][N] on `dst` (None on the other ranks)."""
+        import torch
+
+        dist = _dist()
+        if dist is not None and self.world > 1:
+            cts_phys = cts_phys.contiguous()
+            dist.broadcast(cts_phys, src=src, group=self.group)
+        if self.local is not None:
+            local = self.local.forward_device(cts_phys)
+        else:
+            local = torch.empty((0,) + tuple(cts_phys.shape[1:]), dtype=cts_phys.dtype, device=cts_phys.device)
+        return gather_blocks(local, self.sizes, dst=dst, group=self.group)
+
+    def __call__(self, cts, meter, src: int = 0, dst: int = 0):
+        """Drop-in form of `mimo_kernel_grouping` (conv.py:268-293): logical ciphertexts in
+        on `src`, logical outputs on `dst` (None elsewhere); `dst` books the layer's counts."""
+        import torch
+
+        from .backend import Ciphertext
+        from .conv import _check_mimo, _kg_book_and_noise
+
+        c_n, n_ib, n_ob = _check_mimo(self.task, cts)
+        stacked = torch.stack([c.data for c in cts])
+        outs = self.forward_device(stacked, src=src, dst=dst)
+        if outs is None:
+            return None
+        noises = _kg_book_and_noise(self.task, [c.noise for c in cts], c_n, n_ib, n_ob, meter)
+        return [Ciphertext._wrap(outs[ob // self.pair], noises[ob], self.task.params, ob % self.pair)
+                for ob in range(n_ob)]

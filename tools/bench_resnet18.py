@@ -19,7 +19,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 
-from paper_2105_01827_b200.resnet import ResNet18Linear  # noqa: E402
+from paper_2105_01827_b200.resnet import ResNet18Linear, layer_costs, resnet18_224  # noqa: E402
+from paper_2105_01827_b200.sharding import gather_objects, max_over_ranks, partition_layers  # noqa: E402
 from plain_check import conv2d_mod_p, dot_mod_p  # noqa: E402
 
 
@@ -29,17 +30,43 @@ def plain_layer(spec, x, w, p):
     return conv2d_mod_p(x, w, p, spec.stride)
 
 
+def _measured_costs():
+    path = os.path.join(ROOT, "profiles", "r1_resnet18_224.jsonl")
+    out = {}
+    if os.path.exists(path):
+        for line in open(path):
+            d = json.loads(line)
+            if "layer" in d:
+                out[d["layer"]] = d["ms"]
+    return out
+
+
 def main():
+    """One process per GPU under torchrun: the layers are partitioned across ranks (LPT on the
+    measured per-layer times, `sharding.partition_layers`); each rank holds and runs its own
+    layers.  The pipelined network period is the max over ranks of the per-rank sums."""
     check = "--no-check" not in sys.argv
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    specs = resnet18_224()
+    parts = partition_layers(layer_costs(specs, _measured_costs()), world)
+    mine = parts[rank]
     t0 = time.perf_counter()
-    net = ResNet18Linear()
+    net = ResNet18Linear(only=mine)
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
     ctx = net.ctx
     rng = np.random.default_rng(7)
     total_ms, ok_all = 0.0, True
     for i, (spec, layer) in enumerate(zip(net.specs, net.layers)):
-        x = net.random_input(i, rng)
+        x = net.random_input(i, rng)        # drawn on every rank: the same inputs as one GPU
+        if layer is None:
+            continue
         if spec.kind == "fc":
             cts = layer.encrypt_frames(x)
             masks = layer.layer.draw_masks(11 + i)
@@ -69,11 +96,23 @@ def main():
             ok = bool(np.array_equal(got, plain_layer(spec, x, net.weights[i], net.params.p)))
             res["correct"] = ok
             ok_all &= ok
+        res["rank"] = rank
         print(json.dumps(res), flush=True)
-    print(json.dumps({"summary": "resnet18_224_linear", "layers": len(net.specs), "total_ms": round(total_ms, 2),
-                      "networks_per_s": round(1e3 / total_ms, 3), "all_correct": ok_all if check else None,
-                      "plaintext_GB": round(net.plaintext_bytes / 1e9, 2), "weight_setup_s": round(setup, 1),
-                      "N": ctx.N, "L": ctx.L, "key_MB": round(ctx.key_bytes() / 1e6, 1)}), flush=True)
+    period = max_over_ranks(total_ms, device=torch.device("cuda"))
+    sums = gather_objects((total_ms, ok_all))
+    if rank == 0:
+        print(json.dumps({"summary": "resnet18_224_linear", "layers": len(net.specs), "n_gpus": world,
+                          "partition": parts, "per_rank_ms": [round(t, 2) for t, _ in sums],
+                          "total_ms": round(sum(t for t, _ in sums), 2),
+                          "pipelined_period_ms": round(period, 2),
+                          "networks_per_s": round(1e3 / period, 3),
+                          "all_correct": all(o for _, o in sums) if check else None,
+                          "plaintext_GB_rank0": round(net.plaintext_bytes / 1e9, 2), "weight_setup_s": round(setup, 1),
+                          "N": ctx.N, "L": ctx.L, "key_MB": round(ctx.key_bytes() / 1e6, 1)}), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
