@@ -16,8 +16,8 @@ buf = np.zeros((1024, 16), np.uint64)
 rc = lib.gala_debug_gtc_prof(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_ulonglong)), 1024)
 rows = buf[buf[:, 11] > 0]
 npos = rows[:, 11].astype(float)
-names = ["prod.wait_empty", "mma.wait_tempty", "mma.wait_full", "mma.wait_bfull", "epi.head", "exp.wait_cpasync",
-         "exp.wait_bempty", "exp.work", "epi.wait_tfull", "exp.wait_empty", "total", "positions", "epi.tld", "epi.iter", "epi.loop"]
+names = ["prod.wait_empty", "mma.wait_tempty", "mma.wait_full", "mma.wait_bfull", "epi.head", "exp.wait_full",
+         "exp.wait_bempty", "exp.work", "epi.wait_tfull", "epi.work", "total", "positions", "epi.tld", "epi.iter", "epi.loop"]
 print("rc", rc, "ctas", len(rows), "positions/cta", npos.mean())
 for i, nm in enumerate(names):
     if nm == "-":
