@@ -134,6 +134,16 @@ int gala_mv_gala2_batch_tc_host(gala_ctx *ctx, const uint64_t *cts_host, int B, 
                                 const uint8_t *wcan_dev, int T, int baby, const uint32_t *r_slots_host,
                                 uint64_t *masked_host);
 
+/* Streamed form for serving: S consecutive batches of B inputs from (pinned) host memory, each
+ * batch through the fused layer as gala_mv_gala2_batch_tc_host (wcan_dev may be NULL: CUDA-core
+ * schedule 2), with the host<->device copies overlapped with the layers -- batch s + 1 is copied in
+ * and batch s - 1 copied out while batch s computes.  Returns when all S batches' masked words are in
+ * masked_host.  cts_host [S][B][2][L][N], r_slots_host [S][B][N], masked_host [S][B][2][L][N];
+ * same words as S separate host calls. */
+int gala_mv_gala2_stream_host(gala_ctx *ctx, const uint64_t *cts_host, int S, int B, const uint64_t *pts2_dev,
+                              const uint8_t *wcan_dev, int T, int baby, const uint32_t *r_slots_host,
+                              uint64_t *masked_host);
+
 /* Batched hoisted rotations (the raw key-switch throughput probe; he_decperm + he_hstperm,
  * backend.py:279-294, for many inputs at once): cts_dev [B][2][L][N], steps_host [S] (non-zero),
  * outs_dev [B][S][2][L][N]; each output equals gala_rotate(input, step). */

@@ -64,6 +64,7 @@ SIGNATURES = [
     ("gala_fc_tc_weights", i32, [vp, vp, i32, i32, vp]),
     ("gala_mv_gala2_batch_tc", i32, [vp, vp, i32, vp, vp, i32, i32, vp, vp, vp]),
     ("gala_mv_gala2_batch_tc_host", i32, [vp, vp, i32, vp, vp, i32, i32, vp, vp]),
+    ("gala_mv_gala2_stream_host", i32, [vp, vp, i32, i32, vp, vp, i32, i32, vp, vp]),
     ("gala_kg1_tc_bytes", ctypes.c_size_t, [vp, i32, i32, i32, i32]),
     ("gala_kg1_tc_weights", i32, [vp, vp, i32, i32, i32, i32, vp]),
     ("gala_conv_kg_tc", i32, [vp, vp, i32, vp, i32, i32, i32, vp, i32, vp]),

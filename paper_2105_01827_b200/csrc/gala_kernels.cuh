@@ -1326,6 +1326,14 @@ __global__ void k_kg_tc_layout_a(const int8_t* __restrict__ A, int rows, int row
     }
 }
 
+// Descriptor upload through the SMs from mapped pinned host memory (zero-copy reads over PCIe): the
+// layers' small tables never queue on the copy engine behind large streamed input / output copies.
+__global__ void k_h2d_copy(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, long long words)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < words; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 // ---------------------------------------------------------------------------
 // GALA schedule 2 on the tensor cores.  Per QP position p = (j, k) the baby-step sums are a small
 // integer matrix product over the baby rotations jj:

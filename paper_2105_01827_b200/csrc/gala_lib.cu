@@ -122,6 +122,9 @@ struct gala_ctx {
     int smem_ntt = 0;         // bytes of one padded polynomial
     cudaStream_t side = nullptr;              // independent work (mask encoding) overlapped with the layer
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // streamed host entry points: copy-in / copy-out streams and per-slot events (created on first use)
+    cudaStream_t cs_in = nullptr, cs_out = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_used[2] = {}, ev_done[2] = {}, ev_d2h[2] = {}, ev_alloc = nullptr;
     std::mutex mu;
     // per-kernel CUDA-event profiling
     bool prof_on = false;
@@ -185,13 +188,20 @@ static int upload(gala_ctx* c, const void* src, size_t bytes, void** dst)
     if (s.done) CK(cudaEventSynchronize(s.done)); // previous upload consumed
     if (bytes > s.cap) {
         if (s.host) cudaFreeHost(s.host);
-        s.cap = bytes < (1 << 16) ? (1 << 16) : bytes;
-        CK(cudaMallocHost(&s.host, s.cap));
+        s.cap = bytes < (1 << 16) ? (1 << 16) : (bytes + 3) / 4 * 4;
+        CK(cudaHostAlloc(&s.host, s.cap, cudaHostAllocMapped));
     }
     if (!s.done) CK(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
     memcpy(s.host, src, bytes);
-    CK(cudaMallocAsync(dst, bytes, c->stream));
-    CK(cudaMemcpyAsync(*dst, s.host, bytes, cudaMemcpyHostToDevice, c->stream));
+    const size_t words = (bytes + 3) / 4;
+    CK(cudaMallocAsync(dst, words * 4, c->stream));
+    // read by the SMs straight from the mapped staging buffer, not by the copy engine: a layer's tables
+    // must not wait behind a streamed batch's 13 MB input copy (gala_mv_gala2_stream_host)
+    void* src_dev = nullptr;
+    CK(cudaHostGetDevicePointer(&src_dev, s.host, 0));
+    const int blocks = (int)((words + 255) / 256 < 32 ? (words + 255) / 256 : 32);
+    k_h2d_copy<<<blocks, 256, 0, c->stream>>>((const uint32_t*)src_dev, (uint32_t*)*dst, (long long)words);
+    CK(cudaGetLastError());
     CK(cudaEventRecord(s.done, c->stream));
     return GALA_OK;
 }
@@ -540,6 +550,15 @@ static void free_ctx(gala_ctx* c)
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    for (cudaStream_t st : {c->cs_in, c->cs_out})
+        if (st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+    for (int i = 0; i < 2; i++)
+        for (cudaEvent_t e : {c->ev_h2d[i], c->ev_used[i], c->ev_done[i], c->ev_d2h[i]})
+            if (e) cudaEventDestroy(e);
+    if (c->ev_alloc) cudaEventDestroy(c->ev_alloc);
     for (auto& r : c->recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -1307,6 +1326,99 @@ int gala_mv_gala2_batch_tc_host(gala_ctx* c, const uint64_t* cts_host, int B, co
                                 int T, int baby, const uint32_t* r_host, uint64_t* masked_host)
 {
     return mv_batch_host(c, 2, cts_host, B, pts2, T, baby, r_host, masked_host, wcan);
+}
+
+// S consecutive batches of B inputs from host memory, the transfers overlapped with the layers: the
+// inputs of batch s + 1 are copied in (cs_in) while batch s computes, and batch s - 1's masked words are
+// copied out (cs_out) -- PCIe is full duplex.  Two staging slots per direction; every batch's H2D and
+// D2H happen inside the call, which returns when the last batch's words are in masked_host.
+// cts_host [S][B][2][L][N] canonical words, r_host [S][B][N], masked_host [S][B][2][L][N].
+static int mv_stream_host(gala_ctx* c, int schedule, const uint64_t* cts_host, int S, int B, const uint64_t* pts,
+                          const uint8_t* wcan, int T, int baby, const uint32_t* r_host, uint64_t* masked_host)
+{
+    if (S <= 0 || B <= 0) return set_err(GALA_ERR_DIM, "empty stream (S=%d, B=%d)", S, B);
+    const int N = c->dc.N, L = c->dc.L;
+    const long long W = 2LL * L * N;
+    if (!c->cs_in) {
+        CK(cudaStreamCreateWithFlags(&c->cs_in, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->cs_out, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; i++)
+            for (cudaEvent_t* e : {&c->ev_h2d[i], &c->ev_used[i], &c->ev_done[i], &c->ev_d2h[i]})
+                CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_alloc, cudaEventDisableTiming));
+    }
+    u64 *hin[2], *hout[2], *ct, *out, *masked;
+    uint32_t* rr[2];
+    for (int i = 0; i < 2; i++) {
+        RET(scratch(c, &hin[i], (size_t)B * W));
+        RET(scratch(c, &hout[i], (size_t)B * W));
+        RET(scratch(c, &rr[i], (size_t)B * N));
+    }
+    RET(scratch(c, &ct, (size_t)B * W));
+    RET(scratch(c, &out, (size_t)B * W));
+    RET(scratch(c, &masked, (size_t)B * W));
+    CK(cudaEventRecord(c->ev_alloc, c->stream));
+    CK(cudaStreamWaitEvent(c->cs_in, c->ev_alloc, 0));
+    CK(cudaStreamWaitEvent(c->cs_out, c->ev_alloc, 0));
+    const char* nc = getenv("GALA_STREAM_NOCOPY");   // experiment: "in", "out" or both skipped
+    const bool noin = nc && strcmp(nc, "out") != 0, noout = nc && strcmp(nc, "in") != 0;
+    // large copies go in 1 MB pieces: the layers' own small descriptor uploads share the copy engine and
+    // would otherwise queue behind a whole 13 MB batch (measured: +0.18 ms per step)
+    auto chunked = [&](void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) -> int {
+        const size_t piece = (size_t)1 << 20;
+        for (size_t o = 0; o < bytes; o += piece)
+            CK(cudaMemcpyAsync((char*)dst + o, (const char*)src + o, bytes - o < piece ? bytes - o : piece, kind, st));
+        return GALA_OK;
+    };
+    auto copy_in = [&](int b) -> int {
+        const int sl = b & 1;
+        if (noin) {
+            CK(cudaEventRecord(c->ev_h2d[sl], c->cs_in));
+            return GALA_OK;
+        }
+        if (b >= 2) CK(cudaStreamWaitEvent(c->cs_in, c->ev_used[sl], 0));   // batch b - 2 consumed the slot
+        RET(chunked(hin[sl], cts_host + (long long)b * B * W, sizeof(u64) * B * W, cudaMemcpyHostToDevice, c->cs_in));
+        CK(cudaMemcpyAsync(rr[sl], r_host + (long long)b * B * N, sizeof(uint32_t) * B * N, cudaMemcpyHostToDevice,
+                           c->cs_in));
+        CK(cudaEventRecord(c->ev_h2d[sl], c->cs_in));
+        return GALA_OK;
+    };
+    RET(copy_in(0));
+    for (int b = 0; b < S; b++) {
+        const int sl = b & 1;
+        if (b + 1 < S) RET(copy_in(b + 1));   // enqueued ahead: overlaps this batch's layers
+        CK(cudaStreamWaitEvent(c->stream, c->ev_h2d[sl], 0));
+        RET(gala_ct_import(c, hin[sl], ct, B));
+        if (schedule == 2) RET(mv2_run(c, ct, B, pts, wcan, T, baby, rr[sl], out, masked));
+        else RET(gala_mv_gala_batch(c, ct, B, pts, T, baby, rr[sl], out, masked));
+        CK(cudaEventRecord(c->ev_used[sl], c->stream));
+        if (b >= 2) CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[sl], 0));   // batch b - 2's words copied out
+        RET(gala_ct_export(c, masked, hout[sl], B));
+        CK(cudaEventRecord(c->ev_done[sl], c->stream));
+        CK(cudaStreamWaitEvent(c->cs_out, c->ev_done[sl], 0));
+        if (!noout)
+            RET(chunked(masked_host + (long long)b * B * W, hout[sl], sizeof(u64) * B * W, cudaMemcpyDeviceToHost,
+                        c->cs_out));
+        CK(cudaEventRecord(c->ev_d2h[sl], c->cs_out));
+    }
+    CK(cudaStreamSynchronize(c->cs_out));
+    CK(cudaStreamSynchronize(c->cs_in));
+    for (int i = 0; i < 2; i++) {
+        release(c, hin[i]);
+        release(c, hout[i]);
+        release(c, rr[i]);
+    }
+    release(c, ct);
+    release(c, out);
+    release(c, masked);
+    CK(cudaStreamSynchronize(c->stream));
+    return GALA_OK;
+}
+
+int gala_mv_gala2_stream_host(gala_ctx* c, const uint64_t* cts_host, int S, int B, const uint64_t* pts2,
+                              const uint8_t* wcan, int T, int baby, const uint32_t* r_host, uint64_t* masked_host)
+{
+    return mv_stream_host(c, 2, cts_host, S, B, pts2, wcan, T, baby, r_host, masked_host);
 }
 
 int gala_mv_gala_host(gala_ctx* c, const uint64_t* ct_host, const uint64_t* pts, int T, int baby,

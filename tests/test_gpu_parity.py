@@ -373,3 +373,36 @@ def test_conv_kg2_post_batch_words(tw):
     for i, im in enumerate(imgs):
         c_out = tw.cpu.conv_kg2(np.stack([c for _, c in im]), kern, u_w, u_h, pair, band_only=True)
         assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
+
+
+@pytest.mark.parametrize("tc", [False, True])
+def test_mv_gala2_stream_host_words(tw, tc):
+    """Streamed host entry point (S batches from host memory, copies overlapped with the layers) ==
+    oracle o_mv_gala2 for every batch, word for word."""
+    import ctypes
+
+    from paper_2105_01827_b200 import _lib
+
+    n = tw.bfv.n
+    T = min(8, n)
+    b, steps = tw.gpu.bsgs_steps(T)
+    if tc and (tw.N % 32 or not tw.gpu.fc_tc_supported(T, b)):
+        pytest.skip("tensor-core path not applicable")
+    tw.keys_for(steps)
+    pts = tw.slots(T)
+    pts2 = tw.gpu.encode_gala_weights(pts, b)
+    wcan = tw.gpu.fc_tc_weights(pts2, T, b) if tc else None
+    S, B = 3, (17 if tc else 2)
+    xs = [[tw.encrypt(tw.slots()) for _ in range(B)] for _ in range(S)]
+    rs = tw.slots(S * B).reshape(S, B, tw.N)
+    host_ct = np.ascontiguousarray(np.stack([np.stack([tw.gpu.export_words(g) for g, _ in batch]) for batch in xs]))
+    host_out = np.zeros_like(host_ct)
+    r = np.ascontiguousarray(rs.astype(np.uint32))
+    _lib.check(tw.gpu.lib.gala_mv_gala2_stream_host(
+        tw.gpu._bind(), ctypes.c_void_p(host_ct.ctypes.data), S, B, ctypes.c_void_p(pts2.data_ptr()),
+        ctypes.c_void_p(wcan.data_ptr() if wcan is not None else None), T, b, ctypes.c_void_p(r.ctypes.data),
+        ctypes.c_void_p(host_out.ctypes.data)))
+    for s in range(S):
+        for i in (0, B - 1):
+            _, c_masked = tw.cpu.mv_gala(xs[s][i][1], pts, rs[s, i], baby=b, schedule=2)
+            assert np.array_equal(host_out[s, i], c_masked), f"batch {s} input {i}"
