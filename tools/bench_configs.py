@@ -22,6 +22,7 @@ from plain_check import conv2d_mod_p, dot_mod_p  # noqa: E402
 from paper_2105_01827_b200 import ConvTask, CostMeter, GalaFC, HEParams, KernelGroupingConv  # noqa: E402
 from paper_2105_01827_b200.conv import encrypt_inputs, unpack_channels  # noqa: E402
 from paper_2105_01827_b200.backend import decrypt  # noqa: E402
+from paper_2105_01827_b200.analytics import survey_conv_roofline, survey_fc_roofline  # noqa: E402
 
 P = 1032193
 dev = torch.device("cuda", 0)
@@ -68,7 +69,8 @@ def fc(name, n, L, n_out, n_in, B):
     return {"config": name, "N": ctx.N, "L": ctx.L, "T": layer.T, "schedule": layer.schedule, "batch": B,
             "ms_per_layer": ms / B,
             "layers_per_s": 1e3 * B / ms, "correct": ok,
-            "breakdown_ms_per_layer": {k: round(v["ms"] / B, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}}
+            "breakdown_ms_per_layer": {k: round(v["ms"] / B, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
+            "roofline": roofline(survey_fc_roofline(ctx.N, ctx.L, layer.T), ms / B, ctx)}
 
 
 def conv(name, n, L, u, frame, c_i, c_o, k, B=1):
@@ -84,6 +86,7 @@ def conv(name, n, L, u, frame, c_i, c_o, k, B=1):
     setup = time.perf_counter() - t0
     ctx = layer.ctx
     cts = encrypt_inputs(task, img)
+    model = survey_conv_roofline(ctx.N, ctx.L, layer.n_ib, layer.n_obp, layer.c_n, layer.k)
     stacked = torch.stack([c.data for c in cts])
     run = lambda: layer.forward_device(stacked)  # noqa: E731
     ms = timeit(run, reps=3)
@@ -119,7 +122,7 @@ def conv(name, n, L, u, frame, c_i, c_o, k, B=1):
             want = conv2d_mod_p(ch if bi == 0 else chs[bi - 1], kern, P)
             okb = okb and bool(np.array_equal(got, want))
             del outs_b
-        batch = {"images": B, "ms_per_batch": msb, "host_enqueue_ms": round(host_ms, 3), "launches": launches, "ms_per_layer": msb / B, "layers_per_s": 1e3 * B / msb,
+        batch = {"roofline": roofline(model, msb / B, ctx), "images": B, "ms_per_batch": msb, "host_enqueue_ms": round(host_ms, 3), "launches": launches, "ms_per_layer": msb / B, "layers_per_s": 1e3 * B / msb,
                  "correct": okb,
                  "breakdown_ms_per_layer": {k2: round(v["ms"] / B, 4)
                                             for k2, v in sorted(profb.items(), key=lambda kv: -kv[1]["ms"])}}
@@ -136,16 +139,33 @@ def conv(name, n, L, u, frame, c_i, c_o, k, B=1):
             "schedule": layer.schedule, "post_mask": layer.post,
             "plaintext_bytes": layer.resident_bytes, "meter": repr(meter),
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
-            "batch": batch}
+            "roofline": roofline(model, ms, ctx), "batch": batch}
 
 
 SCHED = int(os.environ["KG_SCHED"]) if os.environ.get("KG_SCHED") else None
+HBM_PEAK = 6536.0   # GB/s, MEASURED_PEAKS.json (fallback)
+try:
+    HBM_PEAK = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", HBM_PEAK))
+except Exception:
+    pass
+_PEAK_MM = []
+
+
+def roofline(model, ms_per_layer, ctx):
+    """roofline time = max(modmuls / measured modmul peak, bytes / HBM peak)."""
+    if not _PEAK_MM:
+        _PEAK_MM.append(ctx.bench_modmul())
+    t_int = model["modmuls"] / _PEAK_MM[0]
+    t_hbm = model["bytes"] / (HBM_PEAK * 1e9)
+    return {"modmuls": model["modmuls"], "bytes": model["bytes"], "peak_gmodmul_s": round(_PEAK_MM[0] / 1e9, 1),
+            "peak_hbm_gbs": HBM_PEAK, "bound": "int" if t_int >= t_hbm else "hbm",
+            "roofline_us": round(max(t_int, t_hbm) * 1e6, 2), "frac": round(max(t_int, t_hbm) / (ms_per_layer / 1e3), 4)}
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4"]
     for w in which:
         if w == "cfg1":
-            r = fc("cfg1", 2048, 1, 16, 2048, int(os.environ.get("CFG1_BATCH", "64")))
+            r = fc("cfg1", 2048, 1, 16, 2048, int(os.environ.get("CFG1_BATCH", "1024")))
         elif w == "cfg2":
             r = fc("cfg2", 4096, 3, 1024, 4096, 32)
         elif w == "cfg3":
