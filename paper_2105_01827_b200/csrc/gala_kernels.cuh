@@ -1545,9 +1545,14 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             for (long long p = p0; p < p1; p++) {
                 GP_WAIT(0, mbar_wait(&empty[s], ph ^ 1));
                 uint8_t* st = sSt + s * GTC_STAGE;
+#ifdef GTC_NO_A   // probe (tools/tc_probe.sh): the MMA runs on stale A tiles
+                (void)st;
+                mbar_arrive(&full[s]);
+#else
                 mbar_expect_tx(&full[s], (uint32_t)GTC_STAGE);
                 for (int kc = 0; kc < 32; kc++)
                     bulk_g2s(st + kc * 1536, Ecan + ((long long)kc * npos + p) * 1536, 1536, &full[s]);
+#endif
                 if (++s == GTC_NST) {
                     s = 0;
                     ph ^= 1;
@@ -1570,10 +1575,13 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t sb = smem_u32(sB + acc * GTC_BB_BYTES);
                 const uint32_t d = tmem + (uint32_t)(acc * 128);
+#ifndef GTC_MMA_REPEAT
+#define GTC_MMA_REPEAT 1   // probe: issue the position's MMAs this many times (MMA throughput)
+#endif
 #pragma unroll 1
-                for (int ks = 0; ks < 16; ks++) {
-                    const uint64_t ad = umma_desc_kmajor(sa + ks * 2 * 1536, 1536, 128);
-                    const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
+                for (int ks = 0; ks < 16 * GTC_MMA_REPEAT; ks++) {
+                    const uint64_t ad = umma_desc_kmajor(sa + (ks & 15) * 2 * 1536, 1536, 128);
+                    const uint64_t bd = umma_desc_kmajor(sb + (ks & 15) * 256, 128, 4096);
                     asm volatile(
                         "{\n\t.reg .pred p;\n\t"
                         "setp.ne.b32 p, %4, 0;\n\t"
@@ -1616,7 +1624,11 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             GP_WAIT(6, mbar_wait(&bempty[b], (uint32_t)(((it >> 1) & 1) ^ 1)));
             GP_MARK(ex0)
             if (et < 8) s_w0[it & 3][et] = w0n;
+#ifdef GTC_NO_B   // probe: no B-tile expansion (MMA on stale B)
+            if (false) {
+#else
             if (act) {
+#endif
                 uint8_t* rowbase = sB + b * GTC_BB_BYTES + (n >> 3) * 4096 + (n & 7) * 16 + kh * 16 * 128;
 #pragma unroll
                 for (int i = 0; i < 16; i++)   // rotations jj = 2 kc, 2 kc + 1 (byte-reversed), kc = 16 kh + i
@@ -1684,6 +1696,13 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
 #pragma unroll
                     for (int t = 0; t < 4; t++) res[pi][t] = mont_mul(xc1, w0[t], md);
                 } else {
+#ifdef GTC_NO_EPI   // probe: accumulator released without reading it
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    res[pi][0] = res[pi][1] = res[pi][2] = res[pi][3] = 0;
+                    continue;
+#endif
                     uint32_t x[32];
                     const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + gh * 64);
 #pragma unroll
