@@ -118,7 +118,11 @@ struct gala_ctx {
     bool has_secret = false;
     std::map<int, u64*> keys; // step -> [L][2][M][N]
     size_t key_bytes = 0;
-    Staging stage;
+    // ring of descriptor staging buffers: an upload waits only for the one GALA_STAGES uploads back, so
+    // the host can enqueue a whole layer (several engine calls) ahead of the GPU
+    static constexpr int GALA_STAGES = 16;
+    Staging stage[GALA_STAGES];
+    int stage_next = 0;
     int smem_ntt = 0;         // bytes of one padded polynomial
     cudaStream_t side = nullptr;              // independent work (mask encoding) overlapped with the layer
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -184,7 +188,8 @@ static void release(gala_ctx* c, void* p)
 // copy a small host table to device via the pinned staging buffer
 static int upload(gala_ctx* c, const void* src, size_t bytes, void** dst)
 {
-    Staging& s = c->stage;
+    Staging& s = c->stage[c->stage_next];
+    c->stage_next = (c->stage_next + 1) % gala_ctx::GALA_STAGES;
     if (s.done) CK(cudaEventSynchronize(s.done)); // previous upload consumed
     if (bytes > s.cap) {
         if (s.host) cudaFreeHost(s.host);
@@ -542,8 +547,10 @@ static void free_ctx(gala_ctx* c)
     if (c->d_S) cudaFree(c->d_S);
     if (c->d_slot_pos) cudaFree(c->d_slot_pos);
     if (c->d_pmod) cudaFree(c->d_pmod);
-    if (c->stage.host) cudaFreeHost(c->stage.host);
-    if (c->stage.done) cudaEventDestroy(c->stage.done);
+    for (Staging& st : c->stage) {
+        if (st.host) cudaFreeHost(st.host);
+        if (st.done) cudaEventDestroy(st.done);
+    }
     if (c->side) {
         cudaStreamSynchronize(c->side);
         cudaStreamDestroy(c->side);
