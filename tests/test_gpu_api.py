@@ -364,3 +364,51 @@ def test_resnet_rules_small():
     fc = FCLayer(spec, w, params)
     masks = fc.layer.draw_masks(3)
     assert np.array_equal(fc.shares(fc.forward_device(fc.encrypt_frames(x), masks), masks), dot_mod_p(w, x, P))
+
+
+def test_kg_schedule1_image_batch():
+    """Schedule 1 over a batch of images sharing the weights (gala_conv_kg_batch) decrypts to
+    conv2d mod p for every image and equals the one-image calls word for word."""
+    import torch
+
+    params = HEParams(n=256, seed=41)
+    rng = np.random.default_rng(8)
+    u, c_i, c_o, k = 8, 8, 8, 3                      # c_n = 4: 2 input cts, 2 output blocks
+    kern = rng.integers(-128, 128, (c_o, c_i, k, k)) % P
+    task = ConvTask(u, u, c_i, k, k, c_o, kern, params)
+    layer = KernelGroupingConv(task, schedule=1, tensor_cores=False)
+    assert layer.batchable
+    imgs = [rng.integers(0, P, (c_i, u, u)) for _ in range(5)]
+    cts = [encrypt_inputs(task, im) for im in imgs]
+    outs = layer.forward_device_batch(torch.stack([torch.stack([c.data for c in cc]) for cc in cts]))
+    ctx = layer.ctx
+    n = params.n
+    for b, im in enumerate(imgs):
+        one = layer.forward_device(torch.stack([c.data for c in cts[b]]))
+        assert np.array_equal(ctx.export_words(outs[b]), ctx.export_words(one))
+        got = np.concatenate([ctx.decrypt_physical(outs[b][ob // 2])[(ob % 2) * n:(ob % 2 + 1) * n]
+                              .reshape(layer.c_n, u, u) for ob in range(layer.n_ob)])
+        assert np.array_equal(got, conv2d_mod_p(im, kern, P))
+
+
+def test_sharded_conv_single_rank_is_the_layer():
+    """ShardedKernelGroupingConv at world size 1 is mimo_kernel_grouping: same words, same counts,
+    same noise (the multi-rank path is covered by the gloo world-2 test)."""
+    from paper_2105_01827_b200.sharding import ShardedKernelGroupingConv
+
+    params = HEParams(n=256, seed=42)
+    rng = np.random.default_rng(9)
+    u, c_i, c_o, k = 8, 8, 12, 3
+    kern = rng.integers(-128, 128, (c_o, c_i, k, k)) % P
+    task = ConvTask(u, u, c_i, k, k, c_o, kern, params)
+    img = rng.integers(0, P, (c_i, u, u))
+    cts = encrypt_inputs(task, img)
+    m1, m2 = CostMeter(), CostMeter()
+    want = mimo_kernel_grouping(task, cts, m1)
+    got = ShardedKernelGroupingConv(task)(cts, m2)
+    assert repr(m1) == repr(m2)
+    for a, b in zip(want, got):
+        assert a.noise == b.noise
+        assert np.array_equal(decrypt(a).slots, decrypt(b).slots)
+    dec = np.concatenate([unpack_channels(decrypt(o), task) for o in got])
+    assert np.array_equal(dec, conv2d_mod_p(img, kern, P))
