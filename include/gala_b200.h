@@ -69,6 +69,11 @@ int gala_encrypt(gala_ctx *ctx, const uint32_t *slots_dev, const uint64_t *a_dev
                  uint64_t *ct_dev);
 /* decrypt (backend.py:237-243); slots_dev [N] */
 int gala_decrypt(gala_ctx *ctx, const uint64_t *ct_dev, uint32_t *slots_dev);
+/* Decrypt and measure the real noise: *noise_frac = max over coefficients of |p v / Q - m|, i.e. the
+ * noise as a fraction of Delta (decryption is exact below 1/2).  The Python decrypt raises
+ * NoiseOverflowError from 1/4 on -- past 1/2 the noise wraps and the slots are silently wrong, so the
+ * check keeps two bits of margin (the reference's mock raises on its own noise recurrence). */
+int gala_decrypt_noise(gala_ctx *ctx, const uint64_t *ct_dev, uint32_t *slots_dev, double *noise_frac);
 /* batch encode of B slot vectors into plaintext operands [B][L][N] */
 int gala_encode_plain(gala_ctx *ctx, const uint32_t *slots_dev, int B, uint64_t *pt_dev);
 

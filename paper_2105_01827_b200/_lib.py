@@ -41,6 +41,7 @@ SIGNATURES = [
     ("gala_key_bytes", szt, [vp]),
     ("gala_encrypt", i32, [vp, vp, vp, vp, vp]),
     ("gala_decrypt", i32, [vp, vp, vp]),
+    ("gala_decrypt_noise", i32, [vp, vp, vp, vp]),
     ("gala_encode_plain", i32, [vp, vp, i32, vp]),
     ("gala_add", i32, [vp, vp, vp, vp]),
     ("gala_scmult", i32, [vp, vp, vp, vp]),

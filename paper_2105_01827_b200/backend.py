@@ -309,10 +309,24 @@ class Context:
                   ctypes.c_void_p(_ptr(d_e)), ctypes.c_void_p(_ptr(ct)))
         return ct
 
-    def decrypt_physical(self, ct) -> np.ndarray:
+    # real-noise guard: decryption is exact while |noise| < Delta / 2; from Delta / 4 on decrypt_physical
+    # raises (past Delta / 2 the noise wraps and the slots would be silently wrong)
+    REAL_NOISE_LIMIT = 0.25
+
+    def decrypt_physical(self, ct, check_noise: bool = True) -> np.ndarray:
+        """Physical slots [N]; with check_noise, raises NoiseOverflowError when the measured noise
+        reaches REAL_NOISE_LIMIT of Delta (gala_decrypt_noise)."""
         torch = _torch()
         out = torch.empty(self.N, dtype=torch.int32, device=self.device)
-        self.call("gala_decrypt", ctypes.c_void_p(_ptr(ct)), ctypes.c_void_p(_ptr(out)))
+        if not check_noise:
+            self.call("gala_decrypt", ctypes.c_void_p(_ptr(ct)), ctypes.c_void_p(_ptr(out)))
+            return out.cpu().numpy().view(np.uint32).astype(np.int64)
+        frac = ctypes.c_double(0.0)
+        self.call("gala_decrypt_noise", ctypes.c_void_p(_ptr(ct)), ctypes.c_void_p(_ptr(out)), ctypes.byref(frac))
+        self.last_noise_frac = float(frac.value)
+        if frac.value >= self.REAL_NOISE_LIMIT:
+            raise NoiseOverflowError(f"measured noise {frac.value:.3f} Delta reached the {self.REAL_NOISE_LIMIT} Delta "
+                                     "limit (the parameters have no budget left for this circuit; use more primes)")
         return out.cpu().numpy().view(np.uint32).astype(np.int64)
 
     def export_words(self, ct) -> np.ndarray:
@@ -627,7 +641,7 @@ class Ciphertext:
     @property
     def payload(self) -> SlotVector:
         """Decrypted logical slots (debug/test accessor; no noise check)."""
-        full = self.ctx.decrypt_physical(self.data)
+        full = self.ctx.decrypt_physical(self.data, check_noise=False)
         n = self.params.n
         return SlotVector._wrap(full[self.row * n:(self.row + 1) * n].copy(), self.params.p)
 
@@ -679,9 +693,13 @@ def encrypt(x: SlotVector, params: HEParams) -> Ciphertext:
 
 
 def decrypt(c: Ciphertext) -> SlotVector:
+    """backend.py:237-243: raises NoiseOverflowError where the reference's mock noise reaches its
+    budget -- and, on real ciphertexts, where the measured noise reaches a quarter of Delta."""
     if c.noise >= c.params.noise_budget:
         raise NoiseOverflowError(f"noise {c.noise:g} reached budget {c.params.noise_budget:g}")
-    return c.payload
+    full = c.ctx.decrypt_physical(c.data, check_noise=True)
+    n = c.params.n
+    return SlotVector._wrap(full[c.row * n:(c.row + 1) * n].copy(), c.params.p)
 
 
 def he_add(a: Ciphertext, b: Ciphertext, meter: CostMeter) -> Ciphertext:

@@ -2062,12 +2062,16 @@ __device__ __forceinline__ u64 frac64(u64 b, u64 q)
     return qt;
 }
 
-// decrypt phase 2 (one CTA): m = round(p x / Q) mod p via RNS; slots = decode(m)
-__global__ void __launch_bounds__(512, 2) k_dec_phase2(DevCtx c, const u64* __restrict__ x, uint32_t* __restrict__ slots)
+// decrypt phase 2 (one CTA): m = round(p x / Q) mod p via RNS; slots = decode(m).
+// maxd (optional): the largest rounding distance |p x / Q - m| over the coefficients, as a 64-bit
+// fixed-point fraction -- the real noise over Delta (p v / Q = m - (Q mod p) m / Q + p e / Q).
+__global__ void __launch_bounds__(512, 2) k_dec_phase2(DevCtx c, const u64* __restrict__ x, uint32_t* __restrict__ slots,
+                                                       unsigned long long* __restrict__ maxd)
 {
     extern __shared__ u64 sm[];
     const int N = c.N, L = c.L, PM = c.M;
     const u64 p = c.p;
+    u64 dmax = 0;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         u64 sum_a = 0, f_lo = 0, f_hi = 0;
         for (int j = 0; j < L; j++) {
@@ -2102,6 +2106,16 @@ __global__ void __launch_bounds__(512, 2) k_dec_phase2(DevCtx c, const u64* __re
         u64 carry = (t < f_lo) ? 1 : 0;
         u64 rounded = sum_a + f_hi + carry;
         sm[pad(i)] = rounded % p;
+        const u64 d = f_lo < (1ull << 63) ? f_lo : (u64)0 - f_lo;
+        dmax = d > dmax ? d : dmax;
+    }
+    if (maxd) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const u64 v = __shfl_xor_sync(0xffffffffu, dmax, o);
+            dmax = v > dmax ? v : dmax;
+        }
+        if ((threadIdx.x & 31) == 0) atomicMax(maxd, (unsigned long long)dmax);
     }
     __syncthreads();
     ntt_fwd_smem(sm, c.twf[PM], p, c.logN);

@@ -861,16 +861,36 @@ int gala_encrypt(gala_ctx* c, const uint32_t* slots, const uint64_t* a, const in
     return GALA_OK;
 }
 
-int gala_decrypt(gala_ctx* c, const uint64_t* ct, uint32_t* slots)
+static int decrypt_run(gala_ctx* c, const uint64_t* ct, uint32_t* slots, double* noise_frac)
 {
     if (!c->has_secret) return set_err(GALA_ERR_STATE, "secret key not set");
     const int N = c->dc.N, L = c->dc.L;
     u64* x;
+    unsigned long long* maxd = nullptr;
     RET(scratch(c, &x, (size_t)L * N));
+    if (noise_frac) {
+        RET(scratch(c, &maxd, 1));
+        CK(cudaMemsetAsync(maxd, 0, sizeof(unsigned long long), c->stream));
+    }
     KLAUNCH(c, "k_dec_phase1", k_dec_phase1<<<L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, ct, x));
-    KLAUNCH(c, "k_dec_phase2", k_dec_phase2<<<1, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, x, slots));
+    KLAUNCH(c, "k_dec_phase2", k_dec_phase2<<<1, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, x, slots, maxd));
     release(c, x);
+    if (noise_frac) {
+        unsigned long long h = 0;
+        CK(cudaMemcpyAsync(&h, maxd, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        release(c, maxd);
+        CK(cudaStreamSynchronize(c->stream));
+        *noise_frac = (double)h / 18446744073709551616.0;
+    }
     return GALA_OK;
+}
+
+int gala_decrypt(gala_ctx* c, const uint64_t* ct, uint32_t* slots) { return decrypt_run(c, ct, slots, nullptr); }
+
+int gala_decrypt_noise(gala_ctx* c, const uint64_t* ct, uint32_t* slots, double* noise_frac)
+{
+    if (!noise_frac) return set_err(GALA_ERR_PARAM, "noise_frac must not be null");
+    return decrypt_run(c, ct, slots, noise_frac);
 }
 
 int gala_add(gala_ctx* c, const uint64_t* a, const uint64_t* b, uint64_t* out)

@@ -171,7 +171,7 @@ if __name__ == "__main__":
         elif w == "cfg3":
             r = conv("cfg3", 2048, 1, 16, 16, 64, 64, 3, B=int(os.environ.get("CFG3_BATCH", "16")))
         elif w == "cfg4":
-            r = conv("cfg4", 4096, 3, 56, 64, 64, 64, 3)
+            r = conv("cfg4", 4096, 3, 56, 64, 64, 64, 3, B=int(os.environ.get("CFG4_BATCH", "4")))
         elif w.startswith("conv:"):     # conv:n:L:u:frame:c_i:c_o:k
             a = [int(v) for v in w.split(":")[1:]]
             r = conv(w, *a)
