@@ -412,3 +412,27 @@ def test_sharded_conv_single_rank_is_the_layer():
         assert np.array_equal(decrypt(a).slots, decrypt(b).slots)
     dec = np.concatenate([unpack_channels(decrypt(o), task) for o in got])
     assert np.array_equal(dec, conv2d_mod_p(img, kern, P))
+
+
+def test_real_noise_guard():
+    """Real noise past Delta / 4 raises instead of returning wrong slots (GAZELLE's fold after the
+    plaintext product at one 62-bit prime); the same circuit at L = 2 decrypts correctly."""
+    from paper_2105_01827_b200.errors import NoiseOverflowError
+    from paper_2105_01827_b200.matvec import mv_hybrid_gazelle, pack_input
+
+    rng = np.random.default_rng(3)
+    w = rng.integers(-128, 128, (16, 2048)) % P
+    x = rng.integers(0, P, 2048)
+    for L, ok in ((1, False), (2, True)):
+        params = HEParams(n=2048, p=P, rns_limbs=L, seed=61)
+        task = MvTask(2048, 16, w, params)
+        ct = encrypt(pack_input(x, task), params)
+        if ok:
+            out = mv_hybrid_gazelle(task, ct, CostMeter(), rng=5)
+            assert np.array_equal((out.client_share.slots + out.server_share.slots) % P, dot_mod_p(w, x, P))
+            assert ct.ctx.last_noise_frac < 0.25
+        else:
+            with pytest.raises(NoiseOverflowError):
+                mv_hybrid_gazelle(task, ct, CostMeter(), rng=5)
+    # a fresh ciphertext is far below the limit
+    assert decrypt(ct).slots is not None and ct.ctx.last_noise_frac < 1e-6
