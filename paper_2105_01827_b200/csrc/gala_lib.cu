@@ -1160,26 +1160,35 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     RET(scratch(c, &rr, (size_t)Z * 2 * N));
     // the tensor-core tile always spans 32 input rows: it pays off from about half a tile of inputs
     // (config 2 at B = 8: 0.139 ms/layer vs 0.097 on the CUDA cores; B = 32: 0.044 vs 0.088)
-    const bool tc = wcan != nullptr && B >= 16 && B <= 32 && G <= 8 && baby <= 64 && (N % 32) == 0 &&
-                    getenv("GALA_FC_NO_TC") == nullptr;
+    // larger batches run the tensor-core pair per tile of 32 inputs (every tile >= 16); the rest of
+    // the layer (decompositions, giant steps, ModDowns) stays batched over all B
+    const bool tc = wcan != nullptr && B >= 16 && (B % 32 == 0 || B % 32 >= 16) && G <= 8 && baby <= 64 &&
+                    (N % 32) == 0 && getenv("GALA_FC_NO_TC") == nullptr;
     if (tc) {
         // tensor-core baby-step sums: E packed as int8 MMA operands, weights as their byte-convolution
         uint8_t* Ecan;
         RET(scratch(c, &Ecan, (size_t)MN * GTC_A_BYTES));
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
         dim3 ge((unsigned)(N / 32), 32, (unsigned)M);
-#define GALA_ECAN(LL) KLAUNCH(c, "k_gala_e", (k_gala_e_can<LL><<<ge, 256, 0, c->stream>>>(c->dc, Dblk, dk, d_gal, baby, B, Ecan)))
+        for (int b0 = 0; b0 < B; b0 += 32) {
+            const int bt = B - b0 < 32 ? B - b0 : 32;
+            const u64* Dt = Dblk + (long long)b0 * blk_words;
+            const u64* Xt = cts + (long long)b0 * 2 * L * N;
+            u64* Ut = U + (long long)b0 * G * 2 * M * N;
+            u64* Ct = Cacc + (long long)b0 * G * 2 * L * N;
+#define GALA_ECAN(LL) KLAUNCH(c, "k_gala_e", (k_gala_e_can<LL><<<ge, 256, 0, c->stream>>>(c->dc, Dt, dk, d_gal, baby, bt, Ecan)))
 #define GALA_TC(LL)                                                                                        \
     KLAUNCH(c, "k_gala_tc", (k_gala_tc<LL><<<c->num_sms, GTC_THREADS, GTC_SMEM, c->stream>>>(                   \
-                                c->dc, Ecan, (const u64*)wcan, cts, pts2, baby, G, B, U, Cacc)))
-        switch (L) {
-            case 1: GALA_ECAN(1); GALA_TC(1); break;
-            case 2: GALA_ECAN(2); GALA_TC(2); break;
-            case 3: GALA_ECAN(3); GALA_TC(3); break;
-            default: GALA_ECAN(4); GALA_TC(4); break;
-        }
+                                c->dc, Ecan, (const u64*)wcan, Xt, pts2, baby, G, bt, Ut, Ct)))
+            switch (L) {
+                case 1: GALA_ECAN(1); GALA_TC(1); break;
+                case 2: GALA_ECAN(2); GALA_TC(2); break;
+                case 3: GALA_ECAN(3); GALA_TC(3); break;
+                default: GALA_ECAN(4); GALA_TC(4); break;
+            }
 #undef GALA_ECAN
 #undef GALA_TC
+        }
         release(c, Ecan);
     } else {
     RET(scratch(c, &E, (size_t)B * (baby - 1) * 2 * MN));
