@@ -384,7 +384,7 @@ def run_ours(args):
     dom_achieved = dom_work / (dom["ms"] / 1e3) if dom["ms"] else 0.0
     layer_achieved = layer_modmuls * layers / world / (total_ms / 1e3)
 
-    tc_on = layer.wcan[0] is not None and B >= 16 and (B % 32 == 0 or B % 32 >= 16)
+    tc_on = layer.wcan[0] is not None and B >= 16 and (B <= 32 or (T >= 128 and (B % 32 == 0 or B % 32 >= 16)))
     traffic = None    # DRAM bytes per launch of the dominant kernel from the committed ncu capture
     try:
         with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:

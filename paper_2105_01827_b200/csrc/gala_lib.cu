@@ -1160,10 +1160,12 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     RET(scratch(c, &rr, (size_t)Z * 2 * N));
     // the tensor-core tile always spans 32 input rows: it pays off from about half a tile of inputs
     // (config 2 at B = 8: 0.139 ms/layer vs 0.097 on the CUDA cores; B = 32: 0.044 vs 0.088)
-    // larger batches run the tensor-core pair per tile of 32 inputs (every tile >= 16); the rest of
-    // the layer (decompositions, giant steps, ModDowns) stays batched over all B
-    const bool tc = wcan != nullptr && B >= 16 && (B % 32 == 0 || B % 32 >= 16) && G <= 8 && baby <= 64 &&
-                    (N % 32) == 0 && getenv("GALA_FC_NO_TC") == nullptr;
+    // larger batches run the tensor-core pair per tile of 32 inputs (every tile >= 16) when the layer is
+    // large enough for a tile's fixed per-position cost (K = 64 rotations x 8 bytes whatever T is) to pay:
+    // T >= 128 (config 2: 17.5k -> 19.3k layers/s at 96 inputs; config 1, T = 8, stays on the CUDA cores,
+    // 0.0016 vs 0.0066 ms per layer at 1024 inputs); the rest of the layer stays batched over all B
+    const bool tc = wcan != nullptr && B >= 16 && (B <= 32 || (T >= 128 && (B % 32 == 0 || B % 32 >= 16))) &&
+                    G <= 8 && baby <= 64 && (N % 32) == 0 && getenv("GALA_FC_NO_TC") == nullptr;
     if (tc) {
         // tensor-core baby-step sums: E packed as int8 MMA operands, weights as their byte-convolution
         uint8_t* Ecan;

@@ -167,7 +167,7 @@ if __name__ == "__main__":
         if w == "cfg1":
             r = fc("cfg1", 2048, 1, 16, 2048, int(os.environ.get("CFG1_BATCH", "1024")))
         elif w == "cfg2":
-            r = fc("cfg2", 4096, 3, 1024, 4096, 32)
+            r = fc("cfg2", 4096, 3, 1024, 4096, int(os.environ.get("CFG2_BATCH", "96")))
         elif w == "cfg3":
             r = conv("cfg3", 2048, 1, 16, 16, 64, 64, 3, B=int(os.environ.get("CFG3_BATCH", "16")))
         elif w == "cfg4":
