@@ -75,7 +75,10 @@ def _next_pow2(x: int) -> int:
 class ConvLayer:
     """One (possibly strided, possibly tiled) convolution on kernel-grouping frames."""
 
-    def __init__(self, spec: LayerSpec, kernels: np.ndarray, params: HEParams):
+    def __init__(self, spec: LayerSpec, kernels: np.ndarray, params: HEParams, shard_blocks: bool = False):
+        """``shard_blocks``: split the layer's physical output ciphertexts across the ranks of the
+        process group (`sharding.ShardedKernelGroupingConv`: inputs broadcast from rank 0, outputs
+        gathered on rank 0) -- the latency form of config 5 on several GPUs."""
         self.spec, self.params = spec, params
         n = params.n
         h = spec.k // 2
@@ -93,12 +96,18 @@ class ConvLayer:
         self.task = task
         # every kept output pixel reads inside the frame's zero margin (or the tile's halo)
         margin_ok = self.tiled or frame - spec.size >= h
-        self.kg = KernelGroupingConv(task, band_only=margin_ok)
+        if shard_blocks:
+            from .sharding import ShardedKernelGroupingConv
+
+            self.kg = ShardedKernelGroupingConv(task, band_only=margin_ok)
+        else:
+            self.kg = KernelGroupingConv(task, band_only=margin_ok)
         self.ctx = self.kg.ctx
 
     @property
     def plaintext_bytes(self) -> int:
-        return self.kg.resident_bytes
+        kg = getattr(self.kg, "local", self.kg)
+        return kg.resident_bytes if kg is not None else 0
 
     def frames(self, x: np.ndarray):
         """Yield (origin_y, origin_x, frame array) covering the input x [c_in][s][s]."""
@@ -193,7 +202,8 @@ class FCLayer:
 class ResNet18Linear:
     """All ResNet-18 linear layers with resident encoded weights on one GPU."""
 
-    def __init__(self, params: HEParams | None = None, seed: int = 2105, layers=None, only=None):
+    def __init__(self, params: HEParams | None = None, seed: int = 2105, layers=None, only=None,
+                 shard_blocks: bool = False):
         """``only``: indices of the layers this process serves (multi-GPU layer partition,
         `sharding.partition_layers`); the others get weights drawn (same stream) but no GPU state."""
         self.params = params or HEParams(n=4096, rns_limbs=3, seed=5)
@@ -208,7 +218,7 @@ class ResNet18Linear:
                 self.layers.append(FCLayer(spec, w, self.params) if i in keep else None)
             else:
                 w = rng.integers(-128, 128, (spec.c_out, spec.c_in, spec.k, spec.k)) % p
-                self.layers.append(ConvLayer(spec, w, self.params) if i in keep else None)
+                self.layers.append(ConvLayer(spec, w, self.params, shard_blocks=shard_blocks) if i in keep else None)
             self.weights.append(w)
         self.ctx = context(self.params)
 

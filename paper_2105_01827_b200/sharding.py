@@ -152,6 +152,38 @@ class ShardedKernelGroupingConv:
             def layer_factory(t):
                 return KernelGroupingConv(t, pair_rows=pair_rows, **kw)
         self.local = layer_factory(self.sub_task) if self.sub_task is not None else None
+        # the layer geometry callers read (ConvLayer.decrypt_output)
+        self.c_n, self.n_ob = c_n, n_ob
+        self.schedule = getattr(self.local, "schedule", None)
+
+    @property
+    def ctx(self):
+        from .backend import context
+
+        return context(self.task.params)
+
+    @property
+    def batchable(self) -> bool:
+        """Every rank's sub-layer has the batched form (same schedule: only c_o differs)."""
+        if self.local is None:
+            return True
+        return bool(getattr(self.local, "batchable", False))
+
+    def forward_device_batch(self, cts_batch, src: int = 0, dst: int = 0):
+        """[B][n_ib][2][L][N] images on `src` -> [B][n_obp][2][L][N] on `dst` (None elsewhere)."""
+        import torch
+
+        dist = _dist()
+        if dist is not None and self.world > 1:
+            cts_batch = cts_batch.contiguous()
+            dist.broadcast(cts_batch, src=src, group=self.group)
+        nb = cts_batch.shape[0]
+        if self.local is not None:
+            local = self.local.forward_device_batch(cts_batch)
+        else:
+            local = torch.empty((nb, 0) + tuple(cts_batch.shape[2:]), dtype=cts_batch.dtype, device=cts_batch.device)
+        out = gather_blocks(local.transpose(0, 1).contiguous(), self.sizes, dst=dst, group=self.group)
+        return None if out is None else out.transpose(0, 1).contiguous()
 
     def forward_device(self, cts_phys, src: int = 0, dst: int = 0):
         """[n_ib][2][L][N] on `src` -> [n_obp][2][L][N] on `dst` (None on the other ranks)."""

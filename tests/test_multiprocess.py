@@ -116,6 +116,13 @@ class _OracleKG:
         out = self.cpu.conv_kg(cts.numpy().view(np.uint64), self.pts, self.taps, self.task.image_slots)
         return torch.from_numpy(out.view(np.int64))
 
+    batchable = True
+
+    def forward_device_batch(self, cts_batch):
+        import torch
+
+        return torch.stack([self.forward_device(c) for c in cts_batch])
+
 
 def _sharded_conv_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -172,6 +179,16 @@ def _sharded_conv_worker(rank, world, port, q):
         else:
             assert out is None
             res = (None, None, layer.sizes)
+        # the batched form (halo tiles / images sharing the weights): gather along the output blocks
+        xb = torch.stack([x, torch.flip(x, dims=[0])]) if rank == 0 else torch.zeros((2,) + tuple(x.shape), dtype=x.dtype)
+        outb = layer.forward_device_batch(xb)
+        if rank == 0:
+            full = _OracleKG(task, cpu)
+            ok_b = all(bool(torch.equal(outb[b], full.forward_device(xb[b]))) for b in range(2))
+            res = res + (ok_b,)
+        else:
+            assert outb is None
+            res = res + (None,)
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -190,7 +207,8 @@ def test_gloo_world2_sharded_conv_output_blocks():
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    words_equal, dec_ok, sizes = outs[0]
+    words_equal, dec_ok, sizes, batch_ok = outs[0]
     assert sizes == [2, 1]
     assert words_equal
     assert dec_ok
+    assert batch_ok

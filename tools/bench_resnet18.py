@@ -46,6 +46,7 @@ def main():
     measured per-layer times, `sharding.partition_layers`); each rank holds and runs its own
     layers.  The pipelined network period is the max over ranks of the per-rank sums."""
     check = "--no-check" not in sys.argv
+    blocks = "--shard-blocks" in sys.argv     # latency form: every conv's output blocks split across ranks
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if world > 1:
@@ -54,10 +55,13 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
     specs = resnet18_224()
-    parts = partition_layers(layer_costs(specs, _measured_costs()), world)
+    if blocks:   # every rank holds a slice of every conv; the FC runs on rank 0
+        parts = [list(range(len(specs)))] + [[i for i, sp in enumerate(specs) if sp.kind == "conv"]] * (world - 1)
+    else:
+        parts = partition_layers(layer_costs(specs, _measured_costs()), world)
     mine = parts[rank]
     t0 = time.perf_counter()
-    net = ResNet18Linear(only=mine)
+    net = ResNet18Linear(only=mine, shard_blocks=blocks and world > 1)
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
     ctx = net.ctx
@@ -85,13 +89,15 @@ def main():
             torch.cuda.synchronize()
             reps.append(a.elapsed_time(b))
         ms = float(np.median(reps))
+        if blocks and world > 1 and spec.kind == "conv":   # every rank ran a slice of this layer
+            ms = max_over_ranks(ms, device=torch.device("cuda"))
         total_ms += ms
         res = {"layer": spec.name, "shape": [spec.c_in, spec.c_out, spec.k, spec.stride, spec.size], "ms": round(ms, 3),
                "ms_reps": [round(v, 3) for v in reps],
                "plaintext_GB": round(layer.plaintext_bytes / 1e9, 3)}
         if spec.kind == "conv":
             res.update(frame=layer.frame, c_n=layer.kg.c_n, tiles=layer.tiles ** 2, schedule=layer.kg.schedule)
-        if check:
+        if check and (not blocks or rank == 0):   # sharded outputs are gathered on rank 0
             got = layer.shares(out, masks) if spec.kind == "fc" else layer.decrypt_output(out)
             ok = bool(np.array_equal(got, plain_layer(spec, x, net.weights[i], net.params.p)))
             res["correct"] = ok
@@ -100,7 +106,13 @@ def main():
         print(json.dumps(res), flush=True)
     period = max_over_ranks(total_ms, device=torch.device("cuda"))
     sums = gather_objects((total_ms, ok_all))
-    if rank == 0:
+    if rank == 0 and blocks:
+        print(json.dumps({"summary": "resnet18_224_linear_latency", "layers": len(net.specs), "n_gpus": world,
+                          "mode": "every conv's output ciphertexts sharded across ranks (inputs broadcast, "
+                                  "outputs gathered on rank 0); per-layer time = max over ranks",
+                          "latency_ms": round(total_ms, 2), "all_correct": ok_all if check else None,
+                          "N": ctx.N, "L": ctx.L}), flush=True)
+    elif rank == 0:
         print(json.dumps({"summary": "resnet18_224_linear", "layers": len(net.specs), "n_gpus": world,
                           "partition": parts, "per_rank_ms": [round(t, 2) for t, _ in sums],
                           "total_ms": round(sum(t for t, _ in sums), 2),
