@@ -406,3 +406,23 @@ def test_mv_gala2_stream_host_words(tw, tc):
         for i in (0, B - 1):
             _, c_masked = tw.cpu.mv_gala(xs[s][i][1], pts, rs[s, i], baby=b, schedule=2)
             assert np.array_equal(host_out[s, i], c_masked), f"batch {s} input {i}"
+
+
+def test_conv_kg_batch_odd_rows_words(tw):
+    """Batched first-Add with an odd accumulator-row count (c_n = 1, 3 outputs: the 2-row register
+    tile's tail) and an odd image count == oracle per image."""
+    n = tw.bfv.n
+    if n < 16:
+        pytest.skip("tiny")
+    c_n, k, n_ib, n_obp, nimg = 1, 3, 2, 3, 3
+    tap_steps = [0, 1, n - 1]
+    tw.keys_for(tap_steps)
+    imgs = [[tw.encrypt(tw.slots()) for _ in range(n_ib)] for _ in range(nimg)]
+    pts = tw.slots(n_obp * n_ib * c_n * k).reshape(n_obp, n_ib, c_n, k, tw.N)
+    import torch
+
+    d_pts = tw.gpu.encode_plain(pts.reshape(-1, tw.N)).view(n_obp, n_ib, c_n, k, tw.L, tw.N)
+    outs = tw.gpu.conv_kg_batch(torch.stack([torch.stack([g for g, _ in im]) for im in imgs]), d_pts, tap_steps, n)
+    for b, im in enumerate(imgs):
+        c_out = tw.cpu.conv_kg(np.stack([c for _, c in im]), pts, tap_steps, n)
+        assert np.array_equal(tw.gpu.export_words(outs[b]), c_out), f"image {b}"
