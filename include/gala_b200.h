@@ -129,7 +129,9 @@ int gala_mv_gala_batch_host(gala_ctx *ctx, const uint64_t *cts_host, int B, cons
  * weights' byte-convolution (Toeplitz) expansion is the MMA B operand (built in shared memory from
  * the position-major weights gala_fc_tc_weights writes to wcan_dev, gala_fc_tc_weight_bytes bytes =
  * 4 KB per position) and E_jj, packed per position, the A operand.  Same words as gala_mv_gala2_batch (exact modular arithmetic).
- * Used for 16 <= B <= 32, T/baby <= 8 and baby <= 64; otherwise the CUDA-core path runs. */
+ * Used for T/baby <= 8, baby <= 64 and 16 <= B <= 32 -- or, for T >= 128, any B whose 32-input
+ * tiles all hold >= 16 inputs (one E / MMA kernel pair per tile, everything else batched over B);
+ * otherwise the CUDA-core path runs. */
 size_t gala_fc_tc_weight_bytes(gala_ctx *ctx);
 int gala_fc_tc_weights(gala_ctx *ctx, const uint64_t *pts2_dev, int T, int baby, uint8_t *wcan_dev);
 int gala_mv_gala2_batch_tc(gala_ctx *ctx, const uint64_t *cts_dev, int B, const uint64_t *pts2_dev,
