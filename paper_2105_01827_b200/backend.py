@@ -63,8 +63,12 @@ class HEParams:
     """Reference parameter set (backend.py:80-114) plus the BFV instance knobs.
 
     rns_limbs: ciphertext primes (None: 1 for N <= 4096, else 3);
-    device: CUDA device of the context; seed: host randomness seed for the
-    context's secret, keys and encryptions.
+    device: CUDA device of the context; seed: None (default) draws the
+    context's secret, rotation keys and encryption randomness from the OS
+    CSPRNG (``sampling.SystemRng``); an integer derives them from seeded
+    NumPy PCG64 streams instead -- reproducible, so the CPU oracle can be
+    handed the same randomness, and therefore INSECURE (word-parity tests and
+    benchmarks only).
     """
 
     n: int = 2048
@@ -77,7 +81,7 @@ class HEParams:
     noise_budget: float | None = None
     rns_limbs: int | None = None
     device: int = 0
-    seed: int = 0
+    seed: int | None = None
 
     def __post_init__(self):
         if not is_power_of_two(self.n):
@@ -195,8 +199,15 @@ class Context:
         self._enc_counter = 0
         self.seed = params.seed
         if secret is None:
-            secret = sampling.secret(np.random.default_rng([self.seed, 0]), self.N)
+            secret = sampling.secret(self._rng(0), self.N)
         self.set_secret(secret)
+
+    def _rng(self, *tags):
+        """The randomness source of one secret / key / encryption: the OS CSPRNG, or (seeded
+        contexts only; insecure) a PCG64 stream keyed by (seed, *tags)."""
+        if self.seed is None:
+            return sampling.SystemRng()
+        return np.random.default_rng([self.seed, *tags])
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -260,8 +271,7 @@ class Context:
         if step == 0:
             return
         if a is None:
-            a, e = sampling.rotation_key_randomness(np.random.default_rng([self.seed, 1, step]), self.bfv,
-                                                    self.params.sigma)
+            a, e = sampling.rotation_key_randomness(self._rng(1, step), self.bfv, self.params.sigma)
         a = np.ascontiguousarray(a, dtype=np.uint64)
         e = np.ascontiguousarray(e, dtype=np.int64)
         self.call("gala_gen_rotation_key", int(step), a.ctypes.data_as(ctypes.c_void_p),
@@ -294,7 +304,7 @@ class Context:
         return pt
 
     def next_encryption_randomness(self):
-        rng = np.random.default_rng([self.seed, 2, self._enc_counter])
+        rng = self._rng(2, self._enc_counter)
         self._enc_counter += 1
         return sampling.encryption_randomness(rng, self.bfv, self.params.sigma)
 
@@ -606,13 +616,14 @@ def context(params: HEParams) -> Context:
 class Ciphertext:
     """A BFV ciphertext in HBM plus the reference's mock noise level.
 
-    ``row`` selects which hypercube row holds this logical vector (API-level
-    ciphertexts replicate it in both rows, row = 0).  The constructor mirrors
-    ``MockCiphertext(payload, noise, params)`` (backend.py:188-204): it
-    encrypts ``payload`` and records ``noise``.
+    ``row`` selects which hypercube row holds this logical vector;
+    ``replicated`` says both rows hold it (every encryption, and every op on
+    replicated operands).  Row-paired layer outputs hold a different vector in
+    the other row.  The constructor mirrors ``MockCiphertext(payload, noise,
+    params)`` (backend.py:188-204): it encrypts ``payload`` and records ``noise``.
     """
 
-    __slots__ = ("data", "noise", "params", "row", "__weakref__")
+    __slots__ = ("data", "noise", "params", "row", "replicated", "__weakref__")
 
     def __init__(self, payload: SlotVector, noise: float, params: HEParams):
         if len(payload) != params.n:
@@ -624,14 +635,16 @@ class Ciphertext:
         self.noise = noise
         self.params = params
         self.row = 0
+        self.replicated = True
 
     @classmethod
-    def _wrap(cls, data, noise: float, params: HEParams, row: int = 0) -> "Ciphertext":
+    def _wrap(cls, data, noise: float, params: HEParams, row: int = 0, replicated: bool = False) -> "Ciphertext":
         c = object.__new__(cls)
         c.data = data
         c.noise = noise
         c.params = params
-        c.row = row
+        c.row = 0 if replicated else row
+        c.replicated = bool(replicated)
         return c
 
     @property
@@ -650,7 +663,8 @@ class Ciphertext:
         return self.ctx.export_words(self.data)
 
     def __repr__(self) -> str:
-        return f"Ciphertext(n={self.params.n}, L={self.ctx.L}, row={self.row}, noise={self.noise:g})"
+        rows = "both" if self.replicated else self.row
+        return f"Ciphertext(n={self.params.n}, L={self.ctx.L}, row={rows}, noise={self.noise:g})"
 
 
 MockCiphertext = Ciphertext  # drop-in name used by reference callers and tests
@@ -667,11 +681,17 @@ class RotationGroup:
         self.digits = digits
 
 
-def _check_same(a: Ciphertext, b: Ciphertext) -> None:
+def _check_same(a: Ciphertext, b: Ciphertext) -> tuple[int, bool]:
+    """(row, replicated) of a slotwise combination of a and b."""
     if a.params != b.params:
         raise DimensionError("ciphertexts built under different parameter sets")
+    if a.replicated and b.replicated:
+        return 0, True
+    if a.replicated or b.replicated:
+        return (b.row if a.replicated else a.row), False
     if a.row != b.row:
         raise DimensionError("ciphertexts hold their vectors in different hypercube rows")
+    return a.row, False
 
 
 def _phys_for(ct: Ciphertext, v: SlotVector) -> np.ndarray:
@@ -689,7 +709,7 @@ def encrypt(x: SlotVector, params: HEParams) -> Ciphertext:
     if x.modulus != params.p:
         raise DimensionError(f"plaintext modulus {x.modulus} != {params.p}")
     ctx = context(params)
-    return Ciphertext._wrap(ctx.encrypt_physical(ctx.physical(x.slots)), params.eta0, params)
+    return Ciphertext._wrap(ctx.encrypt_physical(ctx.physical(x.slots)), params.eta0, params, replicated=True)
 
 
 def decrypt(c: Ciphertext) -> SlotVector:
@@ -703,10 +723,10 @@ def decrypt(c: Ciphertext) -> SlotVector:
 
 
 def he_add(a: Ciphertext, b: Ciphertext, meter: CostMeter) -> Ciphertext:
-    _check_same(a, b)
+    row, rep = _check_same(a, b)
     out = a.ctx.add(a.data, b.data)
     meter.add += 1
-    return Ciphertext._wrap(out, a.noise + b.noise, a.params, a.row)
+    return Ciphertext._wrap(out, a.noise + b.noise, a.params, row, rep)
 
 
 def he_scmult(a: Ciphertext, s: SlotVector, meter: CostMeter) -> Ciphertext:
@@ -716,7 +736,7 @@ def he_scmult(a: Ciphertext, s: SlotVector, meter: CostMeter) -> Ciphertext:
     pt = ctx.encode_plain(_phys_for(a, s))
     out = ctx.scmult(a.data, pt[0])
     meter.sc_mult += 1
-    return Ciphertext._wrap(out, a.noise * a.params.eta_mult, a.params, a.row)
+    return Ciphertext._wrap(out, a.noise * a.params.eta_mult, a.params, a.row, a.replicated)
 
 
 def he_perm(a: Ciphertext, k: int, meter: CostMeter) -> Ciphertext:
@@ -725,7 +745,7 @@ def he_perm(a: Ciphertext, k: int, meter: CostMeter) -> Ciphertext:
         return a
     out = a.ctx.rotate(a.data, k)
     meter.full_perm += 1
-    return Ciphertext._wrap(out, a.noise + a.params.eta_rot, a.params, a.row)
+    return Ciphertext._wrap(out, a.noise + a.params.eta_rot, a.params, a.row, a.replicated)
 
 
 def he_decperm(a: Ciphertext, meter: CostMeter) -> RotationGroup:
@@ -742,7 +762,7 @@ def he_hstperm(g: RotationGroup, k: int, meter: CostMeter) -> Ciphertext:
         g.digits = src.ctx.decompose(src.data)
     out = src.ctx.rotate_hoisted(src.data, g.digits, k)
     meter.hst_perm += 1
-    return Ciphertext._wrap(out, src.noise + src.params.eta_rot, src.params, src.row)
+    return Ciphertext._wrap(out, src.noise + src.params.eta_rot, src.params, src.row, src.replicated)
 
 
 def subtract_plain(a: Ciphertext, r: SlotVector, meter: CostMeter) -> Ciphertext:
@@ -750,7 +770,7 @@ def subtract_plain(a: Ciphertext, r: SlotVector, meter: CostMeter) -> Ciphertext
         raise DimensionError("mask vector does not match ciphertext layout")
     out = a.ctx.sub_plain(a.data, _phys_for(a, r))
     meter.add += 1
-    return Ciphertext._wrap(out, a.noise + a.params.eta0, a.params, a.row)
+    return Ciphertext._wrap(out, a.noise + a.params.eta0, a.params, a.row, a.replicated)
 
 
 _PARAM_KEYS = {"n", "p", "q_bits", "sigma", "eta0", "eta_mult", "eta_rot", "noise_budget", "rns_limbs",

@@ -1782,7 +1782,9 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     const int Kreal = n_ib * k * (post ? 1 : nb);
     const int rows = post ? Mr * nb : Mr;     // GEMM rows
     if (Kp % 16 || Kp < Kreal) return set_err(GALA_ERR_DIM, "Kp=%d must be a multiple of 16 covering K=%d", Kp, Kreal);
-    if (Kp > (1 << 17)) return set_err(GALA_ERR_DIM, "K too large for exact int32 accumulation");
+    // every int8 x int8 product has |a b| <= 128 * 128 = 2^14 (both operands may be -128: coefficients
+    // and 0x80-biased bytes), so the int32 GEMM sums stay exact while Kp * 2^14 <= INT32_MAX (Kp < 2^17)
+    if ((long long)Kp * 16384 > 2147483647LL) return set_err(GALA_ERR_DIM, "K too large for exact int32 accumulation");
     std::vector<int> tsteps(k);
     bool any_rot = false;
     for (int t = 0; t < k; t++) {

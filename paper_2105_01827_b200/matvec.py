@@ -264,8 +264,8 @@ def mv_gala(task: MvTask, ct_xpack: Ciphertext, meter: CostMeter, rng=None) -> M
     book_gala(lin, T)
     meter.merge(lin)
     out_noise = _gala_noise(ct_xpack.noise, T, params)
-    ct_out = Ciphertext._wrap(out, out_noise, params, ct_xpack.row)
-    ct_masked = Ciphertext._wrap(masked, out_noise + params.eta0, params, ct_xpack.row)
+    ct_out = Ciphertext._wrap(out, out_noise, params, ct_xpack.row, ct_xpack.replicated)
+    ct_masked = Ciphertext._wrap(masked, out_noise + params.eta0, params, ct_xpack.row, ct_xpack.replicated)
     share_meter = CostMeter(lin.cost_model)
     share_meter.add += 1
     start, end = task.fold_spec()

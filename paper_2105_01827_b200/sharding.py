@@ -90,6 +90,26 @@ def gather_objects(obj):
     return out
 
 
+def _host_staged(dist, t, group=None) -> bool:
+    """gloo moves host tensors only: CUDA tensors go through host memory (CPU tests of the
+    multi-rank path with real CUDA layers); NCCL moves them over NVLink directly."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def broadcast_tensor(t, src: int = 0, group=None):
+    """In-place broadcast of `t` from `src` (host-staged under gloo)."""
+    dist = _dist()
+    if dist is None or dist.get_world_size(group) == 1:
+        return t
+    if _host_staged(dist, t, group):
+        h = t.cpu()
+        dist.broadcast(h, src=src, group=group)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, src=src, group=group)
+    return t
+
+
 def gather_blocks(local, sizes, dst: int = 0, group=None):
     """Gather per-rank ciphertext blocks [n_r][...] to `dst` -> [sum n_r][...] (None elsewhere).
 
@@ -106,11 +126,14 @@ def gather_blocks(local, sizes, dst: int = 0, group=None):
     if local.shape[0] < m:
         pad = torch.zeros((m - local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
         local = torch.cat([local, pad])
+    dev = local.device
+    if _host_staged(dist, local, group):
+        local = local.cpu()
     bufs = [torch.empty_like(local) for _ in range(world)] if rank == dst else None
     dist.gather(local.contiguous(), bufs, dst=dst, group=group)
     if rank != dst:
         return None
-    return torch.cat([b[:n] for b, n in zip(bufs, sizes)])
+    return torch.cat([b[:n] for b, n in zip(bufs, sizes)]).to(dev)
 
 
 def sub_conv_task(task, obp: range, pair: int):
@@ -146,15 +169,26 @@ class ShardedKernelGroupingConv:
         self.sizes = [len(s) for s in self.shards]
         mine = self.shards[self.rank]
         self.sub_task = sub_conv_task(task, mine, self.pair) if len(mine) else None
+        # the schedule, mask form and first-Add engine are decided once from the FULL task and imposed
+        # on every shard: a decision taken per shard (its kernels' int8 range, its row count, its
+        # plaintext bytes) could differ between ranks, so the gathered words would not be the
+        # single-GPU layer's and the ranks could reach the collectives with different shapes
+        self.plan = kw.pop("plan", None)
         if layer_factory is None:
-            from .conv import KernelGroupingConv
+            from .backend import context
+            from .conv import KernelGroupingConv, kg_plan
+
+            if self.plan is None:
+                ctx = context(task.params)
+                plan_kw = {k: kw[k] for k in ("band_only", "tensor_cores", "host_encode", "schedule") if k in kw}
+                self.plan = kg_plan(task, self.pair, ctx.L, ctx.N, **plan_kw)
 
             def layer_factory(t):
-                return KernelGroupingConv(t, pair_rows=pair_rows, **kw)
+                return KernelGroupingConv(t, pair_rows=pair_rows, plan=self.plan, **kw)
         self.local = layer_factory(self.sub_task) if self.sub_task is not None else None
         # the layer geometry callers read (ConvLayer.decrypt_output)
         self.c_n, self.n_ob = c_n, n_ob
-        self.schedule = getattr(self.local, "schedule", None)
+        self.schedule = self.plan.schedule if self.plan is not None else getattr(self.local, "schedule", None)
 
     @property
     def ctx(self):
@@ -164,19 +198,19 @@ class ShardedKernelGroupingConv:
 
     @property
     def batchable(self) -> bool:
-        """Every rank's sub-layer has the batched form (same schedule: only c_o differs)."""
-        if self.local is None:
-            return True
-        return bool(getattr(self.local, "batchable", False))
+        """The full layer's batched form (rank-independent: every rank takes the same branch; a
+        shard without the fused batched form runs its images one by one inside
+        forward_device_batch)."""
+        if self.plan is not None:
+            return bool(self.plan.batchable)
+        return bool(getattr(self.local, "batchable", True))
 
     def forward_device_batch(self, cts_batch, src: int = 0, dst: int = 0):
         """[B][n_ib][2][L][N] images on `src` -> [B][n_obp][2][L][N] on `dst` (None elsewhere)."""
         import torch
 
-        dist = _dist()
-        if dist is not None and self.world > 1:
-            cts_batch = cts_batch.contiguous()
-            dist.broadcast(cts_batch, src=src, group=self.group)
+        if self.world > 1:
+            cts_batch = broadcast_tensor(cts_batch.contiguous(), src=src, group=self.group)
         nb = cts_batch.shape[0]
         if self.local is not None:
             local = self.local.forward_device_batch(cts_batch)
@@ -189,10 +223,8 @@ class ShardedKernelGroupingConv:
         """[n_ib][2][L][N] on `src` -> [n_obp][2][L][N] on `dst` (None on the other ranks)."""
         import torch
 
-        dist = _dist()
-        if dist is not None and self.world > 1:
-            cts_phys = cts_phys.contiguous()
-            dist.broadcast(cts_phys, src=src, group=self.group)
+        if self.world > 1:
+            cts_phys = broadcast_tensor(cts_phys.contiguous(), src=src, group=self.group)
         if self.local is not None:
             local = self.local.forward_device(cts_phys)
         else:
@@ -206,12 +238,21 @@ class ShardedKernelGroupingConv:
 
         from .backend import Ciphertext
         from .conv import _check_mimo, _kg_book_and_noise
+        from .errors import DimensionError
 
         c_n, n_ib, n_ob = _check_mimo(self.task, cts)
+        if self.pair == 2 and not all(c.replicated for c in cts):
+            raise DimensionError("row-paired kernel grouping expects replicated input ciphertexts")
+        rows = {c.row for c in cts if not c.replicated}
+        if len(rows) > 1:
+            raise DimensionError("input ciphertexts hold their vectors in different hypercube rows")
         stacked = torch.stack([c.data for c in cts])
         outs = self.forward_device(stacked, src=src, dst=dst)
         if outs is None:
             return None
         noises = _kg_book_and_noise(self.task, [c.noise for c in cts], c_n, n_ib, n_ob, meter)
-        return [Ciphertext._wrap(outs[ob // self.pair], noises[ob], self.task.params, ob % self.pair)
-                for ob in range(n_ob)]
+        if self.pair == 2:
+            return [Ciphertext._wrap(outs[ob // 2], noises[ob], self.task.params, ob % 2) for ob in range(n_ob)]
+        rep = not rows
+        row = rows.pop() if rows else 0
+        return [Ciphertext._wrap(outs[ob], noises[ob], self.task.params, row, replicated=rep) for ob in range(n_ob)]

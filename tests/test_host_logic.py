@@ -338,3 +338,45 @@ def test_kg_schedule_selection():
     assert kg_schedule(big, 1, 3) == 1                         # not int8 after centring
     neg = ConvTask(8, 8, 2, 3, 3, 2, np.full((2, 2, 3, 3), p - 128, dtype=np.int64), params)
     assert kg_schedule(neg, 1, 3) == 2                         # -128 mod p centres into int8
+
+
+def test_system_rng_samplers():
+    """Default (seed=None) contexts draw secrets, keys and encryption randomness from the OS CSPRNG:
+    the samplers' ranges and moments hold, and two draws differ."""
+    from paper_2105_01827_b200 import sampling
+
+    g = sampling.SystemRng()
+    assert HEParams().seed is None
+    s = sampling.secret(g, 1 << 14)
+    assert set(np.unique(s).tolist()) == {-1, 0, 1}
+    assert abs(float(np.mean(s == 0)) - 1 / 3) < 0.03
+    q = (1 << 60) - 93
+    u = sampling.uniform(g, [q, 1032193], 4096)
+    assert u.dtype == np.uint64 and u.shape == (2, 4096)
+    assert int(u[0].max()) < q and int(u[1].max()) < 1032193
+    assert abs(float(u[1].astype(np.float64).mean()) / 1032193 - 0.5) < 0.03
+    e = sampling.gaussian(g, 1 << 15, 3.2)
+    assert abs(float(e.std()) - 3.2) < 0.15 and abs(float(e.mean())) < 0.15 and int(np.abs(e).max()) <= 20
+    assert not np.array_equal(sampling.secret(g, 256), sampling.secret(g, 256))
+    # the seeded (insecure, reproducible) stream stays available for word-parity tests
+    a = sampling.secret(np.random.default_rng([5, 0]), 64)
+    assert np.array_equal(a, sampling.secret(np.random.default_rng([5, 0]), 64))
+
+
+def test_kg_plan_is_taken_from_the_full_task():
+    """Schedule / mask form / first-Add engine come from the full layer: a shard whose kernels alone
+    fit int8 still follows the full layer's schedule (sharding.ShardedKernelGroupingConv)."""
+    from paper_2105_01827_b200.conv import kg_plan, kg_schedule
+    from paper_2105_01827_b200.sharding import shard_range, sub_conv_task
+
+    params = HEParams(n=1024, rns_limbs=3)
+    rng = np.random.default_rng(5)
+    kern = rng.integers(-128, 128, (24, 8, 3, 3))
+    kern[0, 0, 0, 0] = 5000
+    task = ConvTask(32, 32, 8, 3, 3, 24, kern % P, params)
+    assert kg_plan(task, 2, 3, 2048).schedule == 1
+    sub = sub_conv_task(task, shard_range(12, 2, 1), 2)
+    assert kg_schedule(sub, 1, 3) == 2
+    p2 = kg_plan(ConvTask(32, 32, 8, 3, 3, 24, rng.integers(-128, 128, (24, 8, 3, 3)) % P, params), 2, 3, 2048,
+                 band_only=True)
+    assert (p2.schedule, p2.post, p2.batchable) == (2, True, True)
