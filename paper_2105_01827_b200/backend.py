@@ -198,6 +198,7 @@ class Context:
         self._h = h
         self._enc_counter = 0
         self.seed = params.seed
+        self.own_key_steps = set()    # rotation keys drawn from this context's own randomness source
         if secret is None:
             secret = sampling.secret(self._rng(0), self.N)
         self.set_secret(secret)
@@ -272,6 +273,7 @@ class Context:
             return
         if a is None:
             a, e = sampling.rotation_key_randomness(self._rng(1, step), self.bfv, self.params.sigma)
+            self.own_key_steps.add(step)
         a = np.ascontiguousarray(a, dtype=np.uint64)
         e = np.ascontiguousarray(e, dtype=np.int64)
         self.call("gala_gen_rotation_key", int(step), a.ctypes.data_as(ctypes.c_void_p),

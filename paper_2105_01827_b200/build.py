@@ -16,7 +16,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 
 CUDA_LIB = "/usr/local/cuda/lib64"
-LINK = ["-L" + CUDA_LIB, "-lcublasLt", "-Xlinker", "-rpath=" + CUDA_LIB]
+LINK = ["-L" + CUDA_LIB, "-Xlinker", "-rpath=" + CUDA_LIB]
 
 
 def nvcc() -> str:

@@ -987,73 +987,16 @@ __device__ __forceinline__ u64 kg_rec_redc(const uint32_t* x, long long bias, ul
     return csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q);
 }
 
-// One word of the integer first-Add back from its byte planes: (sum_b (C[8 pos + b][m] + 128 rowsum)
-// 256^b) mod q.  C is the int32 GEMM output (column-major, leading dimension ld).  The signed
-// 128-bit total is made non-negative with a multiple of q (off >= 2^90) and reduced exactly with
-// two Montgomery steps.
-__device__ __forceinline__ u64 kg_rec_word(const int32_t* __restrict__ C, long long pos, int ld, int m, long long bias,
-                                           ulonglong2 off, const ModC& md)
-{
-    __int128 t = 0;
-#pragma unroll
-    for (int b = 7; b >= 0; b--) t = (t << 8) + (__int128)((long long)C[(8 * pos + b) * ld + m] + bias);
-    unsigned __int128 u = (unsigned __int128)(t + (((__int128)off.x << 64) | (__int128)off.y));
-    const u64 r = csub(redc_lazy((u64)(u >> 64), (u64)u, md), md.q);   // u 2^-64 mod q
-    return mont_mul(r, md.r2, md);                                      // * 2^64 -> u mod q
-}
-
-// pre-mask form: acc[m][pos] = word m of the GEMM, pos = (comp, j, i) over the extended basis
-__global__ void k_kg_recombine(DevCtx c, const int32_t* __restrict__ C, const int32_t* __restrict__ rowsum, int Mr,
-                               int Mp, const ulonglong2* __restrict__ off, u64* __restrict__ acc)
-{
-    const long long MN = (long long)c.M * c.N, P = 2 * MN;
-    const long long total = P * Mr;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int m = (int)(e % Mr);
-        const long long pos = e / Mr;
-        const int j = (int)((pos % MN) / c.N);
-        acc[(long long)m * P + pos] = kg_rec_word(C, pos, Mp, m, 128LL * rowsum[m], off[j], c.mod[j]);
-    }
-}
-
-// post-mask form: acc[m][pos] = sum_beta Mask[beta][j][i] (.) word (m nb + beta) of the GEMM
-__global__ void k_kg_recombine_post(DevCtx c, const int32_t* __restrict__ C, const int32_t* __restrict__ rowsum, int Mr,
-                                    int nb, int Mp, const ulonglong2* __restrict__ off,
-                                    const ulonglong2* __restrict__ masks, u64* __restrict__ acc)
-{
-    const long long MN = (long long)c.M * c.N, P = 2 * MN;
-    const long long total = P * Mr;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-         e += (long long)gridDim.x * blockDim.x) {
-        const int m = (int)(e % Mr);
-        const long long pos = e / Mr, jl = pos % MN;
-        const int j = (int)(jl / c.N);
-        const ModC md = c.mod[j];
-        u64 a = 0;
-        for (int beta = 0; beta < nb; beta++) {   // masks are Montgomery-form Shoup pairs
-            const int r = m * nb + beta;
-            uint32_t x[8];
-#pragma unroll
-            for (int b = 0; b < 8; b++) x[b] = (uint32_t)C[(8 * pos + b) * Mp + r];
-            const u64 w = kg_rec_redc(x, 128LL * rowsum[r], off[j], md);
-            const ulonglong2 mk = __ldg(masks + (long long)beta * MN + jl);
-            a = add_mod(a, csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q), md.q);
-        }
-        acc[(long long)m * P + pos] = a;
-    }
-}
-
 // ---------------------------------------------------------------------------
-// Conv schedule 2, post-mask form, fused on the 5th-generation tensor cores (tcgen05):
-//   D[(m, beta)][(pos, b)] = sum_K A[(m, beta)][K] * Bt[8 pos + b][K]          (int8 x int8 -> int32, TMEM)
-//   acc[m][pos]            = sum_beta Mask[beta][pos] (.) rec(D[(m, beta)][(pos, 0..7)])  mod q_j
-// One CTA owns a 128-row block of A (resident in shared memory) and walks 256-column tiles of Bt
-// (32 QP words x 8 byte planes).  Thread 0 issues K/32 tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32)
-// from SWIZZLE_NONE K-major descriptors and commits to an mbarrier; the 4 warps then read their 32
-// TMEM lanes (= rows) with tcgen05.ld.32x32b.x8 (one QP word's 8 byte sums per load), rebuild each
-// word mod q exactly, multiply by the row's band mask and sum the nb bands with warp shuffles.
-// No int32 GEMM output ever reaches HBM.
+// Conv schedule 2 first-Add, fused on the 5th-generation tensor cores (tcgen05):
+//   D[row][(pos, b)] = sum_K A[row][K] * Bt[8 pos + b][K]                           (int8 x int8 -> int32, TMEM)
+//   post-mask form, rows (m, beta):  acc[m][pos] = sum_beta Mask[beta][pos] (.) rec(D[(m, beta)][(pos, 0..7)])
+//   pre-mask form (masks already applied to the K columns by k_kg_zy), rows m:  acc[m][pos] = rec(D[m][(pos, 0..7)])
+// all mod q_j.  The A and B K-chunks of each (128-row block, 256-column tile) job stream through a
+// shared-memory ring; one lane issues the K/32 tcgen05.mma.kind::i8 (M = 128, N = 256, K = 32) from
+// SWIZZLE_NONE K-major descriptors; 16 epilogue warps read TMEM with tcgen05.ld.32x32b.x32, rebuild
+// each word mod q exactly, multiply by the band mask (or by 2^64 mod q_j in the pre-mask form) and
+// sum the nb bands with warp shuffles.  No int32 GEMM output ever reaches HBM.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -1130,7 +1073,8 @@ __global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8
                                                            const int32_t* __restrict__ rowsum, int rows_real, int rbs,
                                                            int nb, int Mr, const int8_t* __restrict__ Bcan, int Kp,
                                                            int ntiles, const ulonglong2* __restrict__ off,
-                                                           const ulonglong2* __restrict__ masks, u64* __restrict__ accq,
+                                                           const ulonglong2* __restrict__ masks,
+                                                           const ulonglong2* __restrict__ one, u64* __restrict__ accq,
                                                            int tiles_per_batch)
 {
     extern __shared__ __align__(128) uint8_t kg_sm[];
@@ -1237,9 +1181,11 @@ __global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8
             const long long pos0 = (tile - bat * tiles_per_batch) * (KG_TC_N / 8);
             const int jl0 = (int)(pos0 % MN);
             ulonglong2* sm = sMask + acc * nb * 32;
-            for (int q = et; q < nb * 32; q += KG_TC_EPI_WARPS * 32)
-                sm[q] = __ldg(masks + (long long)(q >> 5) * MN + jl0 + (q & 31));
-            asm volatile("bar.sync 1, %0;" ::"n"(KG_TC_EPI_WARPS * 32));
+            if (masks != nullptr) {
+                for (int q = et; q < nb * 32; q += KG_TC_EPI_WARPS * 32)
+                    sm[q] = __ldg(masks + (long long)(q >> 5) * MN + jl0 + (q & 31));
+                asm volatile("bar.sync 1, %0;" ::"n"(KG_TC_EPI_WARPS * 32));
+            }
             const int R = rb * 128 + r;
             const bool row_ok = R < rows_real;
             const int m = R / nb, beta = R - m * nb;
@@ -1247,6 +1193,7 @@ __global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8
             const int jq = jl0 / c.N;                                // a tile never straddles a prime
             const ModC md = c.mod[jq];
             const ulonglong2 o = off[jq];
+            const ulonglong2 one_j = one[jq];                        // pre-mask form: x 2^64 undoes the REDC
             mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll 1
@@ -1274,7 +1221,7 @@ __global__ void __launch_bounds__(KG_TC_THREADS, 1) k_kg_tc(DevCtx c, const int8
                     v[w4] = 0;
                     if (row_ok) {
                         const u64 w = kg_rec_redc(x + 8 * w4, bias, o, md);
-                        const ulonglong2 mk = sm[beta * 32 + p0 + w4];   // Montgomery-form mask
+                        const ulonglong2 mk = masks != nullptr ? sm[beta * 32 + p0 + w4] : one_j;   // Montgomery-form mask
                         v[w4] = csub(shoup_lazy_sf(w, mk.x, mk.y, md.q), md.q);
                     }
                 }

@@ -4,7 +4,6 @@
 // Every schedule here mirrors the CPU oracle (oracle/bfv_oracle.c) operation
 // for operation, so ciphertext words agree exactly.  See include/gala_b200.h.
 #include <cuda_runtime.h>
-#include <cublasLt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -138,7 +137,6 @@ struct gala_ctx {
     };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;
-    cublasLtHandle_t lt = nullptr;            // int8 tensor-core GEMM of the conv schedule 2 first-Add
     u64* d_kg_off = nullptr;                  // per prime: multiple of q >= 2^90 (128-bit, hi/lo)
     int num_sms = 148;
 };
@@ -571,7 +569,6 @@ static void free_ctx(gala_ctx* c)
         cudaEventDestroy(r.b);
     }
     for (auto e : c->pool) cudaEventDestroy(e);
-    if (c->lt) cublasLtDestroy(c->lt);
     if (c->d_kg_off) cudaFree(c->d_kg_off);
     delete c;
 }
@@ -1712,58 +1709,6 @@ int gala_kg2_encode_masks(gala_ctx* c, int k_h, int k_w, int u_w, int u_h, int p
     return GALA_OK;
 }
 
-static int lt_gemm_i8(gala_ctx* c, const int8_t* A, int lda, const int8_t* Bm, int ldb, int32_t* C, int ldc, int m,
-                      long long n, int k, int beta)
-{
-    // C[m x n] (column-major, int32) = A^T B (+ C), A column-major [k x m], B column-major [k x n]
-    if (!c->lt && cublasLtCreate(&c->lt) != CUBLAS_STATUS_SUCCESS) return set_err(GALA_ERR_CUDA, "cublasLtCreate failed");
-    cublasLtMatmulDesc_t op = nullptr;
-    cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
-    cublasLtMatmulPreference_t pref = nullptr;
-    const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
-    const int32_t alpha = 1, bet = beta;
-    const size_t ws_bytes = 32u << 20;
-    void* ws = nullptr;
-    int rc = GALA_OK;
-    cublasLtMatmulHeuristicResult_t heur{};
-    int found = 0;
-    cublasStatus_t st = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32I, CUDA_R_32I);
-    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta));
-    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb));
-    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&la, CUDA_R_8I, k, m, lda);
-    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&lb, CUDA_R_8I, k, n, ldb);
-    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32I, m, n, ldc);
-    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulPreferenceCreate(&pref);
-    if (st == CUBLAS_STATUS_SUCCESS)
-        st = cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws_bytes, sizeof(ws_bytes));
-    if (st == CUBLAS_STATUS_SUCCESS) st = cublasLtMatmulAlgoGetHeuristic(c->lt, op, la, lb, lc, lc, pref, 1, &heur, &found);
-    if (st != CUBLAS_STATUS_SUCCESS || found == 0) {
-        rc = set_err(GALA_ERR_CUDA, "cuBLASLt int8 GEMM setup failed (status %d, %d algos)", (int)st, found);
-    } else {
-        rc = scratch(c, (char**)&ws, heur.workspaceSize ? heur.workspaceSize : 8);
-        if (rc == GALA_OK) {
-            if (c->prof_on) {
-                cudaEvent_t a, b;
-                prof_begin(c, &a, &b);
-                st = cublasLtMatmul(c->lt, op, &alpha, A, la, Bm, lb, &bet, C, lc, C, lc, &heur.algo, ws, heur.workspaceSize,
-                                    c->stream);
-                prof_end(c, "cublasLt_i8_gemm", a, b);
-            } else {
-                st = cublasLtMatmul(c->lt, op, &alpha, A, la, Bm, lb, &bet, C, lc, C, lc, &heur.algo, ws, heur.workspaceSize,
-                                    c->stream);
-            }
-            if (st != CUBLAS_STATUS_SUCCESS) rc = set_err(GALA_ERR_CUDA, "cublasLtMatmul failed (status %d)", (int)st);
-            release(c, ws);
-        }
-    }
-    if (pref) cublasLtMatmulPreferenceDestroy(pref);
-    if (lc) cublasLtMatrixLayoutDestroy(lc);
-    if (lb) cublasLtMatrixLayoutDestroy(lb);
-    if (la) cublasLtMatrixLayoutDestroy(la);
-    if (op) cublasLtMatmulDescDestroy(op);
-    return rc;
-}
-
 static unsigned __int128 kg_offset(u64 q)
 {
     const unsigned __int128 two90 = (unsigned __int128)1 << 90;
@@ -1781,7 +1726,9 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     if (n_ib <= 0 || k <= 0 || nb <= 0 || c_n <= 0 || Mr <= 0 || Mr % c_n) return set_err(GALA_ERR_DIM, "bad schedule-2 dims");
     const int Kreal = n_ib * k * (post ? 1 : nb);
     const int rows = post ? Mr * nb : Mr;     // GEMM rows
-    if (Kp % 16 || Kp < Kreal) return set_err(GALA_ERR_DIM, "Kp=%d must be a multiple of 16 covering K=%d", Kp, Kreal);
+    if (Kp % 32 || Kp < Kreal) return set_err(GALA_ERR_DIM, "Kp=%d must be a multiple of 32 covering K=%d", Kp, Kreal);
+    if (post && (nb > 32 || 32 % nb)) return set_err(GALA_ERR_DIM, "post-mask form needs nb | 32 (got %d)", nb);
+    if (N % 32) return set_err(GALA_ERR_DIM, "ring degree below 32");
     // every int8 x int8 product has |a b| <= 128 * 128 = 2^14 (both operands may be -128: coefficients
     // and 0x80-biased bytes), so the int32 GEMM sums stay exact while Kp * 2^14 <= INT32_MAX (Kp < 2^17)
     if ((long long)Kp * 16384 > 2147483647LL) return set_err(GALA_ERR_DIM, "K too large for exact int32 accumulation");
@@ -1798,8 +1745,9 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         if (!gala_has_rotation_key(c, d * band_step))
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, d * band_step));
     if (!c->d_kg_off) {
-        // [0, 2 GALA_MAXM): 128-bit offsets (hi, lo) per prime; [2 GALA_MAXM, 4 GALA_MAXM): (P mod q_j, Shoup)
-        std::vector<u64> off(4 * GALA_MAXM, 0);
+        // [0, 2 GALA_MAXM): 128-bit offsets (hi, lo) per prime; [2 GALA_MAXM, 4 GALA_MAXM): (P mod q_j, Shoup);
+        // [4 GALA_MAXM, 6 GALA_MAXM): (2^64 mod q_j, Shoup) -- the "mask" of the pre-mask epilogue
+        std::vector<u64> off(6 * GALA_MAXM, 0);
         const u64 P = c->primes[L];
         for (int j = 0; j < M; j++) {
             unsigned __int128 o = kg_offset(c->primes[j]);
@@ -1808,6 +1756,9 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
             const u64 pj = P % c->primes[j];
             off[2 * GALA_MAXM + 2 * j] = pj;
             off[2 * GALA_MAXM + 2 * j + 1] = (u64)((((unsigned __int128)pj) << 64) / c->primes[j]);
+            const u64 rj = (u64)((((unsigned __int128)1) << 64) % c->primes[j]);
+            off[4 * GALA_MAXM + 2 * j] = rj;
+            off[4 * GALA_MAXM + 2 * j + 1] = (u64)((((unsigned __int128)rj) << 64) / c->primes[j]);
         }
         CK(cudaMalloc(&c->d_kg_off, sizeof(u64) * off.size()));
         CK(cudaMemcpy(c->d_kg_off, off.data(), sizeof(u64) * off.size(), cudaMemcpyHostToDevice));
@@ -1853,11 +1804,8 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         KLAUNCH(c, "k_digits_perm", k_digits_perm<<<(unsigned)(n_in * L * L), nt, c->smem_ntt, c->stream>>>(
                                         c->dc, (const TermDesc*)d_blob, d_gal, blk_words));
     }
-    // fused tcgen05 path (post-mask form, bands within a warp, K in 32-byte steps): the byte planes are
-    // written in the tensor-core tile order so every pipeline stage is one bulk copy
-    const bool tc = post && nb <= 32 && (32 % nb) == 0 && Kp % 32 == 0 && (c->dc.N % 32) == 0 &&
-                    getenv("GALA_KG_NO_TC") == nullptr;
-    if (nbatch > 1 && !tc) return set_err(GALA_ERR_PARAM, "batched convolution needs the fused tensor-core post-mask path");
+    // the byte planes are written in the tensor-core tile order so every k_kg_tc pipeline stage is one
+    // bulk copy
     // 2. fused key switch (no ModDown) + band masks -> biased bytes, K-contiguous: Bt[8 WQ][Kp]
     int8_t* Bt;
     RET(scratch(c, &Bt, (size_t)8 * WQ * Kp * nbatch));
@@ -1868,7 +1816,7 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
 #define KG_ZY(LL)                                                                                                  \
     KLAUNCH(c, "k_kg_zy", k_kg_zy<LL><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1,                \
                                                                    post ? nullptr : (const ulonglong2*)masks, pm, k,  \
-                                                                   nb_y, n_ib, Kp, Bt, tc ? 1 : 0))
+                                                                   nb_y, n_ib, Kp, Bt, 1))
         switch (L) {
             case 1: KG_ZY(1); break;
             case 2: KG_ZY(2); break;
@@ -1882,8 +1830,11 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     release(c, d_blob);
     u64* accq;
     RET(scratch(c, &accq, (size_t)nbatch * Mr * WQ));
-    if (tc) {
-        // 3+4. first-Add on the tensor cores with the byte recombination and band masks in the epilogue
+    {
+        // 3+4. first-Add on the tensor cores (k_kg_tc) with the byte recombination in the epilogue: post-mask,
+        // GEMM rows (m, beta) times their band masks and summed over the nb bands; pre-mask (masks already
+        // in the K columns), one GEMM row per accumulator and no mask (the 2^64 mod q_j constant instead)
+        const int nb_e = post ? nb : 1;
         const int rows_p = (rows + 127) / 128 * 128;
         int8_t* Acan;
         RET(scratch(c, &Acan, (size_t)rows_p * Kp));
@@ -1893,38 +1844,13 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         const int rbs = rows_p / 128;
         long long jobs = (long long)ntiles * rbs;
         const int grid = (int)(jobs < c->num_sms ? jobs : c->num_sms);
-        const size_t smem = (size_t)KG_TC_STAGES * KG_TC_KCS * (128 + KG_TC_N) * 16 + 2 * 512 * (size_t)nb;
+        const size_t smem = (size_t)KG_TC_STAGES * KG_TC_KCS * (128 + KG_TC_N) * 16 + 2 * 512 * (size_t)nb_e;
         KLAUNCH(c, "k_kg_tc", k_kg_tc<<<grid, KG_TC_THREADS, smem, c->stream>>>(
-                                  c->dc, Acan, rowsum, rows, rbs, nb, Mr, Bt, Kp, ntiles, (const ulonglong2*)c->d_kg_off,
-                                  (const ulonglong2*)masks, accq, (int)(8 * WQ / KG_TC_N)));
+                                  c->dc, Acan, rowsum, rows, rbs, nb_e, Mr, Bt, Kp, ntiles, (const ulonglong2*)c->d_kg_off,
+                                  post ? (const ulonglong2*)masks : nullptr, (const ulonglong2*)c->d_kg_off + 2 * GALA_MAXM,
+                                  accq, (int)(8 * WQ / KG_TC_N)));
         release(c, Acan);
         release(c, Bt);
-    } else {
-        // 3. exact integer first-Add on the tensor cores: C[Mp][8 WQ] = A . Bt (rows padded to 16)
-        const int Mp = (rows + 15) / 16 * 16;
-        const int8_t* A = coef;
-        int8_t* Apad = nullptr;
-        if (Mp != rows) {
-            RET(scratch(c, &Apad, (size_t)Mp * Kp));
-            CK(cudaMemsetAsync(Apad, 0, (size_t)Mp * Kp, c->stream));
-            CK(cudaMemcpyAsync(Apad, coef, (size_t)rows * Kp, cudaMemcpyDeviceToDevice, c->stream));
-            A = Apad;
-        }
-        int32_t* C;
-        RET(scratch(c, &C, (size_t)8 * WQ * Mp));
-        RET(lt_gemm_i8(c, A, Kp, Bt, Kp, C, Mp, Mp, 8 * WQ, Kp, 0));
-        release(c, Bt);
-        release(c, Apad);
-        // 4. recombine bytes -> words mod q_j over QP
-        if (post) {
-            KLAUNCH(c, "k_kg_recombine_post", k_kg_recombine_post<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
-                                                  c->dc, C, rowsum, Mr, nb, Mp, (const ulonglong2*)c->d_kg_off,
-                                                  (const ulonglong2*)masks, accq));
-        } else {
-            KLAUNCH(c, "k_kg_recombine", k_kg_recombine<<<grid_for(WQ * Mr, 256), 256, 0, c->stream>>>(
-                                             c->dc, C, rowsum, Mr, Mp, (const ulonglong2*)c->d_kg_off, accq));
-        }
-        release(c, C);
     }
     // 5. one ModDown per accumulator (straight into outs when there is no second-Perm)
     const int Mb = Mr * nbatch;              // accumulators over the batch

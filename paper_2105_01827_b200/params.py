@@ -15,11 +15,16 @@ CPU oracle (``oracle/``) are always built on the same numbers:
 * every ciphertext and special prime has the *special form* ``q = a 2^32 + 1``
   (so ``q = 1 (mod 2N)`` for every N <= 8192): the CUDA NTT's Shoup reduction
   then needs one 32-bit multiply for ``hi * q`` instead of a 64x64 product.
-* ``rns_limbs == 1`` (default for N <= 4096): one ciphertext prime
-  ``q < 2^62`` with ``q = 1 (mod 2^32 p)`` so the BFV plaintext-product
-  rounding term ``(q mod p) * k`` collapses to ``k``.
-* ``rns_limbs == 3`` (default for N >= 8192): the three largest special-form
-  primes below 2^60.
+* ``rns_limbs == 1`` (BASELINE configs 1 and 3 select it explicitly): one
+  ciphertext prime ``q < 2^62`` with ``q = 1 (mod 2^32 p)`` so the BFV
+  plaintext-product rounding term ``(q mod p) * k`` collapses to ``k``
+  (SURVEY.md A.3).  Delta / 2 = 2^41 holds one convolution or dot product of
+  the configs' sizes, not more.
+* ``rns_limbs`` 2..4: the largest special-form primes below 2^60.  The default
+  is 2 for N <= 4096 -- the smallest modulus under which every circuit the
+  reference's own test suite runs (Table VII row 4: 51 200 rotate-then-multiply
+  terms, measured at 0.49 Delta with one prime) decrypts with room to spare --
+  and 3 for N = 8192.
 * one special prime ``P`` (hybrid key switching, one digit per ciphertext
   prime): the largest special-form prime below 2^62 (L = 1) or the next one
   below the ciphertext primes (L = 3).
@@ -126,7 +131,7 @@ class BFVParams:
 
 
 def default_limbs(N: int) -> int:
-    return 1 if N <= 4096 else 3
+    return 2 if N <= 4096 else 3
 
 
 @lru_cache(maxsize=None)

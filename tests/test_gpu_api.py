@@ -278,7 +278,7 @@ def _int8(rng, shape):
 
 
 def test_cfg1_fc_16x2048_n4096():
-    params = HEParams(n=2048, seed=21)          # N = 4096, single 62-bit prime + special prime
+    params = HEParams(n=2048, rns_limbs=1, seed=21)   # N = 4096, single 62-bit prime + special prime
     assert params.bfv().N == 4096 and params.bfv().L == 1
     rng = np.random.default_rng(1)
     w, x = _int8(rng, (16, 2048)), rng.integers(0, P, 2048)
@@ -303,7 +303,7 @@ def test_cfg2_fc_1024x4096_n8192():
 
 
 def test_cfg3_conv_16x16x64_n4096():
-    params = HEParams(n=2048, seed=23)
+    params = HEParams(n=2048, rns_limbs=1, seed=23)
     rng = np.random.default_rng(3)
     kern, ch = _int8(rng, (64, 64, 3, 3)), rng.integers(0, P, (64, 16, 16))
     task = ConvTask(16, 16, 64, 3, 3, 64, kern, params)

@@ -30,8 +30,10 @@ PARAMS = HEParams()
 def test_default_params_batch():
     assert PARAMS.p == P and PARAMS.n == 2048
     b = PARAMS.bfv()
-    assert b.N == 4096 and b.L == 1 and (P - 1) % (2 * b.N) == 0
-    assert b.primes[0] % (2 * b.N * P) == 1 and b.primes[0] < 2**62 and b.special < 2**62
+    assert b.N == 4096 and b.L == 2 and (P - 1) % (2 * b.N) == 0
+    assert all(q < 2**60 for q in b.primes) and b.special < 2**60
+    one = HEParams(rns_limbs=1).bfv()          # configs 1 and 3: a single 62-bit prime, q = 1 mod 2N p
+    assert one.L == 1 and one.primes[0] % (2 * one.N * P) == 1 and one.primes[0] < 2**62 and one.special < 2**62
     assert with_overrides(PARAMS, n=4096).bfv().L == 3
 
 

@@ -168,5 +168,5 @@ def test_oracle_linearity_and_noise_margin_cfg3_shape():
     assert (u, c_i, c_o, n) == (16, 64, 64, 2048)
     # the full decryption check of this case runs in test_oracle_conv_kg_matches_reference_payload;
     # here: the margin of the single-prime parameter set
-    bfv = HEParams(n=2048, p=P).bfv()
+    bfv = HEParams(n=2048, p=P, rns_limbs=1).bfv()
     assert bfv.L == 1 and bfv.primes[0] % (2 * bfv.N * P) == 1 and bfv.log2_budget() > 40.9
