@@ -130,6 +130,9 @@ def modmul_model(N, L, T, baby, schedule):
     groups = G + (1 if G > 1 else 0)
     if schedule == 2:
         giant = G - 1
+        # ModDowns as executed: the c1 of each giant group g >= 1 (one component) + one final
+        # two-component ModDown per input ("Deferred c0 ModDown")
+        md_comps = giant + 2
         per_kernel = {
             "k_gala_e": (baby - 1) * 2 * L * M * N,
             "k_gala_mac2": G * (baby - 1) * (2 * M * N + L * N) + G * 2 * L * N,
@@ -137,8 +140,8 @@ def modmul_model(N, L, T, baby, schedule):
             "k_digits_intt": (1 + giant) * L * h,
             "k_digits_perm": (1 + giant) * L * L * h,
             "k_ks_mac": giant * 2 * L * M * N,
-            "k_ntt_inv[moddown]": groups * 2 * h,
-            "k_moddown": groups * (2 * L * h + 2 * L * N),
+            "k_ntt_inv[moddown]": md_comps * h,
+            "k_moddown": md_comps * (L * h + L * N),
         }
         return per_kernel, physical_mv_counts(N, L, T, baby, 2)["modmuls"]
     per_kernel = {
@@ -162,20 +165,23 @@ def ks_modmuls_one(N, L):
 
 
 def hbm_model(N, L, T, baby, B, tc):
-    """Algorithmic DRAM bytes per launch of the schedule-2 baby-step kernels (batch of B inputs)."""
-    M, G = L + 1, T // baby
+    """Algorithmic DRAM bytes per step of the schedule-2 baby-step kernels (batch of B inputs).
+
+    SURVEY.md 8(d) counts the layer's own objects only -- input ciphertexts, weight plaintexts,
+    keys, outputs -- and no intermediates (they are the fusion target).  Per kernel that leaves:
+    k_gala_e (-> E_jj, an intermediate): the inputs' identity digit blocks and the baby-step keys
+    (read once per 32-input tile); k_gala_tc / k_gala_mac2: the weights and the inputs' c1 (the
+    step-0 product).  The group sums U, C they write are intermediates too (the giant steps consume
+    them).  `traffic` (ncu) against these shows the round trips still to remove."""
+    M = L + 1
     MN = M * N
-    outs = B * G * (2 * MN + 2 * L * N) * 8                       # U (QP) + Cacc (Q)
-    dig = B * (L * M + L) * N * 8                                 # identity digit blocks
+    dig = B * (L * M + L) * N * 8                                 # identity digit blocks (of the inputs)
     keys = (baby - 1) * L * 2 * MN * 8
+    x_c1 = B * L * N * 8
     if tc:
         tiles = (B + 31) // 32                                    # one e_can / tc pair per 32 inputs
-        ecan = MN * 96 * 64 * 8 * tiles                           # packed E / sigma(c0), 32 input rows per tile
-        return {"k_gala_e": dig + keys * tiles + ecan,
-                "k_gala_tc": ecan + MN * 512 * 8 * tiles + B * 2 * L * N * 8 + outs}
-    e = B * (baby - 1) * (2 * MN + L * N) * 8
-    return {"k_gala_e": dig + keys + e,
-            "k_gala_mac2": e + T * MN * 8 + B * 2 * L * N * 8 + outs}
+        return {"k_gala_e": dig + keys * tiles, "k_gala_tc": T * MN * 8 * tiles + x_c1}
+    return {"k_gala_e": dig + keys, "k_gala_mac2": T * MN * 8 + x_c1}
 
 
 def run_ours(args):
@@ -427,8 +433,12 @@ def run_ours(args):
         macs = (L + 1) * N * 128 * 128 * 512 * launches_per_step  # issued int8 MACs (byte-convolution tiles)
         int8_peak = 2 * peaks.get("bf16_tflops", 1639.9) * 1e12   # dense int8 = 2x dense bf16 on B200
         a = 2 * macs / dom_s if dom_s else 0.0
+        # useful share of the issued MACs: 96 of the 128 M rows carry data (3 streams x 32 inputs), and of
+        # the 16 byte shifts x 8 byte positions of each (row, group, rotation) only the 64 with
+        # 0 <= s' - a < 8 are non-zero Toeplitz entries
         roofs["tensor"] = {"achieved": round(a / 1e12, 2), "peak": round(int8_peak / 1e12, 1), "unit": "TOP/s",
-                           "frac": round(a / int8_peak, 4),
+                           "frac": round(a / int8_peak, 4), "useful_mac_frac": 0.375,
+                           "useful_frac_of_peak": round(0.375 * a / int8_peak, 4),
                            "peak_source": "2x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)"}
     bound = max(roofs, key=lambda r: roofs[r]["frac"]) if roofs else "int"
     br = roofs.get(bound, {"achieved": 0.0, "peak": 0.0, "unit": "", "frac": 0.0})
@@ -470,10 +480,10 @@ def run_ours(args):
             "traffic_unit": "bytes per launch (dram read + write, ncu --set full, profiles/r1_ncu_summary.md)",
             "kernel_share_of_step": round(dom["ms"] / step_ms_prof, 4) if step_ms_prof else None,
             "roofs": roofs,
-            "layer": {"achieved": round(layer_achieved / 1e9, 2), "frac": round(layer_achieved / peak_modmul, 4),
+            "layer": {"modmul_equivalents_per_s": round(layer_achieved / 1e9, 2), "unit": "G/s",
                       "modmuls_per_layer": layer_modmuls,
-                      "note": "modmul-equivalents of the whole layer against the CUDA-core roof; the baby-step "
-                              "products run on the int8 tensor cores, so this can exceed 1"},
+                      "note": "the whole layer's schedule-2 modmul count per second -- a rate, not a roofline "
+                              "fraction: the baby-step products run on the int8 tensor cores, not the IMAD pipe"},
             "hbm": {"algorithmic_bytes_per_layer": int(layer_bytes),
                     "achieved_gbs": round(layer_bytes * layers / world / (total_ms / 1e3) / 1e9, 2),
                     "peak_gbs": hbm_peak},
@@ -513,6 +523,58 @@ def _oracle_for(bfv, seed):
     return o
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+_MOCK_SNIPPET = r"""
+import sys, time, json
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from gala.backend import CostMeter, HEParams
+from gala.matvec import MvTask, run_mv
+P, reps = int(sys.argv[2]), int(sys.argv[3])
+rng = np.random.default_rng(2105)
+w = rng.integers(-128, 128, (1024, 4096), dtype=np.int64) % P
+x = rng.integers(0, P, 4096, dtype=np.int64)
+params = HEParams(n=4096, p=P)
+task = MvTask(4096, 1024, w, params)
+run_mv("gala", task, x, CostMeter(), rng=1)
+ts = []
+for i in range(reps):
+    t0 = time.perf_counter()
+    run_mv("gala", task, x, CostMeter(), rng=i)
+    ts.append(time.perf_counter() - t0)
+print(json.dumps({"median_s": float(np.median(ts)), "T": task.groups}))
+"""
+
+
+def reference_mock_baseline(reps: int = 3):
+    """SURVEY.md 8(d) baseline 1: the reference package itself (baseline/_ref, unmodified), its own
+    run_mv("gala") on the config-2 matrix at n = 4096 (T = 1024), single-threaded NumPy.  It times
+    slot arithmetic on a mock backend -- no HE -- so it is reported, not compared."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "gala")):
+        return {"unavailable": "baseline/_ref not installed (see DESIGN.md section 8)"}
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    try:
+        r = subprocess.run([sys.executable, "-c", _MOCK_SNIPPET, ref, str(P), str(reps)], capture_output=True,
+                           text=True, timeout=300, env=env)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:   # noqa: BLE001
+        return {"unavailable": f"reference mock run failed: {e}"}
+    return {"value": round(1.0 / d["median_s"], 3), "unit": "layers/s", "cores": 1, "kind": "reference",
+            "sample": f"reference run_mv('gala') on the 1024x4096 matrix, HEParams(n=4096, p={P}) (T={d['T']}), "
+                      f"median of {reps}; NumPy slot mock, no HE arithmetic"}
+
+
 def cpu_baseline(ctx, layer, ct, phys_r, masked_gpu):
     """Oracle port of the same fused layer, timed on the host cores (one layer = the sample)."""
     from oracle.bfv import num_threads
@@ -534,7 +596,8 @@ def cpu_baseline(ctx, layer, ct, phys_r, masked_gpu):
     match = bool(np.array_equal(m, ctx.export_words(masked_gpu)))
     return {"value": round(1.0 / dt, 4), "unit": "layers/s", "cores": num_threads(), "kind": "port",
             "sample": "1 layer (same input ct, keys and mask as GPU input 0); oracle/bfv_oracle.c, OpenMP",
-            "words_match_gpu": match, "host_cpus": os.cpu_count()}
+            "words_match_gpu": match, "host_cpus": os.cpu_count(), "cpu_model": cpu_model(),
+            "reference_mock": reference_mock_baseline()}
 
 
 def run_reference(args):
@@ -587,7 +650,8 @@ def run_reference(args):
         "data": "synthetic", "impl": "reference",
         "config": {"workload": WORKLOAD, "N": bfv.N, "L": bfv.L, "bsgs_baby": baby, "batch_per_step": 1},
         "cpu_baseline": {"value": round(value, 4), "unit": "layers/s", "cores": num_threads(), "kind": "port",
-                         "sample": "1 layer per step: oracle/bfv_oracle.c (same algorithm), OpenMP, all host threads"},
+                         "sample": "1 layer per step: oracle/bfv_oracle.c (same algorithm), OpenMP, all host threads",
+                         "cpu_model": cpu_model(), "host_cpus": os.cpu_count()},
         "e2e": {"value": round(value, 4), "unit": "layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference package's own backend is a pure-Python slot mock without HE arithmetic; "
                 "the CPU arm runs the restated RNS-BFV algorithm (oracle/) on the host cores",

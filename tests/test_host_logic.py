@@ -195,6 +195,16 @@ def test_table_v_counts():
 def test_physical_work_model():
     w = physical_mv_counts(8192, 3, 512, 32)
     assert w["rotations"] == 511 and w["moddowns"] == 17 and w["modmuls"] > 4e8
+    # schedule 2 as executed (b = 64, G = 8): 7 one-component inner ModDowns (the giant groups' c1)
+    # + one final two-component ModDown = 9 ModDown components, not 9 two-component ModDowns
+    w2 = physical_mv_counts(8192, 3, 512, 64, schedule=2)
+    assert w2["moddown_components"] == 9 and w2["moddowns"] == 8
+    h = 8192 // 2 * 13
+    one = 4 * h + 3 * 8192
+    decomp, giant = (3 + 9) * h, 7 * ((3 + 9) * h + 2 * 3 * 4 * 8192)
+    baby = 63 * 2 * 3 * 4 * 8192 + 8 * 63 * (2 * 4 * 8192 + 3 * 8192) + 8 * 2 * 3 * 8192
+    mask = h + 3 * h + 3 * 8192
+    assert w2["modmuls"] == decomp + baby + giant + 9 * one + mask
 
 
 # --- meters / config -----------------------------------------------------------------
