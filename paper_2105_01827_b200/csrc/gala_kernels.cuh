@@ -1696,6 +1696,354 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
 }
 
 // ---------------------------------------------------------------------------
+// Fused schedule-2 baby steps: the E_jj key products computed straight into the tcgen05 A stage.
+//
+// k_gala_tc above reads its A tiles (E_jj, sigma_jj(c0) as bytes) from Ecan, which k_gala_e_can
+// writes: 1.5 GB out and 1.75 GB back per 32-input tile, the largest HBM round trip of the FC step.
+// k_gala_tcf computes the A tile of each position in shared memory instead.  E warps (lane = input
+// bi of the tile, one warp per K chunk kc = (jj = 2 kc, 2 kc + 1)) form
+//     E_jj[c] = sum_i sigma_jj(D_i)[p] ksk_jj[i][c][p]       (AccPP partial products, one REDC)
+// and sigma_jj(c0)[p], and store them as the three 16-byte rows (c0 stream, c1 stream, x.c0 stream)
+// of chunk kc in the core-matrix layout; 32 lanes write 512 contiguous bytes.  The digit blocks of
+// the tile are read input-minor (Dt[slot][k][32], k_gala_dt) so a warp's gather of sigma_jj(k) for
+// its 32 inputs is one coalesced 256-byte load.  The MMA lane, expanders and epilogue are
+// k_gala_tc's; the stage's full barrier counts the E warps' arrivals instead of TMA bytes.
+//
+// Dblk [b][(L M + L)][N] of the tile's inputs -> Dt [(L M + L)][N][32] (inputs >= B zero)
+__global__ void k_gala_dt(DevCtx c, const u64* __restrict__ Dblk, int B, u64* __restrict__ Dt)
+{
+    __shared__ u64 t[32][33];
+    const int N = c.N;
+    const long long bw = (long long)(c.L * c.M + c.L) * N;
+    const long long nk = bw / 32;   // 32-word column blocks over (slot, k)
+    const int x = threadIdx.x & 31, y = threadIdx.x >> 5;     // 256 threads: 8 rows per pass
+    for (long long blk = blockIdx.x; blk < nk; blk += gridDim.x) {
+        const long long w0 = blk * 32;
+        for (int b = y; b < 32; b += 8) t[b][x] = b < B ? __ldcs((const unsigned long long*)(Dblk + b * bw + w0 + x)) : 0ull;
+        __syncthreads();
+        for (int kk = y; kk < 32; kk += 8) Dt[(w0 + kk) * 32 + x] = t[x][kk];
+        __syncthreads();
+    }
+}
+
+// keys of the baby rotations position-major: Kt[p][jj][6] = (k_0^0, k_0^1, k_1^0, k_1^1, k_2^0, k_2^1) of
+// ksk_jj (digit i, component c) at position p -- an E warp's keys for one chunk are 96 contiguous bytes
+// (zero for jj = 0 and jj >= baby)
+template <int L>
+__global__ void k_gala_kt(DevCtx c, const u64* const* __restrict__ keys, int baby, u64* __restrict__ Kt)
+{
+    const long long MN = (long long)c.M * c.N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN * 64; e += (long long)gridDim.x * blockDim.x) {
+        const int jj = (int)(e / MN);
+        const long long p = e - jj * MN;
+        u64 v[2 * L];
+#pragma unroll
+        for (int w = 0; w < 2 * L; w++) v[w] = (jj >= 1 && jj < baby) ? __ldg(keys[jj] + w * MN + p) : 0ull;
+        u64* o = Kt + (p * 64 + jj) * (2 * L);
+#pragma unroll
+        for (int w = 0; w < 2 * L; w++) o[w] = v[w];
+    }
+}
+
+#ifndef GTCF_NE
+#define GTCF_NE 7                          // E warps (24 warps in all: 6 per SM sub-partition)
+#endif
+#define GTCF_WARPS (18 + GTCF_NE - 1)            // warp 0 + warps 18.. are E warps
+#define GTCF_THREADS (GTCF_WARPS * 32)
+// registers are allocated per SM sub-partition (16384 each, warps dealt round-robin)
+#define GTCF_MAXREG ((16384 / (((GTCF_WARPS + 3) / 4) * 32)) & ~7)
+template <int L>
+__global__ void __maxnreg__(GTCF_MAXREG) k_gala_tcf(DevCtx c, const u64* __restrict__ Dt,
+                                                             const u64* __restrict__ Kt,
+                                                             const unsigned* __restrict__ gal,
+                                                             const u64* __restrict__ wT, const u64* __restrict__ X,
+                                                             int baby, int G, int B,
+                                                             u64* __restrict__ U, u64* __restrict__ Cacc)
+{
+    extern __shared__ __align__(128) uint8_t gtc_sm[];
+    constexpr int M = L + 1;
+    __shared__ uint64_t full[GTC_NST], empty[GTC_NST], tfull[2], tempty[2], bfull[2], bempty[2];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ u64 s_w0[4][8];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int N = c.N, logN = c.logN;
+    const long long MN = (long long)M * N, npos = MN;
+    const long long per = ((npos + gridDim.x - 1) / gridDim.x + 3) & ~3LL;
+    const long long p0 = blockIdx.x * per, p1 = p0 + per < npos ? p0 + per : npos;
+    uint8_t* sB = gtc_sm;
+    uint8_t* sSt = gtc_sm + 2 * GTC_BB_BYTES;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < GTC_NST; i++) {
+            mbar_init(&full[i], GTCF_NE);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 8);
+            mbar_init(&bfull[i], 8);
+            mbar_init(&bempty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base_sh;
+    if (warp == 0 || warp >= 18) {   // E warps: lane = input bi, chunks kc = ew, ew + NE, ...
+        constexpr int NCH = (32 + GTCF_NE - 1) / GTCF_NE;
+        const int ew = warp == 0 ? 0 : warp - 17;
+        const int nch = (32 - ew + GTCF_NE - 1) / GTCF_NE;   // this warp's chunks
+        const int bi = lane;
+        const uint32_t NN = (uint32_t)N;
+        // keys of the warp's chunks at one position: lane l < 6 L holds word l % (2 L) of jj = 2 kc + l / (2 L)
+        u64 kcur[NCH], knext[NCH];
+        auto load_keys = [&](long long pp, u64* kr) {
+#pragma unroll
+            for (int ci = 0; ci < NCH; ci++) {
+                const int kc = ew + ci * GTCF_NE;
+                kr[ci] = (ci < nch && lane < 4 * L) ? __ldg(Kt + (pp * 64 + 2 * kc) * (2 * L) + lane) : 0ull;
+            }
+        };
+        // the chunk's gathered words: d[h][i] = sigma_jj(D_i)[p], d[h][L] = sigma_jj(c0)[p]
+        auto load_d = [&](int kc, int j, int k, u64 (*d)[L + 1]) {
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int jj = 2 * kc + h;
+                const bool ok = jj < baby && bi < B;
+                const int src = jj == 0 ? k : auto_src(k, gal[jj < baby ? jj : 0], logN);
+#pragma unroll
+                for (int i = 0; i <= L; i++) {
+                    const uint32_t slot = i < L ? (uint32_t)(i * M + j) : (uint32_t)(L * M + j);
+                    const bool need = ok && (i < L ? jj >= 1 : j < L);
+                    d[h][i] = need ? __ldg(Dt + ((slot * NN + (uint32_t)src) * 32u + (uint32_t)bi)) : 0ull;
+                }
+            }
+        };
+        int s = 0;
+        uint32_t ph = 0;
+        int j = (int)(p0 / N), k = (int)(p0 - (long long)j * N);
+        if (p0 < p1) load_keys(p0, kcur);
+        for (long long p = p0; p < p1; p++) {
+            const u64 q = c.mod[j].q;
+            if (p + 1 < p1) load_keys(p + 1, knext);
+            u64 da[2][L + 1], db[2][L + 1];
+            load_d(ew, j, k, da);
+            mbar_wait(&empty[s], ph ^ 1);
+            uint8_t* st = sSt + s * GTC_STAGE;
+#pragma unroll
+            for (int ci = 0; ci < NCH; ci++) {
+                if (ci >= nch) break;
+                const int kc = ew + ci * GTCF_NE;
+                if (ci + 1 < nch) load_d(kc + GTCF_NE, j, k, (ci & 1) ? da : db);
+                u64 (*d)[L + 1] = (ci & 1) ? db : da;
+                u64 e0[2], e1[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    AccPP<true> s0, s1;
+#pragma unroll
+                    for (int i = 0; i < L; i++) {
+                        const u64 ka = __shfl_sync(0xffffffffu, kcur[ci], h * 2 * L + 2 * i);
+                        const u64 kb = __shfl_sync(0xffffffffu, kcur[ci], h * 2 * L + 2 * i + 1);
+                        if (i == 0) {
+                            s0.set(d[h][i], ka);
+                            s1.set(d[h][i], kb);
+                        } else {
+                            s0.mac(d[h][i], ka);
+                            s1.mac(d[h][i], kb);
+                        }
+                    }
+                    e0[h] = s0.reduce_sf(q);   // zero keys (jj = 0, jj >= baby) and zero digits give 0
+                    e1[h] = s1.reduce_sf(q);
+                }
+                // rows r = stream 32 + bi of chunk kc: (r / 8) 128 + (r % 8) 16 within the chunk's 1.5 KB
+                uint8_t* cb = st + kc * 1536 + (bi >> 3) * 128 + (bi & 7) * 16;
+                *(ulonglong2*)(cb) = make_ulonglong2(e0[0], e0[1]);
+                *(ulonglong2*)(cb + 512) = make_ulonglong2(e1[0], e1[1]);
+                *(ulonglong2*)(cb + 1024) = make_ulonglong2(d[0][L], d[1][L]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);
+            if (++s == GTC_NST) {
+                s = 0;
+                ph ^= 1;
+            }
+            if (++k == N) {
+                k = 0;
+                j++;
+            }
+#pragma unroll
+            for (int ci = 0; ci < NCH; ci++) kcur[ci] = knext[ci];
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (long long p = p0; p < p1; p++, it++) {
+                const int acc = it & 1;
+                mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
+                mbar_wait(&full[s], ph);
+                const uint32_t sa = smem_u32(sSt + s * GTC_STAGE);
+                mbar_wait(&bfull[acc], (uint32_t)((it >> 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sb = smem_u32(sB + acc * GTC_BB_BYTES);
+                const uint32_t d = tmem + (uint32_t)(acc * 128);
+#pragma unroll 1
+                for (int ks = 0; ks < 16; ks++) {
+                    const uint64_t ad = umma_desc_kmajor(sa + ks * 2 * 1536, 1536, 128);
+                    const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\t"
+                        "setp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                        ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
+                }
+                umma_commit(&bempty[acc]);
+                umma_commit(&empty[s]);
+                umma_commit(&tfull[acc]);
+                if (++s == GTC_NST) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 10) {   // 8 expander warps (k_gala_tc's)
+        const int et = tid - 10 * 32;
+        const int n = et >> 1, kh = et & 1;
+        const int g = n >> 4, sp = n & 15;
+        const bool act = sp < 15;
+        const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? 8 * (sp - 7) : 0;
+        ulonglong2 r[16];
+        u64 w0n = 0;
+        auto load_raw = [&](long long pp) {
+            if (pp >= p1) return;
+            const ulonglong2* src = (const ulonglong2*)(wT + pp * GTC_W_WORDS) + g * 32 + kh * 16;
+            if (act) {
+#pragma unroll
+                for (int i = 0; i < 16; i++) r[i] = __ldg(src + i);
+            }
+            if (et < 8) w0n = __ldg(wT + pp * GTC_W_WORDS + 512 + et);
+        };
+        load_raw(p0);
+        int it = 0;
+        for (long long p = p0; p < p1; p++, it++) {
+            const int b = it & 1;
+            mbar_wait(&bempty[b], (uint32_t)(((it >> 1) & 1) ^ 1));
+            if (et < 8) s_w0[it & 3][et] = w0n;
+            if (act) {
+                uint8_t* rowbase = sB + b * GTC_BB_BYTES + (n >> 3) * 4096 + (n & 7) * 16 + kh * 16 * 128;
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    *(ulonglong2*)(rowbase + i * 128) = make_ulonglong2((r[i].x >> sh_r) << sh_l, (r[i].y >> sh_r) << sh_l);
+            }
+            load_raw(p + 1);
+            asm volatile("fence.proxy.async.shared::cta;");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bfull[b]);
+        }
+    } else {   // epilogue warps 2..9 (k_gala_tc's)
+        const int lg = warp & 3, sidx = lg, bi = lane, gh = (warp - 2) >> 2;
+        const long long W = 2LL * L * N;
+        const long long gstride = sidx < 2 ? 2LL * M * N : 2LL * L * N;
+        auto rebuild = [&](const uint32_t* xg, const ModC& md) -> u64 {
+            const u64 q = md.q;
+            u64 lo5 = 0, mi5 = 0, hi5 = 0;
+#pragma unroll
+            for (int u = 0; u < 5; u++) {
+                lo5 += (u64)xg[u] << (8 * u);
+                mi5 += (u64)xg[5 + u] << (8 * u);
+                hi5 += (u64)xg[10 + u] << (8 * u);
+            }
+            const u64 lo = lo5 + (mi5 << 40);
+            u64 hi = (mi5 >> 24) + (hi5 << 16) + (lo < lo5 ? 1ull : 0ull);
+            if (hi >= 2 * q) hi -= 2 * q;
+            if (hi >= 2 * q) hi -= 2 * q;
+            if (hi >= q) hi -= q;
+            return csub(redc_lazy(hi, lo, md), q);
+        };
+        int it = 0;
+        int j = (int)(p0 / N), k = (int)(p0 - (long long)j * N);
+        for (long long p = p0; p < p1; p += 4) {
+            const ModC md = c.mod[j];
+            const bool active = (sidx < 2 || j < L) && bi < B;
+            const long long z0 = (long long)bi * G + 4 * gh;
+            u64* out0 = sidx == 3 ? Cacc + ((z0 * 2 + 1) * L + j) * (long long)N + k
+                      : sidx < 2  ? U + ((z0 * 2 + sidx) * M + j) * (long long)N + k
+                                  : Cacc + ((z0 * 2 + 0) * L + j) * (long long)N + k;
+            ulonglong2 xa = make_ulonglong2(0, 0), xb = make_ulonglong2(0, 0);
+            if (sidx == 3 && active) {
+                const ulonglong2* xs = (const ulonglong2*)(X + (long long)bi * W + (long long)(L + j) * N + k);
+                xa = __ldg(xs);
+                xb = __ldg(xs + 1);
+            }
+            u64 res[4][4];
+#pragma unroll
+            for (int pi = 0; pi < 4; pi++, it++) {
+                const int acc = it & 1;
+                mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                u64 w0[4];
+#pragma unroll
+                for (int t = 0; t < 4; t++) w0[t] = s_w0[it & 3][4 * gh + t];
+                if (sidx == 3) {
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[acc]);
+                    const u64 xc1 = pi == 0 ? xa.x : pi == 1 ? xa.y : pi == 2 ? xb.x : xb.y;
+#pragma unroll
+                    for (int t = 0; t < 4; t++) res[pi][t] = mont_mul(xc1, w0[t], md);
+                } else {
+                    uint32_t x[32];
+                    const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 128 + gh * 64);
+#pragma unroll
+                    for (int hf = 0; hf < 2; hf++) {
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+                            "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+                            "%30, %31}, [%32];"
+                            : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),
+                              "=r"(x[7]), "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]),
+                              "=r"(x[14]), "=r"(x[15]), "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]),
+                              "=r"(x[21]), "=r"(x[22]), "=r"(x[23]), "=r"(x[24]), "=r"(x[25]), "=r"(x[26]), "=r"(x[27]),
+                              "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
+                            : "r"(taddr + 32 * hf));
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        if (hf == 1) {
+                            asm volatile("tcgen05.fence::before_thread_sync;");
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&tempty[acc]);
+                        }
+                        res[pi][2 * hf] = rebuild(x, md);
+                        res[pi][2 * hf + 1] = rebuild(x + 16, md);
+                    }
+                }
+            }
+            if (active) {
+#pragma unroll
+                for (int t = 0; t < 4; t++)
+                    if (4 * gh + t < G)
+                        asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(out0 + t * gstride),
+                                     "l"(res[0][t]), "l"(res[1][t]), "l"(res[2][t]), "l"(res[3][t])
+                                     : "memory");
+            }
+            k += 4;
+            if (k == N) {
+                k = 0;
+                j++;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// ---------------------------------------------------------------------------
 // Conv schedule 1 first-Add on the tensor cores.  Per Q position p = (j, x):
 //   acc[r][comp] = sum_w R[comp][w] pt[r][w]      (r = o c_n + d, w = ib k + tap)
 // with 8-byte operands is, as in k_gala_tc, one int8 byte-convolution MMA per position:

@@ -733,6 +733,10 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_gala_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_tcf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_tcf<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_tcf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_tcf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_kg1_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CKC(cudaFuncSetAttribute(k_kg1_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1163,7 +1167,42 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     // 0.0016 vs 0.0066 ms per layer at 1024 inputs); the rest of the layer stays batched over all B
     const bool tc = wcan != nullptr && B >= 16 && (B <= 32 || (T >= 128 && (B % 32 == 0 || B % 32 >= 16))) &&
                     G <= 8 && baby <= 64 && (N % 32) == 0 && getenv("GALA_FC_NO_TC") == nullptr;
-    if (tc) {
+    // fused E + MMA kernel (k_gala_tcf): experiment, slower than the k_gala_e_can / k_gala_tc pair so far
+    // (the E warps are load-latency bound at 7-11 warps per SM; profiles/r2_experiments.md)
+    const bool fused = tc && getenv("GALA_FC_FUSED") != nullptr;
+    if (fused) {
+        // tensor-core baby-step sums with the E_jj key products computed in the kernel (k_gala_tcf):
+        // per tile of 32 inputs, the digit blocks input-minor (k_gala_dt), then one persistent kernel
+        u64 *Dt, *Kt;
+        RET(scratch(c, &Dt, (size_t)blk_words * 32));
+        RET(scratch(c, &Kt, (size_t)MN * 64 * 2 * L));
+        const u64* const* dk = (const u64* const*)(d_blob + o_keys);
+        switch (L) {
+            case 1: KLAUNCH(c, "k_gala_kt", (k_gala_kt<1><<<grid_for(MN * 64, 256), 256, 0, c->stream>>>(c->dc, dk, baby, Kt))); break;
+            case 2: KLAUNCH(c, "k_gala_kt", (k_gala_kt<2><<<grid_for(MN * 64, 256), 256, 0, c->stream>>>(c->dc, dk, baby, Kt))); break;
+            case 3: KLAUNCH(c, "k_gala_kt", (k_gala_kt<3><<<grid_for(MN * 64, 256), 256, 0, c->stream>>>(c->dc, dk, baby, Kt))); break;
+            default: KLAUNCH(c, "k_gala_kt", (k_gala_kt<4><<<grid_for(MN * 64, 256), 256, 0, c->stream>>>(c->dc, dk, baby, Kt))); break;
+        }
+        for (int b0 = 0; b0 < B; b0 += 32) {
+            const int bt = B - b0 < 32 ? B - b0 : 32;
+            KLAUNCH(c, "k_gala_dt", k_gala_dt<<<c->num_sms * 8, 256, 0, c->stream>>>(c->dc, Dblk + (long long)b0 * blk_words, bt, Dt));
+            const u64* Xt = cts + (long long)b0 * 2 * L * N;
+            u64* Ut = U + (long long)b0 * G * 2 * M * N;
+            u64* Ct = Cacc + (long long)b0 * G * 2 * L * N;
+#define GALA_TCF(LL)                                                                                       \
+    KLAUNCH(c, "k_gala_tc", (k_gala_tcf<LL><<<c->num_sms, GTCF_THREADS, GTC_SMEM, c->stream>>>(               \
+                                c->dc, Dt, Kt, d_gal, (const u64*)wcan, Xt, baby, G, bt, Ut, Ct)))
+            switch (L) {
+                case 1: GALA_TCF(1); break;
+                case 2: GALA_TCF(2); break;
+                case 3: GALA_TCF(3); break;
+                default: GALA_TCF(4); break;
+            }
+#undef GALA_TCF
+        }
+        release(c, Dt);
+        release(c, Kt);
+    } else if (tc) {
         // tensor-core baby-step sums: E packed as int8 MMA operands, weights as their byte-convolution
         uint8_t* Ecan;
         RET(scratch(c, &Ecan, (size_t)MN * GTC_A_BYTES));
