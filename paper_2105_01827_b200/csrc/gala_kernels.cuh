@@ -349,6 +349,137 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fused key switch for terms rotated by ONE Galois element (FC giant steps, schedule-1 products,
+// the conv second-Perm): per (term, prime j of QP) one CTA takes the term's digit coefficients
+// d_i (k_digits_intt) to prime j -- NTT_j(d_i) for i != j, the NTT-domain limb (X (.) pt).c1[j]
+// itself for i == j -- into L shared-memory buffers, then forms the key inner product straight
+// from shared memory through the automorphism:
+//   part[t][c][j][k]  = sum_i NTT_j(d_i)[sigma(k)] ksk[i][c][j][k]      (AccPP, one REDC)
+//   cpart[t][j][k]    = (X (.) pt).c0[j][sigma(k)]                       (j < L)
+// No sigma-permuted digit block goes through HBM (k_digits_perm + k_ks_mac write and re-read one of
+// (L M + L) N words per rotation).  k_ks_sum folds the parts of each group.
+struct FusedTerm {
+    const u64* X;      // [2][L][N] NTT
+    const u64* pt;     // [L][N] Montgomery or null
+    const u64* dig;    // [L][N] digit coefficients
+    const u64* key;    // [L][2][M][N] key of the term's rotation
+    unsigned gal;
+    int c0_zero;
+};
+
+template <int L>
+__global__ void __launch_bounds__(1024, 1) k_ks_fused(DevCtx c, const FusedTerm* __restrict__ terms,
+                                                     u64* __restrict__ part, u64* __restrict__ cpart)
+{
+    extern __shared__ u64 sm[];
+    constexpr int M = L + 1;
+    const int N = c.N, logN = c.logN, PW = padded_words(N);
+    const int ti = blockIdx.x / M, j = blockIdx.x % M;
+    const FusedTerm t = terms[ti];
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+#pragma unroll 1
+    for (int i = 0; i < L; i++) {
+        u64* b = sm + i * PW;
+        if (i == j) {
+            __syncthreads();
+            for (int k = threadIdx.x; k < N; k += blockDim.x) {
+                u64 v = __ldg(t.X + (long long)(L + j) * N + k);
+                if (t.pt) v = mont_mul(v, __ldg(t.pt + (long long)j * N + k), md);
+                b[pad(k)] = v;
+            }
+        } else {
+            const u64* d = t.dig + (long long)i * N;   // d < q_i < 4 q_j: lazy NTT input
+            ntt_fwd_g([=](int k) { return ld_cs(d + k); }, b, c.twf[j], q, logN);
+        }
+    }
+    __syncthreads();
+    const long long MN = (long long)M * N;
+    u64* p0 = part + (long long)ti * 2 * MN + (long long)j * N;
+    const u64* key = t.key + (long long)j * N;
+    for (int k = threadIdx.x; k < N; k += blockDim.x) {
+        const int src = auto_src(k, t.gal, logN);
+        AccPP<true> s0, s1;   // L <= 3 canonical products per sum
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+            u64 v = sm[i * PW + pad(src)];
+            if (i != j) v = csub(csub(v, 2 * q), q);
+            const u64 ka = __ldg(key + (2 * i) * MN + k), kb = __ldg(key + (2 * i + 1) * MN + k);
+            if (i == 0) {
+                s0.set(v, ka);
+                s1.set(v, kb);
+            } else {
+                s0.mac(v, ka);
+                s1.mac(v, kb);
+            }
+        }
+        st_cs(p0 + k, s0.reduce_sf(q));
+        st_cs(p0 + MN + k, s1.reduce_sf(q));
+        if (j < L && !t.c0_zero) {
+            u64 v = __ldg(t.X + (long long)j * N + src);
+            if (t.pt) v = mont_mul(v, __ldg(t.pt + (long long)j * N + src), md);
+            st_cs(cpart + ((long long)ti * L + j) * N + k, v);
+        }
+    }
+}
+
+struct SumMember {
+    const u64* part;   // rotated member: [2][M][N] (null: step-0 member)
+    const u64* cpart;  // [L][N] sigma-copied c0 (null: zero)
+    const u64* X;      // step-0 member source
+    const u64* pt;
+};
+
+// U[g] = qp_add[g] + sum of the group's parts; Cacc[g] = q_add[g] + step-0 members (X (.) pt) + the
+// parts' sigma(c0).  grid (N / blockDim, M, G)
+__global__ void __launch_bounds__(256) k_ks_sum(DevCtx c, const SumMember* __restrict__ mem, const int* __restrict__ off,
+                                                u64* __restrict__ U, u64* __restrict__ Cacc,
+                                                const u64* __restrict__ qp_add, const u64* __restrict__ q_add)
+{
+    const int N = c.N, L = c.L, M = c.M;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, g = blockIdx.z;
+    if (k >= N) return;
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    const long long NN = N, MN = (long long)M * N;
+    u64 u0 = 0, u1 = 0, a0 = 0, a1 = 0;
+    if (qp_add) {
+        u0 = qp_add[(((long long)g * 2 + 0) * M + j) * NN + k];
+        u1 = qp_add[(((long long)g * 2 + 1) * M + j) * NN + k];
+    }
+    if (q_add && j < L) {
+        a0 = q_add[(((long long)g * 2 + 0) * L + j) * NN + k];
+        a1 = q_add[(((long long)g * 2 + 1) * L + j) * NN + k];
+    }
+    for (int it = off[g]; it < off[g + 1]; it++) {
+        const SumMember m = mem[it];
+        if (m.part == nullptr) {
+            if (j < L) {
+                u64 x0 = m.X[(long long)j * NN + k], x1 = m.X[((long long)L + j) * NN + k];
+                if (m.pt) {
+                    const u64 w = __ldg(&m.pt[(long long)j * NN + k]);
+                    x0 = mont_mul(x0, w, md);
+                    x1 = mont_mul(x1, w, md);
+                }
+                a0 = add_mod(a0, x0, q);
+                a1 = add_mod(a1, x1, q);
+            }
+            continue;
+        }
+        u0 = add_mod(u0, ld_cs(m.part + (long long)j * NN + k), q);
+        u1 = add_mod(u1, ld_cs(m.part + MN + (long long)j * NN + k), q);
+        if (j < L && m.cpart) a0 = add_mod(a0, ld_cs(m.cpart + (long long)j * NN + k), q);
+    }
+    U[(((long long)g * 2 + 0) * M + j) * NN + k] = u0;
+    U[(((long long)g * 2 + 1) * M + j) * NN + k] = u1;
+    if (j < L) {
+        Cacc[(((long long)g * 2 + 0) * L + j) * NN + k] = a0;
+        Cacc[(((long long)g * 2 + 1) * L + j) * NN + k] = a1;
+    }
+}
+
 // U[g] = sum of the chunk sums Uv[v], v in [vstart[g], vstart[g] + vcount[g]) (and Cacc likewise):
 // groups k_ks_mac split into several grid slices.  grid (N / 256, M, G)
 __global__ void k_fold_groups(DevCtx c, const u64* __restrict__ Uv, const u64* __restrict__ Cv,

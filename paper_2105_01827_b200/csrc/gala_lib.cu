@@ -268,6 +268,132 @@ struct EngMember {
 
 static const u64* key_for(gala_ctx* c, int step);
 
+static int moddown_groups(gala_ctx* c, u64* U, u64* Cacc, int G, u64* const* d_outs)
+{
+    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
+    u64* r;
+    RET(scratch(c, &r, (size_t)G * 2 * N));
+    RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
+                          "k_ntt_inv[moddown]"));
+    MdArgs a{};
+    a.r = r;
+    a.U = U;
+    a.add0 = Cacc;
+    a.add1 = Cacc + (long long)L * N;
+    a.add_is = 2LL * L * N;
+    a.out = nullptr;
+    a.out_is = 0;
+    a.outs = d_outs;
+    KLAUNCH(c, "k_moddown", k_moddown<<<G * 2 * L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, a));
+    release(c, r);
+    return GALA_OK;
+}
+
+// The fused form of rotate_engine (every rotated term has one rotation): k_digits_intt (digit
+// coefficients only), k_ks_fused (digit NTTs + key inner product per (term, prime)), k_ks_sum (group
+// sums with the step-0 members and addends), one lazy ModDown per group.  Same words.
+static int rotate_engine_fused(gala_ctx* c, const std::vector<EngTerm>& terms,
+                               const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs,
+                               const u64* qp_add, const u64* q_add)
+{
+    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
+    const int G = (int)groups.size();
+    std::vector<int> rot_idx(terms.size(), -1);
+    int n_rot = 0;
+    for (size_t t = 0; t < terms.size(); t++) {
+        if (terms[t].steps.empty()) continue;
+        if (!key_for(c, terms[t].steps[0])) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, terms[t].steps[0]));
+        rot_idx[t] = n_rot++;
+    }
+    u64 *dig = nullptr, *part = nullptr, *cpart = nullptr;
+    if (n_rot) {
+        RET(scratch(c, &dig, (size_t)n_rot * L * N));
+        RET(scratch(c, &part, (size_t)n_rot * 2 * M * N));
+        RET(scratch(c, &cpart, (size_t)n_rot * L * N));
+    }
+    std::vector<TermDesc> td;
+    std::vector<FusedTerm> ft;
+    for (size_t t = 0; t < terms.size(); t++) {
+        if (rot_idx[t] < 0) continue;
+        TermDesc d{};
+        d.X = terms[t].X;
+        d.pt = terms[t].pt;
+        d.dig = dig + (long long)rot_idx[t] * L * N;
+        d.blk = nullptr;               // no sigma-copies: k_ks_fused reads the limbs itself
+        d.rot_off = 0;
+        d.rot_cnt = 0;
+        td.push_back(d);
+        FusedTerm f{};
+        f.X = terms[t].X;
+        f.pt = terms[t].pt;
+        f.dig = d.dig;
+        f.key = key_for(c, terms[t].steps[0]);
+        f.gal = galois_of(c, terms[t].steps[0]);
+        f.c0_zero = terms[t].c0_zero ? 1 : 0;
+        ft.push_back(f);
+    }
+    std::vector<SumMember> mem;
+    std::vector<int> off;
+    for (const auto& g : groups) {
+        off.push_back((int)mem.size());
+        for (const auto& m : g) {
+            const EngTerm& T = terms[m.term];
+            SumMember sm{};
+            if (m.rot < 0) {
+                sm.X = T.X;
+                sm.pt = T.pt;
+            } else {
+                const int r = rot_idx[m.term];
+                sm.part = part + (long long)r * 2 * M * N;
+                sm.cpart = T.c0_zero ? nullptr : cpart + (long long)r * L * N;
+            }
+            mem.push_back(sm);
+        }
+    }
+    off.push_back((int)mem.size());
+    auto align = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    const size_t o_td = 0, o_ft = align(td.size() * sizeof(TermDesc));
+    const size_t o_mem = align(o_ft + ft.size() * sizeof(FusedTerm));
+    const size_t o_off = align(o_mem + mem.size() * sizeof(SumMember));
+    const size_t o_out = align(o_off + off.size() * sizeof(int));
+    std::vector<char> blob(o_out + outs.size() * sizeof(u64*));
+    if (!td.empty()) memcpy(blob.data() + o_td, td.data(), td.size() * sizeof(TermDesc));
+    if (!ft.empty()) memcpy(blob.data() + o_ft, ft.data(), ft.size() * sizeof(FusedTerm));
+    memcpy(blob.data() + o_mem, mem.data(), mem.size() * sizeof(SumMember));
+    memcpy(blob.data() + o_off, off.data(), off.size() * sizeof(int));
+    memcpy(blob.data() + o_out, outs.data(), outs.size() * sizeof(u64*));
+    char* d_blob;
+    RET(upload(c, blob.data(), blob.size(), (void**)&d_blob));
+    if (n_rot) {
+        const int nt = ntt_threads(N);
+        KLAUNCH(c, "k_digits_intt", k_digits_intt<<<(unsigned)(n_rot * L), nt, c->smem_ntt, c->stream>>>(
+                                        c->dc, (const TermDesc*)(d_blob + o_td), nullptr, 0));
+        const size_t smem = (size_t)L * padded_words(N) * 8;
+        const FusedTerm* dft = (const FusedTerm*)(d_blob + o_ft);
+        // one CTA per SM (L smem polynomials): twice the NTT kernels' threads, so the SM keeps 32 warps
+        const int ntf = N >= 1024 ? 2 * nt : nt;
+        switch (L) {
+            case 1: KLAUNCH(c, "k_ks_fused", (k_ks_fused<1><<<(unsigned)(n_rot * M), ntf, smem, c->stream>>>(c->dc, dft, part, cpart))); break;
+            case 2: KLAUNCH(c, "k_ks_fused", (k_ks_fused<2><<<(unsigned)(n_rot * M), ntf, smem, c->stream>>>(c->dc, dft, part, cpart))); break;
+            default: KLAUNCH(c, "k_ks_fused", (k_ks_fused<3><<<(unsigned)(n_rot * M), ntf, smem, c->stream>>>(c->dc, dft, part, cpart))); break;
+        }
+    }
+    u64 *U, *Cacc;
+    RET(scratch(c, &U, (size_t)G * 2 * M * N));
+    RET(scratch(c, &Cacc, (size_t)G * 2 * L * N));
+    const int th = N < 256 ? N : 256;
+    KLAUNCH(c, "k_ks_sum", k_ks_sum<<<dim3((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)G), th, 0, c->stream>>>(
+                               c->dc, (const SumMember*)(d_blob + o_mem), (const int*)(d_blob + o_off), U, Cacc, qp_add, q_add));
+    release(c, dig);
+    release(c, part);
+    release(c, cpart);
+    RET(moddown_groups(c, U, Cacc, G, (u64* const*)(d_blob + o_out)));
+    release(c, U);
+    release(c, Cacc);
+    release(c, d_blob);
+    return GALA_OK;
+}
+
 // qp_add [G][2][M][N] (optional) is added to each group's key-switch sum before its ModDown, q_add
 // [G][2][L][N] (optional) after it.
 static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
@@ -277,6 +403,12 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const int G = (int)groups.size();
     if (G == 0) return GALA_OK;
+    // every rotated term rotated by exactly one element, no hoisted identity block: the fused key
+    // switch (digit NTTs + key inner product in one kernel, no permuted block in HBM)
+    bool fusable = L <= 3 && getenv("GALA_KS_FUSED") != nullptr;
+    for (const auto& t : terms)
+        if (!t.steps.empty() && (t.steps.size() != 1 || t.ntt_block)) fusable = false;
+    if (fusable) return rotate_engine_fused(c, terms, groups, outs, qp_add, q_add);
     const long long blk_words = (long long)(L * M + L) * N;
     // rotated terms and their rotation slices
     std::vector<int> term_rot_base(terms.size(), -1);
@@ -733,6 +865,9 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_gala_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_ks_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_ks_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_ks_fused<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kMaxSmem));
     CKC(cudaFuncSetAttribute(k_gala_tcf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tcf<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tcf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
