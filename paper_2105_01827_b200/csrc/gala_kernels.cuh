@@ -965,6 +965,10 @@ __global__ void k_kg_mask_slots(DevCtx c, KgGeom g, uint32_t* __restrict__ out)
 // loads run along pos and the 16-byte stores along K (XOR swizzle: both phases conflict-free).
 #define KG_PT 32
 #define KG_KT 128
+#define KG_MAXK 64          // taps per convolution (7 x 7 = 49 at most here)
+#ifndef KG_ZU
+#define KG_ZU 2             // post-mask columns per load round
+#endif
 __device__ __forceinline__ int kg_swz(int pp, int kk) { return pp * KG_KT + (kk ^ ((pp + 4 * (kk >> 4)) & 15)); }
 
 // Montgomery-form operands [count][M][N] -> Shoup pairs (w, floor(w 2^64 / q)).  With w_m = w 2^64
@@ -995,16 +999,36 @@ __device__ __forceinline__ void bytes4x4(uint32_t x0, uint32_t x1, uint32_t x2, 
     o[3] = __byte_perm(t1, t3, 0x7632);
 }
 
-template <int L>
+// LOGN > 0: the ring degree at compile time (the MN-strided digit / key loads then take immediate
+// offsets from one address per column); 0: runtime
+template <int L, int LOGN>
 __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__ Dblk, const u64* __restrict__ X,
                                                const u64* const* __restrict__ keys, const unsigned* __restrict__ gal,
                                                const ulonglong2* __restrict__ masks, const ulonglong2* __restrict__ pconst,
                                                int k, int nb, int n_ib, int Kp, int8_t* __restrict__ Bt, int canon)
 {
     __shared__ u64 sm[KG_PT * KG_KT];
+    // per-block tables: each tap's key pointer and, per position of the block, its automorphism source
+    // index (the inner loop then issues no dependent pointer loads and no bit reversals)
+    __shared__ const u64* s_key[KG_MAXK];
+    __shared__ int s_src[KG_MAXK][KG_PT];
+    __shared__ int s_col[KG_KT];      // post-mask: column gl -> (input ib << 8) | tap, -1 past the last column
     constexpr int M = L + 1;
-    const int N = c.N, logN = c.logN, MN = M * N, P2 = 2 * MN;
+    const int N = LOGN ? (1 << LOGN) : c.N, logN = LOGN ? LOGN : c.logN, MN = M * N, P2 = 2 * MN;
     const int pos0 = blockIdx.x * KG_PT, K0 = blockIdx.y * KG_KT;
+    for (int e = threadIdx.x; e < k * KG_PT; e += blockDim.x) {
+        const int t = e / KG_PT, pp = e - t * KG_PT;
+        const int pos = pos0 + pp, comp = pos >= MN ? 1 : 0, jl = pos - comp * MN;
+        const u64* kt = keys[t];
+        if (pp == 0) s_key[t] = kt;
+        s_src[t][pp] = kt ? auto_src(jl & (N - 1), gal[t], logN) : 0;
+    }
+    if (masks == nullptr)
+        for (int gl = threadIdx.x; gl < KG_KT; gl += blockDim.x) {
+            const int g = K0 + gl;      // nb == 1 in the post-mask form
+            s_col[gl] = g < n_ib * k ? ((g / k) << 8) | (g % k) : -1;
+        }
+    __syncthreads();
     // batch element blockIdx.z: its inputs follow the previous elements' (n_ib each), its byte planes
     // continue the tile order (canon only)
     Dblk += (long long)blockIdx.z * n_ib * ((L * M + L) * (long long)N);
@@ -1025,17 +1049,73 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
         // (ib, t) of g = g0 + gl, advanced incrementally (gl steps by 8): no division in the loop
         int gfirst = g0 + w;
         int ib = gfirst / k, t = gfirst - ib * k;
+        if (masks == nullptr) {
+            // post-mask form, lean inner loop: every column's (input, tap) comes from the block's column
+            // table, addresses are 32-bit word offsets from block-invariant bases, and KG_ZU columns'
+            // loads are issued before any product (the loop is load-latency bound)
+            const uint32_t uMN = (uint32_t)MN, uN = (uint32_t)N;
+            const uint32_t dj = (uint32_t)j * uN;
+            const uint32_t xo = (uint32_t)comp * (uint32_t)L * uN + (uint32_t)jl;
+            const bool has_c0 = comp == 0 && j < L;
+            for (int gl0 = w; gl0 < gpt; gl0 += 8 * KG_ZU) {
+                u64 dv[KG_ZU][L + 1], kv[KG_ZU][L];
+                int kind[KG_ZU];   // 0: nothing, 1: P x.c0 only (step 0), 2: key switch
+#pragma unroll
+                for (int u = 0; u < KG_ZU; u++) {
+                    const int gl = gl0 + 8 * u;
+                    const int cm = gl < gpt ? s_col[gl] : -1;
+                    kind[u] = 0;
+                    if (cm >= 0 && pos < P2) {
+                        const int ibu = cm >> 8, tt = cm & 255;
+                        const u64* key = s_key[tt];
+                        if (key == nullptr) {
+                            kind[u] = 1;
+                            dv[u][0] = j < L ? __ldg(X + ((uint32_t)ibu * 2u * (uint32_t)L * uN + xo)) : 0ull;
+                        } else {
+                            kind[u] = 2;
+                            const u64* dp = Dblk + ((uint32_t)ibu * (uint32_t)bw + dj + (uint32_t)s_src[tt][pp]);
+                            const u64* kp = key + koff;
+#pragma unroll
+                            for (int l = 0; l < L; l++) {
+                                dv[u][l] = __ldg(dp + l * MN);
+                                kv[u][l] = __ldg(kp + l * 2 * MN);
+                            }
+                            dv[u][L] = has_c0 ? __ldg(dp + L * MN) : 0ull;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < KG_ZU; u++) {
+                    const int gl = gl0 + 8 * u;
+                    if (gl >= gpt) break;
+                    u64 z = 0;
+                    if (kind[u] == 1) {
+                        z = csub(shoup_lazy_sf(dv[u][0], pc.x, pc.y, q), q);
+                    } else if (kind[u] == 2) {
+                        AccPP<true> s;
+#pragma unroll
+                        for (int l = 0; l < L; l++) {
+                            if (l == 0) s.set(dv[u][0], kv[u][0]);
+                            else s.mac(dv[u][l], kv[u][l]);
+                        }
+                        z = s.reduce_sf(q);
+                        if (has_c0) z = add_mod(z, csub(shoup_lazy_sf(dv[u][L], pc.x, pc.y, q), q), q);
+                    }
+                    sm[kg_swz(pp, gl)] = z ^ 0x8080808080808080ull;
+                }
+            }
+        } else
         for (int gl = w; gl < gpt; gl += 8) {
             const int g = g0 + gl;
             const bool valid = g < G && pos < P2;
             const int tt = t;
             u64 z = 0;
             if (valid) {
-                const u64* key = keys[tt];
+                const u64* key = s_key[tt];
                 if (key == nullptr) {
                     if (j < L) z = csub(shoup_lazy_sf(__ldg(Xj + (long long)ib * 2 * L * N), pc.x, pc.y, q), q);
                 } else {
-                    const int src = auto_src(i, gal[tt], logN);
+                    const int src = s_src[tt][pp];
                     const u64* D = Dj + (long long)ib * bw + src;
                     const u64* kp = key + koff;
                     AccPP<true> s;   // L <= 4 canonical products
@@ -1101,6 +1181,138 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
     int8_t* o = Bt + (long long)pos * 8 * Kp + K0 + ch * 16;
 #pragma unroll
     for (int b = 0; b < 8; b++) *(uint4*)(o + (long long)b * Kp) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
+}
+
+// Post-mask form of k_kg_zy with BOTH key-switch components of a position in one thread: Z[0] and
+// Z[1] at (j, i) share the gathered digits sigma_t(D_l)[j][i] (and the c0 term goes to component 0),
+// so the digit gathers -- one 256-byte row per (input, tap, slot) and warp, the kernel's dominant L2
+// traffic -- are halved.  Block: 32 positions (j, i) x 128 K columns = 64 output rows of the byte
+// planes (the two components' tiles); columns come from the block's table ((ib << 8) | tap).
+// Dynamic shared memory: 2 x KG_PT x KG_KT words.
+template <int L, int LOGN>
+__global__ void __launch_bounds__(256) k_kg_zy2(DevCtx c, const u64* __restrict__ Dblk, const u64* __restrict__ X,
+                                                const u64* const* __restrict__ keys, const unsigned* __restrict__ gal,
+                                                const ulonglong2* __restrict__ pconst, int k, int n_ib, int Kp,
+                                                int8_t* __restrict__ Bt)
+{
+    extern __shared__ u64 zsm[];                 // [comp][KG_PT * KG_KT], swizzled as kg_swz
+    __shared__ const u64* s_key[KG_MAXK];
+    __shared__ int s_src[KG_MAXK][KG_PT];
+    __shared__ int s_col[KG_KT];
+    constexpr int M = L + 1;
+    const int N = LOGN ? (1 << LOGN) : c.N, logN = LOGN ? LOGN : c.logN, MN = M * N, P2 = 2 * MN;
+    const int jl0 = blockIdx.x * KG_PT, K0 = blockIdx.y * KG_KT;
+    for (int e = threadIdx.x; e < k * KG_PT; e += blockDim.x) {
+        const int t = e / KG_PT, pp = e - t * KG_PT;
+        const u64* kt = keys[t];
+        if (pp == 0) s_key[t] = kt;
+        s_src[t][pp] = kt ? auto_src((jl0 + pp) & (N - 1), gal[t], logN) : 0;
+    }
+    for (int gl = threadIdx.x; gl < KG_KT; gl += blockDim.x) {
+        const int g = K0 + gl;
+        s_col[gl] = g < n_ib * k ? ((g / k) << 8) | (g % k) : -1;
+    }
+    __syncthreads();
+    Dblk += (long long)blockIdx.z * n_ib * ((L * M + L) * (long long)N);
+    X += (long long)blockIdx.z * n_ib * 2 * L * (long long)N;
+    Bt += (long long)blockIdx.z * 8 * P2 * (long long)Kp;
+    {
+        const int pp = threadIdx.x & 31, w = threadIdx.x >> 5;
+        const int jl = jl0 + pp, j = jl >> logN, i = jl & (N - 1);
+        const u64 q = c.mod[j].q;
+        const ulonglong2 pc = pconst[j];
+        const bool has_c0 = j < L;
+        const uint32_t bw = (uint32_t)(L * M + L) * (uint32_t)N;
+        const uint32_t dj = (uint32_t)j * (uint32_t)N;
+        const uint32_t koff = (uint32_t)j * (uint32_t)N + (uint32_t)i;
+        for (int gl0 = w; gl0 < KG_KT; gl0 += 8 * KG_ZU) {
+            u64 dv[KG_ZU][L + 1], k0v[KG_ZU][L], k1v[KG_ZU][L];
+            int kind[KG_ZU];
+#pragma unroll
+            for (int u = 0; u < KG_ZU; u++) {
+                const int gl = gl0 + 8 * u;
+                const int cm = s_col[gl];
+                kind[u] = 0;
+                if (cm >= 0) {
+                    const int ibu = cm >> 8, tt = cm & 255;
+                    const u64* key = s_key[tt];
+                    if (key == nullptr) {        // step 0: Z = P x (no key switch)
+                        kind[u] = 1;
+                        const u64* xp = X + ((uint32_t)ibu * 2u * (uint32_t)L * (uint32_t)N + (uint32_t)jl);
+                        dv[u][0] = has_c0 ? __ldg(xp) : 0ull;
+                        dv[u][1] = has_c0 ? __ldg(xp + L * N) : 0ull;
+                    } else {
+                        kind[u] = 2;
+                        const u64* dp = Dblk + ((uint32_t)ibu * bw + dj + (uint32_t)s_src[tt][pp]);
+                        const u64* kp = key + koff;
+#pragma unroll
+                        for (int l = 0; l < L; l++) {
+                            dv[u][l] = __ldg(dp + l * MN);
+                            k0v[u][l] = __ldg(kp + (2 * l) * MN);
+                            k1v[u][l] = __ldg(kp + (2 * l + 1) * MN);
+                        }
+                        dv[u][L] = has_c0 ? __ldg(dp + L * MN) : 0ull;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < KG_ZU; u++) {
+                const int gl = gl0 + 8 * u;
+                u64 z0 = 0, z1 = 0;
+                if (kind[u] == 1) {
+                    z0 = csub(shoup_lazy_sf(dv[u][0], pc.x, pc.y, q), q);
+                    z1 = csub(shoup_lazy_sf(dv[u][1], pc.x, pc.y, q), q);
+                } else if (kind[u] == 2) {
+                    AccPP<true> s0, s1;
+#pragma unroll
+                    for (int l = 0; l < L; l++) {
+                        if (l == 0) {
+                            s0.set(dv[u][0], k0v[u][0]);
+                            s1.set(dv[u][0], k1v[u][0]);
+                        } else {
+                            s0.mac(dv[u][l], k0v[u][l]);
+                            s1.mac(dv[u][l], k1v[u][l]);
+                        }
+                    }
+                    z0 = s0.reduce_sf(q);
+                    z1 = s1.reduce_sf(q);
+                    if (has_c0) z0 = add_mod(z0, csub(shoup_lazy_sf(dv[u][L], pc.x, pc.y, q), q), q);
+                }
+                zsm[kg_swz(pp, gl)] = z0 ^ 0x8080808080808080ull;
+                zsm[KG_PT * KG_KT + kg_swz(pp, gl)] = z1 ^ 0x8080808080808080ull;
+            }
+        }
+    }
+    __syncthreads();
+    const int pp = threadIdx.x >> 3, ch = threadIdx.x & 7;
+    if (K0 + ch * 16 >= Kp) return;
+#pragma unroll 1
+    for (int comp = 0; comp < 2; comp++) {
+        const u64* zs = zsm + comp * KG_PT * KG_KT;
+        const long long pos = (long long)comp * MN + jl0 + pp;
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int w = 0; w < 16; w++) {
+            const u64 v = zs[kg_swz(pp, ch * 16 + w)];
+            lo[w] = (uint32_t)v;
+            hi[w] = (uint32_t)(v >> 32);
+        }
+        uint32_t pl[8][4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; q4++) {
+            uint32_t o[4];
+            bytes4x4(lo[4 * q4], lo[4 * q4 + 1], lo[4 * q4 + 2], lo[4 * q4 + 3], o);
+#pragma unroll
+            for (int b = 0; b < 4; b++) pl[b][q4] = o[b];
+            bytes4x4(hi[4 * q4], hi[4 * q4 + 1], hi[4 * q4 + 2], hi[4 * q4 + 3], o);
+#pragma unroll
+            for (int b = 0; b < 4; b++) pl[4 + b][q4] = o[b];
+        }
+        // tcgen05 tile layout: [tile = pos / 32][16-byte K chunk][256 rows (pos % 32, b)][16]
+        int8_t* o = Bt + ((((pos >> 5) * (Kp >> 4) + (K0 >> 4) + ch) * 256) + 8 * (pos & 31)) * 16;
+#pragma unroll
+        for (int b = 0; b < 8; b++) *(uint4*)(o + b * 16) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
+    }
 }
 
 // sum_b (x_b + bias) 256^b (signed, |.| < 2^90) made non-negative with off (a multiple of q >= 2^90)

@@ -865,6 +865,12 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_gala_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+#define ZY2_ATTR(LL, LN) CKC(cudaFuncSetAttribute(k_kg_zy2<LL, LN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KG_PT * KG_KT * 8))
+    ZY2_ATTR(1, 0); ZY2_ATTR(1, 12); ZY2_ATTR(1, 13);
+    ZY2_ATTR(2, 0); ZY2_ATTR(2, 12); ZY2_ATTR(2, 13);
+    ZY2_ATTR(3, 0); ZY2_ATTR(3, 12); ZY2_ATTR(3, 13);
+    ZY2_ATTR(4, 0); ZY2_ATTR(4, 12); ZY2_ATTR(4, 13);
+#undef ZY2_ATTR
     CKC(cudaFuncSetAttribute(k_ks_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_ks_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
     CKC(cudaFuncSetAttribute(k_ks_fused<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kMaxSmem));
@@ -1898,6 +1904,7 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const long long W = 2LL * L * N, WQ = 2LL * M * N;
     if (n_ib <= 0 || k <= 0 || nb <= 0 || c_n <= 0 || Mr <= 0 || Mr % c_n) return set_err(GALA_ERR_DIM, "bad schedule-2 dims");
+    if (k > KG_MAXK) return set_err(GALA_ERR_DIM, "at most %d kernel taps", KG_MAXK);
     const int Kreal = n_ib * k * (post ? 1 : nb);
     const int rows = post ? Mr * nb : Mr;     // GEMM rows
     if (Kp % 32 || Kp < Kreal) return set_err(GALA_ERR_DIM, "Kp=%d must be a multiple of 32 covering K=%d", Kp, Kreal);
@@ -1987,17 +1994,47 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         dim3 grid((unsigned)((WQ + KG_PT - 1) / KG_PT), (unsigned)((Kp + KG_KT - 1) / KG_KT), (unsigned)nbatch);
         const u64* const* dk = (const u64* const*)(d_blob + o_keys);
         const ulonglong2* pm = (const ulonglong2*)(c->d_kg_off + 2 * GALA_MAXM);
-#define KG_ZY(LL)                                                                                                  \
-    KLAUNCH(c, "k_kg_zy", k_kg_zy<LL><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1,                \
+#define KG_ZYN(LL, LN)                                                                                              \
+    KLAUNCH(c, "k_kg_zy", (k_kg_zy<LL, LN><<<grid, 256, 0, c->stream>>>(c->dc, Dblk, cts, dk, d_gal + 1,           \
                                                                    post ? nullptr : (const ulonglong2*)masks, pm, k,  \
-                                                                   nb_y, n_ib, Kp, Bt, 1))
-        switch (L) {
-            case 1: KG_ZY(1); break;
-            case 2: KG_ZY(2); break;
-            case 3: KG_ZY(3); break;
-            default: KG_ZY(4); break;
+                                                                   nb_y, n_ib, Kp, Bt, 1)))
+#define KG_ZY(LL)                                                                                                  \
+    do {                                                                                                           \
+        if (c->dc.logN == 13) KG_ZYN(LL, 13);                                                                      \
+        else if (c->dc.logN == 12) KG_ZYN(LL, 12);                                                                 \
+        else KG_ZYN(LL, 0);                                                                                        \
+    } while (0)
+#define KG_ZY2N(LL, LN)                                                                                             \
+    KLAUNCH(c, "k_kg_zy", (k_kg_zy2<LL, LN><<<grid2, 256, 2 * KG_PT * KG_KT * 8, c->stream>>>(                       \
+                              c->dc, Dblk, cts, dk, d_gal + 1, pm, k, n_ib, Kp, Bt)))
+#define KG_ZY2(LL)                                                                                                 \
+    do {                                                                                                           \
+        if (c->dc.logN == 13) KG_ZY2N(LL, 13);                                                                     \
+        else if (c->dc.logN == 12) KG_ZY2N(LL, 12);                                                                \
+        else KG_ZY2N(LL, 0);                                                                                       \
+    } while (0)
+        // post-mask: both key-switch components per thread (k_kg_zy2; N >= 32, so a block of 32
+        // positions never straddles a prime)
+        const dim3 grid2((unsigned)((WQ / 2 + KG_PT - 1) / KG_PT), (unsigned)((Kp + KG_KT - 1) / KG_KT), (unsigned)nbatch);
+        if (post && getenv("GALA_KG_ZY1") == nullptr) {
+            switch (L) {
+                case 1: KG_ZY2(1); break;
+                case 2: KG_ZY2(2); break;
+                case 3: KG_ZY2(3); break;
+                default: KG_ZY2(4); break;
+            }
+        } else {
+            switch (L) {
+                case 1: KG_ZY(1); break;
+                case 2: KG_ZY(2); break;
+                case 3: KG_ZY(3); break;
+                default: KG_ZY(4); break;
+            }
         }
 #undef KG_ZY
+#undef KG_ZYN
+#undef KG_ZY2
+#undef KG_ZY2N
     }
     release(c, dig);
     release(c, Dblk);
