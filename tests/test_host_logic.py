@@ -392,3 +392,53 @@ def test_kg_plan_is_taken_from_the_full_task():
     p2 = kg_plan(ConvTask(32, 32, 8, 3, 3, 24, rng.integers(-128, 128, (24, 8, 3, 3)) % P, params), 2, 3, 2048,
                  band_only=True)
     assert (p2.schedule, p2.post, p2.batchable) == (2, True, True)
+
+
+# --- network files (reference layer-list format, profiler.py:9-17, 61-88) -------------------------
+def test_parse_network_format_and_errors():
+    from paper_2105_01827_b200.errors import NetworkParseError
+    from paper_2105_01827_b200.netfile import parse_network
+
+    assert parse_network("") == [] and parse_network("# only a comment\n\n") == []
+    specs = parse_network("conv 8 8 4 3 3 16  # a conv\nnonlinear relu\nfc 128 10\n")
+    assert [s.kind for s in specs] == ["conv", "nonlinear", "fc"]
+    assert (specs[0].u_w, specs[0].c_i, specs[0].k_h, specs[0].c_o) == (8, 4, 3, 16)
+    assert (specs[2].n_i, specs[2].n_o) == (128, 10) and specs[1].label == "relu"
+    for bad, line in (("conv 8 8 4 3 3\n", 1), ("fc 1 2\npool 2\n", 2), ("\nfc x 2\n", 2), ("conv 0 8 4 3 3 16", 1)):
+        with pytest.raises(NetworkParseError) as e:
+            parse_network(bad)
+        assert e.value.line_no == line
+
+
+def test_resnet18_224_network_file_is_the_config5_layer_list():
+    from paper_2105_01827_b200.netfile import fc_padded, load_network, network_layers
+    from paper_2105_01827_b200.resnet import resnet18_224
+
+    got = network_layers(load_network("resnet18_224.net"))
+    want = resnet18_224()
+    assert [(s.kind, s.c_in, s.c_out, s.k, s.stride, s.size) for s in got] == \
+           [(s.kind, s.c_in, s.c_out, s.k, s.stride, s.size) for s in want]
+    assert fc_padded(512, 1000, 4096) == (1024, 1024)          # profiler._fc_padded
+    assert fc_padded(24, 40, 4096) == (64, 64)
+    with pytest.raises(ParameterError):
+        fc_padded(8, 5000, 4096)
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir("/root/reference/pkg/src/gala"),
+                    reason="reference not mounted (it is only present in the build container)")
+def test_network_file_parses_identically_with_the_reference_parser():
+    import sys
+
+    from paper_2105_01827_b200.netfile import NETWORKS, parse_network
+
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        from gala.profiler import parse_network as ref_parse
+    finally:
+        sys.path.pop(0)
+        for m in [m for m in sys.modules if m == "gala" or m.startswith("gala.")]:
+            del sys.modules[m]
+    text = open(f"{NETWORKS}/resnet18_224.net").read()
+    ours, ref = parse_network(text), ref_parse(text)
+    assert [(s.kind, s.u_w, s.u_h, s.c_i, s.k_w, s.k_h, s.c_o, s.n_i, s.n_o, s.label) for s in ours] == \
+           [(s.kind, s.u_w, s.u_h, s.c_i, s.k_w, s.k_h, s.c_o, s.n_i, s.n_o, s.label) for s in ref]

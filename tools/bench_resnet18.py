@@ -55,13 +55,18 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         dist.init_process_group("nccl")
     specs = resnet18_224()
+    if "--net" in sys.argv:       # layers from a network file (reference layer-list format)
+        from paper_2105_01827_b200.netfile import load_network, network_layers
+
+        names = [sp.name for sp in specs]
+        specs = network_layers(load_network(sys.argv[sys.argv.index("--net") + 1]), names=names)
     if blocks:   # every rank holds a slice of every conv; the FC runs on rank 0
         parts = [list(range(len(specs)))] + [[i for i, sp in enumerate(specs) if sp.kind == "conv"]] * (world - 1)
     else:
         parts = partition_layers(layer_costs(specs, _measured_costs()), world)
     mine = parts[rank]
     t0 = time.perf_counter()
-    net = ResNet18Linear(only=mine, shard_blocks=blocks and world > 1)
+    net = ResNet18Linear(only=mine, shard_blocks=blocks and world > 1, layers=specs)
     torch.cuda.synchronize()
     setup = time.perf_counter() - t0
     ctx = net.ctx
