@@ -132,6 +132,20 @@ int gala_mv_gala_batch_host(gala_ctx *ctx, const uint64_t *cts_host, int B, cons
  * Used for T/baby <= 8, baby <= 64 and 16 <= B <= 32 -- or, for T >= 128, any B whose 32-input
  * tiles all hold >= 16 inputs (one E / MMA kernel pair per tile, everything else batched over B);
  * otherwise the CUDA-core path runs. */
+/* Multi-GPU split of one schedule-2 layer across its giant groups (
+ * reference: "independent output blocks may be computed in parallel with per-block
+ * meters merged", backend.py:134-139 CostMeter.merge).  Each rank runs gala_mv_gala2_partial on its
+ * group range [g_lo, g_hi) (every rank the same inputs and weights), returning per input the QP sum
+ * before the final ModDown, qp_sum [B][2][L+1][N], and the Q addend q_add [B][2][L][N] (wcan may be
+ * null: CUDA-core baby-step sums).  The element-wise u64 sums of all ranks' buffers (an NCCL
+ * reduce: every word < q_j, at most 8 ranks, so < 2^63 and exact) go to gala_mv_gala2_finish on
+ * the root, which reduces them mod q_j, applies the final ModDown, adds q_add and masks: the same
+ * words as gala_mv_gala2_batch(_tc) on one GPU. */
+int gala_mv_gala2_partial(gala_ctx *ctx, const uint64_t *cts_dev, int B, const uint64_t *pts2_dev,
+                          const uint8_t *wcan_dev, int T, int baby, int g_lo, int g_hi, uint64_t *qp_sum_dev,
+                          uint64_t *q_add_dev);
+int gala_mv_gala2_finish(gala_ctx *ctx, uint64_t *qp_sum_dev, uint64_t *q_add_dev, int B, const uint32_t *r_dev,
+                         uint64_t *outs_dev, uint64_t *masked_dev);
 size_t gala_fc_tc_weight_bytes(gala_ctx *ctx);
 int gala_fc_tc_weights(gala_ctx *ctx, const uint64_t *pts2_dev, int T, int baby, uint8_t *wcan_dev);
 int gala_mv_gala2_batch_tc(gala_ctx *ctx, const uint64_t *cts_dev, int B, const uint64_t *pts2_dev,

@@ -55,6 +55,8 @@ SIGNATURES = [
     ("gala_mv_gala_batch", i32, [vp, vp, i32, vp, i32, i32, vp, vp, vp]),
     ("gala_encode_gala_weights", i32, [vp, vp, i32, i32, vp]),
     ("gala_mv_gala2_batch", i32, [vp, vp, i32, vp, i32, i32, vp, vp, vp]),
+    ("gala_mv_gala2_partial", i32, [vp, vp, i32, vp, vp, i32, i32, i32, i32, vp, vp]),
+    ("gala_mv_gala2_finish", i32, [vp, vp, vp, i32, vp, vp, vp]),
     ("gala_mv_gala2_batch_host", i32, [vp, vp, i32, vp, i32, i32, vp, vp]),
     ("gala_mv_gala_host", i32, [vp, vp, vp, i32, i32, vp, vp]),
     ("gala_mv_gala_batch_host", i32, [vp, vp, i32, vp, i32, i32, vp, vp]),

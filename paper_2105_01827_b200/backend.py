@@ -492,6 +492,28 @@ class Context:
             self.call("gala_mv_gala2_batch", *common, *tail)
         return outs, masked
 
+    def mv_gala2_partial(self, cts, pts2, T: int, baby: int, g_lo: int, g_hi: int, wcan=None):
+        """Giant groups [g_lo, g_hi) of a schedule-2 layer: (QP sums before the final ModDown
+        [B][2][L+1][N], Q addends [B][2][L][N]) -- one rank's share of a multi-GPU layer."""
+        torch = _torch()
+        B = cts.shape[0]
+        qp = torch.empty((B, 2, self.L + 1, self.N), dtype=torch.int64, device=self.device)
+        qa = torch.empty((B, 2, self.L, self.N), dtype=torch.int64, device=self.device)
+        self.call("gala_mv_gala2_partial", ctypes.c_void_p(_ptr(cts)), int(B), ctypes.c_void_p(_ptr(pts2)),
+                  ctypes.c_void_p(_ptr(wcan)) if wcan is not None else None, int(T), int(baby), int(g_lo), int(g_hi),
+                  ctypes.c_void_p(_ptr(qp)), ctypes.c_void_p(_ptr(qa)))
+        return qp, qa
+
+    def mv_gala2_finish(self, qp, qa, d_r=None):
+        """Sums of every shard's partials (element-wise u64) -> (outs, masked), as gala_mv_gala2_batch."""
+        B = qp.shape[0]
+        outs = self.empty_ct(B)
+        masked = self.empty_ct(B) if d_r is not None else None
+        self.call("gala_mv_gala2_finish", ctypes.c_void_p(_ptr(qp)), ctypes.c_void_p(_ptr(qa)), int(B),
+                  ctypes.c_void_p(_ptr(d_r)) if d_r is not None else None, ctypes.c_void_p(_ptr(outs)),
+                  ctypes.c_void_p(_ptr(masked)) if masked is not None else None)
+        return outs, masked
+
     def fc_tc_supported(self, T: int, baby: int) -> bool:
         return T % baby == 0 and T // baby <= 8 and baby <= 64 and self.N % 32 == 0
 

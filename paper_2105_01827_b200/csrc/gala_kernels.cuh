@@ -17,7 +17,9 @@ struct PolyMap {
     int src_div;      // source poly within item: w / nprimes (1) or w (0)
     long long src_is; // item strides (words)
     long long dst_is;
-    int skip_per;     // >0: item index x -> (x/(skip_per-1))*skip_per + 1 + x%(skip_per-1)
+    int skip_per;     // >0: item index x -> (x/cnt)*skip_per + first + x%cnt
+    int skip_first;   // (first, cnt) = (1, skip_per - 1) when skip_cnt == 0
+    int skip_cnt;
 };
 
 __device__ __forceinline__ void polymap_resolve(const PolyMap& pm, int p, int N, long long& src_off,
@@ -26,8 +28,8 @@ __device__ __forceinline__ void polymap_resolve(const PolyMap& pm, int p, int N,
     int item = p / pm.per, w = p - item * pm.per;
     long long src_item = item;
     if (pm.skip_per > 0) {
-        int sp = pm.skip_per - 1;
-        src_item = (long long)(item / sp) * pm.skip_per + 1 + item % sp;
+        const int sp = pm.skip_cnt > 0 ? pm.skip_cnt : pm.skip_per - 1, f = pm.skip_cnt > 0 ? pm.skip_first : 1;
+        src_item = (long long)(item / sp) * pm.skip_per + f + item % sp;
     }
     prime = pm.prime_base + w % pm.nprimes;
     src_off = src_item * pm.src_is + (long long)(pm.src_div ? w / pm.nprimes : w) * N;
@@ -103,7 +105,9 @@ struct MdArgs {
     u64* const* outs;  // optional per-group output pointers
     int comps;         // components per item (0 = 2); 1: only component comp0
     int comp0;
-    int skip_per;      // > 0: item x reads source item (x / (skip_per - 1)) skip_per + 1 + x % (skip_per - 1)
+    int skip_per;      // > 0: item x reads source item (x / cnt) skip_per + first + x % cnt
+    int skip_first;    // (first, cnt) = (1, skip_per - 1) when skip_cnt == 0
+    int skip_cnt;
 };
 
 __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
@@ -113,7 +117,8 @@ __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
     const int comps = a.comps ? a.comps : 2;
     const int x = blockIdx.x / (comps * L), w = blockIdx.x % (comps * L);
     const int comp = a.comp0 + w / L, j = w % L;
-    const long long g = a.skip_per > 0 ? (long long)(x / (a.skip_per - 1)) * a.skip_per + 1 + x % (a.skip_per - 1) : x;
+    const int scnt = a.skip_cnt > 0 ? a.skip_cnt : a.skip_per - 1, sfirst = a.skip_cnt > 0 ? a.skip_first : 1;
+    const long long g = a.skip_per > 0 ? (long long)(x / scnt) * a.skip_per + sfirst + x % scnt : x;
     const ModC md = c.mod[j];
     const u64 q = md.q, P = c.mod[L].q, halfP = P >> 1;
     const u64* r = a.r + ((long long)x * comps + (comp - a.comp0)) * N;
@@ -516,7 +521,8 @@ __global__ void k_fold_groups(DevCtx c, const u64* __restrict__ Uv, const u64* _
 // (sigma_g = the automorphism of the giant step g b; identity for step 0).  The final ModDown of S plus
 // the giant-step key switches, plus Qadd, is the layer output.  grid (N / 256, M, B)
 __global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __restrict__ Cacc,
-                           const unsigned* __restrict__ gal, int G, u64* __restrict__ S, u64* __restrict__ Qadd)
+                           const unsigned* __restrict__ gal, int G, int g_lo, int g_hi, u64* __restrict__ S,
+                           u64* __restrict__ Qadd)
 {
     const int N = c.N, L = c.L, M = c.M;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -526,7 +532,7 @@ __global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __res
     const long long NN = N;
     u64 s0 = 0, s1 = 0, c0 = 0, c1 = 0;
 #pragma unroll 1
-    for (int g = 0; g < G; g++) {
+    for (int g = g_lo; g < g_hi; g++) {       // a multi-GPU shard sums its own groups only
         const long long z = (long long)b * G + g;
         const unsigned ge = gal[g];
         const int src = ge == 1u ? k : auto_src(k, ge, c.logN);
@@ -542,6 +548,17 @@ __global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __res
     if (j < L) {
         Qadd[(((long long)b * 2 + 0) * L + j) * NN + k] = c0;
         Qadd[(((long long)b * 2 + 1) * L + j) * NN + k] = c1;
+    }
+}
+
+// Sums of per-rank partials (each word < q_j, at most 8 ranks: < 2^63) reduced mod q_j in place.
+// x [count][comps][primes][N] over the prime set (prime_base + w) of `primes` moduli
+__global__ void k_reduce_mod(DevCtx c, u64* __restrict__ x, long long count, int primes)
+{
+    const long long per = (long long)primes * c.N;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count * per; e += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)((e % per) / c.N);
+        x[e] %= c.mod[j].q;
     }
 }
 

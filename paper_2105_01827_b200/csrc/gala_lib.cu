@@ -398,7 +398,8 @@ static int rotate_engine_fused(gala_ctx* c, const std::vector<EngTerm>& terms,
 // [G][2][L][N] (optional) after it.
 static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
                          const std::vector<std::vector<EngMember>>& groups, const std::vector<u64*>& outs,
-                         const u64* qp_add = nullptr, const u64* q_add = nullptr)
+                         const u64* qp_add = nullptr, const u64* q_add = nullptr, u64* raw_U = nullptr,
+                         u64* raw_C = nullptr)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     const int G = (int)groups.size();
@@ -408,7 +409,7 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     bool fusable = L <= 3 && getenv("GALA_KS_FUSED") != nullptr;
     for (const auto& t : terms)
         if (!t.steps.empty() && (t.steps.size() != 1 || t.ntt_block)) fusable = false;
-    if (fusable) return rotate_engine_fused(c, terms, groups, outs, qp_add, q_add);
+    if (fusable && !raw_U) return rotate_engine_fused(c, terms, groups, outs, qp_add, q_add);
     const long long blk_words = (long long)(L * M + L) * N;
     // rotated terms and their rotation slices
     std::vector<int> term_rot_base(terms.size(), -1);
@@ -557,6 +558,10 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         release(c, Uv);
         release(c, Cv);
     }
+    if (raw_U) {   // multi-GPU partial: the groups' QP sums and Q addends before any ModDown
+        CK(cudaMemcpyAsync(raw_U, U, sizeof(u64) * (size_t)G * 2 * M * N, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(raw_C, Cacc, sizeof(u64) * (size_t)G * 2 * L * N, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
     RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
     MdArgs a{};
@@ -569,6 +574,7 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     a.out_is = 0;
     a.outs = (u64* const*)(d_blob + o_out);
     KLAUNCH(c, "k_moddown", k_moddown<<<G * 2 * L, nt, c->smem_ntt, c->stream>>>(c->dc, a));
+    }
     release(c, U);
     release(c, Cacc);
     release(c, r);
@@ -1227,8 +1233,14 @@ int gala_encode_gala_weights(gala_ctx* c, const uint32_t* slots, int T, int baby
     return GALA_OK;
 }
 
+// g_lo / g_hi: only the giant groups [g_lo, g_hi) (a multi-GPU shard; the baby-step sums of every group
+// are computed, the giant-step key switches and inner ModDowns of the shard's groups only).  raw_U /
+// raw_Q: return, per input, the QP sum before the final ModDown [B][2][M][N] and the Q addend
+// [B][2][L][N] instead of outs / masked (gala_mv_gala2_finish completes the layer from the sums of
+// every shard's raw outputs).
 static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2, const uint8_t* wcan, int T, int baby,
-                   const uint32_t* r, uint64_t* outs, uint64_t* masked)
+                   const uint32_t* r, uint64_t* outs, uint64_t* masked, int g_lo = 0, int g_hi = -1,
+                   uint64_t* raw_U = nullptr, uint64_t* raw_Q = nullptr)
 {
     const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
     if (T <= 0 || B <= 0) return set_err(GALA_ERR_DIM, "T and B must be positive");
@@ -1236,6 +1248,9 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     if (T % baby) return set_err(GALA_ERR_PARAM, "baby step %d does not divide T=%d", baby, T);
     const int G = T / baby;
     if ((long long)T > N / 2) return set_err(GALA_ERR_DIM, "T=%d exceeds the %d slots of a row", T, N / 2);
+    if (g_hi < 0) g_hi = G;
+    if (g_lo < 0 || g_lo >= g_hi || g_hi > G) return set_err(GALA_ERR_PARAM, "bad giant-group range [%d, %d) of %d", g_lo, g_hi, G);
+    if ((g_lo != 0 || g_hi != G) && !raw_U) return set_err(GALA_ERR_PARAM, "a giant-group shard returns raw sums");
     const long long W = 2LL * L * N, MN = (long long)M * N;
     const long long blk_words = (long long)(L * M + L) * N;
     for (int j = 1; j < baby; j++)
@@ -1243,6 +1258,7 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     for (int g = 1; g < G; g++)
         if (!gala_has_rotation_key(c, g * baby))
             return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, g * baby));
+    if (baby == 1 && raw_U) return set_err(GALA_ERR_PARAM, "sharded trees need a baby step > 1");
     if (baby == 1) {   // T == 1 (a single group with one member) or degenerate trees: plain products + giant sum
         u64* prods;
         RET(scratch(c, &prods, (size_t)B * T * W));
@@ -1258,7 +1274,7 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
         return GALA_OK;
     }
     u64* DM = nullptr;
-    if (r && masked) RET(mask_begin(c, r, B, &DM));   // overlaps the layer on the side stream
+    if (r && masked && !raw_U) RET(mask_begin(c, r, B, &DM));   // overlaps the layer on the side stream
     // 1. one decomposition per input: identity digit block [(L*M + L)][N] (digits of x.c1 in every
     //    prime of QP, then x.c0)
     u64 *dig, *Dblk;
@@ -1417,15 +1433,19 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     {
         const int th = N < 256 ? N : 256;
         dim3 gq((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)B);
-        KLAUNCH(c, "k_giant_qp", k_giant_qp<<<gq, th, 0, c->stream>>>(c->dc, U, Cacc, d_ggal, G, S, Qadd));
+        KLAUNCH(c, "k_giant_qp", k_giant_qp<<<gq, th, 0, c->stream>>>(c->dc, U, Cacc, d_ggal, G, g_lo, g_hi, S, Qadd));
     }
-    const int Zi = B * (G - 1);
+    const int ga = g_lo > 1 ? g_lo : 1;                 // the shard's giant groups g >= 1
+    const int Gs = g_hi > ga ? g_hi - ga : 0;
+    const int Zi = B * Gs;
     u64* inner = nullptr;
     if (Zi > 0) {
         // inner ModDown of c1 for the groups g >= 1 (item x -> z = (x / (G-1)) G + 1 + x % (G-1))
         RET(scratch(c, &inner, (size_t)Zi * W));
-        RET(launch_inv<false>(c, U + (long long)(M + L) * N, rr, Zi, pm_make(1, 1, L, 0, 2LL * M * N, N, G),
-                              "k_ntt_inv[moddown]"));
+        PolyMap pmi = pm_make(1, 1, L, 0, 2LL * M * N, N, G);
+        pmi.skip_first = ga;
+        pmi.skip_cnt = Gs;
+        RET(launch_inv<false>(c, U + (long long)(M + L) * N, rr, Zi, pmi, "k_ntt_inv[moddown]"));
         MdArgs a{};
         a.r = rr;
         a.U = U;
@@ -1438,6 +1458,8 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
         a.comps = 1;
         a.comp0 = 1;
         a.skip_per = G;
+        a.skip_first = ga;
+        a.skip_cnt = Gs;
         KLAUNCH(c, "k_moddown", k_moddown<<<Zi * L, nt, c->smem_ntt, c->stream>>>(c->dc, a));
     }
     release(c, U);
@@ -1451,9 +1473,9 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
         std::vector<u64*> eouts;
         terms.reserve((size_t)Zi);
         for (int b = 0; b < B; b++) {
-            for (int g = 1; g < G; g++) {
+            for (int g = ga; g < g_hi; g++) {
                 EngTerm t;
-                t.X = inner + ((long long)b * (G - 1) + (g - 1)) * W;
+                t.X = inner + ((long long)b * Gs + (g - ga)) * W;
                 t.pt = nullptr;
                 t.ntt_block = nullptr;
                 t.c0_zero = true;
@@ -1463,7 +1485,7 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
             }
             eouts.push_back(outs + (long long)b * W);
         }
-        RET(rotate_engine(c, terms, groups, eouts, S, Qadd));
+        RET(rotate_engine(c, terms, groups, eouts, S, Qadd, raw_U, raw_Q));
     }
     release(c, inner);
     release(c, S);
@@ -1483,6 +1505,40 @@ int gala_mv_gala2_batch_tc(gala_ctx* c, const uint64_t* cts, int B, const uint64
                            int baby, const uint32_t* r, uint64_t* outs, uint64_t* masked)
 {
     return mv2_run(c, cts, B, pts2, wcan, T, baby, r, outs, masked);
+}
+
+int gala_mv_gala2_partial(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2, const uint8_t* wcan, int T,
+                          int baby, int g_lo, int g_hi, uint64_t* qp_sum, uint64_t* q_add)
+{
+    if (!qp_sum || !q_add) return set_err(GALA_ERR_PARAM, "partial sums need output buffers");
+    return mv2_run(c, cts, B, pts2, wcan, T, baby, nullptr, nullptr, nullptr, g_lo, g_hi, qp_sum, q_add);
+}
+
+int gala_mv_gala2_finish(gala_ctx* c, uint64_t* qp_sum, uint64_t* q_add, int B, const uint32_t* r, uint64_t* outs,
+                         uint64_t* masked)
+{
+    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
+    if (B <= 0) return set_err(GALA_ERR_DIM, "empty batch");
+    // the words are sums over the shards of values below q_j: exact reduction first
+    KLAUNCH(c, "k_reduce_mod", k_reduce_mod<<<grid_for((long long)B * 2 * M * N, 256), 256, 0, c->stream>>>(c->dc, qp_sum, 2LL * B, M));
+    KLAUNCH(c, "k_reduce_mod", k_reduce_mod<<<grid_for((long long)B * 2 * L * N, 256), 256, 0, c->stream>>>(c->dc, q_add, 2LL * B, L));
+    u64* rr;
+    RET(scratch(c, &rr, (size_t)B * 2 * N));
+    RET(launch_inv<false>(c, qp_sum + (long long)L * N, rr, B * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
+                          "k_ntt_inv[moddown]"));
+    MdArgs a{};
+    a.r = rr;
+    a.U = qp_sum;
+    a.add0 = q_add;
+    a.add1 = q_add + (long long)L * N;
+    a.add_is = 2LL * L * N;
+    a.out = outs;
+    a.out_is = 2LL * L * N;
+    a.outs = nullptr;
+    KLAUNCH(c, "k_moddown", k_moddown<<<B * 2 * L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, a));
+    release(c, rr);
+    if (r && masked) RET(sub_plain_batch(c, outs, r, B, masked));
+    return GALA_OK;
 }
 
 size_t gala_fc_tc_weight_bytes(gala_ctx* c) { return (size_t)c->dc.M * c->dc.N * GTC_W_BYTES; }

@@ -8,6 +8,10 @@ across ranks, one process per GPU:
 
 * **inputs / layers** (configs 1, 2, 5): replicas, or a cost-balanced assignment
   of whole layers to ranks (`partition_layers`); no data-path collective;
+* **giant groups of one FC layer** (config 2; `ShardedGalaFC`): every rank takes a range of the
+  BSGS giant groups, and the QP partial sums before the final ModDown meet in one exact modular
+  reduce (an element-wise u64 sum: every word < q_j < 2^60 and at most 8 ranks) on the root, which
+  finishes the layer -- the same words as one GPU;
 * **output blocks of one convolution** (configs 3, 4, 5): `ShardedKernelGroupingConv`
   broadcasts the input ciphertexts from the source rank, every rank runs the fused
   layer on its contiguous range of physical output ciphertexts, and only the final
@@ -256,3 +260,61 @@ class ShardedKernelGroupingConv:
         rep = not rows
         row = rows.pop() if rows else 0
         return [Ciphertext._wrap(outs[ob], noises[ob], self.task.params, row, replicated=rep) for ob in range(n_ob)]
+
+
+def reduce_sum_u64(t, dst: int = 0, group=None):
+    """Element-wise u64 sum of `t` over the ranks onto `dst` (in place there; int64 two's-complement
+    addition is u64 addition).  The caller keeps every word < 2^64 / world (here < q_j < 2^60, at most
+    8 ranks), so the sum is exact and one mod-q_j reduction after it gives the modular sum."""
+    dist = _dist()
+    if dist is None or dist.get_world_size(group) == 1:
+        return t
+    if _host_staged(dist, t, group):
+        h = t.cpu()
+        dist.reduce(h, dst=dst, op=dist.ReduceOp.SUM, group=group)
+        if dist.get_rank(group) == dst:
+            t.copy_(h)
+    else:
+        dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+class ShardedGalaFC:
+    """One schedule-2 GALA FC layer (`matvec.GalaFC`) split across ranks by its giant groups
+    (SURVEY.md 8(e), config 2).  Every rank holds the layer's weights and receives the inputs; rank r
+    runs the baby-step sums and the giant-step key switches of its group range (`shard_range` over the
+    G = T / b groups) and returns the QP sums before the final ModDown; `reduce_sum_u64` meets them on
+    `dst`, which reduces mod q_j, applies the one final ModDown and the mask (gala_mv_gala2_finish).
+    ModDown is linear only up to rounding, so it is applied once, to the total: the words equal the
+    single-GPU layer's."""
+
+    def __init__(self, w, params, group=None, tensor_cores: bool = True, **kw):
+        from .matvec import GalaFC
+
+        self.layer = GalaFC(w, params, tensor_cores=tensor_cores, **kw)
+        if self.layer.schedule != 2:
+            raise ValueError("the giant-group split needs the schedule-2 layer")
+        self.group = group
+        self.world, self.rank = world_rank(group)
+        self.G = self.layer.T // self.layer.baby
+        if self.world > self.G:
+            raise ValueError(f"{self.world} ranks for {self.G} giant groups")
+        self.groups = shard_range(self.G, self.world, self.rank)
+
+    @property
+    def ctx(self):
+        return self.layer.ctx
+
+    def forward_device(self, cts, d_r, block: int = 0, src: int = 0, dst: int = 0):
+        """cts [B][2][L][N] and masks d_r [B][N] on `src` -> (outs, masked) on `dst`, None elsewhere."""
+        if self.world > 1:
+            cts = broadcast_tensor(cts.contiguous(), src=src, group=self.group)
+        lay = self.layer
+        tasks, pts2, T = lay.blocks[block]
+        qp, qa = lay.ctx.mv_gala2_partial(cts, pts2, T, lay.baby, self.groups.start, self.groups.stop,
+                                          wcan=lay.wcan[block])
+        reduce_sum_u64(qp, dst=dst, group=self.group)
+        reduce_sum_u64(qa, dst=dst, group=self.group)
+        if self.rank != dst:
+            return None
+        return lay.ctx.mv_gala2_finish(qp, qa, d_r)

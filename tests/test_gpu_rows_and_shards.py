@@ -7,6 +7,9 @@
 * ``ShardedKernelGroupingConv`` with the real CUDA sub-layers on two gloo ranks (both on cuda:0,
   host-staged collectives): the gathered words equal the single-rank layer's, with uneven shards
   whose kernels alone would pick a different schedule than the full layer.
+* ``ShardedGalaFC``: one schedule-2 FC layer split across 2 and 3 ranks by its BSGS giant groups;
+  the exact u64 reduce of the QP partial sums and the root's single final ModDown give the
+  single-GPU layer's words (backend.py:134-139).
 """
 import os
 import socket
@@ -172,3 +175,63 @@ def test_sharded_conv_two_ranks_cuda():
     assert r0["local_schedule"] == r1["local_schedule"] == 1
     assert r0["words_equal"] and r0["dec_ok"]
     assert r1["none_off_dst"]
+
+
+# --- one FC layer split across ranks by its giant groups ----------------------------------------
+def _fc_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.plain import dot_mod_p
+        from paper_2105_01827_b200.sharding import ShardedGalaFC
+
+        params = HEParams(n=1024, p=P, rns_limbs=3, seed=78)     # same seed: same secret and keys everywhere
+        rng = np.random.default_rng(8)
+        w = rng.integers(-128, 128, (256, 1024)) % P
+        sharded = ShardedGalaFC(w, params)
+        lay, ctx = sharded.layer, sharded.ctx
+        B = 3
+        xs = [rng.integers(0, P, 1024) for _ in range(B)]
+        masks = [lay.draw_masks(40 + b) for b in range(B)]
+        cts = torch.stack([lay.encrypt_input(x)[0] for x in xs])
+        d_r = ctx.to_device_u32(np.stack([ctx.physical(m[0][0].slots, m[0][1].slots) for m in masks]))
+        if rank != 0:
+            cts = torch.zeros_like(cts)                             # only the source rank holds the inputs
+        res = sharded.forward_device(cts, d_r)
+        out = {"groups": (sharded.groups.start, sharded.groups.stop), "G": sharded.G}
+        if rank == 0:
+            _, masked = res
+            _, want = lay.run_batch(cts, lay.blocks[0][1], d_r, block=0)     # the single-GPU layer
+            out["words_equal"] = bool(np.array_equal(ctx.export_words(masked), ctx.export_words(want)))
+            out["dec_ok"] = all(bool(np.array_equal((lay.client_shares([masked[b]]) + lay.server_shares(masks[b])) % P,
+                                                    dot_mod_p(w, xs[b], P))) for b in range(B))
+        else:
+            out["none_off_dst"] = res is None
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fc_giant_group_split_cuda(world):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fc_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    outs = dict(q.get(timeout=600) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    G = outs[0]["G"]
+    spans = sorted(outs[r]["groups"] for r in range(world))
+    assert spans[0][0] == 0 and spans[-1][1] == G and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert outs[0]["words_equal"] and outs[0]["dec_ok"]
+    assert all(outs[r]["none_off_dst"] for r in range(1, world))
