@@ -393,7 +393,7 @@ def run_ours(args):
     tc_on = layer.wcan[0] is not None and B >= 16 and (B <= 32 or (T >= 128 and (B % 32 == 0 or B % 32 >= 16)))
     traffic = None    # DRAM bytes per launch of the dominant kernel from the committed ncu capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             tj = json.load(f)
         # per launch: a capture at batch 32 (one full tile) stands for every batch of full tiles
         tb = int(tj.get("batch", 0))
@@ -442,6 +442,19 @@ def run_ours(args):
                            "peak_source": "2x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)"}
     bound = max(roofs, key=lambda r: roofs[r]["frac"]) if roofs else "int"
     br = roofs.get(bound, {"achieved": 0.0, "peak": 0.0, "unit": "", "frac": 0.0})
+    # the whole step against SURVEY.md 8(d)'s formula with the work the schedule executes
+    # (analytics.fc_executed_work: CUDA-core modmuls at the modmul peak, int8 MACs at 2x the bf16 peak,
+    # bytes at HBM): the slowest roof over the measured step time
+    from paper_2105_01827_b200.analytics import executed_roofline, fc_executed_work
+
+    work = fc_executed_work(N, L, T, baby, B, tc_on)
+    lr = executed_roofline(work, work["bytes"], ms_per_step / 1e3, peak_modmul,
+                           2 * peaks.get("bf16_tflops", 1639.9) * 1e12, hbm_peak * 1e9)
+    layer_roof = {"bound": lr["bound"], "frac": lr["frac"], "roofline_us_per_step": lr["roofline_us"],
+                  "measured_us_per_step": round(ms_per_step * 1e3, 1), "modmuls_per_step": lr["modmuls"],
+                  "int8_macs_per_step": lr["int8_macs"], "bytes_per_step": lr["bytes"],
+                  "roof_times_us": {k: round(v * 1e6, 2) for k, v in lr["times_s"].items()},
+                  "model": "analytics.fc_executed_work (schedule 2 as executed; SURVEY 8(d) formula)"}
 
     result = {
         "metric": METRIC,
@@ -477,13 +490,10 @@ def run_ours(args):
             "unit": br["unit"],
             "frac": br["frac"],
             "traffic": traffic,
-            "traffic_unit": "bytes per launch (dram read + write, ncu --set full, profiles/r1_ncu_summary.md)",
+            "traffic_unit": "bytes per launch (dram read + write, ncu --set full, profiles/r2_ncu_summary.md)",
             "kernel_share_of_step": round(dom["ms"] / step_ms_prof, 4) if step_ms_prof else None,
             "roofs": roofs,
-            "layer": {"modmul_equivalents_per_s": round(layer_achieved / 1e9, 2), "unit": "G/s",
-                      "modmuls_per_layer": layer_modmuls,
-                      "note": "the whole layer's schedule-2 modmul count per second -- a rate, not a roofline "
-                              "fraction: the baby-step products run on the int8 tensor cores, not the IMAD pipe"},
+            "layer": layer_roof,
             "hbm": {"algorithmic_bytes_per_layer": int(layer_bytes),
                     "achieved_gbs": round(layer_bytes * layers / world / (total_ms / 1e3) / 1e9, 2),
                     "peak_gbs": hbm_peak},

@@ -22,7 +22,13 @@ from plain_check import conv2d_mod_p, dot_mod_p  # noqa: E402
 from paper_2105_01827_b200 import ConvTask, CostMeter, GalaFC, HEParams, KernelGroupingConv  # noqa: E402
 from paper_2105_01827_b200.conv import encrypt_inputs, unpack_channels  # noqa: E402
 from paper_2105_01827_b200.backend import decrypt  # noqa: E402
-from paper_2105_01827_b200.analytics import survey_conv_roofline, survey_fc_roofline  # noqa: E402
+from paper_2105_01827_b200.analytics import (  # noqa: E402
+    executed_roofline,
+    fc_executed_work,
+    kg2_executed_work,
+    survey_conv_roofline,
+    survey_fc_roofline,
+)
 
 P = 1032193
 dev = torch.device("cuda", 0)
@@ -70,7 +76,29 @@ def fc(name, n, L, n_out, n_in, B):
             "ms_per_layer": ms / B,
             "layers_per_s": 1e3 * B / ms, "correct": ok,
             "breakdown_ms_per_layer": {k: round(v["ms"] / B, 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
-            "roofline": roofline(survey_fc_roofline(ctx.N, ctx.L, layer.T), ms / B, ctx)}
+            "roofline": roofline(survey_fc_roofline(ctx.N, ctx.L, layer.T), ms / B, ctx),
+            "roofline_executed": fc_exec(layer, ctx, B, ms)}
+
+
+def fc_exec(layer, ctx, B, ms):
+    if layer.schedule != 2:
+        return None
+    T, b = layer.T, layer.baby
+    tc = layer.wcan[0] is not None and B >= 16 and (B <= 32 or (T >= 128 and (B % 32 == 0 or B % 32 >= 16)))
+    w = fc_executed_work(ctx.N, ctx.L, T, b, B, tc)
+    return exec_roof(w, w["bytes"], ms, ctx)
+
+
+def conv_exec(layer, ctx, ms, images=1):
+    """Schedule 2: analytics.kg2_executed_work; schedule 1 on the CUDA cores is the survey model itself."""
+    if layer.schedule != 2:
+        return None
+    L, N = ctx.L, ctx.N
+    w = kg2_executed_work(N, L, layer.n_ib, layer.k, layer.pair * layer.c_n, layer.n_obp * layer.c_n, layer.c_n,
+                          layer.n_obp, layer.post, images)
+    keys = (layer.k - 1 + layer.c_n - 1) * 2 * L * (L + 1) * N * 8
+    nbytes = images * (layer.n_ib + layer.n_obp) * 2 * L * N * 8 + keys + layer.resident_bytes
+    return exec_roof(w, nbytes, ms, ctx)
 
 
 def conv(name, n, L, u, frame, c_i, c_o, k, B=1):
@@ -122,7 +150,7 @@ def conv(name, n, L, u, frame, c_i, c_o, k, B=1):
             want = conv2d_mod_p(ch if bi == 0 else chs[bi - 1], kern, P)
             okb = okb and bool(np.array_equal(got, want))
             del outs_b
-        batch = {"roofline": roofline(model, msb / B, ctx), "images": B, "ms_per_batch": msb, "host_enqueue_ms": round(host_ms, 3), "launches": launches, "ms_per_layer": msb / B, "layers_per_s": 1e3 * B / msb,
+        batch = {"roofline": roofline(model, msb / B, ctx), "roofline_executed": conv_exec(layer, ctx, msb, B), "images": B, "ms_per_batch": msb, "host_enqueue_ms": round(host_ms, 3), "launches": launches, "ms_per_layer": msb / B, "layers_per_s": 1e3 * B / msb,
                  "correct": okb,
                  "breakdown_ms_per_layer": {k2: round(v["ms"] / B, 4)
                                             for k2, v in sorted(profb.items(), key=lambda kv: -kv[1]["ms"])}}
@@ -139,7 +167,7 @@ def conv(name, n, L, u, frame, c_i, c_o, k, B=1):
             "schedule": layer.schedule, "post_mask": layer.post,
             "plaintext_bytes": layer.resident_bytes, "meter": repr(meter),
             "breakdown_ms": {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
-            "roofline": roofline(model, ms, ctx), "batch": batch}
+            "roofline": roofline(model, ms, ctx), "roofline_executed": conv_exec(layer, ctx, ms), "batch": batch}
 
 
 SCHED = int(os.environ["KG_SCHED"]) if os.environ.get("KG_SCHED") else None
@@ -151,8 +179,24 @@ except Exception:
 _PEAK_MM = []
 
 
+def exec_roof(work, nbytes, ms_per_layer, ctx):
+    """The schedule as executed (analytics.*_executed_work) against every roof: CUDA-core modmuls at the
+    measured modmul peak, int8 MACs at 2x the measured bf16 peak, bytes at HBM."""
+    if not _PEAK_MM:
+        _PEAK_MM.append(ctx.bench_modmul())
+    bf16 = 1639.9
+    try:
+        bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", bf16))
+    except Exception:
+        pass
+    r = executed_roofline(work, nbytes, ms_per_layer / 1e3, _PEAK_MM[0], 2 * bf16 * 1e12, HBM_PEAK * 1e9)
+    return {"bound": r["bound"], "frac": r["frac"], "roofline_us": r["roofline_us"], "modmuls": r["modmuls"],
+            "int8_macs": r["int8_macs"], "bytes": r["bytes"]}
+
+
 def roofline(model, ms_per_layer, ctx):
-    """roofline time = max(modmuls / measured modmul peak, bytes / HBM peak)."""
+    """roofline time = max(modmuls / measured modmul peak, bytes / HBM peak), with the
+    survey's per-operation counts (the reference's schedule: one key switch per rotation)."""
     if not _PEAK_MM:
         _PEAK_MM.append(ctx.bench_modmul())
     t_int = model["modmuls"] / _PEAK_MM[0]
