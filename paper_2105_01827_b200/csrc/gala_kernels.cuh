@@ -1206,11 +1206,11 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
 // traffic -- are halved.  Block: 32 positions (j, i) x 128 K columns = 64 output rows of the byte
 // planes (the two components' tiles); columns come from the block's table ((ib << 8) | tap).
 // Dynamic shared memory: 2 x KG_PT x KG_KT words.
-template <int L, int LOGN>
-__global__ void __launch_bounds__(256) k_kg_zy2(DevCtx c, const u64* __restrict__ Dblk, const u64* __restrict__ X,
+template <int L, int LOGN, bool PRE>
+__global__ void __launch_bounds__(256, 3) k_kg_zy2(DevCtx c, const u64* __restrict__ Dblk, const u64* __restrict__ X,
                                                 const u64* const* __restrict__ keys, const unsigned* __restrict__ gal,
-                                                const ulonglong2* __restrict__ pconst, int k, int n_ib, int Kp,
-                                                int8_t* __restrict__ Bt)
+                                                const ulonglong2* __restrict__ masks, const ulonglong2* __restrict__ pconst,
+                                                int k, int nb, int n_ib, int Kp, int8_t* __restrict__ Bt)
 {
     extern __shared__ u64 zsm[];                 // [comp][KG_PT * KG_KT], swizzled as kg_swz
     __shared__ const u64* s_key[KG_MAXK];
@@ -1225,8 +1225,9 @@ __global__ void __launch_bounds__(256) k_kg_zy2(DevCtx c, const u64* __restrict_
         if (pp == 0) s_key[t] = kt;
         s_src[t][pp] = kt ? auto_src((jl0 + pp) & (N - 1), gal[t], logN) : 0;
     }
-    for (int gl = threadIdx.x; gl < KG_KT; gl += blockDim.x) {
-        const int g = K0 + gl;
+    const int gpt = KG_KT / nb;                 // (input, tap) groups per block: nb K columns each (pre-mask)
+    for (int gl = threadIdx.x; gl < gpt; gl += blockDim.x) {
+        const int g = K0 / nb + gl;
         s_col[gl] = g < n_ib * k ? ((g / k) << 8) | (g % k) : -1;
     }
     __syncthreads();
@@ -1242,13 +1243,14 @@ __global__ void __launch_bounds__(256) k_kg_zy2(DevCtx c, const u64* __restrict_
         const uint32_t bw = (uint32_t)(L * M + L) * (uint32_t)N;
         const uint32_t dj = (uint32_t)j * (uint32_t)N;
         const uint32_t koff = (uint32_t)j * (uint32_t)N + (uint32_t)i;
-        for (int gl0 = w; gl0 < KG_KT; gl0 += 8 * KG_ZU) {
+        for (int gl0 = w; gl0 < gpt; gl0 += 8 * KG_ZU) {
             u64 dv[KG_ZU][L + 1], k0v[KG_ZU][L], k1v[KG_ZU][L];
-            int kind[KG_ZU];
+            int kind[KG_ZU], tap[KG_ZU];
 #pragma unroll
             for (int u = 0; u < KG_ZU; u++) {
                 const int gl = gl0 + 8 * u;
-                const int cm = s_col[gl];
+                const int cm = gl < gpt ? s_col[gl] : -1;
+                tap[u] = cm & 255;
                 kind[u] = 0;
                 if (cm >= 0) {
                     const int ibu = cm >> 8, tt = cm & 255;
@@ -1275,6 +1277,7 @@ __global__ void __launch_bounds__(256) k_kg_zy2(DevCtx c, const u64* __restrict_
 #pragma unroll
             for (int u = 0; u < KG_ZU; u++) {
                 const int gl = gl0 + 8 * u;
+                if (gl >= gpt) break;
                 u64 z0 = 0, z1 = 0;
                 if (kind[u] == 1) {
                     z0 = csub(shoup_lazy_sf(dv[u][0], pc.x, pc.y, q), q);
@@ -1295,8 +1298,23 @@ __global__ void __launch_bounds__(256) k_kg_zy2(DevCtx c, const u64* __restrict_
                     z1 = s1.reduce_sf(q);
                     if (has_c0) z0 = add_mod(z0, csub(shoup_lazy_sf(dv[u][L], pc.x, pc.y, q), q), q);
                 }
-                zsm[kg_swz(pp, gl)] = z0 ^ 0x8080808080808080ull;
-                zsm[KG_PT * KG_KT + kg_swz(pp, gl)] = z1 ^ 0x8080808080808080ull;
+                if (!PRE) {
+                    zsm[kg_swz(pp, gl)] = z0 ^ 0x8080808080808080ull;
+                    zsm[KG_PT * KG_KT + kg_swz(pp, gl)] = z1 ^ 0x8080808080808080ull;
+                    continue;
+                }
+                // pre-mask form: the nb band masks of the tap (shared by both components) per K column
+                const ulonglong2* mk = masks + (long long)tap[u] * nb * MN + jl;
+                for (int beta = 0; beta < nb; beta++) {
+                    u64 v0 = 0, v1 = 0;
+                    if (kind[u]) {
+                        const ulonglong2 m = __ldg(mk + (long long)beta * MN);
+                        v0 = csub(shoup_lazy_sf(z0, m.x, m.y, q), q);
+                        v1 = csub(shoup_lazy_sf(z1, m.x, m.y, q), q);
+                    }
+                    zsm[kg_swz(pp, gl * nb + beta)] = v0 ^ 0x8080808080808080ull;
+                    zsm[KG_PT * KG_KT + kg_swz(pp, gl * nb + beta)] = v1 ^ 0x8080808080808080ull;
+                }
             }
         }
     }

@@ -871,12 +871,14 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_gala_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
-#define ZY2_ATTR(LL, LN) CKC(cudaFuncSetAttribute(k_kg_zy2<LL, LN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KG_PT * KG_KT * 8))
+#define ZY2_ATTR1(LL, LN, PR) CKC(cudaFuncSetAttribute(k_kg_zy2<LL, LN, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KG_PT * KG_KT * 8))
+#define ZY2_ATTR(LL, LN) ZY2_ATTR1(LL, LN, false); ZY2_ATTR1(LL, LN, true)
     ZY2_ATTR(1, 0); ZY2_ATTR(1, 12); ZY2_ATTR(1, 13);
     ZY2_ATTR(2, 0); ZY2_ATTR(2, 12); ZY2_ATTR(2, 13);
     ZY2_ATTR(3, 0); ZY2_ATTR(3, 12); ZY2_ATTR(3, 13);
     ZY2_ATTR(4, 0); ZY2_ATTR(4, 12); ZY2_ATTR(4, 13);
 #undef ZY2_ATTR
+#undef ZY2_ATTR1
     CKC(cudaFuncSetAttribute(k_ks_fused<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_ks_fused<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
     CKC(cudaFuncSetAttribute(k_ks_fused<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * kMaxSmem));
@@ -2060,19 +2062,25 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
         else if (c->dc.logN == 12) KG_ZYN(LL, 12);                                                                 \
         else KG_ZYN(LL, 0);                                                                                        \
     } while (0)
+#define KG_ZY2P(LL, LN, PRE)                                                                                        \
+    KLAUNCH(c, "k_kg_zy", (k_kg_zy2<LL, LN, PRE><<<grid2, 256, 2 * KG_PT * KG_KT * 8, c->stream>>>(                  \
+                              c->dc, Dblk, cts, dk, d_gal + 1, post ? nullptr : (const ulonglong2*)masks, pm, k, nb_y, \
+                              n_ib, Kp, Bt)))
 #define KG_ZY2N(LL, LN)                                                                                             \
-    KLAUNCH(c, "k_kg_zy", (k_kg_zy2<LL, LN><<<grid2, 256, 2 * KG_PT * KG_KT * 8, c->stream>>>(                       \
-                              c->dc, Dblk, cts, dk, d_gal + 1, pm, k, n_ib, Kp, Bt)))
+    do {                                                                                                           \
+        if (post) KG_ZY2P(LL, LN, false);                                                                          \
+        else KG_ZY2P(LL, LN, true);                                                                                \
+    } while (0)
 #define KG_ZY2(LL)                                                                                                 \
     do {                                                                                                           \
         if (c->dc.logN == 13) KG_ZY2N(LL, 13);                                                                     \
         else if (c->dc.logN == 12) KG_ZY2N(LL, 12);                                                                \
         else KG_ZY2N(LL, 0);                                                                                       \
     } while (0)
-        // post-mask: both key-switch components per thread (k_kg_zy2; N >= 32, so a block of 32
-        // positions never straddles a prime)
+        // both key-switch components per thread (k_kg_zy2; N >= 32, so a block of 32 positions never
+        // straddles a prime); GALA_KG_ZY1 selects the one-component kernel (A/B experiments)
         const dim3 grid2((unsigned)((WQ / 2 + KG_PT - 1) / KG_PT), (unsigned)((Kp + KG_KT - 1) / KG_KT), (unsigned)nbatch);
-        if (post && getenv("GALA_KG_ZY1") == nullptr) {
+        if (getenv("GALA_KG_ZY1") == nullptr) {
             switch (L) {
                 case 1: KG_ZY2(1); break;
                 case 2: KG_ZY2(2); break;
@@ -2091,6 +2099,7 @@ static int conv_kg2_run(gala_ctx* c, bool post, const uint64_t* cts, int n_ib, c
 #undef KG_ZYN
 #undef KG_ZY2
 #undef KG_ZY2N
+#undef KG_ZY2P
     }
     release(c, dig);
     release(c, Dblk);
