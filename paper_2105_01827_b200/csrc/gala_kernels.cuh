@@ -1799,8 +1799,16 @@ __global__ void __launch_bounds__(256) k_gala_e_can(DevCtx c, const u64* __restr
 //                  each (input, stream, group) sum from its 15 byte-shifted columns, reduce once mod
 //                  q, write U / Cacc (plus the step-0 member for stream 2).
 #define GTC_THREADS 576
-#define GTC_NST 2
-#define GTC_STAGE GTC_A_BYTES
+// A tiles stream in GTC_SPLIT stages per position (the same 96 KB of stages).  Measured: 1 (two
+// whole-position stages) 0.469 ms per tile, 2 (half positions) 0.494, 4: 0.538 -- the MMAs do not wait
+// on the A stream; more stages only add barrier traffic
+#ifndef GTC_SPLIT
+#define GTC_SPLIT 1
+#endif
+#define GTC_NST (2 * GTC_SPLIT)
+#define GTC_STAGE (GTC_A_BYTES / GTC_SPLIT)
+#define GTCF_NST 2                  // k_gala_tcf: whole-position stages written by the E warps
+#define GTCF_STAGE GTC_A_BYTES
 #define GTC_BB_BYTES (16 * 4096)   // 128 B rows (8 groups x 16 shifts; shift 15 is never read)
 // + 512 B: the M 128 A read of the last stage runs past its 96 rows (rows 96..127 are don't-care)
 #define GTC_SMEM (2 * GTC_BB_BYTES + GTC_NST * GTC_STAGE + 512)
@@ -1868,6 +1876,8 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             int s = 0;
             uint32_t ph = 0;
             for (long long p = p0; p < p1; p++) {
+#pragma unroll 1
+              for (int h = 0; h < GTC_SPLIT; h++) {
                 GP_WAIT(0, mbar_wait(&empty[s], ph ^ 1));
                 uint8_t* st = sSt + s * GTC_STAGE;
 #ifdef GTC_NO_A   // probe (tools/tc_probe.sh): the MMA runs on stale A tiles
@@ -1875,13 +1885,16 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
                 mbar_arrive(&full[s]);
 #else
                 mbar_expect_tx(&full[s], (uint32_t)GTC_STAGE);
-                for (int kc = 0; kc < 32; kc++)
-                    bulk_g2s(st + kc * 1536, Ecan + ((long long)kc * npos + p) * 1536, 1536, &full[s]);
+                for (int i = 0; i < 32 / GTC_SPLIT; i++) {
+                    const int kc = h * (32 / GTC_SPLIT) + i;
+                    bulk_g2s(st + i * 1536, Ecan + ((long long)kc * npos + p) * 1536, 1536, &full[s]);
+                }
 #endif
                 if (++s == GTC_NST) {
                     s = 0;
                     ph ^= 1;
                 }
+              }
             }
         }
     } else if (warp == 1) {
@@ -1894,32 +1907,38 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
             for (long long p = p0; p < p1; p++, it++) {
                 const int acc = it & 1;
                 GP_WAIT(1, mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1)));
-                GP_WAIT(2, mbar_wait(&full[s], ph));
-                const uint32_t sa = smem_u32(sSt + s * GTC_STAGE);
-                GP_WAIT(3, mbar_wait(&bfull[acc], (uint32_t)((it >> 1) & 1)));
-                asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t sb = smem_u32(sB + acc * GTC_BB_BYTES);
                 const uint32_t d = tmem + (uint32_t)(acc * 128);
 #ifndef GTC_MMA_REPEAT
 #define GTC_MMA_REPEAT 1   // probe: issue the position's MMAs this many times (MMA throughput)
 #endif
 #pragma unroll 1
-                for (int ks = 0; ks < 16 * GTC_MMA_REPEAT; ks++) {
-                    const uint64_t ad = umma_desc_kmajor(sa + (ks & 15) * 2 * 1536, 1536, 128);
-                    const uint64_t bd = umma_desc_kmajor(sb + (ks & 15) * 256, 128, 4096);
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\t"
-                        "setp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                        ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(ks));
+                for (int h = 0; h < GTC_SPLIT; h++) {
+                    GP_WAIT(2, mbar_wait(&full[s], ph));
+                    const uint32_t sa = smem_u32(sSt + s * GTC_STAGE);
+                    if (h == 0) GP_WAIT(3, mbar_wait(&bfull[acc], (uint32_t)((it >> 1) & 1)));
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    constexpr int KS = 16 / GTC_SPLIT;       // K = 32 MMAs per stage
+#pragma unroll 1
+                    for (int r = 0; r < KS * GTC_MMA_REPEAT; r++) {
+                        const int ks = h * KS + (r % KS);
+                        const uint64_t ad = umma_desc_kmajor(sa + (r % KS) * 2 * 1536, 1536, 128);
+                        const uint64_t bd = umma_desc_kmajor(sb + ks * 256, 128, 4096);
+                        const uint32_t accum = (h > 0 || r > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n\t.reg .pred p;\n\t"
+                            "setp.ne.b32 p, %4, 0;\n\t"
+                            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                            ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+                    }
+                    if (h == GTC_SPLIT - 1) umma_commit(&bempty[acc]);
+                    umma_commit(&empty[s]);
+                    if (++s == GTC_NST) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
-                umma_commit(&bempty[acc]);
-                umma_commit(&empty[s]);
                 umma_commit(&tfull[acc]);
-                if (++s == GTC_NST) {
-                    s = 0;
-                    ph ^= 1;
-                }
             }
         }
     } else if (warp >= 10) {   // 8 expander warps: thread -> B row n = 16 g + s' x one K half
@@ -2140,7 +2159,7 @@ __global__ void __maxnreg__(GTCF_MAXREG) k_gala_tcf(DevCtx c, const u64* __restr
 {
     extern __shared__ __align__(128) uint8_t gtc_sm[];
     constexpr int M = L + 1;
-    __shared__ uint64_t full[GTC_NST], empty[GTC_NST], tfull[2], tempty[2], bfull[2], bempty[2];
+    __shared__ uint64_t full[GTCF_NST], empty[GTCF_NST], tfull[2], tempty[2], bfull[2], bempty[2];
     __shared__ uint32_t tmem_base_sh;
     __shared__ u64 s_w0[4][8];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -2155,7 +2174,7 @@ __global__ void __maxnreg__(GTCF_MAXREG) k_gala_tcf(DevCtx c, const u64* __restr
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
-        for (int i = 0; i < GTC_NST; i++) {
+        for (int i = 0; i < GTCF_NST; i++) {
             mbar_init(&full[i], GTCF_NE);
             mbar_init(&empty[i], 1);
         }
@@ -2211,7 +2230,7 @@ __global__ void __maxnreg__(GTCF_MAXREG) k_gala_tcf(DevCtx c, const u64* __restr
             u64 da[2][L + 1], db[2][L + 1];
             load_d(ew, j, k, da);
             mbar_wait(&empty[s], ph ^ 1);
-            uint8_t* st = sSt + s * GTC_STAGE;
+            uint8_t* st = sSt + s * GTCF_STAGE;
 #pragma unroll
             for (int ci = 0; ci < NCH; ci++) {
                 if (ci >= nch) break;
@@ -2246,7 +2265,7 @@ __global__ void __maxnreg__(GTCF_MAXREG) k_gala_tcf(DevCtx c, const u64* __restr
             asm volatile("fence.proxy.async.shared::cta;");
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[s]);
-            if (++s == GTC_NST) {
+            if (++s == GTCF_NST) {
                 s = 0;
                 ph ^= 1;
             }
@@ -2267,7 +2286,7 @@ __global__ void __maxnreg__(GTCF_MAXREG) k_gala_tcf(DevCtx c, const u64* __restr
                 const int acc = it & 1;
                 mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
                 mbar_wait(&full[s], ph);
-                const uint32_t sa = smem_u32(sSt + s * GTC_STAGE);
+                const uint32_t sa = smem_u32(sSt + s * GTCF_STAGE);
                 mbar_wait(&bfull[acc], (uint32_t)((it >> 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t sb = smem_u32(sB + acc * GTC_BB_BYTES);
@@ -2285,7 +2304,7 @@ __global__ void __maxnreg__(GTCF_MAXREG) k_gala_tcf(DevCtx c, const u64* __restr
                 umma_commit(&bempty[acc]);
                 umma_commit(&empty[s]);
                 umma_commit(&tfull[acc]);
-                if (++s == GTC_NST) {
+                if (++s == GTCF_NST) {
                     s = 0;
                     ph ^= 1;
                 }
