@@ -519,7 +519,8 @@ __global__ void k_fold_groups(DevCtx c, const u64* __restrict__ Uv, const u64* _
 //   S[b].c0 = sum_g sigma_g(U_z.c0)            (QP)      Qadd[b].c0 = sum_g sigma_g(C_z.c0)      (Q)
 //   S[b].c1 = sum_{g: step 0} U_z.c1           (QP)      Qadd[b].c1 = sum_{g: step 0} C_z.c1     (Q)
 // (sigma_g = the automorphism of the giant step g b; identity for step 0).  The final ModDown of S plus
-// the giant-step key switches, plus Qadd, is the layer output.  grid (N / 256, M, B)
+// the giant-step key switches, plus Qadd, is the layer output.  Cacc null (key-folded path: the Q-side
+// addends are already lifted into U as P C): Qadd = 0.  grid (N / 256, M, B)
 __global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __restrict__ Cacc,
                            const unsigned* __restrict__ gal, int G, int g_lo, int g_hi, u64* __restrict__ S,
                            u64* __restrict__ Qadd)
@@ -537,10 +538,10 @@ __global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __res
         const unsigned ge = gal[g];
         const int src = ge == 1u ? k : auto_src(k, ge, c.logN);
         s0 = add_mod(s0, __ldg(U + ((z * 2 + 0) * M + j) * NN + src), q);
-        if (j < L) c0 = add_mod(c0, __ldg(Cacc + ((z * 2 + 0) * L + j) * NN + src), q);
+        if (j < L && Cacc) c0 = add_mod(c0, __ldg(Cacc + ((z * 2 + 0) * L + j) * NN + src), q);
         if (ge == 1u) {
             s1 = add_mod(s1, __ldg(U + ((z * 2 + 1) * M + j) * NN + k), q);
-            if (j < L) c1 = add_mod(c1, __ldg(Cacc + ((z * 2 + 1) * L + j) * NN + k), q);
+            if (j < L && Cacc) c1 = add_mod(c1, __ldg(Cacc + ((z * 2 + 1) * L + j) * NN + k), q);
         }
     }
     S[(((long long)b * 2 + 0) * M + j) * NN + k] = s0;
@@ -1387,6 +1388,20 @@ __device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lb
     return d;
 }
 
+#ifdef KF_SUSPEND   // experiment: try_wait with a suspend-time hint (ns)
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(phase), "r"(KF_SUSPEND)
+        : "memory");
+    return ok != 0;
+}
+#else
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase)
 {
     uint32_t ok;
@@ -1399,6 +1414,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t phase)
         : "memory");
     return ok != 0;
 }
+#endif
 
 // K-major, no swizzle: 16-byte chunk (row r, k-chunk c) at (r % 8) 16 + (r / 8) SBO + c 128, SBO = 8 Kp
 __device__ __forceinline__ uint32_t kg_tc_off(int r, int c, int Kp) { return (r & 7) * 16 + (r >> 3) * 8 * Kp + c * 128; }
@@ -1428,6 +1444,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity)
 {
     while (!mbar_try_wait(smem_u32(b), parity)) {
     }
+}
+// a whole warp waits: lane 0 polls, the others hold at __syncwarp (no shared-memory spinning by 32 lanes:
+// many polling warps starve the MMA issuer's own barrier traffic)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* b, uint32_t parity)
+{
+    if ((threadIdx.x & 31) == 0) mbar_wait(b, parity);
+    __syncwarp();
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b)
 {
@@ -2090,6 +2113,577 @@ __global__ void __launch_bounds__(GTC_THREADS, 1) k_gala_tc(DevCtx c, const uint
     if (warp == 0 || warp == 1 || warp == 2 || warp == 10) GP_FLUSH(warp == 0)
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
+// ---------------------------------------------------------------------------
+// GALA schedule 2, key-folded tensor-core baby steps (the production FC path).
+//
+// Group g's baby-step sum in component cc at QP position p = (j, k), for input b, is
+//   U_cc[b][g][p] = sum_{jj >= 1} w_{g,jj}[p] E_cc,jj[b][p]  +  P [j < L] X_cc[b][g][p]
+//   E_cc,jj = sum_i sigma_jj(D_i)[b][p] ksk_jj[i][cc][p],  X_0 = sum_jj w_{g,jj} sigma_jj(c0),  X_1 = w_{g,0} c1
+// (the split form k_gala_e_can / k_gala_tc keeps X in a separate Q-side addend Cacc; P X is the same
+// addend lifted into QP: ModDown(Y + P X) = ModDown(Y) + X exactly, so the words do not change).  The key
+// limbs and P do not depend on the input, so they fold into the weights:
+//   U_cc[b][g][p] = sum_{jj < 64, st < 4} A[b][jj][st][p] Wk[p][cc][jj][g][st]
+//   A[b][jj][st] = sigma_jj(D_st)[b] (st < L),  sigma_jj(c0)[b] (st = 3, j < L),  0 otherwise
+//   Wk[cc][jj][g][i] = ksk_jj[i][cc] w_{g,jj} (jj >= 1),  Wk[1][0][g][j] = P w_{g,0},  Wk[0][jj][g][3] = P w_{g,jj}
+// (mod q_j, Montgomery).  Per position that is one integer matrix product, M = 256 inputs, N = 2 x 8
+// outputs, K = 64 rotations x 4 streams, exact as a byte convolution on the int8 tensor cores:
+//   D[b][(cc, g, s')] = sum_(jj, st, a) A_a[b][(jj, st)] * w_(s' - a)[(cc, g)][(jj, st)],   value = sum_s' 256^s' D_s'
+// with A in natural little-endian byte order (K = (jj, st, a), 32 bytes per rotation) and B the
+// byte-shift (Toeplitz) expansion of the folded weights.  Every column D_s' < 2048 * 255^2 < 2^27 is exact
+// in int32; the value is rebuilt mod q_j from three 40-bit-spaced partial sums and one REDC.
+// E_jj never exists: the kernel streams the digit blocks (8 KB per position, read 64 times from L2 --
+// positions run prime by prime across the grid so a prime's blocks stay resident) and the folded
+// weights (32 KB per position, once per tile of 256 inputs).
+#define KF_W_WORDS (2 * 64 * 8 * 4)     // folded weights per position: [cc][jj][g][st], byte-reversed words
+#define KF_W_BYTES (KF_W_WORDS * 8)
+__device__ __forceinline__ u64 mad_wide_u32(uint32_t a, uint32_t b, u64 c)
+{
+    u64 r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+    return r;
+}
+// 32 consecutive TMEM columns of the warp's lane group into registers (completion: tcgen05.wait::ld)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* x)
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+        "%30, %31}, [%32];"
+        : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]),
+          "=r"(x[7]), "=r"(x[8]), "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]),
+          "=r"(x[14]), "=r"(x[15]), "=r"(x[16]), "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]),
+          "=r"(x[21]), "=r"(x[22]), "=r"(x[23]), "=r"(x[24]), "=r"(x[25]), "=r"(x[26]), "=r"(x[27]),
+          "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
+        : "r"(taddr));
+}
+
+// Wk from the schedule-2 plaintexts (pts2 [T][M][N], Montgomery, sigma_jj pre-applied) and the baby-step
+// rotation keys ([L][2][M][N] per step, keys[jj]); pmod[j] = P mod q_j.  Zero outside g < G, jj < baby.
+template <int L>
+__global__ void k_gala_kfw(DevCtx c, const u64* __restrict__ pts2, const u64* const* __restrict__ keys,
+                           const u64* __restrict__ pmod, int baby, int G, u64* __restrict__ Wk)
+{
+    constexpr int M = L + 1;
+    const long long MN = (long long)M * c.N;
+    const long long total = MN * KF_W_WORDS;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(e % KF_W_WORDS);
+        const long long p = e / KF_W_WORDS;
+        const int st = i & 3, g = (i >> 2) & 7, jj = (i >> 5) & 63, cc = i >> 11;
+        const int j = (int)(p / c.N);
+        u64 v = 0;
+        if (g < G && jj < baby) {
+            const ModC md = c.mod[j];
+            const u64 w = __ldg(pts2 + (long long)(g * baby + jj) * MN + p);
+            const u64 pm = mont_mul(__ldg(pmod + j), md.r2, md);     // P R mod q_j
+            if (st < L) {
+                if (jj >= 1) v = mont_mul(__ldg(keys[jj] + (long long)(2 * st + cc) * MN + p), w, md);
+                else if (cc == 1 && st == j) v = mont_mul(w, pm, md);
+            } else if (st == 3 && cc == 0 && j < L) {
+                v = mont_mul(w, pm, md);
+            }
+        }
+        Wk[e] = bswap64(v);
+    }
+}
+
+// A operand of one tile of <= 256 inputs: the identity digit blocks (Dblk [b][(L M + L)][N], b < B)
+// rearranged per position into Dq[p][half][kc][row group][8][16 B] (tcgen05 K-major core-matrix order
+// per M = 128 half; row = input, 32 bytes = streams D_0, D_1, D_2, c0; rows >= B and absent streams
+// zero): 8 KB per position, half h = inputs 128 h .. 128 h + 127 (the CTA of rank h of a pair reads it).
+// grid (M N / KF_DQ_POS), 256 threads.
+#define KF_ROWS 256
+#define KF_DQ_BYTES (KF_ROWS * 32)
+#define KF_DQ_POS 8
+#define KF_DQ_STRIDE (KF_DQ_BYTES + 16)        // padded per-position stride in shared memory (bank spread)
+template <int L>
+__global__ void __launch_bounds__(256) k_gala_dq(DevCtx c, const u64* __restrict__ Dblk, int B, uint8_t* __restrict__ Dq)
+{
+    extern __shared__ __align__(16) uint8_t dq_sm[];
+    constexpr int M = L + 1;
+    const int N = c.N;
+    const long long p0 = (long long)blockIdx.x * KF_DQ_POS;
+    const int j = (int)(p0 / N), k0 = (int)(p0 - (long long)j * N);
+    const long long bw = (long long)(L * M + L) * N;
+    for (int idx = threadIdx.x; idx < KF_ROWS * 4 * KF_DQ_POS; idx += blockDim.x) {
+        const int kl = idx % KF_DQ_POS, st = (idx / KF_DQ_POS) & 3, b = idx / (4 * KF_DQ_POS);
+        int slot = -1;
+        if (st < L) slot = st * M + j;
+        else if (st == 3 && j < L) slot = L * M + j;
+        u64 v = 0;
+        if (b < B && slot >= 0) v = __ldg(Dblk + b * bw + (long long)slot * N + k0 + kl);
+        *(u64*)(dq_sm + kl * KF_DQ_STRIDE + (b >> 7) * 4096 + (st >> 1) * 2048 + ((b & 127) >> 3) * 128 + (b & 7) * 16 +
+                (st & 1) * 8) = v;
+    }
+    __syncthreads();
+    uint4* dst = (uint4*)(Dq + p0 * KF_DQ_BYTES);
+    for (int idx = threadIdx.x; idx < KF_DQ_POS * (KF_DQ_BYTES / 16); idx += blockDim.x)
+        dst[idx] = *(const uint4*)(dq_sm + (idx / (KF_DQ_BYTES / 16)) * KF_DQ_STRIDE + (idx % (KF_DQ_BYTES / 16)) * 16);
+}
+#define KF_DQ_SMEM (KF_DQ_POS * KF_DQ_STRIDE)
+
+// bulk copy with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* b, uint64_t pol)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// cluster helpers (CTA pairs)
+__device__ __forceinline__ uint32_t cluster_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr)
+{
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity)
+{
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// commit the issuing thread's prior MMAs to the same barrier in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* b)
+{
+    const uint16_t mask = 3;
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(b)), "h"(mask) : "memory");
+}
+
+// The key-folded baby-step sums of a tile of <= 256 inputs on CTA pairs (cta_group::2).  The pair's MMA
+// is M = 256 (rank r holds inputs 128 r .. 128 r + 127 of A and its accumulator rows), N = 256 (rank r
+// holds the B rows of component cc = r: 8 groups x 16 shifts), K = 32 per rotation; each CTA's TMEM has
+// two 256-column accumulators (positions alternate).  Cluster c of the grid takes position blocks
+// (4 consecutive k) c, c + clusters, ... -- the whole grid sweeps the primes in order.  Per CTA:
+//   warp 0 lane 0   producer: its component's folded weights in chunks of KF_WJ rotations (4 KB, two
+//                   chunks ahead) and, per stage of KF_JS rotations, its half of each digit block
+//                   sigma_jj(p) (one 4 KB bulk copy per rotation);
+//   warp 1 lane 0   rank 0: the MMA issuer -- per stage ONE wait (full[s]: both CTAs' stage complete),
+//                   KF_JS tcgen05.mma.cta_group::2.kind::i8, ONE commit multicast to both CTAs' empty[s];
+//                   rank 1: relay -- waits its own full[s] and arrives on rank 0's full[s];
+//   warps 2..5      expanders: thread = B row (g, s') of component cc = rank; per rotation the 4 streams'
+//                   8-byte windows (byte reversal + shift) of the folded weights;
+//   warps 6..13     epilogue: TMEM lane group warp % 4 (lane = input), component (warp - 6) / 4: rebuild the
+//                   8 group sums mod q_j, one 32-byte store per output per 4 positions; the accumulator's
+//                   release (tempty, counted on rank 0) comes from both CTAs' epilogues.
+// Why this shape (measured, profiles/r2_experiments.md): a thread cannot keep the tensor pipe fed
+// through fine-grained mbarrier waits and every role pays a fixed cost per stage (tools/mma_bench.cu,
+// tools/kf_trace.py), so stages carry several MMAs; the pair halves each SM's Toeplitz expansion and
+// shared-memory bytes per MMA (A 4 KB + B 4 KB), leaving room for KF_ST stages and for two accumulators
+// (the epilogue of position p overlaps the MMAs of p + 1).  (14 warps: <= 4 per SM sub-partition.)
+#ifndef KF_JS
+#define KF_JS 4                          // rotations per stage
+#endif
+#ifndef KF_ST
+#define KF_ST 6                          // ring depth
+#endif
+#define KF_WJ 16                         // rotations per folded-weight chunk
+#define KF_WST 4
+#define KF_WCH_BYTES (KF_WJ * 256)       // one component's weights for KF_WJ rotations
+#define KF_LAG 2                         // A stages in flight per producer warp (cp.async groups)
+#define KF_A_STAGE (KF_JS * 4096)
+#define KF_B_STAGE (KF_JS * 4096)
+#define KF_SMEM (KF_ST * (KF_A_STAGE + KF_B_STAGE) + KF_WST * KF_WCH_BYTES)
+#define KF_THREADS (14 * 32)
+#define KF_EPI0 6
+#ifdef KF_TRACE   // timeline of CTA 0 (tools/kf_trace.py): [event][index] clock64 stamps
+__device__ unsigned long long g_kf_trace[32][1024];
+#define KF_T(ev, idx) do { if (blockIdx.x == 0 && (idx) < 1024) g_kf_trace[ev][idx] = clock64(); } while (0)
+#else
+#define KF_T(ev, idx) do { } while (0)
+#endif
+template <int L>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KF_THREADS, 1)
+k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, const unsigned* __restrict__ gal,
+          int baby, int G, int B, u64* __restrict__ U)
+{
+    extern __shared__ __align__(128) uint8_t kf_sm[];
+    constexpr int M = L + 1;
+    __shared__ uint64_t full[KF_ST], empty[KF_ST], wfull[KF_WST], wempty[KF_WST], tfull[2], tempty[2];
+    __shared__ uint32_t tmem_base_sh;
+    __shared__ u64 s_c40[M], s_c80[M];
+    __shared__ unsigned s_gal[64];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_rank();
+    const int N = c.N, logN = c.logN;
+    const long long nblk = (long long)M * N / 4;
+    const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int nst = (baby + KF_JS - 1) / KF_JS;          // stages per position (rotations >= baby: zero weights)
+    uint8_t* sA = kf_sm;
+    uint8_t* sB = kf_sm + KF_ST * KF_A_STAGE;
+    uint8_t* sW = sB + KF_ST * KF_B_STAGE;
+    if (tid < 64) s_gal[tid] = gal[tid];
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < KF_ST; i++) {
+            // rank 0: own producer (expect_tx) + 4 own expander warps + rank 1's relay; rank 1: 1 + 4
+            mbar_init(&full[i], rank == 0 ? 1 + 4 + 1 : 1 + 4);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < KF_WST; i++) {
+            mbar_init(&wfull[i], 1);
+            mbar_init(&wempty[i], 4);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 16);       // rank 0's: 8 epilogue warps of each CTA
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (tid < M) {   // 2^40, 2^80 mod q_j for the rebuild
+        const u64 q = c.mod[tid].q;
+        u64 v = 1;
+        for (int i = 0; i < 80; i++) {
+            v = add_mod(v, v, q);
+            if (i == 39) s_c40[tid] = v;
+        }
+        s_c80[tid] = v;
+    }
+    // B rows s' = 15 are never written by the expanders: zero every B stage once
+    for (int i = tid; i < KF_ST * KF_B_STAGE / 16; i += blockDim.x) ((uint4*)sB)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();                  // barriers initialised in both CTAs before any remote arrive
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base_sh;
+    if (warp == 0) {
+        {   // the whole warp: lane 0 waits and arms the barriers, lanes 0 .. KF_JS - 1 issue one copy each
+            // (one thread issuing every bulk copy was the bottleneck: ~200 clk per cp.async.bulk issue)
+            int sa = 0, ws = 0;
+            uint32_t pha = 0, phw = 0;
+            // L2: the digit blocks of the current prime are re-read 64 times (keep), the weights stream (once)
+            const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+            const int nch = (nst * KF_JS + KF_WJ - 1) / KF_WJ;            // weight chunks per position
+            const long long npos = nblk > cid ? ((nblk - 1 - cid) / ncl + 1) * 4 : 0;
+            const long long wtotal = npos * nch;
+            long long wnext = 0;                                         // next weight chunk to issue
+            auto issue_w_upto = [&](long long last) {                     // chunks [wnext, last]
+                for (; wnext <= last && wnext < wtotal; wnext++) {
+                    const long long itw = wnext / nch;
+                    const int ch = (int)(wnext - itw * nch);
+                    const long long pw = (cid + (itw >> 2) * ncl) * 4 + (itw & 3);
+                    mbar_wait(&wempty[ws], phw ^ 1);
+#ifdef KF_NO_W   // probe builds (tools/kf_probe.sh): role isolation, results are garbage
+                    mbar_arrive(&wfull[ws]);
+#else
+                    mbar_expect_tx(&wfull[ws], (uint32_t)KF_WCH_BYTES);
+                    bulk_g2s_hint(sW + ws * KF_WCH_BYTES,
+                                  (const uint8_t*)(Wk + pw * KF_W_WORDS) + rank * (KF_W_BYTES / 2) + ch * KF_WCH_BYTES, KF_WCH_BYTES,
+                                  &wfull[ws], pol_stream);
+#endif
+                    if (++ws == KF_WST) {
+                        ws = 0;
+                        phw ^= 1;
+                    }
+                }
+            };
+            long long itp = 0;
+#ifndef KF_A_TMA
+            long long gsp = 0;   // stages issued (cp.async groups committed)
+#endif
+            for (long long blk = cid; blk < nblk; blk += ncl) {
+                for (int pi = 0; pi < 4; pi++, itp++) {
+                    const long long p = blk * 4 + pi;
+                    const int j = (int)(p / N), k = (int)(p - (long long)j * N);
+                    const uint8_t* base = Dq + (long long)j * N * KF_DQ_BYTES + rank * 4096;
+                    for (int s = 0; s < nst; s++) {
+#ifndef KF_A_TMA
+                        // A by LDGSTS from all 32 lanes (bulk copies are serviced ~one at a time per SM: 4 KB each
+                        // capped the gather at ~12 B/clk); a stage's copies complete KF_LAG stages later
+                        if (lane == 0) {
+                            issue_w_upto(itp * nch + (s * KF_JS) / KF_WJ + KF_WST - 2);   // 2 chunks ahead, 1 slot of slack
+                            mbar_wait(&empty[sa], pha ^ 1);
+                            KF_T(2, itp * nst + s);
+                        }
+                        __syncwarp();
+#ifndef KF_NO_A
+#pragma unroll
+                        for (int jl = 0; jl < KF_JS; jl++) {
+                            const int jj = s * KF_JS + jl;
+                            const unsigned ge = s_gal[jj];
+                            const int src = ge == 1u ? k : auto_src(k, ge, logN);
+                            const uint8_t* g = base + (long long)src * KF_DQ_BYTES + lane * 16;
+                            const uint32_t d = smem_u32(sA + sa * KF_A_STAGE + jl * 4096) + lane * 16;
+#pragma unroll
+                            for (int i = 0; i < 8; i++)
+                                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
+                                             ::"r"(d + i * 512), "l"(g + i * 512), "l"(pol_keep) : "memory");
+                        }
+#endif
+                        asm volatile("cp.async.commit_group;" ::: "memory");
+                        if (gsp >= KF_LAG) {
+                            asm volatile("cp.async.wait_group %0;" ::"n"(KF_LAG) : "memory");
+                            asm volatile("fence.proxy.async.shared::cta;");
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&full[(int)((gsp - KF_LAG) % KF_ST)]);
+                        }
+                        gsp++;
+                        if (lane == 0) KF_T(3, itp * nst + s);
+                        if (++sa == KF_ST) {
+                            sa = 0;
+                            pha ^= 1;
+                        }
+                        continue;
+#endif
+                        if (lane == 0) {
+                            issue_w_upto(itp * nch + (s * KF_JS) / KF_WJ + KF_WST - 2);   // 2 chunks ahead, 1 slot of slack
+                            mbar_wait(&empty[sa], pha ^ 1);
+                            KF_T(2, itp * nst + s);
+#ifdef KF_NO_A
+                            mbar_arrive(&full[sa]);
+#else
+                            mbar_expect_tx(&full[sa], (uint32_t)KF_A_STAGE);
+#endif
+                        }
+                        __syncwarp();
+#ifndef KF_NO_A
+                        if (lane < KF_JS) {
+                            const int jj = s * KF_JS + lane;
+                            const unsigned ge = s_gal[jj];
+                            const int src = ge == 1u ? k : auto_src(k, ge, logN);
+                            bulk_g2s_hint(sA + sa * KF_A_STAGE + lane * 4096, base + (long long)src * KF_DQ_BYTES, 4096, &full[sa],
+                                          pol_keep);
+                        }
+#endif
+                        if (lane == 0) KF_T(3, itp * nst + s);
+                        if (++sa == KF_ST) {
+                            sa = 0;
+                            pha ^= 1;
+                        }
+                    }
+                }
+            }
+#ifndef KF_A_TMA
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;");
+            __syncwarp();
+            for (long long g2 = gsp - KF_LAG < 0 ? 0 : gsp - KF_LAG; g2 < gsp; g2++)
+                if (lane == 0) mbar_arrive(&full[(int)(g2 % KF_ST)]);
+#endif
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {   // the pair's MMA issuer
+            // M 256 (cta_group::2), N 256, s32 accumulate, unsigned bytes
+            const uint32_t idesc = (2u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+            int sa = 0, it = 0;
+            uint32_t pha = 0;
+            long long gs = 0;
+            for (long long blk = cid; blk < nblk; blk += ncl) {
+                for (int pi = 0; pi < 4; pi++, it++) {
+                    const int acc = it & 1;
+                    mbar_wait_cluster(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
+                    KF_T(6, it);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                    const uint32_t d = tmem + (uint32_t)(acc * 256);
+                    for (int s = 0; s < nst; s++, gs++) {
+                        KF_T(9, gs);
+                        mbar_wait_cluster(&full[sa], pha);
+                        KF_T(0, gs);
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        const uint32_t a0 = smem_u32(sA + sa * KF_A_STAGE), b0 = smem_u32(sB + sa * KF_B_STAGE);
+#pragma unroll
+                        for (int jl = 0; jl < KF_JS; jl++) {
+                            const uint64_t ad = umma_desc_kmajor(a0 + jl * 4096, 2048, 128);
+                            const uint64_t bd = umma_desc_kmajor(b0 + jl * 4096, 2048, 128);
+                            const uint32_t accum = (s | jl) ? 1u : 0u;
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\t"
+                                "setp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                                ::"r"(d), "l"(ad), "l"(bd), "r"(idesc), "r"(accum));
+                        }
+                        umma_commit_pair(&empty[sa]);
+                        KF_T(1, gs);
+                        if (++sa == KF_ST) {
+                            sa = 0;
+                            pha ^= 1;
+                        }
+                    }
+                    umma_commit_pair(&tfull[acc]);
+                }
+            }
+        } else if (lane == 0) {   // rank 1: relay its stages' completion to the issuer's barrier
+            const uint32_t peer_full0 = mapa_shared(smem_u32(&full[0]), 0);
+            int sa = 0;
+            uint32_t pha = 0;
+            for (long long blk = cid; blk < nblk; blk += ncl)
+                for (int pi = 0; pi < 4; pi++)
+                    for (int s = 0; s < nst; s++) {
+                        mbar_wait(&full[sa], pha);
+                        mbar_arrive_remote(peer_full0 + (uint32_t)(sa * sizeof(uint64_t)));
+                        if (++sa == KF_ST) {
+                            sa = 0;
+                            pha ^= 1;
+                        }
+                    }
+        }
+    } else if (warp < KF_EPI0) {   // expanders: thread = B row n = 16 g + s' of component cc = rank
+        const int n = tid - 64;
+        const int sp = n & 15, g = n >> 4;
+        const bool act = sp < 15;
+        const int sh_r = sp <= 7 ? 8 * (7 - sp) : 0, sh_l = sp > 7 ? 8 * (sp - 7) : 0;
+        int sb = 0, ws = 0;
+        long long gse = 0;
+        uint32_t phb = 0, phw = 0;
+        for (long long blk = cid; blk < nblk; blk += ncl) {
+            for (int pi = 0; pi < 4; pi++) {
+                for (int s = 0; s < nst; s++, gse++) {
+                    const int jw0 = (s * KF_JS) % KF_WJ;     // first rotation of the stage within its weight chunk
+                    if (jw0 == 0) mbar_wait(&wfull[ws], phw);
+                    mbar_wait(&empty[sb], phb ^ 1);
+#ifdef KF_NO_B
+                    if (false) {
+#else
+                    if (act) {
+#endif
+                        const uint8_t* wsrc = sW + ws * KF_WCH_BYTES + g * 32 + jw0 * 256;
+                        uint8_t* dst = sB + sb * KF_B_STAGE + n * 16;
+                        ulonglong2 r[KF_JS][2];
+#pragma unroll
+                        for (int jl = 0; jl < KF_JS; jl++) {
+                            const ulonglong2* src = (const ulonglong2*)(wsrc + jl * 256);
+                            r[jl][0] = src[0];
+                            r[jl][1] = src[1];
+                        }
+#pragma unroll
+                        for (int jl = 0; jl < KF_JS; jl++) {
+                            uint8_t* o = dst + jl * 4096;
+                            const ulonglong2 r0 = r[jl][0], r1 = r[jl][1];
+                            *(ulonglong2*)o = make_ulonglong2((r0.x >> sh_r) << sh_l, (r0.y >> sh_r) << sh_l);
+                            *(ulonglong2*)(o + 2048) = make_ulonglong2((r1.x >> sh_r) << sh_l, (r1.y >> sh_r) << sh_l);
+                        }
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&full[sb]);
+                    if (++sb == KF_ST) {
+                        sb = 0;
+                        phb ^= 1;
+                    }
+                    if (jw0 + KF_JS == KF_WJ || s == nst - 1) {   // weight chunk consumed
+                        if (lane == 0) mbar_arrive(&wempty[ws]);
+                        if (++ws == KF_WST) {
+                            ws = 0;
+                            phw ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else {   // epilogue
+        const int lg = warp & 3, cc = (warp - KF_EPI0) >> 2, b = (int)rank * 128 + lg * 32 + lane;
+        const bool active = b < B;
+        const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+        const uint64_t pol_out = policy_evict_first();   // U is read back by the next kernels, not by this one
+        int it = 0;
+        for (long long blk = cid; blk < nblk; blk += ncl) {
+            const long long p = blk * 4;
+            const int j = (int)(p / N), k = (int)(p - (long long)j * N);
+            const u64 q = c.mod[j].q, c80 = s_c80[j];
+            auto rebuild = [&](const uint32_t* x) -> u64 {
+                // three 40-bit-spaced partial sums: one IMAD.WIDE.U32 per column for 256^u < 2^32 (x < 2^27),
+                // the 256^4 column added into the high word
+                u64 lo5 = x[0], mi5 = x[5], hi5 = x[10];
+#pragma unroll
+                for (int u = 1; u < 4; u++) {
+                    lo5 = mad_wide_u32(x[u], 1u << (8 * u), lo5);
+                    mi5 = mad_wide_u32(x[5 + u], 1u << (8 * u), mi5);
+                    hi5 = mad_wide_u32(x[10 + u], 1u << (8 * u), hi5);
+                }
+                lo5 += (u64)x[4] << 32;
+                mi5 += (u64)x[9] << 32;
+                hi5 += (u64)x[14] << 32;
+                // value = lo5 + 2^40 mi5 + 2^80 hi5 == (lo5 + 2^40 mi5) + c80 hi5 (mod q): the first part is
+                // < 2^100, the product < 2^59 q, the sum < 2^62 q (REDC input bound q 2^64)
+                u64 lo = hi5 * c80, hi = __umul64hi(hi5, c80);
+                const u64 m = mi5 << 40;
+                lo += m;
+                hi += (mi5 >> 24) + (lo < m ? 1ull : 0ull);
+                lo += lo5;
+                hi += lo < lo5 ? 1ull : 0ull;
+                return csub(redc_sf_lazy(hi, lo, q), q);
+            };
+            u64 res[4][8];
+#pragma unroll
+            for (int pi = 0; pi < 4; pi++, it++) {
+                const int acc = it & 1;
+                mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t taddr = tmem + ((uint32_t)(lg * 32) << 16) + (uint32_t)(acc * 256 + cc * 128);
+#ifdef KF_NO_EPI
+                asm volatile("tcgen05.fence::before_thread_sync;");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(tempty0 + (uint32_t)(acc * sizeof(uint64_t)));
+                for (int h = 0; h < 8; h++) res[pi][h] = taddr;
+                continue;
+#endif
+#pragma unroll
+                for (int h = 0; h < 4; h++) {
+                    uint32_t x[32];
+                    tmem_ld32(taddr + 32 * h, x);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (h == 3) {   // this warp's accumulator columns are in registers
+                        asm volatile("tcgen05.fence::before_thread_sync;");
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(tempty0 + (uint32_t)(acc * sizeof(uint64_t)));
+                        if (warp == KF_EPI0 && lane == 0) KF_T(8, it);
+                    }
+                    res[pi][2 * h] = rebuild(x);
+                    res[pi][2 * h + 1] = rebuild(x + 16);
+                }
+            }
+            if (active) {
+                u64* out0 = U + (((long long)b * G * 2 + cc) * M + j) * (long long)N + k;
+                const long long gstride = 2LL * M * N;
+#pragma unroll
+                for (int g = 0; g < 8; g++)
+                    if (g < G)
+                        asm volatile("st.global.L2::cache_hint.v4.u64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(out0 + g * gstride),
+                                     "l"(res[0][g]), "l"(res[1][g]), "l"(res[2][g]), "l"(res[3][g]), "l"(pol_out)
+                                     : "memory");
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    cluster_sync_all();                  // no CTA leaves while its pair may still read its smem / barriers
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 // ---------------------------------------------------------------------------

@@ -139,6 +139,8 @@ struct gala_ctx {
     std::vector<cudaEvent_t> pool;
     u64* d_kg_off = nullptr;                  // per prime: multiple of q >= 2^90 (128-bit, hi/lo)
     int num_sms = 148;
+    // tensor-core FC weights: key-folded (k_gala_kf, default) or the split E / MMA pair (GALA_FC_KF=0)
+    bool fc_kf = true;
 };
 
 static void prof_begin(gala_ctx* c, cudaEvent_t* a, cudaEvent_t* b)
@@ -267,6 +269,23 @@ struct EngMember {
 };
 
 static const u64* key_for(gala_ctx* c, int step);
+// experiments: GALA_DEBUG_DUMP=prefix writes a device buffer to prefix_<tag>.bin (synchronous)
+static void debug_dump(gala_ctx* c, const char* tag, const u64* d, size_t words)
+{
+    const char* pre = getenv("GALA_DEBUG_DUMP");
+    if (!pre || !d) return;
+    std::vector<u64> h(words);
+    cudaStreamSynchronize(c->stream);
+    cudaMemcpy(h.data(), d, words * 8, cudaMemcpyDeviceToHost);
+    std::string fn = std::string(pre) + "_" + tag + ".bin";
+    FILE* f = fopen(fn.c_str(), "wb");
+    if (f) {
+        fwrite(h.data(), 8, words, f);
+        fclose(f);
+    }
+}
+// key-folded tensor-core FC weights (k_gala_kf) for this context
+static bool fc_kf_on(const gala_ctx* c) { return c->fc_kf && c->dc.L <= 3 && c->dc.N % 16 == 0; }
 
 static int moddown_groups(gala_ctx* c, u64* U, u64* Cacc, int G, u64* const* d_outs)
 {
@@ -887,6 +906,16 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_gala_tcf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tcf<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
     CKC(cudaFuncSetAttribute(k_gala_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, GTC_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_kf<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, KF_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_kf<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, KF_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_kf<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, KF_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_dq<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, KF_DQ_SMEM));  // 64 KB
+    CKC(cudaFuncSetAttribute(k_gala_dq<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, KF_DQ_SMEM));
+    CKC(cudaFuncSetAttribute(k_gala_dq<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, KF_DQ_SMEM));
+    {
+        const char* e = getenv("GALA_FC_KF");
+        c->fc_kf = !(e && e[0] == '0');
+    }
     CKC(cudaFuncSetAttribute(k_kg1_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CKC(cudaFuncSetAttribute(k_kg1_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CKC(cudaFuncSetAttribute(k_kg1_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1324,12 +1353,49 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     // large enough for a tile's fixed per-position cost (K = 64 rotations x 8 bytes whatever T is) to pay:
     // T >= 128 (config 2: 17.5k -> 19.3k layers/s at 96 inputs; config 1, T = 8, stays on the CUDA cores,
     // 0.0016 vs 0.0066 ms per layer at 1024 inputs); the rest of the layer stays batched over all B
-    const bool tc = wcan != nullptr && B >= 16 && (B <= 32 || (T >= 128 && (B % 32 == 0 || B % 32 >= 16))) &&
+    const bool kf = wcan != nullptr && fc_kf_on(c) && B >= 16 && G <= 8 && baby <= 64 && getenv("GALA_FC_NO_TC") == nullptr;
+    const bool tc = !kf && wcan != nullptr && !fc_kf_on(c) && B >= 16 &&
+                    (B <= 32 || (T >= 128 && (B % 32 == 0 || B % 32 >= 16))) &&
                     G <= 8 && baby <= 64 && (N % 32) == 0 && getenv("GALA_FC_NO_TC") == nullptr;
     // fused E + MMA kernel (k_gala_tcf): experiment, slower than the k_gala_e_can / k_gala_tc pair so far
     // (the E warps are load-latency bound at 7-11 warps per SM; profiles/r2_experiments.md)
     const bool fused = tc && getenv("GALA_FC_FUSED") != nullptr;
-    if (fused) {
+    if (kf) {
+        // key-folded tensor-core baby steps: per tile of <= 256 inputs the A blocks (k_gala_dq), then one
+        // persistent kernel; U carries the Q-side addends lifted into QP (P C), so Cacc is not formed
+        release(c, Cacc);
+        Cacc = nullptr;
+        uint8_t* Dq;
+        RET(scratch(c, &Dq, (size_t)MN * KF_DQ_BYTES));
+        std::vector<unsigned> gal64(64, 1u);
+        for (int jj = 1; jj < baby; jj++) gal64[jj] = gal[jj];
+        unsigned* d_gal64;
+        RET(upload(c, gal64.data(), gal64.size() * sizeof(unsigned), (void**)&d_gal64));
+        // CTA pairs (cta_group::2): an even grid of at most one CTA per SM
+        const long long nblk = MN / 4;
+        int grid = (int)(2 * nblk < c->num_sms ? 2 * nblk : c->num_sms) & ~1;
+        if (grid < 2) grid = 2;
+        for (int b0 = 0; b0 < B; b0 += KF_ROWS) {
+            const int bt = B - b0 < KF_ROWS ? B - b0 : KF_ROWS;
+            const u64* Dt = Dblk + (long long)b0 * blk_words;
+            u64* Ut = U + (long long)b0 * G * 2 * M * N;
+#define GALA_KF(LL)                                                                                               \
+    do {                                                                                                          \
+        KLAUNCH(c, "k_gala_dq", (k_gala_dq<LL><<<(unsigned)(MN / KF_DQ_POS), 256, KF_DQ_SMEM, c->stream>>>(c->dc, Dt, bt, Dq))); \
+        KLAUNCH(c, "k_gala_kf", (k_gala_kf<LL><<<grid, KF_THREADS, KF_SMEM, c->stream>>>(c->dc, Dq, (const u64*)wcan,   \
+                                                                                     d_gal64, baby, G, bt, Ut)));  \
+    } while (0)
+            switch (L) {
+                case 1: GALA_KF(1); break;
+                case 2: GALA_KF(2); break;
+                default: GALA_KF(3); break;
+            }
+#undef GALA_KF
+        }
+        release(c, Dq);
+        release(c, d_gal64);
+        debug_dump(c, "U", U, (size_t)Z * 2 * M * N);
+    } else if (fused) {
         // tensor-core baby-step sums with the E_jj key products computed in the kernel (k_gala_tcf):
         // per tile of 32 inputs, the digit blocks input-minor (k_gala_dt), then one persistent kernel
         u64 *Dt, *Kt;
@@ -1387,6 +1453,8 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
 #undef GALA_TC
         }
         release(c, Ecan);
+        debug_dump(c, "U", U, (size_t)Z * 2 * M * N);
+        debug_dump(c, "C", Cacc, (size_t)Z * 2 * L * N);
     } else {
     RET(scratch(c, &E, (size_t)B * (baby - 1) * 2 * MN));
     RET(scratch(c, &R0, (size_t)B * (baby - 1) * L * N));
@@ -1452,7 +1520,7 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
         a.r = rr;
         a.U = U;
         a.add0 = Cacc;
-        a.add1 = Cacc + (long long)L * N;
+        a.add1 = Cacc ? Cacc + (long long)L * N : nullptr;
         a.add_is = 2LL * L * N;
         a.out = inner;
         a.out_is = W;
@@ -1543,13 +1611,36 @@ int gala_mv_gala2_finish(gala_ctx* c, uint64_t* qp_sum, uint64_t* q_add, int B, 
     return GALA_OK;
 }
 
-size_t gala_fc_tc_weight_bytes(gala_ctx* c) { return (size_t)c->dc.M * c->dc.N * GTC_W_BYTES; }
+size_t gala_fc_tc_weight_bytes(gala_ctx* c)
+{
+    return (size_t)c->dc.M * c->dc.N * (fc_kf_on(c) ? (size_t)KF_W_BYTES : (size_t)GTC_W_BYTES);
+}
 
 int gala_fc_tc_weights(gala_ctx* c, const uint64_t* pts2, int T, int baby, uint8_t* wcan)
 {
     if (baby <= 0 || T % baby) return set_err(GALA_ERR_PARAM, "baby %d must divide T=%d", baby, T);
     const int G = T / baby;
     if (G > 8 || baby > 64) return set_err(GALA_ERR_PARAM, "tensor-core FC path needs T/baby <= 8 and baby <= 64");
+    if (fc_kf_on(c)) {
+        // key-folded weights: the baby-step rotation keys and P multiplied into the plaintexts (k_gala_kfw)
+        std::vector<const u64*> keys(64, nullptr);
+        for (int jj = 1; jj < baby; jj++) {
+            keys[jj] = key_for(c, jj);
+            if (!keys[jj]) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d (generate the baby-step keys "
+                                                          "before the tensor-core weights)", jj);
+        }
+        const u64** dk;
+        RET(upload(c, keys.data(), keys.size() * sizeof(u64*), (void**)&dk));
+        const long long total = (long long)c->dc.M * c->dc.N * KF_W_WORDS;
+        const int gr = grid_for(total, 256);
+        switch (c->dc.L) {
+            case 1: KLAUNCH(c, "k_gala_kfw", (k_gala_kfw<1><<<gr, 256, 0, c->stream>>>(c->dc, pts2, dk, c->d_pmod, baby, G, (u64*)wcan))); break;
+            case 2: KLAUNCH(c, "k_gala_kfw", (k_gala_kfw<2><<<gr, 256, 0, c->stream>>>(c->dc, pts2, dk, c->d_pmod, baby, G, (u64*)wcan))); break;
+            default: KLAUNCH(c, "k_gala_kfw", (k_gala_kfw<3><<<gr, 256, 0, c->stream>>>(c->dc, pts2, dk, c->d_pmod, baby, G, (u64*)wcan))); break;
+        }
+        release(c, (void*)dk);
+        return GALA_OK;
+    }
     const long long total = (long long)c->dc.M * c->dc.N * GTC_W_WORDS;
     KLAUNCH(c, "k_gala_wt", k_gala_wt<<<grid_for(total, 256), 256, 0, c->stream>>>(c->dc, pts2, baby, G, (u64*)wcan));
     return GALA_OK;
@@ -2267,3 +2358,14 @@ extern "C" int gala_debug_gtc_prof(unsigned long long* out, int rows)
 }
 #endif
 
+
+// k_gala_kf timeline of CTA 0 (experiment builds with -DKF_TRACE; tools/kf_trace.py)
+extern "C" int gala_debug_kf_trace(unsigned long long* out)
+{
+#ifdef KF_TRACE
+    return (int)cudaMemcpyFromSymbol(out, g_kf_trace, sizeof(unsigned long long) * 32 * 1024);
+#else
+    (void)out;
+    return -1;
+#endif
+}

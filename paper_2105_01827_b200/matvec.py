@@ -334,11 +334,12 @@ class GalaFC:
         for blk in self.blocks:    # resident encoded weights, in the layout of the chosen schedule
             blk[1] = (self.ctx.encode_gala_weights(blk[1], self.baby) if self.schedule == 2
                       else self.ctx.encode_plain(blk[1]))
-        # tensor-core baby-step sums (schedule 2): the weights' byte-convolution expansion, per block
+        self.ctx.ensure_keys(self.steps)
+        # tensor-core baby-step sums (schedule 2): the weights with the baby-step rotation keys folded in
+        # (gala_fc_tc_weights), per block -- after the keys exist
         self.wcan = [None] * len(self.blocks)
         if tensor_cores and self.schedule == 2 and self.ctx.fc_tc_supported(self.T, self.baby):
             self.wcan = [self.ctx.fc_tc_weights(blk[1], self.T, self.baby) for blk in self.blocks]
-        self.ctx.ensure_keys(self.steps)
 
     def encrypt_input(self, x) -> list:
         """Client side: one physical ciphertext per column block."""

@@ -295,7 +295,7 @@ def test_conv_kg2_kernel_sizes(tw, ksz, post):
     assert np.array_equal(tw.gpu.export_words(g_out), c_out)
 
 
-@pytest.mark.parametrize("T,nb", [(2, 17), (4, 17), (8, 17), (16, 17), (8, 48), (16, 64)])
+@pytest.mark.parametrize("T,nb", [(2, 17), (4, 17), (8, 17), (16, 17), (8, 48), (16, 64), (16, 130)])
 def test_mv_gala2_tensor_core_words(tw, T, nb):
     """Tensor-core baby-step sums (byte-convolution int8 MMA) == CUDA-core schedule 2 == oracle o_mv_gala2."""
     import torch
@@ -310,7 +310,7 @@ def test_mv_gala2_tensor_core_words(tw, T, nb):
     pts = tw.slots(T)
     pts2 = tw.gpu.encode_gala_weights(pts, b)
     wcan = tw.gpu.fc_tc_weights(pts2, T, b)
-    # one tensor-core tile per 32 inputs (every tile >= 16): 17 = one partial tile, 48 = 32 + 16, 64 = 2 x 32
+    # key-folded tiles of 128 inputs: 17 .. 64 = one partial tile, 130 = 128 + 2
     xs = [tw.encrypt(tw.slots()) for _ in range(nb)]
     rs = tw.slots(nb)
     cts = torch.stack([g for g, _ in xs])
