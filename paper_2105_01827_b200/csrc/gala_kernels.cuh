@@ -2189,21 +2189,28 @@ __global__ void k_gala_kfw(DevCtx c, const u64* __restrict__ pts2, const u64* co
     }
 }
 
-// A operand of one tile of <= 256 inputs: the identity digit blocks (Dblk [b][(L M + L)][N], b < B)
-// rearranged per position into Dq[p][half][kc][row group][8][16 B] (tcgen05 K-major core-matrix order
-// per M = 128 half; row = input, 32 bytes = streams D_0, D_1, D_2, c0; rows >= B and absent streams
-// zero): 8 KB per position, half h = inputs 128 h .. 128 h + 127 (the CTA of rank h of a pair reads it).
-// grid (M N / KF_DQ_POS), 256 threads.
+// A operand of one tile of <= 256 inputs, in rotation-orbit order.  The baby rotations are sigma_jj = sigma^jj
+// (Galois element 3^jj), and in the NTT domain sigma moves slot k to sigma(k) = auto_src(k, 3); the slots of
+// a prime fall into two orbits x_0, x_1 = sigma(x_0), ... of length N / 2.  Position x_t needs the digit
+// blocks of x_t, x_t+1, ..., x_t+63 -- a contiguous run when the blocks are stored in orbit order, so a
+// pipeline stage of KF_JS rotations is ONE bulk copy (the TMA services bulk copies ~one at a time per SM,
+// ~350 clk each: one 4 KB copy per rotation capped the gather at ~12 B/clk).  Each orbit is padded with
+// its first 64 blocks again (no wrap-around).  Layout: Dq[j][orbit][half][t][4 KB], half h = inputs
+// 128 h .. 128 h + 127 (read by the CTA of rank h of a pair), each 4 KB block the tcgen05 K-major
+// core-matrix order [kc][row group][8][16 B] of 128 rows x 32 bytes (streams D_0, D_1, D_2, c0; rows >= B
+// and absent streams zero).  orb[k] = orbit * KF_ORB(N) + t.  grid (M N / KF_DQ_POS), 256 threads.
 #define KF_ROWS 256
 #define KF_DQ_BYTES (KF_ROWS * 32)
+#define KF_ORB(N) ((N) / 2 + 64)
 #define KF_DQ_POS 8
 #define KF_DQ_STRIDE (KF_DQ_BYTES + 16)        // padded per-position stride in shared memory (bank spread)
 template <int L>
-__global__ void __launch_bounds__(256) k_gala_dq(DevCtx c, const u64* __restrict__ Dblk, int B, uint8_t* __restrict__ Dq)
+__global__ void __launch_bounds__(256) k_gala_dq(DevCtx c, const u64* __restrict__ Dblk, int B, const int* __restrict__ orb,
+                                                 uint8_t* __restrict__ Dq)
 {
     extern __shared__ __align__(16) uint8_t dq_sm[];
     constexpr int M = L + 1;
-    const int N = c.N;
+    const int N = c.N, ORB = KF_ORB(N);
     const long long p0 = (long long)blockIdx.x * KF_DQ_POS;
     const int j = (int)(p0 / N), k0 = (int)(p0 - (long long)j * N);
     const long long bw = (long long)(L * M + L) * N;
@@ -2218,9 +2225,15 @@ __global__ void __launch_bounds__(256) k_gala_dq(DevCtx c, const u64* __restrict
                 (st & 1) * 8) = v;
     }
     __syncthreads();
-    uint4* dst = (uint4*)(Dq + p0 * KF_DQ_BYTES);
-    for (int idx = threadIdx.x; idx < KF_DQ_POS * (KF_DQ_BYTES / 16); idx += blockDim.x)
-        dst[idx] = *(const uint4*)(dq_sm + (idx / (KF_DQ_BYTES / 16)) * KF_DQ_STRIDE + (idx % (KF_DQ_BYTES / 16)) * 16);
+    // position k0 + kl -> orbit slot (and its padding copy); 16-byte chunks, half-major within the block
+    for (int idx = threadIdx.x; idx < KF_DQ_POS * (KF_DQ_BYTES / 16); idx += blockDim.x) {
+        const int kl = idx / (KF_DQ_BYTES / 16), w = idx % (KF_DQ_BYTES / 16), h = w >> 8, off = (w & 255) * 16;
+        const int ot = __ldg(orb + k0 + kl), o = ot / ORB, t = ot - o * ORB;
+        const uint4 v = *(const uint4*)(dq_sm + kl * KF_DQ_STRIDE + h * 4096 + off);
+        uint8_t* base = Dq + (((long long)(j * 2 + o) * 2 + h) * ORB) * 4096 + off;
+        *(uint4*)(base + (long long)t * 4096) = v;
+        if (t < 64) *(uint4*)(base + (long long)(t + N / 2) * 4096) = v;
+    }
 }
 #define KF_DQ_SMEM (KF_DQ_POS * KF_DQ_STRIDE)
 
@@ -2241,6 +2254,18 @@ __device__ __forceinline__ uint64_t policy_evict_first()
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+// Position order of k_gala_kf: blocks of 4 consecutive slots, prime by prime and, within a prime, orbit by
+// orbit (orbit 0 = slots with bit logN - 2 clear: k in [0, N/4) and [N/2, 3N/4)), so that the digit
+// blocks in use at any time are one orbit's (34 MB for 256 inputs), not a prime's.  Returns the first
+// position j N + k of block `blk`.
+__device__ __forceinline__ long long kf_block_pos(long long blk, int N)
+{
+    const int q4 = N / 4, q8 = N / 8, q16 = N / 16;
+    const long long j = blk / q4;
+    const int r = (int)(blk - j * q4), o = r / q8, r2 = r - o * q8;
+    const int kb = (r2 / q16) * q8 + o * q16 + (r2 % q16);
+    return j * N + 4LL * kb;
 }
 // cluster helpers (CTA pairs)
 __device__ __forceinline__ uint32_t cluster_rank()
@@ -2289,8 +2314,8 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* b)
 // two 256-column accumulators (positions alternate).  Cluster c of the grid takes position blocks
 // (4 consecutive k) c, c + clusters, ... -- the whole grid sweeps the primes in order.  Per CTA:
 //   warp 0 lane 0   producer: its component's folded weights in chunks of KF_WJ rotations (4 KB, two
-//                   chunks ahead) and, per stage of KF_JS rotations, its half of each digit block
-//                   sigma_jj(p) (one 4 KB bulk copy per rotation);
+//                   chunks ahead) and, per stage of KF_JS rotations, its half of the stage's digit blocks
+//                   sigma_jj(p) -- consecutive in orbit order: one KF_JS x 4 KB bulk copy;
 //   warp 1 lane 0   rank 0: the MMA issuer -- per stage ONE wait (full[s]: both CTAs' stage complete),
 //                   KF_JS tcgen05.mma.cta_group::2.kind::i8, ONE commit multicast to both CTAs' empty[s];
 //                   rank 1: relay -- waits its own full[s] and arrives on rank 0's full[s];
@@ -2313,7 +2338,6 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* b)
 #define KF_WJ 16                         // rotations per folded-weight chunk
 #define KF_WST 4
 #define KF_WCH_BYTES (KF_WJ * 256)       // one component's weights for KF_WJ rotations
-#define KF_LAG 2                         // A stages in flight per producer warp (cp.async groups)
 #define KF_A_STAGE (KF_JS * 4096)
 #define KF_B_STAGE (KF_JS * 4096)
 #define KF_SMEM (KF_ST * (KF_A_STAGE + KF_B_STAGE) + KF_WST * KF_WCH_BYTES)
@@ -2321,31 +2345,32 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* b)
 #define KF_EPI0 6
 #ifdef KF_TRACE   // timeline of CTA 0 (tools/kf_trace.py): [event][index] clock64 stamps
 __device__ unsigned long long g_kf_trace[32][1024];
-#define KF_T(ev, idx) do { if (blockIdx.x == 0 && (idx) < 1024) g_kf_trace[ev][idx] = clock64(); } while (0)
+#ifndef KF_TRACE_CTA
+#define KF_TRACE_CTA 0
+#endif
+#define KF_T(ev, idx) do { if (blockIdx.x == KF_TRACE_CTA && (idx) < 1024) g_kf_trace[ev][idx] = clock64(); } while (0)
 #else
 #define KF_T(ev, idx) do { } while (0)
 #endif
 template <int L>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KF_THREADS, 1)
-k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, const unsigned* __restrict__ gal,
+k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, const int* __restrict__ orb,
           int baby, int G, int B, u64* __restrict__ U)
 {
     extern __shared__ __align__(128) uint8_t kf_sm[];
     constexpr int M = L + 1;
     __shared__ uint64_t full[KF_ST], empty[KF_ST], wfull[KF_WST], wempty[KF_WST], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
-    __shared__ u64 s_c40[M], s_c80[M];
-    __shared__ unsigned s_gal[64];
+    __shared__ u64 s_c80[M];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_rank();
-    const int N = c.N, logN = c.logN;
+    const int N = c.N, ORB = KF_ORB(N);
     const long long nblk = (long long)M * N / 4;
     const long long cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const int nst = (baby + KF_JS - 1) / KF_JS;          // stages per position (rotations >= baby: zero weights)
     uint8_t* sA = kf_sm;
     uint8_t* sB = kf_sm + KF_ST * KF_A_STAGE;
     uint8_t* sW = sB + KF_ST * KF_B_STAGE;
-    if (tid < 64) s_gal[tid] = gal[tid];
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)), "r"(512));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
@@ -2366,13 +2391,10 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
         }
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
-    if (tid < M) {   // 2^40, 2^80 mod q_j for the rebuild
+    if (tid < M) {   // 2^80 mod q_j for the rebuild
         const u64 q = c.mod[tid].q;
         u64 v = 1;
-        for (int i = 0; i < 80; i++) {
-            v = add_mod(v, v, q);
-            if (i == 39) s_c40[tid] = v;
-        }
+        for (int i = 0; i < 80; i++) v = add_mod(v, v, q);
         s_c80[tid] = v;
     }
     // B rows s' = 15 are never written by the expanders: zero every B stage once
@@ -2383,8 +2405,7 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base_sh;
     if (warp == 0) {
-        {   // the whole warp: lane 0 waits and arms the barriers, lanes 0 .. KF_JS - 1 issue one copy each
-            // (one thread issuing every bulk copy was the bottleneck: ~200 clk per cp.async.bulk issue)
+        if (lane == 0) {
             int sa = 0, ws = 0;
             uint32_t pha = 0, phw = 0;
             // L2: the digit blocks of the current prime are re-read 64 times (keep), the weights stream (once)
@@ -2397,15 +2418,15 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                 for (; wnext <= last && wnext < wtotal; wnext++) {
                     const long long itw = wnext / nch;
                     const int ch = (int)(wnext - itw * nch);
-                    const long long pw = (cid + (itw >> 2) * ncl) * 4 + (itw & 3);
+                    const long long pw = kf_block_pos(cid + (itw >> 2) * ncl, N) + (itw & 3);
                     mbar_wait(&wempty[ws], phw ^ 1);
 #ifdef KF_NO_W   // probe builds (tools/kf_probe.sh): role isolation, results are garbage
                     mbar_arrive(&wfull[ws]);
 #else
                     mbar_expect_tx(&wfull[ws], (uint32_t)KF_WCH_BYTES);
                     bulk_g2s_hint(sW + ws * KF_WCH_BYTES,
-                                  (const uint8_t*)(Wk + pw * KF_W_WORDS) + rank * (KF_W_BYTES / 2) + ch * KF_WCH_BYTES, KF_WCH_BYTES,
-                                  &wfull[ws], pol_stream);
+                                  (const uint8_t*)(Wk + pw * KF_W_WORDS) + rank * (KF_W_BYTES / 2) + ch * KF_WCH_BYTES,
+                                  KF_WCH_BYTES, &wfull[ws], pol_stream);
 #endif
                     if (++ws == KF_WST) {
                         ws = 0;
@@ -2414,74 +2435,24 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                 }
             };
             long long itp = 0;
-#ifndef KF_A_TMA
-            long long gsp = 0;   // stages issued (cp.async groups committed)
-#endif
             for (long long blk = cid; blk < nblk; blk += ncl) {
                 for (int pi = 0; pi < 4; pi++, itp++) {
-                    const long long p = blk * 4 + pi;
+                    const long long p = kf_block_pos(blk, N) + pi;
                     const int j = (int)(p / N), k = (int)(p - (long long)j * N);
-                    const uint8_t* base = Dq + (long long)j * N * KF_DQ_BYTES + rank * 4096;
+                    const int ot = __ldg(orb + k), o = ot / ORB, t = ot - o * ORB;
+                    // this CTA's half of the orbit run x_t, x_t+1, ... of prime j
+                    const uint8_t* run = Dq + ((((long long)(j * 2 + o) * 2 + rank) * ORB) + t) * 4096;
                     for (int s = 0; s < nst; s++) {
-#ifndef KF_A_TMA
-                        // A by LDGSTS from all 32 lanes (bulk copies are serviced ~one at a time per SM: 4 KB each
-                        // capped the gather at ~12 B/clk); a stage's copies complete KF_LAG stages later
-                        if (lane == 0) {
-                            issue_w_upto(itp * nch + (s * KF_JS) / KF_WJ + KF_WST - 2);   // 2 chunks ahead, 1 slot of slack
-                            mbar_wait(&empty[sa], pha ^ 1);
-                            KF_T(2, itp * nst + s);
-                        }
-                        __syncwarp();
-#ifndef KF_NO_A
-#pragma unroll
-                        for (int jl = 0; jl < KF_JS; jl++) {
-                            const int jj = s * KF_JS + jl;
-                            const unsigned ge = s_gal[jj];
-                            const int src = ge == 1u ? k : auto_src(k, ge, logN);
-                            const uint8_t* g = base + (long long)src * KF_DQ_BYTES + lane * 16;
-                            const uint32_t d = smem_u32(sA + sa * KF_A_STAGE + jl * 4096) + lane * 16;
-#pragma unroll
-                            for (int i = 0; i < 8; i++)
-                                asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;"
-                                             ::"r"(d + i * 512), "l"(g + i * 512), "l"(pol_keep) : "memory");
-                        }
-#endif
-                        asm volatile("cp.async.commit_group;" ::: "memory");
-                        if (gsp >= KF_LAG) {
-                            asm volatile("cp.async.wait_group %0;" ::"n"(KF_LAG) : "memory");
-                            asm volatile("fence.proxy.async.shared::cta;");
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(&full[(int)((gsp - KF_LAG) % KF_ST)]);
-                        }
-                        gsp++;
-                        if (lane == 0) KF_T(3, itp * nst + s);
-                        if (++sa == KF_ST) {
-                            sa = 0;
-                            pha ^= 1;
-                        }
-                        continue;
-#endif
-                        if (lane == 0) {
-                            issue_w_upto(itp * nch + (s * KF_JS) / KF_WJ + KF_WST - 2);   // 2 chunks ahead, 1 slot of slack
-                            mbar_wait(&empty[sa], pha ^ 1);
-                            KF_T(2, itp * nst + s);
+                        issue_w_upto(itp * nch + (s * KF_JS) / KF_WJ + KF_WST - 2);   // 2 chunks ahead, 1 slot of slack
+                        mbar_wait(&empty[sa], pha ^ 1);
+                        KF_T(2, itp * nst + s);
 #ifdef KF_NO_A
-                            mbar_arrive(&full[sa]);
+                        mbar_arrive(&full[sa]);
 #else
-                            mbar_expect_tx(&full[sa], (uint32_t)KF_A_STAGE);
+                        mbar_expect_tx(&full[sa], (uint32_t)KF_A_STAGE);
+                        bulk_g2s_hint(sA + sa * KF_A_STAGE, run + (long long)s * KF_A_STAGE, KF_A_STAGE, &full[sa], pol_keep);
 #endif
-                        }
-                        __syncwarp();
-#ifndef KF_NO_A
-                        if (lane < KF_JS) {
-                            const int jj = s * KF_JS + lane;
-                            const unsigned ge = s_gal[jj];
-                            const int src = ge == 1u ? k : auto_src(k, ge, logN);
-                            bulk_g2s_hint(sA + sa * KF_A_STAGE + lane * 4096, base + (long long)src * KF_DQ_BYTES, 4096, &full[sa],
-                                          pol_keep);
-                        }
-#endif
-                        if (lane == 0) KF_T(3, itp * nst + s);
+                        KF_T(3, itp * nst + s);
                         if (++sa == KF_ST) {
                             sa = 0;
                             pha ^= 1;
@@ -2489,13 +2460,6 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                     }
                 }
             }
-#ifndef KF_A_TMA
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            asm volatile("fence.proxy.async.shared::cta;");
-            __syncwarp();
-            for (long long g2 = gsp - KF_LAG < 0 ? 0 : gsp - KF_LAG; g2 < gsp; g2++)
-                if (lane == 0) mbar_arrive(&full[(int)(g2 % KF_ST)]);
-#endif
         }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {   // the pair's MMA issuer
@@ -2542,10 +2506,12 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
             const uint32_t peer_full0 = mapa_shared(smem_u32(&full[0]), 0);
             int sa = 0;
             uint32_t pha = 0;
+            long long gr = 0;
             for (long long blk = cid; blk < nblk; blk += ncl)
                 for (int pi = 0; pi < 4; pi++)
-                    for (int s = 0; s < nst; s++) {
+                    for (int s = 0; s < nst; s++, gr++) {
                         mbar_wait(&full[sa], pha);
+                        KF_T(4, gr);
                         mbar_arrive_remote(peer_full0 + (uint32_t)(sa * sizeof(uint64_t)));
                         if (++sa == KF_ST) {
                             sa = 0;
@@ -2566,7 +2532,9 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                 for (int s = 0; s < nst; s++, gse++) {
                     const int jw0 = (s * KF_JS) % KF_WJ;     // first rotation of the stage within its weight chunk
                     if (jw0 == 0) mbar_wait(&wfull[ws], phw);
+                    if (lane == 0) KF_T(20 + warp - 2, gse);
                     mbar_wait(&empty[sb], phb ^ 1);
+                    if (lane == 0) KF_T(16 + warp - 2, gse);
 #ifdef KF_NO_B
                     if (false) {
 #else
@@ -2592,6 +2560,7 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                     asm volatile("fence.proxy.async.shared::cta;");
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&full[sb]);
+                    if (lane == 0) KF_T(12 + warp - 2, gse);
                     if (++sb == KF_ST) {
                         sb = 0;
                         phb ^= 1;
@@ -2613,7 +2582,7 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
         const uint64_t pol_out = policy_evict_first();   // U is read back by the next kernels, not by this one
         int it = 0;
         for (long long blk = cid; blk < nblk; blk += ncl) {
-            const long long p = blk * 4;
+            const long long p = kf_block_pos(blk, N);
             const int j = (int)(p / N), k = (int)(p - (long long)j * N);
             const u64 q = c.mod[j].q, c80 = s_c80[j];
             auto rebuild = [&](const uint32_t* x) -> u64 {

@@ -141,6 +141,7 @@ struct gala_ctx {
     int num_sms = 148;
     // tensor-core FC weights: key-folded (k_gala_kf, default) or the split E / MMA pair (GALA_FC_KF=0)
     bool fc_kf = true;
+    int* d_kf_orb = nullptr;                  // NTT slot -> orbit * KF_ORB(N) + t (k_gala_dq / k_gala_kf)
 };
 
 static void prof_begin(gala_ctx* c, cudaEvent_t* a, cudaEvent_t* b)
@@ -285,7 +286,33 @@ static void debug_dump(gala_ctx* c, const char* tag, const u64* d, size_t words)
     }
 }
 // key-folded tensor-core FC weights (k_gala_kf) for this context
-static bool fc_kf_on(const gala_ctx* c) { return c->fc_kf && c->dc.L <= 3 && c->dc.N % 16 == 0; }
+static bool fc_kf_on(const gala_ctx* c) { return c->fc_kf && c->dc.L <= 3 && c->dc.N % 16 == 0 && c->dc.N >= 128; }
+
+// The rotation orbits of the NTT slots (k_gala_dq): slot k has evaluation exponent e = 2 brv(k) + 1 mod 2N;
+// the baby rotation sigma^jj multiplies it by 3^jj, so e = +-3^t splits the slots into orbit 0 (+) and
+// orbit 1 (-) of length N / 2 each, and x_t (orbit o, index t) needs the blocks x_t .. x_t+63.
+static int kf_orbit_table(gala_ctx* c, const int** out)
+{
+    if (!c->d_kf_orb) {
+        const int N = c->dc.N, logN = c->dc.logN;
+        const u64 twoN = 2 * (u64)N;
+        std::vector<int> orb(N, -1);
+        for (int o = 0; o < 2; o++) {
+            u64 e = o == 0 ? 1 : twoN - 1;
+            for (int t = 0; t < N / 2; t++) {
+                const int k = h_brv((int)((e - 1) / 2), logN);
+                orb[k] = o * KF_ORB(N) + t;
+                e = (e * 3) % twoN;
+            }
+        }
+        for (int k = 0; k < N; k++)
+            if (orb[k] < 0) return set_err(GALA_ERR_PARAM, "internal: NTT slot %d outside the rotation orbits", k);
+        CK(cudaMalloc(&c->d_kf_orb, sizeof(int) * N));
+        CK(cudaMemcpy(c->d_kf_orb, orb.data(), sizeof(int) * N, cudaMemcpyHostToDevice));
+    }
+    *out = c->d_kf_orb;
+    return GALA_OK;
+}
 
 static int moddown_groups(gala_ctx* c, u64* U, u64* Cacc, int G, u64* const* d_outs)
 {
@@ -702,6 +729,7 @@ static void free_ctx(gala_ctx* c)
     if (c->d_S) cudaFree(c->d_S);
     if (c->d_slot_pos) cudaFree(c->d_slot_pos);
     if (c->d_pmod) cudaFree(c->d_pmod);
+    if (c->d_kf_orb) cudaFree(c->d_kf_orb);
     for (Staging& st : c->stage) {
         if (st.host) cudaFreeHost(st.host);
         if (st.done) cudaEventDestroy(st.done);
@@ -1361,16 +1389,15 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     // (the E warps are load-latency bound at 7-11 warps per SM; profiles/r2_experiments.md)
     const bool fused = tc && getenv("GALA_FC_FUSED") != nullptr;
     if (kf) {
-        // key-folded tensor-core baby steps: per tile of <= 256 inputs the A blocks (k_gala_dq), then one
-        // persistent kernel; U carries the Q-side addends lifted into QP (P C), so Cacc is not formed
+        // key-folded tensor-core baby steps: per tile of <= 256 inputs the A blocks in rotation-orbit order
+        // (k_gala_dq), then one persistent kernel on CTA pairs; U carries the Q-side addends lifted into QP
+        // (P C), so Cacc is not formed
         release(c, Cacc);
         Cacc = nullptr;
+        const int* orb;
+        RET(kf_orbit_table(c, &orb));
         uint8_t* Dq;
-        RET(scratch(c, &Dq, (size_t)MN * KF_DQ_BYTES));
-        std::vector<unsigned> gal64(64, 1u);
-        for (int jj = 1; jj < baby; jj++) gal64[jj] = gal[jj];
-        unsigned* d_gal64;
-        RET(upload(c, gal64.data(), gal64.size() * sizeof(unsigned), (void**)&d_gal64));
+        RET(scratch(c, &Dq, (size_t)M * 4 * KF_ORB(N) * 4096));
         // CTA pairs (cta_group::2): an even grid of at most one CTA per SM
         const long long nblk = MN / 4;
         int grid = (int)(2 * nblk < c->num_sms ? 2 * nblk : c->num_sms) & ~1;
@@ -1381,9 +1408,9 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
             u64* Ut = U + (long long)b0 * G * 2 * M * N;
 #define GALA_KF(LL)                                                                                               \
     do {                                                                                                          \
-        KLAUNCH(c, "k_gala_dq", (k_gala_dq<LL><<<(unsigned)(MN / KF_DQ_POS), 256, KF_DQ_SMEM, c->stream>>>(c->dc, Dt, bt, Dq))); \
+        KLAUNCH(c, "k_gala_dq", (k_gala_dq<LL><<<(unsigned)(MN / KF_DQ_POS), 256, KF_DQ_SMEM, c->stream>>>(c->dc, Dt, bt, orb, Dq))); \
         KLAUNCH(c, "k_gala_kf", (k_gala_kf<LL><<<grid, KF_THREADS, KF_SMEM, c->stream>>>(c->dc, Dq, (const u64*)wcan,   \
-                                                                                     d_gal64, baby, G, bt, Ut)));  \
+                                                                                     orb, baby, G, bt, Ut)));      \
     } while (0)
             switch (L) {
                 case 1: GALA_KF(1); break;
@@ -1393,7 +1420,6 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
 #undef GALA_KF
         }
         release(c, Dq);
-        release(c, d_gal64);
         debug_dump(c, "U", U, (size_t)Z * 2 * M * N);
     } else if (fused) {
         // tensor-core baby-step sums with the E_jj key products computed in the kernel (k_gala_tcf):

@@ -12,7 +12,7 @@ flags() {
     j4s4_noB) echo "-DKF_JS=4 -DKF_ST=4 -DKF_NO_B" ;;
     susp) echo "-DKF_SUSPEND=1000000" ;; susp_onlyMMA) echo "-DKF_SUSPEND=1000000 -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
     trace_susp_onlyMMA) echo "-DKF_TRACE -DKF_SUSPEND=1000000 -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
-    trace) echo "-DKF_TRACE" ;; trace_onlyMMA) echo "-DKF_TRACE -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
+    trace) echo "-DKF_TRACE" ;; trace1) echo "-DKF_TRACE -DKF_TRACE_CTA=1" ;; trace_onlyMMA) echo "-DKF_TRACE -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
   esac
 }
 if [ "$1" = "build" ]; then

@@ -32,3 +32,12 @@ g2 = gs[:-ST]
 print(f"issuer commit(s) -> producer sees empty for s+ST: median {np.median(t[2, g2 + ST] - t[1, g2]):.0f}")
 print(f"producer issued A(s) -> issuer full ok(s): median {np.median(t[0, gs] - t[3, gs]):.0f} mean {np.mean(t[0, gs] - t[3, gs]):.0f}")
 print(f"producer issued A(s) -> issuer starts waiting: median {np.median(t[9, gs] - t[3, gs]):.0f}")
+if os.environ.get("RANK1"):
+    print(f"rank 1: producer issued A(s) -> relay sees full(s): median {np.median(t[4, gs] - t[3, gs]):.0f}")
+    print(f"rank 1: producer empty ok -> issued: median {np.median(t[3, gs] - t[2, gs]):.0f}")
+    print(f"rank 1: relay period median {np.median(np.diff(t[4, lo:hi + 1])):.0f}")
+exp_last = np.max(t[12:16, gs], axis=0)
+print(f"expanders' last arrive(s) - producer issued A(s): median {np.median(exp_last - t[3, gs]):.0f}")
+print(f"issuer full ok(s) - expanders' last arrive(s): median {np.median(t[0, gs] - exp_last):.0f}")
+print(f"expander: wfull ok -> empty ok median {np.median(t[16, gs] - t[20, gs]):.0f}; empty ok -> arrive median {np.median(t[12, gs] - t[16, gs]):.0f}")
+print(f"expander: arrive(s-1) -> wfull ok(s) median {np.median(t[20, gs[1:]] - t[12, gs[1:] - 1]):.0f}")
