@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -42,8 +43,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=96,
-                    help="independent layers (inputs) per step per GPU (tensor-core tiles of 32)")
+    ap.add_argument("--batch", type=int, default=256,
+                    help="independent layers (inputs) per step per GPU (key-folded tensor-core tiles of 256)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--baby", type=int, default=0, help="BSGS baby-step count (0: library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -137,6 +138,7 @@ def modmul_model(N, L, T, baby, schedule):
             "k_gala_e": (baby - 1) * 2 * L * M * N,
             "k_gala_mac2": G * (baby - 1) * (2 * M * N + L * N) + G * 2 * L * N,
             "k_gala_tc": G * 2 * L * N,                      # step-0 products; the sums run on the tensor cores
+            "k_gala_kf": G * 2 * M * N,                      # rebuild + REDC per group-sum word (sums: tensor cores)
             "k_digits_intt": (1 + giant) * L * h,
             "k_digits_perm": (1 + giant) * L * L * h,
             "k_ks_mac": giant * 2 * L * M * N,
@@ -178,6 +180,12 @@ def hbm_model(N, L, T, baby, B, tc):
     dig = B * (L * M + L) * N * 8                                 # identity digit blocks (of the inputs)
     keys = (baby - 1) * L * 2 * MN * 8
     x_c1 = B * L * N * 8
+    if tc == "kf":
+        # k_gala_kf: the inputs' digit blocks (reordered by k_gala_dq) and the weights + baby-step keys it
+        # folds (k_gala_kfw re-encodes them offline; the folded form is read once per 256-input tile)
+        from paper_2105_01827_b200.analytics import kf_tiles
+
+        return {"k_gala_kf": dig + (T * MN * 8 + keys) * kf_tiles(B), "k_gala_dq": dig}
     if tc:
         tiles = (B + 31) // 32                                    # one e_can / tc pair per 32 inputs
         return {"k_gala_e": dig + keys * tiles, "k_gala_tc": T * MN * 8 * tiles + x_c1}
@@ -390,7 +398,9 @@ def run_ours(args):
     dom_achieved = dom_work / (dom["ms"] / 1e3) if dom["ms"] else 0.0
     layer_achieved = layer_modmuls * layers / world / (total_ms / 1e3)
 
-    tc_on = layer.wcan[0] is not None and B >= 16 and (B <= 32 or (T >= 128 and (B % 32 == 0 or B % 32 >= 16)))
+    kf_on = "k_gala_kf" in prof            # key-folded tensor-core baby steps (the library's default form)
+    tc_on = layer.wcan[0] is not None and B >= 16 and (kf_on or B <= 32 or (T >= 128 and (B % 32 == 0 or B % 32 >= 16)))
+    tc_form = "kf" if kf_on else tc_on
     traffic = None    # DRAM bytes per launch of the dominant kernel from the committed ncu capture
     try:
         with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
@@ -417,13 +427,20 @@ def run_ours(args):
     # the reported bound is the tightest one (highest fraction)
     dom_s = dom["ms"] / 1e3 if dom["ms"] else 0.0          # profile pass = one step
     # the tensor-core pair runs once per tile of 32 inputs: per-launch figures divide by the tiles
-    launches_per_step = (B + 31) // 32 if tc_on and dom_name in ("k_gala_e", "k_gala_tc") else 1
+    from paper_2105_01827_b200.analytics import KF_MACS_PER_POSITION, kf_tiles, kf_useful_mac_frac
+
+    if kf_on and dom_name in ("k_gala_kf", "k_gala_dq"):
+        launches_per_step = kf_tiles(B)
+    elif tc_on and dom_name in ("k_gala_e", "k_gala_tc"):
+        launches_per_step = (B + 31) // 32
+    else:
+        launches_per_step = 1
     roofs = {}
     if per_kernel.get(dom_name):
         a = per_kernel[dom_name] * B / dom_s if dom_s else 0.0
         roofs["int"] = {"achieved": round(a / 1e9, 2), "peak": round(peak_modmul / 1e9, 2), "unit": "Gmodmul/s",
                         "frac": round(a / peak_modmul, 4), "peak_source": "measured live: gala_bench_modmul"}
-    hb = hbm_model(N, L, T, baby, B, tc_on).get(dom_name)
+    hb = hbm_model(N, L, T, baby, B, tc_form).get(dom_name)
     if hb:
         a = hb / dom_s if dom_s else 0.0
         roofs["hbm"] = {"achieved": round(a / 1e9, 2), "peak": hbm_peak, "unit": "GB/s", "frac": round(a / 1e9 / hbm_peak, 4),
@@ -440,6 +457,15 @@ def run_ours(args):
                            "frac": round(a / int8_peak, 4), "useful_mac_frac": 0.375,
                            "useful_frac_of_peak": round(0.375 * a / int8_peak, 4),
                            "peak_source": "2x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)"}
+    if dom_name == "k_gala_kf":
+        macs = (L + 1) * N * KF_MACS_PER_POSITION * launches_per_step   # issued int8 MACs (CTA-pair MMAs)
+        int8_peak = 2 * peaks.get("bf16_tflops", 1639.9) * 1e12
+        a = 2 * macs / dom_s if dom_s else 0.0
+        uf = kf_useful_mac_frac(B, L, T // baby, baby)
+        roofs["tensor"] = {"achieved": round(a / 1e12, 2), "peak": round(int8_peak / 1e12, 1), "unit": "TOP/s",
+                           "frac": round(a / int8_peak, 4), "useful_mac_frac": round(uf, 4),
+                           "useful_frac_of_peak": round(uf * a / int8_peak, 4),
+                           "peak_source": "2x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)"}
     bound = max(roofs, key=lambda r: roofs[r]["frac"]) if roofs else "int"
     br = roofs.get(bound, {"achieved": 0.0, "peak": 0.0, "unit": "", "frac": 0.0})
     # the whole step against SURVEY.md 8(d)'s formula with the work the schedule executes
@@ -447,7 +473,7 @@ def run_ours(args):
     # bytes at HBM): the slowest roof over the measured step time
     from paper_2105_01827_b200.analytics import executed_roofline, fc_executed_work
 
-    work = fc_executed_work(N, L, T, baby, B, tc_on)
+    work = fc_executed_work(N, L, T, baby, B, tc_form)
     lr = executed_roofline(work, work["bytes"], ms_per_step / 1e3, peak_modmul,
                            2 * peaks.get("bf16_tflops", 1639.9) * 1e12, hbm_peak * 1e9)
     layer_roof = {"bound": lr["bound"], "frac": lr["frac"], "roofline_us_per_step": lr["roofline_us"],
@@ -471,7 +497,8 @@ def run_ours(args):
         "data": "synthetic (seeded int8 weights mapped to Z_p, uniform Z_p inputs)",
         "config": {"workload": WORKLOAD, "layer": "GALA FC 1024x4096 (2 paired MvTasks of 512x4096, T=512)",
                    "gala_schedule": layer.schedule,
-                   "baby_step_sums": "tcgen05 int8 MMA" if tc_on else "CUDA cores",
+                   "baby_step_sums": ("tcgen05 int8 MMA, key-folded weights, CTA pairs (k_gala_kf)" if kf_on else
+                                      "tcgen05 int8 MMA (k_gala_e_can + k_gala_tc)" if tc_on else "CUDA cores"),
                    "N": N, "L": L, "special_primes": 1, "p": P, "bsgs_baby": baby, "batch_per_gpu": B,
                    "parallelism": f"replicas x{world} (independent inputs per GPU)",
                    "l2": "flushed (256 MB write) before every timed step"},
@@ -629,9 +656,8 @@ def run_reference(args):
     tasks = [MvTask(N_IN, N_OUT // 2, w[:N_OUT // 2], params), MvTask(N_IN, N_OUT // 2, w[N_OUT // 2:], params)]
     pts = np.concatenate([gala_weight_slots(tasks[0]), gala_weight_slots(tasks[1])], axis=1).astype(np.uint32)
     T = pts.shape[0]
-    from oracle.bfv import bsgs_baby
-
-    baby = bsgs_baby(T)
+    # the GPU arm's baby-step split (Context.gala2_baby: b = 2^round(log2 sqrt(7 T)), 64 at T = 512)
+    baby = 1 << int(round(math.log2(math.sqrt(7 * T))))
     G = T // baby
     for s in sorted({j for j in range(1, baby)} | {g * baby for g in range(1, G)}):
         a, e = sampling.rotation_key_randomness(np.random.default_rng([seed, 1, s]), bfv)
