@@ -459,13 +459,18 @@ def run_ours(args):
                            "peak_source": "2x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)"}
     if dom_name == "k_gala_kf":
         macs = (L + 1) * N * KF_MACS_PER_POSITION * launches_per_step   # issued int8 MACs (CTA-pair MMAs)
-        int8_peak = 2 * peaks.get("bf16_tflops", 1639.9) * 1e12
+        # the measured tcgen05 kind::i8 issue rate (tools/mma_bench.cu, profiles/r2_mma_bench.txt: 8192 MACs
+        # per clock per SM) at the maximum SM clock -- higher than 2x the cuBLAS bf16 figure, so the stricter roof
+        int8_peak = max(2 * peaks.get("bf16_tflops", 1639.9) * 1e12,
+                        2 * 8192 * torch.cuda.get_device_properties(dev).multi_processor_count
+                        * peaks.get("sm_max_mhz", 1965.0) * 1e6)
         a = 2 * macs / dom_s if dom_s else 0.0
         uf = kf_useful_mac_frac(B, L, T // baby, baby)
         roofs["tensor"] = {"achieved": round(a / 1e12, 2), "peak": round(int8_peak / 1e12, 1), "unit": "TOP/s",
                            "frac": round(a / int8_peak, 4), "useful_mac_frac": round(uf, 4),
                            "useful_frac_of_peak": round(uf * a / int8_peak, 4),
-                           "peak_source": "2x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)"}
+                           "peak_source": "tcgen05 kind::i8 issue rate measured by tools/mma_bench.cu (8192 MAC/clk/SM) "
+                                          "x SMs x MEASURED_PEAKS.json sm_max_mhz"}
     bound = max(roofs, key=lambda r: roofs[r]["frac"]) if roofs else "int"
     br = roofs.get(bound, {"achieved": 0.0, "peak": 0.0, "unit": "", "frac": 0.0})
     # the whole step against SURVEY.md 8(d)'s formula with the work the schedule executes

@@ -2326,17 +2326,24 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* b)
 //                   release (tempty, counted on rank 0) comes from both CTAs' epilogues.
 // Why this shape (measured, profiles/r2_experiments.md): a thread cannot keep the tensor pipe fed
 // through fine-grained mbarrier waits and every role pays a fixed cost per stage (tools/mma_bench.cu,
-// tools/kf_trace.py), so stages carry several MMAs; the pair halves each SM's Toeplitz expansion and
+// tools/kf_trace.py), so stages carry several MMAs; the TMA services one 1-D bulk copy per SM in a
+// roughly fixed time whatever its size (tools/bulk_bench.cu: 4 KB ~6-8 B/clk, 32 KB ~50 B/clk), so a
+// stage's digit blocks move as ONE 32 KB copy (8 rotations: 5.2 -> 3.0 ms per 256-input tile against
+// 4-rotation stages; separate, deeper A and B rings measured slower); the pair halves each SM's Toeplitz expansion and
 // shared-memory bytes per MMA (A 4 KB + B 4 KB), leaving room for KF_ST stages and for two accumulators
 // (the epilogue of position p overlaps the MMAs of p + 1).  (14 warps: <= 4 per SM sub-partition.)
 #ifndef KF_JS
-#define KF_JS 4                          // rotations per stage
+#define KF_JS 8                          // rotations per stage: one 32 KB A copy (tools/bulk_bench.cu)
 #endif
 #ifndef KF_ST
-#define KF_ST 6                          // ring depth
+#define KF_ST 3                          // ring depth
 #endif
+#ifndef KF_WJ
 #define KF_WJ 16                         // rotations per folded-weight chunk
+#endif
+#ifndef KF_WST
 #define KF_WST 4
+#endif
 #define KF_WCH_BYTES (KF_WJ * 256)       // one component's weights for KF_WJ rotations
 #define KF_A_STAGE (KF_JS * 4096)
 #define KF_B_STAGE (KF_JS * 4096)

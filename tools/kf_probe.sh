@@ -6,6 +6,13 @@ flags() {
   case $1 in
     base) echo "" ;; noA) echo "-DKF_NO_A" ;; noW) echo "-DKF_NO_W" ;; noB) echo "-DKF_NO_B" ;; noE) echo "-DKF_NO_EPI" ;;
     onlyMMA) echo "-DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;; noAnoB) echo "-DKF_NO_A -DKF_NO_B" ;;
+    j8s3) echo "-DKF_JS=8 -DKF_ST=3" ;; j8s3w32) echo "-DKF_JS=8 -DKF_ST=3 -DKF_WJ=32 -DKF_WST=2" ;;
+    j8s3trace) echo "-DKF_JS=8 -DKF_ST=3 -DKF_TRACE" ;; j8s3only) echo "-DKF_JS=8 -DKF_ST=3 -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
+    j8s3noA) echo "-DKF_JS=8 -DKF_ST=3 -DKF_NO_A" ;; j8s3noB) echo "-DKF_JS=8 -DKF_ST=3 -DKF_NO_B" ;; j8s3noE) echo "-DKF_JS=8 -DKF_ST=3 -DKF_NO_EPI" ;;
+    a4b2) echo "" ;; a3b3) echo "-DKF_AST=3 -DKF_BST=3" ;; a5b1) echo "-DKF_AST=5 -DKF_BST=1" ;;
+    j4a8b4) echo "-DKF_JS=4 -DKF_AST=8 -DKF_BST=4" ;; j4a10b2) echo "-DKF_JS=4 -DKF_AST=10 -DKF_BST=2" ;;
+    a4b2only) echo "-DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;; a4b2trace) echo "-DKF_TRACE" ;;
+    j16s1) echo "-DKF_JS=16 -DKF_ST=1" ;; j8s2w32) echo "-DKF_JS=8 -DKF_ST=2 -DKF_WJ=32 -DKF_WST=2" ;;
     j4s4) echo "-DKF_JS=4 -DKF_ST=4" ;; j8s2) echo "-DKF_JS=8 -DKF_ST=2" ;;
     j4s4_onlyMMA) echo "-DKF_JS=4 -DKF_ST=4 -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
     j8s2_onlyMMA) echo "-DKF_JS=8 -DKF_ST=2 -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
