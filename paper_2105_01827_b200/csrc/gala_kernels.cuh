@@ -2339,16 +2339,23 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* b)
 #define KF_ST 3                          // ring depth
 #endif
 #ifndef KF_WJ
-#define KF_WJ 16                         // rotations per folded-weight chunk
+#define KF_WJ 32                         // rotations per folded-weight chunk (8 KB per component)
 #endif
 #ifndef KF_WST
-#define KF_WST 4
+#define KF_WST 2
 #endif
 #define KF_WCH_BYTES (KF_WJ * 256)       // one component's weights for KF_WJ rotations
 #define KF_A_STAGE (KF_JS * 4096)
 #define KF_B_STAGE (KF_JS * 4096)
 #define KF_SMEM (KF_ST * (KF_A_STAGE + KF_B_STAGE) + KF_WST * KF_WCH_BYTES)
+#ifndef KF_NO_WSPLIT   // the folded-weight copies from a 15th warp: a second TMA-issuing thread (2.95 vs 3.05 ms)
+#define KF_WSPLIT
+#endif
+#ifdef KF_WSPLIT
+#define KF_THREADS (15 * 32)
+#else
 #define KF_THREADS (14 * 32)
+#endif
 #define KF_EPI0 6
 #ifdef KF_TRACE   // timeline of CTA 0 (tools/kf_trace.py): [event][index] clock64 stamps
 __device__ unsigned long long g_kf_trace[32][1024];
@@ -2411,7 +2418,7 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
     cluster_sync_all();                  // barriers initialised in both CTAs before any remote arrive
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base_sh;
-    if (warp == 0) {
+    if (warp == 0 || warp == 14) {
         if (lane == 0) {
             int sa = 0, ws = 0;
             uint32_t pha = 0, phw = 0;
@@ -2441,6 +2448,9 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                     }
                 }
             };
+            if (warp == 14) {   // KF_WSPLIT: every weight chunk, in order, as the ring frees
+                issue_w_upto(wtotal - 1);
+            } else {
             long long itp = 0;
             for (long long blk = cid; blk < nblk; blk += ncl) {
                 for (int pi = 0; pi < 4; pi++, itp++) {
@@ -2450,7 +2460,9 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                     // this CTA's half of the orbit run x_t, x_t+1, ... of prime j
                     const uint8_t* run = Dq + ((((long long)(j * 2 + o) * 2 + rank) * ORB) + t) * 4096;
                     for (int s = 0; s < nst; s++) {
+#ifndef KF_WSPLIT
                         issue_w_upto(itp * nch + (s * KF_JS) / KF_WJ + KF_WST - 2);   // 2 chunks ahead, 1 slot of slack
+#endif
                         mbar_wait(&empty[sa], pha ^ 1);
                         KF_T(2, itp * nst + s);
 #ifdef KF_NO_A
@@ -2466,6 +2478,7 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                         }
                     }
                 }
+            }
             }
         }
     } else if (warp == 1) {

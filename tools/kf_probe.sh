@@ -12,6 +12,8 @@ flags() {
     a4b2) echo "" ;; a3b3) echo "-DKF_AST=3 -DKF_BST=3" ;; a5b1) echo "-DKF_AST=5 -DKF_BST=1" ;;
     j4a8b4) echo "-DKF_JS=4 -DKF_AST=8 -DKF_BST=4" ;; j4a10b2) echo "-DKF_JS=4 -DKF_AST=10 -DKF_BST=2" ;;
     a4b2only) echo "-DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;; a4b2trace) echo "-DKF_TRACE" ;;
+    wsplit) echo "-DKF_WSPLIT" ;; wsplit_a4) echo "-DKF_WSPLIT -DKF_JS=8 -DKF_ST=3 -DKF_WST=4" ;; wsplit_w32) echo "-DKF_WSPLIT -DKF_WJ=32 -DKF_WST=2" ;;
+    st4w2) echo "-DKF_ST=4 -DKF_WJ=8 -DKF_WST=2" ;; js16st1) echo "-DKF_JS=16 -DKF_ST=1 -DKF_WJ=16 -DKF_WST=4" ;;
     j16s1) echo "-DKF_JS=16 -DKF_ST=1" ;; j8s2w32) echo "-DKF_JS=8 -DKF_ST=2 -DKF_WJ=32 -DKF_WST=2" ;;
     j4s4) echo "-DKF_JS=4 -DKF_ST=4" ;; j8s2) echo "-DKF_JS=8 -DKF_ST=2" ;;
     j4s4_onlyMMA) echo "-DKF_JS=4 -DKF_ST=4 -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
