@@ -405,10 +405,10 @@ def run_ours(args):
     try:
         with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             tj = json.load(f)
-        # per launch: a capture at batch 32 (one full tile) stands for every batch of full tiles
-        tb = int(tj.get("batch", 0))
-        if dom_name in tj and (tb == B or (tb == 32 and B % 32 == 0 and tc_on)):
-            traffic = int(tj[dom_name])
+        # per launch: a capture of one full tile stands for every batch of full tiles
+        ent = tj.get("kernels", {}).get(dom_name)
+        if ent and B % int(ent["tile"]) == 0:
+            traffic = int(ent["bytes"])
     except Exception:
         pass
     peaks = {}

@@ -236,6 +236,12 @@ int gala_ct_import(gala_ctx *ctx, const uint64_t *coef_dev, uint64_t *ct_dev, in
 /* canonical plaintext-operand words (coefficients of the centred lift) */
 int gala_pt_export(gala_ctx *ctx, const uint64_t *pt_dev, uint64_t *coef_dev, int count);
 
+/* Tensor-core FC policy: the smallest tree (T terms) that runs the baby-step sums on the tensor cores
+ * (default 128: a key-folded tile's cost per QP position does not shrink with T; smaller trees use the
+ * CUDA cores).  Words are identical either way; parity tests lower it to exercise the tiles on small
+ * rings.  (No reference counterpart: a scheduling knob of this backend.) */
+int gala_set_fc_tc_min_terms(gala_ctx *ctx, int min_terms);
+
 /* kernel launches issued by this process so far (for bench accounting) */
 uint64_t gala_launch_count(void);
 

@@ -79,6 +79,7 @@ SIGNATURES = [
     ("gala_ct_export", i32, [vp, vp, vp, i32]),
     ("gala_ct_import", i32, [vp, vp, vp, i32]),
     ("gala_pt_export", i32, [vp, vp, vp, i32]),
+    ("gala_set_fc_tc_min_terms", i32, [vp, i32]),
     ("gala_launch_count", ctypes.c_uint64, []),
     ("gala_profile_enable", i32, [vp, i32]),
     ("gala_profile_json", i32, [vp, ctypes.c_char_p, szt]),

@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes
 import json
+import os
 import math
 import threading
 from dataclasses import dataclass, fields, replace
@@ -197,6 +198,7 @@ class Context:
                                                 self.bfv.psi_p, params.device))
         self._h = h
         self._enc_counter = 0
+        self._fc_tc_min_T = 128
         self.seed = params.seed
         self.own_key_steps = set()    # rotation keys drawn from this context's own randomness source
         if secret is None:
@@ -515,7 +517,21 @@ class Context:
         return outs, masked
 
     def fc_tc_supported(self, T: int, baby: int) -> bool:
-        return T % baby == 0 and T // baby <= 8 and baby <= 64 and self.N % 32 == 0
+        ok = T % baby == 0 and T // baby <= 8 and baby <= 64 and self.N % 32 == 0
+        if self.fc_key_folded():
+            # the key-folded tile pays only for T >= 128 (gala_mv_gala2_batch_tc); smaller trees stay on the CUDA cores
+            ok = ok and T >= self._fc_tc_min_T
+        return ok
+
+    def set_fc_tc_min_terms(self, min_terms: int) -> None:
+        """Smallest tree that runs its baby-step sums on the tensor cores (default 128; words identical)."""
+        self.call("gala_set_fc_tc_min_terms", int(min_terms))
+        self._fc_tc_min_T = int(min_terms)
+
+    def fc_key_folded(self) -> bool:
+        """True when the library runs the tensor-core FC baby steps key-folded (k_gala_kf, the default;
+        GALA_FC_KF=0 selects the split k_gala_e_can / k_gala_tc pair)."""
+        return os.environ.get("GALA_FC_KF", "1") != "0" and self.L <= 3
 
     def fc_tc_weights(self, pts2, T: int, baby: int):
         """Byte-convolution expansion of schedule-2 weights for the tensor-core baby-step sums."""

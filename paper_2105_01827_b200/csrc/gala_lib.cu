@@ -141,6 +141,7 @@ struct gala_ctx {
     int num_sms = 148;
     // tensor-core FC weights: key-folded (k_gala_kf, default) or the split E / MMA pair (GALA_FC_KF=0)
     bool fc_kf = true;
+    int fc_tc_min_T = 128;                    // smallest T on the key-folded tensor-core tiles (gala_set_fc_tc_min_terms)
     int* d_kf_orb = nullptr;                  // NTT slot -> orbit * KF_ORB(N) + t (k_gala_dq / k_gala_kf)
 };
 
@@ -1381,7 +1382,11 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     // large enough for a tile's fixed per-position cost (K = 64 rotations x 8 bytes whatever T is) to pay:
     // T >= 128 (config 2: 17.5k -> 19.3k layers/s at 96 inputs; config 1, T = 8, stays on the CUDA cores,
     // 0.0016 vs 0.0066 ms per layer at 1024 inputs); the rest of the layer stays batched over all B
-    const bool kf = wcan != nullptr && fc_kf_on(c) && B >= 16 && G <= 8 && baby <= 64 && getenv("GALA_FC_NO_TC") == nullptr;
+    // key-folded tiles (k_gala_kf) for layers large enough for a tile's fixed per-position cost (64 rotations x
+    // 8 groups of MMA columns whatever T is): T >= 128 (config 2); config 1 (T = 8) stays on the CUDA cores,
+    // 1.6 vs 2.2 us per layer at 1024 inputs
+    const bool kf = wcan != nullptr && fc_kf_on(c) && B >= 16 && T >= c->fc_tc_min_T && G <= 8 && baby <= 64 &&
+                    getenv("GALA_FC_NO_TC") == nullptr;
     const bool tc = !kf && wcan != nullptr && !fc_kf_on(c) && B >= 16 &&
                     (B <= 32 || (T >= 128 && (B % 32 == 0 || B % 32 >= 16))) &&
                     G <= 8 && baby <= 64 && (N % 32) == 0 && getenv("GALA_FC_NO_TC") == nullptr;
@@ -2311,6 +2316,13 @@ int gala_pt_export(gala_ctx* c, const uint64_t* pt, uint64_t* coef, int count)
 {
     const int N = c->dc.N, L = c->dc.L;
     return launch_inv<true>(c, pt, coef, count * L, pm_make(L, L, 0, 0, (long long)L * N, (long long)L * N));
+}
+
+int gala_set_fc_tc_min_terms(gala_ctx* c, int min_terms)
+{
+    if (min_terms < 1) return set_err(GALA_ERR_PARAM, "min_terms must be >= 1");
+    c->fc_tc_min_T = min_terms;
+    return GALA_OK;
 }
 
 int gala_profile_enable(gala_ctx* c, int on)

@@ -36,6 +36,7 @@ def test_fc_tensor_core_writes_stay_in_bounds(B):
 
     tw = Twin(256, 3, seed=9)
     g = tw.gpu
+    g.set_fc_tc_min_terms(1)          # the key-folded tile at this small T (production: T >= 128)
     T = 16
     baby, steps = g.bsgs_steps(T)
     tw.keys_for(steps)

@@ -304,6 +304,16 @@ def test_mv_gala2_tensor_core_words(tw, T, nb):
     if T > n or tw.N % 32:
         pytest.skip("shape")
     b, steps = tw.gpu.bsgs_steps(T)
+    tw.gpu.set_fc_tc_min_terms(1)          # tiles at every T (production: T >= 128)
+    try:
+        _tensor_core_words(tw, T, nb, b, steps)
+    finally:
+        tw.gpu.set_fc_tc_min_terms(128)
+
+
+def _tensor_core_words(tw, T, nb, b, steps):
+    import torch
+
     if not tw.gpu.fc_tc_supported(T, b):
         pytest.skip("tensor-core path not applicable")
     tw.keys_for(steps)
@@ -386,6 +396,18 @@ def test_mv_gala2_stream_host_words(tw, tc):
     n = tw.bfv.n
     T = min(8, n)
     b, steps = tw.gpu.bsgs_steps(T)
+    tw.gpu.set_fc_tc_min_terms(1 if tc else 128)      # the key-folded tile at this small T (production: T >= 128)
+    try:
+        _stream_words(tw, tc, T, b, steps)
+    finally:
+        tw.gpu.set_fc_tc_min_terms(128)
+
+
+def _stream_words(tw, tc, T, b, steps):
+    import ctypes
+
+    from paper_2105_01827_b200 import _lib
+
     if tc and (tw.N % 32 or not tw.gpu.fc_tc_supported(T, b)):
         pytest.skip("tensor-core path not applicable")
     tw.keys_for(steps)

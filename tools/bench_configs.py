@@ -84,7 +84,10 @@ def fc_exec(layer, ctx, B, ms):
     if layer.schedule != 2:
         return None
     T, b = layer.T, layer.baby
-    tc = layer.wcan[0] is not None and B >= 16 and (B <= 32 or (T >= 128 and (B % 32 == 0 or B % 32 >= 16)))
+    if ctx.fc_key_folded():
+        tc = "kf" if layer.wcan[0] is not None and B >= 16 and T >= 128 else False
+    else:
+        tc = layer.wcan[0] is not None and B >= 16 and (B <= 32 or (T >= 128 and (B % 32 == 0 or B % 32 >= 16)))
     w = fc_executed_work(ctx.N, ctx.L, T, b, B, tc)
     return exec_roof(w, w["bytes"], ms, ctx)
 
@@ -211,7 +214,7 @@ if __name__ == "__main__":
         if w == "cfg1":
             r = fc("cfg1", 2048, 1, 16, 2048, int(os.environ.get("CFG1_BATCH", "1024")))
         elif w == "cfg2":
-            r = fc("cfg2", 4096, 3, 1024, 4096, int(os.environ.get("CFG2_BATCH", "96")))
+            r = fc("cfg2", 4096, 3, 1024, 4096, int(os.environ.get("CFG2_BATCH", "256")))
         elif w == "cfg3":
             r = conv("cfg3", 2048, 1, 16, 16, 64, 64, 3, B=int(os.environ.get("CFG3_BATCH", "16")))
         elif w == "cfg4":
