@@ -2366,6 +2366,30 @@ __device__ unsigned long long g_kf_trace[32][1024];
 #else
 #define KF_T(ev, idx) do { } while (0)
 #endif
+// Experiment (-DKF_FLAG, off): stage hand-off to the MMA issuer through shared-memory counters instead of
+// mbarriers.  A thread that waits on an mbarrier after issuing tcgen05.mma stalls until its MMAs drain
+// (tools/mma2_bench.cu: a commit/wait ring runs 230 clk per M128 N256 K32 MMA per SM instead of 128; with
+// the waits done by a helper thread that publishes counters, 144), but in k_gala_kf the counters measured
+// slower (3.10 vs 2.95 ms per tile; the MMA-only probe 2.44 vs 2.48): the issuer's waits are not what
+// paces this kernel (profiles/r2_experiments.md).
+#if defined(KF_FLAG) && !defined(KF_WSPLIT)
+#error "KF_FLAG runs its helper in lane 1 of the weight-producer warp (KF_WSPLIT)"
+#endif
+__device__ __forceinline__ void kf_publish(uint32_t* p, uint32_t v)
+{
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void kf_await(const uint32_t* p, uint32_t v)
+{
+    uint32_t x;
+    do {
+#ifdef KF_FLAG_VOLATILE
+        asm volatile("ld.volatile.shared::cta.u32 %0, [%1];" : "=r"(x) : "r"(smem_u32(p)) : "memory");
+#else
+        asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(x) : "r"(smem_u32(p)) : "memory");
+#endif
+    } while ((int)(x - v) < 0);
+}
 template <int L>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KF_THREADS, 1)
 k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, const int* __restrict__ orb,
@@ -2375,6 +2399,7 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
     constexpr int M = L + 1;
     __shared__ uint64_t full[KF_ST], empty[KF_ST], wfull[KF_WST], wempty[KF_WST], tfull[2], tempty[2];
     __shared__ uint32_t tmem_base_sh;
+    __shared__ uint32_t s_ready, s_tready;   // KF_FLAG: stages / accumulators published to the issuer
     __shared__ u64 s_c80[M];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t rank = cluster_rank();
@@ -2403,6 +2428,8 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 16);       // rank 0's: 8 epilogue warps of each CTA
         }
+        s_ready = 0;
+        s_tready = 0;
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     if (tid < M) {   // 2^80 mod q_j for the rebuild
@@ -2418,6 +2445,29 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
     cluster_sync_all();                  // barriers initialised in both CTAs before any remote arrive
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base_sh;
+#ifdef KF_FLAG
+    if (warp == KF_THREADS / 32 - 1 && lane == 1 && rank == 0) {
+        // the issuer's hand-off helper: in the issuer's order, each accumulator's release (tempty) and each
+        // stage's completion (full: both CTAs' copies and expanders) become counters the issuer polls
+        int sa = 0, it = 0;
+        uint32_t pha = 0;
+        uint32_t gs = 0;
+        for (long long blk = cid; blk < nblk; blk += ncl) {
+            for (int pi = 0; pi < 4; pi++, it++) {
+                mbar_wait_cluster(&tempty[it & 1], (uint32_t)(((it >> 1) & 1) ^ 1));
+                kf_publish(&s_tready, (uint32_t)(it + 1));
+                for (int s = 0; s < nst; s++) {
+                    mbar_wait_cluster(&full[sa], pha);
+                    kf_publish(&s_ready, ++gs);
+                    if (++sa == KF_ST) {
+                        sa = 0;
+                        pha ^= 1;
+                    }
+                }
+            }
+        }
+    } else
+#endif
     if (warp == 0 || warp == 14) {
         if (lane == 0) {
             int sa = 0, ws = 0;
@@ -2491,13 +2541,21 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
             for (long long blk = cid; blk < nblk; blk += ncl) {
                 for (int pi = 0; pi < 4; pi++, it++) {
                     const int acc = it & 1;
+#ifdef KF_FLAG
+                    kf_await(&s_tready, (uint32_t)(it + 1));
+#else
                     mbar_wait_cluster(&tempty[acc], (uint32_t)(((it >> 1) & 1) ^ 1));
+#endif
                     KF_T(6, it);
                     asm volatile("tcgen05.fence::after_thread_sync;");
                     const uint32_t d = tmem + (uint32_t)(acc * 256);
                     for (int s = 0; s < nst; s++, gs++) {
                         KF_T(9, gs);
+#ifdef KF_FLAG
+                        kf_await(&s_ready, (uint32_t)(gs + 1));
+#else
                         mbar_wait_cluster(&full[sa], pha);
+#endif
                         KF_T(0, gs);
                         asm volatile("tcgen05.fence::after_thread_sync;");
                         const uint32_t a0 = smem_u32(sA + sa * KF_A_STAGE), b0 = smem_u32(sB + sa * KF_B_STAGE);

@@ -14,6 +14,9 @@ flags() {
     a4b2only) echo "-DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;; a4b2trace) echo "-DKF_TRACE" ;;
     wsplit) echo "-DKF_WSPLIT" ;; wsplit_a4) echo "-DKF_WSPLIT -DKF_JS=8 -DKF_ST=3 -DKF_WST=4" ;; wsplit_w32) echo "-DKF_WSPLIT -DKF_WJ=32 -DKF_WST=2" ;;
     st4w2) echo "-DKF_ST=4 -DKF_WJ=8 -DKF_WST=2" ;; js16st1) echo "-DKF_JS=16 -DKF_ST=1 -DKF_WJ=16 -DKF_WST=4" ;;
+    flag) echo "" ;; flagvol) echo "-DKF_FLAG_VOLATILE" ;; noflag) echo "-DKF_NO_FLAG" ;;
+    flagonly) echo "-DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;; flagtrace) echo "-DKF_TRACE" ;;
+    flagonlytrace) echo "-DKF_TRACE -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;; noflagonlytrace) echo "-DKF_NO_FLAG -DKF_TRACE -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
     j16s1) echo "-DKF_JS=16 -DKF_ST=1" ;; j8s2w32) echo "-DKF_JS=8 -DKF_ST=2 -DKF_WJ=32 -DKF_WST=2" ;;
     j4s4) echo "-DKF_JS=4 -DKF_ST=4" ;; j8s2) echo "-DKF_JS=8 -DKF_ST=2" ;;
     j4s4_onlyMMA) echo "-DKF_JS=4 -DKF_ST=4 -DKF_NO_A -DKF_NO_W -DKF_NO_B -DKF_NO_EPI" ;;
