@@ -192,6 +192,12 @@ def hbm_model(N, L, T, baby, B, tc):
     return {"k_gala_e": dig + keys, "k_gala_mac2": T * MN * 8 + x_c1}
 
 
+def layer_config(N, L, T, baby, schedule):
+    """The headline layer (BASELINE.json configs[1]) -- the same dict in both arms' lines."""
+    return {"workload": WORKLOAD, "layer": "GALA FC 1024x4096 (2 paired MvTasks of 512x4096, T=512)",
+            "N": N, "L": L, "special_primes": 1, "p": P, "T": T, "bsgs_baby": baby, "gala_schedule": schedule}
+
+
 def run_ours(args):
     import torch
 
@@ -500,13 +506,14 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "u64 (RNS residues mod 60-bit primes)",
         "data": "synthetic (seeded int8 weights mapped to Z_p, uniform Z_p inputs)",
-        "config": {"workload": WORKLOAD, "layer": "GALA FC 1024x4096 (2 paired MvTasks of 512x4096, T=512)",
-                   "gala_schedule": layer.schedule,
-                   "baby_step_sums": ("tcgen05 int8 MMA, key-folded weights, CTA pairs (k_gala_kf)" if kf_on else
-                                      "tcgen05 int8 MMA (k_gala_e_can + k_gala_tc)" if tc_on else "CUDA cores"),
-                   "N": N, "L": L, "special_primes": 1, "p": P, "bsgs_baby": baby, "batch_per_gpu": B,
-                   "parallelism": f"replicas x{world} (independent inputs per GPU)",
-                   "l2": "flushed (256 MB write) before every timed step"},
+        # the layer both arms compute (identical dict in the reference arm's line); how this arm runs it
+        # (batching, tensor cores, L2 policy) is under "run"
+        "config": layer_config(N, L, T, baby, layer.schedule),
+        "run": {"batch_per_gpu": B,
+                "baby_step_sums": ("tcgen05 int8 MMA, key-folded weights, CTA pairs (k_gala_kf)" if kf_on else
+                                   "tcgen05 int8 MMA (k_gala_e_can + k_gala_tc)" if tc_on else "CUDA cores"),
+                "parallelism": f"replicas x{world} (independent inputs per GPU)",
+                "l2": "flushed (256 MB write) before every timed step"},
         "rotations_per_s": round(value * (T - 1), 1),
         "ks_probe": {"rotations_per_s": round(ks_rot_per_s, 1), "batch": B, "steps_per_input": len(ks_steps),
                      "ms": round(ks_ms_med, 4),
@@ -689,7 +696,8 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64 (RNS residues mod 60-bit primes)",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD, "N": bfv.N, "L": bfv.L, "bsgs_baby": baby, "batch_per_step": 1},
+        "config": layer_config(bfv.N, bfv.L, T, baby, schedule),
+        "run": {"layers_per_step": 1, "threads": num_threads()},
         "cpu_baseline": {"value": round(value, 4), "unit": "layers/s", "cores": num_threads(), "kind": "port",
                          "sample": "1 layer per step: oracle/bfv_oracle.c (same algorithm), OpenMP, all host threads",
                          "cpu_model": cpu_model(), "host_cpus": os.cpu_count()},
