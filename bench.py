@@ -429,6 +429,13 @@ def run_ours(args):
     ct_bytes = 2 * L * N * 8
     layer_bytes = pt_bytes / B + key_bytes / B + 3 * ct_bytes + N * 4   # weights/keys amortised over the batch
 
+    # int8 tensor roof: the measured tcgen05 kind::i8 issue rate (tools/mma_bench.cu, profiles/r2_mma_bench.txt:
+    # 8192 MACs per clock per SM) at the maximum SM clock -- higher than 2x the cuBLAS bf16 figure, so the
+    # stricter roof
+    from paper_2105_01827_b200.analytics import tensor_i8_peak_ops
+
+    i8_peak = tensor_i8_peak_ops(torch.cuda.get_device_properties(dev).multi_processor_count,
+                                 peaks.get("sm_max_mhz", 1965.0), peaks.get("bf16_tflops", 1639.9))
     # dominant kernel against every roof it has (integer multiplies, HBM bytes, int8 tensor MACs);
     # the reported bound is the tightest one (highest fraction)
     dom_s = dom["ms"] / 1e3 if dom["ms"] else 0.0          # profile pass = one step
@@ -454,7 +461,7 @@ def run_ours(args):
                         "launches_per_step": launches_per_step, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     if dom_name == "k_gala_tc":
         macs = (L + 1) * N * 128 * 128 * 512 * launches_per_step  # issued int8 MACs (byte-convolution tiles)
-        int8_peak = 2 * peaks.get("bf16_tflops", 1639.9) * 1e12   # dense int8 = 2x dense bf16 on B200
+        int8_peak = i8_peak
         a = 2 * macs / dom_s if dom_s else 0.0
         # useful share of the issued MACs: 96 of the 128 M rows carry data (3 streams x 32 inputs), and of
         # the 16 byte shifts x 8 byte positions of each (row, group, rotation) only the 64 with
@@ -462,14 +469,10 @@ def run_ours(args):
         roofs["tensor"] = {"achieved": round(a / 1e12, 2), "peak": round(int8_peak / 1e12, 1), "unit": "TOP/s",
                            "frac": round(a / int8_peak, 4), "useful_mac_frac": 0.375,
                            "useful_frac_of_peak": round(0.375 * a / int8_peak, 4),
-                           "peak_source": "2x MEASURED_PEAKS.json bf16_tflops (dense int8 = 2x bf16)"}
+                           "peak_source": "tcgen05 kind::i8 issue rate measured by tools/mma_bench.cu x SMs x sm_max_mhz"}
     if dom_name == "k_gala_kf":
         macs = (L + 1) * N * KF_MACS_PER_POSITION * launches_per_step   # issued int8 MACs (CTA-pair MMAs)
-        # the measured tcgen05 kind::i8 issue rate (tools/mma_bench.cu, profiles/r2_mma_bench.txt: 8192 MACs
-        # per clock per SM) at the maximum SM clock -- higher than 2x the cuBLAS bf16 figure, so the stricter roof
-        int8_peak = max(2 * peaks.get("bf16_tflops", 1639.9) * 1e12,
-                        2 * 8192 * torch.cuda.get_device_properties(dev).multi_processor_count
-                        * peaks.get("sm_max_mhz", 1965.0) * 1e6)
+        int8_peak = i8_peak
         a = 2 * macs / dom_s if dom_s else 0.0
         uf = kf_useful_mac_frac(B, L, T // baby, baby)
         roofs["tensor"] = {"achieved": round(a / 1e12, 2), "peak": round(int8_peak / 1e12, 1), "unit": "TOP/s",
@@ -485,8 +488,7 @@ def run_ours(args):
     from paper_2105_01827_b200.analytics import executed_roofline, fc_executed_work
 
     work = fc_executed_work(N, L, T, baby, B, tc_form)
-    lr = executed_roofline(work, work["bytes"], ms_per_step / 1e3, peak_modmul,
-                           2 * peaks.get("bf16_tflops", 1639.9) * 1e12, hbm_peak * 1e9)
+    lr = executed_roofline(work, work["bytes"], ms_per_step / 1e3, peak_modmul, i8_peak, hbm_peak * 1e9)
     layer_roof = {"bound": lr["bound"], "frac": lr["frac"], "roofline_us_per_step": lr["roofline_us"],
                   "measured_us_per_step": round(ms_per_step * 1e3, 1), "modmuls_per_step": lr["modmuls"],
                   "int8_macs_per_step": lr["int8_macs"], "bytes_per_step": lr["bytes"],

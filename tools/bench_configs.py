@@ -184,15 +184,21 @@ _PEAK_MM = []
 
 def exec_roof(work, nbytes, ms_per_layer, ctx):
     """The schedule as executed (analytics.*_executed_work) against every roof: CUDA-core modmuls at the
-    measured modmul peak, int8 MACs at 2x the measured bf16 peak, bytes at HBM."""
+    measured modmul peak, int8 MACs at the measured tcgen05 i8 rate (analytics.tensor_i8_peak_ops), bytes at HBM."""
+    import torch
+
+    from paper_2105_01827_b200.analytics import tensor_i8_peak_ops
+
     if not _PEAK_MM:
         _PEAK_MM.append(ctx.bench_modmul())
-    bf16 = 1639.9
+    bf16, mhz = 1639.9, 1965.0
     try:
-        bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflops", bf16))
+        pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        bf16, mhz = float(pk.get("bf16_tflops", bf16)), float(pk.get("sm_max_mhz", mhz))
     except Exception:
         pass
-    r = executed_roofline(work, nbytes, ms_per_layer / 1e3, _PEAK_MM[0], 2 * bf16 * 1e12, HBM_PEAK * 1e9)
+    i8 = tensor_i8_peak_ops(torch.cuda.get_device_properties(ctx.device).multi_processor_count, mhz, bf16)
+    r = executed_roofline(work, nbytes, ms_per_layer / 1e3, _PEAK_MM[0], i8, HBM_PEAK * 1e9)
     return {"bound": r["bound"], "frac": r["frac"], "roofline_us": r["roofline_us"], "modmuls": r["modmuls"],
             "int8_macs": r["int8_macs"], "bytes": r["bytes"]}
 
