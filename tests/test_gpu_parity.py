@@ -295,15 +295,18 @@ def test_conv_kg2_kernel_sizes(tw, ksz, post):
     assert np.array_equal(tw.gpu.export_words(g_out), c_out)
 
 
-@pytest.mark.parametrize("T,nb", [(2, 17), (4, 17), (8, 17), (16, 17), (8, 48), (16, 64), (16, 130)])
+@pytest.mark.parametrize("T,nb", [(2, 17), (4, 17), (8, 17), (16, 17), (8, 48), (16, 64), (16, 130), (128, 17),
+                                  (256, 40), (128, 259)])
 def test_mv_gala2_tensor_core_words(tw, T, nb):
     """Tensor-core baby-step sums (byte-convolution int8 MMA) == CUDA-core schedule 2 == oracle o_mv_gala2."""
     import torch
 
     n = tw.bfv.n
-    if T > n or tw.N % 32:
-        pytest.skip("shape")
+    if T > n or tw.N % 32 or (nb > 256 and tw.N > 4096):
+        pytest.skip("shape")               # (two key-folded tiles: checked on the smaller rings)
     b, steps = tw.gpu.bsgs_steps(T)
+    if T >= 64:                            # the production split for schedule 2 (Context.gala2_baby)
+        b, steps = tw.gpu.bsgs_steps(T, tw.gpu.gala2_baby(T))
     tw.gpu.set_fc_tc_min_terms(1)          # tiles at every T (production: T >= 128)
     try:
         _tensor_core_words(tw, T, nb, b, steps)
@@ -320,7 +323,7 @@ def _tensor_core_words(tw, T, nb, b, steps):
     pts = tw.slots(T)
     pts2 = tw.gpu.encode_gala_weights(pts, b)
     wcan = tw.gpu.fc_tc_weights(pts2, T, b)
-    # key-folded tiles of 128 inputs: 17 .. 64 = one partial tile, 130 = 128 + 2
+    # key-folded tiles of 256 inputs: 17 .. 130 = one partial tile, 259 = 256 + 3 (two tiles)
     xs = [tw.encrypt(tw.slots()) for _ in range(nb)]
     rs = tw.slots(nb)
     cts = torch.stack([g for g, _ in xs])
