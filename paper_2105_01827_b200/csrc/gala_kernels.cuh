@@ -3367,6 +3367,40 @@ __global__ void __launch_bounds__(512, 2) k_encode(DevCtx c, const uint32_t* __r
 }
 
 // decrypt phase 1: per prime j: x_j = INTT(c0 + c1 * S)
+// Delta-encode split in two (the masks of a batch, MODE 1 of k_encode): the INTT mod p of a mask is the
+// same for every ciphertext prime, so it runs once per mask (k_encode_p: slots -> N^-1-scaled
+// coefficients m < p) and each prime's CTA only lifts and transforms (k_encode_q: Delta m mod q_j ->
+// NTT_j).  One polynomial of shared memory each (two CTAs per SM, where k_encode<1> needs two); the same
+// words as k_encode<1>.
+__global__ void __launch_bounds__(512, 2) k_encode_p(DevCtx c, const uint32_t* __restrict__ slots, uint32_t* __restrict__ m)
+{
+    extern __shared__ u64 smem_enc[];
+    u64* sm = smem_enc;
+    const int N = c.N, PM = c.M;
+    const uint32_t* sl = slots + (long long)blockIdx.x * N;
+    const u64 p = c.p;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(c.slot_pos[i])] = sl[i] % p;
+    __syncthreads();
+    ntt_inv_smem(sm, c.twi[PM], p, c.logN);
+    uint32_t* o = m + (long long)blockIdx.x * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) o[i] = (uint32_t)shoup(sm[pad(i)], c.ninv[PM], c.ninv_sh[PM], p);
+}
+__global__ void __launch_bounds__(512, 2) k_encode_q(DevCtx c, const uint32_t* __restrict__ m, u64* __restrict__ out)
+{
+    extern __shared__ u64 smem_enc[];
+    u64* sm = smem_enc;
+    const int N = c.N, L = c.L;
+    const int b = blockIdx.x / L, j = blockIdx.x % L;
+    const uint32_t* mb = m + (long long)b * N;
+    const ModC md = c.mod[j];
+    const u64 q = md.q, dl = c.delta[j], dsh = c.delta_sh[j];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm[pad(i)] = shoup((u64)__ldg(mb + i), dl, dsh, q);
+    __syncthreads();
+    ntt_fwd_smem(sm, c.twf[j], q, c.logN);
+    u64* o = out + ((long long)b * L + j) * N;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) o[i] = csub(csub(sm[pad(i)], 2 * q), q);
+}
+
 __global__ void __launch_bounds__(512, 2) k_dec_phase1(DevCtx c, const u64* __restrict__ ct, u64* __restrict__ x)
 {
     extern __shared__ u64 sm[];

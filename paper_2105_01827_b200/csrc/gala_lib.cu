@@ -679,11 +679,19 @@ static int mask_begin(gala_ctx* c, const uint32_t* r, int B, u64** DM)
     cudaStream_t main = c->stream;
     cudaEvent_t a = nullptr, b = nullptr;
     c->stream = c->side;   // profiling events belong on the side stream
+    uint32_t* mcoef;
+    int rs = scratch(c, &mcoef, (size_t)B * N);   // B x N u32 coefficients
+    if (rs != GALA_OK) {
+        c->stream = main;
+        return rs;
+    }
     if (c->prof_on) prof_begin(c, &a, &b);
-    k_encode<1><<<B * L, ntt_threads(N), 2 * c->smem_ntt, c->side>>>(c->dc, r, *DM);
+    k_encode_p<<<B, ntt_threads(N), c->smem_ntt, c->side>>>(c->dc, r, mcoef);
+    k_encode_q<<<B * L, ntt_threads(N), c->smem_ntt, c->side>>>(c->dc, mcoef, *DM);
     if (c->prof_on) prof_end(c, "k_encode", a, b);
+    release(c, mcoef);
     c->stream = main;
-    g_launches++;
+    g_launches += 2;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(GALA_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
     CK(cudaEventRecord(c->ev_join, c->side));
@@ -706,7 +714,11 @@ static int sub_plain_batch(gala_ctx* c, const u64* ct, const uint32_t* r, int B,
     const long long W = 2LL * L * N, LN = (long long)L * N;
     u64* DM;
     RET(scratch(c, &DM, (size_t)B * LN));
-    KLAUNCH(c, "k_encode", k_encode<1><<<B * L, ntt_threads(N), 2 * c->smem_ntt, c->stream>>>(c->dc, r, DM));
+    uint32_t* mcoef;
+    RET(scratch(c, &mcoef, (size_t)B * N));
+    KLAUNCH(c, "k_encode", k_encode_p<<<B, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, r, mcoef));
+    KLAUNCH(c, "k_encode", k_encode_q<<<B * L, ntt_threads(N), c->smem_ntt, c->stream>>>(c->dc, mcoef, DM));
+    release(c, mcoef);
     KLAUNCH(c, "k_sub_plain", k_sub_plain<<<grid_for((long long)B * W, 256), 256, 0, c->stream>>>(c->dc, ct, DM, out, B));
     release(c, DM);
     return GALA_OK;
@@ -961,6 +973,8 @@ int gala_ctx_create(gala_ctx** out, int N, int L, const uint64_t* primes, const 
     CKC(cudaFuncSetAttribute(k_block_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_encode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
     CKC(cudaFuncSetAttribute(k_encode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_encode_p, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CKC(cudaFuncSetAttribute(k_encode_q, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_encode<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kMaxSmem));
     CKC(cudaFuncSetAttribute(k_dec_phase1, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     CKC(cudaFuncSetAttribute(k_dec_phase2, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
