@@ -256,6 +256,7 @@ struct MacMember {
     const u64* X;      // step-0 member source
     const u64* pt;
     int no_c0;         // rotated member whose c0 is zero (block c0 slots not written)
+    unsigned gal;      // > 1: blk is the term's identity block and the member's sigma is applied as a gather
 };
 
 // grid (N / blockDim, M, G); U [G][2][M][N]; Cacc [G][2][L][N].
@@ -311,6 +312,19 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
     constexpr int LMAX = L;
     u64 dv[LMAX], kb[LMAX], ka[LMAX], cv = 0;
     auto fetch = [&](const MacMember& m) {
+        if (m.gal > 1u) {   // hoisted rotation: gather sigma(D) from the term's identity block (kept in L2)
+            const int src = auto_src(k, m.gal, c.logN);
+#pragma unroll
+            for (int i = 0; i < LMAX; i++) {
+                if (i < L) {
+                    dv[i] = __ldg(m.blk + ((long long)i * M + j) * NN + src);
+                    kb[i] = __ldg(&m.key[(((long long)i * 2 + 0) * M + j) * NN + k]);
+                    ka[i] = __ldg(&m.key[(((long long)i * 2 + 1) * M + j) * NN + k]);
+                }
+            }
+            cv = (j < L && !m.no_c0) ? __ldg(m.blk + ((long long)L * M + j) * NN + src) : 0ull;
+            return;
+        }
 #pragma unroll
         for (int i = 0; i < LMAX; i++) {
             if (i < L) {

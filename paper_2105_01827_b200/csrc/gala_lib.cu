@@ -458,6 +458,11 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         if (!t.steps.empty() && (t.steps.size() != 1 || t.ntt_block)) fusable = false;
     if (fusable && !raw_U) return rotate_engine_fused(c, terms, groups, outs, qp_add, q_add);
     const long long blk_words = (long long)(L * M + L) * N;
+    // hoisted terms (several rotations of one decomposition): ONE identity block per term, and k_ks_mac
+    // applies each member's sigma as a gather from it (the block stays in L2 while the term's rotations
+    // run) instead of one sigma-permuted block per rotation in HBM.  GALA_KS_GATHER=0: permuted blocks.
+    const bool gather = !(getenv("GALA_KS_GATHER") && getenv("GALA_KS_GATHER")[0] == '0');
+    auto gathered = [&](const EngTerm& T) { return gather && T.steps.size() > 1; };
     // rotated terms and their rotation slices
     std::vector<int> term_rot_base(terms.size(), -1);
     int n_rot = 0, n_dig = 0;
@@ -465,8 +470,9 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         for (int s : terms[t].steps)
             if (!key_for(c, s)) return set_err(GALA_ERR_NOKEY, "missing rotation key for step %d", norm_step(c, s));
         if (!terms[t].steps.empty()) {
+            if (gathered(terms[t]) && terms[t].ntt_block) continue;   // reads the caller's identity block
             term_rot_base[t] = n_rot;
-            n_rot += (int)terms[t].steps.size();
+            n_rot += gathered(terms[t]) ? 1 : (int)terms[t].steps.size();
             if (!terms[t].ntt_block) n_dig++;
         }
     }
@@ -478,6 +484,7 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     int di = 0;
     for (size_t t = 0; t < terms.size(); t++) {
         if (terms[t].steps.empty()) continue;
+        if (gathered(terms[t]) && terms[t].ntt_block) continue;
         TermDesc d{};
         d.X = terms[t].X;
         d.pt = terms[t].pt;
@@ -485,8 +492,13 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         d.dig = terms[t].ntt_block ? nullptr : dig + (long long)(di++) * L * N;
         d.blk = blk + (long long)term_rot_base[t] * blk_words;
         d.rot_off = (int)gal.size();
-        d.rot_cnt = (int)terms[t].steps.size();
-        for (int s : terms[t].steps) gal.push_back(galois_of(c, s));
+        if (gathered(terms[t])) {   // the identity block only
+            d.rot_cnt = 1;
+            gal.push_back(1u);
+        } else {
+            d.rot_cnt = (int)terms[t].steps.size();
+            for (int s : terms[t].steps) gal.push_back(galois_of(c, s));
+        }
         if (terms[t].ntt_block) {
             d.X = terms[t].ntt_block;   // identity block as the permutation source
             td_hoisted.push_back(d);
@@ -529,7 +541,12 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
                 mm.X = T.X;
                 mm.pt = T.pt;
             } else {
-                mm.blk = blk + (long long)(term_rot_base[m.term] + m.rot) * blk_words;
+                if (gathered(T)) {
+                    mm.blk = T.ntt_block ? T.ntt_block : blk + (long long)term_rot_base[m.term] * blk_words;
+                    mm.gal = galois_of(c, T.steps[m.rot]);
+                } else {
+                    mm.blk = blk + (long long)(term_rot_base[m.term] + m.rot) * blk_words;
+                }
                 mm.key = key_for(c, T.steps[m.rot]);
                 mm.X = nullptr;
                 mm.pt = nullptr;
