@@ -264,8 +264,10 @@ struct MacMember {
 // rotated members follow.  Digit/key products accumulate in 128 bits across
 // digits *and* members and are Montgomery-reduced only every c.lazy[j]
 // products (k q^2 < q 2^64).  The next member's loads are issued before the
-// current member's multiplies (software pipelining over the member loop).
-template <int L>
+// current member's multiplies (software pipelining over the member loop).  GATHER: some members read
+// their digits through a sigma gather from an identity block (MacMember.gal > 1; a separate
+// instantiation so the permuted-block form keeps its registers).
+template <int L, bool GATHER = false>
 __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __restrict__ mem,
                                                 const int* __restrict__ group_off, u64* __restrict__ U,
                                                 u64* __restrict__ Cacc, const u64* __restrict__ qp_add,
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(256) k_ks_mac(DevCtx c, const MacMember* __res
     constexpr int LMAX = L;
     u64 dv[LMAX], kb[LMAX], ka[LMAX], cv = 0;
     auto fetch = [&](const MacMember& m) {
-        if (m.gal > 1u) {   // hoisted rotation: gather sigma(D) from the term's identity block (kept in L2)
+        if (GATHER && m.gal > 1u) {   // hoisted rotation: gather sigma(D) from the term's identity block (in L2)
             const int src = auto_src(k, m.gal, c.logN);
 #pragma unroll
             for (int i = 0; i < LMAX; i++) {

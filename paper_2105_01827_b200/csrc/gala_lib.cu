@@ -604,12 +604,22 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         u64* const Co = V > G ? Cv : Cacc;
         const MacMember* dm = (const MacMember*)(d_blob + o_mem);
         const int* doff = (const int*)(d_blob + o_off);
+        bool any_gather = false;
+        for (const auto& m : mem) any_gather = any_gather || m.gal > 1u;
+#define KSMAC(LL)                                                                                                   \
+    do {                                                                                                            \
+        if (any_gather)                                                                                             \
+            KLAUNCH(c, "k_ks_mac", (k_ks_mac<LL, true><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add))); \
+        else                                                                                                        \
+            KLAUNCH(c, "k_ks_mac", (k_ks_mac<LL, false><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add))); \
+    } while (0)
         switch (L) {
-            case 1: KLAUNCH(c, "k_ks_mac", k_ks_mac<1><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add)); break;
-            case 2: KLAUNCH(c, "k_ks_mac", k_ks_mac<2><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add)); break;
-            case 3: KLAUNCH(c, "k_ks_mac", k_ks_mac<3><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add)); break;
-            default: KLAUNCH(c, "k_ks_mac", k_ks_mac<4><<<grid, th, 0, c->stream>>>(c->dc, dm, doff, Uo, Co, qp_add, q_add)); break;
+            case 1: KSMAC(1); break;
+            case 2: KSMAC(2); break;
+            case 3: KSMAC(3); break;
+            default: KSMAC(4); break;
         }
+#undef KSMAC
     }
     if (V > G) {   // fold the chunk sums of every split group
         int* d_vsc;
