@@ -389,6 +389,59 @@ struct FusedTerm {
     int c0_zero;
 };
 
+// Uniform hoisted rotations (every term rotated by the same R steps, one member per group, groups
+// term-major): U[(b R + r)] = sum_i sigma_r(D_i^b) ksk_r[i] and Cacc[(b R + r)].c0 = sigma_r(x_b.c0) --
+// what k_ks_mac<L, true> computes for these groups, word for word, with the loops turned around: a
+// thread (position k, prime j) takes KH_TB terms for every step r, so step r's key words and sigma_r
+// source index are loaded once and reused KH_TB times, and the KH_TB identity blocks stay hot in L1/L2
+// across the R steps.  grid (N / 256, M, ceil(terms / KH_TB)).
+#define KH_TB 8
+template <int L>
+__global__ void __launch_bounds__(256) k_ks_hoist(DevCtx c, const u64* const* __restrict__ blocks,
+                                                  const unsigned* __restrict__ gal, const u64* const* __restrict__ keys,
+                                                  int R, int nterms, int no_c0, u64* __restrict__ U, u64* __restrict__ Cacc)
+{
+    const int N = c.N, M = L + 1;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, b0 = blockIdx.z * KH_TB;
+    if (k >= N) return;
+    const u64 q = c.mod[j].q;
+    const long long NN = N;
+    const int nb = nterms - b0 < KH_TB ? nterms - b0 : KH_TB;
+    for (int r = 0; r < R; r++) {
+        const int src = auto_src(k, gal[r], c.logN);
+        const u64* key = keys[r];
+        u64 kb[L], ka[L];
+#pragma unroll
+        for (int i = 0; i < L; i++) {
+            kb[i] = __ldg(&key[(((long long)i * 2 + 0) * M + j) * NN + k]);
+            ka[i] = __ldg(&key[(((long long)i * 2 + 1) * M + j) * NN + k]);
+        }
+        for (int bi = 0; bi < nb; bi++) {
+            const u64* blk = blocks[b0 + bi];
+            u64 dv[L];
+#pragma unroll
+            for (int i = 0; i < L; i++) dv[i] = __ldg(blk + ((long long)i * M + j) * NN + src);
+            const u64 cv = (j < L && !no_c0) ? __ldg(blk + ((long long)L * M + j) * NN + src) : 0ull;
+            AccPP<> s0, s1;
+            s0.clear();
+            s1.clear();
+#pragma unroll
+            for (int i = 0; i < L; i++) {
+                s0.mac(dv[i], kb[i]);
+                s1.mac(dv[i], ka[i]);
+            }
+            const long long g = (long long)(b0 + bi) * R + r;
+            U[((g * 2 + 0) * M + j) * NN + k] = add_mod(0, s0.reduce_sf(q), q);
+            U[((g * 2 + 1) * M + j) * NN + k] = add_mod(0, s1.reduce_sf(q), q);
+            if (j < L) {
+                Cacc[((g * 2 + 0) * L + j) * NN + k] = add_mod(0, cv, q);
+                Cacc[((g * 2 + 1) * L + j) * NN + k] = 0;
+            }
+        }
+    }
+}
+
 template <int L>
 __global__ void __launch_bounds__(1024, 1) k_ks_fused(DevCtx c, const FusedTerm* __restrict__ terms,
                                                      u64* __restrict__ part, u64* __restrict__ cpart)

@@ -606,6 +606,45 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         const int* doff = (const int*)(d_blob + o_off);
         bool any_gather = false;
         for (const auto& m : mem) any_gather = any_gather || m.gal > 1u;
+        // uniform hoisted rotations (every term rotated by the same steps, gathered, one member per group,
+        // groups term-major, no addends): k_ks_hoist reuses each step's key words across KH_TB terms
+        const int R = terms.empty() ? 0 : (int)terms[0].steps.size();
+        bool hoist = any_gather && V == G && qp_add == nullptr && q_add == nullptr && !raw_U && R > 1 &&
+                     (long long)terms.size() * R == G && getenv("GALA_KS_HOIST") == nullptr;
+        for (size_t t = 0; hoist && t < terms.size(); t++)
+            hoist = gathered(terms[t]) && terms[t].steps == terms[0].steps && terms[t].c0_zero == terms[0].c0_zero;
+        for (int g = 0; hoist && g < G; g++)
+            hoist = groups[g].size() == 1 && groups[g][0].term == g / R && groups[g][0].rot == g % R;
+        if (hoist) {
+            std::vector<const u64*> hb(terms.size()), hk(R);
+            std::vector<unsigned> hg(R);
+            for (size_t t = 0; t < terms.size(); t++)
+                hb[t] = terms[t].ntt_block ? terms[t].ntt_block : blk + (long long)term_rot_base[t] * blk_words;
+            for (int r = 0; r < R; r++) {
+                hk[r] = key_for(c, terms[0].steps[r]);
+                hg[r] = galois_of(c, terms[0].steps[r]);
+            }
+            std::vector<char> hbl(sizeof(u64*) * (hb.size() + R) + sizeof(unsigned) * R);
+            memcpy(hbl.data(), hb.data(), sizeof(u64*) * hb.size());
+            memcpy(hbl.data() + sizeof(u64*) * hb.size(), hk.data(), sizeof(u64*) * R);
+            memcpy(hbl.data() + sizeof(u64*) * (hb.size() + R), hg.data(), sizeof(unsigned) * R);
+            char* d_h;
+            RET(upload(c, hbl.data(), hbl.size(), (void**)&d_h));
+            const u64* const* d_hb = (const u64* const*)d_h;
+            const u64* const* d_hk = d_hb + hb.size();
+            const unsigned* d_hg = (const unsigned*)(d_hk + R);
+            const dim3 gh((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)((terms.size() + KH_TB - 1) / KH_TB));
+            const int nterms = (int)terms.size(), nc0 = terms[0].c0_zero ? 1 : 0;
+#define KSH(LL) KLAUNCH(c, "k_ks_mac", (k_ks_hoist<LL><<<gh, th, 0, c->stream>>>(c->dc, d_hb, d_hg, d_hk, R, nterms, nc0, U, Cacc)))
+            switch (L) {
+                case 1: KSH(1); break;
+                case 2: KSH(2); break;
+                case 3: KSH(3); break;
+                default: KSH(4); break;
+            }
+#undef KSH
+            release(c, d_h);
+        } else {
 #define KSMAC(LL)                                                                                                   \
     do {                                                                                                            \
         if (any_gather)                                                                                             \
@@ -620,6 +659,7 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
             default: KSMAC(4); break;
         }
 #undef KSMAC
+        }
     }
     if (V > G) {   // fold the chunk sums of every split group
         int* d_vsc;
