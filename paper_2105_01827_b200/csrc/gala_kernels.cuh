@@ -442,6 +442,106 @@ __global__ void __launch_bounds__(256) k_ks_hoist(DevCtx c, const u64* const* __
     }
 }
 
+// Giant-step key switches of a batch (FC schedule 2): every group (input) b sums the same R rotated terms
+// b R + r, term r of every group rotated by the same step (key r), each term's sigma-permuted digit block
+// written by k_digits_perm, plus the optional QP / Q addends -- what k_ks_mac<L, false> computes for
+// these groups, with each thread (position k, prime j) taking KG_IB groups so that every key word is
+// loaded once per KG_IB inputs.  grid (N / 256, M, ceil(G / KG_IB)).
+#define KG_IB 2
+template <int L>
+__global__ void __launch_bounds__(256) k_ks_giant(DevCtx c, const u64* const* __restrict__ blocks,
+                                                  const u64* const* __restrict__ keys, int R, int G, int no_c0,
+                                                  u64* __restrict__ U, u64* __restrict__ Cacc,
+                                                  const u64* __restrict__ qp_add, const u64* __restrict__ q_add)
+{
+    const int N = c.N, M = L + 1;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y, g0 = blockIdx.z * KG_IB;
+    if (k >= N) return;
+    const ModC md = c.mod[j];
+    const u64 q = md.q;
+    const int lazy = c.lazy[j];
+    const long long NN = N;
+    const int ng = G - g0 < KG_IB ? G - g0 : KG_IB;
+    u64 u0[KG_IB], u1[KG_IB], a0[KG_IB], a1[KG_IB];
+    AccPP<> s0[KG_IB], s1[KG_IB];
+#pragma unroll
+    for (int i = 0; i < KG_IB; i++) {
+        const long long g = g0 + (i < ng ? i : 0);
+        u0[i] = qp_add ? qp_add[((g * 2 + 0) * M + j) * NN + k] : 0;
+        u1[i] = qp_add ? qp_add[((g * 2 + 1) * M + j) * NN + k] : 0;
+        a0[i] = (q_add && j < L) ? q_add[((g * 2 + 0) * L + j) * NN + k] : 0;
+        a1[i] = (q_add && j < L) ? q_add[((g * 2 + 1) * L + j) * NN + k] : 0;
+        s0[i].clear();
+        s1[i].clear();
+    }
+    int pending = 0;
+    // software pipeline: step r + 1's key words and digits are in flight while step r multiplies
+    u64 kb[L], ka[L], dv[KG_IB][L], cv[KG_IB];
+    auto fetch = [&](int r) {
+        const u64* key = keys[r];
+#pragma unroll
+        for (int l = 0; l < L; l++) {
+            kb[l] = __ldg(&key[(((long long)l * 2 + 0) * M + j) * NN + k]);
+            ka[l] = __ldg(&key[(((long long)l * 2 + 1) * M + j) * NN + k]);
+        }
+#pragma unroll
+        for (int i = 0; i < KG_IB; i++) {
+            const u64* blk = blocks[(long long)(g0 + (i < ng ? i : 0)) * R + r];
+#pragma unroll
+            for (int l = 0; l < L; l++) dv[i][l] = __ldcs((const unsigned long long*)(blk + ((long long)l * M + j) * NN + k));
+            cv[i] = (j < L && !no_c0) ? __ldcs((const unsigned long long*)(blk + ((long long)L * M + j) * NN + k)) : 0ull;
+        }
+    };
+    fetch(0);
+    for (int r = 0; r < R; r++) {
+        u64 k0[L], k1[L], d[KG_IB][L], cc[KG_IB];
+#pragma unroll
+        for (int l = 0; l < L; l++) {
+            k0[l] = kb[l];
+            k1[l] = ka[l];
+        }
+#pragma unroll
+        for (int i = 0; i < KG_IB; i++) {
+            cc[i] = cv[i];
+#pragma unroll
+            for (int l = 0; l < L; l++) d[i][l] = dv[i][l];
+        }
+        if (r + 1 < R) fetch(r + 1);
+        if (pending + L > lazy) {
+#pragma unroll
+            for (int i = 0; i < KG_IB; i++) {
+                u0[i] = add_mod(u0[i], s0[i].reduce_sf(q), q);
+                u1[i] = add_mod(u1[i], s1[i].reduce_sf(q), q);
+                s0[i].clear();
+                s1[i].clear();
+            }
+            pending = 0;
+        }
+#pragma unroll
+        for (int i = 0; i < KG_IB; i++) {
+#pragma unroll
+            for (int l = 0; l < L; l++) {
+                s0[i].mac(d[i][l], k0[l]);
+                s1[i].mac(d[i][l], k1[l]);
+            }
+            if (j < L) a0[i] = add_mod(a0[i], cc[i], q);
+        }
+        pending += L;
+    }
+#pragma unroll
+    for (int i = 0; i < KG_IB; i++) {
+        if (i >= ng) break;
+        const long long g = g0 + i;
+        U[((g * 2 + 0) * M + j) * NN + k] = add_mod(u0[i], s0[i].reduce_sf(q), q);
+        U[((g * 2 + 1) * M + j) * NN + k] = add_mod(u1[i], s1[i].reduce_sf(q), q);
+        if (j < L) {
+            Cacc[((g * 2 + 0) * L + j) * NN + k] = a0[i];
+            Cacc[((g * 2 + 1) * L + j) * NN + k] = a1[i];
+        }
+    }
+}
+
 template <int L>
 __global__ void __launch_bounds__(1024, 1) k_ks_fused(DevCtx c, const FusedTerm* __restrict__ terms,
                                                      u64* __restrict__ part, u64* __restrict__ cpart)

@@ -615,7 +615,40 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
             hoist = gathered(terms[t]) && terms[t].steps == terms[0].steps && terms[t].c0_zero == terms[0].c0_zero;
         for (int g = 0; hoist && g < G; g++)
             hoist = groups[g].size() == 1 && groups[g][0].term == g / R && groups[g][0].rot == g % R;
-        if (hoist) {
+        // giant steps of a batch (every group sums the same R single-step terms, term-major, no gather, no
+        // step-0 members): k_ks_giant reuses each key word across KG_IB groups
+        const int Rg = G > 0 ? (int)groups[0].size() : 0;
+        bool giant = !any_gather && V == G && Rg >= 1 && (long long)Rg * G == (long long)terms.size() && !raw_U &&
+                     getenv("GALA_KS_GIANT") == nullptr;
+        for (size_t t = 0; giant && t < terms.size(); t++)
+            giant = terms[t].steps.size() == 1 && !terms[t].ntt_block && terms[t].steps[0] == terms[t % Rg].steps[0] &&
+                    terms[t].c0_zero == terms[0].c0_zero;
+        for (int g = 0; giant && g < G; g++) {
+            giant = (int)groups[g].size() == Rg;
+            for (int r = 0; giant && r < Rg; r++) giant = groups[g][r].term == g * Rg + r && groups[g][r].rot == 0;
+        }
+        if (giant) {
+            std::vector<const u64*> gb(terms.size()), gk(Rg);
+            for (size_t t = 0; t < terms.size(); t++) gb[t] = blk + (long long)term_rot_base[t] * blk_words;
+            for (int r = 0; r < Rg; r++) gk[r] = key_for(c, terms[r].steps[0]);
+            std::vector<const u64*> gall(gb);
+            gall.insert(gall.end(), gk.begin(), gk.end());
+            char* d_g;
+            RET(upload(c, gall.data(), gall.size() * sizeof(u64*), (void**)&d_g));
+            const u64* const* d_gb = (const u64* const*)d_g;
+            const u64* const* d_gk = d_gb + gb.size();
+            const dim3 gg((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)((G + KG_IB - 1) / KG_IB));
+            const int nc0 = terms[0].c0_zero ? 1 : 0;
+#define KSG(LL) KLAUNCH(c, "k_ks_mac", (k_ks_giant<LL><<<gg, th, 0, c->stream>>>(c->dc, d_gb, d_gk, Rg, G, nc0, U, Cacc, qp_add, q_add)))
+            switch (L) {
+                case 1: KSG(1); break;
+                case 2: KSG(2); break;
+                case 3: KSG(3); break;
+                default: KSG(4); break;
+            }
+#undef KSG
+            release(c, d_g);
+        } else if (hoist) {
             std::vector<const u64*> hb(terms.size()), hk(R);
             std::vector<unsigned> hg(R);
             for (size_t t = 0; t < terms.size(); t++)
