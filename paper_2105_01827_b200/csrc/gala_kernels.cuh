@@ -392,22 +392,22 @@ struct FusedTerm {
 // Uniform hoisted rotations (every term rotated by the same R steps, one member per group, groups
 // term-major): U[(b R + r)] = sum_i sigma_r(D_i^b) ksk_r[i] and Cacc[(b R + r)].c0 = sigma_r(x_b.c0) --
 // what k_ks_mac<L, true> computes for these groups, word for word, with the loops turned around: a
-// thread (position k, prime j) takes KH_TB terms for every step r, so step r's key words and sigma_r
-// source index are loaded once and reused KH_TB times, and the KH_TB identity blocks stay hot in L1/L2
-// across the R steps.  grid (N / 256, M, ceil(terms / KH_TB)).
-#define KH_TB 8
+// thread (position k, prime j) takes tb terms (up to 8; fewer when the grid would not fill the GPU) for
+// every step r, so step r's key words and sigma_r source index are loaded once and reused tb times, and
+// the tb identity blocks stay hot in L1/L2 across the R steps.  grid (N / 256, M, ceil(terms / tb)).
 template <int L>
 __global__ void __launch_bounds__(256) k_ks_hoist(DevCtx c, const u64* const* __restrict__ blocks,
                                                   const unsigned* __restrict__ gal, const u64* const* __restrict__ keys,
-                                                  int R, int nterms, int no_c0, u64* __restrict__ U, u64* __restrict__ Cacc)
+                                                  int R, int nterms, int tb, int no_c0, u64* __restrict__ U,
+                                                  u64* __restrict__ Cacc)
 {
     const int N = c.N, M = L + 1;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y, b0 = blockIdx.z * KH_TB;
+    const int j = blockIdx.y, b0 = blockIdx.z * tb;
     if (k >= N) return;
     const u64 q = c.mod[j].q;
     const long long NN = N;
-    const int nb = nterms - b0 < KH_TB ? nterms - b0 : KH_TB;
+    const int nb = nterms - b0 < tb ? nterms - b0 : tb;
     for (int r = 0; r < R; r++) {
         const int src = auto_src(k, gal[r], c.logN);
         const u64* key = keys[r];

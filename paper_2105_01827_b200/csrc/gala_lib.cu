@@ -607,7 +607,7 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         bool any_gather = false;
         for (const auto& m : mem) any_gather = any_gather || m.gal > 1u;
         // uniform hoisted rotations (every term rotated by the same steps, gathered, one member per group,
-        // groups term-major, no addends): k_ks_hoist reuses each step's key words across KH_TB terms
+        // groups term-major, no addends): k_ks_hoist reuses each step's key words across up to 8 terms
         const int R = terms.empty() ? 0 : (int)terms[0].steps.size();
         bool hoist = any_gather && V == G && qp_add == nullptr && q_add == nullptr && !raw_U && R > 1 &&
                      (long long)terms.size() * R == G && getenv("GALA_KS_HOIST") == nullptr;
@@ -619,7 +619,8 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         // step-0 members): k_ks_giant reuses each key word across KG_IB groups
         const int Rg = G > 0 ? (int)groups[0].size() : 0;
         bool giant = !any_gather && V == G && Rg >= 1 && (long long)Rg * G == (long long)terms.size() && !raw_U &&
-                     getenv("GALA_KS_GIANT") == nullptr;
+                     getenv("GALA_KS_GIANT") == nullptr &&
+                     (long long)((N + th - 1) / th) * M * ((G + KG_IB - 1) / KG_IB) >= 2LL * c->num_sms;   // fills the GPU
         for (size_t t = 0; giant && t < terms.size(); t++)
             giant = terms[t].steps.size() == 1 && !terms[t].ntt_block && terms[t].steps[0] == terms[t % Rg].steps[0] &&
                     terms[t].c0_zero == terms[0].c0_zero;
@@ -666,9 +667,12 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
             const u64* const* d_hb = (const u64* const*)d_h;
             const u64* const* d_hk = d_hb + hb.size();
             const unsigned* d_hg = (const unsigned*)(d_hk + R);
-            const dim3 gh((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)((terms.size() + KH_TB - 1) / KH_TB));
             const int nterms = (int)terms.size(), nc0 = terms[0].c0_zero ? 1 : 0;
-#define KSH(LL) KLAUNCH(c, "k_ks_mac", (k_ks_hoist<LL><<<gh, th, 0, c->stream>>>(c->dc, d_hb, d_hg, d_hk, R, nterms, nc0, U, Cacc)))
+            const long long xy = (long long)((N + th - 1) / th) * M;
+            int tb = 8;   // terms per thread: key reuse, unless the grid would then underfill the GPU
+            while (tb > 1 && xy * ((nterms + tb - 1) / tb) < 2LL * c->num_sms) tb /= 2;
+            const dim3 gh((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)((nterms + tb - 1) / tb));
+#define KSH(LL) KLAUNCH(c, "k_ks_mac", (k_ks_hoist<LL><<<gh, th, 0, c->stream>>>(c->dc, d_hb, d_hg, d_hk, R, nterms, tb, nc0, U, Cacc)))
             switch (L) {
                 case 1: KSH(1); break;
                 case 2: KSH(2); break;
