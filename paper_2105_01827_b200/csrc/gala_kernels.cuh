@@ -998,7 +998,7 @@ __global__ void k_sub_plain(DevCtx c, const u64* __restrict__ ct, const u64* __r
 // T = hi 2^64 + lo: every c.lazy[j] products the high word is brought back below q by one
 // conditional subtraction (T - q 2^64 == T mod q; lazy products of canonical operands add less
 // than q to hi), so the sum never leaves its 4 registers; one REDC at the end.  grid: (N / blockDim, L * ceil(nimg / IMG), ceil(rows / ODT)).
-template <int IMG, int ODT>
+template <int IMG, int ODT, bool PP>
 __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __restrict__ R, long long R_bs, int n_ib,
                                                        int ib0, int ib1, int k, const u64* __restrict__ pts, int c_n,
                                                        int rows, int nimg, int accumulate, u64* __restrict__ acc,
@@ -1013,7 +1013,21 @@ __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __re
     const u64 q = c.mod[j].q;
     const int lazy = c.lazy[j];
     const long long LN = (long long)L * N, W = 2 * LN;
-    Acc128 a[ODT][IMG][2];
+    // PP: partial-product sums (4 IMAD.WIDE.U32 per product instead of a 64x64 -> 128 multiply; the kernel
+    // is FMA-heavy-pipe bound), flushed through one REDC every c.lazy[j] products into a value mod q -- more
+    // registers, so it pays where the grid, not occupancy, limits (one image)
+    Acc128 ac[ODT][IMG][2];
+    AccPP<> a[ODT][IMG][2];
+    u64 v[ODT][IMG][2];
+#pragma unroll
+    for (int r = 0; r < ODT; r++)
+#pragma unroll
+        for (int i = 0; i < IMG; i++)
+#pragma unroll
+            for (int cp = 0; cp < 2; cp++) {
+                a[r][i][cp].clear();
+                v[r][i][cp] = 0;
+            }
     const u64* prow[ODT];
 #pragma unroll
     for (int r = 0; r < ODT; r++) {
@@ -1033,7 +1047,14 @@ __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __re
 #pragma unroll
                     for (int i = 0; i < IMG; i++)
 #pragma unroll
-                        for (int cp = 0; cp < 2; cp++) a[r][i][cp].hi = csub(a[r][i][cp].hi, q);
+                        for (int cp = 0; cp < 2; cp++) {
+                            if (PP) {
+                                v[r][i][cp] = add_mod(v[r][i][cp], a[r][i][cp].reduce_sf(q), q);
+                                a[r][i][cp].clear();
+                            } else {
+                                ac[r][i][cp].hi = csub(ac[r][i][cp].hi, q);
+                            }
+                        }
                 pending = 0;
             }
             u64 rv[IMG][2];
@@ -1048,8 +1069,13 @@ __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __re
                 const u64 w = __ldcs((const unsigned long long*)(prow[r] + (long long)ib * pt_ib + t * LN));
 #pragma unroll
                 for (int i = 0; i < IMG; i++) {
-                    a[r][i][0].mac(rv[i][0], w);
-                    a[r][i][1].mac(rv[i][1], w);
+                    if (PP) {
+                        a[r][i][0].mac(rv[i][0], w);
+                        a[r][i][1].mac(rv[i][1], w);
+                    } else {
+                        ac[r][i][0].mac(rv[i][0], w);
+                        ac[r][i][1].mac(rv[i][1], w);
+                    }
                 }
             }
             pending++;
@@ -1061,8 +1087,14 @@ __global__ void __launch_bounds__(256) k_kg_accumulate(DevCtx c, const u64* __re
 #pragma unroll
         for (int i = 0; i < IMG; i++) {
             if (i >= nb) break;
-            u64 v0 = csub(redc_sf_lazy(csub(a[r][i][0].hi, q), a[r][i][0].lo, q), q);
-            u64 v1 = csub(redc_sf_lazy(csub(a[r][i][1].hi, q), a[r][i][1].lo, q), q);
+            u64 v0, v1;
+            if (PP) {
+                v0 = add_mod(v[r][i][0], a[r][i][0].reduce_sf(q), q);
+                v1 = add_mod(v[r][i][1], a[r][i][1].reduce_sf(q), q);
+            } else {
+                v0 = csub(redc_sf_lazy(csub(ac[r][i][0].hi, q), ac[r][i][0].lo, q), q);
+                v1 = csub(redc_sf_lazy(csub(ac[r][i][1].hi, q), ac[r][i][1].lo, q), q);
+            }
             u64* out = acc + (long long)(b0 + i) * acc_bs + (long long)(od0 + r) * W + (long long)j * N + x;
             if (accumulate) {
                 v0 = add_mod(v0, out[0], q);

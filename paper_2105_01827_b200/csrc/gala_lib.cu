@@ -2081,6 +2081,10 @@ static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_
             odt = b2;
         }
     }
+    // partial-product accumulators: one image (config 3: 84 -> 60 us; grid-limited), not the 2-image tile
+    // (30 -> 33 us per image at 16 images: register-limited)
+    bool pp = img == 1;
+    if (const char* e = getenv("GALA_KGACC_PP")) pp = atoi(e) != 0;
     dim3 grid((N + th - 1) / th, L * ((B + img - 1) / img), (rows + odt - 1) / odt);
     // input-block chunks whose rotated inputs (k * W words each, every image) fit comfortably in L2 (~48 MB)
     const long long chunk_bytes = 48ll << 20;
@@ -2089,7 +2093,15 @@ static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_
     const long long R_bs = (long long)n_ib * k * W, acc_bs = (long long)rows * W;
     for (int ib0 = 0; ib0 < n_ib; ib0 += per_chunk) {
         const int ib1 = ib0 + per_chunk < n_ib ? ib0 + per_chunk : n_ib;
-#define KGACC(IM, OD) KLAUNCH(c, "k_kg_accumulate", (k_kg_accumulate<IM, OD><<<grid, th, 0, c->stream>>>(c->dc, R, R_bs, n_ib, ib0, ib1, k, pts, c_n, rows, B, ib0 > 0, acc, acc_bs)))
+#define KGACC(IM, OD)                                                                                              \
+    do {                                                                                                           \
+        if (pp)                                                                                                    \
+            KLAUNCH(c, "k_kg_accumulate", (k_kg_accumulate<IM, OD, true><<<grid, th, 0, c->stream>>>(              \
+                                              c->dc, R, R_bs, n_ib, ib0, ib1, k, pts, c_n, rows, B, ib0 > 0, acc, acc_bs))); \
+        else                                                                                                       \
+            KLAUNCH(c, "k_kg_accumulate", (k_kg_accumulate<IM, OD, false><<<grid, th, 0, c->stream>>>(             \
+                                              c->dc, R, R_bs, n_ib, ib0, ib1, k, pts, c_n, rows, B, ib0 > 0, acc, acc_bs))); \
+    } while (0)
         if (img == 2) {
             if (odt == 4) KGACC(2, 4);
             else if (odt == 2) KGACC(2, 2);
