@@ -618,9 +618,12 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
         // giant steps of a batch (every group sums the same R single-step terms, term-major, no gather, no
         // step-0 members): k_ks_giant reuses each key word across KG_IB groups
         const int Rg = G > 0 ? (int)groups[0].size() : 0;
+        // GALA_KS_GIANT: unset -> when the grid fills the GPU; "force" -> always (tests); anything else -> never
+        const char* ge = getenv("GALA_KS_GIANT");
+        const bool g_force = ge && strcmp(ge, "force") == 0;
         bool giant = !any_gather && V == G && Rg >= 1 && (long long)Rg * G == (long long)terms.size() && !raw_U &&
-                     getenv("GALA_KS_GIANT") == nullptr &&
-                     (long long)((N + th - 1) / th) * M * ((G + KG_IB - 1) / KG_IB) >= 2LL * c->num_sms;   // fills the GPU
+                     (ge == nullptr || g_force) &&
+                     (g_force || (long long)((N + th - 1) / th) * M * ((G + KG_IB - 1) / KG_IB) >= 2LL * c->num_sms);
         for (size_t t = 0; giant && t < terms.size(); t++)
             giant = terms[t].steps.size() == 1 && !terms[t].ntt_block && terms[t].steps[0] == terms[t % Rg].steps[0] &&
                     terms[t].c0_zero == terms[0].c0_zero;

@@ -356,6 +356,51 @@ def test_rotate_batch_words(tw):
             assert np.array_equal(tw.gpu.export_words(outs[b, i]), want[i])
 
 
+@pytest.mark.parametrize("form", ["hoist", "generic"])
+def test_rotate_batch_forms_words(tw, form, monkeypatch):
+    """Hoisted rotations of a batch through k_ks_hoist (step keys shared by up to 8 inputs per thread) and
+    through the generic k_ks_mac (GALA_KS_HOIST) == oracle, word for word."""
+    import torch
+
+    n = tw.bfv.n
+    steps = sorted({1 % n, 2 % n, 5 % n, (n - 1) % n} - {0})
+    if len(steps) < 2:
+        pytest.skip("tiny")
+    if form == "generic":
+        monkeypatch.setenv("GALA_KS_HOIST", "off")
+    tw.keys_for(steps)
+    xs = [tw.encrypt(tw.slots()) for _ in range(11)]
+    outs = tw.gpu.rotate_batch(torch.stack([g for g, _ in xs]), steps)
+    for b in (0, 5, 10):
+        want = tw.cpu.rotate_hoisted(xs[b][1], steps)
+        for i in range(len(steps)):
+            assert np.array_equal(tw.gpu.export_words(outs[b, i]), want[i])
+
+
+@pytest.mark.parametrize("form", ["force", "off"])
+def test_mv_gala2_giant_forms_words(tw, form, monkeypatch):
+    """FC giant-step key switches through k_ks_giant (forced on this small ring; production enables it when
+    its grid fills the GPU) and through the generic k_ks_mac == oracle o_mv_gala2, word for word."""
+    import torch
+
+    n = tw.bfv.n
+    T = min(16, n)
+    b, steps = tw.gpu.bsgs_steps(T, 4 if T >= 16 else None)
+    if T // b < 2:
+        pytest.skip("one giant group")
+    monkeypatch.setenv("GALA_KS_GIANT", form)
+    tw.keys_for(steps)
+    pts = tw.slots(T)
+    pts2 = tw.gpu.encode_gala_weights(pts, b)
+    nb = 5
+    xs = [tw.encrypt(tw.slots()) for _ in range(nb)]
+    rs = tw.slots(nb)
+    _, masked = tw.gpu.mv_gala2_batch(torch.stack([g for g, _ in xs]), pts2, T, tw.gpu.to_device_u32(rs), b)
+    for i in (0, nb - 1):
+        _, c_masked = tw.cpu.mv_gala(xs[i][1], pts, rs[i], baby=b, schedule=2)
+        assert np.array_equal(tw.gpu.export_words(masked[i]), c_masked)
+
+
 def test_conv_kg2_post_batch_words(tw):
     """Batched post-mask convolution (several images in one pass) == per-image calls == oracle."""
     import torch
