@@ -715,7 +715,7 @@ __global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __res
     }
     S[(((long long)b * 2 + 0) * M + j) * NN + k] = s0;
     S[(((long long)b * 2 + 1) * M + j) * NN + k] = s1;
-    if (j < L) {
+    if (j < L && Qadd) {   // (no Q-side addend in the key-folded form: it rides in U as P X)
         Qadd[(((long long)b * 2 + 0) * L + j) * NN + k] = c0;
         Qadd[(((long long)b * 2 + 1) * L + j) * NN + k] = c1;
     }

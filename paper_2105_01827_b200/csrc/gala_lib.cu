@@ -1649,9 +1649,9 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     for (int g = 1; g < G; g++) ggal[g] = galois_of(c, g * baby);
     unsigned* d_ggal;
     RET(upload(c, ggal.data(), ggal.size() * sizeof(unsigned), (void**)&d_ggal));
-    u64 *S, *Qadd;
+    u64 *S, *Qadd = nullptr;
     RET(scratch(c, &S, (size_t)B * 2 * M * N));
-    RET(scratch(c, &Qadd, (size_t)B * 2 * L * N));
+    if (Cacc) RET(scratch(c, &Qadd, (size_t)B * 2 * L * N));   // key-folded form: no Q-side addend
     {
         const int th = N < 256 ? N : 256;
         dim3 gq((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)B);
