@@ -94,6 +94,13 @@ def main():
             torch.cuda.synchronize()
             reps.append(a.elapsed_time(b))
         ms = float(np.median(reps))
+        breakdown = None
+        if "--profile" in sys.argv:   # one extra traced run: per-kernel CUDA-event times of this layer
+            ctx.profile(True)
+            out = run()
+            prof = ctx.profile_read()
+            ctx.profile(False)
+            breakdown = {k: round(v["ms"], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
         if blocks and world > 1 and spec.kind == "conv":   # every rank ran a slice of this layer
             ms = max_over_ranks(ms, device=torch.device("cuda"))
         total_ms += ms
@@ -102,6 +109,8 @@ def main():
                "plaintext_GB": round(layer.plaintext_bytes / 1e9, 3)}
         if spec.kind == "conv":
             res.update(frame=layer.frame, c_n=layer.kg.c_n, tiles=layer.tiles ** 2, schedule=layer.kg.schedule)
+        if breakdown is not None:
+            res["breakdown_ms"] = breakdown
         if check and (not blocks or rank == 0):   # sharded outputs are gathered on rank 0
             got = layer.shares(out, masks) if spec.kind == "fc" else layer.decrypt_output(out)
             ok = bool(np.array_equal(got, plain_layer(spec, x, net.weights[i], net.params.p)))
