@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(256) k_kg_zy(DevCtx c, const u64* __restrict__
             // post-mask form, lean inner loop: every column's (input, tap) comes from the block's column
             // table, addresses are 32-bit word offsets from block-invariant bases, and KG_ZU columns'
             // loads are issued before any product (the loop is load-latency bound)
-            const uint32_t uMN = (uint32_t)MN, uN = (uint32_t)N;
+            const uint32_t uN = (uint32_t)N;
             const uint32_t dj = (uint32_t)j * uN;
             const uint32_t xo = (uint32_t)comp * (uint32_t)L * uN + (uint32_t)jl;
             const bool has_c0 = comp == 0 && j < L;

@@ -2002,7 +2002,7 @@ int gala_conv_kg_batch(gala_ctx* c, const uint64_t* cts, int B, int n_ib, const 
 static int conv_kg_run(gala_ctx* c, const uint64_t* cts, int n_ib, const uint64_t* pts, const uint64_t* ptcan, int n_obp,
                        int c_n, int k, const int* tap_steps, int band_step, uint64_t* outs, int B)
 {
-    const int N = c->dc.N, L = c->dc.L, M = c->dc.M;
+    const int N = c->dc.N, L = c->dc.L;
     const long long W = 2LL * L * N;
     if (n_ib <= 0 || n_obp <= 0 || c_n <= 0 || k <= 0) return set_err(GALA_ERR_DIM, "empty convolution");
     std::vector<int> rot_taps;
