@@ -22,6 +22,14 @@ lo, hi = 2 * NST, min(1000, 40 * NST)
 gs = np.arange(lo, hi)
 period = np.diff(t[9, lo:hi + 1])
 print(f"stages {lo}..{hi}: period mean {period.mean():.0f} median {np.median(period):.0f} clk")
+print("period percentiles 10/50/90/99:", [int(np.percentile(period, x)) for x in (10, 50, 90, 99)])
+big = np.where(period > 4000)[0]
+print("stages with period > 4000 clk (index within position, position):", [(int((lo + i) % NST), int((lo + i) // NST)) for i in big[:20]])
+print("mean period by stage within position:", [int(period[(gs % NST) == s_].mean()) if np.any((gs % NST) == s_) else 0 for s_ in range(NST)])
+iss = t[1, gs] - t[0, gs]
+print("issue+commit by stage within position:", [int(iss[(gs % NST) == s_].mean()) for s_ in range(NST)])
+fw = t[0, gs] - t[9, gs]
+print("full wait by stage within position:", [int(fw[(gs % NST) == s_].mean()) for s_ in range(NST)])
 print(f"issuer full wait: mean {np.mean(t[0, gs] - t[9, gs]):.0f} median {np.median(t[0, gs] - t[9, gs]):.0f}")
 print(f"issuer issue+commit: mean {np.mean(t[1, gs] - t[0, gs]):.0f}")
 pos = np.arange(2, hi // NST - 1)
