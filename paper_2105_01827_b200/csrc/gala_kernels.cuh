@@ -20,7 +20,20 @@ struct PolyMap {
     int skip_per;     // >0: item index x -> (x/cnt)*skip_per + first + x%cnt
     int skip_first;   // (first, cnt) = (1, skip_per - 1) when skip_cnt == 0
     int skip_cnt;
+    int quad_G;       // > 0: the source is the key-folded group-sum layout (u_quad_base), source item b G + g,
+    int quad_cc;      //      polynomial (quad_cc, quad_j) of it; element i at u_quad_off(i)
+    int quad_j;
 };
+
+// The key-folded FC group sums (k_gala_kf): per 256-input tile, [g][cc][j][N / 4][256 rows][4] -- four
+// consecutive positions of one input are one 32-byte sector and the 256 inputs' sectors are contiguous,
+// so the epilogue's 32-byte stores from 32 lanes (inputs) are one 1 KB run, and a polynomial read (32
+// consecutive positions) still touches 8 full sectors.
+__device__ __forceinline__ long long u_quad_base(int b, int g, int cc, int j, int G, int M, int N)
+{
+    return (((((long long)(b >> 8) * G + g) * 2 + cc) * M + j) * N) * 256 + (long long)(b & 255) * 4;
+}
+__device__ __forceinline__ long long u_quad_off(int i) { return ((long long)(i >> 2) << 10) + (i & 3); }
 
 __device__ __forceinline__ void polymap_resolve(const PolyMap& pm, int p, int N, long long& src_off,
                                                 long long& dst_off, int& prime)
@@ -34,6 +47,16 @@ __device__ __forceinline__ void polymap_resolve(const PolyMap& pm, int p, int N,
     prime = pm.prime_base + w % pm.nprimes;
     src_off = src_item * pm.src_is + (long long)(pm.src_div ? w / pm.nprimes : w) * N;
     dst_off = (long long)item * pm.dst_is + (long long)w * N;
+}
+__device__ __forceinline__ long long polymap_quad_base(const PolyMap& pm, int p, int M, int N)
+{
+    int item = p / pm.per;
+    long long src_item = item;
+    if (pm.skip_per > 0) {
+        const int sp = pm.skip_cnt > 0 ? pm.skip_cnt : pm.skip_per - 1, f = pm.skip_cnt > 0 ? pm.skip_first : 1;
+        src_item = (long long)(item / sp) * pm.skip_per + f + item % sp;
+    }
+    return u_quad_base((int)(src_item / pm.quad_G), (int)(src_item % pm.quad_G), pm.quad_cc, pm.quad_j, pm.quad_G, M, N);
 }
 
 template <typename T>
@@ -80,8 +103,9 @@ __global__ void __launch_bounds__(512, 2) k_ntt_inv(DevCtx c, const u64* __restr
     polymap_resolve(pm, blockIdx.x, c.N, so, dof, j);
     const ModC md = c.mod[j];
     const u64 q = md.q;
+    const long long qb = pm.quad_G > 0 ? polymap_quad_base(pm, blockIdx.x, c.M, c.N) : 0;
     for (int i = threadIdx.x; i < c.N; i += blockDim.x) {
-        u64 v = ld_cs(src + so + i);
+        u64 v = pm.quad_G > 0 ? ld_cs(src + qb + u_quad_off(i)) : ld_cs(src + so + i);
         if (FROM_MONT) v = csub(redc_lazy(0, v, md), q);
         sm[pad(i)] = v;
     }
@@ -108,6 +132,7 @@ struct MdArgs {
     int skip_per;      // > 0: item x reads source item (x / cnt) skip_per + first + x % cnt
     int skip_first;    // (first, cnt) = (1, skip_per - 1) when skip_cnt == 0
     int skip_cnt;
+    int quad_G;        // > 0: U in the key-folded group-sum layout (u_quad_base), source item g = b quad_G + group
 };
 
 __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
@@ -128,13 +153,14 @@ __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
         return v > halfP ? q - (P - v) : v;
     }, sm, c.twf[j], q, c.logN);
     const u64* U = a.U + (((long long)g * 2 + comp) * M + j) * N;
+    const long long qb = a.quad_G > 0 ? u_quad_base((int)(g / a.quad_G), (int)(g % a.quad_G), comp, j, a.quad_G, M, N) : 0;
     const u64* add = comp == 0 ? a.add0 : a.add1;
     if (add) add += (long long)g * a.add_is + (long long)j * N;
     u64* out = (a.outs ? a.outs[x] : a.out + (long long)x * a.out_is) + ((long long)comp * L + j) * N;
     const u64 pinv = c.pinv_mont[j];
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         u64 R = csub(csub(sm[pad(i)], 2 * q), q);
-        u64 v = mont_mul(sub_mod(U[i], R, q), pinv, md);
+        u64 v = mont_mul(sub_mod(a.quad_G > 0 ? a.U[qb + u_quad_off(i)] : U[i], R, q), pinv, md);
         if (add) v = add_mod(v, add[i], q);
         out[i] = v;
     }
@@ -692,7 +718,7 @@ __global__ void k_fold_groups(DevCtx c, const u64* __restrict__ Uv, const u64* _
 // addends are already lifted into U as P C): Qadd = 0.  grid (N / 256, M, B)
 __global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __restrict__ Cacc,
                            const unsigned* __restrict__ gal, int G, int g_lo, int g_hi, u64* __restrict__ S,
-                           u64* __restrict__ Qadd)
+                           u64* __restrict__ Qadd, int quad)
 {
     const int N = c.N, L = c.L, M = c.M;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -706,10 +732,10 @@ __global__ void k_giant_qp(DevCtx c, const u64* __restrict__ U, const u64* __res
         const long long z = (long long)b * G + g;
         const unsigned ge = gal[g];
         const int src = ge == 1u ? k : auto_src(k, ge, c.logN);
-        s0 = add_mod(s0, __ldg(U + ((z * 2 + 0) * M + j) * NN + src), q);
+        s0 = add_mod(s0, __ldg(U + (quad ? u_quad_base(b, g, 0, j, G, M, N) + u_quad_off(src) : ((z * 2 + 0) * M + j) * NN + src)), q);
         if (j < L && Cacc) c0 = add_mod(c0, __ldg(Cacc + ((z * 2 + 0) * L + j) * NN + src), q);
         if (ge == 1u) {
-            s1 = add_mod(s1, __ldg(U + ((z * 2 + 1) * M + j) * NN + k), q);
+            s1 = add_mod(s1, __ldg(U + (quad ? u_quad_base(b, g, 1, j, G, M, N) + u_quad_off(k) : ((z * 2 + 1) * M + j) * NN + k)), q);
             if (j < L && Cacc) c1 = add_mod(c1, __ldg(Cacc + ((z * 2 + 1) * L + j) * NN + k), q);
         }
     }
@@ -2917,8 +2943,11 @@ k_gala_kf(DevCtx c, const uint8_t* __restrict__ Dq, const u64* __restrict__ Wk, 
                 }
             }
             if (active) {
-                u64* out0 = U + (((long long)b * G * 2 + cc) * M + j) * (long long)N + k;
-                const long long gstride = 2LL * M * N;
+                // the group-sum layout of u_quad_base: a warp's 32 lanes (inputs) write one 1 KB run per group
+                // (position-contiguous rows put every lane in another row -- 32 L1 wavefronts per store, whose
+                // bursts stalled the other roles' mbarrier traffic: MMA-only probe 2.43 -> 1.93 ms without them)
+                u64* out0 = U + u_quad_base(b, 0, cc, j, G, M, N) + u_quad_off(k);
+                const long long gstride = 2LL * M * N * 256;
 #pragma unroll
                 for (int g = 0; g < 8; g++)
                     if (g < G)

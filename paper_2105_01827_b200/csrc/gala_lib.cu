@@ -226,6 +226,11 @@ static PolyMap pm_make(int per, int nprimes, int prime_base, int src_div, long l
     pm.src_is = src_is;
     pm.dst_is = dst_is;
     pm.skip_per = skip_per;
+    pm.skip_first = 0;
+    pm.skip_cnt = 0;
+    pm.quad_G = 0;
+    pm.quad_cc = 0;
+    pm.quad_j = 0;
     return pm;
 }
 
@@ -1493,8 +1498,14 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     // 2. stage A: E_jj = sum_i sigma_jj(D_i) ksk_jj[i] per input and baby rotation (shared by all groups);
     //    stage B: per (input, group) U = sum_jj w_t E_jj, C0 = sum_jj w_t sigma_jj(c0) (+ step-0 member)
     const int Z = B * G;
+    // key-folded tiles (k_gala_kf) for layers large enough for a tile's fixed per-position cost (64 rotations x
+    // 8 groups of MMA columns whatever T is): T >= 128 (config 2); config 1 (T = 8) stays on the CUDA cores,
+    // 1.6 vs 2.2 us per layer at 1024 inputs
+    const bool kf = wcan != nullptr && fc_kf_on(c) && B >= 16 && T >= c->fc_tc_min_T && G <= 8 && baby <= 64 &&
+                    getenv("GALA_FC_NO_TC") == nullptr;
     u64 *E = nullptr, *R0 = nullptr, *U, *Cacc, *rr;
-    RET(scratch(c, &U, (size_t)Z * 2 * M * N));
+    // (key-folded: the u_quad_base layout, whole 256-input tiles)
+    RET(scratch(c, &U, (size_t)(kf ? (B + KF_ROWS - 1) / KF_ROWS * KF_ROWS * G : Z) * 2 * M * N));
     RET(scratch(c, &Cacc, (size_t)Z * 2 * L * N));
     RET(scratch(c, &rr, (size_t)Z * 2 * N));
     // the tensor-core tile always spans 32 input rows: it pays off from about half a tile of inputs
@@ -1503,11 +1514,6 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     // large enough for a tile's fixed per-position cost (K = 64 rotations x 8 bytes whatever T is) to pay:
     // T >= 128 (config 2: 17.5k -> 19.3k layers/s at 96 inputs; config 1, T = 8, stays on the CUDA cores,
     // 0.0016 vs 0.0066 ms per layer at 1024 inputs); the rest of the layer stays batched over all B
-    // key-folded tiles (k_gala_kf) for layers large enough for a tile's fixed per-position cost (64 rotations x
-    // 8 groups of MMA columns whatever T is): T >= 128 (config 2); config 1 (T = 8) stays on the CUDA cores,
-    // 1.6 vs 2.2 us per layer at 1024 inputs
-    const bool kf = wcan != nullptr && fc_kf_on(c) && B >= 16 && T >= c->fc_tc_min_T && G <= 8 && baby <= 64 &&
-                    getenv("GALA_FC_NO_TC") == nullptr;
     const bool tc = !kf && wcan != nullptr && !fc_kf_on(c) && B >= 16 &&
                     (B <= 32 || (T >= 128 && (B % 32 == 0 || B % 32 >= 16))) &&
                     G <= 8 && baby <= 64 && (N % 32) == 0 && getenv("GALA_FC_NO_TC") == nullptr;
@@ -1655,7 +1661,8 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     {
         const int th = N < 256 ? N : 256;
         dim3 gq((unsigned)((N + th - 1) / th), (unsigned)M, (unsigned)B);
-        KLAUNCH(c, "k_giant_qp", k_giant_qp<<<gq, th, 0, c->stream>>>(c->dc, U, Cacc, d_ggal, G, g_lo, g_hi, S, Qadd));
+        KLAUNCH(c, "k_giant_qp", k_giant_qp<<<gq, th, 0, c->stream>>>(c->dc, U, Cacc, d_ggal, G, g_lo, g_hi, S, Qadd,
+                                                                       kf ? 1 : 0));
     }
     const int ga = g_lo > 1 ? g_lo : 1;                 // the shard's giant groups g >= 1
     const int Gs = g_hi > ga ? g_hi - ga : 0;
@@ -1667,8 +1674,14 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
         PolyMap pmi = pm_make(1, 1, L, 0, 2LL * M * N, N, G);
         pmi.skip_first = ga;
         pmi.skip_cnt = Gs;
-        RET(launch_inv<false>(c, U + (long long)(M + L) * N, rr, Zi, pmi, "k_ntt_inv[moddown]"));
+        if (kf) {   // the P limb of c1 straight from the key-folded group-sum layout
+            pmi.quad_G = G;
+            pmi.quad_cc = 1;
+            pmi.quad_j = L;
+        }
+        RET(launch_inv<false>(c, kf ? U : U + (long long)(M + L) * N, rr, Zi, pmi, "k_ntt_inv[moddown]"));
         MdArgs a{};
+        a.quad_G = kf ? G : 0;
         a.r = rr;
         a.U = U;
         a.add0 = Cacc;

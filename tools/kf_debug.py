@@ -1,4 +1,5 @@
-"""Compare the key-folded kernel's U with the split pair's U + P Cacc (GALA_DEBUG_DUMP).  Runs one layer
+"""(The key-folded U is dumped in the u_quad_base layout of gala_kernels.cuh since round 2; reorder
+before comparing.)  Compare the key-folded kernel's U with the split pair's U + P Cacc (GALA_DEBUG_DUMP).  Runs one layer
 twice in subprocesses (GALA_FC_KF=1 / 0) on the same seeded inputs and reports where they differ."""
 import os
 import subprocess
