@@ -43,9 +43,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=256,
+    ap.add_argument("--batch", type=int, default=512,
                     help="independent layers (inputs) per step per GPU (key-folded tensor-core tiles of 256)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--stream-steps", type=int, default=32,
+                    help="batches per streamed e2e call (pinned host staging: ~0.2 GB per batch of 256)")
     ap.add_argument("--baby", type=int, default=0, help="BSGS baby-step count (0: library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tensor-cores", action="store_true", help="CUDA-core baby-step sums (k_gala_mac2)")
@@ -336,7 +338,7 @@ def run_ours(args):
     # returns all K steps' masked words there; each step's H2D and D2H overlap the neighbouring steps' layers
     # (gala_mv_gala2_stream_host).  Every step's copies are inside the timed region.
     K = args.steps
-    S = min(K, 16)          # batches per streamed call (pinned staging bounded); K steps = ceil(K / S) calls
+    S = max(1, min(K, args.stream_steps))   # batches per streamed call (pinned staging bounded); K steps = ceil(K / S) calls
     stream_ct = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(host_ct.numpy()[None], (S,) + tuple(host_ct.shape)))).pin_memory()
     stream_r = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(host_r.numpy()[None], (S,) + tuple(host_r.shape)))).pin_memory()
     stream_out = torch.empty((S, B, 2, L, N), dtype=torch.int64).pin_memory()
@@ -543,7 +545,7 @@ def run_ours(args):
         "e2e": {"value": round(e2e_value, 3), "unit": "layers/s",
                 "h2d_bytes_per_step": B * (ct_bytes + N * 4), "d2h_bytes_per_step": B * ct_bytes,
                 "path": ("gala_mv_gala2_stream_host (C-ABI, pinned host buffers, canonical words; one call per "
-                         "16 steps, each step's H2D and D2H overlapped with the neighbouring steps' layers; "
+                         f"{S} steps, each step's H2D and D2H overlapped with the neighbouring steps' layers; "
                          "words of the first, middle and last batch of a call checked against the device path)")
                         if e2e_stream_value is not None else
                         (f"gala_mv_gala{layer.schedule if layer.schedule == 2 else ''}_batch_host"
