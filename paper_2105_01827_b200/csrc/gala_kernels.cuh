@@ -166,6 +166,36 @@ __global__ void __launch_bounds__(512, 2) k_moddown(DevCtx c, MdArgs a)
     }
 }
 
+// ModDown + mask in the coefficient domain, for results that leave as canonical (coefficient) words
+// (gala_mv_gala2_stream_host): Uc = INTT of every limb of the QP sums [G][2][M][N], m = the masks'
+// coefficients mod p [G][N] (k_encode_p), out [G][2][L][N]:
+//   out[g][comp][j] = (Uc[g][comp][j] - centred Uc[g][comp][P]) * P^-1 - (comp == 0) Delta_j m[g]   (mod q_j)
+// The NTT is linear mod q_j, so these are the words of k_moddown + k_sub_plain + the export INTT with
+// 9 fewer NTT-sized transforms per result (no NTT of the lifted P limb or of the mask, no export INTT).
+__global__ void k_moddown_coef(DevCtx c, const u64* __restrict__ Uc, const uint32_t* __restrict__ m,
+                               u64* __restrict__ out, int G)
+{
+    const int L = c.L, M = c.M, N = c.N;
+    const long long total = (long long)G * 2 * N;
+    const u64 P = c.mod[L].q, halfP = P >> 1;
+    for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+         x += (long long)gridDim.x * blockDim.x) {
+        const long long gc = x >> c.logN;      // g * 2 + comp
+        const int k = (int)(x & (N - 1));
+        const u64* u = Uc + gc * M * N + k;
+        const u64 v = ld_cs(u + (long long)L * N);
+        const uint32_t mk = (gc & 1) == 0 && m ? __ldg(m + (gc >> 1) * N + k) : 0u;
+        for (int j = 0; j < L; j++) {
+            const ModC md = c.mod[j];
+            const u64 q = md.q;
+            const u64 R = v > halfP ? q - (P - v) : v;
+            u64 w = mont_mul(sub_mod(ld_cs(u + (long long)j * N), R, q), c.pinv_mont[j], md);
+            if ((gc & 1) == 0 && m) w = sub_mod(w, shoup((u64)mk, c.delta[j], c.delta_sh[j], q), q);
+            st_cs(out + (gc * L + j) * N + k, w);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Key-switch engine v2.  A "term" is a source ciphertext X, optionally times a
 // plaintext operand pt (so ScMult fuses into the key switch), to be rotated by

@@ -124,6 +124,10 @@ struct gala_ctx {
     int stage_next = 0;
     int smem_ntt = 0;         // bytes of one padded polynomial
     cudaStream_t side = nullptr;              // independent work (mask encoding) overlapped with the layer
+    // coefficient-domain finish (gala_mv_gala2_stream_host): when set, the final ModDown of the fused FC layer writes
+    // masked canonical words here (k_moddown_coef) instead of NTT-form outputs; coef_m = the masks' coefficients mod p
+    u64* coef_out = nullptr;
+    uint32_t* coef_m = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // streamed host entry points: copy-in / copy-out streams and per-slot events (created on first use)
     cudaStream_t cs_in = nullptr, cs_out = nullptr;
@@ -720,6 +724,20 @@ static int rotate_engine(gala_ctx* c, const std::vector<EngTerm>& terms,
     if (raw_U) {   // multi-GPU partial: the groups' QP sums and Q addends before any ModDown
         CK(cudaMemcpyAsync(raw_U, U, sizeof(u64) * (size_t)G * 2 * M * N, cudaMemcpyDeviceToDevice, c->stream));
         CK(cudaMemcpyAsync(raw_C, Cacc, sizeof(u64) * (size_t)G * 2 * L * N, cudaMemcpyDeviceToDevice, c->stream));
+    } else if (c->coef_out) {
+        // results leave as canonical words: INTT every limb of the QP sums, then ModDown and the mask pointwise
+        // in the coefficient domain (same words; no NTT of the lifted P limb, no export INTT)
+        if (q_add) return set_err(GALA_ERR_PARAM, "internal: coefficient-domain finish with a Q-side addend");
+        for (const EngTerm& t : terms)
+            if (!t.c0_zero || t.steps.empty())
+                return set_err(GALA_ERR_PARAM, "internal: coefficient-domain finish needs rotated terms without c0");
+        u64* Uc;
+        RET(scratch(c, &Uc, (size_t)G * 2 * M * N));
+        RET(launch_inv<false>(c, U, Uc, G * 2 * M, pm_make(2 * M, M, 0, 0, 2LL * M * N, 2LL * M * N), "k_ntt_inv[moddown]"));
+        if (c->coef_m) CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+        KLAUNCH(c, "k_moddown", k_moddown_coef<<<grid_for((long long)G * 2 * N, 256), 256, 0, c->stream>>>(
+                                    c->dc, Uc, c->coef_m, c->coef_out, G));
+        release(c, Uc);
     } else {
     RET(launch_inv<false>(c, U + (long long)L * N, r, G * 2, pm_make(1, 1, L, 0, (long long)M * N, N),
                           "k_ntt_inv[moddown]"));
@@ -816,6 +834,27 @@ static int mask_finish(gala_ctx* c, const u64* ct, u64* DM, int B, u64* out)
     CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     KLAUNCH(c, "k_sub_plain", k_sub_plain<<<grid_for((long long)B * W, 256), 256, 0, c->stream>>>(c->dc, ct, DM, out, B));
     release(c, DM);
+    return GALA_OK;
+}
+
+// The coefficient-domain finish needs only the masks' coefficients mod p (k_encode_p), on the side stream
+static int mask_begin_coef(gala_ctx* c, const uint32_t* r, int B, uint32_t** mcoef)
+{
+    const int N = c->dc.N;
+    RET(scratch(c, mcoef, (size_t)B * N));
+    CK(cudaEventRecord(c->ev_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    cudaStream_t main = c->stream;
+    cudaEvent_t a = nullptr, b = nullptr;
+    c->stream = c->side;
+    if (c->prof_on) prof_begin(c, &a, &b);
+    k_encode_p<<<B, ntt_threads(N), c->smem_ntt, c->side>>>(c->dc, r, *mcoef);
+    if (c->prof_on) prof_end(c, "k_encode", a, b);
+    c->stream = main;
+    g_launches += 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(GALA_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+    CK(cudaEventRecord(c->ev_join, c->side));
     return GALA_OK;
 }
 
@@ -1460,7 +1499,8 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
         return GALA_OK;
     }
     u64* DM = nullptr;
-    if (r && masked && !raw_U) RET(mask_begin(c, r, B, &DM));   // overlaps the layer on the side stream
+    if (c->coef_out && r && !raw_U) RET(mask_begin_coef(c, r, B, &c->coef_m));
+    else if (r && masked && !raw_U) RET(mask_begin(c, r, B, &DM));   // overlaps the layer on the side stream
     // 1. one decomposition per input: identity digit block [(L*M + L)][N] (digits of x.c1 in every
     //    prime of QP, then x.c0)
     u64 *dig, *Dblk;
@@ -1726,6 +1766,10 @@ static int mv2_run(gala_ctx* c, const uint64_t* cts, int B, const uint64_t* pts2
     release(c, S);
     release(c, Qadd);
     release(c, d_ggal);
+    if (c->coef_m) {
+        release(c, c->coef_m);
+        c->coef_m = nullptr;
+    }
     if (DM) RET(mask_finish(c, outs, DM, B, masked));
     return GALA_OK;
 }
@@ -1889,6 +1933,14 @@ static int mv_stream_host(gala_ctx* c, int schedule, const uint64_t* cts_host, i
     CK(cudaEventRecord(c->ev_alloc, c->stream));
     CK(cudaStreamWaitEvent(c->cs_in, c->ev_alloc, 0));
     CK(cudaStreamWaitEvent(c->cs_out, c->ev_alloc, 0));
+    // the coefficient-domain finish applies where mv2_run takes the key-folded form (its predicate, restated)
+    bool coef = false;
+    if (schedule == 2 && r_host && masked_host) {
+        const int bb = baby > 0 ? baby : gala_bsgs_baby(T);
+        const char* ce = getenv("GALA_STREAM_COEF");
+        coef = wcan != nullptr && fc_kf_on(c) && B >= 16 && T >= c->fc_tc_min_T && bb > 1 && T % bb == 0 && T / bb <= 8 &&
+               bb <= 64 && getenv("GALA_FC_NO_TC") == nullptr && !(ce && ce[0] == '0');
+    }
     const char* nc = getenv("GALA_STREAM_NOCOPY");   // experiment: "in", "out" or both skipped
     const bool noin = nc && strcmp(nc, "out") != 0, noout = nc && strcmp(nc, "in") != 0;
     // large copies go in 1 MB pieces: the layers' own small descriptor uploads share the copy engine and
@@ -1918,11 +1970,26 @@ static int mv_stream_host(gala_ctx* c, int schedule, const uint64_t* cts_host, i
         if (b + 1 < S) RET(copy_in(b + 1));   // enqueued ahead: overlaps this batch's layers
         CK(cudaStreamWaitEvent(c->stream, c->ev_h2d[sl], 0));
         RET(gala_ct_import(c, hin[sl], ct, B));
+        if (coef) {
+            // key-folded layers finish in the coefficient domain: the final ModDown writes the masked canonical
+            // words straight into the staging slot (k_moddown_coef), no mask NTT and no export INTT
+            if (b >= 2) CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[sl], 0));   // batch b - 2's words copied out
+            c->coef_out = hout[sl];
+            const int rc = mv2_run(c, ct, B, pts, wcan, T, baby, rr[sl], out, masked);
+            c->coef_out = nullptr;
+            if (c->coef_m) {
+                release(c, c->coef_m);
+                c->coef_m = nullptr;
+            }
+            RET(rc);
+            CK(cudaEventRecord(c->ev_used[sl], c->stream));
+        } else {
         if (schedule == 2) RET(mv2_run(c, ct, B, pts, wcan, T, baby, rr[sl], out, masked));
         else RET(gala_mv_gala_batch(c, ct, B, pts, T, baby, rr[sl], out, masked));
         CK(cudaEventRecord(c->ev_used[sl], c->stream));
         if (b >= 2) CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[sl], 0));   // batch b - 2's words copied out
         RET(gala_ct_export(c, masked, hout[sl], B));
+        }
         CK(cudaEventRecord(c->ev_done[sl], c->stream));
         CK(cudaStreamWaitEvent(c->cs_out, c->ev_done[sl], 0));
         if (!noout)
