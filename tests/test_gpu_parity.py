@@ -433,14 +433,15 @@ def test_conv_kg2_post_batch_words(tw):
         assert np.array_equal(tw.gpu.export_words(outs[i]), c_out)
 
 
+@pytest.mark.parametrize("coef", ["1", "0"])
 @pytest.mark.parametrize("tc", [False, True])
-def test_mv_gala2_stream_host_words(tw, tc):
+def test_mv_gala2_stream_host_words(tw, tc, coef, monkeypatch):
     """Streamed host entry point (S batches from host memory, copies overlapped with the layers) ==
-    oracle o_mv_gala2 for every batch, word for word."""
-    import ctypes
-
-    from paper_2105_01827_b200 import _lib
-
+    oracle o_mv_gala2 for every batch, word for word; key-folded layers with the coefficient-domain
+    finish (k_moddown_coef, the default) and with the NTT-domain ModDown + export (GALA_STREAM_COEF=0)."""
+    if coef == "0" and not tc:
+        pytest.skip("the coefficient-domain finish only applies to key-folded layers")
+    monkeypatch.setenv("GALA_STREAM_COEF", coef)
     n = tw.bfv.n
     T = min(8, n)
     b, steps = tw.gpu.bsgs_steps(T)
